@@ -1,0 +1,215 @@
+"""ctypes wrapper around oracle/qva_oracle.c plus the small dense (numpy/scipy) oracles.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Citations are to
+/root/reference/PAPER.md line numbers; readings R1..R22 are in DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from functools import lru_cache
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "qva_oracle.c")
+_LIB = os.path.join(_HERE, "libqva_oracle.so")
+
+__all__ = [
+    "build_oracle", "lib", "num_threads", "maxcut_q", "init_uniform", "phase", "mixer_x",
+    "mixer_circulant_dense", "mixer_complete", "expectation", "norm2", "probabilities",
+    "evolve_x", "evolve_complete", "evolve_circulant_dense", "lightcone_maxcut",
+    "dense_sum_x", "mixer_sparse_dense", "evolve_sparse_dense", "c128",
+]
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile the C oracle (plain -O2, no fast-math; OpenMP only splits independent loops)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-fPIC",
+               "-shared", "-std=c11", "-o", _LIB, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _LIB
+
+
+@lru_cache(maxsize=1)
+def lib():
+    build_oracle()
+    L = ctypes.CDLL(_LIB)
+    d, i, u64 = ctypes.c_double, ctypes.c_int, ctypes.c_uint64
+    P = ctypes.c_void_p
+    L.or_num_threads.restype = i
+    L.or_maxcut_q.argtypes = [i, i, P, P, P, P]
+    L.or_init_uniform.argtypes = [u64, P]
+    L.or_phase.argtypes = [u64, P, P, d]
+    L.or_mixer_x.argtypes = [i, P, d]
+    L.or_mixer_circulant_dense.argtypes = [u64, P, P, d]
+    L.or_mixer_complete.argtypes = [u64, P, d, d, d]
+    L.or_expectation.argtypes = [u64, P, P]
+    L.or_expectation.restype = d
+    L.or_norm2.argtypes = [u64, P]
+    L.or_norm2.restype = d
+    L.or_probabilities.argtypes = [u64, P, P]
+    L.or_evolve_x.argtypes = [i, P, P, P, i]
+    L.or_evolve_complete.argtypes = [u64, P, P, P, i, d, d]
+    L.or_evolve_circulant_dense.argtypes = [u64, P, P, P, P, i]
+    L.or_lightcone_maxcut.argtypes = [i, i, P, P, P, P, i, i, P]
+    L.or_lightcone_maxcut.restype = d
+    return L
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def c128(psi) -> np.ndarray:
+    a = np.ascontiguousarray(psi, dtype=np.complex128)
+    return a
+
+
+def num_threads() -> int:
+    return int(lib().or_num_threads())
+
+
+def maxcut_q(n: int, u, v, w=None) -> np.ndarray:
+    """q_x = -cut_w(x) (PAPER.md:721-726 Eq. maxcut-cost, cfg sign, R10)."""
+    u = np.ascontiguousarray(u, np.int32)
+    v = np.ascontiguousarray(v, np.int32)
+    q = np.empty(1 << n, np.float64)
+    wp = None
+    if w is not None:
+        w = np.ascontiguousarray(w, np.float64)
+        wp = _ptr(w)
+    lib().or_maxcut_q(n, len(u), _ptr(u), _ptr(v), wp, _ptr(q))
+    return q
+
+
+def init_uniform(N: int) -> np.ndarray:
+    psi = np.empty(N, np.complex128)
+    lib().or_init_uniform(N, _ptr(psi))
+    return psi
+
+
+def phase(psi: np.ndarray, q: np.ndarray, gamma: float) -> np.ndarray:
+    """In place; returns psi.  PAPER.md:152-155, :307-313."""
+    assert psi.dtype == np.complex128 and psi.flags.c_contiguous
+    q = np.ascontiguousarray(q, np.float64)
+    lib().or_phase(len(psi), _ptr(psi), _ptr(q), float(gamma))
+    return psi
+
+
+def mixer_x(psi: np.ndarray, beta: float) -> np.ndarray:
+    """In place; PAPER.md:159-171 (R1: W = sum_j X_j)."""
+    n = int(len(psi)).bit_length() - 1
+    assert (1 << n) == len(psi)
+    lib().or_mixer_x(n, _ptr(psi), float(beta))
+    return psi
+
+
+def mixer_circulant_dense(psi: np.ndarray, lam: np.ndarray, beta: float) -> np.ndarray:
+    """In place; O(N^2) definition of F^-1 diag(e^{-i beta lam}) F (R3, R4)."""
+    lam = np.ascontiguousarray(lam, np.float64)
+    lib().or_mixer_circulant_dense(len(psi), _ptr(psi), _ptr(lam), float(beta))
+    return psi
+
+
+def mixer_complete(psi: np.ndarray, beta: float, lam0: float, lam_rest: float) -> np.ndarray:
+    """In place; closed form for lambda = (lam0, c, ..., c) (R5)."""
+    lib().or_mixer_complete(len(psi), _ptr(psi), float(beta), float(lam0), float(lam_rest))
+    return psi
+
+
+def expectation(psi: np.ndarray, q: np.ndarray) -> float:
+    q = np.ascontiguousarray(q, np.float64)
+    return float(lib().or_expectation(len(psi), _ptr(psi), _ptr(q)))
+
+
+def norm2(psi: np.ndarray) -> float:
+    return float(lib().or_norm2(len(psi), _ptr(psi)))
+
+
+def probabilities(psi: np.ndarray) -> np.ndarray:
+    out = np.empty(len(psi), np.float64)
+    lib().or_probabilities(len(psi), _ptr(psi), _ptr(out))
+    return out
+
+
+def evolve_x(n: int, q: np.ndarray, theta, psi0: np.ndarray | None = None) -> np.ndarray:
+    """QAOA state.  theta = [g1, b1, ...] (R7)."""
+    theta = np.ascontiguousarray(theta, np.float64)
+    p = len(theta) // 2
+    psi = init_uniform(1 << n) if psi0 is None else np.array(psi0, np.complex128, copy=True)
+    q = np.ascontiguousarray(q, np.float64)
+    lib().or_evolve_x(n, _ptr(psi), _ptr(q), _ptr(theta), p)
+    return psi
+
+
+def evolve_complete(q: np.ndarray, theta, lam0: float, lam_rest: float,
+                    psi0: np.ndarray | None = None) -> np.ndarray:
+    """QWOA state with the complete-graph-family spectrum (R5, R20)."""
+    theta = np.ascontiguousarray(theta, np.float64)
+    N = len(q)
+    psi = init_uniform(N) if psi0 is None else np.array(psi0, np.complex128, copy=True)
+    q = np.ascontiguousarray(q, np.float64)
+    lib().or_evolve_complete(N, _ptr(psi), _ptr(q), _ptr(theta), len(theta) // 2,
+                             float(lam0), float(lam_rest))
+    return psi
+
+
+def evolve_circulant_dense(q: np.ndarray, lam: np.ndarray, theta,
+                           psi0: np.ndarray | None = None) -> np.ndarray:
+    theta = np.ascontiguousarray(theta, np.float64)
+    N = len(q)
+    psi = init_uniform(N) if psi0 is None else np.array(psi0, np.complex128, copy=True)
+    q = np.ascontiguousarray(q, np.float64)
+    lam = np.ascontiguousarray(lam, np.float64)
+    lib().or_evolve_circulant_dense(N, _ptr(psi), _ptr(q), _ptr(lam), _ptr(theta), len(theta) // 2)
+    return psi
+
+
+def lightcone_maxcut(n: int, u, v, w, theta, max_qubits: int = 28):
+    """Exact <Q> for q = -cut_w by per-edge light-cone simulation.  Returns (value, cone_sizes)."""
+    u = np.ascontiguousarray(u, np.int32)
+    v = np.ascontiguousarray(v, np.int32)
+    theta = np.ascontiguousarray(theta, np.float64)
+    sizes = np.zeros(len(u), np.int32)
+    wp = None
+    if w is not None:
+        w = np.ascontiguousarray(w, np.float64)
+        wp = _ptr(w)
+    val = lib().or_lightcone_maxcut(n, len(u), _ptr(u), _ptr(v), wp, _ptr(theta), len(theta) // 2,
+                                    max_qubits, _ptr(sizes))
+    return float(val), sizes
+
+
+# ---------------------------------------------------------------------------------------
+# Dense small-N oracles (library primitives: scipy.linalg.expm, numpy matmul).
+# ---------------------------------------------------------------------------------------
+
+def dense_sum_x(n: int) -> np.ndarray:
+    """W = sum_j X_j as a dense real matrix (hypercube adjacency)."""
+    N = 1 << n
+    W = np.zeros((N, N))
+    for j in range(n):
+        idx = np.arange(N)
+        W[idx, idx ^ (1 << j)] = 1.0
+    return W
+
+
+def mixer_sparse_dense(psi: np.ndarray, W_dense: np.ndarray, beta: float) -> np.ndarray:
+    """exp(-i beta W) psi by scipy's dense expm -- the definition of the sparse mixer's
+    result (PAPER.md:72-77 Eq. 4, :333).  Small N only."""
+    from scipy.linalg import expm
+    return expm(-1j * beta * np.asarray(W_dense, np.complex128)) @ psi
+
+
+def evolve_sparse_dense(q: np.ndarray, W_dense: np.ndarray, theta,
+                        psi0: np.ndarray | None = None) -> np.ndarray:
+    """Generic QVA (Eq. 1) with phase U_Q and mixer exp(-i beta W) (dense)."""
+    N = len(q)
+    psi = init_uniform(N) if psi0 is None else np.array(psi0, np.complex128, copy=True)
+    for k in range(len(theta) // 2):
+        phase(psi, q, theta[2 * k])
+        psi = np.ascontiguousarray(mixer_sparse_dense(psi, W_dense, theta[2 * k + 1]))
+    return psi

@@ -1,0 +1,372 @@
+"""Pins of the CPU oracle against things other than itself (`-m "not gpu"`).
+
+Each test names the pin (P1..P15) and the passage it follows.
+Independent sources: scipy.linalg.expm, numpy.fft, networkx.cut_size, closed forms,
+special cases and worked examples from SPEC.md.
+"""
+import math
+
+import networkx as nx
+import numpy as np
+import pytest
+from scipy.linalg import circulant, expm
+
+import oracle as O
+from qva_inputs import make_config, random_regular_graph, erdos_renyi_graph, fd_batch_thetas
+
+
+def _rand_state(N, rng):
+    psi = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    return np.ascontiguousarray(psi / np.linalg.norm(psi))
+
+
+# ---------------------------------------------------------------- qualities (Eq. 24) ----
+@pytest.mark.parametrize("weighted", [False, True])
+def test_maxcut_q_vs_networkx(weighted):
+    """q_x = -cut_w(x) (R10) against networkx.cut_size on every x."""
+    rng = np.random.default_rng(11)
+    n = 7
+    u, v = erdos_renyi_graph(n, 0.6, rng)
+    w = rng.uniform(0, 1, len(u)) if weighted else None
+    G = nx.Graph()
+    G.add_nodes_from(range(n))
+    for k in range(len(u)):
+        G.add_edge(int(u[k]), int(v[k]), weight=float(w[k]) if weighted else 1.0)
+    q = O.maxcut_q(n, u, v, w)
+    for x in range(1 << n):
+        S = [j for j in range(n) if (x >> j) & 1]
+        ref = nx.cut_size(G, S, weight="weight")
+        assert q[x] == pytest.approx(-ref, abs=1e-13)
+
+
+def test_maxcut_q_single_edge_spec_example():
+    """SPEC.md:446 single edge (0,1), n=2: equal-bit states are uncut -> q = -(0,1,1,0)."""
+    q = O.maxcut_q(2, [0], [1])
+    assert list(q) == [0.0, -1.0, -1.0, 0.0]
+
+
+# ---------------------------------------------------------------- phase / expectation ----
+def test_phase_spec_example():
+    """P15: SPEC.md:129-131: gamma=pi, o=(0,1,2,3), uniform_4 -> (1,-1,1,-1)/2."""
+    psi = O.init_uniform(4)
+    O.phase(psi, np.array([0.0, 1, 2, 3]), math.pi)
+    np.testing.assert_allclose(psi, np.array([1, -1, 1, -1]) / 2, atol=1e-15)
+
+
+def test_phase_vs_expm_diag():
+    """exp(-i gamma diag(q)) via scipy expm (Eq. 3)."""
+    rng = np.random.default_rng(3)
+    N = 32
+    q = rng.standard_normal(N)
+    psi = _rand_state(N, rng)
+    ref = expm(-1j * 0.77 * np.diag(q)) @ psi
+    O.phase(psi, q, 0.77)
+    np.testing.assert_allclose(psi, ref, atol=1e-14)
+
+
+def test_expectation_spec_examples():
+    """P15: SPEC.md:65-66: uniform over N=4, q=(0,1,2,3) -> 1.5; basis |k> -> q_k."""
+    q = np.array([0.0, 1, 2, 3])
+    assert O.expectation(O.init_uniform(4), q) == pytest.approx(1.5, abs=1e-15)
+    for k in range(4):
+        e = np.zeros(4, np.complex128)
+        e[k] = 1j
+        assert O.expectation(e, q) == q[k]
+    assert O.norm2(O.init_uniform(1024)) == pytest.approx(1.0, abs=1e-15)
+
+
+def test_probabilities():
+    rng = np.random.default_rng(5)
+    psi = _rand_state(64, rng)
+    np.testing.assert_allclose(O.probabilities(psi), np.abs(psi) ** 2, rtol=1e-15)
+
+
+# ---------------------------------------------------------------- X mixer (P1..P4) ----
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8])
+def test_P1_mixer_x_vs_dense_expm(n):
+    """P1: U_M(beta) = expm(-i beta sum_j X_j) (R1) via scipy."""
+    rng = np.random.default_rng(100 + n)
+    psi = _rand_state(1 << n, rng)
+    beta = 0.91
+    ref = expm(-1j * beta * O.dense_sum_x(n)) @ psi
+    O.mixer_x(psi, beta)
+    np.testing.assert_allclose(psi, ref, atol=1e-13)
+
+
+def test_P1_full_qaoa_vs_dense():
+    """P1: full p-layer QAOA vs products of dense expm, n=6, p=3."""
+    rng = np.random.default_rng(7)
+    n = 6
+    u, v = random_regular_graph(n, 3, rng)
+    q = O.maxcut_q(n, u, v)
+    theta = rng.uniform(0, math.pi, 6)
+    W = O.dense_sum_x(n)
+    ref = np.full(1 << n, 1 / math.sqrt(1 << n), np.complex128)
+    for k in range(3):
+        ref = expm(-1j * theta[2 * k] * np.diag(q)) @ ref
+        ref = expm(-1j * theta[2 * k + 1] * W) @ ref
+    psi = O.evolve_x(n, q, theta)
+    np.testing.assert_allclose(psi, ref, atol=1e-12)
+
+
+def test_P2_basis_state_closed_form():
+    """P2: <y|U_M|x0> = cos^{n-d} beta (-i sin beta)^d, d = popcount(x0 ^ y)."""
+    n, beta, x0 = 12, 0.6, 0b101100111010
+    psi = np.zeros(1 << n, np.complex128)
+    psi[x0] = 1.0
+    O.mixer_x(psi, beta)
+    ys = np.arange(1 << n)
+    d = np.array([bin(int(y) ^ x0).count("1") for y in ys])
+    ref = np.cos(beta) ** (n - d) * (-1j * np.sin(beta)) ** d
+    np.testing.assert_allclose(psi, ref, atol=1e-15)
+
+
+def test_P3_special_angles():
+    """P3: beta=pi/2 -> (-i)^n psi[x ^ (2^n-1)]; beta=pi -> (-1)^n psi; beta=0 -> identity."""
+    n = 9
+    rng = np.random.default_rng(9)
+    psi = _rand_state(1 << n, rng)
+    a = psi.copy()
+    O.mixer_x(a, math.pi / 2)
+    np.testing.assert_allclose(a, (-1j) ** n * psi[np.arange(1 << n) ^ ((1 << n) - 1)], atol=1e-14)
+    b = psi.copy()
+    O.mixer_x(b, math.pi)
+    np.testing.assert_allclose(b, (-1) ** n * psi, atol=1e-14)
+    c = psi.copy()
+    O.mixer_x(c, 0.0)
+    np.testing.assert_array_equal(c, psi)
+
+
+def test_P4_plus_eigenstate_and_semigroup():
+    """P4: U_M(beta)|+> = e^{-i beta n}|+>;  U_M(b1) U_M(b2) = U_M(b1 + b2)."""
+    n = 10
+    psi = O.init_uniform(1 << n)
+    O.mixer_x(psi, 0.37)
+    np.testing.assert_allclose(psi, np.exp(-1j * 0.37 * n) / math.sqrt(1 << n), atol=1e-14)
+    rng = np.random.default_rng(4)
+    s = _rand_state(1 << n, rng)
+    a = s.copy()
+    O.mixer_x(a, 0.2)
+    O.mixer_x(a, 0.5)
+    b = s.copy()
+    O.mixer_x(b, 0.7)
+    np.testing.assert_allclose(a, b, atol=1e-14)
+
+
+# ---------------------------------------------------------------- invariants (P5, P6) ----
+def test_P5_norm_and_P6_theta_zero():
+    """P5: |norm^2 - 1| <= 1e-12; P6: theta=0 -> <Q> = mean(q) = -sum(w)/2."""
+    wl = make_config("cfg1")
+    q = O.maxcut_q(wl.n_qubits, wl.edges_u, wl.edges_v)
+    psi = O.evolve_x(wl.n_qubits, q, wl.theta)
+    assert abs(O.norm2(psi) - 1) <= 1e-12
+    psi0 = O.evolve_x(wl.n_qubits, q, np.zeros(2 * wl.p))
+    assert O.expectation(psi0, q) == pytest.approx(-len(wl.edges_u) / 2, rel=1e-13)
+    assert len(wl.edges_u) == 15  # 3-regular on 10 vertices -> -7.5
+
+
+# ---------------------------------------------------------------- analytic p=1 (P7, P8) ----
+@pytest.mark.parametrize("n", [4, 5, 8, 11])
+def test_P7_ring_closed_form(n):
+    """P7: ring C_n, unit weights, q=-cut, p=1:  <Q> = -n/2 + (n/4) sin(4b) sin(2g)."""
+    u = np.arange(n)
+    v = (u + 1) % n
+    uu, vv = np.minimum(u, v), np.maximum(u, v)
+    q = O.maxcut_q(n, uu, vv)
+    for g, b in [(0.7, 0.3), (2.1, 1.3), (0.05, 2.9)]:
+        f = O.expectation(O.evolve_x(n, q, [g, b]), q)
+        assert f == pytest.approx(-n / 2 + (n / 4) * math.sin(4 * b) * math.sin(2 * g), abs=1e-12)
+
+
+def _p1_weighted_closed_form(n, u, v, w, g, b):
+    """P8: weighted p=1 max-cut closed form (Heisenberg picture), q = -cut_w."""
+    W = {}
+    for a, c, x in zip(u, v, w):
+        W[(int(a), int(c))] = x
+        W[(int(c), int(a))] = x
+    nbr = {i: set() for i in range(n)}
+    for a, c in zip(u, v):
+        nbr[int(a)].add(int(c))
+        nbr[int(c)].add(int(a))
+    total = 0.0
+    for a, c, wuv in zip(u, v, w):
+        a, c = int(a), int(c)
+        Pu = np.prod([math.cos(g * W[(a, k)]) for k in nbr[a] - {c}])
+        Pv = np.prod([math.cos(g * W[(c, k)]) for k in nbr[c] - {a}])
+        T = (nbr[a] & nbr[c])
+        U = nbr[a] - T - {c}
+        V = nbr[c] - T - {a}
+        t1 = 0.5 * math.sin(4 * b) * math.sin(g * wuv) * (Pu + Pv)
+        pu = np.prod([math.cos(g * W[(a, k)]) for k in U])
+        pv = np.prod([math.cos(g * W[(c, k)]) for k in V])
+        tm = np.prod([math.cos(g * (W[(a, k)] - W[(c, k)])) for k in T])
+        tp = np.prod([math.cos(g * (W[(a, k)] + W[(c, k)])) for k in T])
+        t2 = 0.5 * math.sin(2 * b) ** 2 * pu * pv * (tm - tp)
+        zz = t1 + t2
+        total += wuv / 2 * (zz - 1)
+    return total
+
+
+def test_P8_weighted_p1_closed_form():
+    """P8 on G(9, 0.5) with triangles and random weights."""
+    rng = np.random.default_rng(8)
+    n = 9
+    u, v = erdos_renyi_graph(n, 0.5, rng)
+    w = rng.uniform(0, 1, len(u))
+    q = O.maxcut_q(n, u, v, w)
+    for g, b in [(0.9, 0.4), (2.5, 2.2)]:
+        f = O.expectation(O.evolve_x(n, q, [g, b]), q)
+        assert f == pytest.approx(_p1_weighted_closed_form(n, u, v, w, g, b), abs=1e-12)
+
+
+# ---------------------------------------------------------------- light cone (P9) ----
+@pytest.mark.parametrize("n,d,p,weighted", [(12, 3, 2, False), (14, 3, 2, True), (12, 4, 1, True), (10, 3, 3, False)])
+def test_P9_lightcone_equals_full_state(n, d, p, weighted):
+    """P9: light-cone <Q> equals the full-state oracle (exact reduction)."""
+    rng = np.random.default_rng(n * 10 + p)
+    u, v = random_regular_graph(n, d, rng)
+    w = rng.uniform(0, 1, len(u)) if weighted else None
+    theta = rng.uniform(0, math.pi, 2 * p)
+    q = O.maxcut_q(n, u, v, w)
+    full = O.expectation(O.evolve_x(n, q, theta), q)
+    lc, sizes = O.lightcone_maxcut(n, u, v, w, theta)
+    assert lc == pytest.approx(full, rel=1e-12, abs=1e-12)
+    assert sizes.max() <= n
+
+
+# ---------------------------------------------------------------- circulant (P10, P11) ----
+@pytest.mark.parametrize("N", [2, 7, 13, 16, 31, 60])
+def test_P11_circulant_dense_vs_expm_symmetric_row(N):
+    """P11: symmetric first row w: C = circulant(w), lambda = fft(w) (R4) -> expm(-i b C) psi."""
+    rng = np.random.default_rng(N)
+    w = rng.uniform(-1, 1, N)
+    w = 0.5 * (w + np.roll(w[::-1], 1))  # w_k = w_{N-k}
+    C = circulant(w)
+    assert np.allclose(C, C.T)
+    lam = np.fft.fft(w).real
+    psi = _rand_state(N, rng)
+    ref = expm(-1j * 0.83 * C) @ psi
+    O.mixer_circulant_dense(psi, lam, 0.83)
+    np.testing.assert_allclose(psi, ref, atol=1e-12)
+
+
+@pytest.mark.parametrize("N", [5, 64, 97, 210, 1024])
+def test_P11_circulant_dense_vs_numpy_fft(N):
+    """P11: arbitrary real spectrum: ifft(exp(-i b lambda) * fft(psi)) (numpy pocketfft)."""
+    rng = np.random.default_rng(N + 1)
+    lam = rng.standard_normal(N) * 3
+    psi = _rand_state(N, rng)
+    ref = np.fft.ifft(np.exp(-1j * 1.9 * lam) * np.fft.fft(psi))
+    O.mixer_circulant_dense(psi, lam, 1.9)
+    np.testing.assert_allclose(psi, ref, atol=1e-12)
+
+
+@pytest.mark.parametrize("N", [2, 6, 24, 120])
+def test_P10_complete_closed_form_vs_expm_laplacian(N):
+    """P10: K_N Laplacian L = N I - J has spectrum (0, N, ..., N) (cfg3, R5).
+    Closed form vs expm(-i b L) and vs the dense circulant definition."""
+    rng = np.random.default_rng(N)
+    psi = _rand_state(N, rng)
+    L = N * np.eye(N) - np.ones((N, N))
+    ref = expm(-1j * 0.41 * L) @ psi
+    a = psi.copy()
+    O.mixer_complete(a, 0.41, 0.0, float(N))
+    np.testing.assert_allclose(a, ref, atol=1e-12)
+    b = psi.copy()
+    lam = np.full(N, float(N))
+    lam[0] = 0.0
+    O.mixer_circulant_dense(b, lam, 0.41)
+    np.testing.assert_allclose(b, ref, atol=1e-12)
+    # adjacency of K_N: spectrum (N-1, -1, ..., -1)
+    A = np.ones((N, N)) - np.eye(N)
+    c = psi.copy()
+    O.mixer_complete(c, 0.41, N - 1.0, -1.0)
+    np.testing.assert_allclose(c, expm(-1j * 0.41 * A) @ psi, atol=1e-12)
+
+
+def test_P10_complete_at_cfg3_size_vs_numpy_fft():
+    """P10 at N = 10! (cfg3 size): closed form vs numpy.fft definition."""
+    N = math.factorial(10)
+    rng = np.random.default_rng(33)
+    psi = _rand_state(N, rng)
+    lam = np.full(N, float(N))
+    lam[0] = 0.0
+    ref = np.fft.ifft(np.exp(-1j * 1.1 * lam) * np.fft.fft(psi))
+    O.mixer_complete(psi, 1.1, 0.0, float(N))
+    np.testing.assert_allclose(psi, ref, atol=1e-12)
+
+
+def test_P4_circulant_uniform_and_semigroup():
+    """P4 for the circulant: uniform state is the j=0 mode -> e^{-i b lambda_0} uniform;
+    semigroup U(b1)U(b2) = U(b1+b2)."""
+    N = 48
+    rng = np.random.default_rng(2)
+    lam = rng.standard_normal(N)
+    u = O.init_uniform(N)
+    O.mixer_circulant_dense(u, lam, 0.7)
+    np.testing.assert_allclose(u, np.exp(-1j * 0.7 * lam[0]) / math.sqrt(N), atol=1e-14)
+    s = _rand_state(N, rng)
+    a = s.copy()
+    O.mixer_circulant_dense(a, lam, 0.3)
+    O.mixer_circulant_dense(a, lam, 0.9)
+    b = s.copy()
+    O.mixer_circulant_dense(b, lam, 1.2)
+    np.testing.assert_allclose(a, b, atol=1e-12)
+
+
+def test_qwoa_evolve_complete_vs_dense():
+    """Full QWOA evolution closed-form mixer vs dense circulant definition."""
+    N = 120
+    rng = np.random.default_rng(12)
+    q = rng.standard_normal(N)
+    theta = rng.uniform(0, math.pi, 8)
+    lam = np.full(N, float(N))
+    lam[0] = 0.0
+    a = O.evolve_complete(q, theta, 0.0, float(N))
+    b = O.evolve_circulant_dense(q, lam, theta)
+    np.testing.assert_allclose(a, b, atol=1e-12)
+    assert abs(O.norm2(a) - 1) < 1e-12
+
+
+# ---------------------------------------------------------------- sparse (P12) ----
+def test_P12_sparse_dense_spec_example():
+    """P12: SPEC.md:159-161: N=2, W=X, t=pi/2, |0> -> -i|1>."""
+    out = O.mixer_sparse_dense(np.array([1.0, 0.0], np.complex128), O.dense_sum_x(1), math.pi / 2)
+    np.testing.assert_allclose(out, [0, -1j], atol=1e-15)
+
+
+# ---------------------------------------------------------------- FD gradient (P13) ----
+def test_P13_central_difference_gradient_vs_analytic_ring():
+    """P13: batch order [theta, theta+h e1, theta-h e1, ...] (R12) and central differences
+    reproduce d<Q>/d(gamma, beta) of the P7 closed form to O(h^2) + roundoff."""
+    n = 8
+    u = np.arange(n)
+    v = (u + 1) % n
+    q = O.maxcut_q(n, np.minimum(u, v), np.maximum(u, v))
+    theta = np.array([0.7, 0.3])
+    h = 1e-6
+    B = fd_batch_thetas(theta, h)
+    f = np.array([O.expectation(O.evolve_x(n, q, t), q) for t in B])
+    grad = [(f[1 + 2 * k] - f[2 + 2 * k]) / (2 * h) for k in range(2)]
+    g, b = theta
+    dg = (n / 4) * math.sin(4 * b) * 2 * math.cos(2 * g)
+    db = (n / 4) * 4 * math.cos(4 * b) * math.sin(2 * g)
+    assert grad[0] == pytest.approx(dg, abs=2e-8)
+    assert grad[1] == pytest.approx(db, abs=2e-8)
+
+
+# ---------------------------------------------------------------- inputs module ----
+def test_input_recipes():
+    for name, (N, p) in {"cfg1": (1024, 2), "cfg4": (1 << 30, 3), "cfg5": (1 << 34, 2)}.items():
+        wl = make_config(name)
+        assert wl.dim == N and wl.p == p and len(wl.theta) == 2 * p
+        assert np.all((wl.theta > 0) & (wl.theta < math.pi))
+        deg = np.bincount(np.concatenate([wl.edges_u, wl.edges_v]), minlength=wl.n_qubits)
+        assert len(set(deg.tolist())) == 1
+        assert np.all(wl.edges_u < wl.edges_v)
+    wl2 = make_config("cfg2")
+    assert wl2.batch_thetas.shape == (21, 10)
+    wl3 = make_config("cfg3", n_override=720)
+    assert wl3.dim == 720 and wl3.q.shape == (720,)
+    # determinism
+    assert np.array_equal(make_config("cfg4").edges_u, make_config("cfg4").edges_u)
