@@ -1,0 +1,194 @@
+/*
+ * qva.h -- C ABI of the B200-native QVA state-evolution library (libqva.so).
+ *
+ * The library computes, on NVIDIA B200 (sm_100a) GPUs, the full-state evolution of a
+ * p-layer quantum variational ansatz and its objective (arXiv 2110.03963, PAPER.md):
+ *
+ *   |psi(theta)> = prod_{k=1..p} U_M(beta_k) U_Q(gamma_k) |psi0>        Eq. 1,
+ *                                                                     Eq. qaoa (:185), Eq. qwoa (:298)
+ *   f(theta)     = <psi|Q|psi> = sum_x |psi_x|^2 q_x                   Eq. 2
+ *
+ *   U_Q(gamma) = exp(-i gamma Q), Q = diag(q)                          Eq. 3 / phase_shift_qaoa (:62-69, :152-155)
+ *   U_M(beta)  = exp(-i beta W) with W one of
+ *     QVA_MIXER_X         W = sum_j X_j (hypercube)                    Eq. mixing_qaoa (:159-171), reading R1
+ *     QVA_MIXER_CIRCULANT W circulant, F^-1 diag(e^{-i beta lambda}) F  Sec. 3 (:315-333), readings R3, R4
+ *     QVA_MIXER_SPARSE    W real symmetric CSR, truncated Taylor action Sec. 3 (:333), reading R13
+ *
+ * Conventions (all calls):
+ *  - theta layout [gamma_1, beta_1, ..., gamma_p, beta_p] (reading R7); layer 1 acts first (R6).
+ *  - States are complex128 stored as interleaved (re, im) doubles, index x = sum_j bit_j 2^j.
+ *  - Every pointer argument is a CALLER-OWNED HOST buffer unless the name ends in _device
+ *    (a device pointer on the plan's device).  The library copies in/out and never retains or
+ *    frees caller memory.  The plan owns all device memory (state, q, spectrum, CSR, scratch,
+ *    receive buffers) and the NCCL communicator, and frees them in qva_plan_destroy
+ *    (Table 1 "destroy").
+ *  - Every call returns qva_status; no exception or abort crosses the ABI.  On error a
+ *    thread-local message is available from qva_last_error().  After a failed evolve the plan
+ *    remains valid but the state is unspecified.
+ *  - Calls are synchronous with respect to the host: they return after the device work they
+ *    enqueue on the plan's stream has completed.
+ *  - Multi-process (world > 1): every rank makes the same calls with the same theta (the paper
+ *    broadcasts theta from rank 0; here the caller does).  Global offsets are used
+ *    for set_xxx and get_xxx ranges; each rank only accepts/returns indices of its own partition
+ *    (COMM-psi contiguous blocks, Eqs. local_i / offset).
+ *  - A plan is single-threaded; several plans may coexist.
+ */
+#ifndef QVA_H
+#define QVA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* every qva_* symbol is exported from libqva.so */
+#endif
+
+typedef struct qva_plan qva_plan; /* opaque */
+
+typedef enum {
+    QVA_OK = 0,
+    QVA_ERR_INVALID_ARGUMENT = 1, /* structural error: NULL/negative/shape error */
+    QVA_ERR_SIZE_MISMATCH = 2,    /* range outside the partition / wrong length */
+    QVA_ERR_NOT_READY = 3,        /* evolve/expectation before set_qualities ("required") */
+    QVA_ERR_NUMERIC = 4,          /* non-finite q/theta/lambda, Taylor non-convergence */
+    QVA_ERR_UNSUPPORTED = 5,      /* e.g. X mixer with dim != 2^n, non-power-of-two world */
+    QVA_ERR_OUT_OF_MEMORY = 6,
+    QVA_ERR_CUDA = 7,
+    QVA_ERR_NCCL = 8
+} qva_status;
+
+typedef enum { QVA_MIXER_X = 0, QVA_MIXER_CIRCULANT = 1, QVA_MIXER_SPARSE = 2 } qva_mixer;
+
+typedef struct {
+    uint64_t dim;            /* N = number of basis states of the (sub)space; X mixer: 2^n_qubits */
+    int32_t n_qubits;        /* log2(dim) for QVA_MIXER_X, else -1 (ignored)                      */
+    int32_t mixer;           /* qva_mixer                                                         */
+    int32_t rank;            /* this process's rank in [0, world)                                 */
+    int32_t world;           /* number of processes (one GPU each); 1 = single GPU                */
+    const void *nccl_unique_id; /* 128-byte ncclUniqueId (from qva_nccl_unique_id on rank 0) when
+                                   world > 1; NULL otherwise                                      */
+    int32_t device;          /* CUDA device ordinal                                               */
+    int32_t virtual_shards;  /* >1: simulate this many COMM-psi shards on ONE device with a
+                                loopback transport (tests the sharded schedule on one GPU); world
+                                must be 1.  0 or 1: normal                                        */
+    void *stream;            /* cudaStream_t to launch on, or NULL (the plan creates one)         */
+    int32_t max_batch;       /* largest B for qva_evolve_batch (0 -> 1)                           */
+    int32_t reserved[7];
+} qva_plan_desc;
+
+/* ---- lifecycle (Table 1 plan / destroy) ------------------------------------ */
+
+/* Allocates device memory for the state (and the sharding receive buffer / batch states).
+ * QVA_ERR_UNSUPPORTED: X mixer with dim != 2^n_qubits, world not a power of two for the X
+ * mixer, world > 1 for the circulant or sparse mixer (not implemented yet). */
+qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out);
+/* NULL-safe; frees everything the plan owns. */
+qva_status qva_plan_destroy(qva_plan *plan);
+/* COMM-psi partition of this rank: local_n = local_i, offset = local_i_offset
+ * (Eqs. local_i, offset).  Contiguous equal blocks for power-of-two N
+ * (rank = top log2(world) index bits); remainder to the lowest ranks otherwise (R16). */
+qva_status qva_plan_get_partition(const qva_plan *plan, uint64_t *local_n, uint64_t *offset);
+/* Host-only partition rule (no plan / no GPU needed): same rule as above. */
+qva_status qva_partition(uint64_t dim, int32_t world, int32_t rank, uint64_t *local_n, uint64_t *offset);
+
+/* ---- operators (Table 2 observable/operator functions) ---------------------- */
+
+/* q[0..count) -> diag(Q) entries [offset, offset+count) (global indices within this rank's
+ * partition).  Chunked uploads allowed.  QVA_ERR_NUMERIC on a non-finite value. */
+qva_status qva_set_qualities(qva_plan *plan, const double *q, uint64_t offset, uint64_t count);
+/* Same from a device pointer (count doubles on the plan's device). */
+qva_status qva_set_qualities_device(qva_plan *plan, const double *q_device, uint64_t offset, uint64_t count);
+/* On-device generation of the max-cut qualities q_x = -cut_w(x) = -sum_e w_e [bit_u(x) != bit_v(x)]
+ * (Eq. maxcut-cost, cfg sign R10) for the whole partition.  u, v: m vertex
+ * indices in [0, n_qubits); w: m weights or NULL for unit weights.  X mixer only. */
+qva_status qva_set_qualities_maxcut(qva_plan *plan, int32_t m, const int32_t *u, const int32_t *v,
+                                    const double *w);
+
+/* Copy diag(Q) entries [offset, offset+count) (global, this rank's partition, layout of the
+ * partition) back to q_out[count]. */
+qva_status qva_get_qualities(qva_plan *plan, double *q_out, uint64_t offset, uint64_t count);
+
+/* Circulant spectrum lambda[j], j = forward-DFT bin (numpy sign convention, R4), entries
+ * [offset, offset+count) of the global length-dim array. */
+qva_status qva_set_circulant_eigenvalues(qva_plan *plan, const double *lambda, uint64_t offset, uint64_t count);
+/* Spectrum of the form (lambda0, c, c, ..., c): the complete-graph family (adjacency: (N-1, -1);
+ * Laplacian: (0, N), cfg3) without storing an N-length array. */
+qva_status qva_set_circulant_eigenvalues_const(qva_plan *plan, double lambda0, double c);
+
+/* Real symmetric sparse mixer W in CSR: rows [0, dim), row_ptr[dim+1]
+ * (int64, row_ptr[0] = 0), col[nnz] (int32), val[nnz] (fp64; NULL = all ones).  The Taylor
+ * action uses s = max(1, ceil(|beta| ||W||_1 / 3)) sub-steps of degree <= 40 (reading R13). */
+qva_status qva_set_sparse_mixer(qva_plan *plan, const int64_t *row_ptr, const int32_t *col,
+                                const double *val, uint64_t nnz);
+
+/* Optional initial state psi0 (default |+>, PAPER.md:174-178 / R2): interleaved re,im,
+ * entries [offset, offset+count). */
+qva_status qva_set_initial_state(qva_plan *plan, const double *re_im, uint64_t offset, uint64_t count);
+/* Return to the default |+> initial state. */
+qva_status qva_clear_initial_state(qva_plan *plan);
+
+/* ---- evolution (Table 3 evolve_state) --------------------------------------- */
+
+/* psi <- psi0 (current state reset). */
+qva_status qva_reset_state(qva_plan *plan);
+/* Step-level operations on the current state (for parity tests of each step). */
+qva_status qva_apply_phase(qva_plan *plan, double gamma);
+qva_status qva_apply_mixer(qva_plan *plan, double beta);
+/* psi <- prod_k U_M(beta_k) U_Q(gamma_k) psi0; theta[2p] host array.  Always restarts from psi0. */
+qva_status qva_evolve(qva_plan *plan, const double *theta, int32_t p);
+/* <psi|Q|psi> of the current state, globally reduced; every rank receives it (Eq. 2). */
+qva_status qva_expectation(qva_plan *plan, double *out);
+/* sum_x |psi_x|^2 (norm check). */
+qva_status qva_norm2(qva_plan *plan, double *out);
+/* Copy amplitudes [offset, offset+count) (global, within this rank's partition) to re_im[2*count]. */
+qva_status qva_get_state(qva_plan *plan, double *re_im, uint64_t offset, uint64_t count);
+/* p_x = |psi_x|^2 for [offset, offset+count) (Table 3 get_probabilities). */
+qva_status qva_get_probabilities(qva_plan *plan, double *out, uint64_t offset, uint64_t count);
+
+/* B independent evolutions (e.g. the 2|theta|+1 central-difference sets of the parallel
+ * gradient) sharing Q: thetas[B][2p] -> f_out[B] = <psi_b|Q|psi_b>.  With
+ * world > 1 the B sets are split across ranks (COMM-grad_f analogue) and every rank receives
+ * all B values.  The current state afterwards is unspecified.  B <= desc.max_batch. */
+qva_status qva_evolve_batch(qva_plan *plan, const double *thetas, int32_t B, int32_t p, double *f_out);
+
+/* ---- NCCL bootstrap (multi-process) ------------------------------------------------------------- */
+
+/* Writes a 128-byte ncclUniqueId into id_out (call on rank 0, broadcast to the other ranks). */
+qva_status qva_nccl_unique_id(void *id_out);
+/* Host-only: which batch entries [first, first+count) rank `rank` evolves (B split across ranks,
+ * remainder to the lowest ranks). */
+qva_status qva_batch_partition(int32_t B, int32_t world, int32_t rank, int32_t *first, int32_t *count);
+
+/* ---- introspection ---------------------------------------------------------------------------- */
+
+/* Pass schedule the X-mixer path uses for (n_local, p): writes up to cap entries of
+ * (tile_set_index, n_rot_before_phase, has_phase, n_rot_after_phase) as 4 int32 per pass and
+ * returns the pass count in *n_passes.  Host-only. */
+qva_status qva_x_schedule(int32_t n_local, int32_t p, int32_t *out, int32_t cap, int32_t *n_passes);
+/* Kernel timing: when enabled, every kernel launch of the plan is bracketed with CUDA events
+ * on the plan's stream; qva_kernel_stats returns, for kernel class `which` (0 = X tile pass,
+ * 1 = small-state fused evolve, 2 = FFT column pass, 3 = FFT row pass, 4 = sparse SpMV,
+ * 5 = reduction, 6 = exchange), the summed device milliseconds, launches and algorithmic
+ * bytes since the last reset. */
+qva_status qva_set_profiling(qva_plan *plan, int32_t enable);
+qva_status qva_kernel_stats(qva_plan *plan, int32_t which, double *ms, int64_t *launches, double *bytes);
+qva_status qva_reset_kernel_stats(qva_plan *plan);
+/* Number of kernel launches issued by the plan since the last reset (all classes). */
+qva_status qva_launch_count(qva_plan *plan, int64_t *launches);
+
+const char *qva_status_string(qva_status s);
+const char *qva_last_error(void);
+/* Library version string. */
+const char *qva_version(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QVA_H */

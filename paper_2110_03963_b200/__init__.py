@@ -1,0 +1,309 @@
+"""B200-native QVA state evolution (arXiv 2110.03963 hot path) -- Python binding.
+
+Thin ctypes marshalling over libqva.so (include/qva.h).  Every step of the method runs in
+the sm_100a kernels behind the C ABI; this module only converts arguments.  There is no
+CPU fallback: the first call into the package without the built library raises ImportError.
+
+Module-level functions carry the ABI names (qva_plan_create, qva_set_qualities, qva_evolve,
+qva_expectation, qva_evolve_batch, ...); `Plan` is a convenience owner of one plan handle.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqva.so")
+
+MIXER_X, MIXER_CIRCULANT, MIXER_SPARSE = 0, 1, 2
+_MIXERS = {"x": MIXER_X, "circulant": MIXER_CIRCULANT, "sparse": MIXER_SPARSE}
+KERNEL_CLASSES = {"tile": 0, "small": 1, "fft_col": 2, "fft_row": 3, "spmv": 4, "reduce": 5,
+                  "exchange": 6, "other": 7}
+
+
+class QvaError(RuntimeError):
+    def __init__(self, func: str, status: int, msg: str):
+        super().__init__(f"{func}: {status_string(status)}: {msg}")
+        self.status = status
+
+
+class PlanDesc(ctypes.Structure):
+    _fields_ = [
+        ("dim", ctypes.c_uint64),
+        ("n_qubits", ctypes.c_int32),
+        ("mixer", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("nccl_unique_id", ctypes.c_void_p),
+        ("device", ctypes.c_int32),
+        ("virtual_shards", ctypes.c_int32),
+        ("stream", ctypes.c_void_p),
+        ("max_batch", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 7),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2110_03963_b200.build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, u64, i32, d = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double
+    sig = {
+        "qva_plan_create": [ctypes.POINTER(PlanDesc), ctypes.POINTER(P)],
+        "qva_plan_destroy": [P],
+        "qva_plan_get_partition": [P, ctypes.POINTER(u64), ctypes.POINTER(u64)],
+        "qva_partition": [u64, i32, i32, ctypes.POINTER(u64), ctypes.POINTER(u64)],
+        "qva_set_qualities": [P, P, u64, u64],
+        "qva_set_qualities_device": [P, P, u64, u64],
+        "qva_set_qualities_maxcut": [P, i32, P, P, P],
+        "qva_get_qualities": [P, P, u64, u64],
+        "qva_set_circulant_eigenvalues": [P, P, u64, u64],
+        "qva_set_circulant_eigenvalues_const": [P, d, d],
+        "qva_set_sparse_mixer": [P, P, P, P, u64],
+        "qva_set_initial_state": [P, P, u64, u64],
+        "qva_clear_initial_state": [P],
+        "qva_reset_state": [P],
+        "qva_apply_phase": [P, d],
+        "qva_apply_mixer": [P, d],
+        "qva_evolve": [P, P, i32],
+        "qva_expectation": [P, ctypes.POINTER(d)],
+        "qva_norm2": [P, ctypes.POINTER(d)],
+        "qva_get_state": [P, P, u64, u64],
+        "qva_get_probabilities": [P, P, u64, u64],
+        "qva_evolve_batch": [P, P, i32, i32, P],
+        "qva_nccl_unique_id": [P],
+        "qva_batch_partition": [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)],
+        "qva_x_schedule": [i32, i32, P, i32, ctypes.POINTER(i32)],
+        "qva_set_profiling": [P, i32],
+        "qva_kernel_stats": [P, i32, ctypes.POINTER(d), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(d)],
+        "qva_reset_kernel_stats": [P],
+        "qva_launch_count": [P, ctypes.POINTER(ctypes.c_int64)],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    for name in ("qva_status_string", "qva_last_error", "qva_version"):
+        getattr(L, name).restype = ctypes.c_char_p
+    L.qva_status_string.argtypes = [ctypes.c_int]
+    return L
+
+
+_L = None
+
+
+def lib():
+    """The loaded libqva.so (loaded on first use so the build module can run without it)."""
+    global _L
+    if _L is None:
+        _L = _load()
+    return _L
+
+
+def status_string(s: int) -> str:
+    return lib().qva_status_string(int(s)).decode()
+
+
+def _call(name: str, *args):
+    st = getattr(lib(), name)(*args)
+    if st != 0:
+        raise QvaError(name, st, lib().qva_last_error().decode())
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def qva_version() -> str:
+    return lib().qva_version().decode()
+
+
+def qva_partition(dim: int, world: int, rank: int):
+    n, o = ctypes.c_uint64(), ctypes.c_uint64()
+    _call("qva_partition", dim, world, rank, ctypes.byref(n), ctypes.byref(o))
+    return n.value, o.value
+
+
+def qva_batch_partition(B: int, world: int, rank: int):
+    f, c = ctypes.c_int32(), ctypes.c_int32()
+    _call("qva_batch_partition", B, world, rank, ctypes.byref(f), ctypes.byref(c))
+    return f.value, c.value
+
+
+def qva_x_schedule(n_local: int, p: int):
+    """[(tile_set, n_rot_before_phase, has_phase, n_rot_after_phase)] of the X-mixer passes."""
+    cap = 4 * (3 * p + 8)
+    out = np.zeros(4 * cap, np.int32)
+    n = ctypes.c_int32()
+    _call("qva_x_schedule", n_local, p, _ptr(out), cap, ctypes.byref(n))
+    return [tuple(int(v) for v in out[4 * i:4 * i + 4]) for i in range(n.value)]
+
+
+def qva_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _call("qva_nccl_unique_id", ctypes.cast(buf, ctypes.c_void_p))
+    return buf.raw
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Plan:
+    """Owns one qva_plan.  Method names follow the C ABI without the `qva_` prefix."""
+
+    def __init__(self, dim: int, mixer: str = "x", n_qubits: int = -1, rank: int = 0, world: int = 1,
+                 nccl_id: Optional[bytes] = None, device: int = 0, virtual_shards: int = 1,
+                 stream: Optional[int] = None, max_batch: int = 1, replicated: bool = False):
+        self._h = ctypes.c_void_p()
+        self._id_buf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+        d = PlanDesc()
+        d.dim = dim
+        d.n_qubits = n_qubits
+        d.mixer = _MIXERS[mixer] if isinstance(mixer, str) else int(mixer)
+        d.rank = rank
+        d.world = world
+        d.nccl_unique_id = ctypes.cast(self._id_buf, ctypes.c_void_p) if self._id_buf is not None else None
+        d.device = device
+        d.virtual_shards = virtual_shards
+        d.stream = stream
+        d.max_batch = max_batch
+        d.reserved[0] = 1 if replicated else 0
+        _call("qva_plan_create", ctypes.byref(d), ctypes.byref(self._h))
+        self.dim, self.mixer, self.world, self.rank = dim, mixer, world, rank
+
+    # ---- lifecycle
+    def destroy(self):
+        if self._h:
+            _call("qva_plan_destroy", self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.destroy()
+
+    def get_partition(self):
+        n, o = ctypes.c_uint64(), ctypes.c_uint64()
+        _call("qva_plan_get_partition", self._h, ctypes.byref(n), ctypes.byref(o))
+        return n.value, o.value
+
+    # ---- operators
+    def set_qualities(self, q, offset: int = 0):
+        q = _f64(q)
+        _call("qva_set_qualities", self._h, _ptr(q), offset, len(q))
+
+    def set_qualities_device(self, ptr: int, offset: int, count: int):
+        _call("qva_set_qualities_device", self._h, ctypes.c_void_p(ptr), offset, count)
+
+    def set_qualities_maxcut(self, u, v, w=None):
+        u = np.ascontiguousarray(u, np.int32)
+        v = np.ascontiguousarray(v, np.int32)
+        w = None if w is None else _f64(w)
+        _call("qva_set_qualities_maxcut", self._h, len(u), _ptr(u), _ptr(v), _ptr(w))
+
+    def get_qualities(self, offset: int = 0, count: Optional[int] = None, out: Optional[np.ndarray] = None):
+        if count is None:
+            n, o = self.get_partition()
+            offset, count = o, n
+        if out is None:
+            out = np.empty(count, np.float64)
+        _call("qva_get_qualities", self._h, _ptr(out), offset, count)
+        return out
+
+    def set_circulant_eigenvalues(self, lam, offset: int = 0):
+        lam = _f64(lam)
+        _call("qva_set_circulant_eigenvalues", self._h, _ptr(lam), offset, len(lam))
+
+    def set_circulant_eigenvalues_const(self, lam0: float, c: float):
+        _call("qva_set_circulant_eigenvalues_const", self._h, float(lam0), float(c))
+
+    def set_sparse_mixer(self, row_ptr, col, val=None):
+        row_ptr = np.ascontiguousarray(row_ptr, np.int64)
+        col = np.ascontiguousarray(col, np.int32)
+        val = None if val is None else _f64(val)
+        _call("qva_set_sparse_mixer", self._h, _ptr(row_ptr), _ptr(col), _ptr(val), len(col))
+
+    def set_initial_state(self, psi, offset: int = 0):
+        psi = np.ascontiguousarray(psi, np.complex128)
+        _call("qva_set_initial_state", self._h, _ptr(psi), offset, len(psi))
+
+    def clear_initial_state(self):
+        _call("qva_clear_initial_state", self._h)
+
+    # ---- evolution
+    def reset_state(self):
+        _call("qva_reset_state", self._h)
+
+    def apply_phase(self, gamma: float):
+        _call("qva_apply_phase", self._h, float(gamma))
+
+    def apply_mixer(self, beta: float):
+        _call("qva_apply_mixer", self._h, float(beta))
+
+    def evolve(self, theta):
+        theta = _f64(theta)
+        _call("qva_evolve", self._h, _ptr(theta), len(theta) // 2)
+
+    def expectation(self) -> float:
+        out = ctypes.c_double()
+        _call("qva_expectation", self._h, ctypes.byref(out))
+        return out.value
+
+    def norm2(self) -> float:
+        out = ctypes.c_double()
+        _call("qva_norm2", self._h, ctypes.byref(out))
+        return out.value
+
+    def get_state(self, offset: int = 0, count: Optional[int] = None, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if count is None:
+            n, o = self.get_partition()
+            offset, count = o, n
+        if out is None:
+            out = np.empty(count, np.complex128)
+        _call("qva_get_state", self._h, _ptr(out), offset, count)
+        return out
+
+    def get_probabilities(self, offset: int = 0, count: Optional[int] = None) -> np.ndarray:
+        if count is None:
+            n, o = self.get_partition()
+            offset, count = o, n
+        out = np.empty(count, np.float64)
+        _call("qva_get_probabilities", self._h, _ptr(out), offset, count)
+        return out
+
+    def evolve_batch(self, thetas) -> np.ndarray:
+        thetas = np.ascontiguousarray(thetas, np.float64)
+        B, P2 = thetas.shape
+        out = np.empty(B, np.float64)
+        _call("qva_evolve_batch", self._h, _ptr(thetas), B, P2 // 2, _ptr(out))
+        return out
+
+    # ---- introspection
+    def set_profiling(self, on: bool = True):
+        _call("qva_set_profiling", self._h, 1 if on else 0)
+
+    def kernel_stats(self, which) -> dict:
+        k = KERNEL_CLASSES[which] if isinstance(which, str) else int(which)
+        ms, n, b = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+        _call("qva_kernel_stats", self._h, k, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(b))
+        return {"ms": ms.value, "launches": n.value, "bytes": b.value}
+
+    def reset_kernel_stats(self):
+        _call("qva_reset_kernel_stats", self._h)
+
+    def launch_count(self) -> int:
+        n = ctypes.c_int64()
+        _call("qva_launch_count", self._h, ctypes.byref(n))
+        return n.value

@@ -1,0 +1,1398 @@
+// api.cu -- the C ABI (include/qva.h): plan lifecycle, layer scheduler, global-qubit exchange,
+// batch sharding and NCCL plumbing.  All arithmetic of the method runs in the kernels of
+// kernels_x.cu / kernels_fft.cu / kernels_sparse.cu; this file only plans and launches.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "qva_internal.h"
+
+namespace qva {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+// ---------------------------------------------------------------------------------------------
+// X-mixer schedule
+//
+// The mixer U_M(beta) = prod_j exp(-i beta X_j) is a product of commuting single-qubit
+// rotations, and the phase is diagonal, so one HBM pass over a tile of 2^12 amplitudes can
+// apply any rotations whose qubits are tile bits, and the phase may sit between two rotation
+// sets (tail of layer k, phase gamma_{k+1}, head of layer k+1).  The evolution is a token
+// stream PHASE(k) ROT(all,k) PHASE(k+1) ROT(all,k+1) ... (sharded: EXCHANGE / ROT(H,k)
+// between epochs) and passes are cut greedily from it.
+// ---------------------------------------------------------------------------------------------
+struct Token {
+    enum Kind { PHASE, ROT, EXCHANGE } kind;
+    uint64_t bits;  // ROT: physical bits to rotate
+    int layer;      // PHASE: gamma index; ROT: beta index
+};
+
+struct PassPlan {
+    bool exchange = false;   // this entry is an exchange, not a tile pass
+    int set = -1;
+    uint32_t r1 = 0, r2 = 0; // tile-local masks
+    int a1 = -1, a2 = -1;    // layer index of beta for R1 / R2
+    int phase = -1;          // layer index of gamma
+    bool expect = false;
+};
+
+static std::vector<std::vector<int>> make_tile_sets(int L) {
+    std::vector<std::vector<int>> sets;
+    std::vector<int> s0;
+    for (int b = 0; b < kTileBits; ++b) s0.push_back(b);
+    sets.push_back(s0);
+    int next = kTileBits;
+    while (next < L) {
+        std::vector<int> s = {0, 1, 2};
+        while ((int)s.size() < kTileBits && next < L) s.push_back(next++);
+        for (int b = 3; (int)s.size() < kTileBits; ++b) s.push_back(b);  // pad with low bits
+        std::sort(s.begin(), s.end());
+        sets.push_back(s);
+    }
+    return sets;
+}
+
+static uint64_t set_mask(const std::vector<int> &s) {
+    uint64_t m = 0;
+    for (int b : s) m |= 1ull << b;
+    return m;
+}
+
+static uint32_t to_local(const std::vector<int> &s, uint64_t phys) {
+    uint32_t m = 0;
+    for (int k = 0; k < (int)s.size(); ++k)
+        if ((phys >> s[k]) & 1) m |= 1u << k;
+    return m;
+}
+
+static std::vector<PassPlan> cut_passes(const std::vector<Token> &toks, const std::vector<std::vector<int>> &sets,
+                                        bool expect_at_end) {
+    std::vector<PassPlan> out;
+    size_t pos = 0;
+    uint64_t pending = 0;
+    int cur_layer = -1;
+    auto best_set = [&](uint64_t want) {
+        int best = 0, bc = -1;
+        for (int i = 0; i < (int)sets.size(); ++i) {
+            int c = __builtin_popcountll(want & set_mask(sets[i]));
+            if (c > bc) { bc = c; best = i; }
+        }
+        return best;
+    };
+    while (true) {
+        if (!pending) {
+            if (pos >= toks.size()) break;
+            const Token &t = toks[pos];
+            if (t.kind == Token::ROT) { pending = t.bits; cur_layer = t.layer; ++pos; continue; }
+            if (t.kind == Token::EXCHANGE) { PassPlan e; e.exchange = true; out.push_back(e); ++pos; continue; }
+        }
+        PassPlan pp;
+        // choose the tile set
+        uint64_t want = pending;
+        if (!want && pos < toks.size() && toks[pos].kind == Token::PHASE && pos + 1 < toks.size() &&
+            toks[pos + 1].kind == Token::ROT)
+            want = toks[pos + 1].bits;
+        pp.set = best_set(want);
+        uint64_t sm = set_mask(sets[pp.set]);
+        uint64_t r1 = pending & sm;
+        pending &= ~r1;
+        pp.r1 = to_local(sets[pp.set], r1);
+        pp.a1 = r1 ? cur_layer : -1;
+        if (!pending && pos < toks.size() && toks[pos].kind == Token::PHASE) {
+            pp.phase = toks[pos].layer;
+            ++pos;
+            if (pos < toks.size() && toks[pos].kind == Token::ROT) {
+                uint64_t r2 = toks[pos].bits & sm;
+                pending = toks[pos].bits & ~r2;
+                cur_layer = toks[pos].layer;
+                pp.r2 = to_local(sets[pp.set], r2);
+                pp.a2 = r2 ? cur_layer : -1;
+                ++pos;
+            }
+        }
+        out.push_back(pp);
+    }
+    if (expect_at_end && !out.empty() && !out.back().exchange) out.back().expect = true;
+    return out;
+}
+
+// tokens of a full evolution over the local bits [0, L) with G shards (g = log2 G global bits)
+static std::vector<Token> evolve_tokens(int L, int g, int p) {
+    std::vector<Token> t;
+    uint64_t all = (L >= 64) ? ~0ull : ((1ull << L) - 1);
+    uint64_t H = 0;
+    for (int b = L - g; b < L; ++b) H |= 1ull << b;
+    for (int k = 0; k < p; ++k) {
+        if (g > 0 && k > 0) t.push_back({Token::ROT, H, k - 1});
+        t.push_back({Token::PHASE, 0, k});
+        t.push_back({Token::ROT, all, k});
+        if (g > 0) t.push_back({Token::EXCHANGE, 0, -1});
+    }
+    if (g > 0 && p > 0) t.push_back({Token::ROT, H, p - 1});
+    return t;
+}
+
+static std::vector<Token> mixer_tokens(int L, int g) {
+    std::vector<Token> t;
+    uint64_t all = (1ull << L) - 1;
+    t.push_back({Token::ROT, all, 0});
+    if (g > 0) {
+        uint64_t H = 0;
+        for (int b = L - g; b < L; ++b) H |= 1ull << b;
+        t.push_back({Token::EXCHANGE, 0, -1});
+        t.push_back({Token::ROT, H, 0});
+    }
+    return t;
+}
+
+static void build_steps(const PassPlan &pp, TilePassParams &tp) {
+    std::vector<PassStep> st;
+    const int order1[3] = {2, 0, 1};
+    for (int g : order1) {
+        int m = (pp.r1 >> (4 * g)) & 15;
+        if (m) st.push_back({(int8_t)g, (int8_t)m, 0, 0});
+    }
+    if (pp.phase >= 0) {
+        if (st.empty()) st.push_back({2, 0, 0, 1});
+        else st.back().phase = 1;
+    }
+    int cur = st.empty() ? 2 : st.back().group;
+    int order2[3];
+    if (cur == 0) { order2[0] = 0; order2[1] = 1; order2[2] = 2; }
+    else { order2[0] = cur; order2[1] = 0; order2[2] = (cur == 1) ? 2 : 1; }
+    for (int g : order2) {
+        int m = (pp.r2 >> (4 * g)) & 15;
+        if (m) st.push_back({(int8_t)g, (int8_t)m, 1, 0});
+    }
+    if (st.empty()) st.push_back({2, 0, 0, 0});
+    if (st.front().group == 0) st.insert(st.begin(), PassStep{2, 0, 0, 0});
+    if (st.back().group == 0) st.push_back({2, 0, 0, 0});
+    tp.n_steps = (int)st.size();
+    for (int i = 0; i < tp.n_steps; ++i) tp.steps[i] = st[i];
+}
+
+}  // namespace qva
+
+using namespace qva;
+
+// ---------------------------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------------------------
+struct KernelStat {
+    double ms = 0.0;
+    int64_t launches = 0;
+    double bytes = 0.0;
+};
+struct PendingEvent {
+    cudaEvent_t a, b;
+    int cls;
+    double bytes;
+};
+
+struct qva_plan {
+    qva_plan_desc d{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint64_t N = 0;
+    int mixer = 0;
+    int world = 1, rank = 0, vshards = 1, G = 1, gbits = 0;
+    bool replicated = false;
+    uint64_t local_n = 0, offset = 0;   // partition of this rank (global indices)
+    int n = -1, L = -1;                 // qubits; local bits per shard
+    uint64_t arr_n = 0;                 // elements held by this process
+    double2 *psi = nullptr, *psi_alt = nullptr, *psi0 = nullptr;
+    double *q = nullptr, *qB = nullptr;
+    bool q_set = false, qB_valid = false, has_psi0 = false;
+    int layout = 0;
+    double *partials = nullptr;
+    uint64_t partials_n = 0;
+    double *red = nullptr;             // [max_batch][2]
+    PassAngles *d_angles = nullptr;
+    size_t angles_cap = 0;
+    double *d_thetas = nullptr;
+    size_t thetas_cap = 0;
+    int *d_flag = nullptr;
+    int max_batch = 1;
+    double2 *batch_psi = nullptr;
+    std::vector<std::vector<int>> sets;
+    // circulant
+    FftPlan *fft = nullptr;
+    double *lambda_perm = nullptr;
+    bool lam_set = false, lam_const = false;
+    double lam0 = 0.0, lamc = 0.0;
+    std::vector<double> lambda_host;   // natural (forward-bin) order mirror
+    // sparse
+    SparseMixer sm;
+    bool sparse_set = false;
+    // nccl
+    ncclComm_t comm = nullptr;
+    // profiling
+    bool prof = false;
+    KernelStat stats[8];
+    std::vector<PendingEvent> pending;
+    std::vector<cudaEvent_t> event_pool;
+    int64_t launches = 0;
+    bool expect_valid = false;
+    double expect_val = 0.0, norm_val = 0.0;
+};
+
+namespace {
+
+cudaEvent_t get_event(qva_plan *P) {
+    if (!P->event_pool.empty()) {
+        cudaEvent_t e = P->event_pool.back();
+        P->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    qva_plan *P;
+    int cls;
+    double bytes;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(qva_plan *P_, int cls_, double bytes_, int64_t nlaunch = 1) : P(P_), cls(cls_), bytes(bytes_) {
+        P->launches += nlaunch;
+        if (P->prof) {
+            a = get_event(P);
+            b = get_event(P);
+            cudaEventRecord(a, P->stream);
+        }
+    }
+    ~ProfScope() {
+        if (P->prof) {
+            cudaEventRecord(b, P->stream);
+            P->pending.push_back({a, b, cls, bytes});
+        }
+    }
+};
+
+struct PlanObserver : LaunchObserver {
+    qva_plan *P;
+    std::vector<ProfScope *> stack;
+    explicit PlanObserver(qva_plan *P_) : P(P_) {}
+    void begin(int cls, double bytes) override { stack.push_back(new ProfScope(P, cls, bytes)); }
+    void end() override {
+        delete stack.back();
+        stack.pop_back();
+    }
+};
+
+qva_status harvest(qva_plan *P) {
+    for (auto &pe : P->pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pe.a, pe.b);
+        P->stats[pe.cls].ms += ms;
+        P->stats[pe.cls].launches += 1;
+        P->stats[pe.cls].bytes += pe.bytes;
+        P->event_pool.push_back(pe.a);
+        P->event_pool.push_back(pe.b);
+    }
+    P->pending.clear();
+    return QVA_OK;
+}
+
+qva_status sync(qva_plan *P) {
+    QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
+    harvest(P);
+    return QVA_OK;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
+int ilog2(uint64_t x) {
+    int r = 0;
+    while ((1ull << r) < x) ++r;
+    return r;
+}
+
+qva_status ensure_partials(qva_plan *P, uint64_t n) {
+    if (P->partials_n >= n) return QVA_OK;
+    if (P->partials) cudaFree(P->partials);
+    P->partials = nullptr;
+    QVA_CUDA_TRY(cudaMalloc(&P->partials, n * 2 * sizeof(double)));
+    P->partials_n = n;
+    return QVA_OK;
+}
+
+qva_status ensure_angles(qva_plan *P, size_t n) {
+    if (P->angles_cap >= n) return QVA_OK;
+    if (P->d_angles) cudaFree(P->d_angles);
+    P->d_angles = nullptr;
+    QVA_CUDA_TRY(cudaMalloc(&P->d_angles, n * sizeof(PassAngles)));
+    P->angles_cap = n;
+    return QVA_OK;
+}
+
+qva_status check_theta(const double *theta, size_t n) {
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(theta[i])) {
+            set_error("non-finite theta");
+            return QVA_ERR_NUMERIC;
+        }
+    return QVA_OK;
+}
+
+// ---- exchange (global <-> local qubit swap; COMM-psi) ----------------------
+// Every shard r sends chunk t (local index top-g bits = t) to shard t, which stores it as its
+// chunk r: a block transpose of the G x G chunk matrix.  The layout flips between A and B.
+template <typename T>
+qva_status exchange_buffers(qva_plan *P, T *src, T *dst) {
+    uint64_t per_shard = 1ull << P->L;
+    uint64_t C = per_shard / P->G;
+    if (P->world == 1) {
+        ProfScope ps(P, K_EXCHANGE, 2.0 * sizeof(T) * (double)P->arr_n);
+        QVA_CUDA_TRY(launch_chunk_transpose<T>(dst, src, P->G, C, P->stream));
+        return QVA_OK;
+    }
+    ProfScope ps(P, K_EXCHANGE, 2.0 * sizeof(T) * (double)P->arr_n);
+    size_t cnt = C * sizeof(T) / sizeof(double);
+    QVA_NCCL_TRY(ncclGroupStart());
+    for (int t = 0; t < P->world; ++t) {
+        if (t == P->rank) continue;
+        QVA_NCCL_TRY(ncclSend((const double *)(src + t * C), cnt, ncclDouble, t, P->comm, P->stream));
+        QVA_NCCL_TRY(ncclRecv((double *)(dst + t * C), cnt, ncclDouble, t, P->comm, P->stream));
+    }
+    QVA_NCCL_TRY(ncclGroupEnd());
+    QVA_CUDA_TRY(cudaMemcpyAsync(dst + P->rank * C, src + P->rank * C, C * sizeof(T), cudaMemcpyDeviceToDevice,
+                                 P->stream));
+    return QVA_OK;
+}
+
+qva_status exchange_state(qva_plan *P) {
+    QVA_TRY(exchange_buffers<double2>(P, P->psi, P->psi_alt));
+    std::swap(P->psi, P->psi_alt);
+    P->layout ^= 1;
+    return QVA_OK;
+}
+
+qva_status ensure_qB(qva_plan *P) {
+    if (P->G == 1 || P->qB_valid) return QVA_OK;
+    if (!P->qB) QVA_CUDA_TRY(cudaMalloc(&P->qB, P->arr_n * sizeof(double)));
+    QVA_TRY(exchange_buffers<double>(P, P->q, P->qB));
+    P->qB_valid = true;
+    return QVA_OK;
+}
+
+qva_status to_layout_A(qva_plan *P) {
+    if (P->layout == 0) return QVA_OK;
+    return exchange_state(P);
+}
+
+// ---- tile-pass execution of a pass list -----------------------------------------------------
+// thetas: [batch][2p]; psi_base/stride: states of the batch members
+qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const double *thetas, int p, int batch,
+                      double2 *psi_base, uint64_t stride, int init_mode, double *expect_out /*[batch][2] host*/) {
+    int n_tile_passes = 0;
+    for (auto &pp : passes) n_tile_passes += !pp.exchange;
+    QVA_TRY(ensure_angles(P, (size_t)n_tile_passes * batch));
+    std::vector<PassAngles> ang((size_t)n_tile_passes * batch);
+    {
+        int j = 0;
+        for (auto &pp : passes) {
+            if (pp.exchange) continue;
+            for (int b = 0; b < batch; ++b) {
+                const double *th = thetas + (size_t)b * 2 * p;
+                PassAngles &a = ang[(size_t)j * batch + b];
+                a.c1 = a.s1 = a.c2 = a.s2 = a.gamma = 0.0;
+                if (pp.a1 >= 0) { a.c1 = cos(th[2 * pp.a1 + 1]); a.s1 = sin(th[2 * pp.a1 + 1]); }
+                if (pp.a2 >= 0) { a.c2 = cos(th[2 * pp.a2 + 1]); a.s2 = sin(th[2 * pp.a2 + 1]); }
+                if (pp.phase >= 0) a.gamma = th[2 * pp.phase];
+            }
+            ++j;
+        }
+    }
+    QVA_CUDA_TRY(cudaMemcpyAsync(P->d_angles, ang.data(), ang.size() * sizeof(PassAngles), cudaMemcpyHostToDevice,
+                                 P->stream));
+    uint64_t n_tiles = P->arr_n >> kTileBits;
+    bool any_expect = false;
+    for (auto &pp : passes) any_expect |= pp.expect;
+    if (any_expect) QVA_TRY(ensure_partials(P, n_tiles * batch));
+    int j = 0;
+    bool first = true;
+    for (auto &pp : passes) {
+        if (pp.exchange) {
+            if (batch != 1 || psi_base != P->psi) {
+                set_error("internal: exchange in batched pass list");
+                return QVA_ERR_INVALID_ARGUMENT;
+            }
+            QVA_TRY(exchange_state(P));
+            psi_base = P->psi;
+            continue;
+        }
+        TilePassParams tp;
+        memset(&tp, 0, sizeof(tp));
+        const std::vector<int> &s = P->sets[pp.set];
+        for (int k = 0; k < kTileBits; ++k) tp.tile_bits[k] = s[k];
+        tp.n_phys_bits = ilog2(P->arr_n);
+        tp.n_tiles = n_tiles;
+        tp.member_stride = stride;
+        tp.psi_in = psi_base;
+        tp.psi_out = psi_base;
+        if (first && init_mode == 2) tp.psi_in = P->psi0;
+        tp.init = first ? init_mode : 0;
+        tp.amp0 = 1.0 / sqrt((double)P->N);
+        if (pp.phase >= 0 || pp.expect) {
+            if (P->layout == 1) QVA_TRY(ensure_qB(P));
+            tp.q = (P->layout == 1) ? P->qB : P->q;
+        }
+        tp.angles = P->d_angles + (size_t)j * batch;
+        tp.expect = pp.expect ? 1 : 0;
+        tp.partials = P->partials;
+        build_steps(pp, tp);
+        double bytes = (double)P->arr_n * batch *
+                       ((tp.init == 1 ? 16.0 : 32.0) + (pp.phase >= 0 ? 8.0 : 0.0) + (pp.expect ? 8.0 : 0.0));
+        {
+            ProfScope ps(P, K_TILE, bytes);
+            QVA_CUDA_TRY(launch_tile_pass(tp, batch, P->stream));
+        }
+        first = false;
+        ++j;
+        if (pp.expect) {
+            ProfScope ps(P, K_REDUCE, 16.0 * n_tiles * batch);
+            QVA_CUDA_TRY(launch_reduce_partials(P->partials, n_tiles, batch, P->red, P->stream));
+        }
+    }
+    if (expect_out) {
+        QVA_CUDA_TRY(cudaMemcpyAsync(expect_out, P->red, sizeof(double) * 2 * batch, cudaMemcpyDeviceToHost,
+                                     P->stream));
+    }
+    return QVA_OK;
+}
+
+qva_status allreduce_host(qva_plan *P, double *vals, int n) {
+    if (P->world == 1) return QVA_OK;
+    double *d;
+    QVA_CUDA_TRY(cudaMallocAsync((void **)&d, n * sizeof(double), P->stream));
+    QVA_CUDA_TRY(cudaMemcpyAsync(d, vals, n * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+    QVA_NCCL_TRY(ncclAllReduce(d, d, n, ncclDouble, ncclSum, P->comm, P->stream));
+    QVA_CUDA_TRY(cudaMemcpyAsync(vals, d, n * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
+    QVA_CUDA_TRY(cudaFreeAsync(d, P->stream));
+    QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
+    return QVA_OK;
+}
+
+// generic (non-tile) expectation over this process's arrays
+qva_status expect_generic(qva_plan *P, const double2 *psi, uint64_t n, const double *q, double *out2) {
+    int blocks = expect_partial_blocks(n);
+    QVA_TRY(ensure_partials(P, blocks));
+    {
+        ProfScope ps(P, K_REDUCE, 24.0 * n);
+        QVA_CUDA_TRY(launch_expect_partials(psi, q, n, P->partials, blocks, P->stream));
+    }
+    {
+        ProfScope ps(P, K_REDUCE, 16.0 * blocks);
+        QVA_CUDA_TRY(launch_reduce_partials(P->partials, blocks, 1, P->red, P->stream));
+    }
+    QVA_CUDA_TRY(cudaMemcpyAsync(out2, P->red, 2 * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
+    return sync(P);
+}
+
+bool use_small(const qva_plan *P) { return P->mixer == QVA_MIXER_X && P->n <= kSmallMaxQubits && P->G == 1; }
+
+// apply one mixer on the current state (no phase)
+qva_status apply_mixer_impl(qva_plan *P, double beta) {
+    if (P->mixer == QVA_MIXER_X) {
+        if (use_small(P)) {
+            SmallEvolveParams sp{};
+            sp.psi = P->psi;
+            sp.q = P->q;
+            sp.n = P->n;
+            sp.p = 1;
+            sp.mode = 2;
+            double th = beta;
+            QVA_CUDA_TRY(cudaMemcpyAsync(P->d_thetas, &th, sizeof(double), cudaMemcpyHostToDevice, P->stream));
+            sp.thetas = P->d_thetas;
+            ProfScope ps(P, K_SMALL, 32.0 * P->arr_n);
+            QVA_CUDA_TRY(launch_small_evolve(sp, 1, P->stream));
+            return QVA_OK;
+        }
+        auto toks = mixer_tokens(P->L, P->gbits);
+        auto passes = cut_passes(toks, P->sets, false);
+        double th[2] = {0.0, beta};
+        QVA_TRY(run_passes(P, passes, th, 1, 1, P->psi, 0, 0, nullptr));
+        return QVA_OK;
+    }
+    if (P->mixer == QVA_MIXER_CIRCULANT) {
+        if (!P->lam_set) {
+            set_error("circulant spectrum not set");
+            return QVA_ERR_NOT_READY;
+        }
+        FftRun r;
+        r.psi = P->psi;
+        r.q = P->q;
+        r.lambda_perm = P->lam_const ? nullptr : P->lambda_perm;
+        r.lam0 = P->lam0;
+        r.lamc = P->lamc;
+        r.theta = &beta;
+        r.mode = 1;
+        PlanObserver obs(P);
+        return fft_run(P->fft, r, P->stream, &obs);
+    }
+    if (P->mixer == QVA_MIXER_SPARSE) {
+        if (!P->sparse_set) {
+            set_error("sparse mixer not set");
+            return QVA_ERR_NOT_READY;
+        }
+        int terms = 0;
+        PlanObserver obs(P);
+        return sparse_apply_mixer(P->sm, P->psi, beta, P->stream, &obs, &terms);
+    }
+    return QVA_ERR_UNSUPPORTED;
+}
+
+qva_status reset_state(qva_plan *P) {
+    if (P->has_psi0) {
+        QVA_CUDA_TRY(cudaMemcpyAsync(P->psi, P->psi0, P->arr_n * sizeof(double2), cudaMemcpyDeviceToDevice, P->stream));
+    } else {
+        QVA_CUDA_TRY(launch_fill_uniform(P->psi, P->arr_n, 1.0 / sqrt((double)P->N), P->stream));
+    }
+    P->layout = 0;
+    return QVA_OK;
+}
+
+qva_status check_range(const qva_plan *P, uint64_t offset, uint64_t count, uint64_t *local_off) {
+    uint64_t lo = P->offset, hi = P->offset + P->local_n;
+    if (offset < lo || offset + count > hi || offset + count < offset) {
+        set_error("range [" + std::to_string(offset) + ", " + std::to_string(offset + count) +
+                  ") outside this rank's partition [" + std::to_string(lo) + ", " + std::to_string(hi) + ")");
+        return QVA_ERR_SIZE_MISMATCH;
+    }
+    *local_off = offset - lo;
+    return QVA_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+const char *qva_version(void) { return "qva-b200 0.1 (sm_100a)"; }
+
+const char *qva_status_string(qva_status s) {
+    switch (s) {
+        case QVA_OK: return "QVA_OK";
+        case QVA_ERR_INVALID_ARGUMENT: return "QVA_ERR_INVALID_ARGUMENT";
+        case QVA_ERR_SIZE_MISMATCH: return "QVA_ERR_SIZE_MISMATCH";
+        case QVA_ERR_NOT_READY: return "QVA_ERR_NOT_READY";
+        case QVA_ERR_NUMERIC: return "QVA_ERR_NUMERIC";
+        case QVA_ERR_UNSUPPORTED: return "QVA_ERR_UNSUPPORTED";
+        case QVA_ERR_OUT_OF_MEMORY: return "QVA_ERR_OUT_OF_MEMORY";
+        case QVA_ERR_CUDA: return "QVA_ERR_CUDA";
+        case QVA_ERR_NCCL: return "QVA_ERR_NCCL";
+    }
+    return "QVA_ERR_UNKNOWN";
+}
+
+const char *qva_last_error(void) { return g_last_error.c_str(); }
+
+qva_status qva_partition(uint64_t dim, int32_t world, int32_t rank, uint64_t *local_n, uint64_t *offset) {
+    if (!local_n || !offset || world < 1 || rank < 0 || rank >= world || dim == 0) {
+        set_error("qva_partition: invalid argument");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    // Eqs. local_i / offset; remainder to the lowest ranks (reading R16)
+    uint64_t base = dim / world, rem = dim % world;
+    *local_n = base + ((uint64_t)rank < rem ? 1 : 0);
+    *offset = base * rank + std::min<uint64_t>(rank, rem);
+    return QVA_OK;
+}
+
+qva_status qva_batch_partition(int32_t B, int32_t world, int32_t rank, int32_t *first, int32_t *count) {
+    if (!first || !count || B < 0 || world < 1 || rank < 0 || rank >= world) {
+        set_error("qva_batch_partition: invalid argument");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    int32_t base = B / world, rem = B % world;
+    *count = base + (rank < rem ? 1 : 0);
+    *first = base * rank + std::min(rank, rem);
+    return QVA_OK;
+}
+
+qva_status qva_x_schedule(int32_t n_local, int32_t p, int32_t *out, int32_t cap, int32_t *n_passes) {
+    if (n_local < kTileBits || n_local > 40 || p < 0 || !n_passes) {
+        set_error("qva_x_schedule: need 12 <= n_local <= 40");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    auto sets = make_tile_sets(n_local);
+    auto passes = cut_passes(evolve_tokens(n_local, 0, p), sets, true);
+    *n_passes = (int32_t)passes.size();
+    for (int i = 0; i < (int)passes.size() && i < cap; ++i) {
+        out[4 * i + 0] = passes[i].set;
+        out[4 * i + 1] = __builtin_popcount(passes[i].r1);
+        out[4 * i + 2] = passes[i].phase >= 0 ? 1 : 0;
+        out[4 * i + 3] = __builtin_popcount(passes[i].r2);
+    }
+    return QVA_OK;
+}
+
+qva_status qva_nccl_unique_id(void *id_out) {
+    if (!id_out) return QVA_ERR_INVALID_ARGUMENT;
+    ncclUniqueId id;
+    QVA_NCCL_TRY(ncclGetUniqueId(&id));
+    memcpy(id_out, &id, sizeof(id));
+    return QVA_OK;
+}
+
+qva_status qva_plan_destroy(qva_plan *P) {
+    if (!P) return QVA_OK;
+    DeviceGuard dg(P->device);
+    if (P->stream) cudaStreamSynchronize(P->stream);
+    harvest(P);
+    cudaFree(P->psi);
+    cudaFree(P->psi_alt);
+    cudaFree(P->psi0);
+    cudaFree(P->q);
+    cudaFree(P->qB);
+    cudaFree(P->partials);
+    cudaFree(P->red);
+    cudaFree(P->d_angles);
+    cudaFree(P->d_thetas);
+    cudaFree(P->d_flag);
+    cudaFree(P->batch_psi);
+    cudaFree(P->lambda_perm);
+    if (P->fft) fft_plan_destroy(P->fft);
+    cudaFree(P->sm.row_ptr);
+    cudaFree(P->sm.col);
+    cudaFree(P->sm.val);
+    cudaFree(P->sm.t0);
+    cudaFree(P->sm.t1);
+    cudaFree(P->sm.scratch);
+    for (auto e : P->event_pool) cudaEventDestroy(e);
+    if (P->comm) ncclCommDestroy(P->comm);
+    if (P->own_stream && P->stream) cudaStreamDestroy(P->stream);
+    delete P;
+    return QVA_OK;
+}
+
+qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
+    if (!desc || !out) {
+        set_error("qva_plan_create: NULL argument");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    const qva_plan_desc &d = *desc;
+    if (d.dim == 0 || d.world < 1 || d.rank < 0 || d.rank >= d.world || d.mixer < 0 || d.mixer > 2) {
+        set_error("qva_plan_create: invalid dim/world/rank/mixer");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    int vs = d.virtual_shards > 1 ? d.virtual_shards : 1;
+    bool replicated = d.reserved[0] != 0;
+    if (vs > 1 && d.world > 1) {
+        set_error("virtual_shards requires world == 1");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    if (d.mixer == QVA_MIXER_X) {
+        if (d.n_qubits < 1 || d.n_qubits > 40 || d.dim != (1ull << d.n_qubits)) {
+            set_error("X mixer needs dim == 2^n_qubits (1 <= n <= 40)");
+            return QVA_ERR_UNSUPPORTED;
+        }
+    }
+    int G = replicated ? 1 : d.world * vs;
+    if (G > 1) {
+        if (d.mixer != QVA_MIXER_X) {
+            set_error("sharded state (world*virtual_shards > 1) is implemented for the X mixer only; "
+                      "use the replicated mode (reserved[0]=1) for batches of circulant/sparse evolutions");
+            return QVA_ERR_UNSUPPORTED;
+        }
+        if (!is_pow2((uint64_t)G)) {
+            set_error("X mixer sharding needs a power-of-two shard count");
+            return QVA_ERR_UNSUPPORTED;
+        }
+        int g = ilog2(G);
+        int L = d.n_qubits - g;
+        if (L < kTileBits || g > L - 3 || g > 9) {
+            set_error("sharded X mixer needs n_qubits - log2(shards) >= 12 local qubits");
+            return QVA_ERR_UNSUPPORTED;
+        }
+    }
+    DeviceGuard dg(d.device);
+    qva_plan *P = new qva_plan();
+    P->d = d;
+    P->device = d.device;
+    P->N = d.dim;
+    P->mixer = d.mixer;
+    P->world = d.world;
+    P->rank = d.rank;
+    P->vshards = vs;
+    P->replicated = replicated;
+    P->G = G;
+    P->gbits = ilog2(G);
+    P->max_batch = d.max_batch > 0 ? d.max_batch : 1;
+    if (d.mixer == QVA_MIXER_X) {
+        P->n = d.n_qubits;
+        P->L = P->n - P->gbits;
+    }
+    if (replicated || d.world == 1) {
+        P->local_n = P->N;
+        P->offset = 0;
+    } else {
+        qva_partition(P->N, d.world, d.rank, &P->local_n, &P->offset);
+    }
+    P->arr_n = P->local_n;  // vshards: the whole vector lives here, in shard-major order
+    auto fail = [&](qva_status s) {
+        qva_plan_destroy(P);
+        return s;
+    };
+    if (d.stream) {
+        P->stream = (cudaStream_t)d.stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            set_error("cudaStreamCreate failed");
+            return fail(QVA_ERR_CUDA);
+        }
+        P->own_stream = true;
+    }
+    auto alloc = [&](void **ptr, size_t bytes) -> bool {
+        if (cudaMalloc(ptr, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+            return false;
+        }
+        return true;
+    };
+    if (!alloc((void **)&P->psi, P->arr_n * sizeof(double2))) return fail(QVA_ERR_OUT_OF_MEMORY);
+    if (!alloc((void **)&P->q, P->arr_n * sizeof(double))) return fail(QVA_ERR_OUT_OF_MEMORY);
+    if (G > 1 && !alloc((void **)&P->psi_alt, P->arr_n * sizeof(double2))) return fail(QVA_ERR_OUT_OF_MEMORY);
+    if (!alloc((void **)&P->red, (size_t)P->max_batch * 2 * sizeof(double))) return fail(QVA_ERR_OUT_OF_MEMORY);
+    if (!alloc((void **)&P->d_flag, sizeof(int))) return fail(QVA_ERR_OUT_OF_MEMORY);
+    P->thetas_cap = 256;
+    if (!alloc((void **)&P->d_thetas, P->thetas_cap * sizeof(double))) return fail(QVA_ERR_OUT_OF_MEMORY);
+    if (P->max_batch > 1) {
+        if (!alloc((void **)&P->batch_psi, (size_t)P->max_batch * P->arr_n * sizeof(double2)))
+            return fail(QVA_ERR_OUT_OF_MEMORY);
+    }
+    if (d.mixer == QVA_MIXER_X && P->L >= kTileBits) P->sets = make_tile_sets(P->L);
+    if (d.mixer == QVA_MIXER_CIRCULANT) {
+        qva_status s = fft_plan_create(P->N, P->device, &P->fft);
+        if (s != QVA_OK) return fail(s);
+    }
+    if (d.world > 1) {
+        if (!d.nccl_unique_id) {
+            set_error("world > 1 needs nccl_unique_id");
+            return fail(QVA_ERR_INVALID_ARGUMENT);
+        }
+        ncclUniqueId id;
+        memcpy(&id, d.nccl_unique_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&P->comm, d.world, id, d.rank);
+        if (r != ncclSuccess) {
+            set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+            return fail(QVA_ERR_NCCL);
+        }
+    }
+    if (reset_state(P) != QVA_OK) return fail(QVA_ERR_CUDA);
+    if (cudaMemsetAsync(P->q, 0, P->arr_n * sizeof(double), P->stream) != cudaSuccess) return fail(QVA_ERR_CUDA);
+    if (cudaStreamSynchronize(P->stream) != cudaSuccess) {
+        set_error("plan init failed");
+        return fail(QVA_ERR_CUDA);
+    }
+    *out = P;
+    return QVA_OK;
+}
+
+qva_status qva_plan_get_partition(const qva_plan *P, uint64_t *local_n, uint64_t *offset) {
+    if (!P || !local_n || !offset) return QVA_ERR_INVALID_ARGUMENT;
+    *local_n = P->local_n;
+    *offset = P->offset;
+    return QVA_OK;
+}
+
+static qva_status set_q_common(qva_plan *P, const double *src, bool device, uint64_t offset, uint64_t count) {
+    uint64_t lo;
+    QVA_TRY(check_range(P, offset, count, &lo));
+    if (count == 0) return QVA_OK;
+    QVA_CUDA_TRY(cudaMemcpyAsync(P->q + lo, src, count * sizeof(double),
+                                 device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P->stream));
+    QVA_CUDA_TRY(cudaMemsetAsync(P->d_flag, 0, sizeof(int), P->stream));
+    QVA_CUDA_TRY(launch_check_finite(P->q + lo, count, P->d_flag, P->stream));
+    int flag = 0;
+    QVA_CUDA_TRY(cudaMemcpyAsync(&flag, P->d_flag, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
+    QVA_TRY(sync(P));
+    if (flag) {
+        set_error("non-finite quality value");
+        return QVA_ERR_NUMERIC;
+    }
+    P->q_set = true;
+    P->qB_valid = false;
+    return QVA_OK;
+}
+
+qva_status qva_set_qualities(qva_plan *P, const double *q, uint64_t offset, uint64_t count) {
+    if (!P || (!q && count)) return QVA_ERR_INVALID_ARGUMENT;
+    DeviceGuard dg(P->device);
+    return set_q_common(P, q, false, offset, count);
+}
+
+qva_status qva_set_qualities_device(qva_plan *P, const double *q, uint64_t offset, uint64_t count) {
+    if (!P || (!q && count)) return QVA_ERR_INVALID_ARGUMENT;
+    DeviceGuard dg(P->device);
+    return set_q_common(P, q, true, offset, count);
+}
+
+qva_status qva_set_qualities_maxcut(qva_plan *P, int32_t m, const int32_t *u, const int32_t *v, const double *w) {
+    if (!P || m < 0 || (m > 0 && (!u || !v))) return QVA_ERR_INVALID_ARGUMENT;
+    if (P->mixer != QVA_MIXER_X) {
+        set_error("qva_set_qualities_maxcut: X mixer plans only");
+        return QVA_ERR_UNSUPPORTED;
+    }
+    for (int e = 0; e < m; ++e) {
+        if (u[e] < 0 || u[e] >= P->n || v[e] < 0 || v[e] >= P->n) {
+            set_error("edge vertex out of range");
+            return QVA_ERR_INVALID_ARGUMENT;
+        }
+        if (w && !std::isfinite(w[e])) {
+            set_error("non-finite edge weight");
+            return QVA_ERR_NUMERIC;
+        }
+    }
+    DeviceGuard dg(P->device);
+    int32_t *du = nullptr, *dv = nullptr;
+    double *dw = nullptr;
+    size_t me = m > 0 ? m : 1;
+    QVA_CUDA_TRY(cudaMallocAsync((void **)&du, me * sizeof(int32_t), P->stream));
+    QVA_CUDA_TRY(cudaMallocAsync((void **)&dv, me * sizeof(int32_t), P->stream));
+    if (m) QVA_CUDA_TRY(cudaMemcpyAsync(du, u, m * sizeof(int32_t), cudaMemcpyHostToDevice, P->stream));
+    if (m) QVA_CUDA_TRY(cudaMemcpyAsync(dv, v, m * sizeof(int32_t), cudaMemcpyHostToDevice, P->stream));
+    if (w) {
+        QVA_CUDA_TRY(cudaMallocAsync((void **)&dw, me * sizeof(double), P->stream));
+        QVA_CUDA_TRY(cudaMemcpyAsync(dw, w, m * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+    }
+    {
+        ProfScope ps(P, K_OTHER, 8.0 * P->arr_n);
+        QVA_CUDA_TRY(launch_maxcut_q(P->q, P->arr_n, P->offset, m, du, dv, dw, P->stream));
+    }
+    cudaFreeAsync(du, P->stream);
+    cudaFreeAsync(dv, P->stream);
+    if (dw) cudaFreeAsync(dw, P->stream);
+    QVA_TRY(sync(P));
+    P->q_set = true;
+    P->qB_valid = false;
+    return QVA_OK;
+}
+
+
+qva_status qva_get_qualities(qva_plan *P, double *q_out, uint64_t offset, uint64_t count) {
+    if (!P || (!q_out && count)) return QVA_ERR_INVALID_ARGUMENT;
+    uint64_t lo;
+    QVA_TRY(check_range(P, offset, count, &lo));
+    DeviceGuard dg(P->device);
+    if (count)
+        QVA_CUDA_TRY(cudaMemcpyAsync(q_out, P->q + lo, count * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
+    return sync(P);
+}
+
+qva_status qva_set_circulant_eigenvalues(qva_plan *P, const double *lambda, uint64_t offset, uint64_t count) {
+    if (!P || (!lambda && count)) return QVA_ERR_INVALID_ARGUMENT;
+    if (P->mixer != QVA_MIXER_CIRCULANT) {
+        set_error("not a circulant-mixer plan");
+        return QVA_ERR_UNSUPPORTED;
+    }
+    if (offset > P->N || count > P->N - offset) {
+        set_error("eigenvalue range outside [0, dim)");
+        return QVA_ERR_SIZE_MISMATCH;
+    }
+    for (uint64_t i = 0; i < count; ++i)
+        if (!std::isfinite(lambda[i])) {
+            set_error("non-finite eigenvalue");
+            return QVA_ERR_NUMERIC;
+        }
+    DeviceGuard dg(P->device);
+    if (P->lambda_host.size() != P->N) P->lambda_host.assign(P->N, 0.0);
+    std::copy(lambda, lambda + count, P->lambda_host.begin() + offset);
+    if (!P->lambda_perm) QVA_CUDA_TRY(cudaMalloc(&P->lambda_perm, P->N * sizeof(double)));
+    std::vector<double> perm(P->N);
+    fft_permute_spectrum(P->fft, P->lambda_host.data(), perm.data());
+    QVA_CUDA_TRY(cudaMemcpyAsync(P->lambda_perm, perm.data(), P->N * sizeof(double), cudaMemcpyHostToDevice,
+                                 P->stream));
+    QVA_TRY(sync(P));
+    P->lam_set = true;
+    P->lam_const = false;
+    return QVA_OK;
+}
+
+qva_status qva_set_circulant_eigenvalues_const(qva_plan *P, double lambda0, double c) {
+    if (!P) return QVA_ERR_INVALID_ARGUMENT;
+    if (P->mixer != QVA_MIXER_CIRCULANT) {
+        set_error("not a circulant-mixer plan");
+        return QVA_ERR_UNSUPPORTED;
+    }
+    if (!std::isfinite(lambda0) || !std::isfinite(c)) {
+        set_error("non-finite eigenvalue");
+        return QVA_ERR_NUMERIC;
+    }
+    P->lam_set = true;
+    P->lam_const = true;
+    P->lam0 = lambda0;
+    P->lamc = c;
+    return QVA_OK;
+}
+
+qva_status qva_set_sparse_mixer(qva_plan *P, const int64_t *row_ptr, const int32_t *col, const double *val,
+                                uint64_t nnz) {
+    if (!P || !row_ptr || (nnz && !col)) return QVA_ERR_INVALID_ARGUMENT;
+    if (P->mixer != QVA_MIXER_SPARSE) {
+        set_error("not a sparse-mixer plan");
+        return QVA_ERR_UNSUPPORTED;
+    }
+    uint64_t rows = P->N;
+    if (row_ptr[0] != 0 || (uint64_t)row_ptr[rows] != nnz) {
+        set_error("row_ptr[0] must be 0 and row_ptr[dim] == nnz");
+        return QVA_ERR_SIZE_MISMATCH;
+    }
+    // ||W||_1 = max_j sum_i |w_ij| = max row abs sum for symmetric W (reading R13); validate
+    double norm1 = 0.0;
+    for (uint64_t r = 0; r < rows; ++r) {
+        if (row_ptr[r + 1] < row_ptr[r]) {
+            set_error("row_ptr not monotone");
+            return QVA_ERR_INVALID_ARGUMENT;
+        }
+        double s = 0.0;
+        for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
+            if (col[k] < 0 || (uint64_t)col[k] >= rows) {
+                set_error("column index out of range");
+                return QVA_ERR_INVALID_ARGUMENT;
+            }
+            double v = val ? val[k] : 1.0;
+            if (!std::isfinite(v)) {
+                set_error("non-finite matrix entry");
+                return QVA_ERR_NUMERIC;
+            }
+            s += fabs(v);
+        }
+        norm1 = std::max(norm1, s);
+    }
+    DeviceGuard dg(P->device);
+    SparseMixer &sm = P->sm;
+    cudaFree(sm.row_ptr);
+    cudaFree(sm.col);
+    cudaFree(sm.val);
+    sm.row_ptr = nullptr; sm.col = nullptr; sm.val = nullptr;
+    QVA_CUDA_TRY(cudaMalloc(&sm.row_ptr, (rows + 1) * sizeof(int64_t)));
+    QVA_CUDA_TRY(cudaMalloc(&sm.col, std::max<uint64_t>(nnz, 1) * sizeof(int32_t)));
+    QVA_CUDA_TRY(cudaMemcpyAsync(sm.row_ptr, row_ptr, (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, P->stream));
+    if (nnz) QVA_CUDA_TRY(cudaMemcpyAsync(sm.col, col, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, P->stream));
+    if (val) {
+        QVA_CUDA_TRY(cudaMalloc(&sm.val, std::max<uint64_t>(nnz, 1) * sizeof(double)));
+        if (nnz) QVA_CUDA_TRY(cudaMemcpyAsync(sm.val, val, nnz * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+    }
+    if (!sm.t0) QVA_CUDA_TRY(cudaMalloc(&sm.t0, rows * sizeof(double2)));
+    if (!sm.t1) QVA_CUDA_TRY(cudaMalloc(&sm.t1, rows * sizeof(double2)));
+    sm.nnz = nnz;
+    sm.rows = rows;
+    sm.norm1 = norm1;
+    QVA_TRY(sync(P));
+    P->sparse_set = true;
+    return QVA_OK;
+}
+
+qva_status qva_set_initial_state(qva_plan *P, const double *re_im, uint64_t offset, uint64_t count) {
+    if (!P || (!re_im && count)) return QVA_ERR_INVALID_ARGUMENT;
+    uint64_t lo;
+    QVA_TRY(check_range(P, offset, count, &lo));
+    DeviceGuard dg(P->device);
+    if (!P->psi0) {
+        QVA_CUDA_TRY(cudaMalloc(&P->psi0, P->arr_n * sizeof(double2)));
+        QVA_CUDA_TRY(cudaMemsetAsync(P->psi0, 0, P->arr_n * sizeof(double2), P->stream));
+    }
+    for (uint64_t i = 0; i < 2 * count; ++i)
+        if (!std::isfinite(re_im[i])) {
+            set_error("non-finite initial amplitude");
+            return QVA_ERR_NUMERIC;
+        }
+    if (count)
+        QVA_CUDA_TRY(cudaMemcpyAsync(P->psi0 + lo, re_im, count * sizeof(double2), cudaMemcpyHostToDevice, P->stream));
+    QVA_TRY(sync(P));
+    P->has_psi0 = true;
+    return QVA_OK;
+}
+
+qva_status qva_clear_initial_state(qva_plan *P) {
+    if (!P) return QVA_ERR_INVALID_ARGUMENT;
+    P->has_psi0 = false;
+    return QVA_OK;
+}
+
+qva_status qva_reset_state(qva_plan *P) {
+    if (!P) return QVA_ERR_INVALID_ARGUMENT;
+    DeviceGuard dg(P->device);
+    QVA_TRY(reset_state(P));
+    P->expect_valid = false;
+    return sync(P);
+}
+
+static const double *q_current(qva_plan *P) { return (P->layout == 1) ? P->qB : P->q; }
+
+qva_status qva_apply_phase(qva_plan *P, double gamma) {
+    if (!P) return QVA_ERR_INVALID_ARGUMENT;
+    if (!std::isfinite(gamma)) {
+        set_error("non-finite gamma");
+        return QVA_ERR_NUMERIC;
+    }
+    if (!P->q_set) {
+        set_error("qualities not set");
+        return QVA_ERR_NOT_READY;
+    }
+    DeviceGuard dg(P->device);
+    if (P->layout == 1) QVA_TRY(ensure_qB(P));
+    {
+        ProfScope ps(P, K_OTHER, 40.0 * P->arr_n);
+        QVA_CUDA_TRY(launch_phase(P->psi, q_current(P), P->arr_n, gamma, P->stream));
+    }
+    P->expect_valid = false;
+    return sync(P);
+}
+
+qva_status qva_apply_mixer(qva_plan *P, double beta) {
+    if (!P) return QVA_ERR_INVALID_ARGUMENT;
+    if (!std::isfinite(beta)) {
+        set_error("non-finite beta");
+        return QVA_ERR_NUMERIC;
+    }
+    DeviceGuard dg(P->device);
+    P->expect_valid = false;
+    QVA_TRY(apply_mixer_impl(P, beta));
+    return sync(P);
+}
+
+// one full evolution of the plan's own state; on return P->red holds (f, norm) (local sums)
+static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *have_red) {
+    *have_red = false;
+    if (P->mixer == QVA_MIXER_X) {
+        if (use_small(P)) {
+            SmallEvolveParams sp{};
+            sp.psi = P->psi;
+            sp.psi0 = P->has_psi0 ? P->psi0 : nullptr;
+            sp.q = P->q;
+            sp.n = P->n;
+            sp.p = p;
+            sp.mode = 0;
+            sp.out = P->red;
+            QVA_CUDA_TRY(cudaMemcpyAsync(P->d_thetas, theta, 2 * p * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+            sp.thetas = P->d_thetas;
+            {
+                ProfScope ps(P, K_SMALL, 24.0 * P->arr_n);
+                QVA_CUDA_TRY(launch_small_evolve(sp, 1, P->stream));
+            }
+            P->layout = 0;
+            *have_red = true;
+            return QVA_OK;
+        }
+        P->layout = 0;
+        if (p == 0) {
+            QVA_TRY(reset_state(P));
+            return QVA_OK;
+        }
+        auto passes = cut_passes(evolve_tokens(P->L, P->gbits, p), P->sets, true);
+        QVA_TRY(run_passes(P, passes, theta, p, 1, P->psi, 0, P->has_psi0 ? 2 : 1, nullptr));
+        *have_red = true;
+        return QVA_OK;
+    }
+    if (P->mixer == QVA_MIXER_CIRCULANT) {
+        if (!P->lam_set) {
+            set_error("circulant spectrum not set");
+            return QVA_ERR_NOT_READY;
+        }
+        FftRun r;
+        r.psi = P->psi;
+        r.q = P->q;
+        r.lambda_perm = P->lam_const ? nullptr : P->lambda_perm;
+        r.lam0 = P->lam0;
+        r.lamc = P->lamc;
+        r.theta = theta;
+        r.p = p;
+        r.mode = 0;
+        if (P->has_psi0 || p == 0) {
+            QVA_TRY(reset_state(P));
+            r.init = 0;
+        } else {
+            r.init = 1;
+            r.amp0 = 1.0 / sqrt((double)P->N);
+        }
+        r.expect = p > 0;
+        r.red_out = P->red;
+        PlanObserver obs(P);
+        QVA_TRY(fft_run(P->fft, r, P->stream, &obs));
+        *have_red = p > 0;
+        return QVA_OK;
+    }
+    // sparse
+    if (!P->sparse_set) {
+        set_error("sparse mixer not set");
+        return QVA_ERR_NOT_READY;
+    }
+    QVA_TRY(reset_state(P));
+    for (int k = 0; k < p; ++k) {
+        {
+            ProfScope ps(P, K_OTHER, 40.0 * P->arr_n);
+            QVA_CUDA_TRY(launch_phase(P->psi, P->q, P->arr_n, theta[2 * k], P->stream));
+        }
+        int terms = 0;
+        PlanObserver obs(P);
+        QVA_TRY(sparse_apply_mixer(P->sm, P->psi, theta[2 * k + 1], P->stream, &obs, &terms));
+    }
+    return QVA_OK;
+}
+
+qva_status qva_evolve(qva_plan *P, const double *theta, int32_t p) {
+    if (!P || p < 0 || (p > 0 && !theta)) return QVA_ERR_INVALID_ARGUMENT;
+    QVA_TRY(check_theta(theta, 2 * (size_t)p));
+    if (!P->q_set) {
+        set_error("qualities not set (PAPER.md:649: set_qualities is required)");
+        return QVA_ERR_NOT_READY;
+    }
+    if ((size_t)2 * p > P->thetas_cap) {
+        set_error("p too large");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    DeviceGuard dg(P->device);
+    P->expect_valid = false;
+    bool have = false;
+    QVA_TRY(evolve_impl(P, theta, p, &have));
+    if (have) {
+        double pair[2];
+        QVA_CUDA_TRY(cudaMemcpyAsync(pair, P->red, sizeof(pair), cudaMemcpyDeviceToHost, P->stream));
+        QVA_TRY(sync(P));
+        if (!P->replicated) QVA_TRY(allreduce_host(P, pair, 2));
+        P->expect_val = pair[0];
+        P->norm_val = pair[1];
+        P->expect_valid = true;
+        return QVA_OK;
+    }
+    return sync(P);
+}
+
+static qva_status expect_now(qva_plan *P) {
+    if (P->expect_valid) return QVA_OK;
+    if (!P->q_set) {
+        set_error("qualities not set");
+        return QVA_ERR_NOT_READY;
+    }
+    if (P->layout == 1) QVA_TRY(ensure_qB(P));
+    double pair[2];
+    QVA_TRY(expect_generic(P, P->psi, P->arr_n, q_current(P), pair));
+    if (!P->replicated) QVA_TRY(allreduce_host(P, pair, 2));
+    P->expect_val = pair[0];
+    P->norm_val = pair[1];
+    P->expect_valid = true;
+    return QVA_OK;
+}
+
+qva_status qva_expectation(qva_plan *P, double *out) {
+    if (!P || !out) return QVA_ERR_INVALID_ARGUMENT;
+    DeviceGuard dg(P->device);
+    QVA_TRY(expect_now(P));
+    *out = P->expect_val;
+    return QVA_OK;
+}
+
+qva_status qva_norm2(qva_plan *P, double *out) {
+    if (!P || !out) return QVA_ERR_INVALID_ARGUMENT;
+    DeviceGuard dg(P->device);
+    if (!P->q_set && !P->expect_valid) {
+        // norm does not need q: use zeros already in P->q
+        double pair[2];
+        QVA_TRY(expect_generic(P, P->psi, P->arr_n, P->q, pair));
+        if (!P->replicated) QVA_TRY(allreduce_host(P, pair, 2));
+        *out = pair[1];
+        return QVA_OK;
+    }
+    QVA_TRY(expect_now(P));
+    *out = P->norm_val;
+    return QVA_OK;
+}
+
+qva_status qva_get_state(qva_plan *P, double *re_im, uint64_t offset, uint64_t count) {
+    if (!P || (!re_im && count)) return QVA_ERR_INVALID_ARGUMENT;
+    uint64_t lo;
+    QVA_TRY(check_range(P, offset, count, &lo));
+    DeviceGuard dg(P->device);
+    if (P->layout == 1) {
+        bool ev = P->expect_valid;
+        QVA_TRY(to_layout_A(P));
+        P->expect_valid = ev;
+    }
+    if (count)
+        QVA_CUDA_TRY(cudaMemcpyAsync(re_im, P->psi + lo, count * sizeof(double2), cudaMemcpyDeviceToHost, P->stream));
+    return sync(P);
+}
+
+qva_status qva_get_probabilities(qva_plan *P, double *out, uint64_t offset, uint64_t count) {
+    if (!P || (!out && count)) return QVA_ERR_INVALID_ARGUMENT;
+    uint64_t lo;
+    QVA_TRY(check_range(P, offset, count, &lo));
+    if (!count) return QVA_OK;
+    DeviceGuard dg(P->device);
+    if (P->layout == 1) {
+        bool ev = P->expect_valid;
+        QVA_TRY(to_layout_A(P));
+        P->expect_valid = ev;
+    }
+    double *d;
+    QVA_CUDA_TRY(cudaMallocAsync((void **)&d, count * sizeof(double), P->stream));
+    {
+        ProfScope ps(P, K_OTHER, 24.0 * count);
+        QVA_CUDA_TRY(launch_probabilities(P->psi + lo, d, count, P->stream));
+    }
+    QVA_CUDA_TRY(cudaMemcpyAsync(out, d, count * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
+    QVA_CUDA_TRY(cudaFreeAsync(d, P->stream));
+    return sync(P);
+}
+
+// batch members [first, first+count) -> vals[2*i] (local sums; not reduced over COMM-psi)
+static qva_status batch_local(qva_plan *P, const double *thetas, int first, int count, int p, double *f_out) {
+    if (count <= 0) return QVA_OK;
+    const double *th = thetas + (size_t)first * 2 * p;
+    if (P->mixer == QVA_MIXER_X && P->G == 1 && (use_small(P) || P->batch_psi)) {
+        int chunk = use_small(P) ? count : std::min(count, P->max_batch);
+        for (int b0 = 0; b0 < count; b0 += chunk) {
+            int nb = std::min(chunk, count - b0);
+            std::vector<double> pairs(2 * (size_t)nb);
+            if (use_small(P)) {
+                size_t need = (size_t)nb * 2 * p;
+                if (need > P->thetas_cap) {
+                    cudaFree(P->d_thetas);
+                    P->d_thetas = nullptr;
+                    QVA_CUDA_TRY(cudaMalloc(&P->d_thetas, need * sizeof(double)));
+                    P->thetas_cap = need;
+                }
+                if ((size_t)nb > (size_t)P->max_batch) {
+                    cudaFree(P->red);
+                    P->red = nullptr;
+                    QVA_CUDA_TRY(cudaMalloc(&P->red, (size_t)nb * 2 * sizeof(double)));
+                    P->max_batch = nb;
+                }
+                double2 *bpsi = nullptr;
+                QVA_CUDA_TRY(cudaMallocAsync((void **)&bpsi, (size_t)nb * P->arr_n * sizeof(double2), P->stream));
+                QVA_CUDA_TRY(cudaMemcpyAsync(P->d_thetas, th + (size_t)b0 * 2 * p, need * sizeof(double),
+                                             cudaMemcpyHostToDevice, P->stream));
+                SmallEvolveParams sp{};
+                sp.psi = bpsi;
+                sp.psi0 = P->has_psi0 ? P->psi0 : nullptr;
+                sp.q = P->q;
+                sp.thetas = P->d_thetas;
+                sp.out = P->red;
+                sp.n = P->n;
+                sp.p = p;
+                sp.mode = 0;
+                {
+                    ProfScope ps(P, K_SMALL, 24.0 * P->arr_n * nb);
+                    QVA_CUDA_TRY(launch_small_evolve(sp, nb, P->stream));
+                }
+                QVA_CUDA_TRY(cudaMemcpyAsync(pairs.data(), P->red, pairs.size() * sizeof(double),
+                                             cudaMemcpyDeviceToHost, P->stream));
+                QVA_CUDA_TRY(cudaFreeAsync(bpsi, P->stream));
+                QVA_TRY(sync(P));
+            } else {
+                auto passes = cut_passes(evolve_tokens(P->L, 0, p), P->sets, true);
+                QVA_TRY(run_passes(P, passes, th + (size_t)b0 * 2 * p, p, nb, P->batch_psi, P->arr_n,
+                                   P->has_psi0 ? 2 : 1, pairs.data()));
+                QVA_TRY(sync(P));
+            }
+            for (int i = 0; i < nb; ++i) f_out[b0 + i] = pairs[2 * i];
+        }
+        return QVA_OK;
+    }
+    // generic: sequential members on the plan's own state
+    for (int i = 0; i < count; ++i) {
+        bool have = false;
+        QVA_TRY(evolve_impl(P, th + (size_t)i * 2 * p, p, &have));
+        double pair[2];
+        if (have) {
+            QVA_CUDA_TRY(cudaMemcpyAsync(pair, P->red, sizeof(pair), cudaMemcpyDeviceToHost, P->stream));
+            QVA_TRY(sync(P));
+        } else {
+            if (P->layout == 1) QVA_TRY(ensure_qB(P));
+            QVA_TRY(expect_generic(P, P->psi, P->arr_n, q_current(P), pair));
+        }
+        f_out[i] = pair[0];
+    }
+    return QVA_OK;
+}
+
+qva_status qva_evolve_batch(qva_plan *P, const double *thetas, int32_t B, int32_t p, double *f_out) {
+    if (!P || B < 0 || p < 0 || (B > 0 && (!thetas || !f_out))) return QVA_ERR_INVALID_ARGUMENT;
+    QVA_TRY(check_theta(thetas, (size_t)B * 2 * p));
+    if (!P->q_set) {
+        set_error("qualities not set");
+        return QVA_ERR_NOT_READY;
+    }
+    if ((size_t)2 * p > P->thetas_cap && !use_small(P)) {
+        set_error("p too large");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    DeviceGuard dg(P->device);
+    P->expect_valid = false;
+    std::vector<double> f((size_t)B, 0.0);
+    if (P->replicated && P->world > 1) {
+        // COMM-grad_f analogue: split the B sets over ranks, then all-reduce
+        int32_t first, cnt;
+        QVA_TRY(qva_batch_partition(B, P->world, P->rank, &first, &cnt));
+        std::vector<double> part(cnt > 0 ? cnt : 1);
+        QVA_TRY(batch_local(P, thetas, first, cnt, p, part.data()));
+        for (int i = 0; i < cnt; ++i) f[first + i] = part[i];
+        QVA_TRY(allreduce_host(P, f.data(), B));
+    } else {
+        QVA_TRY(batch_local(P, thetas, 0, B, p, f.data()));
+        if (!P->replicated && P->world > 1) QVA_TRY(allreduce_host(P, f.data(), B));
+    }
+    std::copy(f.begin(), f.end(), f_out);
+    return QVA_OK;
+}
+
+qva_status qva_set_profiling(qva_plan *P, int32_t enable) {
+    if (!P) return QVA_ERR_INVALID_ARGUMENT;
+    P->prof = enable != 0;
+    return QVA_OK;
+}
+
+qva_status qva_kernel_stats(qva_plan *P, int32_t which, double *ms, int64_t *launches, double *bytes) {
+    if (!P || which < 0 || which >= 8) return QVA_ERR_INVALID_ARGUMENT;
+    DeviceGuard dg(P->device);
+    QVA_TRY(sync(P));
+    if (ms) *ms = P->stats[which].ms;
+    if (launches) *launches = P->stats[which].launches;
+    if (bytes) *bytes = P->stats[which].bytes;
+    return QVA_OK;
+}
+
+qva_status qva_reset_kernel_stats(qva_plan *P) {
+    if (!P) return QVA_ERR_INVALID_ARGUMENT;
+    DeviceGuard dg(P->device);
+    QVA_TRY(sync(P));
+    for (auto &s : P->stats) s = KernelStat();
+    P->launches = 0;
+    return QVA_OK;
+}
+
+qva_status qva_launch_count(qva_plan *P, int64_t *launches) {
+    if (!P || !launches) return QVA_ERR_INVALID_ARGUMENT;
+    *launches = P->launches;
+    return QVA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+"""C-ABI library checks that need no GPU (`-m "not gpu"`): the library loads, exports every
+symbol include/qva.h declares, and its host-only logic (partition, batch split, X-mixer pass
+schedule) is right."""
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "qva.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(qva_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def Q():
+    import paper_2110_03963_b200 as Q
+    return Q
+
+
+def test_library_exports_every_declared_symbol(Q):
+    import ctypes
+    lib = ctypes.CDLL(Q.LIB_PATH)
+    declared = _declared_symbols()
+    assert len(declared) >= 30
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+    assert "sm_100a" in Q.qva_version()
+
+
+def test_library_is_sm100a_only(Q):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", Q.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_\d+a?", out))
+    assert archs == {"sm_100a"}, archs
+
+
+@pytest.mark.parametrize("N,world,sizes,offsets", [
+    (16, 4, [4, 4, 4, 4], [0, 4, 8, 12]),
+    (10, 4, [3, 3, 2, 2], [0, 3, 6, 8]),       # SPEC.md:46 remainder to leading ranks (R16)
+    (2, 4, [1, 1, 0, 0], [0, 1, 2, 2]),        # SPEC.md:47 zero-size ranks
+    (1 << 34, 8, [1 << 31] * 8, [r << 31 for r in range(8)]),
+])
+def test_partition(Q, N, world, sizes, offsets):
+    """Eqs. local_i / offset."""
+    got = [Q.qva_partition(N, world, r) for r in range(world)]
+    assert [g[0] for g in got] == sizes
+    assert [g[1] for g in got] == offsets
+
+
+def test_partition_errors(Q):
+    with pytest.raises(Q.QvaError):
+        Q.qva_partition(16, 0, 0)
+    with pytest.raises(Q.QvaError):
+        Q.qva_partition(16, 2, 2)
+
+
+@pytest.mark.parametrize("B,world", [(21, 1), (21, 2), (21, 8), (3, 8), (0, 4)])
+def test_batch_partition(Q, B, world):
+    parts = [Q.qva_batch_partition(B, world, r) for r in range(world)]
+    covered = []
+    for f, c in parts:
+        covered += list(range(f, f + c))
+    assert covered == list(range(B))
+    counts = [c for _, c in parts]
+    assert max(counts) - min(counts) <= 1
+
+
+@pytest.mark.parametrize("n,p", [(12, 1), (13, 2), (20, 5), (21, 3), (24, 2), (30, 3), (31, 2), (33, 4), (34, 2)])
+def test_x_schedule_covers_every_rotation_once(Q, n, p):
+    """The pass schedule applies each of the n single-qubit rotations exactly once per layer
+    and exactly p phases, with one HBM pass per tile set plus shared
+    layer-boundary passes."""
+    sched = Q.qva_x_schedule(n, p)
+    rots = sum(s[1] + s[3] for s in sched)
+    phases = sum(s[2] for s in sched)
+    assert rots == n * p
+    assert phases == p
+    n_sets = 1 + -(-(n - 12) // 9) if n > 12 else 1
+    # every layer boundary shares a pass: passes = (n_sets - 1) * p + 1 for n_sets >= 2
+    if n_sets >= 2:
+        assert len(sched) == (n_sets - 1) * p + 1
+    assert sched[0][1] == 0 and sched[0][2] == 1  # first pass: phase then rotations
+
+
+def test_x_schedule_n30_p3(Q):
+    """cfg4: 7 passes for 3 layers (vs 9 without layer-boundary fusion)."""
+    sched = Q.qva_x_schedule(30, 3)
+    assert len(sched) == 7
+
+
+def test_plan_create_without_gpu_fails_cleanly(Q):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(Q.QvaError) as ei:
+        Q.Plan(1 << 10, "x", n_qubits=10)
+    assert ei.value.status in (7, 6)  # QVA_ERR_CUDA / OUT_OF_MEMORY
+
+
+def test_plan_argument_errors(Q):
+    with pytest.raises(Q.QvaError) as ei:
+        Q.Plan(1000, "x", n_qubits=10)
+    assert ei.value.status == 5  # UNSUPPORTED: dim != 2^n
+    with pytest.raises(Q.QvaError) as ei:
+        Q.Plan(1 << 20, "x", n_qubits=20, virtual_shards=3)
+    assert ei.value.status == 5  # non power of two shards
+    with pytest.raises(Q.QvaError) as ei:
+        Q.Plan(720, "circulant", world=2, rank=0)
+    assert ei.value.status == 5

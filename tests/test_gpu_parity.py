@@ -1,0 +1,343 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tolerances (BASELINE.json north_star): max|d amplitude| <= 1e-10, relative <Q> error <= 1e-9
+(reading R14: scaled by max(|<Q>|, <|Q|>) when <Q> is near 0).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from qva_inputs import make_config, random_regular_graph, erdos_renyi_graph
+
+pytestmark = pytest.mark.gpu
+
+AMP_TOL = 1e-10
+F_TOL = 1e-9
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def Q():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2110_03963_b200 as Q
+    return Q
+
+
+def _f_close(got, ref, scale=None):
+    s = max(abs(ref), scale or 0.0, 1e-300)
+    assert abs(got - ref) <= F_TOL * s, (got, ref, abs(got - ref) / s)
+
+
+def _amp_close(got, ref):
+    d = np.max(np.abs(got - ref)) if len(ref) else 0.0
+    assert d <= AMP_TOL, d
+
+
+# ---------------------------------------------------------------- cfg1 (small path) ----
+def test_cfg1_full_state(Q):
+    wl = make_config("cfg1")
+    n = wl.n_qubits
+    q = O.maxcut_q(n, wl.edges_u, wl.edges_v)
+    ref = O.evolve_x(n, q, wl.theta)
+    with Q.Plan(wl.dim, "x", n_qubits=n) as P:
+        P.set_qualities_maxcut(wl.edges_u, wl.edges_v)
+        P.evolve(wl.theta)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, q))
+        assert abs(P.norm2() - 1) < 1e-12
+        np.testing.assert_allclose(P.get_probabilities(), np.abs(ref) ** 2, atol=1e-12)
+        # host-q path gives the same
+        P.set_qualities(q)
+        P.evolve(wl.theta)
+        _amp_close(P.get_state(), ref)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 9, 12])
+def test_small_path_sizes(Q, n):
+    rng = np.random.default_rng(n)
+    q = rng.standard_normal(1 << n)
+    theta = rng.uniform(0, math.pi, 6)
+    ref = O.evolve_x(n, q, theta)
+    with Q.Plan(1 << n, "x", n_qubits=n) as P:
+        P.set_qualities(q)
+        P.evolve(theta)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+
+
+# ---------------------------------------------------------------- tile path ----
+@pytest.mark.parametrize("n,p,weighted", [(13, 1, False), (14, 2, True), (16, 3, False), (20, 2, True),
+                                          (21, 4, False), (22, 1, True), (24, 2, False)])
+def test_tile_path_full_state(Q, n, p, weighted):
+    rng = np.random.default_rng(100 + n)
+    u, v = random_regular_graph(n, 3 if n % 2 == 0 else 4, rng)
+    w = rng.uniform(0, 1, len(u)) if weighted else None
+    theta = rng.uniform(0, math.pi, 2 * p)
+    q = O.maxcut_q(n, u, v, w)
+    ref = O.evolve_x(n, q, theta)
+    with Q.Plan(1 << n, "x", n_qubits=n) as P:
+        P.set_qualities_maxcut(u, v, w)
+        P.evolve(theta)
+        _f_close(P.expectation(), O.expectation(ref, q))
+        _amp_close(P.get_state(), ref)
+
+
+def test_tile_path_p0_and_norm(Q):
+    n = 14
+    q = np.linspace(-1, 1, 1 << n)
+    with Q.Plan(1 << n, "x", n_qubits=n) as P:
+        P.set_qualities(q)
+        P.evolve([])
+        _amp_close(P.get_state(), O.init_uniform(1 << n))
+        _f_close(P.expectation(), float(np.mean(q)), 1.0)
+
+
+@pytest.mark.parametrize("n", [8, 15])
+def test_step_level_phase_and_mixer(Q, n):
+    """qva_apply_phase / qva_apply_mixer on an arbitrary initial state vs oracle steps."""
+    rng = np.random.default_rng(7 + n)
+    psi0 = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi0 /= np.linalg.norm(psi0)
+    q = rng.standard_normal(1 << n) * 5
+    with Q.Plan(1 << n, "x", n_qubits=n) as P:
+        P.set_qualities(q)
+        P.set_initial_state(psi0)
+        P.reset_state()
+        P.apply_phase(0.83)
+        ref = O.phase(psi0.copy(), q, 0.83)
+        _amp_close(P.get_state(), ref)
+        P.apply_mixer(2.1)
+        O.mixer_x(ref, 2.1)
+        _amp_close(P.get_state(), ref)
+        # evolve from the custom psi0
+        theta = [0.3, 1.2, 2.2, 0.4]
+        P.evolve(theta)
+        _amp_close(P.get_state(), O.evolve_x(n, q, theta, psi0=psi0))
+        P.clear_initial_state()
+        P.evolve(theta)
+        _amp_close(P.get_state(), O.evolve_x(n, q, theta))
+
+
+def test_P2_basis_state_closed_form_on_gpu(Q):
+    """P2 at n=22 through the tile path: <y|U_M|x0> = cos^{n-d} b (-i sin b)^d."""
+    n, beta, x0 = 22, 0.7, 0b1011001110100101101001
+    psi0 = np.zeros(1 << n, np.complex128)
+    psi0[x0] = 1.0
+    with Q.Plan(1 << n, "x", n_qubits=n) as P:
+        P.set_qualities(np.zeros(1 << n))
+        P.set_initial_state(psi0)
+        P.reset_state()
+        P.apply_mixer(beta)
+        got = P.get_state()
+    ys = np.arange(1 << n, dtype=np.int64)
+    d = np.zeros(1 << n, np.int64)
+    xx = ys ^ x0
+    for j in range(n):
+        d += (xx >> j) & 1
+    ref = np.cos(beta) ** (n - d) * (-1j * np.sin(beta)) ** d
+    _amp_close(got, ref)
+
+
+# ---------------------------------------------------------------- cfg2 batch ----
+def test_cfg2_batch_gradient(Q):
+    wl = make_config("cfg2")
+    n = wl.n_qubits
+    q = O.maxcut_q(n, wl.edges_u, wl.edges_v, wl.weights)
+    ref = np.array([O.expectation(O.evolve_x(n, q, t), q) for t in wl.batch_thetas])
+    with Q.Plan(wl.dim, "x", n_qubits=n, max_batch=21) as P:
+        P.set_qualities_maxcut(wl.edges_u, wl.edges_v, wl.weights)
+        f = P.evolve_batch(wl.batch_thetas)
+        for a, b in zip(f, ref):
+            _f_close(a, b)
+        # member 0 equals an independent evolve (P13)
+        P.evolve(wl.batch_thetas[0])
+        assert abs(P.expectation() - f[0]) <= 1e-12 * abs(f[0])
+    h = wl.fd_h
+    g = (f[1::2] - f[2::2]) / (2 * h)
+    gref = (ref[1::2] - ref[2::2]) / (2 * h)
+    np.testing.assert_allclose(g, gref, atol=1e-6)
+
+
+def test_small_batch(Q):
+    wl = make_config("cfg1")
+    n = wl.n_qubits
+    q = O.maxcut_q(n, wl.edges_u, wl.edges_v)
+    rng = np.random.default_rng(3)
+    th = rng.uniform(0, math.pi, (9, 2 * wl.p))
+    ref = [O.expectation(O.evolve_x(n, q, t), q) for t in th]
+    with Q.Plan(wl.dim, "x", n_qubits=n) as P:
+        P.set_qualities(q)
+        f = P.evolve_batch(th)
+    for a, b in zip(f, ref):
+        _f_close(a, b)
+
+
+# ---------------------------------------------------------------- cfg3 circulant ----
+def test_cfg3_full(Q):
+    wl = make_config("cfg3")
+    ref = O.evolve_complete(wl.q, wl.theta, wl.lam0, wl.lam_rest)
+    fref = O.expectation(ref, wl.q)
+    aref = O.expectation(ref, np.abs(wl.q))
+    with Q.Plan(wl.dim, "circulant") as P:
+        P.set_qualities(wl.q)
+        P.set_circulant_eigenvalues_const(wl.lam0, wl.lam_rest)
+        P.evolve(wl.theta)
+        _f_close(P.expectation(), fref, aref)
+        _amp_close(P.get_state(), ref)
+        # same spectrum as an explicit array (generic lambda path)
+        lam = np.full(wl.dim, wl.lam_rest)
+        lam[0] = wl.lam0
+        P.set_circulant_eigenvalues(lam)
+        P.evolve(wl.theta)
+        _amp_close(P.get_state(), ref)
+
+
+@pytest.mark.parametrize("N", [2, 7, 13, 96, 720, 1001, 4096, 5040, 6144])
+def test_circulant_random_spectrum_vs_dense(Q, N):
+    """Generic real spectrum: whole-CTA kernel (N <= 4096) and four-step (N > 4096)."""
+    rng = np.random.default_rng(N)
+    q = rng.standard_normal(N)
+    lam = rng.standard_normal(N) * 4
+    theta = rng.uniform(0, math.pi, 4)
+    ref = O.evolve_circulant_dense(q, lam, theta)
+    with Q.Plan(N, "circulant") as P:
+        P.set_qualities(q)
+        P.set_circulant_eigenvalues(lam)
+        P.evolve(theta)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+        # single mixer step
+        P.reset_state()
+        P.apply_mixer(0.9)
+        _amp_close(P.get_state(), O.mixer_circulant_dense(O.init_uniform(N), lam, 0.9))
+
+
+# ---------------------------------------------------------------- cfg4 full size ----
+def test_cfg4_full_size_vs_golden(Q):
+    g = json.load(open(os.path.join(GOLD, "cfg4_n30.json")))
+    wl = make_config("cfg4")
+    assert np.allclose(g["theta"], wl.theta, rtol=0, atol=0)
+    with Q.Plan(wl.dim, "x", n_qubits=wl.n_qubits) as P:
+        P.set_qualities_maxcut(wl.edges_u, wl.edges_v)
+        P.evolve(wl.theta)
+        _f_close(P.expectation(), g["expectation_full_state"])
+        _f_close(P.expectation(), g["expectation_lightcone"])
+        assert abs(P.norm2() - 1) < 1e-12
+        idx = np.asarray(g["sample_index"], np.int64)
+        ref = np.asarray(g["sample_re"]) + 1j * np.asarray(g["sample_im"])
+        got = np.array([P.get_state(int(i), 1)[0] for i in idx])
+        _amp_close(got, ref)
+
+
+# ---------------------------------------------------------------- sharded schedule ----
+@pytest.mark.parametrize("n,G,p", [(14, 2, 1), (15, 4, 2), (16, 8, 3), (20, 8, 2), (21, 2, 3)])
+def test_virtual_shards_vs_oracle(Q, n, G, p):
+    """COMM-psi sharding with G shards on one GPU (loopback exchange):
+    same schedule, layouts and exchange mapping as the multi-GPU path."""
+    rng = np.random.default_rng(n * G)
+    u, v = random_regular_graph(n, 4, rng)
+    w = rng.uniform(0, 1, len(u))
+    theta = rng.uniform(0, math.pi, 2 * p)
+    q = O.maxcut_q(n, u, v, w)
+    ref = O.evolve_x(n, q, theta)
+    with Q.Plan(1 << n, "x", n_qubits=n, virtual_shards=G) as P:
+        P.set_qualities(q)  # generic path: layout-B q is built by the exchange (C7)
+        P.evolve(theta)
+        _f_close(P.expectation(), O.expectation(ref, q))
+        _amp_close(P.get_state(), ref)
+        P.set_qualities_maxcut(u, v, w)
+        P.evolve(theta)
+        _amp_close(P.get_state(), ref)
+        # step-level mixer on the sharded state
+        P.reset_state()
+        P.apply_phase(0.5)
+        P.apply_mixer(1.3)
+        r2 = O.init_uniform(1 << n)
+        O.phase(r2, q, 0.5)
+        O.mixer_x(r2, 1.3)
+        _amp_close(P.get_state(), r2)
+
+
+# ---------------------------------------------------------------- sparse (Taylor) ----
+def _csr(W):
+    rows, cols = np.nonzero(W)
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    rp = np.zeros(W.shape[0] + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    return np.cumsum(rp), cols.astype(np.int32), W[rows, cols]
+
+
+def test_sparse_spec_example(Q):
+    """N=2, W=X, t=pi/2, |0> -> -i|1>."""
+    with Q.Plan(2, "sparse") as P:
+        rp, c, v = _csr(np.array([[0.0, 1.0], [1.0, 0.0]]))
+        P.set_sparse_mixer(rp, c, v)
+        P.set_qualities([0.0, 0.0])
+        P.set_initial_state(np.array([1.0, 0.0], np.complex128))
+        P.reset_state()
+        P.apply_mixer(math.pi / 2)
+        _amp_close(P.get_state(), np.array([0, -1j]))
+
+
+@pytest.mark.parametrize("N,density", [(64, 0.1), (300, 0.03), (1024, 0.005)])
+def test_sparse_vs_dense_expm(Q, N, density):
+    rng = np.random.default_rng(N)
+    A = (rng.random((N, N)) < density) * rng.uniform(-1, 1, (N, N))
+    W = np.triu(A, 1)
+    W = W + W.T + np.diag(rng.uniform(-1, 1, N))
+    q = rng.standard_normal(N)
+    theta = rng.uniform(0, math.pi, 4)
+    ref = O.evolve_sparse_dense(q, W, theta)
+    rp, c, v = _csr(W)
+    with Q.Plan(N, "sparse") as P:
+        P.set_sparse_mixer(rp, c, v)
+        P.set_qualities(q)
+        P.evolve(theta)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+
+
+def test_sparse_hypercube_vs_x_mixer(Q):
+    """X mixer given as a CSR hypercube adjacency (val=NULL) vs the X-mixer oracle, n=14."""
+    n = 14
+    N = 1 << n
+    idx = np.arange(N)
+    cols = np.stack([idx ^ (1 << j) for j in range(n)], axis=1)
+    cols.sort(axis=1)
+    rp = np.arange(0, N * n + 1, n, dtype=np.int64)
+    rng = np.random.default_rng(1)
+    u, v = random_regular_graph(n, 3, rng)
+    q = O.maxcut_q(n, u, v)
+    theta = [0.4, 2.5, 1.1, 0.6]
+    with Q.Plan(N, "sparse") as P:
+        P.set_sparse_mixer(rp, cols.reshape(-1).astype(np.int32), None)
+        P.set_qualities(q)
+        P.evolve(theta)
+        _amp_close(P.get_state(), O.evolve_x(n, q, theta))
+
+
+# ---------------------------------------------------------------- errors ----
+def test_error_paths(Q):
+    with Q.Plan(1 << 13, "x", n_qubits=13) as P:
+        with pytest.raises(Q.QvaError) as ei:
+            P.evolve([0.1, 0.2])
+        assert ei.value.status == 3  # NOT_READY
+        q = np.zeros(1 << 13)
+        q[5] = np.nan
+        with pytest.raises(Q.QvaError) as ei:
+            P.set_qualities(q)
+        assert ei.value.status == 4  # NUMERIC
+        with pytest.raises(Q.QvaError) as ei:
+            P.get_state(8000, 500)
+        assert ei.value.status == 2  # SIZE_MISMATCH
+        P.set_qualities(np.zeros(1 << 13))
+        with pytest.raises(Q.QvaError) as ei:
+            P.evolve([0.1, float("inf")])
+        assert ei.value.status == 4
