@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Benchmark of the QVA hot path (BASELINE.json metric: amplitude-layers/s and achieved HBM
+GB/s, fp64 complex, at 1/2/4/8 B200).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4|cfg5|cfg5w|cfg2|cfg3|cfg1]
+                  [--impl ours|reference]
+  N > 1: python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+             --master-port P bench.py --gpus N ...
+
+A step = one full evaluation of the objective f(theta) = <psi(theta)|Q|psi(theta)>
+(all p layers of phase + mixer, then <Q>) on seeded synthetic inputs (qva_inputs).
+Default workload: N=1 -> cfg4 (QAOA MaxCut n=30, p=3); N>1 -> cfg5 family with 2^30
+amplitudes per GPU (n = 30 + log2 N, p=2, sharded over the GPUs with the global<->local
+qubit all-to-all), i.e. weak scaling.  Every state is 16 GiB per GPU, larger than L2, so no
+L2 flush is needed between steps.
+
+`value`  : device-timed (CUDA events on the launch stream, barrier + synchronize on both sides,
+           max over ranks) whole-job amp-layers/s with q already resident in HBM.
+`e2e`    : same metric through the public API with HOST buffers: each step uploads q from
+           pinned host memory (qva_set_qualities), evolves from a host theta and reads <Q> back.
+`roofline`: dominant kernel (the X-mixer tile pass): algorithmic bytes per launch / mean launch
+           time (CUDA events around each launch on the plan's stream) vs measured HBM copy peak.
+`cpu_baseline` / --impl reference: the CPU oracle (oracle/) on a bounded sample of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from qva_inputs import make_config  # noqa: E402
+
+METRIC = "amplitude-layers/sec and achieved HBM GB/s (fp64 complex) at 1/2/4/8 B200"
+UNIT = "amp-layers/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _ncu_traffic(kernel: str):
+    """dram read+write bytes per launch from the committed ncu --set full capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+
+        def reader():
+            for line in self.proc.stdout:
+                self.rows.append([x.strip() for x in line.split(",")])
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+                for k, nm in enumerate(names):
+                    if r[3 + k].lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload_for(args, world):
+    if args.workload:
+        name = args.workload
+    else:
+        name = "cfg4" if world == 1 else "cfg5w"
+    if name == "cfg5w":
+        n = 30 + int(round(math.log2(world)))
+        wl = make_config("cfg5", n_override=n)
+        desc = f"cfg5 family weak scaling: QAOA weighted MaxCut n={n} (2^30 amps/GPU), 4-regular, p={wl.p}"
+    elif name == "cfg5":
+        wl = make_config("cfg5")
+        desc = f"cfg5: QAOA weighted MaxCut n={wl.n_qubits}, 4-regular, p={wl.p}, sharded"
+    elif name == "cfg4":
+        wl = make_config("cfg4")
+        desc = f"cfg4: QAOA MaxCut n={wl.n_qubits} (16 GiB state), random 3-regular, unit weights, p={wl.p}"
+    elif name == "cfg2":
+        wl = make_config("cfg2")
+        desc = "cfg2: QAOA weighted MaxCut n=20, G(20,0.5), p=5, batch of 21 FD parameter sets"
+    elif name == "cfg3":
+        wl = make_config("cfg3")
+        desc = "cfg3: QWOA N=10!, q~N(0,1), complete-graph Laplacian circulant mixer via FFT, p=4"
+    elif name == "cfg1":
+        wl = make_config("cfg1")
+        desc = "cfg1: QAOA MaxCut n=10, 3-regular, p=2"
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    return name, wl, desc
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU oracle arm (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------------------------
+def oracle_sample(name, wl, budget_s=20.0):
+    """Time the CPU oracle, as it stands, on a bounded sample of the same workload.
+    Returns (amp-layers/s, seconds, cores, sample description)."""
+    import oracle as O
+    cores = O.num_threads()
+
+    def run(swl):
+        q = O.maxcut_q(swl.n_qubits, swl.edges_u, swl.edges_v, swl.weights)
+        t0 = time.perf_counter()
+        psi = O.evolve_x(swl.n_qubits, q, swl.theta)
+        f = O.expectation(psi, q)
+        return time.perf_counter() - t0, f
+
+    if wl.mixer == "x" and name in ("cfg4", "cfg5", "cfg5w"):
+        fam = "cfg4" if name == "cfg4" else "cfg5"
+        step = 2 if fam == "cfg4" else 1          # 3-regular graphs need an even vertex count
+        n0 = 20
+        t0, _ = run(make_config(fam, n_override=n0))
+        n = n0
+        while n + step <= wl.n_qubits and t0 * 2 ** (n + step - n0) * (n + step) / n0 <= budget_s:
+            n += step
+        swl = make_config(fam, n_override=n)
+        dt, f = run(swl)
+        desc = (f"oracle full p={swl.p} evolution + <Q> of the {fam} recipe at n={n} (2^{n} amplitudes; "
+                f"the full workload has 2^{wl.n_qubits}), {cores} OpenMP threads, f={f:.6f}")
+        return (1 << n) * swl.p / dt, dt, cores, desc
+    if wl.mixer == "x":
+        B = len(wl.batch_thetas) if wl.batch_thetas is not None else 1
+        q = O.maxcut_q(wl.n_qubits, wl.edges_u, wl.edges_v, wl.weights)
+        t0 = time.perf_counter()
+        nb = 0
+        thetas = wl.batch_thetas if wl.batch_thetas is not None else [wl.theta]
+        for th in thetas:
+            O.expectation(O.evolve_x(wl.n_qubits, q, th), q)
+            nb += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        desc = f"oracle evolution + <Q> of {nb} of the {B} parameter sets of {name} (n={wl.n_qubits}), {cores} threads"
+        return wl.dim * wl.p * nb / dt, dt, cores, desc
+    # circulant: closed-form oracle on the full cfg3 size
+    t0 = time.perf_counter()
+    psi = O.evolve_complete(wl.q, wl.theta, wl.lam0, wl.lam_rest)
+    O.expectation(psi, wl.q)
+    dt = time.perf_counter() - t0
+    return wl.dim * wl.p / dt, dt, cores, f"oracle closed-form QWOA evolution at N={wl.dim}, p={wl.p}, {cores} threads"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    name, wl, desc = workload_for(args, world)
+    budget = max(3.0, 150.0 / max(1, args.steps + args.warmup))
+    vals, times = [], []
+    info = None
+    for i in range(args.warmup + args.steps):
+        v, dt, cores, sdesc = oracle_sample(name, wl, budget_s=budget)
+        if i >= args.warmup:
+            vals.append(v)
+            times.append(dt)
+        info = (cores, sdesc)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info[0], "kind": "oracle", "sample": info[1]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import paper_2110_03963_b200 as Q
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    name, wl, desc = workload_for(args, world)
+    # a dedicated (non-default) stream: the plan launches on it and the CUDA events below are
+    # recorded on it, so they bracket exactly the plan's kernels
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+
+    nccl_id = None
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(Q.qva_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+
+    batch = wl.batch_thetas if name == "cfg2" else None
+    plan = Q.Plan(wl.dim, wl.mixer, n_qubits=wl.n_qubits, rank=rank, world=world, nccl_id=nccl_id,
+                  device=local_rank, stream=stream.cuda_stream, max_batch=len(batch) if batch is not None else 1)
+    if wl.mixer == "x":
+        plan.set_qualities_maxcut(wl.edges_u, wl.edges_v, wl.weights)
+    else:
+        plan.set_qualities(wl.q)
+        plan.set_circulant_eigenvalues_const(wl.lam0, wl.lam_rest)
+    local_n, offset = plan.get_partition()
+    theta = wl.theta
+    B = len(batch) if batch is not None else 1
+
+    def step():
+        if batch is not None:
+            return plan.evolve_batch(batch)
+        plan.evolve(theta)
+        return plan.expectation()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    plan.reset_kernel_stats()
+    plan.set_profiling(True)
+    l0 = plan.launch_count()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        f = step()
+    ev1.record(stream)
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = plan.launch_count() - l0
+    plan.set_profiling(False)
+    clk = clocks.stop()
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    amp_layers = float(wl.dim) * wl.p * B  # whole job, per step
+    value = amp_layers / (ms_step * 1e-3)
+
+    # dominant kernel
+    cls = "tile" if wl.mixer == "x" and wl.n_qubits > 12 else ("small" if wl.mixer == "x" else "fft_col")
+    st = plan.kernel_stats(cls)
+    kernel_share = None
+    total_kernel_ms = sum(plan.kernel_stats(c)["ms"] for c in Q.KERNEL_CLASSES)
+    if total_kernel_ms > 0:
+        kernel_share = st["ms"] / total_kernel_ms
+    peak, peak_src = _peaks()
+    roof = None
+    if st["launches"] > 0 and st["ms"] > 0:
+        per_launch_bytes = st["bytes"] / st["launches"]
+        per_launch_s = st["ms"] * 1e-3 / st["launches"]
+        achieved = per_launch_bytes / per_launch_s / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": _ncu_traffic(cls), "kernel": f"{cls} pass", "algorithmic_bytes_per_launch": per_launch_bytes,
+                "mean_launch_ms": st["ms"] / st["launches"], "launches": st["launches"],
+                "share_of_kernel_time": kernel_share, "peak_source": peak_src}
+    # whole-step model bytes (all kernels' algorithmic bytes) / step time
+    total_bytes = sum(plan.kernel_stats(c)["bytes"] for c in Q.KERNEL_CLASSES)
+    achieved_step_gbs = total_bytes / args.steps / (ms_step * 1e-3) / 1e9 / max(1, 1)
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e and wl.mixer == "x" and batch is None:
+        q_host = torch.empty(local_n, dtype=torch.float64, pin_memory=True)
+        qn = q_host.numpy()
+        plan.get_qualities(offset, local_n, out=qn)
+        th_host = np.ascontiguousarray(theta, np.float64)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        ksteps = max(2, min(args.steps, 5))
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(ksteps):
+            plan.set_qualities(qn, offset)
+            plan.evolve(th_host)
+            fe = plan.expectation()
+        e1.record(stream)
+        barrier()
+        wall = time.perf_counter() - t0
+        ems = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": amp_layers / (ems / ksteps * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(local_n * 8 + th_host.nbytes), "d2h_bytes_per_step": 8,
+               "ms_per_step": ems / ksteps, "wall_ms_per_step": wall * 1e3 / ksteps, "steps": ksteps,
+               "what": "qva_set_qualities(pinned host q) + qva_evolve(host theta) + qva_expectation -> host"}
+        assert abs(fe - f) <= 1e-9 * max(1.0, abs(f))
+        del q_host
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, cores, sdesc = oracle_sample(name, wl, budget_s=20.0)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sdesc, "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "dim": wl.dim, "p": wl.p, "batch": B,
+                       "amplitudes_per_gpu": local_n,
+                       "l2": "inputs larger than L2: 16 GiB state per GPU, no flush" if local_n >= (1 << 26)
+                       else "state fits in L2 (126 MB); no flush (L2-resident workload)",
+                       "parallelism": f"state sharded over {world} GPUs" if world > 1 else "1 GPU"},
+            "achieved_hbm_gbs_step": achieved_step_gbs,
+            "objective": f if batch is None else float(np.asarray(f)[0]),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    plan.destroy()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
