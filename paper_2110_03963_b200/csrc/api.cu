@@ -17,6 +17,15 @@ namespace qva {
 
 static thread_local std::string g_last_error;
 void set_error(const std::string &msg) { g_last_error = msg; }
+// QVA_TRACE=1: per-launch device times of profiled plans on stderr; 2: also each pass's program
+static int g_tstore = [] {
+    const char *e = getenv("QVA_TSTORE");
+    return e ? atoi(e) : -1;
+}();
+static int g_trace = [] {
+    const char *e = getenv("QVA_TRACE");
+    return e ? atoi(e) : 0;
+}();
 
 // ---------------------------------------------------------------------------------------------
 // X-mixer schedule
@@ -78,10 +87,18 @@ static std::vector<PassPlan> cut_passes(const std::vector<Token> &toks, const st
     size_t pos = 0;
     uint64_t pending = 0;
     int cur_layer = -1;
+    // Each qubit is rotated by the set that owns it: set 0 owns its 12 bits, set i > 0 owns the
+    // bits it adds (its copies of bits 0..2 and padding bits only carry 128-B contiguity).
+    std::vector<uint64_t> own(sets.size());
+    uint64_t seen = 0;
+    for (size_t i = 0; i < sets.size(); ++i) {
+        own[i] = set_mask(sets[i]) & ~seen;
+        seen |= set_mask(sets[i]);
+    }
     auto best_set = [&](uint64_t want) {
         int best = 0, bc = -1;
         for (int i = 0; i < (int)sets.size(); ++i) {
-            int c = __builtin_popcountll(want & set_mask(sets[i]));
+            int c = __builtin_popcountll(want & own[i]);
             if (c > bc) { bc = c; best = i; }
         }
         return best;
@@ -100,7 +117,7 @@ static std::vector<PassPlan> cut_passes(const std::vector<Token> &toks, const st
             toks[pos + 1].kind == Token::ROT)
             want = toks[pos + 1].bits;
         pp.set = best_set(want);
-        uint64_t sm = set_mask(sets[pp.set]);
+        uint64_t sm = own[pp.set];
         uint64_t r1 = pending & sm;
         pending &= ~r1;
         pp.r1 = to_local(sets[pp.set], r1);
@@ -152,30 +169,105 @@ static std::vector<Token> mixer_tokens(int L, int g) {
     return t;
 }
 
-static void build_steps(const PassPlan &pp, TilePassParams &tp) {
-    std::vector<PassStep> st;
-    const int order1[3] = {2, 0, 1};
-    for (int g : order1) {
-        int m = (pp.r1 >> (4 * g)) & 15;
-        if (m) st.push_back({(int8_t)g, (int8_t)m, 0, 0});
+// Register groups (tile-local bits).  Every rotated tile bit belongs to
+// exactly one group: 3..7 -> X, 8..11 -> Y, 0..2 -> W.  Lanes 0-2 of X and Y address tile bits
+// 0..2 (128-B contiguous global stores); W's lanes 0-2 address bits 3..5.  Under SWIZZLE_128B
+// both choices make every 8-lane phase of a 16-byte smem access conflict-free.
+static const TileGroup kGroups[kMaxGroups] = {
+    {{3, 4, 5, 6, 7}, {0, 1, 2, 8, 9, 10, 11}},   // X
+    {{8, 9, 10, 11, 3}, {0, 1, 2, 4, 5, 6, 7}},   // Y
+    {{0, 1, 2, 6, 7}, {3, 4, 5, 8, 9, 10, 11}},   // W
+};
+static int group_of_bit(int b) { return b >= 8 ? 1 : (b >= 3 ? 0 : 2); }
+static int ebit_index(int g, int b) {
+    for (int j = 0; j < kGroupBits; ++j)
+        if (kGroups[g].ebit[j] == b) return j;
+    return -1;
+}
+
+// Step list of one pass: R1 (angle slot 0), optional phase, R2 (slot 1), optional expectation,
+// over the fewest group changes.  pref_gq: preferred q group (reuse of an existing q copy).
+static void build_steps(const PassPlan &pp, TilePassParams &tp, int pref_gq, bool half1, bool half2) {
+    int m1[kMaxGroups] = {0, 0, 0}, m2[kMaxGroups] = {0, 0, 0};
+    for (int b = 0; b < kTileBits; ++b) {
+        int g = group_of_bit(b), j = ebit_index(g, b);
+        if ((pp.r1 >> b) & 1) m1[g] |= 1 << j;
+        if ((pp.r2 >> b) & 1) m2[g] |= 1 << j;
     }
-    if (pp.phase >= 0) {
-        if (st.empty()) st.push_back({2, 0, 0, 1});
-        else st.back().phase = 1;
+    std::vector<int> G1, G2;
+    for (int g = 0; g < kMaxGroups; ++g) {
+        if (m1[g]) G1.push_back(g);
+        if (m2[g]) G2.push_back(g);
     }
-    int cur = st.empty() ? 2 : st.back().group;
-    int order2[3];
-    if (cur == 0) { order2[0] = 0; order2[1] = 1; order2[2] = 2; }
-    else { order2[0] = cur; order2[1] = 0; order2[2] = (cur == 1) ? 2 : 1; }
-    for (int g : order2) {
-        int m = (pp.r2 >> (4 * g)) & 15;
-        if (m) st.push_back({(int8_t)g, (int8_t)m, 1, 0});
+    const bool phase = pp.phase >= 0, expect = pp.expect;
+    std::vector<PassStep> best;
+    int best_gq = -1;
+    double best_cost = 1e30;
+    std::vector<int> o1 = G1;
+    std::sort(o1.begin(), o1.end());
+    do {
+        std::vector<int> o2 = G2;
+        std::sort(o2.begin(), o2.end());
+        do {
+            for (int gp_choice = 0; gp_choice < kMaxGroups; ++gp_choice) {
+                std::vector<PassStep> st;
+                for (int g : o1) {
+                    st.push_back({(int8_t)g, (int8_t)m1[g], 0, 0});
+                    if (half1) st.push_back({(int8_t)g, (int8_t)m1[g], 0, 0});  // two half-angle steps
+                }
+                int gp = -1;
+                if (phase) {
+                    if (!st.empty()) gp = st.back().group;
+                    else if (!o2.empty()) gp = o2.front();
+                    else gp = gp_choice;
+                    if (!st.empty()) st.back().phase = 1;
+                    else st.push_back({(int8_t)gp, 0, 0, 1});
+                } else if (gp_choice) {
+                    continue;
+                }
+                for (int g : o2) {
+                    st.push_back({(int8_t)g, (int8_t)m2[g], 1, 0});
+                    if (half2) st.push_back({(int8_t)g, (int8_t)m2[g], 1, 0});
+                }
+                if (st.empty()) st.push_back({(int8_t)(expect && pref_gq >= 0 ? pref_gq : 0), 0, 0, 0});
+                int gq = phase ? gp : (expect ? st.back().group : -1);
+                if (expect && phase && st.back().group != gp) st.push_back({(int8_t)gp, 0, 0, 0});
+                double cost = 0.0;
+                for (size_t i = 1; i < st.size(); ++i) cost += st[i].group != st[i - 1].group;
+                if (st.back().group == 2) cost += 0.25;      // W: 16-B (not 128-B) store runs per lane group
+                if (gq >= 0 && pref_gq >= 0 && gq != pref_gq) cost += 0.5;  // would need another q copy
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best = st;
+                    best_gq = gq;
+                }
+            }
+        } while (std::next_permutation(o2.begin(), o2.end()));
+    } while (std::next_permutation(o1.begin(), o1.end()));
+    tp.n_groups = kMaxGroups;
+    for (int g = 0; g < kMaxGroups; ++g) tp.groups[g] = kGroups[g];
+    tp.n_steps = (int)best.size();
+    for (int i = 0; i < tp.n_steps; ++i) tp.steps[i] = best[i];
+    tp.gq = best_gq;
+    const TileGroup &gf = kGroups[best.back().group];
+    for (int j = 0; j < kGroupBits; ++j) tp.st_estr[j] = 1ull << tp.tile_bits[gf.ebit[j]];
+    for (int j = 0; j < kCT_BITS; ++j) tp.st_tphys[j] = tp.tile_bits[gf.tbit[j]];
+}
+
+// the compile-time program (kTileProgs) whose shape equals this pass, or 0 (generic)
+static int match_prog(const TilePassParams &tp) {
+    for (int q = 1; q < kNumTileProgs; ++q) {
+        const TileProg &D = kTileProgs[q];
+        if (D.n != tp.n_steps || D.expect != (tp.expect != 0)) continue;
+        if ((q == 5) != (tp.init == 1)) continue;  // program 5 starts from |+> without a load
+        bool ok = true;
+        for (int k = 0; k < D.n && ok; ++k) {
+            const PassStep &st = tp.steps[k];
+            ok = st.group == D.g[k] && (st.phase != 0) == (k == D.phase_k) && (D.rot[k] || st.mask == 0);
+        }
+        if (ok) return q;
     }
-    if (st.empty()) st.push_back({2, 0, 0, 0});
-    if (st.front().group == 0) st.insert(st.begin(), PassStep{2, 0, 0, 0});
-    if (st.back().group == 0) st.push_back({2, 0, 0, 0});
-    tp.n_steps = (int)st.size();
-    for (int i = 0; i < tp.n_steps; ++i) tp.steps[i] = st[i];
+    return 0;
 }
 
 }  // namespace qva
@@ -211,6 +303,23 @@ struct qva_plan {
     double2 *psi = nullptr, *psi_alt = nullptr, *psi0 = nullptr;
     double *q = nullptr, *qB = nullptr;
     bool q_set = false, qB_valid = false, has_psi0 = false;
+    // compact integer quality codes (q integer-valued in a small range)
+    int q_mode = 0;                    // 0 fp64, 1 int8, 2 int16
+    int qmin = 0, qmax = 0;
+    void *qc = nullptr, *qcB = nullptr;
+    bool qcB_valid = false;
+    bool q_classified = false;
+    double2 *d_tab = nullptr;
+    size_t tab_cap = 0;
+    double *d_gam = nullptr;
+    size_t gam_cap = 0;
+    // q permuted into the consumer order of (layout, tile set, register group): see
+    // qt_gather_kernel.  Rebuilt lazily after every change of q.
+    struct QtEntry {
+        int layout, set, group, qbytes;
+        void *buf;
+    };
+    std::vector<QtEntry> qt_cache;
     int layout = 0;
     double *partials = nullptr;
     uint64_t partials_n = 0;
@@ -293,6 +402,7 @@ qva_status harvest(qva_plan *P) {
     for (auto &pe : P->pending) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, pe.a, pe.b);
+        if (g_trace) fprintf(stderr, "[qva] class %d %.3f ms %.3f GB\n", pe.cls, ms, pe.bytes * 1e-9);
         P->stats[pe.cls].ms += ms;
         P->stats[pe.cls].launches += 1;
         P->stats[pe.cls].bytes += pe.bytes;
@@ -390,16 +500,128 @@ qva_status exchange_state(qva_plan *P) {
 }
 
 qva_status ensure_qB(qva_plan *P) {
-    if (P->G == 1 || P->qB_valid) return QVA_OK;
-    if (!P->qB) QVA_CUDA_TRY(cudaMalloc(&P->qB, P->arr_n * sizeof(double)));
-    QVA_TRY(exchange_buffers<double>(P, P->q, P->qB));
-    P->qB_valid = true;
+    if (P->G == 1) return QVA_OK;
+    if (!P->qB_valid) {
+        if (!P->qB) QVA_CUDA_TRY(cudaMalloc(&P->qB, P->arr_n * sizeof(double)));
+        QVA_TRY(exchange_buffers<double>(P, P->q, P->qB));
+        P->qB_valid = true;
+    }
+    if (P->q_mode && !P->qcB_valid) {
+        int eb = P->q_mode == 1 ? 1 : 2;
+        if (!P->qcB) QVA_CUDA_TRY(cudaMalloc(&P->qcB, P->arr_n * eb));
+        uint64_t C = (1ull << P->L) / P->G;
+        if (P->world == 1) {
+            ProfScope ps(P, K_EXCHANGE, 2.0 * eb * (double)P->arr_n);
+            QVA_CUDA_TRY(launch_chunk_transpose_bytes(P->qcB, P->qc, P->G, C, eb, P->stream));
+        } else {
+            ProfScope ps(P, K_EXCHANGE, 2.0 * eb * (double)P->arr_n);
+            const char *src = (const char *)P->qc;
+            char *dst = (char *)P->qcB;
+            QVA_NCCL_TRY(ncclGroupStart());
+            for (int t = 0; t < P->world; ++t) {
+                if (t == P->rank) continue;
+                QVA_NCCL_TRY(ncclSend(src + t * C * eb, C * eb, ncclInt8, t, P->comm, P->stream));
+                QVA_NCCL_TRY(ncclRecv(dst + t * C * eb, C * eb, ncclInt8, t, P->comm, P->stream));
+            }
+            QVA_NCCL_TRY(ncclGroupEnd());
+            QVA_CUDA_TRY(cudaMemcpyAsync(dst + P->rank * C * eb, src + P->rank * C * eb, C * eb,
+                                         cudaMemcpyDeviceToDevice, P->stream));
+        }
+        P->qcB_valid = true;
+    }
     return QVA_OK;
+}
+
+// Classify q after an upload: integer-valued within int8/int16 range -> compact codes + phase
+// tables (exact: the table entry for k is the same fp64 sincos of fl(gamma*k)).
+void drop_qt(qva_plan *P);
+qva_status classify_q(qva_plan *P) {
+    drop_qt(P);
+    P->q_mode = 0;
+    P->qcB_valid = false;
+    if (P->mixer != QVA_MIXER_X || P->L < kTileBits) return QVA_OK;
+    int blocks = q_range_blocks(P->arr_n);
+    double *mm = nullptr;
+    QVA_CUDA_TRY(cudaMallocAsync((void **)&mm, 2 * blocks * sizeof(double), P->stream));
+    QVA_CUDA_TRY(cudaMemsetAsync(P->d_flag, 0, sizeof(int), P->stream));
+    {
+        ProfScope ps(P, K_OTHER, 8.0 * P->arr_n);
+        QVA_CUDA_TRY(launch_q_range(P->q, P->arr_n, P->d_flag, mm, blocks, P->stream));
+    }
+    std::vector<double> h(2 * blocks);
+    int flag = 0;
+    QVA_CUDA_TRY(cudaMemcpyAsync(h.data(), mm, h.size() * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
+    QVA_CUDA_TRY(cudaMemcpyAsync(&flag, P->d_flag, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
+    QVA_CUDA_TRY(cudaFreeAsync(mm, P->stream));
+    QVA_TRY(sync(P));
+    double lo = INFINITY, hi = -INFINITY;
+    for (int b = 0; b < blocks; ++b) {
+        lo = std::min(lo, h[2 * b]);
+        hi = std::max(hi, h[2 * b + 1]);
+    }
+    if (P->world > 1) {
+        double v[3] = {(double)flag, -lo, hi};
+        // max-reduce via NCCL
+        double *d;
+        QVA_CUDA_TRY(cudaMallocAsync((void **)&d, sizeof(v), P->stream));
+        QVA_CUDA_TRY(cudaMemcpyAsync(d, v, sizeof(v), cudaMemcpyHostToDevice, P->stream));
+        QVA_NCCL_TRY(ncclAllReduce(d, d, 3, ncclDouble, ncclMax, P->comm, P->stream));
+        QVA_CUDA_TRY(cudaMemcpyAsync(v, d, sizeof(v), cudaMemcpyDeviceToHost, P->stream));
+        QVA_CUDA_TRY(cudaFreeAsync(d, P->stream));
+        QVA_TRY(sync(P));
+        flag = v[0] != 0.0;
+        lo = -v[1];
+        hi = v[2];
+    }
+    if (flag || !(hi - lo <= 4095.0)) return QVA_OK;
+    int eb = 0;
+    if (lo >= -128 && hi <= 127) eb = 1;
+    else if (lo >= -32768 && hi <= 32767) eb = 2;
+    if (!eb) return QVA_OK;
+    if (P->qc) cudaFree(P->qc);
+    P->qc = nullptr;
+    QVA_CUDA_TRY(cudaMalloc(&P->qc, P->arr_n * eb));
+    if (P->qcB) cudaFree(P->qcB);
+    P->qcB = nullptr;
+    {
+        ProfScope ps(P, K_OTHER, (8.0 + eb) * P->arr_n);
+        QVA_CUDA_TRY(launch_q_encode(P->q, P->arr_n, P->qc, eb, P->stream));
+    }
+    P->q_mode = eb == 1 ? 1 : 2;
+    P->qmin = (int)lo;
+    P->qmax = (int)hi;
+    return sync(P);
 }
 
 qva_status to_layout_A(qva_plan *P) {
     if (P->layout == 0) return QVA_OK;
     return exchange_state(P);
+}
+
+void drop_qt(qva_plan *P) {
+    for (auto &e : P->qt_cache) cudaFree(e.buf);
+    P->qt_cache.clear();
+}
+
+// q (current layout) in the consumer order of group g of tile set `set` (tp: tile bits + runs)
+qva_status ensure_qt(qva_plan *P, int set, int g, int qbytes, const TilePassParams &tp, void **out) {
+    for (auto &e : P->qt_cache)
+        if (e.layout == P->layout && e.set == set && e.group == g && e.qbytes == qbytes) {
+            *out = e.buf;
+            return QVA_OK;
+        }
+    const void *src;
+    if (qbytes == 8) src = (P->layout == 1) ? (const void *)P->qB : (const void *)P->q;
+    else src = (P->layout == 1) ? P->qcB : P->qc;
+    void *buf = nullptr;
+    QVA_CUDA_TRY(cudaMalloc(&buf, P->arr_n * (size_t)qbytes));
+    {
+        ProfScope ps(P, K_OTHER, 2.0 * qbytes * (double)P->arr_n);
+        QVA_CUDA_TRY(launch_qt_gather(buf, src, qbytes, tp, kGroups[g], P->arr_n >> kTileBits, P->qmin, P->stream));
+    }
+    P->qt_cache.push_back({P->layout, set, g, qbytes, buf});
+    *out = buf;
+    return QVA_OK;
 }
 
 // ---- tile-pass execution of a pass list -----------------------------------------------------
@@ -408,32 +630,92 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
                       double2 *psi_base, uint64_t stride, int init_mode, double *expect_out /*[batch][2] host*/) {
     int n_tile_passes = 0;
     for (auto &pp : passes) n_tile_passes += !pp.exchange;
+    if (P->q_set && !P->q_classified) {
+        QVA_TRY(classify_q(P));
+        P->q_classified = true;
+    }
     QVA_TRY(ensure_angles(P, (size_t)n_tile_passes * batch));
     std::vector<PassAngles> ang((size_t)n_tile_passes * batch);
+    std::vector<char> half1(n_tile_passes, 0), half2(n_tile_passes, 0);
     {
         int j = 0;
-        for (auto &pp : passes) {
+        for (const PassPlan &pp : passes) {
             if (pp.exchange) continue;
             for (int b = 0; b < batch; ++b) {
                 const double *th = thetas + (size_t)b * 2 * p;
+                if (pp.a1 >= 0 && fabs(cos(th[2 * pp.a1 + 1])) < 0x1p-10) half1[j] = 1;
+                if (pp.a2 >= 0 && fabs(cos(th[2 * pp.a2 + 1])) < 0x1p-10) half2[j] = 1;
+            }
+            ++j;
+        }
+    }
+    std::vector<double> gam;  // [phase pass][batch]
+    std::vector<int> tab_index(passes.size(), -1);
+    {
+        int j = 0, np = 0;
+        for (size_t pi = 0; pi < passes.size(); ++pi) {
+            const PassPlan &pp = passes[pi];
+            if (pp.exchange) continue;
+            if (pp.phase >= 0 && P->q_mode) tab_index[pi] = np++;
+            int n1 = __builtin_popcount(pp.r1), n2 = __builtin_popcount(pp.r2);
+            for (int b = 0; b < batch; ++b) {
+                const double *th = thetas + (size_t)b * 2 * p;
                 PassAngles &a = ang[(size_t)j * batch + b];
-                a.c1 = a.s1 = a.c2 = a.s2 = a.gamma = 0.0;
-                if (pp.a1 >= 0) { a.c1 = cos(th[2 * pp.a1 + 1]); a.s1 = sin(th[2 * pp.a1 + 1]); }
-                if (pp.a2 >= 0) { a.c2 = cos(th[2 * pp.a2 + 1]); a.s2 = sin(th[2 * pp.a2 + 1]); }
-                if (pp.phase >= 0) a.gamma = th[2 * pp.phase];
+                memset(&a, 0, sizeof(a));
+                double sr = 1.0, si = 0.0;  // accumulated dropped factor
+                // factored rotation: t = tan(beta), dropped factor cos(beta) per rotated qubit;
+                // |cos beta| < 2^-10: two steps of beta/2 (for every member of the slot)
+                auto factor = [&](int layer, int count, bool half, double &t) {
+                    double beta = th[2 * layer + 1];
+                    if (half) beta *= 0.5;
+                    const double c = cos(beta);
+                    t = sin(beta) / c;
+                    for (int k = 0; k < (half ? 2 : 1) * count; ++k) sr *= c;
+                };
+                if (pp.a1 >= 0) factor(pp.a1, n1, half1[j], a.t1);
+                if (pp.a2 >= 0) factor(pp.a2, n2, half2[j], a.t2);
+                a.scale = make_double2(sr, si);
+                if (pp.phase >= 0) {
+                    a.gamma = th[2 * pp.phase];
+                    if (P->q_mode) gam.push_back(a.gamma);
+                }
             }
             ++j;
         }
     }
     QVA_CUDA_TRY(cudaMemcpyAsync(P->d_angles, ang.data(), ang.size() * sizeof(PassAngles), cudaMemcpyHostToDevice,
                                  P->stream));
+    const int ntab = P->q_mode ? (P->qmax - P->qmin + 1) : 0;
+    if (!gam.empty()) {
+        if (P->gam_cap < gam.size()) {
+            cudaFree(P->d_gam);
+            P->d_gam = nullptr;
+            QVA_CUDA_TRY(cudaMalloc(&P->d_gam, gam.size() * sizeof(double)));
+            P->gam_cap = gam.size();
+        }
+        if (P->tab_cap < gam.size() * ntab) {
+            cudaFree(P->d_tab);
+            P->d_tab = nullptr;
+            QVA_CUDA_TRY(cudaMalloc(&P->d_tab, gam.size() * ntab * sizeof(double2)));
+            P->tab_cap = gam.size() * ntab;
+        }
+        QVA_CUDA_TRY(cudaMemcpyAsync(P->d_gam, gam.data(), gam.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                     P->stream));
+        ProfScope ps(P, K_OTHER, 16.0 * gam.size() * ntab);
+        QVA_CUDA_TRY(launch_phase_table(P->d_tab, P->d_gam, (int)gam.size(), P->qmin, ntab, P->stream));
+    }
     uint64_t n_tiles = P->arr_n >> kTileBits;
     bool any_expect = false;
     for (auto &pp : passes) any_expect |= pp.expect;
-    if (any_expect) QVA_TRY(ensure_partials(P, n_tiles * batch));
+    const int grid = tile_pass_grid(n_tiles * (uint64_t)batch);
+    const int nslot = grid * tile_consumer_warps();
+    if (any_expect) QVA_TRY(ensure_partials(P, (uint64_t)nslot * batch));
+    const int n_phys = ilog2(P->arr_n);
+    const int qbytes = P->q_mode == 1 ? 1 : (P->q_mode == 2 ? 2 : 8);
     int j = 0;
     bool first = true;
-    for (auto &pp : passes) {
+    for (size_t pi = 0; pi < passes.size(); ++pi) {
+        const PassPlan &pp = passes[pi];
         if (pp.exchange) {
             if (batch != 1 || psi_base != P->psi) {
                 set_error("internal: exchange in batched pass list");
@@ -446,34 +728,95 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         TilePassParams tp;
         memset(&tp, 0, sizeof(tp));
         const std::vector<int> &s = P->sets[pp.set];
-        for (int k = 0; k < kTileBits; ++k) tp.tile_bits[k] = s[k];
-        tp.n_phys_bits = ilog2(P->arr_n);
+        uint64_t tmask = 0;
+        for (int k = 0; k < kTileBits; ++k) {
+            tp.tile_bits[k] = s[k];
+            tmask |= 1ull << s[k];
+        }
+        // runs of non-tile physical bits: tile number bits -> physical positions
+        {
+            int src = 0, b = 0;
+            tp.n_runs = 0;
+            while (b < n_phys) {
+                if ((tmask >> b) & 1) { ++b; continue; }
+                int st = b;
+                while (b < n_phys && !((tmask >> b) & 1)) ++b;
+                if (tp.n_runs == kMaxRuns) {
+                    set_error("internal: tile set leaves more than 4 runs of non-tile bits");
+                    return QVA_ERR_UNSUPPORTED;
+                }
+                tp.run_src[tp.n_runs] = src;
+                tp.run_dst[tp.n_runs] = st;
+                tp.run_w[tp.n_runs] = b - st;
+                tp.run_mask[tp.n_runs] = (1ull << (b - st)) - 1;
+                src += b - st;
+                ++tp.n_runs;
+            }
+        }
         tp.n_tiles = n_tiles;
+        tp.log2_tiles = ilog2(n_tiles);
+        tp.batch = batch;
         tp.member_stride = stride;
-        tp.psi_in = psi_base;
         tp.psi_out = psi_base;
-        if (first && init_mode == 2) tp.psi_in = P->psi0;
-        tp.init = first ? init_mode : 0;
+        const double2 *psi_in = (first && init_mode == 2) ? P->psi0 : psi_base;
+        tp.init = (first && init_mode == 1) ? 1 : 0;
         tp.amp0 = 1.0 / sqrt((double)P->N);
-        if (pp.phase >= 0 || pp.expect) {
+        const bool needs_q = pp.phase >= 0 || pp.expect;
+        int pref = -1;
+        if (needs_q)
+            for (auto &e : P->qt_cache)
+                if (e.layout == P->layout && e.set == pp.set && e.qbytes == qbytes) pref = e.group;
+        build_steps(pp, tp, pref, half1[j], half2[j]);
+        if (needs_q) {
             if (P->layout == 1) QVA_TRY(ensure_qB(P));
-            tp.q = (P->layout == 1) ? P->qB : P->q;
+            void *qt = nullptr;
+            QVA_TRY(ensure_qt(P, pp.set, tp.gq, qbytes, tp, &qt));
+            tp.qt = qt;
+            tp.qmin = P->qmin;
+            tp.ntab = ntab;
+            if (tab_index[pi] >= 0) tp.tab = P->d_tab + (size_t)tab_index[pi] * batch * ntab;
+        } else {
+            tp.gq = -1;
         }
         tp.angles = P->d_angles + (size_t)j * batch;
         tp.expect = pp.expect ? 1 : 0;
         tp.partials = P->partials;
-        build_steps(pp, tp);
+        tp.apply_scale = (pp.r1 | pp.r2) ? 1 : 0;
+        // last step touching shared memory: a group switch (smem transpose) or the phase (q stage)
+        tp.release_step = (tp.init == 1 && tp.gq < 0) ? -1 : 0;
+        for (int k = 0; k < tp.n_steps; ++k)
+            if ((k > 0 && tp.steps[k].group != tp.steps[k - 1].group) || tp.steps[k].phase) tp.release_step = k;
+        if (tp.expect) tp.release_step = tp.n_steps;
+        const int prog = match_prog(tp);
+        // tiles go back through a TMA tensor store (measured faster than st.global from registers for
+        // every tile shape; env QVA_TSTORE=0 selects the register stores for comparison)
+        tp.tma_store = (g_tstore >= 0) ? g_tstore : 1;
+        CUtensorMap map, map_out;
+        QVA_TRY(make_tile_tensor_map(psi_in, n_phys, batch, tp, &map));
+        QVA_TRY(make_tile_tensor_map(tp.psi_out, n_phys, batch, tp, &map_out));
+        if (g_trace > 1) {
+            fprintf(stderr, "[qva] pass set %d prog %d init %d gq %d expect %d release %d steps:", pp.set, prog, tp.init,
+                    tp.gq, tp.expect, tp.release_step);
+            for (int k = 0; k < tp.n_steps; ++k)
+                fprintf(stderr, " (g%d m%02x a%d p%d)", tp.steps[k].group, tp.steps[k].mask, tp.steps[k].angle,
+                        tp.steps[k].phase);
+            fprintf(stderr, " dims:");
+            for (int d = 0; d < 5; ++d) fprintf(stderr, " [%d,%d]", tp.dim_src[d], tp.dim_w[d]);
+            fprintf(stderr, "\n");
+        }
         double bytes = (double)P->arr_n * batch *
-                       ((tp.init == 1 ? 16.0 : 32.0) + (pp.phase >= 0 ? 8.0 : 0.0) + (pp.expect ? 8.0 : 0.0));
+                       ((tp.init == 1 ? 16.0 : 32.0) + (pp.phase >= 0 ? qbytes : 0.0) + (pp.expect ? qbytes : 0.0));
+        if (pp.expect)
+            QVA_CUDA_TRY(cudaMemsetAsync(P->partials, 0, (size_t)nslot * batch * 2 * sizeof(double), P->stream));
         {
             ProfScope ps(P, K_TILE, bytes);
-            QVA_CUDA_TRY(launch_tile_pass(tp, batch, P->stream));
+            QVA_CUDA_TRY(launch_tile_pass(map, map_out, tp, needs_q ? qbytes : 0, prog, grid, P->stream));
         }
         first = false;
         ++j;
         if (pp.expect) {
-            ProfScope ps(P, K_REDUCE, 16.0 * n_tiles * batch);
-            QVA_CUDA_TRY(launch_reduce_partials(P->partials, n_tiles, batch, P->red, P->stream));
+            ProfScope ps(P, K_REDUCE, 16.0 * nslot * batch);
+            QVA_CUDA_TRY(launch_reduce_partials(P->partials, nslot, batch, P->red, P->stream));
         }
     }
     if (expect_out) {
@@ -669,6 +1012,11 @@ qva_status qva_plan_destroy(qva_plan *P) {
     cudaFree(P->psi0);
     cudaFree(P->q);
     cudaFree(P->qB);
+    cudaFree(P->qc);
+    cudaFree(P->qcB);
+    cudaFree(P->d_tab);
+    cudaFree(P->d_gam);
+    for (auto &e : P->qt_cache) cudaFree(e.buf);
     cudaFree(P->partials);
     cudaFree(P->red);
     cudaFree(P->d_angles);
@@ -839,6 +1187,9 @@ static qva_status set_q_common(qva_plan *P, const double *src, bool device, uint
     }
     P->q_set = true;
     P->qB_valid = false;
+    P->q_classified = false;
+    P->q_mode = 0;
+    drop_qt(P);
     return QVA_OK;
 }
 
@@ -892,6 +1243,9 @@ qva_status qva_set_qualities_maxcut(qva_plan *P, int32_t m, const int32_t *u, co
     QVA_TRY(sync(P));
     P->q_set = true;
     P->qB_valid = false;
+    P->q_classified = false;
+    P->q_mode = 0;
+    drop_qt(P);
     return QVA_OK;
 }
 
@@ -1268,7 +1622,7 @@ static qva_status batch_local(qva_plan *P, const double *thetas, int first, int 
     if (count <= 0) return QVA_OK;
     const double *th = thetas + (size_t)first * 2 * p;
     if (P->mixer == QVA_MIXER_X && P->G == 1 && (use_small(P) || P->batch_psi)) {
-        int chunk = use_small(P) ? count : std::min(count, P->max_batch);
+        int chunk = use_small(P) ? count : std::min(std::min(count, P->max_batch), kMaxBatchSmem);
         for (int b0 = 0; b0 < count; b0 += chunk) {
             int nb = std::min(chunk, count - b0);
             std::vector<double> pairs(2 * (size_t)nb);

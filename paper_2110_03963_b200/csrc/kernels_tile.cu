@@ -1,0 +1,722 @@
+// kernels_tile.cu -- the X-mixer tile pass: one HBM round trip over the state that applies, to
+// every tile of 2^12 amplitudes, any subset of the single-qubit rotations exp(-i beta X_j)
+// whose qubits are tile bits (Eq. mixing_qaoa, reading R1), optionally the
+// phase exp(-i gamma q_x) between two rotation sets (Eq. phase_shift_qaoa, PAPER.md:152-155;
+// diagonal action, Sec. 3) and optionally the partial sums of
+// <psi|Q|psi> = sum |psi_x|^2 q_x and of the norm (Eq. 2).
+//
+// sm_100a design:
+//  * persistent grid, one CTA per SM, 5 warps: warp 4 lane 0 is the TMA producer, warps 0-3
+//    (128 threads) are consumers holding 32 amplitudes each in registers;
+//  * a STAGES-deep ring of 64 KiB shared-memory tiles filled by cp.async.bulk.tensor (one 5-D
+//    box per tile: the tile bits are box dimensions, the other index bits are coordinates, so
+//    strided high-qubit tiles cost one instruction) with SWIZZLE_128B, completion on mbarriers;
+//  * the qualities (fp64 or compact integer codes) arrive in the same stage by a 1-D bulk copy
+//    from a copy of q pre-permuted into consumer order (conflict-free 16-byte smem reads);
+//  * rotations run on register groups of 5 tile bits; a group change is one in-place swizzled
+//    smem transpose (conflict-free LDS.128/STS.128); results are stored straight from
+//    registers with st.global.cs (full 128-B segments on the X/Y groups).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <type_traits>
+#include <utility>
+
+#include "qva_internal.h"
+
+namespace qva {
+
+namespace {
+
+constexpr int kTile = 1 << kTileBits;      // 4096 amplitudes
+constexpr int kWG = 2;                      // consumer warpgroups (alternate tiles)
+constexpr int kCT = 128;                    // consumer threads per warpgroup
+constexpr int kCW = kWG * kCT / 32;         // consumer warps per CTA
+constexpr int kAPT = kTile / kCT;           // 32 amplitudes per consumer thread
+constexpr int kThreads = kWG * kCT;         // no producer warp: each warpgroup refills what it frees
+constexpr int kTabRep = 8;                  // smem phase-table replicas (one per 16-B bank group)
+constexpr int kTabSmemMax = 64;             // entries held in smem (int8 codes, batch == 1)
+
+static_assert(kAPT == 1 << kGroupBits, "group width");
+static_assert(kCT == 1 << kCT_BITS, "warpgroup width");
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap *map, uint32_t bar, const int (&c)[5]) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap *map, uint32_t src, const int (&c)[5]) {
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(src)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void wg_sync(int wg) { asm volatile("bar.sync %0, %1;" ::"r"(1 + wg), "n"(kCT) : "memory"); }
+
+// Rotation exp(-i beta X) on the pair (a, b) (a: bit clear, b: bit set) in factored form:
+// a' = a - i t b, b' = b - i t a with t = tan beta (4 DFMA); the dropped scalar cos beta is applied
+// once per pass (PassAngles::scale).  Intermediates of k factored rotations are bounded by
+// (|cos|+|sin|)^k <= 2^(k/2) times the final magnitude, so the factoring costs at most ~k/2
+// bits of relative accuracy.  t = 0 is an exact identity, which is how a register bit that is
+// not rotated in a step is skipped without a branch.  |cos beta| < 2^-10 is handled on the
+// host by applying two half-angle steps.
+__device__ __forceinline__ void fbutterfly(double2 &a, double2 &b, double t) {
+    const double ar = a.x, ai = a.y, br = b.x, bi = b.y;
+    a = make_double2(fma(t, bi, ar), fma(-t, br, ai));
+    b = make_double2(fma(t, ai, br), fma(-t, ar, bi));
+}
+
+template <int J>
+__device__ __forceinline__ void rot_bit(double2 (&v)[kAPT], double t) {
+#pragma unroll
+    for (int e = 0; e < kAPT; ++e)
+        if (!(e & (1 << J))) fbutterfly(v[e], v[e | (1 << J)], t);
+}
+
+// register bits a group can rotate: X all 5, Y its first 4 (its 5th bit, tile bit 3, belongs to
+// X), W its first 3 (tile bits 0..2)
+template <int G>
+__device__ __forceinline__ void rotate_group(double2 (&v)[kAPT], int mask, double t) {
+    rot_bit<0>(v, (mask & 1) ? t : 0.0);
+    rot_bit<1>(v, (mask & 2) ? t : 0.0);
+    rot_bit<2>(v, (mask & 4) ? t : 0.0);
+    if (G != 2) rot_bit<3>(v, (mask & 8) ? t : 0.0);
+    if (G == 0) rot_bit<4>(v, (mask & 16) ? t : 0.0);
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+// Shared-memory address of register element e of consumer thread c in register group G (the
+// compile-time twin of api.cu kGroups) under SWIZZLE_128B (16-byte slot = i ^ ((i >> 3) & 7)):
+//   X: ebit {3,4,5,6,7}   tbit {0,1,2,8,9,10,11}  slot = (l ^ e[0:3]) | e << 3 | h << 8
+//   Y: ebit {8,9,10,11,3} tbit {0,1,2,4,5,6,7}    slot = (l ^ (e4 | h[0:2] << 1)) | e4 << 3 | h << 4 | e[0:4] << 8
+//   W: ebit {0,1,2,6,7}   tbit {3,4,5,8,9,10,11}  slot = (e[0:3] ^ l) | l << 3 | e[3:5] << 6 | h << 8
+// (l = c & 7, h = c >> 3).  In bytes every address is (A ^ x(e)) + k(e) with a per-thread base A,
+// x(e) < 128 and k(e) a multiple of 128, so each access is one LOP3 + LDS/STS with an immediate.
+// A is laundered through a register move per item so ptxas cannot hoist the 8 XOR variants of
+// every stage out of the loop (they would not fit the register budget).
+template <int G>
+__device__ __forceinline__ uint32_t group_base(uint32_t buf, int c) {
+    const uint32_t l = c & 7, h = c >> 3;
+    uint32_t a;
+    if (G == 0) a = buf + (l << 4) + (h << 12);
+    else if (G == 1) a = buf + ((l ^ ((h & 3) << 1)) << 4) + (h << 8);
+    else a = buf + (l << 4) + (l << 7) + (h << 12);
+    asm volatile("mov.b32 %0, %0;" : "+r"(a));
+    return a;
+}
+template <int G>
+__device__ __forceinline__ uint32_t group_addr(uint32_t A, int e) {
+    if (G == 0) return (A ^ ((e & 7) << 4)) + (e << 7);
+    if (G == 1) return (A ^ ((e >> 4) << 4)) + ((e >> 4) << 7) + ((e & 15) << 12);
+    return (A ^ ((e & 7) << 4)) + ((e >> 3) << 10);
+}
+__device__ __forceinline__ double2 lds128(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, double2 v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+
+template <int G>
+__device__ __forceinline__ void smem_read_g(double2 (&v)[kAPT], uint32_t buf, int c) {
+    const uint32_t A = group_base<G>(buf, c);
+#pragma unroll
+    for (int e = 0; e < kAPT; ++e) v[e] = lds128(group_addr<G>(A, e));
+}
+template <int G>
+__device__ __forceinline__ void smem_write_g(const double2 (&v)[kAPT], uint32_t buf, int c) {
+    const uint32_t A = group_base<G>(buf, c);
+#pragma unroll
+    for (int e = 0; e < kAPT; ++e) sts128(group_addr<G>(A, e), v[e]);
+}
+// The q stage holds the tile's q in consumer order (qt_gather_kernel): fp64 values, or integer
+// codes stored as j = code - qmin (uint8 / uint16).  Chunk c of 16 bytes of thread t sits at
+// 16-byte index c * kCT + t (conflict-free LDS.128).
+template <int QB>
+__device__ __forceinline__ void apply_phase_group(double2 (&v)[kAPT], const unsigned char *qs, int c, int lane,
+                                                  double gamma, const double2 *tab_s, const double2 *tab_g) {
+    if (QB == 8) {
+        const double2 *q2 = reinterpret_cast<const double2 *>(qs);
+#pragma unroll
+        for (int k = 0; k < kAPT / 2; ++k) {
+            const double2 qq = q2[k * kCT + c];
+            double sn, cs;
+            sincos(gamma * qq.x, &sn, &cs);
+            v[2 * k] = cmul(v[2 * k], make_double2(cs, -sn));
+            sincos(gamma * qq.y, &sn, &cs);
+            v[2 * k + 1] = cmul(v[2 * k + 1], make_double2(cs, -sn));
+        }
+    } else {
+        constexpr int PER = 16 / (QB > 0 ? QB : 1);  // codes per 16-byte chunk
+        const uint4 *q4 = reinterpret_cast<const uint4 *>(qs);
+        const double2 *tab_l = tab_s + (lane & (kTabRep - 1));
+#pragma unroll
+        for (int k = 0; k < kAPT / PER; ++k) {
+            const uint4 w = q4[k * kCT + c];
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int m = 0; m < PER; ++m) {
+                int j;
+                if (QB == 1) j = (int)((ww[m >> 2] >> (8 * (m & 3))) & 0xff);
+                else j = (int)((ww[m >> 1] >> (16 * (m & 1))) & 0xffff);
+                const double2 f = tab_s ? tab_l[j * kTabRep] : __ldg(tab_g + j);
+                v[k * PER + m] = cmul(v[k * PER + m], f);
+            }
+        }
+    }
+}
+
+template <int QB>
+__device__ __forceinline__ void accumulate_expect(const double2 (&v)[kAPT], const unsigned char *qs, int c, int qmin,
+                                                  double &acc, double &nrm) {
+    if (QB == 8) {
+        const double2 *q2 = reinterpret_cast<const double2 *>(qs);
+#pragma unroll
+        for (int k = 0; k < kAPT / 2; ++k) {
+            const double2 qq = q2[k * kCT + c];
+            const double p0 = v[2 * k].x * v[2 * k].x + v[2 * k].y * v[2 * k].y;
+            const double p1 = v[2 * k + 1].x * v[2 * k + 1].x + v[2 * k + 1].y * v[2 * k + 1].y;
+            acc = fma(p0, qq.x, acc);
+            acc = fma(p1, qq.y, acc);
+            nrm += p0 + p1;
+        }
+    } else {
+        constexpr int PER = 16 / (QB > 0 ? QB : 1);
+        const uint4 *q4 = reinterpret_cast<const uint4 *>(qs);
+#pragma unroll
+        for (int k = 0; k < kAPT / PER; ++k) {
+            const uint4 w = q4[k * kCT + c];
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int m = 0; m < PER; ++m) {
+                int j;
+                if (QB == 1) j = (int)((ww[m >> 2] >> (8 * (m & 3))) & 0xff);
+                else j = (int)((ww[m >> 1] >> (16 * (m & 1))) & 0xffff);
+                const double2 a = v[k * PER + m];
+                const double pr = a.x * a.x + a.y * a.y;
+                acc = fma(pr, (double)(j + qmin), acc);
+                nrm += pr;
+            }
+        }
+    }
+}
+
+template <int STAGES, int QB>
+constexpr size_t tile_smem_bytes() {
+    return (size_t)STAGES * (kTile * sizeof(double2) + (size_t)kTile * QB) +
+           (QB == 1 ? (size_t)kTabSmemMax * kTabRep * sizeof(double2) : 0) + 2 * STAGES * sizeof(uint64_t) +
+           (size_t)kMaxBatchSmem * sizeof(PassAngles);
+}
+
+__device__ __forceinline__ void tma_coords(const TilePassParams &P, uint64_t member, uint64_t t, int (&c)[5]) {
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        const int w = P.dim_w[d];
+        int x = (int)((t >> P.dim_src[d]) & ((1ull << w) - 1));
+        if (d == P.member_dim) x += (int)(member << w);
+        c[d] = x;
+    }
+}
+
+__device__ __forceinline__ void flush_partial(const TilePassParams &P, int64_t member, int warp, int lane, double &acc,
+                                              double &nrm) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    }
+    if (lane == 0) {
+        double2 *slot =
+            reinterpret_cast<double2 *>(P.partials) + ((uint64_t)member * gridDim.x + blockIdx.x) * kCW + warp;
+        const double2 old = *slot;
+        *slot = make_double2(old.x + acc, old.y + nrm);
+    }
+    acc = nrm = 0.0;
+}
+
+// Pass programs: the group sequence, phase position and expectation of the common pass shapes
+// fixed at compile time (straight-line code, no register reshuffling at control-flow joins);
+// masks and angle slots stay runtime (PassStep).  Program 0 interprets P.steps at run time.
+// kTileProgs in qva_internal.h lists the same shapes for the host-side matcher.
+template <int PROG>
+__device__ __forceinline__ constexpr TileProg prog_def() {
+    return kTileProgs[PROG];
+}
+template <int PROG>
+__device__ __forceinline__ constexpr int prog_release() {
+    constexpr TileProg D = prog_def<PROG>();
+    if (D.expect) return D.n;
+    int r = 0;
+    for (int k = 1; k < D.n; ++k)
+        if (D.g[k] != D.g[k - 1]) r = k;
+    if (D.phase_k > r) r = D.phase_k;
+    return r;
+}
+
+template <typename F, int... K>
+__device__ __forceinline__ void static_for_impl(F &f, std::integer_sequence<int, K...>) {
+    (f(std::integral_constant<int, K>()), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F &&f) {
+    static_for_impl(f, std::make_integer_sequence<int, N>());
+}
+
+template <int STAGES, int QB, int PROG>
+__global__ void __launch_bounds__(kThreads, 1)
+tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_out,
+                 const __grid_constant__ TilePassParams P) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];  // SWIZZLE_128B needs 1024-B alignment
+    unsigned char *sm = smem_raw;
+    double2 *psi_s = reinterpret_cast<double2 *>(sm);
+    unsigned char *q_s = sm + (size_t)STAGES * kTile * sizeof(double2);
+    double2 *tab_s = reinterpret_cast<double2 *>(q_s + (size_t)STAGES * kTile * QB);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(tab_s) +
+                                                  (QB == 1 ? kTabSmemMax * kTabRep * sizeof(double2) : 0));
+    PassAngles *ang_s = reinterpret_cast<PassAngles *>(bars + 2 * STAGES);  // [batch]
+    // full[round & 1][stage]: item `it` is round it / STAGES of stage it % STAGES.  Rounds r and
+    // r - 2 of a stage belong to the same warpgroup, so each barrier is waited by one warpgroup
+    // at most one phase ahead (no parity aliasing).
+    const uint32_t full0 = smem_u32(bars);
+    auto full_bar = [&](uint32_t it) { return full0 + 8 * (((it / STAGES) & 1) * STAGES + it % STAGES); };
+
+    constexpr TileProg D = prog_def<PROG>();
+    constexpr bool kPhase = PROG == 0 ? QB > 0 : D.phase_k >= 0;
+    constexpr bool kExpect = PROG == 0 ? QB > 0 : D.expect;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const uint64_t n_items = P.n_tiles * (uint64_t)P.batch;
+    const uint32_t n_it = (uint32_t)((n_items > blockIdx.x) ? (n_items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
+    const bool load_psi = (P.init != 1);
+    const bool tstore = P.tma_store != 0;  // output through a TMA store of the final smem tile
+    const bool load_q = (QB > 0) && (P.gq >= 0);
+    const bool use_tab_s = (QB == 1) && kPhase && P.batch == 1 && P.ntab <= kTabSmemMax && P.tab != nullptr;
+    const uint32_t qbytes = load_q ? (uint32_t)(kTile * QB) : 0u;
+    const uint32_t bytes = (load_psi ? kTile * (uint32_t)sizeof(double2) : 0u) + qbytes;
+    const unsigned char *qt = reinterpret_cast<const unsigned char *>(P.qt);
+
+    // TMA traffic for CTA iteration j (item blockIdx.x + j * gridDim.x)
+    auto issue = [&](uint32_t j) {
+        const uint64_t item = blockIdx.x + (uint64_t)j * gridDim.x;
+        const uint64_t member = item >> P.log2_tiles, t = item & (P.n_tiles - 1);
+        const int s = j % STAGES;
+        const uint32_t bar = full_bar(j);
+        mbar_expect_tx(bar, bytes);
+        if (load_psi) {
+            int cc[5];
+            tma_coords(P, member, t, cc);
+            tma_load_5d(smem_u32(psi_s + (size_t)s * kTile), &tmap, bar, cc);
+        }
+        if (qbytes) bulk_load(smem_u32(q_s + (size_t)s * kTile * QB), qt + t * (uint64_t)qbytes, qbytes, bar);
+    };
+
+    if (tid == 0) {
+        if (smem_u32(smem_raw) & 1023) __trap();
+        for (int k = 0; k < 2 * STAGES; ++k) mbar_init(full0 + 8 * k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (use_tab_s)
+        for (int k = tid; k < P.ntab * kTabRep; k += kThreads) tab_s[k] = P.tab[k / kTabRep];
+    for (int k = tid; k < P.batch; k += kThreads) ang_s[k] = P.angles[k];
+    __syncthreads();
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+        for (uint32_t j = 0; j < (uint32_t)STAGES && j < n_it; ++j) issue(j);
+    }
+
+    // ---------------- warpgroup wg takes CTA iterations wg, wg + 2, ... ----------------
+    const int wg = tid / kCT;
+    const int c = tid % kCT;
+    // store addressing of the final group (host-computed): phys = member*stride + base(t)
+    //   + sum_j c_j << st_tphys[j] + sum_j e_j st_estr[j]
+    uint64_t tbase = 0;
+#pragma unroll
+    for (int j = 0; j < kCT_BITS; ++j) tbase |= (uint64_t)((c >> j) & 1) << P.st_tphys[j];
+
+    double acc = 0.0, nrm = 0.0;
+    int64_t acc_member = -1;
+
+    for (uint32_t it = wg; it < n_it; it += kWG) {
+        const uint64_t item = blockIdx.x + (uint64_t)it * gridDim.x;
+        const int s = it % STAGES;
+        const uint64_t member = item >> P.log2_tiles;
+        const uint64_t t = item & (P.n_tiles - 1);
+        const PassAngles *ang = ang_s + member;
+        const double2 *tab_g = P.tab ? P.tab + member * P.ntab : nullptr;
+        if (QB > 0 && kExpect && P.expect && (int64_t)member != acc_member) {
+            if (acc_member >= 0) flush_partial(P, acc_member, warp, lane, acc, nrm);
+            acc_member = (int64_t)member;
+        }
+
+        const uint32_t buf = smem_u32(psi_s + (size_t)s * kTile);
+        const unsigned char *qs = q_s + (size_t)s * kTile * QB;
+        mbar_wait(full_bar(it), ((it / STAGES) >> 1) & 1);
+
+        // hand stage s back: the whole warpgroup is done with it, so one thread refills it with
+        // iteration it + STAGES (the async-proxy write must follow our generic-proxy accesses)
+        auto release = [&]() {
+            fence_proxy_async();
+            wg_sync(wg);
+            if (c == 0 && it + STAGES < n_it) issue(it + STAGES);
+        };
+        double2 v[kAPT];
+        if (!load_psi) {
+#pragma unroll
+            for (int e = 0; e < kAPT; ++e) v[e] = make_double2(P.amp0, 0.0);
+        }
+        if constexpr (PROG == 0) {
+            if (P.release_step < 0 && !tstore) release();
+            // every step is straight-line code for a compile-time group: read the tile in that
+            // group's layout if the previous step used another one, rotate, apply the phase, and
+            // write the tile back if the next step switches
+            int prev = load_psi ? -1 : P.steps[0].group;
+            for (int k = 0; k < P.n_steps; ++k) {
+                const PassStep st = P.steps[k];
+                const int next = (k + 1 < P.n_steps) ? P.steps[k + 1].group : st.group;
+                const double tt = st.mask ? (st.angle ? ang->t2 : ang->t1) : 0.0;
+                auto body = [&](auto gc) {
+                    constexpr int G = decltype(gc)::value;
+                    if (prev != G) {
+                        if (prev >= 0) wg_sync(wg);
+                        smem_read_g<G>(v, buf, c);
+                    }
+                    if (st.mask) rotate_group<G>(v, st.mask, tt);
+                    if (QB > 0 && st.phase)
+                        apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
+                    if (next != G) smem_write_g<G>(v, buf, c);
+                };
+                if (st.group == 0) body(std::integral_constant<int, 0>());
+                else if (st.group == 1) body(std::integral_constant<int, 1>());
+                else body(std::integral_constant<int, 2>());
+                prev = st.group;
+                if (k == P.release_step && !tstore) release();
+            }
+        } else {
+            constexpr int REL = prog_release<PROG>();
+            static_for<D.n>([&](auto kc) {
+                constexpr int K = decltype(kc)::value;
+                constexpr int G = prog_def<PROG>().g[K];
+                if constexpr (K == 0) {
+                    if (load_psi) smem_read_g<G>(v, buf, c);
+                } else if constexpr (prog_def<PROG>().g[K - 1] != G) {
+                    wg_sync(wg);
+                    smem_read_g<G>(v, buf, c);
+                }
+                if constexpr (prog_def<PROG>().rot[K]) {
+                    const PassStep st = P.steps[K];
+                    rotate_group<G>(v, st.mask, st.angle ? ang->t2 : ang->t1);
+                }
+                if constexpr (QB > 0 && K == prog_def<PROG>().phase_k)
+                    apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
+                if constexpr (K == REL) {
+                    if (!tstore) release();
+                }
+                if constexpr (K + 1 < prog_def<PROG>().n && prog_def<PROG>().g[K + 1] != G) smem_write_g<G>(v, buf, c);
+            });
+        }
+        if (P.apply_scale) {
+            const double2 sc = ang->scale;
+#pragma unroll
+            for (int e = 0; e < kAPT; ++e) v[e] = cmul(v[e], sc);
+        }
+        if constexpr (QB > 0 && kExpect) {
+            if (P.expect) accumulate_expect<QB>(v, qs, c, P.qmin, acc, nrm);
+        }
+        if (tstore) {
+            // the tile goes back through shared memory in the load layout and out with one TMA
+            // store; the stage is refilled once the store engine has read it
+            if constexpr (PROG == 0) {
+                const int gf = P.steps[P.n_steps - 1].group;
+                if (gf == 0) smem_write_g<0>(v, buf, c);
+                else if (gf == 1) smem_write_g<1>(v, buf, c);
+                else smem_write_g<2>(v, buf, c);
+            } else {
+                smem_write_g<prog_def<PROG>().g[prog_def<PROG>().n - 1]>(v, buf, c);
+            }
+            fence_proxy_async();
+            wg_sync(wg);
+            if (c == 0) {
+                int cc[5];
+                tma_coords(P, member, t, cc);
+                tma_store_5d(&tmap_out, buf, cc);
+                bulk_wait_read_all();
+                if (it + STAGES < n_it) issue(it + STAGES);
+            }
+            continue;
+        }
+        if constexpr (PROG == 0) {
+            if (P.release_step >= P.n_steps) release();
+        } else if constexpr (prog_release<PROG>() >= prog_def<PROG>().n) {
+            release();
+        }
+
+        uint64_t base = member * P.member_stride;
+#pragma unroll
+        for (int r = 0; r < kMaxRuns; ++r) base |= ((t >> P.run_src[r]) & P.run_mask[r]) << P.run_dst[r];
+        double2 *dst = P.psi_out + base + tbase;
+#pragma unroll
+        for (int e = 0; e < kAPT; ++e) {
+            uint64_t o = 0;
+#pragma unroll
+            for (int j = 0; j < kGroupBits; ++j)
+                if (e & (1 << j)) o += P.st_estr[j];
+            __stcs(dst + o, v[e]);
+        }
+    }
+    if (tstore && c == 0) bulk_wait_all();
+    if (QB > 0 && kExpect && P.expect && acc_member >= 0) flush_partial(P, acc_member, warp, lane, acc, nrm);
+}
+
+// q (fp64 or integer codes) permuted into the consumer order of register group G of tile set S:
+// dst[t][pos(tid, e)] = src[phys(t, i(tid, e))], pos as read by apply_phase_group/accumulate_expect.
+template <typename T>
+__global__ void qt_gather_kernel(T *dst, const T *src, const __grid_constant__ TilePassParams P, TileGroup G,
+                                 uint64_t n_tiles, int qmin) {
+    const uint64_t total = n_tiles * (uint64_t)kTile;
+    constexpr int PER = (sizeof(T) == 8) ? 2 : 16 / (int)sizeof(T);
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = k >> kTileBits;
+        const int pos = (int)(k & (kTile - 1));
+        // invert pos = ((e / PER) * kCT + tid) * PER + e % PER
+        const int within = pos % PER, chunk = pos / PER;
+        const int tid = chunk % kCT, e = (chunk / kCT) * PER + within;
+        int i = 0;
+        for (int j = 0; j < kCT_BITS; ++j) i |= ((tid >> j) & 1) << G.tbit[j];
+        for (int j = 0; j < kGroupBits; ++j) i |= ((e >> j) & 1) << G.ebit[j];
+        uint64_t phys = 0;
+        for (int r = 0; r < P.n_runs; ++r) phys |= ((t >> P.run_src[r]) & ((1ull << P.run_w[r]) - 1)) << P.run_dst[r];
+        for (int b = 0; b < kTileBits; ++b) phys |= (uint64_t)((i >> b) & 1) << P.tile_bits[b];
+        if (sizeof(T) == 8) dst[k] = src[phys];
+        else dst[k] = (T)((int)src[phys] - qmin);  // integer codes stored as j = code - qmin
+    }
+}
+
+template <int STAGES, int QB, int PROG>
+cudaError_t launch_one(const CUtensorMap &map, const CUtensorMap &map_out, const TilePassParams &p, int grid,
+                       cudaStream_t s) {
+    static bool configured = false;
+    constexpr size_t smem = tile_smem_bytes<STAGES, QB>();
+    static_assert(smem <= 232448, "shared memory budget");
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(tile_pass_kernel<STAGES, QB, PROG>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    tile_pass_kernel<STAGES, QB, PROG><<<grid, kThreads, smem, s>>>(map, map_out, p);
+    return cudaGetLastError();
+}
+
+template <int STAGES, int QB>
+cudaError_t launch_prog(const CUtensorMap &map, const CUtensorMap &mo, const TilePassParams &p, int prog, int grid,
+                        cudaStream_t s) {
+    switch (prog) {
+        case 1: return launch_one<STAGES, QB, 1>(map, mo, p, grid, s);
+        case 2: return launch_one<STAGES, QB, 2>(map, mo, p, grid, s);
+        case 3: return launch_one<STAGES, QB, 3>(map, mo, p, grid, s);
+        case 4: return launch_one<STAGES, QB, 4>(map, mo, p, grid, s);
+        case 5: return launch_one<STAGES, QB, 5>(map, mo, p, grid, s);
+        default: return launch_one<STAGES, QB, 0>(map, mo, p, grid, s);
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+
+int tile_pass_grid(uint64_t items) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    uint64_t g = std::min<uint64_t>(items, (uint64_t)sms);
+    return (int)std::max<uint64_t>(g, 1);
+}
+
+// Tensor map of one member array (or `batch` consecutive members of member_stride = 2^L
+// elements) seen through tile set P.tile_bits: dims in ascending physical order, each maximal
+// run of tile bits split into <= 8-bit box dims (bits 0-2 = 16 doubles = one 128-B swizzle
+// row), each run of non-tile bits one dim with box 1 (its coordinate comes from the tile
+// number), the member index folded into the topmost non-tile dim.  Fills P.dim_* fields.
+qva_status make_tile_tensor_map(const double2 *psi, int L, int batch, TilePassParams &P, CUtensorMap *map) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled entry point unavailable");
+        return QVA_ERR_CUDA;
+    }
+    uint64_t tmask = 0;
+    for (int k = 0; k < kTileBits; ++k) tmask |= 1ull << P.tile_bits[k];
+    // dims as (first bit, width, is_tile)
+    struct D {
+        int lo, w;
+        bool tile;
+    };
+    std::vector<D> dims;
+    int b = 0;
+    while (b < L) {
+        bool tile = (tmask >> b) & 1;
+        int st = b;
+        while (b < L && (((tmask >> b) & 1) != 0) == tile) ++b;
+        if (tile) {
+            int x = st;
+            while (x < b) {
+                int w = (x == 0) ? std::min(3, b - x) : std::min(8, b - x);
+                dims.push_back({x, w, true});
+                x += w;
+            }
+        } else {
+            dims.push_back({st, b - st, false});
+        }
+    }
+    if (dims.empty() || !dims[0].tile || dims[0].lo != 0 || dims[0].w != 3) {
+        set_error("tile set must contain physical bits 0,1,2");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    int member_dim = -1;
+    uint64_t member_extra = 1;
+    if (batch > 1) {
+        if (!dims.back().tile) {
+            member_dim = (int)dims.size() - 1;
+            member_extra = (uint64_t)batch;
+        } else {
+            dims.push_back({L, 0, false});
+            member_dim = (int)dims.size() - 1;
+            member_extra = (uint64_t)batch;
+        }
+    }
+    if (dims.size() > 5) {
+        set_error("tile set needs more than 5 TMA dimensions");
+        return QVA_ERR_UNSUPPORTED;
+    }
+    cuuint64_t gdim[5], gstride[4];
+    cuuint32_t box[5], estr[5];
+    int src = 0;
+    for (int d = 0; d < 5; ++d) {
+        estr[d] = 1;
+        if (d < (int)dims.size()) {
+            const D &x = dims[d];
+            uint64_t sz = 1ull << x.w;
+            if (d == member_dim) sz *= member_extra;
+            gdim[d] = (d == 0) ? 2 * sz : sz;  // dim 0 counts doubles (re, im)
+            box[d] = x.tile ? (cuuint32_t)((d == 0) ? 2 * sz : sz) : 1;
+            if (d > 0) gstride[d - 1] = (cuuint64_t)(1ull << x.lo) * sizeof(double2);
+            if (x.tile) {
+                P.dim_src[d] = 0;
+                P.dim_w[d] = 0;
+            } else {
+                P.dim_src[d] = src;
+                P.dim_w[d] = x.w;
+                src += x.w;
+            }
+        } else {
+            gdim[d] = 1;
+            box[d] = 1;
+            gstride[d - 1] = 16;  // size-1 padding dim: any legal stride
+            P.dim_src[d] = 0;
+            P.dim_w[d] = 0;
+        }
+    }
+    P.member_dim = member_dim;
+    // L2 fill granule: 256 B only when every box row run is >= 256 B contiguous (tile bits 0..3)
+    const bool wide = dims.size() > 1 && dims[1].tile && dims[1].lo == 3;
+    static const int promo_env = [] {
+        const char *e = getenv("QVA_L2PROMO");
+        return e ? atoi(e) : -1;
+    }();
+    CUtensorMapL2promotion promo = wide ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    if (promo_env >= 0 && !wide) promo = (CUtensorMapL2promotion)promo_env;
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2 *>(psi), gdim, gstride, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        return QVA_ERR_CUDA;
+    }
+    return QVA_OK;
+}
+
+cudaError_t launch_tile_pass(const CUtensorMap &map, const CUtensorMap &map_out, const TilePassParams &p, int qbytes,
+                             int prog, int grid, cudaStream_t s) {
+    // programs without phase/expectation never take q; those with it always do
+    const bool qprog = prog == 0 || kTileProgs[prog].phase_k >= 0 || kTileProgs[prog].expect;
+    switch (qbytes) {
+        case 0: return qprog && prog != 0 ? cudaErrorInvalidValue : launch_prog<3, 0>(map, map_out, p, prog, grid, s);
+        case 1: return qprog ? launch_prog<3, 1>(map, map_out, p, prog, grid, s) : cudaErrorInvalidValue;
+        case 2: return qprog ? launch_prog<3, 2>(map, map_out, p, prog, grid, s) : cudaErrorInvalidValue;
+        case 8: return qprog ? launch_prog<2, 8>(map, map_out, p, prog, grid, s) : cudaErrorInvalidValue;
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_qt_gather(void *dst, const void *src, int qbytes, const TilePassParams &p, const TileGroup &g,
+                             uint64_t n_tiles, int qmin, cudaStream_t s) {
+    const uint64_t total = n_tiles * (uint64_t)kTile;
+    int blocks = (int)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+    if (qbytes == 8)
+        qt_gather_kernel<double><<<blocks, 256, 0, s>>>((double *)dst, (const double *)src, p, g, n_tiles, 0);
+    else if (qbytes == 2)
+        qt_gather_kernel<int16_t><<<blocks, 256, 0, s>>>((int16_t *)dst, (const int16_t *)src, p, g, n_tiles, qmin);
+    else qt_gather_kernel<int8_t><<<blocks, 256, 0, s>>>((int8_t *)dst, (const int8_t *)src, p, g, n_tiles, qmin);
+    return cudaGetLastError();
+}
+
+int tile_consumer_warps() { return kCW; }
+
+}  // namespace qva

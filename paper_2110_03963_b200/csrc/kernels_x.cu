@@ -1,14 +1,7 @@
 // kernels_x.cu -- sm_100a kernels of the X-mixer (QAOA) path and the shared elementwise /
 // reduction kernels.
 //
-//  * tile_pass_kernel: one HBM round trip over the state.  A CTA owns a tile of 2^12
-//    amplitudes whose tile-local bits map to 12 physical index bits (the three lowest
-//    physical bits are always included so every warp access is >= 128 B contiguous).
-//    Inside the tile it applies, in registers, any subset of the single-qubit rotations
-//    exp(-i beta X_j) (reading R1), optionally the phase exp(-i gamma q)
-//     between two rotation sets, and optionally accumulates
-//    sum |psi|^2 q and sum |psi|^2 (Eq. 2).  Register groups of 4 tile bits
-//    are exchanged through a swizzled shared-memory tile (conflict-free 16-B accesses).
+//  (the tile pass of the X mixer lives in kernels_tile.cu)
 //  * small_evolve_kernel: whole p-layer evolution of a <= 2^12-amplitude state in one CTA.
 //  * maxcut_q_kernel: q_x = -cut_w(x) (Eq. maxcut-cost, reading R10).
 //  * fixed-order fp64 reductions (deterministic), elementwise phase, transpose for the
@@ -16,45 +9,21 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "qva_internal.h"
 
 namespace qva {
 
 namespace {
 
-constexpr int kTile = 1 << kTileBits;          // 4096 amplitudes
-constexpr int kPerThread = kTile / kTileThreads;  // 16
-
-__device__ __forceinline__ int smem_slot(int i) { return i ^ ((i >> 4) & 7); }
-
-// tile-local index held by (tid, e) in register group g
-__device__ __forceinline__ int map_index(int g, int tid, int e) {
-    if (g == 0) return (tid << 4) | e;                              // A: register bits = tile bits 0..3
-    if (g == 1) return ((tid >> 4) << 8) | (e << 4) | (tid & 15);   // B: tile bits 4..7
-    return (e << 8) | tid;                                          // C: tile bits 8..11
-}
-
-// a' = c a - i s b ; b' = -i s a + c b   (exp(-i beta X) on the pair)
+// a' = c a - i s b ; b' = -i s a + c b   (exp(-i beta X) on the pair; small-state kernel)
 __device__ __forceinline__ void butterfly(double2 &a, double2 &b, double c, double s) {
     double ar = a.x, ai = a.y, br = b.x, bi = b.y;
     a.x = fma(c, ar, s * bi);
     a.y = fma(c, ai, -s * br);
     b.x = fma(c, br, s * ai);
     b.y = fma(c, bi, -s * ar);
-}
-
-template <int B>
-__device__ __forceinline__ void rot_bit(double2 (&v)[kPerThread], double c, double s) {
-#pragma unroll
-    for (int e = 0; e < kPerThread; ++e)
-        if (!(e & (1 << B))) butterfly(v[e], v[e | (1 << B)], c, s);
-}
-
-__device__ __forceinline__ void rotate_mask(double2 (&v)[kPerThread], int mask, double c, double s) {
-    if (mask & 1) rot_bit<0>(v, c, s);
-    if (mask & 2) rot_bit<1>(v, c, s);
-    if (mask & 4) rot_bit<2>(v, c, s);
-    if (mask & 8) rot_bit<3>(v, c, s);
 }
 
 __device__ __forceinline__ void apply_phase(double2 &a, double qv, double gamma) {
@@ -90,101 +59,49 @@ __device__ __forceinline__ void block_reduce2(double &a, double &b, double *red)
     }
 }
 
-__global__ void __launch_bounds__(kTileThreads, 2)
-tile_pass_kernel(const TilePassParams P) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *tile = reinterpret_cast<double2 *>(smem_raw);
-    uint64_t *off_lo = reinterpret_cast<uint64_t *>(smem_raw + kTile * sizeof(double2));
-    uint64_t *off_hi = off_lo + 64;
-    __shared__ double red[2 * (kTileThreads / 32)];
-
-    const int tid = threadIdx.x;
-    const uint64_t t = blockIdx.x;
-    const int member = blockIdx.y;
-
-    // physical offset tables of the tile-local index (bits 0..5 and 6..11)
-    if (tid < 128) {
-        int j = tid & 63, hi = tid >> 6;
-        uint64_t o = 0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k)
-            if ((j >> k) & 1) o |= (uint64_t)1 << P.tile_bits[k + 6 * hi];
-        (hi ? off_hi : off_lo)[j] = o;
+__global__ void phase_table_kernel(double2 *tab, const double *gammas, int batch, int qmin, int ntab) {
+    int total = batch * ntab;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+        int b = k / ntab, j = k - b * ntab;
+        double sn, cs;
+        sincos(gammas[b] * (double)(qmin + j), &sn, &cs);
+        tab[k] = make_double2(cs, -sn);
     }
-    // base: deposit the tile number into the non-tile physical bits
-    uint64_t tmask = 0;
-#pragma unroll
-    for (int k = 0; k < kTileBits; ++k) tmask |= (uint64_t)1 << P.tile_bits[k];
-    uint64_t base = 0, tt = t;
-    for (int b = 0; b < P.n_phys_bits; ++b) {
-        if (!((tmask >> b) & 1)) {
-            base |= (tt & 1) << b;
-            tt >>= 1;
-        }
+}
+
+// flags[0] |= non-integer seen; partial min/max per block
+__global__ void q_range_kernel(const double *q, uint64_t n, int *flags, double *mm) {
+    __shared__ double smin[256], smax[256];
+    double lo = INFINITY, hi = -INFINITY;
+    int nonint = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        double x = q[i];
+        lo = fmin(lo, x);
+        hi = fmax(hi, x);
+        if (x != rint(x)) nonint = 1;
     }
+    if (nonint) atomicOr(flags, 1);
+    smin[threadIdx.x] = lo;
+    smax[threadIdx.x] = hi;
     __syncthreads();
-
-    const PassAngles ang = P.angles[member];
-    const double2 *src = P.psi_in + (uint64_t)member * P.member_stride;
-    double2 *dst = P.psi_out + (uint64_t)member * P.member_stride;
-
-    double2 v[kPerThread];
-    int g = P.steps[0].group;
-    if (P.init == 1) {
-#pragma unroll
-        for (int e = 0; e < kPerThread; ++e) v[e] = make_double2(P.amp0, 0.0);
-    } else {
-#pragma unroll
-        for (int e = 0; e < kPerThread; ++e) {
-            int i = map_index(g, tid, e);
-            v[e] = src[base + off_lo[i & 63] + off_hi[i >> 6]];
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + s]);
+            smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
         }
+        __syncthreads();
     }
-
-    for (int k = 0; k < P.n_steps; ++k) {
-        const PassStep st = P.steps[k];
-        if (st.group != g) {
-#pragma unroll
-            for (int e = 0; e < kPerThread; ++e) tile[smem_slot(map_index(g, tid, e))] = v[e];
-            __syncthreads();
-            g = st.group;
-#pragma unroll
-            for (int e = 0; e < kPerThread; ++e) v[e] = tile[smem_slot(map_index(g, tid, e))];
-            __syncthreads();
-        }
-        if (st.mask) {
-            double c = st.angle ? ang.c2 : ang.c1;
-            double s = st.angle ? ang.s2 : ang.s1;
-            rotate_mask(v, st.mask, c, s);
-        }
-        if (st.phase) {
-#pragma unroll
-            for (int e = 0; e < kPerThread; ++e) {
-                int i = map_index(g, tid, e);
-                apply_phase(v[e], __ldg(P.q + base + off_lo[i & 63] + off_hi[i >> 6]), ang.gamma);
-            }
-        }
+    if (threadIdx.x == 0) {
+        mm[2 * blockIdx.x] = smin[0];
+        mm[2 * blockIdx.x + 1] = smax[0];
     }
+}
 
-    double acc = 0.0, nrm = 0.0;
-#pragma unroll
-    for (int e = 0; e < kPerThread; ++e) {
-        int i = map_index(g, tid, e);
-        uint64_t o = base + off_lo[i & 63] + off_hi[i >> 6];
-        dst[o] = v[e];
-        if (P.expect) {
-            double pr = v[e].x * v[e].x + v[e].y * v[e].y;
-            acc = fma(pr, __ldg(P.q + o), acc);
-            nrm += pr;
-        }
-    }
-    if (P.expect) {
-        block_reduce2(acc, nrm, red);
-        if (tid == 0) {
-            double *pp = P.partials + 2 * ((uint64_t)member * P.n_tiles + t);
-            pp[0] = acc;
-            pp[1] = nrm;
-        }
+__global__ void q_encode_kernel(const double *q, uint64_t n, void *codes, int bytes) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        int c = (int)q[i];
+        if (bytes == 1) reinterpret_cast<int8_t *>(codes)[i] = (int8_t)c;
+        else reinterpret_cast<int16_t *>(codes)[i] = (int16_t)c;
     }
 }
 
@@ -367,17 +284,21 @@ inline int grid_for(uint64_t n, int threads) {
 
 }  // namespace
 
-cudaError_t launch_tile_pass(const TilePassParams &p, int batch, cudaStream_t s) {
-    static bool configured = false;
-    size_t smem = kTile * sizeof(double2) + 128 * sizeof(uint64_t);
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tile_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    dim3 grid((unsigned)p.n_tiles, (unsigned)batch);
-    tile_pass_kernel<<<grid, kTileThreads, smem, s>>>(p);
+cudaError_t launch_phase_table(double2 *tab, const double *gammas, int batch, int qmin, int ntab, cudaStream_t s) {
+    int total = batch * ntab;
+    phase_table_kernel<<<(total + 255) / 256, 256, 0, s>>>(tab, gammas, batch, qmin, ntab);
+    return cudaGetLastError();
+}
+
+int q_range_blocks(uint64_t n) { return grid_for(n, 256); }
+
+cudaError_t launch_q_range(const double *q, uint64_t n, int *flags, double *mm, int blocks, cudaStream_t s) {
+    q_range_kernel<<<blocks, 256, 0, s>>>(q, n, flags, mm);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_q_encode(const double *q, uint64_t n, void *codes, int bytes, cudaStream_t s) {
+    q_encode_kernel<<<grid_for(n, 256), 256, 0, s>>>(q, n, codes, bytes);
     return cudaGetLastError();
 }
 
@@ -407,6 +328,15 @@ cudaError_t launch_chunk_transpose(T *out, const T *in, int G, uint64_t C, cudaS
 }
 template cudaError_t launch_chunk_transpose<double2>(double2 *, const double2 *, int, uint64_t, cudaStream_t);
 template cudaError_t launch_chunk_transpose<double>(double *, const double *, int, uint64_t, cudaStream_t);
+
+cudaError_t launch_chunk_transpose_bytes(void *out, const void *in, int G, uint64_t C, int elem_bytes, cudaStream_t s) {
+    uint64_t total = (uint64_t)G * G * C;
+    if (elem_bytes == 1)
+        chunk_transpose_kernel<int8_t><<<grid_for(total, 256), 256, 0, s>>>((int8_t *)out, (const int8_t *)in, G, C);
+    else
+        chunk_transpose_kernel<int16_t><<<grid_for(total, 256), 256, 0, s>>>((int16_t *)out, (const int16_t *)in, G, C);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_reduce_partials(const double *partials, uint64_t n, int batch, double *out, cudaStream_t s) {
     reduce_partials_kernel<<<batch, 1024, 0, s>>>(partials, n, out);

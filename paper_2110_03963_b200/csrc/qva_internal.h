@@ -2,6 +2,7 @@
 // Product code only: nothing here is shared with oracle/ (DESIGN.md "Oracle").
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>
@@ -43,45 +44,116 @@ void set_error(const std::string &msg);
     } while (0)
 
 // ---------------------------------------------------------------------------------------------
-// X-mixer tile passes (kernels_x.cu)
+// X-mixer tile passes (kernels_tile.cu)
 // ---------------------------------------------------------------------------------------------
-constexpr int kTileBits = 12;                 // 2^12 amplitudes (64 KiB) per CTA tile
-constexpr int kTileThreads = 256;             // 16 amplitudes per thread in registers
-constexpr int kMaxSteps = 8;
+constexpr int kTileBits = 12;                 // 2^12 amplitudes (64 KiB) per tile
+constexpr int kGroupBits = 5;                 // 32 amplitudes per consumer thread in registers
+constexpr int kCT_BITS = 7;                   // 128 consumer threads
+constexpr int kMaxSteps = 16;
+constexpr int kMaxGroups = 3;
 constexpr int kSmallMaxQubits = 12;           // whole-state-in-one-CTA path
 
-// One register-group step of a pass.  Tile-local bits are split in three 4-bit groups:
-// group 0 (A) = tile bits 0..3, group 1 (B) = 4..7, group 2 (C) = 8..11.
-struct PassStep {
-    int8_t group;      // 0 A, 1 B, 2 C
-    int8_t mask;       // 4-bit rotation mask inside the group
-    int8_t angle;      // 0: first beta slot (R1), 1: second (R2)
-    int8_t phase;      // apply the phase after the rotations of this step
+// Register group: which tile-local bits the 5 register-index bits (ebit) and the 7 consumer
+// thread-index bits (tbit) address.  Chosen on the host so that every 8-lane phase of a
+// 16-byte smem access hits 8 distinct bank groups under SWIZZLE_128B.
+struct TileGroup {
+    int8_t ebit[kGroupBits];
+    int8_t tbit[kCT_BITS];
 };
 
-// Per-member angle record for one pass (device array [batch][kPassAngles]).
-struct PassAngles {
-    double c1, s1, c2, s2, gamma;
+struct PassStep {
+    int8_t group;      // index into TilePassParams::groups
+    int8_t mask;       // 5-bit rotation mask over the group's register bits
+    int8_t angle;      // 0: first beta slot (R1), 1: second (R2)
+    int8_t phase;      // apply the phase after the rotations of this step (group must be gq)
 };
+
+// Per-member angle record for one pass (device array [batch]).  Rotations use the factored
+// form a' = a - i t b, b' = b - i t a (t = tan beta); the dropped scalar cos beta (per rotation)
+// is applied once at the end of the pass as `scale`.  When |cos beta| < 2^-10 the host applies
+// two steps of half the angle instead.
+struct PassAngles {
+    double t1, t2;           // R1 / R2 tan(beta) (of beta/2 when halved)
+    double gamma;            // phase angle
+    double2 scale;           // product of the dropped rotation factors of this pass
+};
+
+// Non-tile physical bits as runs: base(t) = sum_r ((t >> src_r) & (2^w_r - 1)) << dst_r
+constexpr int kMaxRuns = 4;
+constexpr int kMaxBatchSmem = 64;            // batch members per tile-pass launch (angles live in smem)
 
 struct TilePassParams {
-    const double2 *psi_in;   // may alias psi_out
-    double2 *psi_out;
-    const double *q;         // qualities in the current layout (phase / expectation)
+    double2 *psi_out;        // output array (input comes through the tensor map; may alias)
+    const void *qt;          // q in consumer order of group gq: [n_tiles][4096] fp64 / int8 / int16
+    const double2 *tab;      // integer codes: [batch][ntab] phase factors exp(-i gamma (qmin + j))
     const PassAngles *angles;// [batch]
-    double *partials;        // [batch][n_tiles][2] (expectation, norm) when expect
+    double *partials;        // [batch][gridDim.x][4 warps][2] (expectation, norm); zeroed by host
     uint64_t member_stride;  // elements between batch members
     uint64_t n_tiles;        // tiles per member
-    int tile_bits[kTileBits];// physical bit positions of tile-local bits (ascending; 0,1,2 first)
-    int n_phys_bits;         // physical index bits of one member's array
+    int batch;
+    int tile_bits[kTileBits];// physical bit of tile-local bit k (ascending)
+    int n_runs;
+    int run_src[kMaxRuns], run_dst[kMaxRuns], run_w[kMaxRuns];
+    uint64_t run_mask[kMaxRuns];  // 2^run_w - 1 (0 for unused runs)
+    int log2_tiles;          // n_tiles = 2^log2_tiles
+    // TMA coordinates: dim d takes bits [dim_src, dim_src + dim_w) of the tile number
+    // (dim_w = 0: a tile dim, coordinate 0); member_dim adds member << dim_w
+    int dim_src[5], dim_w[5];
+    int member_dim;
+    int n_groups;
+    TileGroup groups[kMaxGroups];
     int n_steps;
     PassStep steps[kMaxSteps];
-    int init;                // 1: first pass, psi = amp0 (no read); 2: first pass, read psi0 (psi_in)
-    int expect;              // accumulate partial <Q> and norm
+    uint64_t st_estr[kGroupBits];  // final group: physical stride of register bit j
+    int st_tphys[kCT_BITS];        // final group: physical bit of consumer-thread bit j
+    int gq;                  // group in which q is consumed (phase / expectation), -1: no q
+    int init;                // 1: first pass, psi = amp0 (no read)
+    int expect;              // accumulate partial <Q> and norm in the final group (== gq)
+    int qmin, ntab;
+    int apply_scale;
+    int tma_store;           // 1: write the tile back with a TMA tensor store (strided tile sets)
+    int release_step;        // step after whose smem accesses the stage is released (n_steps: after
+                             // the expectation; -1: before any step, i.e. init passes without q)
     double amp0;
 };
 
-cudaError_t launch_tile_pass(const TilePassParams &p, int batch, cudaStream_t s);
+// Compile-time pass programs (kernels_tile.cu): group sequence g[0..n), which steps rotate,
+// the step after whose rotations the phase is applied (-1: none) and whether the expectation is
+// accumulated.  Program 0 = the generic interpreter of TilePassParams::steps.
+struct TileProg {
+    int n;
+    int g[5];
+    bool rot[5];
+    int phase_k;
+    bool expect;
+};
+constexpr int kNumTileProgs = 6;
+constexpr TileProg kTileProgs[kNumTileProgs] = {
+    {0, {0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}, -1, false},  // 0: generic
+    {2, {0, 1, 0, 0, 0}, {1, 1, 0, 0, 0}, -1, false},  // 1: X Y            (B/C pass)
+    {3, {0, 2, 1, 0, 0}, {1, 1, 1, 0, 0}, -1, false},  // 2: X W Y          (A pass)
+    {4, {0, 1, 1, 0, 0}, {1, 1, 1, 1, 0}, 1, false},   // 3: X Y | P | Y X  (B/C pass across a layer boundary)
+    {2, {0, 1, 0, 0, 0}, {1, 1, 0, 0, 0}, -1, true},   // 4: X Y + <Q>      (last pass)
+    {4, {0, 0, 2, 1, 0}, {0, 1, 1, 1, 0}, 0, false},   // 5: P | X W Y      (first pass, from |+>)
+};
+
+int tile_pass_grid(uint64_t items);
+int tile_consumer_warps();
+// builds the 5-D tensor map of psi seen through P.tile_bits (and fills P.dim_*, P.member_dim)
+qva_status make_tile_tensor_map(const double2 *psi, int L, int batch, TilePassParams &P, CUtensorMap *map);
+// qbytes: 0 (no q), 1 (int8 codes), 2 (int16 codes), 8 (fp64)
+cudaError_t launch_tile_pass(const CUtensorMap &map, const CUtensorMap &map_out, const TilePassParams &p, int qbytes,
+                             int prog, int grid, cudaStream_t s);
+cudaError_t launch_qt_gather(void *dst, const void *src, int qbytes, const TilePassParams &p, const TileGroup &g,
+                             uint64_t n_tiles, int qmin, cudaStream_t s);
+// phase tables tab[b][j] = exp(-i gammas[b] (qmin + j)), j < ntab (same fp64 sincos as the
+// per-element path, so integer-valued q give identical factors)
+cudaError_t launch_phase_table(double2 *tab, const double *gammas, int batch, int qmin, int ntab, cudaStream_t s);
+// integer-valuedness / range of q: out[0] = all integer (1/0), out[1] = min, out[2] = max
+cudaError_t launch_q_range(const double *q, uint64_t n, int *flags, double *minmax_partials, int blocks,
+                           cudaStream_t s);
+int q_range_blocks(uint64_t n);
+cudaError_t launch_q_encode(const double *q, uint64_t n, void *codes, int bytes, cudaStream_t s);
 
 struct SmallEvolveParams {
     double2 *psi;            // [batch][2^n]
@@ -100,6 +172,9 @@ cudaError_t launch_maxcut_q(double *q, uint64_t count, uint64_t offset, int m, c
 // block transpose of G x G chunks of C elements: out[t][r] = in[r][t]
 template <typename T>
 cudaError_t launch_chunk_transpose(T *out, const T *in, int G, uint64_t C, cudaStream_t s);
+// same for raw bytes (int8/int16 code arrays): elem_bytes in {1, 2}
+cudaError_t launch_chunk_transpose_bytes(void *out, const void *in, int G, uint64_t C, int elem_bytes,
+                                         cudaStream_t s);
 // fixed-order reduction of partials [batch][n][2] -> out [batch][2]
 cudaError_t launch_reduce_partials(const double *partials, uint64_t n, int batch, double *out,
                                    cudaStream_t s);
