@@ -258,13 +258,7 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
-    nccl_id = None
-    if world > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(Q.qva_nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tobytes())
+    nccl_id = Q.nccl_id_broadcast() if world > 1 else None
 
     batch = wl.batch_thetas if name == "cfg2" else None
     plan = Q.Plan(wl.dim, wl.mixer, n_qubits=wl.n_qubits, rank=rank, world=world, nccl_id=nccl_id,

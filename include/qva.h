@@ -161,6 +161,15 @@ qva_status qva_nccl_unique_id(void *id_out);
 /* Host-only: which batch entries [first, first+count) rank `rank` evolves (B split across ranks,
  * remainder to the lowest ranks). */
 qva_status qva_batch_partition(int32_t B, int32_t world, int32_t rank, int32_t *first, int32_t *count);
+/* Host-only: the global<->local qubit swap of the sharded X mixer (COMM-psi)
+ * as a chunk exchange.  Every shard's local array (2^L elements) is G equal chunks, chunk index
+ * = the top g = log2 G local bits.  For local chunk t of shard `rank`: peer_of_chunk[t] = the
+ * shard it is sent to and received from (t), peer_chunk[t] = the chunk index it occupies there
+ * (rank).  Applying it swaps the g global index bits with the top g local bits (a G x G block
+ * transpose); it is an involution, so the same plan returns to layout A.  Both arrays hold G
+ * entries (caller-owned).  QVA_ERR_INVALID_ARGUMENT unless G is a power of two and
+ * 0 <= rank < G. */
+qva_status qva_exchange_plan(int32_t G, int32_t rank, int32_t *peer_of_chunk, int32_t *peer_chunk);
 
 /* ---- introspection ---------------------------------------------------------------------------- */
 

@@ -77,6 +77,7 @@ def _load():
         "qva_evolve_batch": [P, P, i32, i32, P],
         "qva_nccl_unique_id": [P],
         "qva_batch_partition": [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)],
+        "qva_exchange_plan": [i32, i32, P, P],
         "qva_x_schedule": [i32, i32, P, i32, ctypes.POINTER(i32)],
         "qva_set_profiling": [P, i32],
         "qva_kernel_stats": [P, i32, ctypes.POINTER(d), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(d)],
@@ -143,10 +144,33 @@ def qva_x_schedule(n_local: int, p: int):
     return [tuple(int(v) for v in out[4 * i:4 * i + 4]) for i in range(n.value)]
 
 
+def qva_exchange_plan(G: int, rank: int):
+    """(peer_of_chunk[G], peer_chunk[G]) of the global<->local qubit swap (include/qva.h)."""
+    peer = np.zeros(G, np.int32)
+    pchunk = np.zeros(G, np.int32)
+    _call("qva_exchange_plan", G, rank, _ptr(peer), _ptr(pchunk))
+    return peer, pchunk
+
+
 def qva_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _call("qva_nccl_unique_id", ctypes.cast(buf, ctypes.c_void_p))
     return buf.raw
+
+
+def nccl_id_broadcast(group=None) -> bytes:
+    """NCCL bootstrap over an initialised torch.distributed group (any backend): rank 0 creates
+    the 128-byte ncclUniqueId with qva_nccl_unique_id, every rank receives it by a uint8
+    broadcast.  Pass the result as Plan(..., nccl_id=...) on every rank."""
+    import torch
+    import torch.distributed as dist
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if dist.get_rank(group) == 0:
+        t.copy_(torch.frombuffer(bytearray(qva_nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(t, 0, group=group)
+    return bytes(t.cpu().numpy().tobytes())
 
 
 def _f64(a) -> np.ndarray:

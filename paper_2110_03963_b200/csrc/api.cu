@@ -480,11 +480,15 @@ qva_status exchange_buffers(qva_plan *P, T *src, T *dst) {
     }
     ProfScope ps(P, K_EXCHANGE, 2.0 * sizeof(T) * (double)P->arr_n);
     size_t cnt = C * sizeof(T) / sizeof(double);
+    std::vector<int32_t> peer(P->world), pchunk(P->world);
+    QVA_TRY(qva_exchange_plan(P->world, P->rank, peer.data(), pchunk.data()));
     QVA_NCCL_TRY(ncclGroupStart());
     for (int t = 0; t < P->world; ++t) {
-        if (t == P->rank) continue;
-        QVA_NCCL_TRY(ncclSend((const double *)(src + t * C), cnt, ncclDouble, t, P->comm, P->stream));
-        QVA_NCCL_TRY(ncclRecv((double *)(dst + t * C), cnt, ncclDouble, t, P->comm, P->stream));
+        if (peer[t] == P->rank) continue;
+        // send our chunk t to peer[t]; receive the peer's chunk pchunk into our chunk t (the plan is
+        // symmetric: the peer sends us its chunk `rank`, which lands in our chunk t)
+        QVA_NCCL_TRY(ncclSend((const double *)(src + t * C), cnt, ncclDouble, peer[t], P->comm, P->stream));
+        QVA_NCCL_TRY(ncclRecv((double *)(dst + t * C), cnt, ncclDouble, peer[t], P->comm, P->stream));
     }
     QVA_NCCL_TRY(ncclGroupEnd());
     QVA_CUDA_TRY(cudaMemcpyAsync(dst + P->rank * C, src + P->rank * C, C * sizeof(T), cudaMemcpyDeviceToDevice,
@@ -974,6 +978,18 @@ qva_status qva_batch_partition(int32_t B, int32_t world, int32_t rank, int32_t *
     int32_t base = B / world, rem = B % world;
     *count = base + (rank < rem ? 1 : 0);
     *first = base * rank + std::min(rank, rem);
+    return QVA_OK;
+}
+
+qva_status qva_exchange_plan(int32_t G, int32_t rank, int32_t *peer_of_chunk, int32_t *peer_chunk) {
+    if (G < 1 || (G & (G - 1)) || rank < 0 || rank >= G || !peer_of_chunk || !peer_chunk) {
+        set_error("qva_exchange_plan: G must be a power of two, 0 <= rank < G");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    for (int32_t t = 0; t < G; ++t) {
+        peer_of_chunk[t] = t;    // chunk t (top local bits = t) goes to the shard whose rank is t
+        peer_chunk[t] = rank;    // ... where it becomes chunk `rank` (top local bits = our rank)
+    }
     return QVA_OK;
 }
 
