@@ -177,6 +177,13 @@ qva_status qva_exchange_plan(int32_t G, int32_t rank, int32_t *peer_of_chunk, in
  * (tile_set_index, n_rot_before_phase, has_phase, n_rot_after_phase) as 4 int32 per pass and
  * returns the pass count in *n_passes.  Host-only. */
 qva_status qva_x_schedule(int32_t n_local, int32_t p, int32_t *out, int32_t cap, int32_t *n_passes);
+/* Host-only: the permuted out-of-place schedule used by qva_evolve on a single shard with
+ * n_local >= 21 qubits.  Per pass, 8 int64 in out[8*i ..]:
+ * {first bit of the 9-bit read window (3 = contiguous tile), layer of the R1 rotations (-1: none),
+ *  layer of the R2 rotations (-1), phase layer (-1), expectation fused (0/1), logical-qubit mask
+ *  of R1, logical-qubit mask of R2, TMA dims of the pass}.  cap = passes that fit in out.
+ * QVA_ERR_INVALID_ARGUMENT unless 21 <= n_local <= 40 and p >= 1. */
+qva_status qva_x_schedule_permuted(int32_t n_local, int32_t p, int64_t *out, int32_t cap, int32_t *n_passes);
 /* Kernel timing: when enabled, every kernel launch of the plan is bracketed with CUDA events
  * on the plan's stream; qva_kernel_stats returns, for kernel class `which` (0 = X tile pass,
  * 1 = small-state fused evolve, 2 = FFT column pass, 3 = FFT row pass, 4 = sparse SpMV,

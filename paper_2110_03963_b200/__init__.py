@@ -79,6 +79,7 @@ def _load():
         "qva_batch_partition": [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)],
         "qva_exchange_plan": [i32, i32, P, P],
         "qva_x_schedule": [i32, i32, P, i32, ctypes.POINTER(i32)],
+        "qva_x_schedule_permuted": [i32, i32, P, i32, ctypes.POINTER(i32)],
         "qva_set_profiling": [P, i32],
         "qva_kernel_stats": [P, i32, ctypes.POINTER(d), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(d)],
         "qva_reset_kernel_stats": [P],
@@ -142,6 +143,17 @@ def qva_x_schedule(n_local: int, p: int):
     n = ctypes.c_int32()
     _call("qva_x_schedule", n_local, p, _ptr(out), cap, ctypes.byref(n))
     return [tuple(int(v) for v in out[4 * i:4 * i + 4]) for i in range(n.value)]
+
+
+def qva_x_schedule_permuted(n_local: int, p: int):
+    """Per pass of the permuted single-shard schedule: dict(window, a1, a2, phase, expect, r1, r2,
+    dims) with r1/r2 the logical-qubit masks rotated before/after the phase (include/qva.h)."""
+    cap = 64 * (p + 1)
+    out = np.zeros(8 * cap, np.int64)
+    n = ctypes.c_int32()
+    _call("qva_x_schedule_permuted", n_local, p, _ptr(out), cap, ctypes.byref(n))
+    keys = ("window", "a1", "a2", "phase", "expect", "r1", "r2", "dims")
+    return [dict(zip(keys, (int(x) for x in out[8 * i:8 * i + 8]))) for i in range(min(n.value, cap))]
 
 
 def qva_exchange_plan(G: int, rank: int):

@@ -45,11 +45,16 @@ struct Token {
 
 struct PassPlan {
     bool exchange = false;   // this entry is an exchange, not a tile pass
-    int set = -1;
+    int set = -1;            // in-place passes: index into the plan's tile sets
     uint32_t r1 = 0, r2 = 0; // tile-local masks
     int a1 = -1, a2 = -1;    // layer index of beta for R1 / R2
     int phase = -1;          // layer index of gamma
     bool expect = false;
+    // permuted out-of-place passes (perm_passes): physical tile bits of the input layout, the
+    // layout before the pass (physical bit -> logical qubit) and the store permutation
+    // (input physical bit -> output physical bit)
+    bool permuted = false;
+    std::vector<int> tbits, lay_in, obit;
 };
 
 static std::vector<std::vector<int>> make_tile_sets(int L) {
@@ -137,6 +142,130 @@ static std::vector<PassPlan> cut_passes(const std::vector<Token> &toks, const st
         out.push_back(pp);
     }
     if (expect_at_end && !out.empty() && !out.back().exchange) out.back().expect = true;
+    return out;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Permuted-layout schedule (single shard).
+//
+// An in-place pass over a strided tile set reads AND writes 128-B rows scattered over the whole
+// state (measured 7.1-8.6 ms per 16-GiB pass vs 5.35 ms for the contiguous set).  Here every pass
+// instead writes its tile out of place as one contiguous 64-KiB block (tile bits -> physical bits
+// 0..11, in order) and reorders the non-tile bit runs so that the qubits the next pass rotates
+// sit in the window 12..20 (128-B rows at a 64-KiB stride: the cheapest strided read).  The
+// state therefore lives in a permuted layout (physical bit -> logical qubit) that the plan
+// records; bits 0..2 never move.  Passes are cut greedily from the same token stream as
+// cut_passes: each pass rotates every pending qubit its tile holds, applies the next phase as soon
+// as the current layer is complete and then starts the next layer on the same tile.
+// ---------------------------------------------------------------------------------------------
+static std::vector<int> window_bits(int w) {
+    std::vector<int> t = {0, 1, 2};
+    for (int b = w; b < w + 9; ++b) t.push_back(b);
+    if (w == 3) t.resize(kTileBits);
+    return t;
+}
+
+static std::vector<PassPlan> perm_passes(int L, int p, std::vector<int> *final_layout) {
+    std::vector<PassPlan> out;
+    std::vector<int> lay(L);
+    for (int b = 0; b < L; ++b) lay[b] = b;
+    const uint64_t all = (1ull << L) - 1;
+    uint64_t pending = 0;
+    int cur_layer = -1, next_phase = 0;
+    std::vector<int> T(kTileBits);
+    for (int k = 0; k < kTileBits; ++k) T[k] = k;
+    auto logical_mask = [&](const std::vector<int> &ly, const std::vector<int> &bits) {
+        uint64_t m = 0;
+        for (int b : bits) m |= 1ull << ly[b];
+        return m;
+    };
+    auto local_mask = [&](uint64_t lm) {
+        uint32_t m = 0;
+        for (int k = 0; k < kTileBits; ++k)
+            if ((lm >> lay[T[k]]) & 1) m |= 1u << k;
+        return m;
+    };
+    for (int guard = 0; guard < 64 * (p + 1); ++guard) {
+        PassPlan pp;
+        pp.permuted = true;
+        pp.tbits = T;
+        pp.lay_in = lay;
+        const uint64_t tl = logical_mask(lay, T);
+        const uint64_t r1 = pending & tl;
+        pending &= ~r1;
+        pp.r1 = local_mask(r1);
+        pp.a1 = r1 ? cur_layer : -1;
+        if (!pending && next_phase < p) {
+            pp.phase = next_phase;
+            cur_layer = next_phase++;
+            uint64_t r2 = all & tl;
+            // a layer-boundary pass leaves the three row bits (always tile bits) to the next pass
+            // of the layer, so its shape stays the compiled X Y | P | Y X program
+            if (r1 && (all & ~tl)) r2 &= ~7ull;
+            pending = all & ~r2;
+            pp.r2 = local_mask(r2);
+            pp.a2 = r2 ? cur_layer : -1;
+        }
+        const bool last = !pending && next_phase >= p;
+        pp.expect = last;
+        // store map: tile bits (ascending) -> 0..11; non-tile runs, split into <= 9-bit pieces,
+        // placed from bit 12 upward in the order that puts the most pending qubits in 12..20
+        std::vector<int> obit(L, -1);
+        for (int k = 0; k < kTileBits; ++k) obit[T[k]] = k;
+        std::vector<std::pair<int, int>> pieces;  // (lo, w)
+        {
+            int b = 0;
+            while (b < L) {
+                if (obit[b] >= 0) { ++b; continue; }
+                int st = b;
+                while (b < L && obit[b] < 0 && b - st < 9) ++b;
+                pieces.push_back({st, b - st});
+            }
+        }
+        std::vector<int> order(pieces.size());
+        for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+        std::vector<int> best_obit, best_lay;
+        int best_score = -1;
+        const bool enumerate = pieces.size() <= 6;
+        do {
+            std::vector<int> ob = obit;
+            int pos = kTileBits;
+            for (int i : order)
+                for (int j = 0; j < pieces[i].second; ++j) ob[pieces[i].first + j] = pos++;
+            if (tile_tma_dims(T.data(), L, ob.data()) > 5) continue;
+            std::vector<int> nl(L);
+            for (int b = 0; b < L; ++b) nl[ob[b]] = lay[b];
+            int score = 0;
+            for (int b = kTileBits; b < std::min(L, kTileBits + 9); ++b) score += (pending >> nl[b]) & 1;
+            if (score > best_score) {
+                best_score = score;
+                best_obit = ob;
+                best_lay = nl;
+            }
+        } while (enumerate && std::next_permutation(order.begin(), order.end()));
+        if (best_score < 0) {  // no order fits 5 TMA dims: keep the runs in place
+            best_obit = obit;
+            int pos = kTileBits;
+            for (auto &pc : pieces)
+                for (int j = 0; j < pc.second; ++j) best_obit[pc.first + j] = pos++;
+            best_lay.assign(L, 0);
+            for (int b = 0; b < L; ++b) best_lay[best_obit[b]] = lay[b];
+        }
+        pp.obit = best_obit;
+        out.push_back(pp);
+        lay = best_lay;
+        if (last) break;
+        // next tile: the 9-bit window (or the contiguous set) holding the most pending qubits
+        int best_w = 12, bc = -1;
+        for (int w = 3; w + 9 <= L; ++w) {
+            if (w > 3 && w < 12) continue;  // windows must not overlap the tile just written
+            int c = 0;
+            for (int b : window_bits(w)) c += (pending >> lay[b]) & 1;
+            if (c > bc || (c == bc && w == 12)) { bc = c; best_w = w; }
+        }
+        T = window_bits(best_w);
+    }
+    if (final_layout) *final_layout = lay;
     return out;
 }
 
@@ -316,11 +445,15 @@ struct qva_plan {
     // q permuted into the consumer order of (layout, tile set, register group): see
     // qt_gather_kernel.  Rebuilt lazily after every change of q.
     struct QtEntry {
-        int layout, set, group, qbytes;
+        std::vector<int> key;  // (sharded layout, tile bits, permuted layout)
+        int group, qbytes;
         void *buf;
     };
     std::vector<QtEntry> qt_cache;
     int layout = 0;
+    // permuted layout of the single-shard state (physical bit -> logical qubit); empty = natural
+    std::vector<int> perm;
+    bool perm_failed = false;
     double *partials = nullptr;
     uint64_t partials_n = 0;
     double *red = nullptr;             // [max_batch][2]
@@ -597,7 +730,9 @@ qva_status classify_q(qva_plan *P) {
     return sync(P);
 }
 
+qva_status to_natural_perm(qva_plan *P);
 qva_status to_layout_A(qva_plan *P) {
+    QVA_TRY(to_natural_perm(P));
     if (P->layout == 0) return QVA_OK;
     return exchange_state(P);
 }
@@ -607,24 +742,81 @@ void drop_qt(qva_plan *P) {
     P->qt_cache.clear();
 }
 
-// q (current layout) in the consumer order of group g of tile set `set` (tp: tile bits + runs)
-qva_status ensure_qt(qva_plan *P, int set, int g, int qbytes, const TilePassParams &tp, void **out) {
+// physical -> logical bit map as runs (nullptr / empty: identity over n bits)
+LayoutRuns layout_runs(const std::vector<int> *lay, int n) {
+    LayoutRuns R;
+    memset(&R, 0, sizeof(R));
+    if (!lay || lay->empty()) {
+        R.n = 1;
+        R.src[0] = 0;
+        R.w[0] = (int8_t)n;
+        R.dst[0] = 0;
+        return R;
+    }
+    const std::vector<int> &l = *lay;
+    int b = 0;
+    while (b < (int)l.size()) {
+        int st = b++;
+        while (b < (int)l.size() && l[b] == l[b - 1] + 1) ++b;
+        if (R.n < kMaxLayoutRuns) {
+            R.src[R.n] = (int8_t)st;
+            R.w[R.n] = (int8_t)(b - st);
+            R.dst[R.n] = (int8_t)l[st];
+        }
+        ++R.n;
+    }
+    // bits above the layout (batch members) map to themselves
+    if (n > (int)l.size() && R.n < kMaxLayoutRuns) {
+        R.src[R.n] = R.dst[R.n] = (int8_t)l.size();
+        R.w[R.n] = (int8_t)(n - (int)l.size());
+        ++R.n;
+    }
+    return R;
+}
+
+// q in the consumer order of group g for the pass tiles described by tp (tile bits + runs) and
+// the permuted layout lay (nullptr: natural / sharded layout P->layout)
+qva_status ensure_qt(qva_plan *P, const std::vector<int> &key, const std::vector<int> *lay, int g, int qbytes,
+                     const TilePassParams &tp, void **out) {
     for (auto &e : P->qt_cache)
-        if (e.layout == P->layout && e.set == set && e.group == g && e.qbytes == qbytes) {
+        if (e.key == key && e.group == g && e.qbytes == qbytes) {
             *out = e.buf;
             return QVA_OK;
         }
     const void *src;
     if (qbytes == 8) src = (P->layout == 1) ? (const void *)P->qB : (const void *)P->q;
     else src = (P->layout == 1) ? P->qcB : P->qc;
+    const LayoutRuns R = layout_runs(lay, ilog2(P->arr_n));
+    if (R.n > kMaxLayoutRuns) {
+        set_error("internal: permuted layout has too many runs");
+        return QVA_ERR_UNSUPPORTED;
+    }
     void *buf = nullptr;
     QVA_CUDA_TRY(cudaMalloc(&buf, P->arr_n * (size_t)qbytes));
     {
         ProfScope ps(P, K_OTHER, 2.0 * qbytes * (double)P->arr_n);
-        QVA_CUDA_TRY(launch_qt_gather(buf, src, qbytes, tp, kGroups[g], P->arr_n >> kTileBits, P->qmin, P->stream));
+        QVA_CUDA_TRY(
+            launch_qt_gather(buf, src, qbytes, tp, kGroups[g], P->arr_n >> kTileBits, P->qmin, R, P->stream));
     }
-    P->qt_cache.push_back({P->layout, set, g, qbytes, buf});
+    P->qt_cache.push_back({key, g, qbytes, buf});
     *out = buf;
+    return QVA_OK;
+}
+
+// return a permuted single-shard state to the natural layout (one gather pass; outside the
+// evolution, e.g. before get_state or a step-level call)
+qva_status to_natural_perm(qva_plan *P) {
+    if (P->perm.empty()) return QVA_OK;
+    bool ident = true;
+    for (size_t b = 0; b < P->perm.size(); ++b) ident &= P->perm[b] == (int)b;
+    if (!ident) {
+        if (!P->psi_alt) QVA_CUDA_TRY(cudaMalloc(&P->psi_alt, P->arr_n * sizeof(double2)));
+        const LayoutRuns R = layout_runs(&P->perm, ilog2(P->arr_n));
+        ProfScope ps(P, K_OTHER, 32.0 * P->arr_n);
+        QVA_CUDA_TRY(launch_permute_copy(P->psi_alt, P->psi, P->arr_n, R, P->stream));
+        std::swap(P->psi, P->psi_alt);
+    }
+    P->perm.clear();
     return QVA_OK;
 }
 
@@ -731,7 +923,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         }
         TilePassParams tp;
         memset(&tp, 0, sizeof(tp));
-        const std::vector<int> &s = P->sets[pp.set];
+        const std::vector<int> &s = pp.permuted ? pp.tbits : P->sets[pp.set];
         uint64_t tmask = 0;
         for (int k = 0; k < kTileBits; ++k) {
             tp.tile_bits[k] = s[k];
@@ -764,17 +956,24 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         tp.psi_out = psi_base;
         const double2 *psi_in = (first && init_mode == 2) ? P->psi0 : psi_base;
         tp.init = (first && init_mode == 1) ? 1 : 0;
+        // permuted passes write out of place (except a first pass, whose input is not psi_base)
+        const bool swap_after = pp.permuted && !(first && init_mode != 0);
+        if (swap_after) tp.psi_out = P->psi_alt;
         tp.amp0 = 1.0 / sqrt((double)P->N);
         const bool needs_q = pp.phase >= 0 || pp.expect;
+        // q copies are keyed by (sharded layout, tile bits, permuted layout)
+        std::vector<int> qkey = {P->layout};
+        qkey.insert(qkey.end(), s.begin(), s.end());
+        if (pp.permuted) qkey.insert(qkey.end(), pp.lay_in.begin(), pp.lay_in.end());
         int pref = -1;
         if (needs_q)
             for (auto &e : P->qt_cache)
-                if (e.layout == P->layout && e.set == pp.set && e.qbytes == qbytes) pref = e.group;
+                if (e.key == qkey && e.qbytes == qbytes) pref = e.group;
         build_steps(pp, tp, pref, half1[j], half2[j]);
         if (needs_q) {
             if (P->layout == 1) QVA_TRY(ensure_qB(P));
             void *qt = nullptr;
-            QVA_TRY(ensure_qt(P, pp.set, tp.gq, qbytes, tp, &qt));
+            QVA_TRY(ensure_qt(P, qkey, pp.permuted ? &pp.lay_in : nullptr, tp.gq, qbytes, tp, &qt));
             tp.qt = qt;
             tp.qmin = P->qmin;
             tp.ntab = ntab;
@@ -795,9 +994,25 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         // tiles go back through a TMA tensor store (measured faster than st.global from registers for
         // every tile shape; env QVA_TSTORE=0 selects the register stores for comparison)
         tp.tma_store = (g_tstore >= 0) ? g_tstore : 1;
+        static int order_env = [] { const char *e = getenv("QVA_ORDER"); return e ? atoi(e) : 0; }();
+        tp.order = order_env;
         CUtensorMap map, map_out;
-        QVA_TRY(make_tile_tensor_map(psi_in, n_phys, batch, tp, &map));
-        QVA_TRY(make_tile_tensor_map(tp.psi_out, n_phys, batch, tp, &map_out));
+        if (pp.permuted) tp.tma_store = 1;  // the permuted store is a TMA store map
+        // L2 block prefetch for strided sets: the block is everything below the highest tile bit;
+        // tiles per block = 2^(coordinate bits below it) (one 64-KiB chunk each)
+        static int pf_env = [] { const char *e = getenv("QVA_PF"); return e ? atoi(e) : 0; }();  // measured slower (8.3 vs 6.2 ms per pass): off by default
+        tp.psi_in = psi_in;
+        if (pf_env && batch == 1 && tp.init != 1) {
+            const int top = s[kTileBits - 1];
+            const int low = top + 1 - kTileBits;  // coordinate bits below the top tile bit
+            if (low > 0 && top + 1 < n_phys) {
+                tp.pf_shift = top + 1;
+                tp.pf_lowbits = low;
+                tp.pf_nblocks = 1ull << (n_phys - top - 1);
+            }
+        }
+        QVA_TRY(make_tile_tensor_maps(psi_in, tp.psi_out, n_phys, batch, tp, pp.permuted ? pp.obit.data() : nullptr,
+                                      &map, &map_out));
         if (g_trace > 1) {
             fprintf(stderr, "[qva] pass set %d prog %d init %d gq %d expect %d release %d steps:", pp.set, prog, tp.init,
                     tp.gq, tp.expect, tp.release_step);
@@ -818,6 +1033,10 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         }
         first = false;
         ++j;
+        if (swap_after) {
+            std::swap(P->psi, P->psi_alt);
+            psi_base = P->psi;
+        }
         if (pp.expect) {
             ProfScope ps(P, K_REDUCE, 16.0 * nslot * batch);
             QVA_CUDA_TRY(launch_reduce_partials(P->partials, nslot, batch, P->red, P->stream));
@@ -859,6 +1078,17 @@ qva_status expect_generic(qva_plan *P, const double2 *psi, uint64_t n, const dou
 }
 
 bool use_small(const qva_plan *P) { return P->mixer == QVA_MIXER_X && P->n <= kSmallMaxQubits && P->G == 1; }
+
+// permuted out-of-place schedule: single shard, >= 21 qubits
+// (a 9-bit read window above the contiguous tile), room for the ping-pong buffer.
+// QVA_PERM=0 selects the in-place schedule.
+bool use_permuted(const qva_plan *P) {
+    static int env = [] {
+        const char *e = getenv("QVA_PERM");
+        return e ? atoi(e) : 1;
+    }();
+    return env != 0 && P->mixer == QVA_MIXER_X && P->G == 1 && P->L >= 21 && !P->perm_failed;
+}
 
 // apply one mixer on the current state (no phase)
 qva_status apply_mixer_impl(qva_plan *P, double beta) {
@@ -918,6 +1148,7 @@ qva_status reset_state(qva_plan *P) {
         QVA_CUDA_TRY(launch_fill_uniform(P->psi, P->arr_n, 1.0 / sqrt((double)P->N), P->stream));
     }
     P->layout = 0;
+    P->perm.clear();
     return QVA_OK;
 }
 
@@ -1006,6 +1237,34 @@ qva_status qva_x_schedule(int32_t n_local, int32_t p, int32_t *out, int32_t cap,
         out[4 * i + 1] = __builtin_popcount(passes[i].r1);
         out[4 * i + 2] = passes[i].phase >= 0 ? 1 : 0;
         out[4 * i + 3] = __builtin_popcount(passes[i].r2);
+    }
+    return QVA_OK;
+}
+
+qva_status qva_x_schedule_permuted(int32_t n_local, int32_t p, int64_t *out, int32_t cap, int32_t *n_passes) {
+    if (n_local < 21 || n_local > 40 || p < 1 || !n_passes) {
+        set_error("qva_x_schedule_permuted: need 21 <= n_local <= 40 and p >= 1");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    std::vector<int> fin;
+    auto passes = perm_passes(n_local, p, &fin);
+    *n_passes = (int32_t)passes.size();
+    for (int i = 0; i < (int)passes.size() && i < cap; ++i) {
+        const PassPlan &pp = passes[i];
+        int64_t l1 = 0, l2 = 0;
+        for (int k = 0; k < kTileBits; ++k) {
+            if ((pp.r1 >> k) & 1) l1 |= 1ll << pp.lay_in[pp.tbits[k]];
+            if ((pp.r2 >> k) & 1) l2 |= 1ll << pp.lay_in[pp.tbits[k]];
+        }
+        int64_t *o = out + 8 * (size_t)i;
+        o[0] = pp.tbits[3];
+        o[1] = pp.a1;
+        o[2] = pp.a2;
+        o[3] = pp.phase;
+        o[4] = pp.expect ? 1 : 0;
+        o[5] = l1;
+        o[6] = l2;
+        o[7] = tile_tma_dims(pp.tbits.data(), n_local, pp.obit.data());
     }
     return QVA_OK;
 }
@@ -1428,6 +1687,7 @@ qva_status qva_apply_phase(qva_plan *P, double gamma) {
         return QVA_ERR_NOT_READY;
     }
     DeviceGuard dg(P->device);
+    QVA_TRY(to_natural_perm(P));
     if (P->layout == 1) QVA_TRY(ensure_qB(P));
     {
         ProfScope ps(P, K_OTHER, 40.0 * P->arr_n);
@@ -1445,6 +1705,7 @@ qva_status qva_apply_mixer(qva_plan *P, double beta) {
     }
     DeviceGuard dg(P->device);
     P->expect_valid = false;
+    QVA_TRY(to_natural_perm(P));
     QVA_TRY(apply_mixer_impl(P, beta));
     return sync(P);
 }
@@ -1473,8 +1734,27 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
             return QVA_OK;
         }
         P->layout = 0;
+        P->perm.clear();
         if (p == 0) {
             QVA_TRY(reset_state(P));
+            return QVA_OK;
+        }
+        if (use_permuted(P)) {
+            if (!P->psi_alt && cudaMalloc(&P->psi_alt, P->arr_n * sizeof(double2)) != cudaSuccess) {
+                cudaGetLastError();
+                P->perm_failed = true;  // no room for the ping-pong buffer: in-place schedule
+            }
+        }
+        if (use_permuted(P)) {
+            std::vector<int> fin;
+            auto passes = perm_passes(P->L, p, &fin);
+            if (passes.empty() || !passes.back().expect) {
+                set_error("internal: permuted schedule did not complete");
+                return QVA_ERR_UNSUPPORTED;
+            }
+            QVA_TRY(run_passes(P, passes, theta, p, 1, P->psi, 0, P->has_psi0 ? 2 : 1, nullptr));
+            P->perm = fin;
+            *have_red = true;
             return QVA_OK;
         }
         auto passes = cut_passes(evolve_tokens(P->L, P->gbits, p), P->sets, true);
@@ -1562,6 +1842,7 @@ static qva_status expect_now(qva_plan *P) {
         set_error("qualities not set");
         return QVA_ERR_NOT_READY;
     }
+    QVA_TRY(to_natural_perm(P));
     if (P->layout == 1) QVA_TRY(ensure_qB(P));
     double pair[2];
     QVA_TRY(expect_generic(P, P->psi, P->arr_n, q_current(P), pair));
@@ -1601,7 +1882,7 @@ qva_status qva_get_state(qva_plan *P, double *re_im, uint64_t offset, uint64_t c
     uint64_t lo;
     QVA_TRY(check_range(P, offset, count, &lo));
     DeviceGuard dg(P->device);
-    if (P->layout == 1) {
+    if (P->layout == 1 || !P->perm.empty()) {
         bool ev = P->expect_valid;
         QVA_TRY(to_layout_A(P));
         P->expect_valid = ev;
@@ -1617,7 +1898,7 @@ qva_status qva_get_probabilities(qva_plan *P, double *out, uint64_t offset, uint
     QVA_TRY(check_range(P, offset, count, &lo));
     if (!count) return QVA_OK;
     DeviceGuard dg(P->device);
-    if (P->layout == 1) {
+    if (P->layout == 1 || !P->perm.empty()) {
         bool ev = P->expect_valid;
         QVA_TRY(to_layout_A(P));
         P->expect_valid = ev;

@@ -84,6 +84,9 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
+__device__ __forceinline__ void l2_prefetch(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void wg_sync(int wg) { asm volatile("bar.sync %0, %1;" ::"r"(1 + wg), "n"(kCT) : "memory"); }
 
@@ -325,7 +328,15 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const uint64_t n_items = P.n_tiles * (uint64_t)P.batch;
-    const uint32_t n_it = (uint32_t)((n_items > blockIdx.x) ? (n_items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
+    // item order: interleaved (CTA b takes b, b + grid, ...) or blocked (CTA b takes a contiguous
+    // range of items, so its in-flight stages hold neighbouring tiles)
+    const uint64_t per_cta = (n_items + gridDim.x - 1) / gridDim.x;
+    const uint64_t blk_lo = min(n_items, (uint64_t)blockIdx.x * per_cta);
+    const uint32_t n_it = P.order ? (uint32_t)(min(n_items, blk_lo + per_cta) - blk_lo)
+                                  : (uint32_t)((n_items > blockIdx.x) ? (n_items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
+    auto item_of = [&](uint32_t j) -> uint64_t {
+        return P.order ? blk_lo + j : blockIdx.x + (uint64_t)j * gridDim.x;
+    };
     const bool load_psi = (P.init != 1);
     const bool tstore = P.tma_store != 0;  // output through a TMA store of the final smem tile
     const bool load_q = (QB > 0) && (P.gq >= 0);
@@ -336,7 +347,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
 
     // TMA traffic for CTA iteration j (item blockIdx.x + j * gridDim.x)
     auto issue = [&](uint32_t j) {
-        const uint64_t item = blockIdx.x + (uint64_t)j * gridDim.x;
+        const uint64_t item = item_of(j);
         const uint64_t member = item >> P.log2_tiles, t = item & (P.n_tiles - 1);
         const int s = j % STAGES;
         const uint32_t bar = full_bar(j);
@@ -347,6 +358,14 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             tma_load_5d(smem_u32(psi_s + (size_t)s * kTile), &tmap, bar, cc);
         }
         if (qbytes) bulk_load(smem_u32(q_s + (size_t)s * kTile * QB), qt + t * (uint64_t)qbytes, qbytes, bar);
+        // strided tile sets: tile (block b, index c) prefetches the contiguous 64-KiB chunk c of
+        // block b + 1 into L2, so the next block's 128-B rows are L2 hits and DRAM sees
+        // sequential reads
+        if (P.pf_shift) {
+            const uint64_t b = t >> P.pf_lowbits, cidx = t & ((1ull << P.pf_lowbits) - 1);
+            if (b + 1 < P.pf_nblocks)
+                l2_prefetch(P.psi_in + ((b + 1) << P.pf_shift) + (cidx << kTileBits), kTile * sizeof(double2));
+        }
     };
 
     if (tid == 0) {
@@ -376,7 +395,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     int64_t acc_member = -1;
 
     for (uint32_t it = wg; it < n_it; it += kWG) {
-        const uint64_t item = blockIdx.x + (uint64_t)it * gridDim.x;
+        const uint64_t item = item_of(it);
         const int s = it % STAGES;
         const uint64_t member = item >> P.log2_tiles;
         const uint64_t t = item & (P.n_tiles - 1);
@@ -506,11 +525,19 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     if (QB > 0 && kExpect && P.expect && acc_member >= 0) flush_partial(P, acc_member, warp, lane, acc, nrm);
 }
 
+// logical index of physical index x under a layout given as bit runs (LayoutRuns)
+__device__ __forceinline__ uint64_t layout_map(const LayoutRuns &R, uint64_t x) {
+    uint64_t y = 0;
+    for (int r = 0; r < R.n; ++r) y |= ((x >> R.src[r]) & ((1ull << R.w[r]) - 1)) << R.dst[r];
+    return y;
+}
+
 // q (fp64 or integer codes) permuted into the consumer order of register group G of tile set S:
-// dst[t][pos(tid, e)] = src[phys(t, i(tid, e))], pos as read by apply_phase_group/accumulate_expect.
+// dst[t][pos(tid, e)] = src[logical(phys(t, i(tid, e)))], pos as read by apply_phase_group /
+// accumulate_expect; `lay` maps the pass's physical layout to the logical index of q.
 template <typename T>
 __global__ void qt_gather_kernel(T *dst, const T *src, const __grid_constant__ TilePassParams P, TileGroup G,
-                                 uint64_t n_tiles, int qmin) {
+                                 uint64_t n_tiles, int qmin, const __grid_constant__ LayoutRuns lay) {
     const uint64_t total = n_tiles * (uint64_t)kTile;
     constexpr int PER = (sizeof(T) == 8) ? 2 : 16 / (int)sizeof(T);
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
@@ -526,9 +553,18 @@ __global__ void qt_gather_kernel(T *dst, const T *src, const __grid_constant__ T
         uint64_t phys = 0;
         for (int r = 0; r < P.n_runs; ++r) phys |= ((t >> P.run_src[r]) & ((1ull << P.run_w[r]) - 1)) << P.run_dst[r];
         for (int b = 0; b < kTileBits; ++b) phys |= (uint64_t)((i >> b) & 1) << P.tile_bits[b];
-        if (sizeof(T) == 8) dst[k] = src[phys];
-        else dst[k] = (T)((int)src[phys] - qmin);  // integer codes stored as j = code - qmin
+        const uint64_t x = layout_map(lay, phys);
+        if (sizeof(T) == 8) dst[k] = src[x];
+        else dst[k] = (T)((int)src[x] - qmin);  // integer codes stored as j = code - qmin
     }
+}
+
+// out[logical(x)] = in[x] for every physical index x: returns a permuted state to the natural
+// layout (reads are coalesced; writes land in 128-B rows because bits 0..2 never move)
+__global__ void permute_copy_kernel(double2 *__restrict__ out, const double2 *__restrict__ in, uint64_t n,
+                                    const __grid_constant__ LayoutRuns lay) {
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (uint64_t)gridDim.x * blockDim.x)
+        out[layout_map(lay, x)] = in[x];
 }
 
 template <int STAGES, int QB, int PROG>
@@ -590,30 +626,24 @@ int tile_pass_grid(uint64_t items) {
     return (int)std::max<uint64_t>(g, 1);
 }
 
-// Tensor map of one member array (or `batch` consecutive members of member_stride = 2^L
-// elements) seen through tile set P.tile_bits: dims in ascending physical order, each maximal
-// run of tile bits split into <= 8-bit box dims (bits 0-2 = 16 doubles = one 128-B swizzle
-// row), each run of non-tile bits one dim with box 1 (its coordinate comes from the tile
-// number), the member index folded into the topmost non-tile dim.  Fills P.dim_* fields.
-qva_status make_tile_tensor_map(const double2 *psi, int L, int batch, TilePassParams &P, CUtensorMap *map) {
-    EncodeTiledFn enc = encode_fn();
-    if (!enc) {
-        set_error("cuTensorMapEncodeTiled entry point unavailable");
-        return QVA_ERR_CUDA;
-    }
+// TMA dims of a tile pass: maximal runs of input-physical bits that agree in tile membership and
+// map to consecutive output bits under obit; tile runs split into <= 8-bit box dims (bits 0-2 =
+// 16 doubles = one 128-B swizzle row).
+struct TmaDim {
+    int lo, w;
+    bool tile;
+};
+static std::vector<TmaDim> tile_dims(const int *tile_bits, int L, const int *obit) {
     uint64_t tmask = 0;
-    for (int k = 0; k < kTileBits; ++k) tmask |= 1ull << P.tile_bits[k];
-    // dims as (first bit, width, is_tile)
-    struct D {
-        int lo, w;
-        bool tile;
-    };
-    std::vector<D> dims;
+    for (int k = 0; k < kTileBits; ++k) tmask |= 1ull << tile_bits[k];
+    auto ob = [&](int b) { return obit ? obit[b] : b; };
+    std::vector<TmaDim> dims;
     int b = 0;
     while (b < L) {
-        bool tile = (tmask >> b) & 1;
-        int st = b;
-        while (b < L && (((tmask >> b) & 1) != 0) == tile) ++b;
+        const bool tile = (tmask >> b) & 1;
+        const int st = b;
+        ++b;
+        while (b < L && (((tmask >> b) & 1) != 0) == tile && ob(b) == ob(b - 1) + 1) ++b;
         if (tile) {
             int x = st;
             while (x < b) {
@@ -625,8 +655,34 @@ qva_status make_tile_tensor_map(const double2 *psi, int L, int batch, TilePassPa
             dims.push_back({st, b - st, false});
         }
     }
-    if (dims.empty() || !dims[0].tile || dims[0].lo != 0 || dims[0].w != 3) {
-        set_error("tile set must contain physical bits 0,1,2");
+    return dims;
+}
+
+int tile_tma_dims(const int *tile_bits, int L, const int *obit) { return (int)tile_dims(tile_bits, L, obit).size(); }
+
+// Tensor maps of one member array (or `batch` consecutive members of member_stride = 2^L
+// elements) seen through tile set P.tile_bits: dims in ascending input-physical order, each
+// maximal run of tile bits split into <= 8-bit box dims (bits 0-2 = 16 doubles = one 128-B
+// swizzle row), each run of non-tile bits one dim with box 1 (its coordinate comes from the
+// tile number), the member index folded into the topmost non-tile dim.  Fills P.dim_* fields.
+//
+// The load map reads the input layout; the store map writes the same box to psi_out through
+// the bit permutation obit (input physical bit b -> output physical bit obit[b]; nullptr =
+// identity, i.e. an in-place style store).  Runs are additionally split wherever obit is not
+// consecutive, so every dim of the shared box maps to one contiguous output run: a permuted
+// store is still one TMA instruction per tile, with its own strides.
+qva_status make_tile_tensor_maps(const double2 *psi_in, double2 *psi_out, int L, int batch, TilePassParams &P,
+                                 const int *obit, CUtensorMap *map_in, CUtensorMap *map_out) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled entry point unavailable");
+        return QVA_ERR_CUDA;
+    }
+    auto ob = [&](int b) { return obit ? obit[b] : b; };
+    std::vector<TmaDim> dims = tile_dims(P.tile_bits, L, obit);
+    if (dims.empty() || !dims[0].tile || dims[0].lo != 0 || dims[0].w != 3 || ob(0) != 0 || ob(1) != 1 ||
+        ob(2) != 2) {
+        set_error("tile set must contain physical bits 0,1,2 (kept in place by the store map)");
         return QVA_ERR_INVALID_ARGUMENT;
     }
     int member_dim = -1;
@@ -634,29 +690,37 @@ qva_status make_tile_tensor_map(const double2 *psi, int L, int batch, TilePassPa
     if (batch > 1) {
         if (!dims.back().tile) {
             member_dim = (int)dims.size() - 1;
-            member_extra = (uint64_t)batch;
         } else {
             dims.push_back({L, 0, false});
             member_dim = (int)dims.size() - 1;
-            member_extra = (uint64_t)batch;
+        }
+        member_extra = (uint64_t)batch;
+        // the member index is folded into the top dim: its output run must stay at the top
+        const TmaDim &m = dims[member_dim];
+        if (m.w > 0 && ob(m.lo) + m.w != L) {
+            set_error("batched tile pass: permuted store must keep the top run in place");
+            return QVA_ERR_UNSUPPORTED;
         }
     }
     if (dims.size() > 5) {
         set_error("tile set needs more than 5 TMA dimensions");
         return QVA_ERR_UNSUPPORTED;
     }
-    cuuint64_t gdim[5], gstride[4];
+    cuuint64_t gdim[5], gstride[4], gstride_o[4];
     cuuint32_t box[5], estr[5];
     int src = 0;
     for (int d = 0; d < 5; ++d) {
         estr[d] = 1;
         if (d < (int)dims.size()) {
-            const D &x = dims[d];
+            const TmaDim &x = dims[d];
             uint64_t sz = 1ull << x.w;
             if (d == member_dim) sz *= member_extra;
             gdim[d] = (d == 0) ? 2 * sz : sz;  // dim 0 counts doubles (re, im)
             box[d] = x.tile ? (cuuint32_t)((d == 0) ? 2 * sz : sz) : 1;
-            if (d > 0) gstride[d - 1] = (cuuint64_t)(1ull << x.lo) * sizeof(double2);
+            if (d > 0) {
+                gstride[d - 1] = (cuuint64_t)(1ull << x.lo) * sizeof(double2);
+                gstride_o[d - 1] = (cuuint64_t)(1ull << (x.lo < L ? ob(x.lo) : L)) * sizeof(double2);
+            }
             if (x.tile) {
                 P.dim_src[d] = 0;
                 P.dim_w[d] = 0;
@@ -669,22 +733,31 @@ qva_status make_tile_tensor_map(const double2 *psi, int L, int batch, TilePassPa
             gdim[d] = 1;
             box[d] = 1;
             gstride[d - 1] = 16;  // size-1 padding dim: any legal stride
+            gstride_o[d - 1] = 16;
             P.dim_src[d] = 0;
             P.dim_w[d] = 0;
         }
     }
     P.member_dim = member_dim;
     // L2 fill granule: 256 B only when every box row run is >= 256 B contiguous (tile bits 0..3)
-    const bool wide = dims.size() > 1 && dims[1].tile && dims[1].lo == 3;
     static const int promo_env = [] {
         const char *e = getenv("QVA_L2PROMO");
         return e ? atoi(e) : -1;
     }();
-    CUtensorMapL2promotion promo = wide ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-    if (promo_env >= 0 && !wide) promo = (CUtensorMapL2promotion)promo_env;
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2 *>(psi), gdim, gstride, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+    auto promo_for = [&](bool wide) {
+        CUtensorMapL2promotion promo = wide ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+        if (promo_env >= 0 && !wide) promo = (CUtensorMapL2promotion)promo_env;
+        return promo;
+    };
+    const bool wide_in = dims.size() > 1 && dims[1].tile && dims[1].lo == 3;
+    const bool wide_out = dims.size() > 1 && dims[1].tile && ob(dims[1].lo) == 3;
+    CUresult r = enc(map_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2 *>(psi_in), gdim, gstride, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo_for(wide_in),
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS && map_out)
+        r = enc(map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, psi_out, gdim, gstride_o, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo_for(wide_out),
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
         return QVA_ERR_CUDA;
@@ -706,14 +779,21 @@ cudaError_t launch_tile_pass(const CUtensorMap &map, const CUtensorMap &map_out,
 }
 
 cudaError_t launch_qt_gather(void *dst, const void *src, int qbytes, const TilePassParams &p, const TileGroup &g,
-                             uint64_t n_tiles, int qmin, cudaStream_t s) {
+                             uint64_t n_tiles, int qmin, const LayoutRuns &lay, cudaStream_t s) {
     const uint64_t total = n_tiles * (uint64_t)kTile;
     int blocks = (int)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
     if (qbytes == 8)
-        qt_gather_kernel<double><<<blocks, 256, 0, s>>>((double *)dst, (const double *)src, p, g, n_tiles, 0);
+        qt_gather_kernel<double><<<blocks, 256, 0, s>>>((double *)dst, (const double *)src, p, g, n_tiles, 0, lay);
     else if (qbytes == 2)
-        qt_gather_kernel<int16_t><<<blocks, 256, 0, s>>>((int16_t *)dst, (const int16_t *)src, p, g, n_tiles, qmin);
-    else qt_gather_kernel<int8_t><<<blocks, 256, 0, s>>>((int8_t *)dst, (const int8_t *)src, p, g, n_tiles, qmin);
+        qt_gather_kernel<int16_t>
+            <<<blocks, 256, 0, s>>>((int16_t *)dst, (const int16_t *)src, p, g, n_tiles, qmin, lay);
+    else qt_gather_kernel<int8_t><<<blocks, 256, 0, s>>>((int8_t *)dst, (const int8_t *)src, p, g, n_tiles, qmin, lay);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_permute_copy(double2 *out, const double2 *in, uint64_t n, const LayoutRuns &lay, cudaStream_t s) {
+    int blocks = (int)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    permute_copy_kernel<<<blocks, 256, 0, s>>>(out, in, n, lay);
     return cudaGetLastError();
 }
 

@@ -115,6 +115,13 @@ struct TilePassParams {
     int release_step;        // step after whose smem accesses the stage is released (n_steps: after
                              // the expectation; -1: before any step, i.e. init passes without q)
     double amp0;
+    int order;               // tile order: 0 interleaved over CTAs, 1 contiguous range per CTA
+    // L2 block prefetch (strided tile sets, batch 1): tile t = (block t >> pf_lowbits, chunk
+    // c = low bits) prefetches psi_in[((block + 1) << pf_shift) + c * 4096 ...] (64 KiB)
+    const double2 *psi_in;
+    int pf_shift;            // 0: off; else log2(elements per block)
+    int pf_lowbits;
+    uint64_t pf_nblocks;
 };
 
 // Compile-time pass programs (kernels_tile.cu): group sequence g[0..n), which steps rotate,
@@ -139,13 +146,27 @@ constexpr TileProg kTileProgs[kNumTileProgs] = {
 
 int tile_pass_grid(uint64_t items);
 int tile_consumer_warps();
-// builds the 5-D tensor map of psi seen through P.tile_bits (and fills P.dim_*, P.member_dim)
-qva_status make_tile_tensor_map(const double2 *psi, int L, int batch, TilePassParams &P, CUtensorMap *map);
+// builds the 5-D load map of psi_in seen through P.tile_bits and the store map of the same box
+// into psi_out through the bit permutation obit (nullptr: identity); fills P.dim_*, P.member_dim
+// number of TMA dims the maps of (tile_bits, obit) need (must be <= 5; batch 1)
+int tile_tma_dims(const int *tile_bits, int L, const int *obit);
+qva_status make_tile_tensor_maps(const double2 *psi_in, double2 *psi_out, int L, int batch, TilePassParams &P,
+                                 const int *obit, CUtensorMap *map_in, CUtensorMap *map_out);
 // qbytes: 0 (no q), 1 (int8 codes), 2 (int16 codes), 8 (fp64)
 cudaError_t launch_tile_pass(const CUtensorMap &map, const CUtensorMap &map_out, const TilePassParams &p, int qbytes,
                              int prog, int grid, cudaStream_t s);
+// A physical -> logical bit permutation as runs: logical = sum_r ((x >> src_r) & (2^w_r - 1)) << dst_r
+// (the identity is one run).  Used where a state is held in a permuted layout (DESIGN.md
+// "Permuted layouts").
+constexpr int kMaxLayoutRuns = 24;
+struct LayoutRuns {
+    int n;
+    int8_t src[kMaxLayoutRuns], w[kMaxLayoutRuns], dst[kMaxLayoutRuns];
+};
 cudaError_t launch_qt_gather(void *dst, const void *src, int qbytes, const TilePassParams &p, const TileGroup &g,
-                             uint64_t n_tiles, int qmin, cudaStream_t s);
+                             uint64_t n_tiles, int qmin, const LayoutRuns &lay, cudaStream_t s);
+// out[logical(x)] = in[x] (restores the natural layout of a permuted state)
+cudaError_t launch_permute_copy(double2 *out, const double2 *in, uint64_t n, const LayoutRuns &lay, cudaStream_t s);
 // phase tables tab[b][j] = exp(-i gammas[b] (qmin + j)), j < ntab (same fp64 sincos as the
 // per-element path, so integer-valued q give identical factors)
 cudaError_t launch_phase_table(double2 *tab, const double *gammas, int batch, int qmin, int ntab, cudaStream_t s);

@@ -93,6 +93,42 @@ def test_x_schedule_n30_p3(Q):
     assert len(sched) == 7
 
 
+@pytest.mark.parametrize("n,p", [(21, 1), (21, 4), (22, 2), (24, 3), (29, 2), (30, 1), (30, 3), (31, 2), (34, 3)])
+def test_permuted_schedule_order(Q, n, p):
+    """Permuted single-shard schedule: in stream order every logical qubit is rotated exactly once
+    per layer, layer k's rotations come after phase k and before phase k+1 (Eq. qaoa, PAPER.md:185:
+    U_M(beta_k) U_Q(gamma_k), layer 1 first; reading R6), the expectation is fused into the last
+    pass only, and every pass fits the 5 TMA dims of one tensor map."""
+    sched = Q.qva_x_schedule_permuted(n, p)
+    events = []  # ("P", k) / ("R", k, mask) in application order
+    for s in sched:
+        assert s["dims"] <= 5
+        if s["r1"]:
+            events.append(("R", s["a1"], s["r1"]))
+        if s["phase"] >= 0:
+            events.append(("P", s["phase"]))
+        if s["r2"]:
+            events.append(("R", s["a2"], s["r2"]))
+    assert [s["expect"] for s in sched] == [0] * (len(sched) - 1) + [1]
+    layer = -1
+    done = 0
+    for e in events:
+        if e[0] == "P":
+            assert e[1] == layer + 1 and (layer < 0 or done == (1 << n) - 1)
+            layer, done = e[1], 0
+        else:
+            assert e[1] == layer and not (done & e[2])
+            done |= e[2]
+    assert layer == p - 1 and done == (1 << n) - 1
+    # every pass after the first reads the 64-KiB-stride window at bit 12
+    assert sched[0]["window"] == 3 and all(s["window"] == 12 for s in sched[1:])
+
+
+def test_permuted_schedule_n30_p3(Q):
+    """cfg4 keeps 2p+1 = 7 passes in the permuted schedule."""
+    assert len(Q.qva_x_schedule_permuted(30, 3)) == 7
+
+
 def test_plan_create_without_gpu_fails_cleanly(Q):
     import torch
     if torch.cuda.is_available():

@@ -98,7 +98,7 @@ def test_tile_path_p0_and_norm(Q):
         _f_close(P.expectation(), float(np.mean(q)), 1.0)
 
 
-@pytest.mark.parametrize("n", [8, 15])
+@pytest.mark.parametrize("n", [8, 15, 21])
 def test_step_level_phase_and_mixer(Q, n):
     """qva_apply_phase / qva_apply_mixer on an arbitrary initial state vs oracle steps."""
     rng = np.random.default_rng(7 + n)
@@ -122,6 +122,32 @@ def test_step_level_phase_and_mixer(Q, n):
         P.clear_initial_state()
         P.evolve(theta)
         _amp_close(P.get_state(), O.evolve_x(n, q, theta))
+
+
+@pytest.mark.parametrize("n,p", [(21, 2), (23, 3)])
+def test_permuted_layout_roundtrip(Q, n, p):
+    """The single-shard evolution leaves the state in a permuted layout (DESIGN.md "Permuted
+    layouts"); every later call sees the natural layout: probabilities, a step-level phase and
+    mixer on top of the evolved state, <Q> of the result, and a second evolution."""
+    rng = np.random.default_rng(900 + n)
+    u, v = random_regular_graph(n, 3 if n % 2 == 0 else 4, rng)
+    w = rng.uniform(0, 1, len(u))
+    theta = rng.uniform(0, math.pi, 2 * p)
+    q = O.maxcut_q(n, u, v, w)
+    ref = O.evolve_x(n, q, theta)
+    with Q.Plan(1 << n, "x", n_qubits=n) as P:
+        P.set_qualities_maxcut(u, v, w)
+        P.evolve(theta)
+        np.testing.assert_allclose(P.get_probabilities(), np.abs(ref) ** 2, rtol=0, atol=1e-12)
+        P.evolve(theta)
+        P.apply_phase(0.61)
+        r2 = O.phase(ref.copy(), q, 0.61)
+        _f_close(P.expectation(), O.expectation(r2, q))
+        P.evolve(theta)
+        P.apply_mixer(1.3)
+        O.mixer_x(ref, 1.3)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, q))
 
 
 def test_P2_basis_state_closed_form_on_gpu(Q):
