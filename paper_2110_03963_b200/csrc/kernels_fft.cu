@@ -1,17 +1,35 @@
 // kernels_fft.cu -- circulant (QWOA) mixer U(beta) = F^-1 diag(exp(-i beta lambda)) F
 // (Sec. 3; sign reading R3, spectrum indexing R4) by hand-written fp64
-// mixed-radix FFTs on sm_100a.
+// mixed-radix FFTs on sm_100a, for any N (mixed radix when N splits into two 13-smooth
+// factors, Bluestein otherwise).
 //
-// Layout: N = N1 * N2 four-step decomposition, index x = x1*N2 + x2.
-//   COL pass  (one CTA per `cw` adjacent columns x2): [inverse length-N1 FFTs of the previous
-//             layer] -> [phase exp(-i gamma q)] -> [forward length-N1 FFTs, twiddle w_N^{x2 k1}]
-//   ROW pass  (one CTA per row k1): forward length-N2 FFT -> * exp(-i beta lambda)/N ->
-//             inverse length-N2 FFT -> twiddle w_N^{-x2 k1}
-// so one layer costs two passes over the state (plus one final inverse COL pass) and the
-// spectrum lives in "transposed" order: position k1*N2 + k2 holds bin k1 + N1*k2.
-// Each length-n sub-FFT is a Stockham autosort FFT in shared memory with radix 2/3/4/5/7/8/11/13
-// stages (ping-pong buffers), twiddles read from small precomputed tables.
-// N <= 4096: the whole p-layer evolution runs in one CTA ("whole" kernel).
+// Convolution engine.  A length-M circulant product F_M^-1 diag(S) F_M v is computed in the
+// four-step form M = M1 * M2, index x = x1*M2 + x2:
+//   COL pass (one CTA per `cw` adjacent columns x2, 128-B rows):
+//       [inverse length-M1 FFTs of the previous product] -> [elementwise ops at natural
+//       index x] -> [forward length-M1 FFTs, twiddle w_M^{x2 k1}]
+//   ROW pass (one CTA per `rb` rows k1): forward length-M2 FFT -> * S -> inverse length-M2
+//       FFT -> twiddle w_M^{-x2 k1}
+// so consecutive products share their COL passes and one mixer layer costs two passes
+// (plus one final inverse COL pass).  The spectrum S lives in "transposed" order: position
+// k1*M2 + k2 holds bin k1 + M1*k2.
+//
+// Direct path (N = N1*N2 with 13-smooth factors): M = N, S = exp(-i beta lambda)/N, the phase
+// exp(-i gamma q) is the elementwise op of the COL pass.
+//
+// Bluestein path (any N): with chirp c_n = exp(-i pi n^2 / N) (n^2 taken mod 2N in integers),
+// nk = (n^2 + k^2 - (k-n)^2)/2 gives  X_k = c_k sum_n (x_n c_n) conj(c_{k-n}),  and the inverse
+// x_n = conj(c_n) sum_k (X_k conj(c_k)) c_{n-k}: two linear convolutions, computed as cyclic
+// convolutions of length M >= 2N-1 (13-smooth) with the fixed kernel spectra B = F_M b,
+// b_m = conj(c_m) (|m| < N, wrapped), and conj(B) (b is even, so F_M conj(b) = conj(B)).
+// One mixer:  v = pad(psi * c) -> conv(B) -> * exp(-i beta lambda_k)/N on k < N (the c_k
+// factors of X_k and of the inverse's pre-multiply cancel) -> conv(conj B) -> psi = v * conj(c)
+// on n < N.  Between layers conj(c) * phase * c = phase, so a layer is four passes over M.
+//
+// Each length-n sub-FFT runs in shared memory in place: every thread loads the inputs of its
+// radix-R butterflies into registers, the block synchronises, then twiddles, transforms and
+// stores them in Stockham (autosort) order, so one buffer per transform suffices.
+// Direct N <= 4096: the whole p-layer evolution runs in one CTA ("whole" kernel).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,10 +41,11 @@
 
 namespace qva {
 
-constexpr int kMaxSub = 4096;     // largest in-CTA sub-FFT
 constexpr int kMaxStages = 24;
-constexpr int kFftThreads = 256;
-constexpr int kWholeThreads = 512;
+constexpr int kFftThreads = 512;
+constexpr int kMaxCta = 8192;                     // points per CTA transform set
+constexpr int kMaxSub = 8192;                     // longest sub-FFT
+constexpr int kColSmemMax = 200 * 1024;
 
 struct SubFft {
     int n = 1;
@@ -34,35 +53,62 @@ struct SubFft {
     int r[kMaxStages];
     int m[kMaxStages];
     int twoff[kMaxStages];
+    // exact division by multiply-high (divu): magic = ceil(2^32 / d) for d = n / r[s] and m[s]
+    uint64_t nbmag[kMaxStages];
+    uint64_t mmag[kMaxStages];
 };
 
+// x / d for x, d < 2^16 given magic = ceil(2^32 / d): the error magic*d - 2^32 < d keeps
+// x * (magic*d - 2^32) < 2^32, so the quotient is exact
+__host__ __device__ __forceinline__ uint32_t divu(uint32_t x, uint64_t magic) {
+    return (uint32_t)(((uint64_t)x * magic) >> 32);
+}
+inline uint64_t div_magic(uint32_t d) { return ((1ull << 32) + d - 1) / d; }
+
 struct FftPlan {
-    uint64_t N = 0;
+    uint64_t N = 0;          // state length
+    uint64_t M = 0;          // transform length (N direct, >= 2N-1 Bluestein)
     int device = 0;
     bool whole = false;
-    int N1 = 1, N2 = 1;
-    int cw = 2;
+    bool bluestein = false;
+    int M1 = 1, M2 = 1;
+    int cw = 8, rb = 1;
     SubFft col, row;
     double2 *d_tw = nullptr;     // stage twiddle tables (col then row)
     double2 *d_big_lo = nullptr, *d_big_hi = nullptr;
-    int big_shift = 11;          // B = 2^big_shift
+    int big_shift = 11;          // w_M^r = hi[r >> s] * lo[r & (2^s - 1)]
+    double2 *work = nullptr;     // Bluestein: length-M buffer
+    double2 *bhat = nullptr;     // Bluestein: F_M b in transposed order
     double *partials = nullptr;
     int n_partials = 0;
 };
 
 namespace {
 
-// roots of unity exp(-2 pi i j / r) for r = 2..16, offset r*(r-1)/2 - 1
+// roots of unity exp(-2 pi i j / r) for r = 2..16, offset r*(r-1)/2 - 1 (kernels copy them to
+// shared memory, s_roots)
 __constant__ double2 c_roots[160];
+__shared__ double2 s_roots[160];
+__device__ __forceinline__ void load_roots() {
+    for (int i = threadIdx.x; i < 160; i += blockDim.x) s_roots[i] = c_roots[i];
+    __syncthreads();
+}
 
 __host__ __device__ constexpr int root_off(int r) { return r * (r - 1) / 2 - 1; }
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 conj_if(double2 a, bool inv) { return inv ? make_double2(a.x, -a.y) : a; }
+// multiply by -i (forward) or +i (inverse)
+__device__ __forceinline__ double2 mul_mi(double2 a, bool inv) {
+    return inv ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
 
 template <int R>
 __device__ __forceinline__ void dft(double2 (&a)[R], bool inv) {
@@ -73,12 +119,52 @@ __device__ __forceinline__ void dft(double2 (&a)[R], bool inv) {
     } else if constexpr (R == 4) {
         double2 s02 = cadd(a[0], a[2]), d02 = csub(a[0], a[2]);
         double2 s13 = cadd(a[1], a[3]), d13 = csub(a[1], a[3]);
-        // w = -i (forward) or +i (inverse) times d13
-        double2 wd = inv ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x);
+        double2 wd = mul_mi(d13, inv);
         a[0] = cadd(s02, s13);
         a[2] = csub(s02, s13);
         a[1] = cadd(d02, wd);
         a[3] = csub(d02, wd);
+    } else if constexpr (R == 3) {
+        // X1,2 = a0 - (a1+a2)/2 -/+ i (sqrt3/2)(a1 - a2)   (signs flip for the inverse)
+        const double h = 0.86602540378443864676;
+        double2 t1 = cadd(a[1], a[2]);
+        double2 t2 = make_double2(fma(-0.5, t1.x, a[0].x), fma(-0.5, t1.y, a[0].y));
+        double2 d = csub(a[1], a[2]);
+        double2 t3 = mul_mi(make_double2(h * d.x, h * d.y), inv);
+        a[0] = cadd(a[0], t1);
+        a[1] = cadd(t2, t3);
+        a[2] = csub(t2, t3);
+    } else if constexpr (R == 5) {
+        const double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;
+        const double s1 = 0.95105651629515357212, s2 = 0.58778525229247312917;
+        double2 t1 = cadd(a[1], a[4]), t2 = cadd(a[2], a[3]);
+        double2 t3 = csub(a[1], a[4]), t4 = csub(a[2], a[3]);
+        double2 b1 = make_double2(fma(c1, t1.x, fma(c2, t2.x, a[0].x)), fma(c1, t1.y, fma(c2, t2.y, a[0].y)));
+        double2 b2 = make_double2(fma(c2, t1.x, fma(c1, t2.x, a[0].x)), fma(c2, t1.y, fma(c1, t2.y, a[0].y)));
+        double2 d1 = mul_mi(make_double2(fma(s1, t3.x, s2 * t4.x), fma(s1, t3.y, s2 * t4.y)), inv);
+        double2 d2 = mul_mi(make_double2(fma(s2, t3.x, -s1 * t4.x), fma(s2, t3.y, -s1 * t4.y)), inv);
+        a[0] = cadd(a[0], cadd(t1, t2));
+        a[1] = cadd(b1, d1);
+        a[4] = csub(b1, d1);
+        a[2] = cadd(b2, d2);
+        a[3] = csub(b2, d2);
+    } else if constexpr (R == 8) {
+        // radix-2 split into two length-4 DFTs: X_k = E_k + w8^k O_k, X_{k+4} = E_k - w8^k O_k
+        double2 e[4] = {a[0], a[2], a[4], a[6]}, o[4] = {a[1], a[3], a[5], a[7]};
+        dft<4>(e, inv);
+        dft<4>(o, inv);
+        const double h = 0.70710678118654752440;
+        double2 w1 = inv ? make_double2(h, h) : make_double2(h, -h);
+        double2 w3 = inv ? make_double2(-h, h) : make_double2(-h, -h);
+        double2 t0 = o[0], t1 = cmul(o[1], w1), t2 = mul_mi(o[2], inv), t3 = cmul(o[3], w3);
+        a[0] = cadd(e[0], t0);
+        a[4] = csub(e[0], t0);
+        a[1] = cadd(e[1], t1);
+        a[5] = csub(e[1], t1);
+        a[2] = cadd(e[2], t2);
+        a[6] = csub(e[2], t2);
+        a[3] = cadd(e[3], t3);
+        a[7] = csub(e[3], t3);
     } else {
         double2 y[R];
 #pragma unroll
@@ -86,7 +172,7 @@ __device__ __forceinline__ void dft(double2 (&a)[R], bool inv) {
             double2 acc = a[0];
 #pragma unroll
             for (int u = 1; u < R; ++u) {
-                double2 w = conj_if(c_roots[root_off(R) + (t * u) % R], inv);
+                double2 w = conj_if(s_roots[root_off(R) + (t * u) % R], inv);
                 acc = cadd(acc, cmul(a[u], w));
             }
             y[t] = acc;
@@ -96,58 +182,86 @@ __device__ __forceinline__ void dft(double2 (&a)[R], bool inv) {
     }
 }
 
-// One Stockham radix-R stage over `count` independent length-n transforms stored contiguously.
+// butterflies a thread holds per round of a radix-R stage (register budget: <= 16 inputs plus
+// the DFT temporaries at 512 threads x 128 registers)
+__host__ __device__ constexpr int nb_of(int R) {
+    return R == 2 ? 8 : R == 3 ? 5 : R == 4 ? 4 : R == 5 ? 3 : R == 7 ? 2 : 1;
+}
+
+// One Stockham radix-R stage, in place, over `count` independent length-n transforms at
+// `stride` elements apart.  Rounds cover whole transforms (a transform's butterflies read and
+// write only its own elements), each round loads all its inputs into registers, synchronises,
+// then twiddles, transforms and stores.  The host guarantees n / R <= nb_of(R) * blockDim.x.
 template <int R>
-__device__ __forceinline__ void fft_stage(const double2 *__restrict__ in, double2 *__restrict__ out, int n, int count,
-                                          int m, const double2 *__restrict__ tw, bool inv) {
+__device__ __forceinline__ void stage_inplace(double2 *buf, int n, int stride, int count, int m,
+                                              const double2 *__restrict__ tw, bool inv, uint64_t nbmag,
+                                              uint64_t mmag) {
+    constexpr int NB = nb_of(R);
     const int nb = n / R;
-    const int total = nb * count;
-    for (int J = threadIdx.x; J < total; J += blockDim.x) {
-        int f = J / nb;
-        int j = J - f * nb;
-        const double2 *x = in + f * n;
-        double2 *y = out + f * n;
-        int k = j % m;
-        double2 a[R];
+    const int per_round = max(1, (int)divu(NB * blockDim.x, nbmag));
+    for (int f0 = 0; f0 < count; f0 += per_round) {
+        const int total = nb * min(per_round, count - f0);
+        double2 a[NB][R];
 #pragma unroll
-        for (int t = 0; t < R; ++t) a[t] = x[j + t * nb];
-        if (m > 1) {
+        for (int b = 0; b < NB; ++b) {
+            const int J = threadIdx.x + b * blockDim.x;
+            if (J < total) {
+                const int fq = (int)divu(J, nbmag);
+                const int f = f0 + fq, j = J - fq * nb;
+                const double2 *x = buf + f * stride;
 #pragma unroll
-            for (int t = 1; t < R; ++t) a[t] = cmul(a[t], conj_if(__ldg(tw + t * k), inv));
+                for (int t = 0; t < R; ++t) a[b][t] = x[j + t * nb];
+            }
         }
-        dft<R>(a, inv);
-        int o = (j - k) * R + k;
+        __syncthreads();
 #pragma unroll
-        for (int t = 0; t < R; ++t) y[o + t * m] = a[t];
+        for (int b = 0; b < NB; ++b) {
+            const int J = threadIdx.x + b * blockDim.x;
+            if (J < total) {
+                const int fq = (int)divu(J, nbmag);
+                const int f = f0 + fq, j = J - fq * nb;
+                const int k = j - (int)divu(j, mmag) * m;
+                if (m > 1) {
+#pragma unroll
+                    for (int t = 1; t < R; ++t) a[b][t] = cmul(a[b][t], conj_if(__ldg(tw + t * k), inv));
+                }
+                dft<R>(a[b], inv);
+                double2 *y = buf + f * stride;
+                const int o = (j - k) * R + k;
+#pragma unroll
+                for (int t = 0; t < R; ++t) y[o + t * m] = a[b][t];
+            }
+        }
+        __syncthreads();
     }
 }
 
-// runs all stages; data starts in A; returns the buffer holding the result
-__device__ double2 *run_fft(double2 *A, double2 *B, const SubFft &sf, const double2 *tw, int count, bool inv) {
-    double2 *src = A, *dst = B;
-    for (int s = 0; s < sf.ns; ++s) {
-        const double2 *t = tw + sf.twoff[s];
-        switch (sf.r[s]) {
-            case 2: fft_stage<2>(src, dst, sf.n, count, sf.m[s], t, inv); break;
-            case 3: fft_stage<3>(src, dst, sf.n, count, sf.m[s], t, inv); break;
-            case 4: fft_stage<4>(src, dst, sf.n, count, sf.m[s], t, inv); break;
-            case 5: fft_stage<5>(src, dst, sf.n, count, sf.m[s], t, inv); break;
-            case 7: fft_stage<7>(src, dst, sf.n, count, sf.m[s], t, inv); break;
-            case 8: fft_stage<8>(src, dst, sf.n, count, sf.m[s], t, inv); break;
-            case 11: fft_stage<11>(src, dst, sf.n, count, sf.m[s], t, inv); break;
-            case 13: fft_stage<13>(src, dst, sf.n, count, sf.m[s], t, inv); break;
-            default: break;
-        }
-        __syncthreads();
-        double2 *tmp = src;
-        src = dst;
-        dst = tmp;
-    }
-    return src;
+__device__ __forceinline__ void run_fft(double2 *buf, const SubFft &sf, const double2 *tw, int count, int stride, bool inv) {
+    // stages are ordered by radix (factor_radices); one loop per radix keeps the live ranges of
+    // different radices apart (a switch inside one stage loop made ptxas spill ~10 KB)
+    int s = 0;
+#define QVA_RADIX_LOOP(R) \
+    for (; s < sf.ns && sf.r[s] == R; ++s)                                                            \
+        stage_inplace<R>(buf, sf.n, stride, count, sf.m[s], tw + sf.twoff[s], inv, sf.nbmag[s], sf.mmag[s]);
+    QVA_RADIX_LOOP(8)
+    QVA_RADIX_LOOP(4)
+    QVA_RADIX_LOOP(2)
+    QVA_RADIX_LOOP(3)
+    QVA_RADIX_LOOP(5)
+    QVA_RADIX_LOOP(7)
+    QVA_RADIX_LOOP(11)
+    QVA_RADIX_LOOP(13)
+#undef QVA_RADIX_LOOP
+}
+// a call boundary around a whole sub-FFT (used by the small whole-evolution kernel, whose
+// layer loop would otherwise spill ~11 KB per thread)
+__device__ __noinline__ void run_fft_call(double2 *buf, const SubFft &sf, const double2 *tw, int count, int stride,
+                                          bool inv) {
+    run_fft(buf, sf, tw, count, stride, inv);
 }
 
 __device__ __forceinline__ double2 big_twiddle(const double2 *lo, const double2 *hi, int shift, uint64_t r, bool inv) {
-    uint64_t mask = (1ull << shift) - 1;
+    const uint64_t mask = (1ull << shift) - 1;
     double2 w = cmul(__ldg(hi + (r >> shift)), __ldg(lo + (r & mask)));
     return conj_if(w, inv);
 }
@@ -156,6 +270,14 @@ __device__ __forceinline__ double2 phase_mul(double2 a, double qv, double gamma)
     double s, c;
     sincos(gamma * qv, &s, &c);
     return make_double2(fma(c, a.x, s * a.y), fma(c, a.y, -s * a.x));
+}
+
+// Bluestein chirp c_x = exp(-i pi x^2 / N), x^2 reduced mod 2N exactly (x < N < 2^31)
+__device__ __forceinline__ double2 chirp(uint64_t x, uint64_t N) {
+    const uint64_t r = (x * x) % (2 * N);
+    double s, c;
+    sincospi((double)r / (double)N, &s, &c);
+    return make_double2(c, -s);
 }
 
 __device__ __forceinline__ void block_reduce2(double &a, double &b, double *red) {
@@ -182,12 +304,29 @@ __device__ __forceinline__ void block_reduce2(double &a, double &b, double *red)
     }
 }
 
+// elementwise ops of a COL pass, applied at natural index x in this order
+enum : int {
+    OP_CHIRP_CONJ = 1,  // v *= conj(c_x)          (end of a Bluestein mixer)
+    OP_EXPECT = 2,      // accumulate |v|^2 q_x, |v|^2
+    OP_PHASE = 4,       // v *= exp(-i gamma q_x)
+    OP_SPEC = 8,        // v *= exp(-i beta lambda_x) / N   (Bluestein middle)
+    OP_CHIRP = 16,      // v *= c_x                 (start of a Bluestein mixer)
+    OP_MASK = 32,       // v = 0 for x >= N
+};
+
 struct ColArgs {
-    double2 *psi;
+    const double2 *in;
+    uint64_t in_len;         // elements x >= in_len read as 0
+    double2 *out;
+    uint64_t out_len;        // elements x >= out_len are not written
     const double *q;
-    int N1, N2, cw;
-    int init, do_inv, do_phase, do_fwd, do_expect;
-    double amp0, gamma;
+    const double *lam;       // natural-order spectrum for OP_SPEC (nullptr: lam0 / lamc)
+    uint64_t N;              // state length (mask, chirp)
+    int M1, M2, cw, lcw;     // cw = 2^lcw columns per CTA
+    uint64_t m1mag;          // divu magic of M1
+    int init;                // 1: v = amp0 for x < N (no load)
+    int do_inv, do_fwd, ops;
+    double amp0, gamma, beta, lam0, lamc, invN;
     const double2 *tw;
     const double2 *big_lo, *big_hi;
     int big_shift;
@@ -195,39 +334,57 @@ struct ColArgs {
     SubFft sf;
 };
 
-__global__ void __launch_bounds__(kFftThreads) fft_col_kernel(const ColArgs a) {
+__global__ void __launch_bounds__(kFftThreads, 1) fft_col_kernel(const ColArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    load_roots();
     __shared__ double red[2 * (kFftThreads / 32)];
-    const int N1 = a.N1, N2 = a.N2;
+    const int M1 = a.M1, M2 = a.M2;
     const int c0 = blockIdx.x * a.cw;
-    const int cwv = min(a.cw, N2 - c0);
+    const int cwv = min(a.cw, M2 - c0);
+    const int stride = cwv > 1 ? M1 + 1 : M1;  // odd padding: column-major stores are conflict-free
     double2 *A = reinterpret_cast<double2 *>(smem_raw);
-    double2 *B = A + a.cw * N1;
-    const int tot = N1 * cwv;
-    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-        int x1 = idx / cwv, c = idx - x1 * cwv;
-        A[c * N1 + x1] = a.init ? make_double2(a.amp0, 0.0) : a.psi[(uint64_t)x1 * N2 + c0 + c];
+    const int tot = M1 * cwv;
+    const int totw = M1 << a.lcw;  // (x1, c) over the full column width; c >= cwv skipped
+    for (int idx = threadIdx.x; idx < totw; idx += blockDim.x) {
+        const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
+        if (c >= cwv) continue;
+        const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
+        double2 v;
+        if (a.init) v = make_double2(x < a.N ? a.amp0 : 0.0, 0.0);
+        else v = x < a.in_len ? a.in[x] : make_double2(0.0, 0.0);
+        A[c * stride + x1] = v;
     }
     __syncthreads();
-    double2 *cur = A, *oth = B;
-    if (a.do_inv) {
-        cur = run_fft(A, B, a.sf, a.tw, cwv, true);
-        oth = (cur == A) ? B : A;
-    }
-    if (a.do_phase || a.do_expect) {
+    if (a.do_inv) run_fft(A, a.sf, a.tw, cwv, stride, true);
+    const int ops = a.ops;
+    if (ops) {
         double acc = 0.0, nrm = 0.0;
         for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-            int c = idx / N1, x1 = idx - c * N1;
-            uint64_t g = (uint64_t)x1 * N2 + c0 + c;
-            double2 v = cur[idx];
-            if (a.do_expect) {
-                double pr = v.x * v.x + v.y * v.y;
-                acc = fma(pr, __ldg(a.q + g), acc);
-                nrm += pr;
+            const int c = (int)divu(idx, a.m1mag), x1 = idx - c * M1;
+            const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
+            double2 &slot = A[c * stride + x1];
+            double2 v = slot;
+            if ((ops & OP_MASK) && x >= a.N) {
+                v = make_double2(0.0, 0.0);
+            } else {
+                if (ops & OP_CHIRP_CONJ) v = cmulc(v, chirp(x, a.N));
+                if (ops & OP_EXPECT) {
+                    const double pr = v.x * v.x + v.y * v.y;
+                    acc = fma(pr, __ldg(a.q + x), acc);
+                    nrm += pr;
+                }
+                if (ops & OP_PHASE) v = phase_mul(v, __ldg(a.q + x), a.gamma);
+                if (ops & OP_SPEC) {
+                    const double lam = a.lam ? __ldg(a.lam + x) : (x == 0 ? a.lam0 : a.lamc);
+                    double s, cs;
+                    sincos(-a.beta * lam, &s, &cs);
+                    v = cmul(v, make_double2(cs * a.invN, s * a.invN));
+                }
+                if (ops & OP_CHIRP) v = cmul(v, chirp(x, a.N));
             }
-            if (a.do_phase) cur[idx] = phase_mul(v, __ldg(a.q + g), a.gamma);
+            slot = v;
         }
-        if (a.do_expect) {
+        if (ops & OP_EXPECT) {
             block_reduce2(acc, nrm, red);
             if (threadIdx.x == 0) {
                 a.partials[2 * blockIdx.x] = acc;
@@ -237,64 +394,81 @@ __global__ void __launch_bounds__(kFftThreads) fft_col_kernel(const ColArgs a) {
         __syncthreads();
     }
     if (a.do_fwd) {
-        double2 *res = run_fft(cur, oth, a.sf, a.tw, cwv, false);
-        cur = res;
+        run_fft(A, a.sf, a.tw, cwv, stride, false);
         for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-            int c = idx / N1, k1 = idx - c * N1;
-            uint64_t r = ((uint64_t)(c0 + c) * (uint64_t)k1) % ((uint64_t)N1 * N2);
-            cur[idx] = cmul(cur[idx], big_twiddle(a.big_lo, a.big_hi, a.big_shift, r, false));
+            const int c = (int)divu(idx, a.m1mag), k1 = idx - c * M1;
+            const uint64_t r = (uint64_t)(c0 + c) * (uint64_t)k1;  // < M: no reduction needed
+            A[c * stride + k1] = cmul(A[c * stride + k1], big_twiddle(a.big_lo, a.big_hi, a.big_shift, r, false));
         }
         __syncthreads();
     }
-    for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-        int x1 = idx / cwv, c = idx - x1 * cwv;
-        a.psi[(uint64_t)x1 * N2 + c0 + c] = cur[c * N1 + x1];
+    for (int idx = threadIdx.x; idx < totw; idx += blockDim.x) {
+        const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
+        if (c >= cwv) continue;
+        const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
+        if (x < a.out_len) a.out[x] = A[c * stride + x1];
     }
 }
 
 struct RowArgs {
-    double2 *psi;
-    int N1, N2;
-    const double *lambda_perm;  // nullptr -> constant spectrum
-    double2 e0, ec;             // exp(-i beta lam0)/N, exp(-i beta c)/N
-    double beta, invN;
+    double2 *buf;
+    int M1, M2, rb;
+    uint64_t m2mag;             // divu magic of M2
+    int fwd_only;               // 1: forward FFT only (spectrum out, no twiddle)
+    int spec;                   // 0: constant (e0 at bin 0, ec elsewhere); 1: real lambda; 2: complex array
+    const double *lam_perm;     // spec 1: transposed order
+    const double2 *bhat;        // spec 2: transposed order
+    int conj_b;
+    double2 e0, ec;             // spec 0 factors (scale included)
+    double beta, scale;
     const double2 *tw;
     const double2 *big_lo, *big_hi;
     int big_shift;
     SubFft sf;
 };
 
-__global__ void __launch_bounds__(kFftThreads) fft_row_kernel(const RowArgs a) {
+__global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N1 = a.N1, N2 = a.N2;
-    const int k1 = blockIdx.x;
+    load_roots();
+    const int M2 = a.M2;
+    const int k1_0 = blockIdx.x * a.rb;
     double2 *A = reinterpret_cast<double2 *>(smem_raw);
-    double2 *B = A + N2;
-    double2 *row = a.psi + (uint64_t)k1 * N2;
-    for (int i = threadIdx.x; i < N2; i += blockDim.x) A[i] = row[i];
+    double2 *rows = a.buf + (uint64_t)k1_0 * M2;
+    const int tot = a.rb * M2;
+    for (int i = threadIdx.x; i < tot; i += blockDim.x) A[i] = rows[i];
     __syncthreads();
-    double2 *cur = run_fft(A, B, a.sf, a.tw, 1, false);
-    double2 *oth = (cur == A) ? B : A;
-    for (int k2 = threadIdx.x; k2 < N2; k2 += blockDim.x) {
+    run_fft(A, a.sf, a.tw, a.rb, M2, false);
+    if (a.fwd_only) {
+        for (int i = threadIdx.x; i < tot; i += blockDim.x) rows[i] = A[i];
+        return;
+    }
+    for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+        const int r = (int)divu(i, a.m2mag), k2 = i - r * M2;
+        const int k1 = k1_0 + r;
+        const uint64_t pos = (uint64_t)k1 * M2 + k2;
         double2 e;
-        if (a.lambda_perm) {
+        if (a.spec == 1) {
             double s, c;
-            sincos(-a.beta * a.lambda_perm[(uint64_t)k1 * N2 + k2], &s, &c);
-            e = make_double2(c * a.invN, s * a.invN);
+            sincos(-a.beta * __ldg(a.lam_perm + pos), &s, &c);
+            e = make_double2(c * a.scale, s * a.scale);
+        } else if (a.spec == 2) {
+            double2 b = __ldg(a.bhat + pos);
+            e = make_double2(b.x * a.scale, (a.conj_b ? -b.y : b.y) * a.scale);
         } else {
             e = (k1 == 0 && k2 == 0) ? a.e0 : a.ec;
         }
-        cur[k2] = cmul(cur[k2], e);
+        A[i] = cmul(A[i], e);
     }
     __syncthreads();
-    cur = run_fft(cur, oth, a.sf, a.tw, 1, true);
-    for (int x2 = threadIdx.x; x2 < N2; x2 += blockDim.x) {
-        uint64_t r = ((uint64_t)x2 * (uint64_t)k1) % ((uint64_t)N1 * N2);
-        row[x2] = cmul(cur[x2], big_twiddle(a.big_lo, a.big_hi, a.big_shift, r, true));
+    run_fft(A, a.sf, a.tw, a.rb, M2, true);
+    for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+        const int r = (int)divu(i, a.m2mag), x2 = i - r * M2;
+        const uint64_t tr = (uint64_t)x2 * (uint64_t)(k1_0 + r);  // < M
+        rows[i] = cmul(A[i], big_twiddle(a.big_lo, a.big_hi, a.big_shift, tr, true));
     }
 }
 
-// whole evolution of an N <= 4096 state in one CTA
+// whole evolution of a (direct, 13-smooth) N <= 4096 state in one CTA
 struct WholeArgs {
     double2 *psi;
     const double *q;
@@ -308,44 +482,41 @@ struct WholeArgs {
     SubFft sf;
 };
 
-__global__ void __launch_bounds__(kWholeThreads) fft_whole_kernel(const WholeArgs a) {
+__global__ void __launch_bounds__(kFftThreads, 1) fft_whole_kernel(const WholeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ double red[2 * (kWholeThreads / 32)];
+    load_roots();
+    __shared__ double red[2 * (kFftThreads / 32)];
     const int N = a.sf.n;
     double2 *A = reinterpret_cast<double2 *>(smem_raw);
-    double2 *B = A + N;
     for (int i = threadIdx.x; i < N; i += blockDim.x) A[i] = a.init ? make_double2(a.amp0, 0.0) : a.psi[i];
     __syncthreads();
-    double2 *cur = A, *oth = B;
     const int layers = a.mode == 0 ? a.p : 1;
     for (int k = 0; k < layers; ++k) {
         double beta;
         if (a.mode == 0) {
-            double gamma = a.theta[2 * k];
+            const double gamma = a.theta[2 * k];
             beta = a.theta[2 * k + 1];
-            for (int i = threadIdx.x; i < N; i += blockDim.x) cur[i] = phase_mul(cur[i], a.q[i], gamma);
+            for (int i = threadIdx.x; i < N; i += blockDim.x) A[i] = phase_mul(A[i], a.q[i], gamma);
             __syncthreads();
         } else {
             beta = a.theta[0];
         }
-        cur = run_fft(cur, oth, a.sf, a.tw, 1, false);
-        oth = (cur == A) ? B : A;
+        run_fft_call(A, a.sf, a.tw, 1, N, false);
         for (int j = threadIdx.x; j < N; j += blockDim.x) {
-            double lam = a.lambda_perm ? a.lambda_perm[j] : (j == 0 ? a.lam0 : a.lamc);
+            const double lam = a.lambda_perm ? a.lambda_perm[j] : (j == 0 ? a.lam0 : a.lamc);
             double s, c;
             sincos(-beta * lam, &s, &c);
-            cur[j] = cmul(cur[j], make_double2(c * a.invN, s * a.invN));
+            A[j] = cmul(A[j], make_double2(c * a.invN, s * a.invN));
         }
         __syncthreads();
-        cur = run_fft(cur, oth, a.sf, a.tw, 1, true);
-        oth = (cur == A) ? B : A;
+        run_fft_call(A, a.sf, a.tw, 1, N, true);
     }
     double acc = 0.0, nrm = 0.0;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        double2 v = cur[i];
+        const double2 v = A[i];
         a.psi[i] = v;
         if (a.do_expect) {
-            double pr = v.x * v.x + v.y * v.y;
+            const double pr = v.x * v.x + v.y * v.y;
             acc = fma(pr, a.q[i], acc);
             nrm += pr;
         }
@@ -362,6 +533,8 @@ __global__ void __launch_bounds__(kWholeThreads) fft_whole_kernel(const WholeArg
 // ------------------------------------------------------------------------------------------
 // host-side planning
 // ------------------------------------------------------------------------------------------
+const long double kPiL = 3.141592653589793238462643383279502884L;
+
 bool factor_radices(int n, std::vector<int> &rs) {
     rs.clear();
     int x = n;
@@ -376,16 +549,20 @@ bool factor_radices(int n, std::vector<int> &rs) {
 bool make_sub(int n, SubFft &sf, std::vector<double2> &tw) {
     std::vector<int> rs;
     if (n < 1 || n > kMaxSub || !factor_radices(n, rs) || (int)rs.size() > kMaxStages) return false;
+    for (int r : rs)
+        if (n / r > nb_of(r) * kFftThreads) return false;  // one transform per stage round
     sf.n = n;
     sf.ns = (int)rs.size();
     int m = 1;
     for (int s = 0; s < sf.ns; ++s) {
         sf.r[s] = rs[s];
         sf.m[s] = m;
-        int L = m * rs[s];
+        sf.nbmag[s] = div_magic(n / rs[s]);
+        sf.mmag[s] = div_magic(m);
+        const int L = m * rs[s];
         sf.twoff[s] = (int)tw.size();
         for (int j = 0; j < L; ++j) {
-            long double ang = -2.0L * 3.141592653589793238462643383279502884L * (long double)j / (long double)L;
+            const long double ang = -2.0L * kPiL * (long double)j / (long double)L;
             tw.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
         }
         m = L;
@@ -394,21 +571,98 @@ bool make_sub(int n, SubFft &sf, std::vector<double2> &tw) {
 }
 
 bool smooth(uint64_t n) {
+    if (n == 0) return false;
     for (uint64_t p : {2, 3, 5, 7, 11, 13})
         while (n % p == 0) n /= p;
     return n == 1;
+}
+
+struct Split {
+    int M1 = 0, M2 = 0, cw = 0, rb = 1;
+};
+
+// four-step split M = M1 * M2: both 13-smooth, M2 <= kMaxSub, cw * M1 <= kMaxCta and the
+// padded column block fits shared memory; widest column block first (cw = 8: 128-B rows),
+// then the most balanced split
+Split choose_split(uint64_t M) {
+    Split best;
+    double best_score = -1e300;
+    for (uint64_t m1 = 2; m1 <= (uint64_t)kMaxSub && m1 <= M; ++m1) {
+        if (M % m1) continue;
+        const uint64_t m2 = M / m1;
+        if (m2 < 2 || m2 > (uint64_t)kMaxSub || !smooth(m1) || !smooth(m2)) continue;
+        int cw = 0;
+        for (int c : {8, 4, 2, 1})
+            if ((uint64_t)c * m1 <= (uint64_t)kMaxCta && (size_t)c * (m1 + 1) * sizeof(double2) <= kColSmemMax) {
+                cw = c;
+                break;
+            }
+        if (!cw) continue;
+        const double score = 10.0 * cw - fabs(log((double)m1) - log((double)m2));
+        if (score > best_score) {
+            best_score = score;
+            best.M1 = (int)m1;
+            best.M2 = (int)m2;
+            best.cw = cw;
+        }
+    }
+    if (best.M1) {
+        // several short rows per CTA when rows are short
+        best.rb = 1;
+        for (int r = 2; r <= 64; ++r)
+            if (best.M1 % r == 0 && r * best.M2 <= 4096) best.rb = r;
+    }
+    return best;
 }
 
 qva_status upload_roots() {
     std::vector<double2> roots(160, make_double2(0, 0));
     for (int r = 2; r <= 16; ++r)
         for (int j = 0; j < r; ++j) {
-            long double ang = -2.0L * 3.141592653589793238462643383279502884L * j / r;
+            const long double ang = -2.0L * kPiL * j / r;
             roots[root_off(r) + j] = make_double2((double)cosl(ang), (double)sinl(ang));
         }
     QVA_CUDA_TRY(cudaMemcpyToSymbol(c_roots, roots.data(), roots.size() * sizeof(double2)));
     return QVA_OK;
 }
+
+size_t col_smem(const FftPlan *fp) { return (size_t)fp->cw * (fp->M1 + (fp->cw > 1 ? 1 : 0)) * sizeof(double2); }
+size_t row_smem(const FftPlan *fp) { return (size_t)fp->rb * fp->M2 * sizeof(double2); }
+
+// launch helpers shared by planning (Bluestein kernel spectrum) and fft_run
+ColArgs col_args(const FftPlan *fp) {
+    ColArgs c{};
+    c.N = fp->N;
+    c.M1 = fp->M1;
+    c.M2 = fp->M2;
+    c.cw = fp->cw;
+    c.lcw = fp->cw == 8 ? 3 : fp->cw == 4 ? 2 : fp->cw == 2 ? 1 : 0;
+    c.m1mag = div_magic((uint32_t)fp->M1);
+    c.invN = 1.0 / (double)fp->N;
+    c.tw = fp->d_tw;
+    c.big_lo = fp->d_big_lo;
+    c.big_hi = fp->d_big_hi;
+    c.big_shift = fp->big_shift;
+    c.partials = fp->partials;
+    c.sf = fp->col;
+    return c;
+}
+RowArgs row_args(const FftPlan *fp, double2 *buf) {
+    RowArgs w{};
+    w.buf = buf;
+    w.M1 = fp->M1;
+    w.M2 = fp->M2;
+    w.rb = fp->rb;
+    w.m2mag = div_magic((uint32_t)fp->M2);
+    w.tw = fp->d_tw;
+    w.big_lo = fp->d_big_lo;
+    w.big_hi = fp->d_big_hi;
+    w.big_shift = fp->big_shift;
+    w.sf = fp->row;
+    return w;
+}
+int col_grid(const FftPlan *fp) { return (fp->M2 + fp->cw - 1) / fp->cw; }
+int row_grid(const FftPlan *fp) { return fp->M1 / fp->rb; }
 
 }  // namespace
 
@@ -417,85 +671,103 @@ qva_status fft_plan_create(uint64_t N, int device, FftPlan **out) {
     FftPlan *fp = new FftPlan();
     fp->N = N;
     fp->device = device;
+    auto fail = [&](qva_status s, const std::string &msg) {
+        fft_plan_destroy(fp);
+        if (!msg.empty()) set_error(msg);
+        return s;
+    };
     std::vector<double2> tw;
-    if (N <= (uint64_t)kMaxSub && smooth(N)) {
+    if (N <= 4096 && smooth(N)) {
         fp->whole = true;
-        fp->N1 = 1;
-        fp->N2 = (int)N;
-        if (!make_sub((int)N, fp->row, tw)) {
-            delete fp;
-            set_error("FFT planning failed");
-            return QVA_ERR_UNSUPPORTED;
-        }
+        fp->M = N;
+        fp->M1 = 1;
+        fp->M2 = (int)N;
+        if (!make_sub((int)N, fp->row, tw)) return fail(QVA_ERR_UNSUPPORTED, "FFT planning failed");
     } else {
-        // pick N1 <= N2, both <= kMaxSub and 13-smooth, N1 as large as possible (balanced)
-        int best1 = 0;
-        for (uint64_t n1 = 2; n1 <= (uint64_t)kMaxSub && n1 * n1 <= N; ++n1) {
-            if (N % n1) continue;
-            uint64_t n2 = N / n1;
-            if (n2 > (uint64_t)kMaxSub || !smooth(n1) || !smooth(n2)) continue;
-            if (n1 * 2 * 2 * sizeof(double2) > 200 * 1024) continue;  // col smem (cw=2, ping-pong)
-            best1 = (int)n1;
+        Split sp = (N >= 4 && smooth(N)) ? choose_split(N) : Split();
+        if (sp.M1) {
+            fp->M = N;
+        } else {
+            // Bluestein: smallest plannable M >= 2N - 1
+            fp->bluestein = true;
+            uint64_t M = 2 * N - 1;
+            const uint64_t Mmax = (uint64_t)kMaxSub * kMaxSub;
+            for (; M <= Mmax; ++M) {
+                if (!smooth(M)) continue;
+                sp = choose_split(M);
+                if (sp.M1) break;
+            }
+            if (!sp.M1)
+                return fail(QVA_ERR_UNSUPPORTED, "circulant mixer: N=" + std::to_string(N) +
+                                                     " too large for the two-level Bluestein FFT");
+            fp->M = M;
         }
-        if (!best1) {
-            delete fp;
-            set_error("circulant mixer: N=" + std::to_string(N) +
-                      " is not a product N1*N2 of two 13-smooth factors <= 4096 (Bluestein path not built yet)");
-            return QVA_ERR_UNSUPPORTED;
-        }
-        fp->N1 = best1;
-        fp->N2 = (int)(N / best1);
-        fp->cw = 2;
-        if (!make_sub(fp->N1, fp->col, tw) || !make_sub(fp->N2, fp->row, tw)) {
-            delete fp;
-            set_error("FFT planning failed");
-            return QVA_ERR_UNSUPPORTED;
-        }
-        // four-step twiddles w_N^r = hi[r >> s] * lo[r & (2^s - 1)]
-        int s = 11;
-        uint64_t B = 1ull << s;
-        uint64_t nhi = (N + B - 1) / B;
+        fp->M1 = sp.M1;
+        fp->M2 = sp.M2;
+        fp->cw = sp.cw;
+        fp->rb = sp.rb;
+        if (!make_sub(fp->M1, fp->col, tw) || !make_sub(fp->M2, fp->row, tw))
+            return fail(QVA_ERR_UNSUPPORTED, "FFT planning failed");
+        // four-step twiddles w_M^r = hi[r >> s] * lo[r & (2^s - 1)]
+        const int s = 11;
+        const uint64_t B = 1ull << s, M = fp->M;
+        const uint64_t nhi = (M + B - 1) / B;
         std::vector<double2> lo(B), hi(nhi);
         for (uint64_t j = 0; j < B; ++j) {
-            long double ang = -2.0L * 3.141592653589793238462643383279502884L * (long double)j / (long double)N;
+            const long double ang = -2.0L * kPiL * (long double)j / (long double)M;
             lo[j] = make_double2((double)cosl(ang), (double)sinl(ang));
         }
         for (uint64_t j = 0; j < nhi; ++j) {
-            long double ang = -2.0L * 3.141592653589793238462643383279502884L * (long double)((j * B) % N) / (long double)N;
+            const long double ang = -2.0L * kPiL * (long double)((j * B) % M) / (long double)M;
             hi[j] = make_double2((double)cosl(ang), (double)sinl(ang));
         }
         fp->big_shift = s;
         if (cudaMalloc(&fp->d_big_lo, B * sizeof(double2)) != cudaSuccess ||
-            cudaMalloc(&fp->d_big_hi, nhi * sizeof(double2)) != cudaSuccess) {
-            fft_plan_destroy(fp);
-            set_error("cudaMalloc (FFT twiddles) failed");
-            return QVA_ERR_OUT_OF_MEMORY;
-        }
+            cudaMalloc(&fp->d_big_hi, nhi * sizeof(double2)) != cudaSuccess)
+            return fail(QVA_ERR_OUT_OF_MEMORY, "cudaMalloc (FFT twiddles) failed");
         cudaMemcpy(fp->d_big_lo, lo.data(), B * sizeof(double2), cudaMemcpyHostToDevice);
         cudaMemcpy(fp->d_big_hi, hi.data(), nhi * sizeof(double2), cudaMemcpyHostToDevice);
-        fp->n_partials = (fp->N2 + fp->cw - 1) / fp->cw;
-        if (cudaMalloc(&fp->partials, fp->n_partials * 2 * sizeof(double)) != cudaSuccess) {
-            fft_plan_destroy(fp);
-            set_error("cudaMalloc (FFT partials) failed");
-            return QVA_ERR_OUT_OF_MEMORY;
-        }
+        fp->n_partials = col_grid(fp);
+        if (cudaMalloc(&fp->partials, fp->n_partials * 2 * sizeof(double)) != cudaSuccess)
+            return fail(QVA_ERR_OUT_OF_MEMORY, "cudaMalloc (FFT partials) failed");
     }
-    if (cudaMalloc(&fp->d_tw, std::max<size_t>(tw.size(), 1) * sizeof(double2)) != cudaSuccess) {
-        fft_plan_destroy(fp);
-        set_error("cudaMalloc (FFT tables) failed");
-        return QVA_ERR_OUT_OF_MEMORY;
-    }
+    if (cudaMalloc(&fp->d_tw, std::max<size_t>(tw.size(), 1) * sizeof(double2)) != cudaSuccess)
+        return fail(QVA_ERR_OUT_OF_MEMORY, "cudaMalloc (FFT tables) failed");
     cudaMemcpy(fp->d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
     qva_status st = upload_roots();
-    if (st != QVA_OK) {
-        fft_plan_destroy(fp);
-        return st;
+    if (st != QVA_OK) return fail(st, "");
+    cudaFuncSetAttribute(fft_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
+    cudaFuncSetAttribute(fft_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSub * (int)sizeof(double2));
+    cudaFuncSetAttribute(fft_whole_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * (int)sizeof(double2));
+    if (fp->bluestein) {
+        // kernel b_m = conj(c_m) for |m| < N on the length-M circle (b is even), then B = F_M b
+        const uint64_t M = fp->M;
+        std::vector<double2> b(M, make_double2(0.0, 0.0));
+        for (uint64_t m = 0; m < N; ++m) {
+            const uint64_t r = (m * m) % (2 * N);
+            const long double ang = kPiL * (long double)r / (long double)N;
+            const double2 v = make_double2((double)cosl(ang), (double)sinl(ang));  // conj(exp(-i ang))
+            b[m] = v;
+            if (m) b[M - m] = v;
+        }
+        if (cudaMalloc(&fp->bhat, M * sizeof(double2)) != cudaSuccess ||
+            cudaMalloc(&fp->work, M * sizeof(double2)) != cudaSuccess)
+            return fail(QVA_ERR_OUT_OF_MEMORY, "cudaMalloc (Bluestein buffers) failed");
+        cudaMemcpy(fp->bhat, b.data(), M * sizeof(double2), cudaMemcpyHostToDevice);
+        ColArgs c = col_args(fp);
+        c.in = fp->bhat;
+        c.in_len = M;
+        c.out = fp->bhat;
+        c.out_len = M;
+        c.N = M;
+        c.do_fwd = 1;
+        fft_col_kernel<<<col_grid(fp), kFftThreads, col_smem(fp)>>>(c);
+        RowArgs w = row_args(fp, fp->bhat);
+        w.fwd_only = 1;
+        fft_row_kernel<<<row_grid(fp), kFftThreads, row_smem(fp)>>>(w);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return fail(QVA_ERR_CUDA, std::string("Bluestein setup: ") + cudaGetErrorString(e));
     }
-    size_t smem_col = (size_t)2 * fp->cw * fp->N1 * sizeof(double2);
-    size_t smem_row = (size_t)2 * fp->N2 * sizeof(double2);
-    cudaFuncSetAttribute(fft_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem_col, 1));
-    cudaFuncSetAttribute(fft_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_row);
-    cudaFuncSetAttribute(fft_whole_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_row);
     *out = fp;
     return QVA_OK;
 }
@@ -506,21 +778,23 @@ void fft_plan_destroy(FftPlan *fp) {
     cudaFree(fp->d_big_lo);
     cudaFree(fp->d_big_hi);
     cudaFree(fp->partials);
+    cudaFree(fp->work);
+    cudaFree(fp->bhat);
     delete fp;
 }
 
 void fft_permute_spectrum(const FftPlan *fp, const double *lambda, double *lambda_perm) {
-    if (fp->whole) {
+    if (fp->whole || fp->bluestein) {  // consumed in natural order
         memcpy(lambda_perm, lambda, fp->N * sizeof(double));
         return;
     }
-    const uint64_t N1 = fp->N1, N2 = fp->N2;
-    for (uint64_t k1 = 0; k1 < N1; ++k1)
-        for (uint64_t k2 = 0; k2 < N2; ++k2) lambda_perm[k1 * N2 + k2] = lambda[k1 + N1 * k2];
+    const uint64_t M1 = fp->M1, M2 = fp->M2;
+    for (uint64_t k1 = 0; k1 < M1; ++k1)
+        for (uint64_t k2 = 0; k2 < M2; ++k2) lambda_perm[k1 * M2 + k2] = lambda[k1 + M1 * k2];
 }
 
 qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver *obs) {
-    const double N = (double)fp->N;
+    const double N = (double)fp->N, M = (double)fp->M;
     const double state_bytes = 16.0 * N, q_bytes = 8.0 * N;
     if (fp->whole) {
         WholeArgs a{};
@@ -538,14 +812,13 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
         a.red_out = r.red_out;
         a.tw = fp->d_tw;
         a.sf = fp->row;
-        int nth = r.mode == 0 ? 2 * r.p : 1;
+        const int nth = r.mode == 0 ? 2 * r.p : 1;
         double *dth = nullptr;
         QVA_CUDA_TRY(cudaMallocAsync((void **)&dth, std::max(nth, 1) * sizeof(double), s));
         if (nth) QVA_CUDA_TRY(cudaMemcpyAsync(dth, r.theta, nth * sizeof(double), cudaMemcpyHostToDevice, s));
         a.theta = dth;
-        size_t smem = (size_t)2 * fp->N2 * sizeof(double2);
         obs->begin(K_FFT_ROW, state_bytes * (r.init ? 1 : 2) + q_bytes * (r.mode == 0 ? 1 : 0));
-        fft_whole_kernel<<<1, kWholeThreads, smem, s>>>(a);
+        fft_whole_kernel<<<1, kFftThreads, (size_t)fp->N * sizeof(double2), s>>>(a);
         cudaError_t e = cudaGetLastError();
         obs->end();
         cudaFreeAsync(dth, s);
@@ -555,44 +828,36 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
         }
         return QVA_OK;
     }
-    ColArgs c{};
-    c.psi = r.psi;
+    const bool blu = fp->bluestein;
+    double2 *W = blu ? fp->work : r.psi;
+    const uint64_t Mi = fp->M;
+    ColArgs c = col_args(fp);
     c.q = r.q;
-    c.N1 = fp->N1;
-    c.N2 = fp->N2;
-    c.cw = fp->cw;
     c.amp0 = r.amp0;
-    c.tw = fp->d_tw;
-    c.big_lo = fp->d_big_lo;
-    c.big_hi = fp->d_big_hi;
-    c.big_shift = fp->big_shift;
-    c.partials = fp->partials;
-    c.sf = fp->col;
-    RowArgs w{};
-    w.psi = r.psi;
-    w.N1 = fp->N1;
-    w.N2 = fp->N2;
-    w.lambda_perm = r.lambda_perm;
-    w.invN = 1.0 / N;
-    w.tw = fp->d_tw;
-    w.big_lo = fp->d_big_lo;
-    w.big_hi = fp->d_big_hi;
-    w.big_shift = fp->big_shift;
-    w.sf = fp->row;
-    const size_t smem_col = (size_t)2 * fp->cw * fp->N1 * sizeof(double2);
-    const size_t smem_row = (size_t)2 * fp->N2 * sizeof(double2);
-    const int col_grid = (fp->N2 + fp->cw - 1) / fp->cw;
+    c.lam0 = r.lam0;
+    c.lamc = r.lamc;
+    c.lam = blu ? r.lambda_perm : nullptr;
+    const size_t smem_c = col_smem(fp), smem_r = row_smem(fp);
+    const int gc = col_grid(fp), gr = row_grid(fp);
 
-    auto launch_col = [&](int init, int inv, int phase, double gamma, int fwd, int expect) -> qva_status {
+    // in/out: nullptr -> W; the state (r.psi, length N) is named explicitly
+    auto launch_col = [&](const double2 *in, uint64_t in_len, double2 *out, uint64_t out_len, int init, int inv,
+                          int ops, double gamma, double beta, int fwd) -> qva_status {
+        c.in = in;
+        c.in_len = in_len;
+        c.out = out;
+        c.out_len = out_len;
         c.init = init;
         c.do_inv = inv;
-        c.do_phase = phase;
-        c.gamma = gamma;
         c.do_fwd = fwd;
-        c.do_expect = expect;
-        double bytes = state_bytes * (init ? 1 : 2) + q_bytes * ((phase || expect) ? 1 : 0);
+        c.ops = ops;
+        c.gamma = gamma;
+        c.beta = beta;
+        const double bytes = (init ? 0.0 : 16.0 * (double)std::min<uint64_t>(in_len, Mi)) +
+                             16.0 * (double)std::min<uint64_t>(out_len, Mi) +
+                             ((ops & (OP_PHASE | OP_EXPECT)) ? q_bytes : 0.0) + ((ops & OP_SPEC) && c.lam ? 8.0 * N : 0.0);
         obs->begin(K_FFT_COL, bytes);
-        fft_col_kernel<<<col_grid, kFftThreads, smem_col, s>>>(c);
+        fft_col_kernel<<<gc, kFftThreads, smem_c, s>>>(c);
         cudaError_t e = cudaGetLastError();
         obs->end();
         if (e != cudaSuccess) {
@@ -601,17 +866,29 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
         }
         return QVA_OK;
     };
-    auto launch_row = [&](double beta) -> qva_status {
-        w.beta = beta;
-        double s0, c0, s1, c1;
-        s0 = sin(-beta * r.lam0);
-        c0 = cos(-beta * r.lam0);
-        s1 = sin(-beta * r.lamc);
-        c1 = cos(-beta * r.lamc);
-        w.e0 = make_double2(c0 / N, s0 / N);
-        w.ec = make_double2(c1 / N, s1 / N);
-        obs->begin(K_FFT_ROW, state_bytes * 2 + (r.lambda_perm ? 8.0 * N : 0.0));
-        fft_row_kernel<<<fp->N1, kFftThreads, smem_row, s>>>(w);
+    // direct: spectrum exp(-i beta lambda)/N; Bluestein: kernel spectrum B (or conj B) / M
+    auto launch_row = [&](double beta, int bconj) -> qva_status {
+        RowArgs w = row_args(fp, W);
+        double extra = 0.0;
+        if (blu) {
+            w.spec = 2;
+            w.bhat = fp->bhat;
+            w.conj_b = bconj;
+            w.scale = 1.0 / M;
+            extra = 16.0 * M;
+        } else if (r.lambda_perm) {
+            w.spec = 1;
+            w.lam_perm = r.lambda_perm;
+            w.beta = beta;
+            w.scale = 1.0 / N;
+            extra = 8.0 * N;
+        } else {
+            w.spec = 0;
+            w.e0 = make_double2(cos(-beta * r.lam0) / N, sin(-beta * r.lam0) / N);
+            w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
+        }
+        obs->begin(K_FFT_ROW, 32.0 * M + extra);
+        fft_row_kernel<<<gr, kFftThreads, smem_r, s>>>(w);
         cudaError_t e = cudaGetLastError();
         obs->end();
         if (e != cudaSuccess) {
@@ -620,27 +897,55 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
         }
         return QVA_OK;
     };
-    if (r.mode == 1) {
-        QVA_TRY(launch_col(0, 0, 0, 0.0, 1, 0));
-        QVA_TRY(launch_row(r.theta[0]));
-        QVA_TRY(launch_col(0, 1, 0, 0.0, 0, 0));
+    auto reduce = [&]() -> qva_status {
+        obs->begin(K_REDUCE, 16.0 * fp->n_partials);
+        cudaError_t e = launch_reduce_partials(fp->partials, fp->n_partials, 1, r.red_out, s);
+        obs->end();
+        if (e != cudaSuccess) {
+            set_error(std::string("reduce: ") + cudaGetErrorString(e));
+            return QVA_ERR_CUDA;
+        }
+        return QVA_OK;
+    };
+    const uint64_t Nn = fp->N;
+    if (!blu) {
+        if (r.mode == 1) {
+            QVA_TRY(launch_col(r.psi, Nn, r.psi, Nn, 0, 0, 0, 0.0, 0.0, 1));
+            QVA_TRY(launch_row(r.theta[0], 0));
+            return launch_col(r.psi, Nn, r.psi, Nn, 0, 1, 0, 0.0, 0.0, 0);
+        }
+        for (int k = 0; k < r.p; ++k) {
+            QVA_TRY(launch_col(r.psi, Nn, r.psi, Nn, k == 0 ? r.init : 0, k > 0, OP_PHASE, r.theta[2 * k], 0.0, 1));
+            QVA_TRY(launch_row(r.theta[2 * k + 1], 0));
+        }
+        if (r.p > 0) {
+            QVA_TRY(launch_col(r.psi, Nn, r.psi, Nn, 0, 1, r.expect ? OP_EXPECT : 0, 0.0, 0.0, 0));
+            if (r.expect) QVA_TRY(reduce());
+        }
         return QVA_OK;
     }
+    // Bluestein
+    if (r.mode == 1) {
+        QVA_TRY(launch_col(r.psi, Nn, W, Mi, 0, 0, OP_CHIRP | OP_MASK, 0.0, 0.0, 1));
+        QVA_TRY(launch_row(0.0, 0));
+        QVA_TRY(launch_col(W, Mi, W, Mi, 0, 1, OP_SPEC | OP_MASK, 0.0, r.theta[0], 1));
+        QVA_TRY(launch_row(0.0, 1));
+        return launch_col(W, Mi, r.psi, Nn, 0, 1, OP_CHIRP_CONJ | OP_MASK, 0.0, 0.0, 0);
+    }
     for (int k = 0; k < r.p; ++k) {
-        QVA_TRY(launch_col(k == 0 ? r.init : 0, k > 0, 1, r.theta[2 * k], 1, 0));
-        QVA_TRY(launch_row(r.theta[2 * k + 1]));
+        if (k == 0) {
+            QVA_TRY(launch_col(r.psi, Nn, W, Mi, r.init, 0, OP_PHASE | OP_CHIRP | OP_MASK, r.theta[0], 0.0, 1));
+        } else {
+            // conj(c) * phase * c = phase
+            QVA_TRY(launch_col(W, Mi, W, Mi, 0, 1, OP_PHASE | OP_MASK, r.theta[2 * k], 0.0, 1));
+        }
+        QVA_TRY(launch_row(0.0, 0));
+        QVA_TRY(launch_col(W, Mi, W, Mi, 0, 1, OP_SPEC | OP_MASK, 0.0, r.theta[2 * k + 1], 1));
+        QVA_TRY(launch_row(0.0, 1));
     }
     if (r.p > 0) {
-        QVA_TRY(launch_col(0, 1, 0, 0.0, 0, r.expect ? 1 : 0));
-        if (r.expect) {
-            obs->begin(K_REDUCE, 16.0 * fp->n_partials);
-            cudaError_t e = launch_reduce_partials(fp->partials, fp->n_partials, 1, r.red_out, s);
-            obs->end();
-            if (e != cudaSuccess) {
-                set_error(std::string("reduce: ") + cudaGetErrorString(e));
-                return QVA_ERR_CUDA;
-            }
-        }
+        QVA_TRY(launch_col(W, Mi, r.psi, Nn, 0, 1, OP_CHIRP_CONJ | OP_MASK | (r.expect ? OP_EXPECT : 0), 0.0, 0.0, 0));
+        if (r.expect) QVA_TRY(reduce());
     }
     return QVA_OK;
 }

@@ -224,9 +224,10 @@ def test_cfg3_full(Q):
         _amp_close(P.get_state(), ref)
 
 
-@pytest.mark.parametrize("N", [2, 7, 13, 96, 720, 1001, 4096, 5040, 6144])
+@pytest.mark.parametrize("N", [2, 7, 13, 17, 96, 97, 720, 1001, 1009, 4096, 4099, 5040, 6144, 8198, 10007])
 def test_circulant_random_spectrum_vs_dense(Q, N):
-    """Generic real spectrum: whole-CTA kernel (N <= 4096) and four-step (N > 4096)."""
+    """Generic real spectrum: whole-CTA kernel (13-smooth N <= 4096), four-step mixed radix
+    (N = N1*N2 13-smooth) and Bluestein (any other N: 17, 97, 1009, 4099, 8198 = 2*4099, 10007)."""
     rng = np.random.default_rng(N)
     q = rng.standard_normal(N)
     lam = rng.standard_normal(N) * 4
@@ -242,6 +243,22 @@ def test_circulant_random_spectrum_vs_dense(Q, N):
         P.reset_state()
         P.apply_mixer(0.9)
         _amp_close(P.get_state(), O.mixer_circulant_dense(O.init_uniform(N), lam, 0.9))
+
+
+@pytest.mark.parametrize("N", [65537, 362881, 1000003])
+def test_bluestein_complete_graph_vs_closed_form(Q, N):
+    """Bluestein at large non-smooth N against the K_N-Laplacian closed form (reading R5):
+    65537 (prime 2^16+1), 9!+1 = 362881 (= 19 * 71 * 269), 1000003 (prime)."""
+    rng = np.random.default_rng(N)
+    q = rng.standard_normal(N)
+    theta = rng.uniform(0, math.pi, 6)
+    ref = O.evolve_complete(q, theta, 0.0, float(N))
+    with Q.Plan(N, "circulant") as P:
+        P.set_qualities(q)
+        P.set_circulant_eigenvalues_const(0.0, float(N))
+        P.evolve(theta)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+        _amp_close(P.get_state(), ref)
 
 
 # ---------------------------------------------------------------- cfg4 full size ----
