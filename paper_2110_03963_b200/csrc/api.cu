@@ -1269,6 +1269,22 @@ qva_status qva_x_schedule_permuted(int32_t n_local, int32_t p, int64_t *out, int
     return QVA_OK;
 }
 
+qva_status qva_circulant_plan_shape(uint64_t dim, int64_t *out) {
+    if (!out) return QVA_ERR_INVALID_ARGUMENT;
+    const FftShape sh = fft_plan_shape(dim);
+    out[0] = sh.ok ? (sh.whole ? 0 : (sh.bluestein ? 2 : 1)) : -1;
+    out[1] = (int64_t)sh.M;
+    out[2] = sh.M1;
+    out[3] = sh.M2;
+    out[4] = sh.cw;
+    out[5] = sh.rb;
+    if (!sh.ok) {
+        set_error("no FFT plan for dim " + std::to_string(dim));
+        return QVA_ERR_UNSUPPORTED;
+    }
+    return QVA_OK;
+}
+
 qva_status qva_nccl_unique_id(void *id_out) {
     if (!id_out) return QVA_ERR_INVALID_ARGUMENT;
     ncclUniqueId id;

@@ -110,6 +110,55 @@ __device__ __forceinline__ double2 mul_mi(double2 a, bool inv) {
     return inv ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
 }
 
+// cos / sin (2 pi j / N) for the two-level radix-16 and radix-9 butterflies (compile-time
+// constants: indices are unrolled, so they fold into immediates)
+__host__ __device__ constexpr double tw_cos(int N, int j) {
+    constexpr double c16[16] = {1.0, 0.9238795325112867, 0.7071067811865476, 0.38268343236508984, 6.123233995736766e-17, -0.3826834323650897, -0.7071067811865475, -0.9238795325112867, -1.0, -0.9238795325112868, -0.7071067811865477, -0.38268343236509034, -1.8369701987210297e-16, 0.38268343236509, 0.7071067811865474, 0.9238795325112865};
+    constexpr double c9[9] = {1.0, 0.766044443118978, 0.17364817766693041, -0.4999999999999998, -0.9396926207859083, -0.9396926207859084, -0.5000000000000004, 0.17364817766692997, 0.7660444431189778};
+    return N == 16 ? c16[j] : c9[j];
+}
+__host__ __device__ constexpr double tw_sin(int N, int j) {
+    constexpr double s16[16] = {0.0, 0.3826834323650898, 0.7071067811865475, 0.9238795325112867, 1.0, 0.9238795325112867, 0.7071067811865476, 0.3826834323650899, 1.2246467991473532e-16, -0.38268343236508967, -0.7071067811865475, -0.9238795325112865, -1.0, -0.9238795325112866, -0.7071067811865477, -0.3826834323650904};
+    constexpr double s9[9] = {0.0, 0.6427876096865393, 0.984807753012208, 0.8660254037844387, 0.3420201433256689, -0.34202014332566866, -0.8660254037844384, -0.9848077530122081, -0.6427876096865396};
+    return N == 16 ? s16[j] : s9[j];
+}
+
+template <int R>
+__device__ __forceinline__ void dft(double2 (&a)[R], bool inv);
+
+// length P*Q DFT as P-point DFTs over n1 (n = Q n1 + n2), twiddles w_PQ^{n2 k1}, Q-point DFTs over
+// n2; output index k = k1 + P k2
+template <int P, int Q>
+__device__ __forceinline__ void dft_pq(double2 (&a)[P * Q], bool inv) {
+    double2 y[Q][P];
+#pragma unroll
+    for (int n2 = 0; n2 < Q; ++n2) {
+        double2 t[P];
+#pragma unroll
+        for (int n1 = 0; n1 < P; ++n1) t[n1] = a[Q * n1 + n2];
+        dft<P>(t, inv);
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) y[n2][k1] = t[k1];
+    }
+#pragma unroll
+    for (int n2 = 1; n2 < Q; ++n2)
+#pragma unroll
+        for (int k1 = 1; k1 < P; ++k1) {
+            const int j = n2 * k1;
+            const double wc = tw_cos(P * Q, j), ws = tw_sin(P * Q, j);
+            y[n2][k1] = cmul(y[n2][k1], make_double2(wc, inv ? ws : -ws));
+        }
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) {
+        double2 t[Q];
+#pragma unroll
+        for (int n2 = 0; n2 < Q; ++n2) t[n2] = y[n2][k1];
+        dft<Q>(t, inv);
+#pragma unroll
+        for (int k2 = 0; k2 < Q; ++k2) a[k1 + P * k2] = t[k2];
+    }
+}
+
 template <int R>
 __device__ __forceinline__ void dft(double2 (&a)[R], bool inv) {
     if constexpr (R == 2) {
@@ -148,6 +197,10 @@ __device__ __forceinline__ void dft(double2 (&a)[R], bool inv) {
         a[4] = csub(b1, d1);
         a[2] = cadd(b2, d2);
         a[3] = csub(b2, d2);
+    } else if constexpr (R == 16) {
+        dft_pq<4, 4>(a, inv);
+    } else if constexpr (R == 9) {
+        dft_pq<3, 3>(a, inv);
     } else if constexpr (R == 8) {
         // radix-2 split into two length-4 DFTs: X_k = E_k + w8^k O_k, X_{k+4} = E_k - w8^k O_k
         double2 e[4] = {a[0], a[2], a[4], a[6]}, o[4] = {a[1], a[3], a[5], a[7]};
@@ -185,7 +238,7 @@ __device__ __forceinline__ void dft(double2 (&a)[R], bool inv) {
 // butterflies a thread holds per round of a radix-R stage (register budget: <= 16 inputs plus
 // the DFT temporaries at 512 threads x 128 registers)
 __host__ __device__ constexpr int nb_of(int R) {
-    return R == 2 ? 8 : R == 3 ? 5 : R == 4 ? 4 : R == 5 ? 3 : R == 7 ? 2 : 1;
+    return R == 2 ? 8 : R == 3 ? 5 : R == 4 ? 4 : R == 5 ? 3 : R == 7 ? 2 : 1;  // 8, 9, 11, 13, 16: 1
 }
 
 // One Stockham radix-R stage, in place, over `count` independent length-n transforms at
@@ -243,9 +296,11 @@ __device__ __forceinline__ void run_fft(double2 *buf, const SubFft &sf, const do
 #define QVA_RADIX_LOOP(R) \
     for (; s < sf.ns && sf.r[s] == R; ++s)                                                            \
         stage_inplace<R>(buf, sf.n, stride, count, sf.m[s], tw + sf.twoff[s], inv, sf.nbmag[s], sf.mmag[s]);
+    QVA_RADIX_LOOP(16)
     QVA_RADIX_LOOP(8)
     QVA_RADIX_LOOP(4)
     QVA_RADIX_LOOP(2)
+    QVA_RADIX_LOOP(9)
     QVA_RADIX_LOOP(3)
     QVA_RADIX_LOOP(5)
     QVA_RADIX_LOOP(7)
@@ -537,13 +592,21 @@ const long double kPiL = 3.141592653589793238462643383279502884L;
 
 bool factor_radices(int n, std::vector<int> &rs) {
     rs.clear();
+    // order must match run_fft's radix loops: 16, 8, 4, 2, 9, 3, 5, 7, 11, 13
     int x = n;
-    while (x % 8 == 0) { rs.push_back(8); x /= 8; }
-    while (x % 4 == 0) { rs.push_back(4); x /= 4; }
-    while (x % 2 == 0) { rs.push_back(2); x /= 2; }
-    for (int p : {3, 5, 7, 11, 13})
+    for (int p : {16, 8, 4, 2, 9, 3, 5, 7, 11, 13})
         while (x % p == 0) { rs.push_back(p); x /= p; }
     return x == 1;
+}
+
+// a length-n sub-FFT is plannable: 13-smooth, <= kMaxSub, and every stage's butterflies of one
+// transform fit one register round (n / r <= nb_of(r) * threads)
+bool sub_ok(int n) {
+    std::vector<int> rs;
+    if (n < 1 || n > kMaxSub || !factor_radices(n, rs) || (int)rs.size() > kMaxStages) return false;
+    for (int r : rs)
+        if (n / r > nb_of(r) * kFftThreads) return false;
+    return true;
 }
 
 bool make_sub(int n, SubFft &sf, std::vector<double2> &tw) {
@@ -590,7 +653,7 @@ Split choose_split(uint64_t M) {
     for (uint64_t m1 = 2; m1 <= (uint64_t)kMaxSub && m1 <= M; ++m1) {
         if (M % m1) continue;
         const uint64_t m2 = M / m1;
-        if (m2 < 2 || m2 > (uint64_t)kMaxSub || !smooth(m1) || !smooth(m2)) continue;
+        if (m2 < 2 || m2 > (uint64_t)kMaxSub || !sub_ok((int)m1) || !sub_ok((int)m2)) continue;
         int cw = 0;
         for (int c : {8, 4, 2, 1})
             if ((uint64_t)c * m1 <= (uint64_t)kMaxCta && (size_t)c * (m1 + 1) * sizeof(double2) <= kColSmemMax) {
@@ -598,7 +661,16 @@ Split choose_split(uint64_t M) {
                 break;
             }
         if (!cw) continue;
-        const double score = 10.0 * cw - fabs(log((double)m1) - log((double)m2));
+        // wave quantisation on 148 SMs (one 512-thread CTA per SM): fraction of CTA slots used
+        auto wave_eff = [](uint64_t blocks) {
+            const uint64_t w = (blocks + 147) / 148;
+            return (double)blocks / (double)(w * 148);
+        };
+        int rb = 1;
+        for (int r = 2; r <= 64; ++r)
+            if (m1 % r == 0 && (uint64_t)r * m2 <= (uint64_t)kMaxCta) rb = r;
+        const double eff = 0.5 * (wave_eff((m2 + cw - 1) / cw) + wave_eff(m1 / rb));
+        const double score = 10.0 * cw + 8.0 * eff - 0.5 * fabs(log((double)m1) - log((double)m2));
         if (score > best_score) {
             best_score = score;
             best.M1 = (int)m1;
@@ -610,7 +682,7 @@ Split choose_split(uint64_t M) {
         // several short rows per CTA when rows are short
         best.rb = 1;
         for (int r = 2; r <= 64; ++r)
-            if (best.M1 % r == 0 && r * best.M2 <= 4096) best.rb = r;
+            if (best.M1 % r == 0 && r * best.M2 <= kMaxCta) best.rb = r;
     }
     return best;
 }
@@ -666,6 +738,41 @@ int row_grid(const FftPlan *fp) { return fp->M1 / fp->rb; }
 
 }  // namespace
 
+// Pure host planning (no device resources): whole-CTA, direct four-step or Bluestein, and the
+// split.  Exposed through qva_circulant_plan_shape for CPU tests.
+FftShape fft_plan_shape(uint64_t N) {
+    FftShape sh;
+    sh.N = N;
+    if (N >= 1 && N <= 4096 && smooth(N) && sub_ok((int)N)) {
+        sh.ok = true;
+        sh.whole = true;
+        sh.M = N;
+        sh.M1 = 1;
+        sh.M2 = (int)N;
+        return sh;
+    }
+    if (N < 2) return sh;
+    Split sp = (N >= 4 && smooth(N)) ? choose_split(N) : Split();
+    uint64_t M = N;
+    if (!sp.M1) {
+        sh.bluestein = true;
+        const uint64_t Mmax = (uint64_t)kMaxSub * kMaxSub;
+        for (M = 2 * N - 1; M <= Mmax; ++M) {
+            if (!smooth(M)) continue;
+            sp = choose_split(M);
+            if (sp.M1) break;
+        }
+        if (!sp.M1) return sh;
+    }
+    sh.ok = true;
+    sh.M = M;
+    sh.M1 = sp.M1;
+    sh.M2 = sp.M2;
+    sh.cw = sp.cw;
+    sh.rb = sp.rb;
+    return sh;
+}
+
 qva_status fft_plan_create(uint64_t N, int device, FftPlan **out) {
     *out = nullptr;
     FftPlan *fp = new FftPlan();
@@ -677,35 +784,20 @@ qva_status fft_plan_create(uint64_t N, int device, FftPlan **out) {
         return s;
     };
     std::vector<double2> tw;
-    if (N <= 4096 && smooth(N)) {
-        fp->whole = true;
-        fp->M = N;
-        fp->M1 = 1;
-        fp->M2 = (int)N;
+    const FftShape sh = fft_plan_shape(N);
+    if (!sh.ok)
+        return fail(QVA_ERR_UNSUPPORTED, "circulant mixer: no FFT plan for N=" + std::to_string(N) +
+                                             " (Bluestein length would exceed 8192^2)");
+    fp->whole = sh.whole;
+    fp->bluestein = sh.bluestein;
+    fp->M = sh.M;
+    fp->M1 = sh.M1;
+    fp->M2 = sh.M2;
+    fp->cw = sh.cw;
+    fp->rb = sh.rb;
+    if (fp->whole) {
         if (!make_sub((int)N, fp->row, tw)) return fail(QVA_ERR_UNSUPPORTED, "FFT planning failed");
     } else {
-        Split sp = (N >= 4 && smooth(N)) ? choose_split(N) : Split();
-        if (sp.M1) {
-            fp->M = N;
-        } else {
-            // Bluestein: smallest plannable M >= 2N - 1
-            fp->bluestein = true;
-            uint64_t M = 2 * N - 1;
-            const uint64_t Mmax = (uint64_t)kMaxSub * kMaxSub;
-            for (; M <= Mmax; ++M) {
-                if (!smooth(M)) continue;
-                sp = choose_split(M);
-                if (sp.M1) break;
-            }
-            if (!sp.M1)
-                return fail(QVA_ERR_UNSUPPORTED, "circulant mixer: N=" + std::to_string(N) +
-                                                     " too large for the two-level Bluestein FFT");
-            fp->M = M;
-        }
-        fp->M1 = sp.M1;
-        fp->M2 = sp.M2;
-        fp->cw = sp.cw;
-        fp->rb = sp.rb;
         if (!make_sub(fp->M1, fp->col, tw) || !make_sub(fp->M2, fp->row, tw))
             return fail(QVA_ERR_UNSUPPORTED, "FFT planning failed");
         // four-step twiddles w_M^r = hi[r >> s] * lo[r & (2^s - 1)]

@@ -225,6 +225,12 @@ struct LaunchObserver {
 // circulant (FFT) mixer (kernels_fft.cu)
 // ---------------------------------------------------------------------------------------------
 struct FftPlan;  // opaque, defined in kernels_fft.cu
+struct FftShape {
+    bool ok = false, whole = false, bluestein = false;
+    uint64_t N = 0, M = 0;   // state length, transform length
+    int M1 = 0, M2 = 0, cw = 0, rb = 0;
+};
+FftShape fft_plan_shape(uint64_t N);
 qva_status fft_plan_create(uint64_t N, int device, FftPlan **out);
 void fft_plan_destroy(FftPlan *fp);
 // permute lambda (forward-bin order, length N) into the plan's internal spectral order

@@ -4,6 +4,7 @@ schedule) is right."""
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -127,6 +128,34 @@ def test_permuted_schedule_order(Q, n, p):
 def test_permuted_schedule_n30_p3(Q):
     """cfg4 keeps 2p+1 = 7 passes in the permuted schedule."""
     assert len(Q.qva_x_schedule_permuted(30, 3)) == 7
+
+
+def _smooth13(m):
+    for p in (2, 3, 5, 7, 11, 13):
+        while m % p == 0:
+            m //= p
+    return m == 1
+
+
+def test_circulant_plan_shapes(Q):
+    """Every N gets an FFT plan (Sec. 3; north_star (c): arbitrary N): 13-smooth
+    N <= 4096 run whole in one CTA, N = N1*N2 with 13-smooth factors <= 8192 use the four-step
+    mixed-radix form, anything else Bluestein with a 13-smooth length M >= 2N - 1."""
+    rng = np.random.default_rng(5)
+    Ns = list(range(1, 300)) + [4096, 4097, 4099, 5040, 6144, 8191, 8192, 3628800, 65537, 1000003,
+                                362881, 2 ** 22, 3 ** 13, 10 ** 7] + [int(x) for x in rng.integers(300, 4_000_000, 40)]
+    for N in Ns:
+        sh = Q.qva_circulant_plan_shape(N)
+        assert sh["kind"] in (0, 1, 2), (N, sh)
+        if sh["kind"] == 0:
+            assert N <= 4096 and _smooth13(N) and sh["M"] == N
+            continue
+        assert sh["M1"] * sh["M2"] == sh["M"] and _smooth13(sh["M1"]) and _smooth13(sh["M2"])
+        assert sh["M2"] <= 8192 and sh["cw"] in (1, 2, 4, 8) and sh["M1"] % sh["rb"] == 0
+        if sh["kind"] == 1:
+            assert sh["M"] == N and _smooth13(N)
+        else:
+            assert sh["M"] >= 2 * N - 1
 
 
 def test_plan_create_without_gpu_fails_cleanly(Q):
