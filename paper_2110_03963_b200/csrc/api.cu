@@ -451,6 +451,20 @@ struct qva_plan {
     };
     std::vector<QtEntry> qt_cache;
     int layout = 0;
+    // MaxCut graph of qva_set_qualities_maxcut: q_x = -cut_w(x) is generated inside the tile passes
+    // from per-tile records; the fp64 vector q is materialised
+    // on demand only (q_dev_valid)
+    bool q_graph = false, q_dev_valid = true;
+    int g_m = 0;
+    bool g_unit = true;
+    std::vector<int> g_u, g_v;
+    std::vector<double> g_w;
+    struct GenEntry {
+        std::vector<int> key;
+        int group, mode;
+        void *rec, *thr, *G;
+    };
+    std::vector<GenEntry> gen_cache;
     // permuted layout of the single-shard state (physical bit -> logical qubit); empty = natural
     std::vector<int> perm;
     bool perm_failed = false;
@@ -629,6 +643,7 @@ qva_status exchange_buffers(qva_plan *P, T *src, T *dst) {
     return QVA_OK;
 }
 
+qva_status ensure_q_dev(qva_plan *P);
 qva_status exchange_state(qva_plan *P) {
     QVA_TRY(exchange_buffers<double2>(P, P->psi, P->psi_alt));
     std::swap(P->psi, P->psi_alt);
@@ -639,6 +654,7 @@ qva_status exchange_state(qva_plan *P) {
 qva_status ensure_qB(qva_plan *P) {
     if (P->G == 1) return QVA_OK;
     if (!P->qB_valid) {
+        QVA_TRY(ensure_q_dev(P));
         if (!P->qB) QVA_CUDA_TRY(cudaMalloc(&P->qB, P->arr_n * sizeof(double)));
         QVA_TRY(exchange_buffers<double>(P, P->q, P->qB));
         P->qB_valid = true;
@@ -672,11 +688,13 @@ qva_status ensure_qB(qva_plan *P) {
 // Classify q after an upload: integer-valued within int8/int16 range -> compact codes + phase
 // tables (exact: the table entry for k is the same fp64 sincos of fl(gamma*k)).
 void drop_qt(qva_plan *P);
+qva_status ensure_q_dev(qva_plan *P);
 qva_status classify_q(qva_plan *P) {
     drop_qt(P);
     P->q_mode = 0;
     P->qcB_valid = false;
     if (P->mixer != QVA_MIXER_X || P->L < kTileBits) return QVA_OK;
+    QVA_TRY(ensure_q_dev(P));
     int blocks = q_range_blocks(P->arr_n);
     double *mm = nullptr;
     QVA_CUDA_TRY(cudaMallocAsync((void **)&mm, 2 * blocks * sizeof(double), P->stream));
@@ -740,6 +758,39 @@ qva_status to_layout_A(qva_plan *P) {
 void drop_qt(qva_plan *P) {
     for (auto &e : P->qt_cache) cudaFree(e.buf);
     P->qt_cache.clear();
+    for (auto &e : P->gen_cache) {
+        cudaFree(e.rec);
+        cudaFree(e.thr);
+        cudaFree(e.G);
+    }
+    P->gen_cache.clear();
+}
+
+// fp64 q of a graph-defined plan, generated on demand (maxcut_q_kernel, 8 B per amplitude)
+qva_status ensure_q_dev(qva_plan *P) {
+    if (!P->q_graph || P->q_dev_valid) return QVA_OK;
+    const int m = P->g_m;
+    int32_t *du = nullptr, *dv = nullptr;
+    double *dw = nullptr;
+    const size_t me = m > 0 ? m : 1;
+    QVA_CUDA_TRY(cudaMallocAsync((void **)&du, me * sizeof(int32_t), P->stream));
+    QVA_CUDA_TRY(cudaMallocAsync((void **)&dv, me * sizeof(int32_t), P->stream));
+    if (m) QVA_CUDA_TRY(cudaMemcpyAsync(du, P->g_u.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice, P->stream));
+    if (m) QVA_CUDA_TRY(cudaMemcpyAsync(dv, P->g_v.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice, P->stream));
+    if (!P->g_unit) {
+        QVA_CUDA_TRY(cudaMallocAsync((void **)&dw, me * sizeof(double), P->stream));
+        QVA_CUDA_TRY(cudaMemcpyAsync(dw, P->g_w.data(), m * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+    }
+    {
+        ProfScope ps(P, K_OTHER, 8.0 * P->arr_n);
+        QVA_CUDA_TRY(launch_maxcut_q(P->q, P->arr_n, P->offset, m, du, dv, dw, P->stream));
+    }
+    cudaFreeAsync(du, P->stream);
+    cudaFreeAsync(dv, P->stream);
+    if (dw) cudaFreeAsync(dw, P->stream);
+    QVA_TRY(sync(P));
+    P->q_dev_valid = true;
+    return QVA_OK;
 }
 
 // physical -> logical bit map as runs (nullptr / empty: identity over n bits)
@@ -820,16 +871,216 @@ qva_status to_natural_perm(qva_plan *P) {
     return QVA_OK;
 }
 
+// ---- generated MaxCut qualities ---------------------------
+constexpr int kGenIntMaxEdges = 4000;  // integer path: cut in [0, m], phase table of m + 1 entries
+
+bool use_qgen(const qva_plan *P) {
+    static int env = [] {
+        const char *e = getenv("QVA_QGEN");
+        return e ? atoi(e) : 1;
+    }();
+    return env != 0 && P->q_graph && P->mixer == QVA_MIXER_X;
+}
+
+// logical qubit of every physical bit of the arrays a pass reads (n_phys bits) and the logical
+// bits that are constant on this process (global qubits of a real shard = its rank bits)
+void pass_layout(const qva_plan *P, const PassPlan &pp, int n_phys, std::vector<int> &lay, uint64_t &cmask,
+                 uint64_t &cval) {
+    lay.resize(n_phys);
+    for (int b = 0; b < n_phys; ++b) lay[b] = b;
+    cmask = cval = 0;
+    if (pp.permuted) {
+        for (int b = 0; b < (int)pp.lay_in.size() && b < n_phys; ++b) lay[b] = pp.lay_in[b];
+        return;
+    }
+    if (P->G <= 1) return;
+    const int L = P->L, g = P->gbits;
+    if (P->world == 1) {  // virtual shards: the shard index is the top physical bits
+        if (P->layout == 1)
+            for (int i = 0; i < g; ++i) {
+                lay[L - g + i] = L + i;
+                lay[L + i] = L - g + i;
+            }
+        return;
+    }
+    if (P->layout == 0) {
+        for (int i = 0; i < g; ++i) cmask |= 1ull << (L + i);
+        cval = (uint64_t)P->rank << L;
+    } else {
+        for (int i = 0; i < g; ++i) lay[L - g + i] = L + i;
+        for (int i = 0; i < g; ++i) cmask |= 1ull << (L - g + i);
+        cval = (uint64_t)P->rank << (L - g);
+    }
+}
+
+// per-tile records + per-thread constants of the generated q for one pass shape (cached)
+qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan &pp, int n_phys, int gq, int mode,
+                      const TilePassParams &tp, const qva_plan::GenEntry **out) {
+    for (auto &e : P->gen_cache)
+        if (e.key == qkey && e.group == gq && e.mode == mode) {
+            *out = &e;
+            return QVA_OK;
+        }
+    std::vector<int> lay;
+    uint64_t cmask, cval;
+    pass_layout(P, pp, n_phys, lay, cmask, cval);
+    // tile-local bit k -> logical; tile-number bit -> logical
+    int tl[kTileBits];
+    std::vector<int> in_tile(64, -1);
+    for (int k = 0; k < kTileBits; ++k) {
+        tl[k] = lay[tp.tile_bits[k]];
+        in_tile[tl[k]] = k;
+    }
+    std::vector<int> tbit_log;
+    for (int r = 0; r < tp.n_runs; ++r)
+        for (int j = 0; j < tp.run_w[r]; ++j) {
+            const int tb = tp.run_src[r] + j;
+            if ((int)tbit_log.size() <= tb) tbit_log.resize(tb + 1, -1);
+            tbit_log[tb] = lay[tp.run_dst[r] + j];
+        }
+    GenPrep gp;
+    memset(&gp, 0, sizeof(gp));
+    {
+        int b = 0;
+        while (b < (int)tbit_log.size()) {
+            int st = b++;
+            while (b < (int)tbit_log.size() && tbit_log[b] == tbit_log[b - 1] + 1) ++b;
+            if (gp.tmap.n == kMaxLayoutRuns) {
+                set_error("internal: tile-number map has too many runs");
+                return QVA_ERR_UNSUPPORTED;
+            }
+            gp.tmap.src[gp.tmap.n] = (int8_t)st;
+            gp.tmap.w[gp.tmap.n] = (int8_t)(b - st);
+            gp.tmap.dst[gp.tmap.n] = (int8_t)tbit_log[st];
+            ++gp.tmap.n;
+        }
+    }
+    gp.const_val = cval;
+    gp.w_unit = P->g_unit ? 1 : 0;
+    // classify the edges (self-loops never cut)
+    std::vector<int2> tt, tb;
+    std::vector<double> ttw, tbw;
+    struct TileEdge {
+        int a, b;
+        double w;
+    };
+    std::vector<TileEdge> te;
+    for (int e = 0; e < P->g_m; ++e) {
+        const int u = P->g_u[e], v = P->g_v[e];
+        if (u == v) continue;
+        const double w = P->g_unit ? 1.0 : P->g_w[e];
+        const int ku = in_tile[u], kv = in_tile[v];
+        if (ku < 0 && kv < 0) {
+            tt.push_back(make_int2(u, v));
+            ttw.push_back(w);
+        } else if (ku >= 0 && kv >= 0) {
+            te.push_back({ku, kv, w});
+        } else {
+            tb.push_back(ku >= 0 ? make_int2(ku, v) : make_int2(kv, u));
+            tbw.push_back(w);
+        }
+    }
+    (void)cmask;
+    gp.n_tt = (int)tt.size();
+    gp.n_tb = (int)tb.size();
+    const bool f64 = mode == kQGenF64;
+    const uint64_t n_tiles = P->arr_n >> kTileBits;
+    const size_t rec_bytes = f64 ? 112 : 16;
+    qva_plan::GenEntry ent;
+    ent.key = qkey;
+    ent.group = gq;
+    ent.mode = mode;
+    ent.rec = ent.thr = ent.G = nullptr;
+    QVA_CUDA_TRY(cudaMalloc(&ent.rec, n_tiles * rec_bytes));
+    QVA_CUDA_TRY(cudaMalloc(&ent.thr, 128 * 8 * sizeof(double)));
+    QVA_CUDA_TRY(cudaMalloc(&ent.G, 32 * sizeof(double)));
+    void *d_edges = nullptr;
+    const size_t eb = (tt.size() + tb.size()) * (sizeof(int2) + sizeof(double)) + 16;
+    QVA_CUDA_TRY(cudaMallocAsync(&d_edges, eb, P->stream));
+    {
+        std::vector<unsigned char> hb(eb, 0);
+        size_t off = 0;
+        auto put = [&](const void *src, size_t n) {
+            memcpy(hb.data() + off, src, n);
+            off += n;
+        };
+        put(tt.data(), tt.size() * sizeof(int2));
+        put(tb.data(), tb.size() * sizeof(int2));
+        const size_t woff = off;
+        put(ttw.data(), ttw.size() * sizeof(double));
+        put(tbw.data(), tbw.size() * sizeof(double));
+        unsigned char *d = (unsigned char *)d_edges;
+        gp.tt_uv = (const int2 *)d;
+        gp.tb_ab = (const int2 *)(d + tt.size() * sizeof(int2));
+        gp.tt_w = (const double *)(d + woff);
+        gp.tb_w = (const double *)(d + woff + ttw.size() * sizeof(double));
+        QVA_CUDA_TRY(cudaMemcpyAsync(d_edges, hb.data(), eb, cudaMemcpyHostToDevice, P->stream));
+        ProfScope ps(P, K_OTHER, (double)n_tiles * rec_bytes);
+        QVA_CUDA_TRY(launch_gen_records(ent.rec, n_tiles, f64 ? 1 : 0, gp, P->stream));
+        QVA_CUDA_TRY(cudaFreeAsync(d_edges, P->stream));
+        // host per-thread constants of group gq: C(c), beta_j(c), and G(e)
+        const TileGroup &g = kGroups[gq];
+        int role[kTileBits], ridx[kTileBits];  // 0: thread bit, 1: register bit
+        for (int j = 0; j < kCT_BITS; ++j) role[g.tbit[j]] = 0, ridx[g.tbit[j]] = j;
+        for (int j = 0; j < kGroupBits; ++j) role[g.ebit[j]] = 1, ridx[g.ebit[j]] = j;
+        std::vector<double> thr(128 * 8, 0.0), G(32, 0.0);
+        std::vector<int> thr_i(128 * 8, 0), G_i(32, 0);
+        for (int c = 0; c < 128; ++c) {
+            double C = 0.0, beta[kGroupBits] = {0, 0, 0, 0, 0};
+            auto xv = [&](int k) { return (c >> ridx[k]) & 1; };
+            for (const TileEdge &x : te) {
+                if (role[x.a] == 0 && role[x.b] == 0) {
+                    C += x.w * (double)(xv(x.a) ^ xv(x.b));
+                } else if (role[x.a] != role[x.b]) {
+                    const int h = role[x.a] == 0 ? x.a : x.b, e = role[x.a] == 0 ? x.b : x.a;
+                    C += x.w * xv(h);
+                    beta[ridx[e]] += x.w * (1.0 - 2.0 * xv(h));
+                }
+            }
+            thr[c * 8] = C;
+            thr_i[c * 8] = (int)C;
+            for (int j = 0; j < kGroupBits; ++j) {
+                thr[c * 8 + 1 + j] = beta[j];
+                thr_i[c * 8 + 1 + j] = (int)beta[j];
+            }
+        }
+        for (int e = 0; e < 32; ++e) {
+            double s = 0.0;
+            for (const TileEdge &x : te)
+                if (role[x.a] == 1 && role[x.b] == 1) s += x.w * (double)(((e >> ridx[x.a]) ^ (e >> ridx[x.b])) & 1);
+            G[e] = s;
+            G_i[e] = (int)s;
+        }
+        if (f64) {
+            QVA_CUDA_TRY(cudaMemcpyAsync(ent.thr, thr.data(), thr.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                         P->stream));
+            QVA_CUDA_TRY(cudaMemcpyAsync(ent.G, G.data(), G.size() * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+        } else {
+            QVA_CUDA_TRY(cudaMemcpyAsync(ent.thr, thr_i.data(), thr_i.size() * sizeof(int), cudaMemcpyHostToDevice,
+                                         P->stream));
+            QVA_CUDA_TRY(cudaMemcpyAsync(ent.G, G_i.data(), G_i.size() * sizeof(int), cudaMemcpyHostToDevice, P->stream));
+        }
+        QVA_TRY(sync(P));  // host staging vectors go out of scope
+    }
+    P->gen_cache.push_back(ent);
+    *out = &P->gen_cache.back();
+    return QVA_OK;
+}
+
 // ---- tile-pass execution of a pass list -----------------------------------------------------
 // thetas: [batch][2p]; psi_base/stride: states of the batch members
 qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const double *thetas, int p, int batch,
                       double2 *psi_base, uint64_t stride, int init_mode, double *expect_out /*[batch][2] host*/) {
     int n_tile_passes = 0;
     for (auto &pp : passes) n_tile_passes += !pp.exchange;
-    if (P->q_set && !P->q_classified) {
+    // graph-defined q: generated inside the passes (integer table path for unit weights)
+    const int gen = use_qgen(P) ? ((P->g_unit && P->g_m <= kGenIntMaxEdges) ? kQGenInt : kQGenF64) : 0;
+    if (!gen && P->q_set && !P->q_classified) {
         QVA_TRY(classify_q(P));
         P->q_classified = true;
     }
+    const bool int_table = gen == kQGenInt || (!gen && P->q_mode != 0);
+    const int tab_qmin = gen == kQGenInt ? -P->g_m : P->qmin;
     QVA_TRY(ensure_angles(P, (size_t)n_tile_passes * batch));
     std::vector<PassAngles> ang((size_t)n_tile_passes * batch);
     std::vector<char> half1(n_tile_passes, 0), half2(n_tile_passes, 0);
@@ -852,7 +1103,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         for (size_t pi = 0; pi < passes.size(); ++pi) {
             const PassPlan &pp = passes[pi];
             if (pp.exchange) continue;
-            if (pp.phase >= 0 && P->q_mode) tab_index[pi] = np++;
+            if (pp.phase >= 0 && int_table) tab_index[pi] = np++;
             int n1 = __builtin_popcount(pp.r1), n2 = __builtin_popcount(pp.r2);
             for (int b = 0; b < batch; ++b) {
                 const double *th = thetas + (size_t)b * 2 * p;
@@ -873,7 +1124,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
                 a.scale = make_double2(sr, si);
                 if (pp.phase >= 0) {
                     a.gamma = th[2 * pp.phase];
-                    if (P->q_mode) gam.push_back(a.gamma);
+                    if (int_table) gam.push_back(a.gamma);
                 }
             }
             ++j;
@@ -881,7 +1132,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
     }
     QVA_CUDA_TRY(cudaMemcpyAsync(P->d_angles, ang.data(), ang.size() * sizeof(PassAngles), cudaMemcpyHostToDevice,
                                  P->stream));
-    const int ntab = P->q_mode ? (P->qmax - P->qmin + 1) : 0;
+    const int ntab = gen == kQGenInt ? P->g_m + 1 : (int_table ? (P->qmax - P->qmin + 1) : 0);
     if (!gam.empty()) {
         if (P->gam_cap < gam.size()) {
             cudaFree(P->d_gam);
@@ -898,7 +1149,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         QVA_CUDA_TRY(cudaMemcpyAsync(P->d_gam, gam.data(), gam.size() * sizeof(double), cudaMemcpyHostToDevice,
                                      P->stream));
         ProfScope ps(P, K_OTHER, 16.0 * gam.size() * ntab);
-        QVA_CUDA_TRY(launch_phase_table(P->d_tab, P->d_gam, (int)gam.size(), P->qmin, ntab, P->stream));
+        QVA_CUDA_TRY(launch_phase_table(P->d_tab, P->d_gam, (int)gam.size(), tab_qmin, ntab, P->stream));
     }
     uint64_t n_tiles = P->arr_n >> kTileBits;
     bool any_expect = false;
@@ -907,7 +1158,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
     const int nslot = grid * tile_consumer_warps();
     if (any_expect) QVA_TRY(ensure_partials(P, (uint64_t)nslot * batch));
     const int n_phys = ilog2(P->arr_n);
-    const int qbytes = P->q_mode == 1 ? 1 : (P->q_mode == 2 ? 2 : 8);
+    const int qbytes = gen ? gen : (P->q_mode == 1 ? 1 : (P->q_mode == 2 ? 2 : 8));
     int j = 0;
     bool first = true;
     for (size_t pi = 0; pi < passes.size(); ++pi) {
@@ -970,7 +1221,17 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             for (auto &e : P->qt_cache)
                 if (e.key == qkey && e.qbytes == qbytes) pref = e.group;
         build_steps(pp, tp, pref, half1[j], half2[j]);
-        if (needs_q) {
+        if (needs_q && gen) {
+            const qva_plan::GenEntry *ge = nullptr;
+            QVA_TRY(ensure_gen(P, qkey, pp, n_phys, tp.gq, gen, tp, &ge));
+            tp.qt = ge->rec;
+            tp.gen_thr = ge->thr;
+            tp.gen_G = ge->G;
+            tp.gen_m = P->g_m;
+            tp.qmin = tab_qmin;
+            tp.ntab = ntab;
+            if (tab_index[pi] >= 0) tp.tab = P->d_tab + (size_t)tab_index[pi] * batch * ntab;
+        } else if (needs_q) {
             if (P->layout == 1) QVA_TRY(ensure_qB(P));
             void *qt = nullptr;
             QVA_TRY(ensure_qt(P, qkey, pp.permuted ? &pp.lay_in : nullptr, tp.gq, qbytes, tp, &qt));
@@ -1023,8 +1284,10 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             for (int d = 0; d < 5; ++d) fprintf(stderr, " [%d,%d]", tp.dim_src[d], tp.dim_w[d]);
             fprintf(stderr, "\n");
         }
+        // algorithmic bytes: the state round trip plus stored q (generated q: the per-tile records)
+        const double qb = gen ? (gen == kQGenInt ? 16.0 : 112.0) / (double)(1 << kTileBits) : (double)qbytes;
         double bytes = (double)P->arr_n * batch *
-                       ((tp.init == 1 ? 16.0 : 32.0) + (pp.phase >= 0 ? qbytes : 0.0) + (pp.expect ? qbytes : 0.0));
+                       ((tp.init == 1 ? 16.0 : 32.0) + ((pp.phase >= 0 || pp.expect) ? qb : 0.0) / batch);
         if (pp.expect)
             QVA_CUDA_TRY(cudaMemsetAsync(P->partials, 0, (size_t)nslot * batch * 2 * sizeof(double), P->stream));
         {
@@ -1465,6 +1728,10 @@ static qva_status set_q_common(qva_plan *P, const double *src, bool device, uint
     uint64_t lo;
     QVA_TRY(check_range(P, offset, count, &lo));
     if (count == 0) return QVA_OK;
+    if (P->q_graph) {  // a partial upload overwrites part of the graph's q: materialise it first
+        QVA_TRY(ensure_q_dev(P));
+        P->q_graph = false;
+    }
     QVA_CUDA_TRY(cudaMemcpyAsync(P->q + lo, src, count * sizeof(double),
                                  device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P->stream));
     QVA_CUDA_TRY(cudaMemsetAsync(P->d_flag, 0, sizeof(int), P->stream));
@@ -1513,25 +1780,16 @@ qva_status qva_set_qualities_maxcut(qva_plan *P, int32_t m, const int32_t *u, co
         }
     }
     DeviceGuard dg(P->device);
-    int32_t *du = nullptr, *dv = nullptr;
-    double *dw = nullptr;
-    size_t me = m > 0 ? m : 1;
-    QVA_CUDA_TRY(cudaMallocAsync((void **)&du, me * sizeof(int32_t), P->stream));
-    QVA_CUDA_TRY(cudaMallocAsync((void **)&dv, me * sizeof(int32_t), P->stream));
-    if (m) QVA_CUDA_TRY(cudaMemcpyAsync(du, u, m * sizeof(int32_t), cudaMemcpyHostToDevice, P->stream));
-    if (m) QVA_CUDA_TRY(cudaMemcpyAsync(dv, v, m * sizeof(int32_t), cudaMemcpyHostToDevice, P->stream));
-    if (w) {
-        QVA_CUDA_TRY(cudaMallocAsync((void **)&dw, me * sizeof(double), P->stream));
-        QVA_CUDA_TRY(cudaMemcpyAsync(dw, w, m * sizeof(double), cudaMemcpyHostToDevice, P->stream));
-    }
-    {
-        ProfScope ps(P, K_OTHER, 8.0 * P->arr_n);
-        QVA_CUDA_TRY(launch_maxcut_q(P->q, P->arr_n, P->offset, m, du, dv, dw, P->stream));
-    }
-    cudaFreeAsync(du, P->stream);
-    cudaFreeAsync(dv, P->stream);
-    if (dw) cudaFreeAsync(dw, P->stream);
-    QVA_TRY(sync(P));
+    // the graph is the input: q_x = -cut_w(x) is generated where it is consumed (tile passes) or
+    // materialised on demand by ensure_q_dev (observables computed in parallel)
+    P->g_m = m;
+    P->g_unit = (w == nullptr);
+    P->g_u.assign(u, u + m);
+    P->g_v.assign(v, v + m);
+    if (w) P->g_w.assign(w, w + m);
+    else P->g_w.clear();
+    P->q_graph = true;
+    P->q_dev_valid = false;
     P->q_set = true;
     P->qB_valid = false;
     P->q_classified = false;
@@ -1546,6 +1804,7 @@ qva_status qva_get_qualities(qva_plan *P, double *q_out, uint64_t offset, uint64
     uint64_t lo;
     QVA_TRY(check_range(P, offset, count, &lo));
     DeviceGuard dg(P->device);
+    QVA_TRY(ensure_q_dev(P));
     if (count)
         QVA_CUDA_TRY(cudaMemcpyAsync(q_out, P->q + lo, count * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
     return sync(P);
@@ -1704,6 +1963,7 @@ qva_status qva_apply_phase(qva_plan *P, double gamma) {
     }
     DeviceGuard dg(P->device);
     QVA_TRY(to_natural_perm(P));
+    QVA_TRY(ensure_q_dev(P));
     if (P->layout == 1) QVA_TRY(ensure_qB(P));
     {
         ProfScope ps(P, K_OTHER, 40.0 * P->arr_n);
@@ -1731,6 +1991,7 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
     *have_red = false;
     if (P->mixer == QVA_MIXER_X) {
         if (use_small(P)) {
+            QVA_TRY(ensure_q_dev(P));
             SmallEvolveParams sp{};
             sp.psi = P->psi;
             sp.psi0 = P->has_psi0 ? P->psi0 : nullptr;
@@ -1859,6 +2120,7 @@ static qva_status expect_now(qva_plan *P) {
         return QVA_ERR_NOT_READY;
     }
     QVA_TRY(to_natural_perm(P));
+    QVA_TRY(ensure_q_dev(P));
     if (P->layout == 1) QVA_TRY(ensure_qB(P));
     double pair[2];
     QVA_TRY(expect_generic(P, P->psi, P->arr_n, q_current(P), pair));
@@ -1940,6 +2202,7 @@ static qva_status batch_local(qva_plan *P, const double *thetas, int first, int 
             int nb = std::min(chunk, count - b0);
             std::vector<double> pairs(2 * (size_t)nb);
             if (use_small(P)) {
+                QVA_TRY(ensure_q_dev(P));
                 size_t need = (size_t)nb * 2 * p;
                 if (need > P->thetas_cap) {
                     cudaFree(P->d_thetas);
@@ -1993,6 +2256,7 @@ static qva_status batch_local(qva_plan *P, const double *thetas, int first, int 
             QVA_CUDA_TRY(cudaMemcpyAsync(pair, P->red, sizeof(pair), cudaMemcpyDeviceToHost, P->stream));
             QVA_TRY(sync(P));
         } else {
+            QVA_TRY(ensure_q_dev(P));
             if (P->layout == 1) QVA_TRY(ensure_qB(P));
             QVA_TRY(expect_generic(P, P->psi, P->arr_n, q_current(P), pair));
         }

@@ -42,6 +42,15 @@ constexpr int kTabSmemMax = 64;             // entries held in smem (int8 codes,
 static_assert(kAPT == 1 << kGroupBits, "group width");
 static_assert(kCT == 1 << kCT_BITS, "warpgroup width");
 
+template <typename F, int... K>
+__device__ __forceinline__ void static_for_impl(F &f, std::integer_sequence<int, K...>) {
+    (f(std::integral_constant<int, K>()), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F &&f) {
+    static_for_impl(f, std::make_integer_sequence<int, N>());
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -243,10 +252,105 @@ __device__ __forceinline__ void accumulate_expect(const double2 (&v)[kAPT], cons
     }
 }
 
+// ---- generated MaxCut qualities (QB = kQGenInt / kQGenF64) --
+// q_x = -cut_w(x) is assembled per element from a per-tile record (the q stage holds it instead
+// of 4096 stored values) and per-pass constants: with the tile's coordinate qubits T, the
+// consumer thread's 7 thread-bit qubits H and its 5 register-bit qubits E,
+//   cut(x) = [TT + K_H + K_E](t) + sum_{a in H, x_a = 1} kappa_a(t) + C(c)
+//            + sum_j e_j (kappa_{E_j}(t) + beta_j(c)) + G(e)
+// (kappa_a = sum over a's T-neighbours of w (1 - 2 x_b); C, beta: edges inside the tile touching
+// H; G: edges among the E qubits).  Exact in integers for unit weights (phase by table), fp64
+// sums otherwise.  Record: int {int32 T, int8 kappa[12]} (16 B) / fp64 {T, kappa[12]} (112 B).
+template <int QB>
+struct QGenT {
+    using V = typename std::conditional<QB == kQGenInt, int, double>::type;
+};
+template <int QB>
+constexpr uint32_t q_stage_bytes() {
+    return QB == kQGenInt ? 16u : (QB == kQGenF64 ? 112u : (uint32_t)kTile * QB);
+}
+template <int QB>
+__device__ __forceinline__ void gen_coeffs(const unsigned char *rec, const TileGroup &g, int c,
+                                           const typename QGenT<QB>::V (&cst)[6], typename QGenT<QB>::V &S,
+                                           typename QGenT<QB>::V (&al)[5]) {
+    if constexpr (QB == kQGenInt) {
+        const int8_t *k8 = reinterpret_cast<const int8_t *>(rec + 4);
+        S = *reinterpret_cast<const int *>(rec) + cst[0];
+#pragma unroll
+        for (int j = 0; j < kCT_BITS; ++j)
+            if ((c >> j) & 1) S += k8[g.tbit[j]];
+#pragma unroll
+        for (int j = 0; j < kGroupBits; ++j) al[j] = k8[g.ebit[j]] + cst[1 + j];
+    } else {
+        const double *kd = reinterpret_cast<const double *>(rec + 8);
+        S = *reinterpret_cast<const double *>(rec) + cst[0];
+#pragma unroll
+        for (int j = 0; j < kCT_BITS; ++j)
+            if ((c >> j) & 1) S += kd[g.tbit[j]];
+#pragma unroll
+        for (int j = 0; j < kGroupBits; ++j) al[j] = kd[g.ebit[j]] + cst[1 + j];
+    }
+}
+template <int QB, int E>
+__device__ __forceinline__ typename QGenT<QB>::V gen_cut(typename QGenT<QB>::V S,
+                                                         const typename QGenT<QB>::V (&al)[5],
+                                                         const typename QGenT<QB>::V *G_s) {
+    typename QGenT<QB>::V x = S + G_s[E];
+    if (E & 1) x += al[0];
+    if (E & 2) x += al[1];
+    if (E & 4) x += al[2];
+    if (E & 8) x += al[3];
+    if (E & 16) x += al[4];
+    return x;
+}
+template <int QB>
+__device__ __forceinline__ void apply_phase_gen(double2 (&v)[kAPT], const unsigned char *rec, const TileGroup &g,
+                                                int c, int lane, const typename QGenT<QB>::V (&cst)[6],
+                                                const typename QGenT<QB>::V *G_s, int m_edges, double gamma,
+                                                const double2 *tab_s, const double2 *tab_g) {
+    using V = typename QGenT<QB>::V;
+    V S, al[5];
+    gen_coeffs<QB>(rec, g, c, cst, S, al);
+    const double2 *tab_l = tab_s + (lane & (kTabRep - 1));
+    static_for<kAPT>([&](auto ec) {
+        constexpr int E = decltype(ec)::value;
+        const V cut = gen_cut<QB, E>(S, al, G_s);
+        if constexpr (QB == kQGenInt) {
+            const int j = m_edges - cut;  // q - qmin with q = -cut, qmin = -m
+            const double2 f = tab_s ? tab_l[j * kTabRep] : __ldg(tab_g + j);
+            v[E] = cmul(v[E], f);
+        } else {
+            double sn, cs;
+            sincos(gamma * (-cut), &sn, &cs);
+            v[E] = cmul(v[E], make_double2(cs, -sn));
+        }
+    });
+}
+template <int QB>
+__device__ __forceinline__ void accumulate_gen(const double2 (&v)[kAPT], const unsigned char *rec, const TileGroup &g,
+                                               int c, const typename QGenT<QB>::V (&cst)[6],
+                                               const typename QGenT<QB>::V *G_s, double &acc, double &nrm) {
+    using V = typename QGenT<QB>::V;
+    V S, al[5];
+    gen_coeffs<QB>(rec, g, c, cst, S, al);
+    static_for<kAPT>([&](auto ec) {
+        constexpr int E = decltype(ec)::value;
+        const V cut = gen_cut<QB, E>(S, al, G_s);
+        const double pr = v[E].x * v[E].x + v[E].y * v[E].y;
+        acc = fma(pr, -(double)cut, acc);
+        nrm += pr;
+    });
+}
+
+template <int QB>
+constexpr bool q_table() { return QB == 1 || QB == kQGenInt; }
+template <int QB>
+constexpr bool q_gen() { return QB == kQGenInt || QB == kQGenF64; }
 template <int STAGES, int QB>
 constexpr size_t tile_smem_bytes() {
-    return (size_t)STAGES * (kTile * sizeof(double2) + (size_t)kTile * QB) +
-           (QB == 1 ? (size_t)kTabSmemMax * kTabRep * sizeof(double2) : 0) + 2 * STAGES * sizeof(uint64_t) +
+    return (size_t)STAGES * (kTile * sizeof(double2) + (size_t)q_stage_bytes<QB>()) +
+           (q_table<QB>() ? (size_t)kTabSmemMax * kTabRep * sizeof(double2) : 0) +
+           (q_gen<QB>() ? 32 * sizeof(double) : 0) + 2 * STAGES * sizeof(uint64_t) +
            (size_t)kMaxBatchSmem * sizeof(PassAngles);
 }
 
@@ -295,14 +399,6 @@ __device__ __forceinline__ constexpr int prog_release() {
     return r;
 }
 
-template <typename F, int... K>
-__device__ __forceinline__ void static_for_impl(F &f, std::integer_sequence<int, K...>) {
-    (f(std::integral_constant<int, K>()), ...);
-}
-template <int N, typename F>
-__device__ __forceinline__ void static_for(F &&f) {
-    static_for_impl(f, std::make_integer_sequence<int, N>());
-}
 
 template <int STAGES, int QB, int PROG>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -310,11 +406,15 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                  const __grid_constant__ TilePassParams P) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];  // SWIZZLE_128B needs 1024-B alignment
     unsigned char *sm = smem_raw;
+    constexpr uint32_t QSB = q_stage_bytes<QB>();
+    using GV = typename QGenT<QB>::V;
     double2 *psi_s = reinterpret_cast<double2 *>(sm);
     unsigned char *q_s = sm + (size_t)STAGES * kTile * sizeof(double2);
-    double2 *tab_s = reinterpret_cast<double2 *>(q_s + (size_t)STAGES * kTile * QB);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(tab_s) +
-                                                  (QB == 1 ? kTabSmemMax * kTabRep * sizeof(double2) : 0));
+    double2 *tab_s = reinterpret_cast<double2 *>(q_s + (size_t)STAGES * QSB);
+    GV *G_s = reinterpret_cast<GV *>(reinterpret_cast<unsigned char *>(tab_s) +
+                                     (q_table<QB>() ? kTabSmemMax * kTabRep * sizeof(double2) : 0));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(G_s) +
+                                                  (q_gen<QB>() ? 32 * sizeof(double) : 0));
     PassAngles *ang_s = reinterpret_cast<PassAngles *>(bars + 2 * STAGES);  // [batch]
     // full[round & 1][stage]: item `it` is round it / STAGES of stage it % STAGES.  Rounds r and
     // r - 2 of a stage belong to the same warpgroup, so each barrier is waited by one warpgroup
@@ -340,8 +440,8 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     const bool load_psi = (P.init != 1);
     const bool tstore = P.tma_store != 0;  // output through a TMA store of the final smem tile
     const bool load_q = (QB > 0) && (P.gq >= 0);
-    const bool use_tab_s = (QB == 1) && kPhase && P.batch == 1 && P.ntab <= kTabSmemMax && P.tab != nullptr;
-    const uint32_t qbytes = load_q ? (uint32_t)(kTile * QB) : 0u;
+    const bool use_tab_s = q_table<QB>() && kPhase && P.batch == 1 && P.ntab <= kTabSmemMax && P.tab != nullptr;
+    const uint32_t qbytes = load_q ? QSB : 0u;
     const uint32_t bytes = (load_psi ? kTile * (uint32_t)sizeof(double2) : 0u) + qbytes;
     const unsigned char *qt = reinterpret_cast<const unsigned char *>(P.qt);
 
@@ -357,7 +457,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             tma_coords(P, member, t, cc);
             tma_load_5d(smem_u32(psi_s + (size_t)s * kTile), &tmap, bar, cc);
         }
-        if (qbytes) bulk_load(smem_u32(q_s + (size_t)s * kTile * QB), qt + t * (uint64_t)qbytes, qbytes, bar);
+        if (qbytes) bulk_load(smem_u32(q_s + (size_t)s * QSB), qt + t * (uint64_t)qbytes, qbytes, bar);
         // strided tile sets: tile (block b, index c) prefetches the contiguous 64-KiB chunk c of
         // block b + 1 into L2, so the next block's 128-B rows are L2 hits and DRAM sees
         // sequential reads
@@ -376,6 +476,17 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     if (use_tab_s)
         for (int k = tid; k < P.ntab * kTabRep; k += kThreads) tab_s[k] = P.tab[k / kTabRep];
     for (int k = tid; k < P.batch; k += kThreads) ang_s[k] = P.angles[k];
+    // generated qualities: per-pass G(e) table and this consumer thread's constants {C, beta[5]}
+    GV gcst[6] = {};
+    if constexpr (q_gen<QB>()) {
+        if (load_q) {
+            const GV *Gg = reinterpret_cast<const GV *>(P.gen_G);
+            for (int k = tid; k < 32; k += kThreads) G_s[k] = Gg[k];
+            const GV *cg = reinterpret_cast<const GV *>(P.gen_thr) + (size_t)(tid % kCT) * 8;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) gcst[k] = cg[k];
+        }
+    }
     __syncthreads();
     if (tid == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
@@ -407,7 +518,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
         }
 
         const uint32_t buf = smem_u32(psi_s + (size_t)s * kTile);
-        const unsigned char *qs = q_s + (size_t)s * kTile * QB;
+        const unsigned char *qs = q_s + (size_t)s * QSB;
         mbar_wait(full_bar(it), ((it / STAGES) >> 1) & 1);
 
         // hand stage s back: the whole warpgroup is done with it, so one thread refills it with
@@ -439,8 +550,13 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                         smem_read_g<G>(v, buf, c);
                     }
                     if (st.mask) rotate_group<G>(v, st.mask, tt);
-                    if (QB > 0 && st.phase)
-                        apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
+                    if (QB > 0 && st.phase) {
+                        if constexpr (q_gen<QB>())
+                            apply_phase_gen<QB>(v, qs, P.groups[P.gq], c, lane, gcst, G_s, P.gen_m, ang->gamma,
+                                                use_tab_s ? tab_s : nullptr, tab_g);
+                        else
+                            apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
+                    }
                     if (next != G) smem_write_g<G>(v, buf, c);
                 };
                 if (st.group == 0) body(std::integral_constant<int, 0>());
@@ -464,8 +580,13 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                     const PassStep st = P.steps[K];
                     rotate_group<G>(v, st.mask, st.angle ? ang->t2 : ang->t1);
                 }
-                if constexpr (QB > 0 && K == prog_def<PROG>().phase_k)
-                    apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
+                if constexpr (QB > 0 && K == prog_def<PROG>().phase_k) {
+                    if constexpr (q_gen<QB>())
+                        apply_phase_gen<QB>(v, qs, P.groups[P.gq], c, lane, gcst, G_s, P.gen_m, ang->gamma,
+                                            use_tab_s ? tab_s : nullptr, tab_g);
+                    else
+                        apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
+                }
                 if constexpr (K == REL) {
                     if (!tstore) release();
                 }
@@ -478,7 +599,10 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             for (int e = 0; e < kAPT; ++e) v[e] = cmul(v[e], sc);
         }
         if constexpr (QB > 0 && kExpect) {
-            if (P.expect) accumulate_expect<QB>(v, qs, c, P.qmin, acc, nrm);
+            if (P.expect) {
+                if constexpr (q_gen<QB>()) accumulate_gen<QB>(v, qs, P.groups[P.gq], c, gcst, G_s, acc, nrm);
+                else accumulate_expect<QB>(v, qs, c, P.qmin, acc, nrm);
+            }
         }
         if (tstore) {
             // the tile goes back through shared memory in the load layout and out with one TMA
@@ -565,6 +689,46 @@ __global__ void permute_copy_kernel(double2 *__restrict__ out, const double2 *__
                                     const __grid_constant__ LayoutRuns lay) {
     for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (uint64_t)gridDim.x * blockDim.x)
         out[layout_map(lay, x)] = in[x];
+}
+
+// Per-tile records of the generated MaxCut qualities (see QGenT): for tile t, with x the logical
+// index pattern of its coordinate (and constant) qubits,
+//   T(t)     = sum_{TT edges} w [x_u != x_v] + sum_{TB edges (a, b)} w x_b
+//   kappa_a  = sum_{TB edges (a, b)} w (1 - 2 x_b)        (a = tile-local bit)
+template <typename V>
+__global__ void gen_records_kernel(unsigned char *rec, uint64_t n_tiles, uint32_t rec_bytes,
+                                   const __grid_constant__ GenPrep g) {
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t x = g.const_val;
+        for (int r = 0; r < g.tmap.n; ++r)
+            x |= ((t >> g.tmap.src[r]) & ((1ull << g.tmap.w[r]) - 1)) << g.tmap.dst[r];
+        V T = 0, kap[kTileBits];
+#pragma unroll
+        for (int a = 0; a < kTileBits; ++a) kap[a] = 0;
+        for (int e = 0; e < g.n_tt; ++e) {
+            const int2 uv = g.tt_uv[e];
+            const V w = g.w_unit ? (V)1 : (V)g.tt_w[e];
+            if (((x >> uv.x) ^ (x >> uv.y)) & 1) T += w;
+        }
+        for (int e = 0; e < g.n_tb; ++e) {
+            const int2 ab = g.tb_ab[e];  // (tile-local bit, logical qubit)
+            const V w = g.w_unit ? (V)1 : (V)g.tb_w[e];
+            const bool xb = (x >> ab.y) & 1;
+            if (xb) T += w;
+#pragma unroll
+            for (int a = 0; a < kTileBits; ++a)
+                if (a == ab.x) kap[a] += xb ? -w : w;
+        }
+        unsigned char *r = rec + t * rec_bytes;
+        if constexpr (std::is_same<V, int>::value) {
+            *reinterpret_cast<int *>(r) = T;
+            for (int a = 0; a < kTileBits; ++a) reinterpret_cast<int8_t *>(r + 4)[a] = (int8_t)kap[a];
+        } else {
+            reinterpret_cast<double *>(r)[0] = T;
+            for (int a = 0; a < kTileBits; ++a) reinterpret_cast<double *>(r + 8)[a] = kap[a];
+        }
+    }
 }
 
 template <int STAGES, int QB, int PROG>
@@ -774,6 +938,8 @@ cudaError_t launch_tile_pass(const CUtensorMap &map, const CUtensorMap &map_out,
         case 1: return qprog ? launch_prog<3, 1>(map, map_out, p, prog, grid, s) : cudaErrorInvalidValue;
         case 2: return qprog ? launch_prog<3, 2>(map, map_out, p, prog, grid, s) : cudaErrorInvalidValue;
         case 8: return qprog ? launch_prog<2, 8>(map, map_out, p, prog, grid, s) : cudaErrorInvalidValue;
+        case kQGenInt: return qprog ? launch_prog<3, kQGenInt>(map, map_out, p, prog, grid, s) : cudaErrorInvalidValue;
+        case kQGenF64: return qprog ? launch_prog<3, kQGenF64>(map, map_out, p, prog, grid, s) : cudaErrorInvalidValue;
     }
     return cudaErrorInvalidValue;
 }
@@ -788,6 +954,13 @@ cudaError_t launch_qt_gather(void *dst, const void *src, int qbytes, const TileP
         qt_gather_kernel<int16_t>
             <<<blocks, 256, 0, s>>>((int16_t *)dst, (const int16_t *)src, p, g, n_tiles, qmin, lay);
     else qt_gather_kernel<int8_t><<<blocks, 256, 0, s>>>((int8_t *)dst, (const int8_t *)src, p, g, n_tiles, qmin, lay);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_records(void *rec, uint64_t n_tiles, int fp64, const GenPrep &g, cudaStream_t s) {
+    int blocks = (int)std::min<uint64_t>((n_tiles + 255) / 256, 148ull * 8);
+    if (fp64) gen_records_kernel<double><<<blocks, 256, 0, s>>>((unsigned char *)rec, n_tiles, 112, g);
+    else gen_records_kernel<int><<<blocks, 256, 0, s>>>((unsigned char *)rec, n_tiles, 16, g);
     return cudaGetLastError();
 }
 

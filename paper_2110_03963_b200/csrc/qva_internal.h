@@ -52,6 +52,8 @@ constexpr int kCT_BITS = 7;                   // 128 consumer threads
 constexpr int kMaxSteps = 16;
 constexpr int kMaxGroups = 3;
 constexpr int kSmallMaxQubits = 12;           // whole-state-in-one-CTA path
+constexpr int kQGenInt = 3;                   // tile-pass q mode: generated MaxCut q, unit weights
+constexpr int kQGenF64 = 9;                   // tile-pass q mode: generated MaxCut q, fp64 weights
 
 // Register group: which tile-local bits the 5 register-index bits (ebit) and the 7 consumer
 // thread-index bits (tbit) address.  Chosen on the host so that every 8-lane phase of a
@@ -118,6 +120,10 @@ struct TilePassParams {
     int order;               // tile order: 0 interleaved over CTAs, 1 contiguous range per CTA
     // L2 block prefetch (strided tile sets, batch 1): tile t = (block t >> pf_lowbits, chunk
     // c = low bits) prefetches psi_in[((block + 1) << pf_shift) + c * 4096 ...] (64 KiB)
+    // generated MaxCut qualities (qbytes kQGenInt / kQGenF64): qt points at the per-tile records
+    const void *gen_thr;     // [128][8] int / double: per consumer thread {C, beta[5]} of group gq
+    const void *gen_G;       // [32] int / double: G(e) over the 5 register bits of group gq
+    int gen_m;               // number of edges (integer mode: qmin = -gen_m)
     const double2 *psi_in;
     int pf_shift;            // 0: off; else log2(elements per block)
     int pf_lowbits;
@@ -165,6 +171,17 @@ struct LayoutRuns {
 };
 cudaError_t launch_qt_gather(void *dst, const void *src, int qbytes, const TilePassParams &p, const TileGroup &g,
                              uint64_t n_tiles, int qmin, const LayoutRuns &lay, cudaStream_t s);
+// generated MaxCut qualities: per-tile record inputs (kernels_tile.cu gen_records_kernel)
+struct GenPrep {
+    LayoutRuns tmap;         // tile-number bits -> logical qubits of the coordinates
+    uint64_t const_val;      // logical bits fixed for this shard (rank bits), 0 elsewhere
+    int n_tt, n_tb, w_unit;  // edge counts; unit weights
+    const int2 *tt_uv;       // [n_tt] logical (u, v): both endpoints outside the tile
+    const double *tt_w;
+    const int2 *tb_ab;       // [n_tb] (tile-local bit a, logical b outside the tile)
+    const double *tb_w;
+};
+cudaError_t launch_gen_records(void *rec, uint64_t n_tiles, int fp64, const GenPrep &g, cudaStream_t s);
 // out[logical(x)] = in[x] (restores the natural layout of a permuted state)
 cudaError_t launch_permute_copy(double2 *out, const double2 *in, uint64_t n, const LayoutRuns &lay, cudaStream_t s);
 // phase tables tab[b][j] = exp(-i gammas[b] (qmin + j)), j < ntab (same fp64 sincos as the

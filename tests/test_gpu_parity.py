@@ -88,6 +88,53 @@ def test_tile_path_full_state(Q, n, p, weighted):
         _amp_close(P.get_state(), ref)
 
 
+@pytest.mark.parametrize("n,p,weighted", [(14, 2, False), (16, 3, True), (21, 2, False), (22, 3, True)])
+def test_generated_vs_stored_qualities(Q, n, p, weighted):
+    """The same MaxCut problem given as a graph (q generated inside the tile passes, DESIGN.md
+    "On-device qualities") and as a stored q vector (consumer-order copies): both match the
+    oracle; the graph plan also materialises q on demand (get_qualities, step-level phase)."""
+    rng = np.random.default_rng(300 + n)
+    u, v = random_regular_graph(n, 3 if n % 2 == 0 else 4, rng)
+    w = rng.uniform(0, 1, len(u)) if weighted else None
+    theta = rng.uniform(0, math.pi, 2 * p)
+    q = O.maxcut_q(n, u, v, w)
+    ref = O.evolve_x(n, q, theta)
+    with Q.Plan(1 << n, "x", n_qubits=n) as P:
+        P.set_qualities_maxcut(u, v, w)
+        P.evolve(theta)
+        _f_close(P.expectation(), O.expectation(ref, q))
+        _amp_close(P.get_state(), ref)
+        np.testing.assert_allclose(P.get_qualities(), q, rtol=0, atol=1e-12)
+        P.apply_phase(0.37)
+        _amp_close(P.get_state(), O.phase(ref.copy(), q, 0.37))
+        P.set_qualities(q)
+        P.evolve(theta)
+        _f_close(P.expectation(), O.expectation(ref, q))
+        _amp_close(P.get_state(), ref)
+
+
+def test_generated_qualities_batch_and_shards(Q):
+    """Generated q in a batched evolution (members share the per-tile records) and in the
+    virtual-shard schedule (layout B swaps the shard bits with the top local bits)."""
+    n, p = 17, 2
+    rng = np.random.default_rng(77)
+    u, v = erdos_renyi_graph(n, 0.4, rng)
+    w = rng.uniform(0, 1, len(u))
+    q = O.maxcut_q(n, u, v, w)
+    thetas = rng.uniform(0, math.pi, (5, 2 * p))
+    refs = [O.expectation(O.evolve_x(n, q, th), q) for th in thetas]
+    with Q.Plan(1 << n, "x", n_qubits=n, max_batch=5) as P:
+        P.set_qualities_maxcut(u, v, w)
+        f = P.evolve_batch(thetas)
+        for a, b in zip(f, refs):
+            _f_close(a, b)
+    with Q.Plan(1 << n, "x", n_qubits=n, virtual_shards=4) as P:
+        P.set_qualities_maxcut(u, v, w)
+        P.evolve(thetas[0])
+        _f_close(P.expectation(), refs[0])
+        _amp_close(P.get_state(), O.evolve_x(n, q, thetas[0]))
+
+
 def test_tile_path_p0_and_norm(Q):
     n = 14
     q = np.linspace(-1, 1, 1 << n)
