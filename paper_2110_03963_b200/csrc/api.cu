@@ -199,9 +199,10 @@ static std::vector<PassPlan> perm_passes(int L, int p, std::vector<int> *final_l
             pp.phase = next_phase;
             cur_layer = next_phase++;
             uint64_t r2 = all & tl;
-            // a layer-boundary pass leaves the three row bits (always tile bits) to the next pass
-            // of the layer, so its shape stays the compiled X Y | P | Y X program
-            if (r1 && (all & ~tl)) r2 &= ~7ull;
+            // a phase pass leaves the three row bits (always tile bits) to the next pass of the
+            // layer: layer boundaries keep the compiled X Y | P | Y X shape, and the first pass
+            // (write-only, compute-bound) drops its W group (P | X Y)
+            if (all & ~tl) r2 &= ~7ull;
             pending = all & ~r2;
             pp.r2 = local_mask(r2);
             pp.a2 = r2 ? cur_layer : -1;
@@ -388,7 +389,7 @@ static int match_prog(const TilePassParams &tp) {
     for (int q = 1; q < kNumTileProgs; ++q) {
         const TileProg &D = kTileProgs[q];
         if (D.n != tp.n_steps || D.expect != (tp.expect != 0)) continue;
-        if ((q == 5) != (tp.init == 1)) continue;  // program 5 starts from |+> without a load
+        if ((q == 5 || q == 6) != (tp.init == 1)) continue;  // programs 5, 6 start from |+> without a load
         bool ok = true;
         for (int k = 0; k < D.n && ok; ++k) {
             const PassStep &st = tp.steps[k];
@@ -1130,6 +1131,32 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             ++j;
         }
     }
+    // The dropped rotation factors are scalars per member, so they commute with every pass: carry
+    // them forward and fold them into the next integer phase table (free) or apply them at the
+    // next fp64 phase / the last pass, instead of a complex multiply per amplitude in every pass.
+    std::vector<char> apply_scale(n_tile_passes, 0);
+    std::vector<double2> tab_mult;  // [phase table row][batch]
+    {
+        std::vector<double2> carry(batch, make_double2(1.0, 0.0));
+        int j = 0;
+        for (size_t pi = 0; pi < passes.size(); ++pi) {
+            const PassPlan &pp = passes[pi];
+            if (pp.exchange) continue;
+            const bool last = (j == n_tile_passes - 1);
+            const bool fold_tab = pp.phase >= 0 && int_table;
+            const bool fold_here = (pp.phase >= 0 && !int_table) || last;
+            for (int b = 0; b < batch; ++b) {
+                PassAngles &a = ang[(size_t)j * batch + b];
+                const double2 f = a.scale, c = carry[b];
+                carry[b] = make_double2(c.x * f.x - c.y * f.y, c.x * f.y + c.y * f.x);
+                if (fold_tab) tab_mult.push_back(carry[b]);
+                if (fold_here) a.scale = carry[b];
+                if (fold_tab || fold_here) carry[b] = make_double2(1.0, 0.0);
+            }
+            apply_scale[j] = fold_here ? 1 : 0;
+            ++j;
+        }
+    }
     QVA_CUDA_TRY(cudaMemcpyAsync(P->d_angles, ang.data(), ang.size() * sizeof(PassAngles), cudaMemcpyHostToDevice,
                                  P->stream));
     const int ntab = gen == kQGenInt ? P->g_m + 1 : (int_table ? (P->qmax - P->qmin + 1) : 0);
@@ -1148,8 +1175,15 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         }
         QVA_CUDA_TRY(cudaMemcpyAsync(P->d_gam, gam.data(), gam.size() * sizeof(double), cudaMemcpyHostToDevice,
                                      P->stream));
-        ProfScope ps(P, K_OTHER, 16.0 * gam.size() * ntab);
-        QVA_CUDA_TRY(launch_phase_table(P->d_tab, P->d_gam, (int)gam.size(), tab_qmin, ntab, P->stream));
+        double2 *d_mult = nullptr;
+        QVA_CUDA_TRY(cudaMallocAsync((void **)&d_mult, gam.size() * sizeof(double2), P->stream));
+        QVA_CUDA_TRY(cudaMemcpyAsync(d_mult, tab_mult.data(), gam.size() * sizeof(double2), cudaMemcpyHostToDevice,
+                                     P->stream));
+        {
+            ProfScope ps(P, K_OTHER, 16.0 * gam.size() * ntab);
+            QVA_CUDA_TRY(launch_phase_table(P->d_tab, P->d_gam, d_mult, (int)gam.size(), tab_qmin, ntab, P->stream));
+        }
+        QVA_CUDA_TRY(cudaFreeAsync(d_mult, P->stream));
     }
     uint64_t n_tiles = P->arr_n >> kTileBits;
     bool any_expect = false;
@@ -1245,7 +1279,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         tp.angles = P->d_angles + (size_t)j * batch;
         tp.expect = pp.expect ? 1 : 0;
         tp.partials = P->partials;
-        tp.apply_scale = (pp.r1 | pp.r2) ? 1 : 0;
+        tp.apply_scale = apply_scale[j];
         // last step touching shared memory: a group switch (smem transpose) or the phase (q stage)
         tp.release_step = (tp.init == 1 && tp.gq < 0) ? -1 : 0;
         for (int k = 0; k < tp.n_steps; ++k)

@@ -59,13 +59,21 @@ __device__ __forceinline__ void block_reduce2(double &a, double &b, double *red)
     }
 }
 
-__global__ void phase_table_kernel(double2 *tab, const double *gammas, int batch, int qmin, int ntab) {
+// tab[b][j] = exp(-i gamma_b (qmin + j)) * mult_b (mult: the scalar factors the passes defer to
+// the phase, see run_passes; nullptr = 1)
+__global__ void phase_table_kernel(double2 *tab, const double *gammas, const double2 *mult, int batch, int qmin,
+                                   int ntab) {
     int total = batch * ntab;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
         int b = k / ntab, j = k - b * ntab;
         double sn, cs;
         sincos(gammas[b] * (double)(qmin + j), &sn, &cs);
-        tab[k] = make_double2(cs, -sn);
+        double2 f = make_double2(cs, -sn);
+        if (mult) {
+            const double2 m = mult[b];
+            f = make_double2(f.x * m.x - f.y * m.y, f.x * m.y + f.y * m.x);
+        }
+        tab[k] = f;
     }
 }
 
@@ -284,9 +292,10 @@ inline int grid_for(uint64_t n, int threads) {
 
 }  // namespace
 
-cudaError_t launch_phase_table(double2 *tab, const double *gammas, int batch, int qmin, int ntab, cudaStream_t s) {
+cudaError_t launch_phase_table(double2 *tab, const double *gammas, const double2 *mult, int batch, int qmin,
+                               int ntab, cudaStream_t s) {
     int total = batch * ntab;
-    phase_table_kernel<<<(total + 255) / 256, 256, 0, s>>>(tab, gammas, batch, qmin, ntab);
+    phase_table_kernel<<<(total + 255) / 256, 256, 0, s>>>(tab, gammas, mult, batch, qmin, ntab);
     return cudaGetLastError();
 }
 

@@ -140,7 +140,7 @@ struct TileProg {
     int phase_k;
     bool expect;
 };
-constexpr int kNumTileProgs = 6;
+constexpr int kNumTileProgs = 7;
 constexpr TileProg kTileProgs[kNumTileProgs] = {
     {0, {0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}, -1, false},  // 0: generic
     {2, {0, 1, 0, 0, 0}, {1, 1, 0, 0, 0}, -1, false},  // 1: X Y            (B/C pass)
@@ -148,6 +148,7 @@ constexpr TileProg kTileProgs[kNumTileProgs] = {
     {4, {0, 1, 1, 0, 0}, {1, 1, 1, 1, 0}, 1, false},   // 3: X Y | P | Y X  (B/C pass across a layer boundary)
     {2, {0, 1, 0, 0, 0}, {1, 1, 0, 0, 0}, -1, true},   // 4: X Y + <Q>      (last pass)
     {4, {0, 0, 2, 1, 0}, {0, 1, 1, 1, 0}, 0, false},   // 5: P | X W Y      (first pass, from |+>)
+    {3, {0, 0, 1, 0, 0}, {0, 1, 1, 0, 0}, 0, false},   // 6: P | X Y        (first pass, row bits deferred)
 };
 
 int tile_pass_grid(uint64_t items);
@@ -184,9 +185,10 @@ struct GenPrep {
 cudaError_t launch_gen_records(void *rec, uint64_t n_tiles, int fp64, const GenPrep &g, cudaStream_t s);
 // out[logical(x)] = in[x] (restores the natural layout of a permuted state)
 cudaError_t launch_permute_copy(double2 *out, const double2 *in, uint64_t n, const LayoutRuns &lay, cudaStream_t s);
-// phase tables tab[b][j] = exp(-i gammas[b] (qmin + j)), j < ntab (same fp64 sincos as the
-// per-element path, so integer-valued q give identical factors)
-cudaError_t launch_phase_table(double2 *tab, const double *gammas, int batch, int qmin, int ntab, cudaStream_t s);
+// phase tables tab[b][j] = exp(-i gammas[b] (qmin + j)) * mult[b], j < ntab (same fp64 sincos as
+// the per-element path; mult = deferred scalar factors of the rotations, nullptr = 1)
+cudaError_t launch_phase_table(double2 *tab, const double *gammas, const double2 *mult, int batch, int qmin,
+                               int ntab, cudaStream_t s);
 // integer-valuedness / range of q: out[0] = all integer (1/0), out[1] = min, out[2] = max
 cudaError_t launch_q_range(const double *q, uint64_t n, int *flags, double *minmax_partials, int blocks,
                            cudaStream_t s);
