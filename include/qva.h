@@ -76,7 +76,10 @@ typedef struct {
                                 must be 1.  0 or 1: normal                                        */
     void *stream;            /* cudaStream_t to launch on, or NULL (the plan creates one)         */
     int32_t max_batch;       /* largest B for qva_evolve_batch (0 -> 1)                           */
-    int32_t reserved[7];
+    int32_t reserved[7];     /* reserved[0]: 1 = replicated mode (every rank holds the whole state;
+                                batches shard over ranks).  reserved[1]: 1 = generate weighted MaxCut
+                                qualities inside the tile passes at every size (default: from 2^26
+                                amplitudes).  Others must be 0. */
 } qva_plan_desc;
 
 /* ---- lifecycle (Table 1 plan / destroy) ------------------------------------ */

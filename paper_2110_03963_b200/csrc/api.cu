@@ -874,6 +874,7 @@ qva_status to_natural_perm(qva_plan *P) {
 
 // ---- generated MaxCut qualities ---------------------------
 constexpr int kGenIntMaxEdges = 4000;  // integer path: cut in [0, m], phase table of m + 1 entries
+constexpr int kGenF64MinQubits = 26;   // weighted graphs: generate q in the pass from 2^26 amplitudes
 
 bool use_qgen(const qva_plan *P) {
     static int env = [] {
@@ -1075,7 +1076,12 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
     int n_tile_passes = 0;
     for (auto &pp : passes) n_tile_passes += !pp.exchange;
     // graph-defined q: generated inside the passes (integer table path for unit weights)
-    const int gen = use_qgen(P) ? ((P->g_unit && P->g_m <= kGenIntMaxEdges) ? kQGenInt : kQGenF64) : 0;
+    // (weighted graphs: generated fp64 q adds ~3 fp64 adds per amplitude next to the sincos, which
+    // measured 7% slower on the compute-bound L2-resident cfg2 batch; it pays where HBM bounds the
+    // pass, i.e. large states)
+    const bool gen_int = P->g_unit && P->g_m <= kGenIntMaxEdges;
+    const bool f64_ok = P->L >= kGenF64MinQubits || P->d.reserved[1] != 0;
+    const int gen = use_qgen(P) && (gen_int || f64_ok) ? (gen_int ? kQGenInt : kQGenF64) : 0;
     if (!gen && P->q_set && !P->q_classified) {
         QVA_TRY(classify_q(P));
         P->q_classified = true;

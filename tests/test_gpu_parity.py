@@ -99,7 +99,7 @@ def test_generated_vs_stored_qualities(Q, n, p, weighted):
     theta = rng.uniform(0, math.pi, 2 * p)
     q = O.maxcut_q(n, u, v, w)
     ref = O.evolve_x(n, q, theta)
-    with Q.Plan(1 << n, "x", n_qubits=n) as P:
+    with Q.Plan(1 << n, "x", n_qubits=n, qgen_f64_always=True) as P:
         P.set_qualities_maxcut(u, v, w)
         P.evolve(theta)
         _f_close(P.expectation(), O.expectation(ref, q))
@@ -123,12 +123,13 @@ def test_generated_qualities_batch_and_shards(Q):
     q = O.maxcut_q(n, u, v, w)
     thetas = rng.uniform(0, math.pi, (5, 2 * p))
     refs = [O.expectation(O.evolve_x(n, q, th), q) for th in thetas]
-    with Q.Plan(1 << n, "x", n_qubits=n, max_batch=5) as P:
-        P.set_qualities_maxcut(u, v, w)
-        f = P.evolve_batch(thetas)
-        for a, b in zip(f, refs):
-            _f_close(a, b)
-    with Q.Plan(1 << n, "x", n_qubits=n, virtual_shards=4) as P:
+    for always in (True, False):
+        with Q.Plan(1 << n, "x", n_qubits=n, max_batch=5, qgen_f64_always=always) as P:
+            P.set_qualities_maxcut(u, v, w)
+            f = P.evolve_batch(thetas)
+            for a, b in zip(f, refs):
+                _f_close(a, b)
+    with Q.Plan(1 << n, "x", n_qubits=n, virtual_shards=4, qgen_f64_always=True) as P:
         P.set_qualities_maxcut(u, v, w)
         P.evolve(thetas[0])
         _f_close(P.expectation(), refs[0])
