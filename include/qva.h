@@ -187,11 +187,13 @@ qva_status qva_x_schedule(int32_t n_local, int32_t p, int32_t *out, int32_t cap,
  *  of R1, logical-qubit mask of R2, TMA dims of the pass}.  cap = passes that fit in out.
  * QVA_ERR_INVALID_ARGUMENT unless 21 <= n_local <= 40 and p >= 1. */
 qva_status qva_x_schedule_permuted(int32_t n_local, int32_t p, int64_t *out, int32_t cap, int32_t *n_passes);
-/* Host-only: the FFT plan the circulant mixer uses for dimension dim (Sec. 3).
+/* Host-only: the FFT plan the circulant mixer uses for dimension dim over `shards` COMM-psi shards
+ * (1 = single GPU; > 1: direct four-step with shards | M1 and shards | M2) (Sec. 3,
+ * PAPER.md:315-333).
  * out[6] = {kind (0: one-CTA whole evolution, 1: four-step mixed radix with M = dim, 2: Bluestein
  * with M >= 2 dim - 1; -1: none), transform length M, M1, M2 (M = M1 * M2), columns per column-pass
  * CTA, rows per row-pass CTA}.  QVA_ERR_UNSUPPORTED when no plan exists (M would exceed 8192^2). */
-qva_status qva_circulant_plan_shape(uint64_t dim, int64_t *out);
+qva_status qva_circulant_plan_shape(uint64_t dim, int32_t shards, int64_t *out);
 /* Kernel timing: when enabled, every kernel launch of the plan is bracketed with CUDA events
  * on the plan's stream; qva_kernel_stats returns, for kernel class `which` (0 = X tile pass,
  * 1 = small-state fused evolve, 2 = FFT column pass, 3 = FFT row pass, 4 = sparse SpMV,

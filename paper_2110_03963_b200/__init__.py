@@ -80,7 +80,7 @@ def _load():
         "qva_exchange_plan": [i32, i32, P, P],
         "qva_x_schedule": [i32, i32, P, i32, ctypes.POINTER(i32)],
         "qva_x_schedule_permuted": [i32, i32, P, i32, ctypes.POINTER(i32)],
-        "qva_circulant_plan_shape": [ctypes.c_uint64, P],
+        "qva_circulant_plan_shape": [ctypes.c_uint64, i32, P],
         "qva_set_profiling": [P, i32],
         "qva_kernel_stats": [P, i32, ctypes.POINTER(d), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(d)],
         "qva_reset_kernel_stats": [P],
@@ -157,10 +157,10 @@ def qva_x_schedule_permuted(n_local: int, p: int):
     return [dict(zip(keys, (int(x) for x in out[8 * i:8 * i + 8]))) for i in range(min(n.value, cap))]
 
 
-def qva_circulant_plan_shape(dim: int):
+def qva_circulant_plan_shape(dim: int, shards: int = 1):
     """dict(kind, M, M1, M2, cw, rb) of the circulant mixer's FFT plan (include/qva.h)."""
     out = np.zeros(6, np.int64)
-    _call("qva_circulant_plan_shape", dim, _ptr(out))
+    _call("qva_circulant_plan_shape", dim, shards, _ptr(out))
     return dict(zip(("kind", "M", "M1", "M2", "cw", "rb"), (int(x) for x in out)))
 
 

@@ -482,6 +482,8 @@ struct qva_plan {
     std::vector<std::vector<int>> sets;
     // circulant
     FftPlan *fft = nullptr;
+    int fft_M1 = 0, fft_M2 = 0;   // four-step split (sharded transposes)
+    void *xfer = nullptr;         // NCCL staging buffer of the sharded circulant path
     double *lambda_perm = nullptr;
     bool lam_set = false, lam_const = false;
     double lam0 = 0.0, lamc = 0.0;
@@ -1393,6 +1395,85 @@ bool use_permuted(const qva_plan *P) {
     return env != 0 && P->mixer == QVA_MIXER_X && P->G == 1 && P->L >= 21 && !P->perm_failed;
 }
 
+// ---- sharded circulant transport: row layout <-> column layout ----------------
+// Row layout: shard s holds rows [s M1/G, (s+1) M1/G) of the M1 x M2 natural matrix; column
+// layout: all rows of columns [s M2/G, (s+1) M2/G).  Virtual shards (one GPU): one block transpose
+// of the whole array.  Real ranks: pack (block transpose) + grouped NCCL send/recv (+ unpack).
+template <typename T>
+qva_status shard_to_col(qva_plan *P, const T *row, T *col) {
+    const int G = P->G;
+    const uint64_t M1 = P->fft_M1, M2 = P->fft_M2, M1s = M1 / G, M2s = M2 / G;
+    ProfScope ps(P, K_EXCHANGE, 2.0 * sizeof(T) * (double)P->arr_n);
+    if (P->world == 1) {
+        QVA_CUDA_TRY(launch_block_transpose<T>(col, row, M1, (uint64_t)G, M2s, P->stream));
+        return QVA_OK;
+    }
+    T *snd = reinterpret_cast<T *>(P->xfer);
+    QVA_CUDA_TRY(launch_block_transpose<T>(snd, row, M1s, (uint64_t)G, M2s, P->stream));
+    const uint64_t chunk = M1s * M2s;
+    const size_t cnt = chunk * sizeof(T) / sizeof(double);
+    QVA_NCCL_TRY(ncclGroupStart());
+    for (int s = 0; s < G; ++s) {
+        if (s == P->rank) continue;
+        QVA_NCCL_TRY(ncclSend((const double *)(snd + s * chunk), cnt, ncclDouble, s, P->comm, P->stream));
+        QVA_NCCL_TRY(ncclRecv((double *)(col + s * chunk), cnt, ncclDouble, s, P->comm, P->stream));
+    }
+    QVA_NCCL_TRY(ncclGroupEnd());
+    QVA_CUDA_TRY(cudaMemcpyAsync(col + P->rank * chunk, snd + P->rank * chunk, chunk * sizeof(T),
+                                 cudaMemcpyDeviceToDevice, P->stream));
+    return QVA_OK;
+}
+template <typename T>
+qva_status shard_to_row(qva_plan *P, const T *col, T *row) {
+    const int G = P->G;
+    const uint64_t M1 = P->fft_M1, M2 = P->fft_M2, M1s = M1 / G, M2s = M2 / G;
+    ProfScope ps(P, K_EXCHANGE, 2.0 * sizeof(T) * (double)P->arr_n);
+    if (P->world == 1) {
+        QVA_CUDA_TRY(launch_block_transpose<T>(row, col, (uint64_t)G, M1, M2s, P->stream));
+        return QVA_OK;
+    }
+    T *rcv = reinterpret_cast<T *>(P->xfer);
+    const uint64_t chunk = M1s * M2s;
+    const size_t cnt = chunk * sizeof(T) / sizeof(double);
+    QVA_NCCL_TRY(ncclGroupStart());
+    for (int s = 0; s < G; ++s) {
+        if (s == P->rank) continue;
+        QVA_NCCL_TRY(ncclSend((const double *)(col + s * chunk), cnt, ncclDouble, s, P->comm, P->stream));
+        QVA_NCCL_TRY(ncclRecv((double *)(rcv + s * chunk), cnt, ncclDouble, s, P->comm, P->stream));
+    }
+    QVA_NCCL_TRY(ncclGroupEnd());
+    QVA_CUDA_TRY(cudaMemcpyAsync(rcv + P->rank * chunk, col + P->rank * chunk, chunk * sizeof(T),
+                                 cudaMemcpyDeviceToDevice, P->stream));
+    QVA_CUDA_TRY(launch_block_transpose<T>(row, rcv, (uint64_t)G, M1s, M2s, P->stream));
+    return QVA_OK;
+}
+
+struct PlanShardIO : FftShardIO {
+    qva_plan *P;
+    explicit PlanShardIO(qva_plan *P_) : P(P_) {}
+    qva_status to_col(const double2 *row, double2 *col) override { return shard_to_col<double2>(P, row, col); }
+    qva_status to_row(const double2 *col, double2 *row) override { return shard_to_row<double2>(P, col, row); }
+};
+
+// buffers of the sharded circulant path: column-layout work array (psi_alt), q in the column
+// layout (qB), NCCL staging (xfer)
+qva_status circ_shard_setup(qva_plan *P, PlanShardIO &io) {
+    if (!P->psi_alt) QVA_CUDA_TRY(cudaMalloc(&P->psi_alt, P->arr_n * sizeof(double2)));
+    if (P->world > 1 && !P->xfer) QVA_CUDA_TRY(cudaMalloc(&P->xfer, P->arr_n * sizeof(double2)));
+    if (P->q_set && !P->qB_valid) {
+        QVA_TRY(ensure_q_dev(P));
+        if (!P->qB) QVA_CUDA_TRY(cudaMalloc(&P->qB, P->arr_n * sizeof(double)));
+        QVA_TRY(shard_to_col<double>(P, P->q, P->qB));
+        P->qB_valid = true;
+    }
+    io.G = P->G;
+    io.local = P->world == 1 ? P->G : 1;
+    io.first = P->world == 1 ? 0 : P->rank;
+    io.col = P->psi_alt;
+    io.q_col = P->qB;
+    return QVA_OK;
+}
+
 // apply one mixer on the current state (no phase)
 qva_status apply_mixer_impl(qva_plan *P, double beta) {
     if (P->mixer == QVA_MIXER_X) {
@@ -1430,6 +1511,11 @@ qva_status apply_mixer_impl(qva_plan *P, double beta) {
         r.theta = &beta;
         r.mode = 1;
         PlanObserver obs(P);
+        if (P->G > 1) {
+            PlanShardIO io(P);
+            QVA_TRY(circ_shard_setup(P, io));
+            return fft_run_sharded(P->fft, r, io, P->stream, &obs);
+        }
         return fft_run(P->fft, r, P->stream, &obs);
     }
     if (P->mixer == QVA_MIXER_SPARSE) {
@@ -1572,9 +1658,9 @@ qva_status qva_x_schedule_permuted(int32_t n_local, int32_t p, int64_t *out, int
     return QVA_OK;
 }
 
-qva_status qva_circulant_plan_shape(uint64_t dim, int64_t *out) {
-    if (!out) return QVA_ERR_INVALID_ARGUMENT;
-    const FftShape sh = fft_plan_shape(dim);
+qva_status qva_circulant_plan_shape(uint64_t dim, int32_t shards, int64_t *out) {
+    if (!out || shards < 1) return QVA_ERR_INVALID_ARGUMENT;
+    const FftShape sh = fft_plan_shape(dim, shards);
     out[0] = sh.ok ? (sh.whole ? 0 : (sh.bluestein ? 2 : 1)) : -1;
     out[1] = (int64_t)sh.M;
     out[2] = sh.M1;
@@ -1603,6 +1689,7 @@ qva_status qva_plan_destroy(qva_plan *P) {
     harvest(P);
     cudaFree(P->psi);
     cudaFree(P->psi_alt);
+    cudaFree(P->xfer);
     cudaFree(P->psi0);
     cudaFree(P->q);
     cudaFree(P->qB);
@@ -1656,10 +1743,16 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
         }
     }
     int G = replicated ? 1 : d.world * vs;
-    if (G > 1) {
+    if (G > 1 && d.mixer == QVA_MIXER_CIRCULANT) {
+        // distributed four-step FFT: needs G | M1 and G | M2 (checked on the FFT plan)
+        if (d.dim % (uint64_t)G) {
+            set_error("sharded circulant mixer needs dim divisible by the shard count");
+            return QVA_ERR_UNSUPPORTED;
+        }
+    } else if (G > 1) {
         if (d.mixer != QVA_MIXER_X) {
-            set_error("sharded state (world*virtual_shards > 1) is implemented for the X mixer only; "
-                      "use the replicated mode (reserved[0]=1) for batches of circulant/sparse evolutions");
+            set_error("sharded state (world*virtual_shards > 1) is implemented for the X and circulant mixers; "
+                      "use the replicated mode (reserved[0]=1) for batches of sparse evolutions");
             return QVA_ERR_UNSUPPORTED;
         }
         if (!is_pow2((uint64_t)G)) {
@@ -1731,8 +1824,18 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
     }
     if (d.mixer == QVA_MIXER_X && P->L >= kTileBits) P->sets = make_tile_sets(P->L);
     if (d.mixer == QVA_MIXER_CIRCULANT) {
-        qva_status s = fft_plan_create(P->N, P->device, &P->fft);
+        qva_status s = fft_plan_create(P->N, P->device, G, &P->fft);
         if (s != QVA_OK) return fail(s);
+        {
+            const FftShape sh = fft_plan_shape(P->N, G);
+            P->fft_M1 = sh.M1;
+            P->fft_M2 = sh.M2;
+        }
+        if (G > 1 && !fft_shardable(P->fft, G)) {
+            set_error("sharded circulant mixer: dim " + std::to_string(P->N) + " has no four-step split M1*M2 with " +
+                      std::to_string(G) + " | M1 and M2 (prime-heavy dims need the single-GPU Bluestein path)");
+            return fail(QVA_ERR_UNSUPPORTED);
+        }
     }
     if (d.world > 1) {
         if (!d.nccl_unique_id) {
@@ -2103,7 +2206,13 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
         r.expect = p > 0;
         r.red_out = P->red;
         PlanObserver obs(P);
-        QVA_TRY(fft_run(P->fft, r, P->stream, &obs));
+        if (P->G > 1) {
+            PlanShardIO io(P);
+            QVA_TRY(circ_shard_setup(P, io));
+            QVA_TRY(fft_run_sharded(P->fft, r, io, P->stream, &obs));
+        } else {
+            QVA_TRY(fft_run(P->fft, r, P->stream, &obs));
+        }
         *have_red = p > 0;
         return QVA_OK;
     }

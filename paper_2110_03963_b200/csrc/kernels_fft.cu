@@ -377,7 +377,8 @@ struct ColArgs {
     const double *q;
     const double *lam;       // natural-order spectrum for OP_SPEC (nullptr: lam0 / lamc)
     uint64_t N;              // state length (mask, chirp)
-    int M1, M2, cw, lcw;     // cw = 2^lcw columns per CTA
+    int M1, M2, cw, lcw;     // cw = 2^lcw columns per CTA; M2 = columns held (row stride)
+    int col_off, M2g;        // sharded column layout: global index of local column 0, global M2
     uint64_t m1mag;          // divu magic of M1
     int init;                // 1: v = amp0 for x < N (no load)
     int do_inv, do_fwd, ops;
@@ -416,7 +417,8 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_col_kernel(const ColArgs a
         double acc = 0.0, nrm = 0.0;
         for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
             const int c = (int)divu(idx, a.m1mag), x1 = idx - c * M1;
-            const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
+            const uint64_t xl = (uint64_t)x1 * M2 + c0 + c;                  // local (q) index
+            const uint64_t x = (uint64_t)x1 * a.M2g + a.col_off + c0 + c;    // natural index
             double2 &slot = A[c * stride + x1];
             double2 v = slot;
             if ((ops & OP_MASK) && x >= a.N) {
@@ -425,10 +427,10 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_col_kernel(const ColArgs a
                 if (ops & OP_CHIRP_CONJ) v = cmulc(v, chirp(x, a.N));
                 if (ops & OP_EXPECT) {
                     const double pr = v.x * v.x + v.y * v.y;
-                    acc = fma(pr, __ldg(a.q + x), acc);
+                    acc = fma(pr, __ldg(a.q + xl), acc);
                     nrm += pr;
                 }
-                if (ops & OP_PHASE) v = phase_mul(v, __ldg(a.q + x), a.gamma);
+                if (ops & OP_PHASE) v = phase_mul(v, __ldg(a.q + xl), a.gamma);
                 if (ops & OP_SPEC) {
                     const double lam = a.lam ? __ldg(a.lam + x) : (x == 0 ? a.lam0 : a.lamc);
                     double s, cs;
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_col_kernel(const ColArgs a
         run_fft(A, a.sf, a.tw, cwv, stride, false);
         for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
             const int c = (int)divu(idx, a.m1mag), k1 = idx - c * M1;
-            const uint64_t r = (uint64_t)(c0 + c) * (uint64_t)k1;  // < M: no reduction needed
+            const uint64_t r = (uint64_t)(a.col_off + c0 + c) * (uint64_t)k1;  // < M: no reduction needed
             A[c * stride + k1] = cmul(A[c * stride + k1], big_twiddle(a.big_lo, a.big_hi, a.big_shift, r, false));
         }
         __syncthreads();
@@ -468,6 +470,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_col_kernel(const ColArgs a
 struct RowArgs {
     double2 *buf;
     int M1, M2, rb;
+    int row_off;                // sharded row layout: global index of local row 0
     uint64_t m2mag;             // divu magic of M2
     int fwd_only;               // 1: forward FFT only (spectrum out, no twiddle)
     int spec;                   // 0: constant (e0 at bin 0, ec elsewhere); 1: real lambda; 2: complex array
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
     extern __shared__ __align__(16) unsigned char smem_raw[];
     load_roots();
     const int M2 = a.M2;
-    const int k1_0 = blockIdx.x * a.rb;
+    const int k1_0 = blockIdx.x * a.rb;  // local row; global row = row_off + local
     double2 *A = reinterpret_cast<double2 *>(smem_raw);
     double2 *rows = a.buf + (uint64_t)k1_0 * M2;
     const int tot = a.rb * M2;
@@ -499,7 +502,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
     }
     for (int i = threadIdx.x; i < tot; i += blockDim.x) {
         const int r = (int)divu(i, a.m2mag), k2 = i - r * M2;
-        const int k1 = k1_0 + r;
+        const int k1 = a.row_off + k1_0 + r;
         const uint64_t pos = (uint64_t)k1 * M2 + k2;
         double2 e;
         if (a.spec == 1) {
@@ -518,7 +521,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
     run_fft(A, a.sf, a.tw, a.rb, M2, true);
     for (int i = threadIdx.x; i < tot; i += blockDim.x) {
         const int r = (int)divu(i, a.m2mag), x2 = i - r * M2;
-        const uint64_t tr = (uint64_t)x2 * (uint64_t)(k1_0 + r);  // < M
+        const uint64_t tr = (uint64_t)x2 * (uint64_t)(a.row_off + k1_0 + r);  // < M
         rows[i] = cmul(A[i], big_twiddle(a.big_lo, a.big_hi, a.big_shift, tr, true));
     }
 }
@@ -647,13 +650,14 @@ struct Split {
 // four-step split M = M1 * M2: both 13-smooth, M2 <= kMaxSub, cw * M1 <= kMaxCta and the
 // padded column block fits shared memory; widest column block first (cw = 8: 128-B rows),
 // then the most balanced split
-Split choose_split(uint64_t M) {
+Split choose_split(uint64_t M, int G = 1) {
     Split best;
     double best_score = -1e300;
     for (uint64_t m1 = 2; m1 <= (uint64_t)kMaxSub && m1 <= M; ++m1) {
         if (M % m1) continue;
         const uint64_t m2 = M / m1;
         if (m2 < 2 || m2 > (uint64_t)kMaxSub || !sub_ok((int)m1) || !sub_ok((int)m2)) continue;
+        if (m1 % G || m2 % G) continue;  // sharded: whole row / column blocks per shard
         int cw = 0;
         for (int c : {8, 4, 2, 1})
             if ((uint64_t)c * m1 <= (uint64_t)kMaxCta && (size_t)c * (m1 + 1) * sizeof(double2) <= kColSmemMax) {
@@ -709,6 +713,8 @@ ColArgs col_args(const FftPlan *fp) {
     c.M2 = fp->M2;
     c.cw = fp->cw;
     c.lcw = fp->cw == 8 ? 3 : fp->cw == 4 ? 2 : fp->cw == 2 ? 1 : 0;
+    c.col_off = 0;
+    c.M2g = fp->M2;
     c.m1mag = div_magic((uint32_t)fp->M1);
     c.invN = 1.0 / (double)fp->N;
     c.tw = fp->d_tw;
@@ -740,9 +746,20 @@ int row_grid(const FftPlan *fp) { return fp->M1 / fp->rb; }
 
 // Pure host planning (no device resources): whole-CTA, direct four-step or Bluestein, and the
 // split.  Exposed through qva_circulant_plan_shape for CPU tests.
-FftShape fft_plan_shape(uint64_t N) {
+FftShape fft_plan_shape(uint64_t N, int G) {
     FftShape sh;
     sh.N = N;
+    if (G > 1) {  // sharded: direct four-step with G | M1, G | M2 only
+        Split sp = (N >= 4 && smooth(N)) ? choose_split(N, G) : Split();
+        if (!sp.M1) return sh;
+        sh.ok = true;
+        sh.M = N;
+        sh.M1 = sp.M1;
+        sh.M2 = sp.M2;
+        sh.cw = sp.cw;
+        sh.rb = sp.rb;
+        return sh;
+    }
     if (N >= 1 && N <= 4096 && smooth(N) && sub_ok((int)N)) {
         sh.ok = true;
         sh.whole = true;
@@ -773,7 +790,7 @@ FftShape fft_plan_shape(uint64_t N) {
     return sh;
 }
 
-qva_status fft_plan_create(uint64_t N, int device, FftPlan **out) {
+qva_status fft_plan_create(uint64_t N, int device, int G, FftPlan **out) {
     *out = nullptr;
     FftPlan *fp = new FftPlan();
     fp->N = N;
@@ -784,10 +801,12 @@ qva_status fft_plan_create(uint64_t N, int device, FftPlan **out) {
         return s;
     };
     std::vector<double2> tw;
-    const FftShape sh = fft_plan_shape(N);
+    const FftShape sh = fft_plan_shape(N, G);
     if (!sh.ok)
-        return fail(QVA_ERR_UNSUPPORTED, "circulant mixer: no FFT plan for N=" + std::to_string(N) +
-                                             " (Bluestein length would exceed 8192^2)");
+        return fail(QVA_ERR_UNSUPPORTED,
+                    G > 1 ? "sharded circulant mixer: N=" + std::to_string(N) + " has no four-step split M1*M2 (13-smooth, <= 8192) with " +
+                                std::to_string(G) + " | M1 and M2"
+                          : "circulant mixer: no FFT plan for N=" + std::to_string(N) + " (Bluestein length would exceed 8192^2)");
     fp->whole = sh.whole;
     fp->bluestein = sh.bluestein;
     fp->M = sh.M;
@@ -1040,6 +1059,124 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
         if (r.expect) QVA_TRY(reduce());
     }
     return QVA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// Sharded four-step (COMM-psi for QWOA): G shards hold contiguous row blocks of
+// the natural layout (x = x1*M2 + x2, rows x1 in [s*M1/G, (s+1)*M1/G)); the column pass runs in a
+// column layout (shard s: all x1, columns x2 in [s*M2/G, ...)), reached by an all-to-all
+// transpose (io.to_col / io.to_row: NCCL, or a block transpose for virtual shards).  Two
+// transposes per layer; the row pass runs on the shard's own rows in place.
+// ------------------------------------------------------------------------------------------
+bool fft_shardable(const FftPlan *fp, int G) {
+    return G >= 1 && !fp->whole && !fp->bluestein && fp->M1 % G == 0 && fp->M2 % G == 0;
+}
+
+qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStream_t s, LaunchObserver *obs) {
+    const int G = io.G;
+    if (!fft_shardable(fp, G)) {
+        set_error("circulant mixer: sharding needs a direct four-step plan with G | M1 and G | M2");
+        return QVA_ERR_UNSUPPORTED;
+    }
+    const uint64_t NG = fp->N / G;
+    const int M1s = fp->M1 / G, M2s = fp->M2 / G;
+    const double N = (double)fp->N;
+    ColArgs c = col_args(fp);
+    c.M2 = M2s;
+    c.M2g = fp->M2;
+    c.amp0 = r.amp0;
+    c.cw = std::min(fp->cw, 8);
+    while (c.cw > 1 && M2s % c.cw) c.cw >>= 1;  // keep whole column blocks inside a shard
+    c.lcw = c.cw == 8 ? 3 : c.cw == 4 ? 2 : c.cw == 2 ? 1 : 0;
+    const int gc = (M2s + c.cw - 1) / c.cw;
+    const size_t smem_c = (size_t)c.cw * (fp->M1 + (c.cw > 1 ? 1 : 0)) * sizeof(double2);
+    int rb = 1;
+    for (int x = 2; x <= 64; ++x)
+        if (M1s % x == 0 && x * fp->M2 <= kMaxCta) rb = x;
+    const size_t smem_r = (size_t)rb * fp->M2 * sizeof(double2);
+    if ((size_t)gc * io.local > (size_t)fp->n_partials) {
+        cudaFree(fp->partials);
+        fp->n_partials = gc * io.local;
+        QVA_CUDA_TRY(cudaMalloc(&fp->partials, fp->n_partials * 2 * sizeof(double)));
+    }
+    auto cols = [&](int init, int inv, int ops, double gamma, int fwd) -> qva_status {
+        for (int ls = 0; ls < io.local; ++ls) {
+            c.in = io.col + ls * NG;
+            c.in_len = NG;
+            c.out = io.col + ls * NG;
+            c.out_len = NG;
+            c.q = io.q_col + ls * NG;
+            c.col_off = (io.first + ls) * M2s;
+            c.partials = fp->partials + 2 * (size_t)ls * gc;
+            c.init = init;
+            c.do_inv = inv;
+            c.do_fwd = fwd;
+            c.ops = ops;
+            c.gamma = gamma;
+            obs->begin(K_FFT_COL, 16.0 * NG * (init ? 1 : 2) + ((ops & (OP_PHASE | OP_EXPECT)) ? 8.0 * NG : 0.0));
+            fft_col_kernel<<<gc, kFftThreads, smem_c, s>>>(c);
+            cudaError_t e = cudaGetLastError();
+            obs->end();
+            if (e != cudaSuccess) {
+                set_error(std::string("fft_col_kernel: ") + cudaGetErrorString(e));
+                return QVA_ERR_CUDA;
+            }
+        }
+        return QVA_OK;
+    };
+    auto rows = [&](double beta) -> qva_status {
+        RowArgs w = row_args(fp, r.psi);
+        w.rb = rb;
+        w.row_off = io.first * M1s;
+        if (r.lambda_perm) {
+            w.spec = 1;
+            w.lam_perm = r.lambda_perm;
+            w.beta = beta;
+            w.scale = 1.0 / N;
+        } else {
+            w.spec = 0;
+            w.e0 = make_double2(cos(-beta * r.lam0) / N, sin(-beta * r.lam0) / N);
+            w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
+        }
+        obs->begin(K_FFT_ROW, 32.0 * NG * io.local + (r.lambda_perm ? 8.0 * NG * io.local : 0.0));
+        fft_row_kernel<<<io.local * M1s / rb, kFftThreads, smem_r, s>>>(w);
+        cudaError_t e = cudaGetLastError();
+        obs->end();
+        if (e != cudaSuccess) {
+            set_error(std::string("fft_row_kernel: ") + cudaGetErrorString(e));
+            return QVA_ERR_CUDA;
+        }
+        return QVA_OK;
+    };
+    if (r.mode == 1) {
+        QVA_TRY(io.to_col(r.psi, io.col));
+        QVA_TRY(cols(0, 0, 0, 0.0, 1));
+        QVA_TRY(io.to_row(io.col, r.psi));
+        QVA_TRY(rows(r.theta[0]));
+        QVA_TRY(io.to_col(r.psi, io.col));
+        QVA_TRY(cols(0, 1, 0, 0.0, 0));
+        return io.to_row(io.col, r.psi);
+    }
+    if (!r.init) QVA_TRY(io.to_col(r.psi, io.col));
+    for (int k = 0; k < r.p; ++k) {
+        QVA_TRY(cols(k == 0 ? r.init : 0, k > 0, OP_PHASE, r.theta[2 * k], 1));
+        QVA_TRY(io.to_row(io.col, r.psi));
+        QVA_TRY(rows(r.theta[2 * k + 1]));
+        QVA_TRY(io.to_col(r.psi, io.col));
+    }
+    if (r.p > 0) {
+        QVA_TRY(cols(0, 1, r.expect ? OP_EXPECT : 0, 0.0, 0));
+        if (r.expect) {
+            obs->begin(K_REDUCE, 16.0 * gc * io.local);
+            cudaError_t e = launch_reduce_partials(fp->partials, (uint64_t)gc * io.local, 1, r.red_out, s);
+            obs->end();
+            if (e != cudaSuccess) {
+                set_error(std::string("reduce: ") + cudaGetErrorString(e));
+                return QVA_ERR_CUDA;
+            }
+        }
+    }
+    return io.to_row(io.col, r.psi);
 }
 
 }  // namespace qva

@@ -338,6 +338,27 @@ cudaError_t launch_chunk_transpose(T *out, const T *in, int G, uint64_t C, cudaS
 template cudaError_t launch_chunk_transpose<double2>(double2 *, const double2 *, int, uint64_t, cudaStream_t);
 template cudaError_t launch_chunk_transpose<double>(double *, const double *, int, uint64_t, cudaStream_t);
 
+template <typename T>
+__global__ void block_transpose_kernel(T *__restrict__ out, const T *__restrict__ in, uint64_t A, uint64_t B,
+                                       uint64_t C) {
+    const uint64_t total = A * B * C;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t c = k % C, ab = k / C;
+        const uint64_t b = ab % B, a = ab / B;  // in[a][b][c] (coalesced reads)
+        out[(b * A + a) * C + c] = in[k];
+    }
+}
+
+template <typename T>
+cudaError_t launch_block_transpose(T *out, const T *in, uint64_t A, uint64_t B, uint64_t C, cudaStream_t s) {
+    block_transpose_kernel<T><<<grid_for(A * B * C, 256), 256, 0, s>>>(out, in, A, B, C);
+    return cudaGetLastError();
+}
+template cudaError_t launch_block_transpose<double2>(double2 *, const double2 *, uint64_t, uint64_t, uint64_t,
+                                                     cudaStream_t);
+template cudaError_t launch_block_transpose<double>(double *, const double *, uint64_t, uint64_t, uint64_t,
+                                                    cudaStream_t);
+
 cudaError_t launch_chunk_transpose_bytes(void *out, const void *in, int G, uint64_t C, int elem_bytes, cudaStream_t s) {
     uint64_t total = (uint64_t)G * G * C;
     if (elem_bytes == 1)

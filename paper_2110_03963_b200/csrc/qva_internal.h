@@ -249,8 +249,8 @@ struct FftShape {
     uint64_t N = 0, M = 0;   // state length, transform length
     int M1 = 0, M2 = 0, cw = 0, rb = 0;
 };
-FftShape fft_plan_shape(uint64_t N);
-qva_status fft_plan_create(uint64_t N, int device, FftPlan **out);
+FftShape fft_plan_shape(uint64_t N, int G = 1);  // G > 1: sharded (direct four-step, G | M1, M2)
+qva_status fft_plan_create(uint64_t N, int device, int G, FftPlan **out);
 void fft_plan_destroy(FftPlan *fp);
 // permute lambda (forward-bin order, length N) into the plan's internal spectral order
 void fft_permute_spectrum(const FftPlan *fp, const double *lambda, double *lambda_perm);
@@ -269,6 +269,20 @@ struct FftRun {
     double *red_out = nullptr;         // device [2] receives the reduced pair when expect
 };
 qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver *obs);
+// sharded four-step: r.psi is this process's row block(s) in natural order (local * N/G)
+struct FftShardIO {
+    int G = 1, local = 1, first = 0;  // shards, shards held by this process, global index of local 0
+    double2 *col = nullptr;           // column-layout work array (local * N/G)
+    const double *q_col = nullptr;    // q in the column layout
+    virtual qva_status to_col(const double2 *row, double2 *col) = 0;  // all-to-all transposes
+    virtual qva_status to_row(const double2 *col, double2 *row) = 0;
+    virtual ~FftShardIO() {}
+};
+bool fft_shardable(const FftPlan *fp, int G);
+qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStream_t s, LaunchObserver *obs);
+// out[b][a][c] = in[a][b][c] for an A x B grid of C-element blocks (sharded FFT transposes)
+template <typename T>
+cudaError_t launch_block_transpose(T *out, const T *in, uint64_t A, uint64_t B, uint64_t C, cudaStream_t s);
 
 // ---------------------------------------------------------------------------------------------
 // sparse (CSR truncated Taylor) mixer (kernels_sparse.cu)

@@ -158,6 +158,21 @@ def test_circulant_plan_shapes(Q):
             assert sh["M"] >= 2 * N - 1
 
 
+@pytest.mark.parametrize("N,G", [(3628800, 2), (3628800, 4), (3628800, 8), (6144, 8), (40320, 4), (1 << 20, 8)])
+def test_sharded_circulant_plan_shapes(Q, N, G):
+    """Sharded QWOA: the four-step split keeps whole row blocks (G | M1) and
+    whole column blocks (G | M2) on every shard; non-smooth N has no sharded plan."""
+    sh = Q.qva_circulant_plan_shape(N, G)
+    assert sh["kind"] == 1 and sh["M"] == N and sh["M1"] * sh["M2"] == N
+    assert sh["M1"] % G == 0 and sh["M2"] % G == 0
+
+
+def test_sharded_circulant_prime_unsupported(Q):
+    with pytest.raises(Q.QvaError) as ei:
+        Q.qva_circulant_plan_shape(1000003, 2)
+    assert ei.value.status == 5
+
+
 def test_plan_create_without_gpu_fails_cleanly(Q):
     import torch
     if torch.cuda.is_available():
@@ -175,5 +190,8 @@ def test_plan_argument_errors(Q):
         Q.Plan(1 << 20, "x", n_qubits=20, virtual_shards=3)
     assert ei.value.status == 5  # non power of two shards
     with pytest.raises(Q.QvaError) as ei:
-        Q.Plan(720, "circulant", world=2, rank=0)
+        Q.Plan(721, "circulant", world=2, rank=0)  # sharded QWOA needs shards | dim
+    assert ei.value.status == 5
+    with pytest.raises(Q.QvaError) as ei:
+        Q.Plan(720, "sparse", world=2, rank=0)  # sharded sparse mixer: replicated mode only
     assert ei.value.status == 5

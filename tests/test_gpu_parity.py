@@ -309,6 +309,43 @@ def test_bluestein_complete_graph_vs_closed_form(Q, N):
         _amp_close(P.get_state(), ref)
 
 
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_cfg3_virtual_shards(Q, G):
+    """Sharded QWOA: G row-block shards on one GPU, the column pass in the
+    column layout reached by all-to-all transposes; same state as the unsharded oracle."""
+    wl = make_config("cfg3")
+    ref = O.evolve_complete(wl.q, wl.theta, wl.lam0, wl.lam_rest)
+    with Q.Plan(wl.dim, "circulant", virtual_shards=G) as P:
+        P.set_qualities(wl.q)
+        P.set_circulant_eigenvalues_const(wl.lam0, wl.lam_rest)
+        P.evolve(wl.theta)
+        _f_close(P.expectation(), O.expectation(ref, wl.q), O.expectation(ref, np.abs(wl.q)))
+        _amp_close(P.get_state(), ref)
+
+
+@pytest.mark.parametrize("N,G", [(6144, 2), (6144, 8), (40320, 4)])
+def test_circulant_virtual_shards_random_spectrum(Q, N, G):
+    rng = np.random.default_rng(N + G)
+    q = rng.standard_normal(N)
+    lam = rng.standard_normal(N) * 3
+    theta = rng.uniform(0, math.pi, 6)
+    psi0 = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    psi0 /= np.linalg.norm(psi0)
+    with Q.Plan(N, "circulant", virtual_shards=G) as P:
+        P.set_qualities(q)
+        P.set_circulant_eigenvalues(lam)
+        P.evolve(theta)
+        ref = O.evolve_circulant_dense(q, lam, theta)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+        P.set_initial_state(psi0)
+        P.evolve(theta)
+        _amp_close(P.get_state(), O.evolve_circulant_dense(q, lam, theta, psi0=psi0))
+        P.reset_state()
+        P.apply_mixer(0.7)
+        _amp_close(P.get_state(), O.mixer_circulant_dense(psi0.copy(), lam, 0.7))
+
+
 # ---------------------------------------------------------------- cfg4 full size ----
 def test_cfg4_full_size_vs_golden(Q):
     g = json.load(open(os.path.join(GOLD, "cfg4_n30.json")))
