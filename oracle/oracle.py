@@ -21,6 +21,7 @@ __all__ = [
     "mixer_circulant_dense", "mixer_complete", "expectation", "norm2", "probabilities",
     "evolve_x", "evolve_complete", "evolve_circulant_dense", "lightcone_maxcut",
     "dense_sum_x", "mixer_sparse_dense", "evolve_sparse_dense", "c128",
+    "mixer_parity", "evolve_parity", "parity_pairs",
 ]
 
 
@@ -54,6 +55,8 @@ def lib():
     L.or_evolve_x.argtypes = [i, P, P, P, i]
     L.or_evolve_complete.argtypes = [u64, P, P, P, i, d, d]
     L.or_evolve_circulant_dense.argtypes = [u64, P, P, P, P, i]
+    L.or_mixer_parity.argtypes = [i, P, P, i, d]
+    L.or_evolve_parity.argtypes = [i, P, P, P, i, P, i]
     L.or_lightcone_maxcut.argtypes = [i, i, P, P, P, P, i, i, P]
     L.or_lightcone_maxcut.restype = d
     return L
@@ -165,6 +168,35 @@ def evolve_circulant_dense(q: np.ndarray, lam: np.ndarray, theta,
     q = np.ascontiguousarray(q, np.float64)
     lam = np.ascontiguousarray(lam, np.float64)
     lib().or_evolve_circulant_dense(N, _ptr(psi), _ptr(q), _ptr(lam), _ptr(theta), len(theta) // 2)
+    return psi
+
+
+def parity_pairs(seq):
+    """(B_odd, B_even, B_last) qubit pairs of the QAOAz mixer over the ordered subsequence seq
+    (PAPER.md:213-248 Eq. parity_terms; reading R19: no wrap in B_even, B_last = (s_{K-1}, s_0)
+    iff K is odd)."""
+    K = len(seq)
+    odd = [(seq[m], seq[m + 1]) for m in range(0, K - 1, 2)]
+    even = [(seq[m], seq[m + 1]) for m in range(1, K - 1, 2)]
+    last = [(seq[K - 1], seq[0])] if K >= 3 and K % 2 == 1 else []
+    return odd, even, last
+
+
+def mixer_parity(psi: np.ndarray, seq, t: float) -> np.ndarray:
+    """In place; U_parity(t) = e^{-itB_last} e^{-itB_even} e^{-itB_odd} (PAPER.md Eq. qaoaz_mixers)."""
+    n = int(len(psi)).bit_length() - 1
+    sq = np.ascontiguousarray(seq, np.int32)
+    lib().or_mixer_parity(n, _ptr(psi), _ptr(sq), len(sq), float(t))
+    return psi
+
+
+def evolve_parity(n: int, q: np.ndarray, seq, theta, psi0: np.ndarray) -> np.ndarray:
+    """QAOAz state (PAPER.md Eq. qaoaz) from a given (parity-constrained) initial state."""
+    theta = np.ascontiguousarray(theta, np.float64)
+    psi = np.array(psi0, np.complex128, copy=True)
+    q = np.ascontiguousarray(q, np.float64)
+    sq = np.ascontiguousarray(seq, np.int32)
+    lib().or_evolve_parity(n, _ptr(psi), _ptr(q), _ptr(sq), len(sq), _ptr(theta), len(theta) // 2)
     return psi
 
 

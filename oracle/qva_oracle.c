@@ -102,6 +102,46 @@ OR_API void or_mixer_x(int n, double *psi, double beta) {
     }
 }
 
+/* QAOAz parity mixer (Eqs. parity_terms / qaoaz_mixers; R19):
+ *   U_parity(t) = exp(-i t B_last) exp(-i t B_even) exp(-i t B_odd)
+ * over the ordered qubit subsequence s[0..K): B_odd pairs (s0,s1), (s2,s3), ...; B_even pairs
+ * (s1,s2), (s3,s4), ... (no wrap); B_last = the wrap pair (s_{K-1}, s0) iff K is odd (K >= 3).
+ * Pairs inside one B act on disjoint qubits, so exp(-i t B) is the product of the pair
+ * exponentials.  X_aX_b + Y_aY_b maps |01> <-> |10> with weight 2 and kills |00>, |11>, so
+ * exp(-i t (XX+YY)) on the pair (a, b): for x with bit a = 1, bit b = 0 and y = x with the two
+ * bits swapped:  u' = cos(2t) u - i sin(2t) v,  v' = -i sin(2t) u + cos(2t) v  (u = psi_x, v = psi_y). */
+static void or_pair_xy(int n, double *psi, int a, int b, double t) {
+    uint64_t N = (uint64_t)1 << n, ba = (uint64_t)1 << a, bb = (uint64_t)1 << b;
+    double c = cos(2.0 * t), s = sin(2.0 * t);
+#pragma omp parallel for schedule(static)
+    for (int64_t x = 0; x < (int64_t)N; ++x) {
+        if (!((uint64_t)x & ba) || ((uint64_t)x & bb)) continue;
+        uint64_t y = ((uint64_t)x ^ ba) | bb;
+        double ur = psi[2 * x], ui = psi[2 * x + 1];
+        double vr = psi[2 * y], vi = psi[2 * y + 1];
+        psi[2 * x] = c * ur + s * vi;
+        psi[2 * x + 1] = c * ui - s * vr;
+        psi[2 * y] = c * vr + s * ui;
+        psi[2 * y + 1] = c * vi - s * ur;
+    }
+}
+
+OR_API void or_mixer_parity(int n, double *psi, const int *sq, int K, double t) {
+    for (int m = 0; m + 1 < K; m += 2) or_pair_xy(n, psi, sq[m], sq[m + 1], t);      /* B_odd  */
+    for (int m = 1; m + 1 < K; m += 2) or_pair_xy(n, psi, sq[m], sq[m + 1], t);      /* B_even */
+    if (K >= 3 && (K & 1)) or_pair_xy(n, psi, sq[K - 1], sq[0], t);                  /* B_last */
+}
+
+/* QAOAz evolution (PAPER.md Eq. qaoaz): for k = 1..p: phase(gamma_k) then U_parity(t_k). */
+OR_API void or_evolve_parity(int n, double *psi, const double *q, const int *sq, int K, const double *theta,
+                             int p) {
+    uint64_t N = (uint64_t)1 << n;
+    for (int k = 0; k < p; ++k) {
+        or_phase(N, psi, q, theta[2 * k]);
+        or_mixer_parity(n, psi, sq, K, theta[2 * k + 1]);
+    }
+}
+
 /* Circulant mixer, definition written out (Sec. 3, sign read as
  * exp(-i beta lambda_j), R3; lambda indexed by forward-DFT bin j, R4):
  *   U = F^{-1} diag(exp(-i beta lambda)) F,  F_{jx} = exp(-2 pi i j x / N), F^{-1} = F^H / N.

@@ -370,3 +370,66 @@ def test_input_recipes():
     assert wl3.dim == 720 and wl3.q.shape == (720,)
     # determinism
     assert np.array_equal(make_config("cfg4").edges_u, make_config("cfg4").edges_u)
+
+
+# ---------------------------------------------------------------- P16 QAOAz parity mixer ----
+_PX = np.array([[0, 1], [1, 0]], complex)
+_PY = np.array([[0, -1j], [1j, 0]], complex)
+
+
+def _dense_pauli(n, ops):
+    """Dense operator of a Pauli product {qubit: 2x2}; qubit j <-> bit j of the index (R8), so
+    qubit n-1 is the leftmost Kronecker factor."""
+    M = np.array([[1.0 + 0j]])
+    for j in reversed(range(n)):
+        M = np.kron(M, ops.get(j, np.eye(2)))
+    return M
+
+
+def _dense_B(n, pairs):
+    B = np.zeros((1 << n, 1 << n), complex)
+    for a, b in pairs:
+        B += _dense_pauli(n, {a: _PX, b: _PX}) + _dense_pauli(n, {a: _PY, b: _PY})
+    return B
+
+
+def test_P16_dense_xy_term_spec_example():
+    """on 2 qubits B_odd = X0X1 + Y0Y1 maps |01> to 2|10> (and kills |00>, |11>)."""
+    B = _dense_B(2, [(0, 1)])
+    e = np.eye(4)
+    # index x = bit0 + 2 bit1: |q1 q0> = |01> is x = 1, |10> is x = 2
+    assert np.allclose(B @ e[1], 2 * e[2]) and np.allclose(B @ e[2], 2 * e[1])
+    assert np.allclose(B @ e[0], 0) and np.allclose(B @ e[3], 0)
+
+
+@pytest.mark.parametrize("n,seq", [(2, [0, 1]), (3, [0, 1, 2]), (4, [3, 1, 0, 2]), (5, [0, 1, 2, 3, 4]),
+                                   (6, [5, 2, 4]), (7, [6, 0, 3, 1, 5, 2, 4])])
+def test_P16_parity_mixer_vs_dense_expm(n, seq):
+    """U_parity(t) = e^{-itB_last} e^{-itB_even} e^{-itB_odd} (PAPER.md Eq. qaoaz_mixers) built from
+    dense Pauli matrices and scipy expm, against the oracle's pair rotations."""
+    rng = np.random.default_rng(n + len(seq))
+    t = float(rng.uniform(0, math.pi))
+    odd, even, last = O.parity_pairs(seq)
+    U = expm(-1j * t * _dense_B(n, last)) @ expm(-1j * t * _dense_B(n, even)) @ expm(-1j * t * _dense_B(n, odd))
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    got = O.mixer_parity(psi.copy(), seq, t)
+    assert np.max(np.abs(got - U @ psi)) < 1e-12
+
+
+def test_P16_parity_conservation_and_special_angle():
+    """Hamming weight on the subsequence is conserved (|0011> stays in weight 2); at
+    t = pi/2 every pair rotation is Z_a Z_b, so U = prod over all pairs of (-1)^(x_a xor x_b)."""
+    n, seq = 6, [0, 1, 2, 3, 4, 5]
+    psi = np.zeros(1 << n, complex)
+    psi[0b000011] = 1.0
+    out = O.mixer_parity(psi.copy(), seq, 0.73)
+    w = np.array([bin(x).count("1") for x in range(1 << n)])
+    assert np.sum(np.abs(out[w != 2]) ** 2) < 1e-12 and abs(np.linalg.norm(out) - 1) < 1e-12
+    rng = np.random.default_rng(3)
+    seq = [4, 0, 2, 5, 1]
+    phi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    odd, even, last = O.parity_pairs(seq)
+    sign = np.ones(1 << n)
+    for a, b in odd + even + last:
+        sign *= np.array([(-1.0) ** (((x >> a) ^ (x >> b)) & 1) for x in range(1 << n)])
+    assert np.max(np.abs(O.mixer_parity(phi.copy(), seq, math.pi / 2) - sign * phi)) < 1e-12
