@@ -13,6 +13,9 @@
  *     QVA_MIXER_X         W = sum_j X_j (hypercube)                    Eq. mixing_qaoa (:159-171), reading R1
  *     QVA_MIXER_CIRCULANT W circulant, F^-1 diag(e^{-i beta lambda}) F  Sec. 3 (:315-333), readings R3, R4
  *     QVA_MIXER_SPARSE    W real symmetric CSR, truncated Taylor action Sec. 3 (:333), reading R13
+ *     QVA_MIXER_PARITY    QAOAz: U = e^{-itB_last} e^{-itB_even} e^{-itB_odd}, B = sum XX+YY over
+ *                         qubit pairs of an ordered subsequence   Eqs. parity_terms / qaoaz_mixers
+ *                                                                   (:213-248), reading R19
  *
  * Conventions (all calls):
  *  - theta layout [gamma_1, beta_1, ..., gamma_p, beta_p] (reading R7); layer 1 acts first (R6).
@@ -60,7 +63,7 @@ typedef enum {
     QVA_ERR_NCCL = 8
 } qva_status;
 
-typedef enum { QVA_MIXER_X = 0, QVA_MIXER_CIRCULANT = 1, QVA_MIXER_SPARSE = 2 } qva_mixer;
+typedef enum { QVA_MIXER_X = 0, QVA_MIXER_CIRCULANT = 1, QVA_MIXER_SPARSE = 2, QVA_MIXER_PARITY = 3 } qva_mixer;
 
 typedef struct {
     uint64_t dim;            /* N = number of basis states of the (sub)space; X mixer: 2^n_qubits */
@@ -126,6 +129,15 @@ qva_status qva_set_circulant_eigenvalues_const(qva_plan *plan, double lambda0, d
  * action uses s = max(1, ceil(|beta| ||W||_1 / 3)) sub-steps of degree <= 40 (reading R13). */
 qva_status qva_set_sparse_mixer(qva_plan *plan, const int64_t *row_ptr, const int32_t *col,
                                 const double *val, uint64_t nnz);
+
+/* QAOAz parity mixer (QVA_MIXER_PARITY plans; PAPER.md:213-248 Eqs. parity_terms, qaoaz_mixers):
+ * the ordered qubit subsequence s[0..count) the mixing operators act on.
+ * B_odd = sum over pairs (s0,s1), (s2,s3), ...; B_even over (s1,s2), (s3,s4), ... (no wrap);
+ * B_last = the pair (s_{count-1}, s0) iff count is odd (reading R19).  Default: all qubits
+ * 0..n-1 in order.  QVA_ERR_INVALID_ARGUMENT: count < 2, an index outside [0, n) or repeated.
+ * The QAOAz initial state (a parity-constrained state) is set with qva_set_initial_state; the
+ * default |+> is allowed but not parity-constrained. */
+qva_status qva_set_parity_mixer(qva_plan *plan, const int32_t *qubits, int32_t count);
 
 /* Optional initial state psi0 (default |+>, PAPER.md:174-178 / R2): interleaved re,im,
  * entries [offset, offset+count). */

@@ -18,8 +18,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libqva.so")
 
-MIXER_X, MIXER_CIRCULANT, MIXER_SPARSE = 0, 1, 2
-_MIXERS = {"x": MIXER_X, "circulant": MIXER_CIRCULANT, "sparse": MIXER_SPARSE}
+MIXER_X, MIXER_CIRCULANT, MIXER_SPARSE, MIXER_PARITY = 0, 1, 2, 3
+_MIXERS = {"x": MIXER_X, "circulant": MIXER_CIRCULANT, "sparse": MIXER_SPARSE, "parity": MIXER_PARITY}
 KERNEL_CLASSES = {"tile": 0, "small": 1, "fft_col": 2, "fft_row": 3, "spmv": 4, "reduce": 5,
                   "exchange": 6, "other": 7}
 
@@ -64,6 +64,7 @@ def _load():
         "qva_set_circulant_eigenvalues": [P, P, u64, u64],
         "qva_set_circulant_eigenvalues_const": [P, d, d],
         "qva_set_sparse_mixer": [P, P, P, P, u64],
+        "qva_set_parity_mixer": [P, P, i32],
         "qva_set_initial_state": [P, P, u64, u64],
         "qva_clear_initial_state": [P],
         "qva_reset_state": [P],
@@ -280,6 +281,11 @@ class Plan:
         col = np.ascontiguousarray(col, np.int32)
         val = None if val is None else _f64(val)
         _call("qva_set_sparse_mixer", self._h, _ptr(row_ptr), _ptr(col), _ptr(val), len(col))
+
+    def set_parity_mixer(self, qubits):
+        """Ordered qubit subsequence of the QAOAz parity mixer (include/qva.h)."""
+        s = np.ascontiguousarray(qubits, np.int32)
+        _call("qva_set_parity_mixer", self._h, _ptr(s), len(s))
 
     def set_initial_state(self, psi, offset: int = 0):
         psi = np.ascontiguousarray(psi, np.complex128)

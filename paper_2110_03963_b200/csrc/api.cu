@@ -488,6 +488,8 @@ struct qva_plan {
     bool lam_set = false, lam_const = false;
     double lam0 = 0.0, lamc = 0.0;
     std::vector<double> lambda_host;   // natural (forward-bin) order mirror
+    // parity (QAOAz): ordered qubit subsequence
+    std::vector<int> parity_seq;
     // sparse
     SparseMixer sm;
     bool sparse_set = false;
@@ -1474,6 +1476,22 @@ qva_status circ_shard_setup(qva_plan *P, PlanShardIO &io) {
     return QVA_OK;
 }
 
+// QAOAz parity mixer U(t) = e^{-itB_last} e^{-itB_even} e^{-itB_odd} (reading R19): pair terms in
+// that order, one coalesced pass over the |01>/|10> halves per pair
+qva_status parity_mix(qva_plan *P, double t) {
+    const std::vector<int> &s = P->parity_seq;
+    const int K = (int)s.size();
+    auto pair = [&](int a, int b) -> qva_status {
+        ProfScope ps(P, K_OTHER, 16.0 * P->arr_n);
+        QVA_CUDA_TRY(launch_parity_pair(P->psi, P->arr_n, a, b, t, P->stream));
+        return QVA_OK;
+    };
+    for (int m = 0; m + 1 < K; m += 2) QVA_TRY(pair(s[m], s[m + 1]));
+    for (int m = 1; m + 1 < K; m += 2) QVA_TRY(pair(s[m], s[m + 1]));
+    if (K >= 3 && (K & 1)) QVA_TRY(pair(s[K - 1], s[0]));
+    return QVA_OK;
+}
+
 // apply one mixer on the current state (no phase)
 qva_status apply_mixer_impl(qva_plan *P, double beta) {
     if (P->mixer == QVA_MIXER_X) {
@@ -1518,6 +1536,7 @@ qva_status apply_mixer_impl(qva_plan *P, double beta) {
         }
         return fft_run(P->fft, r, P->stream, &obs);
     }
+    if (P->mixer == QVA_MIXER_PARITY) return parity_mix(P, beta);
     if (P->mixer == QVA_MIXER_SPARSE) {
         if (!P->sparse_set) {
             set_error("sparse mixer not set");
@@ -1726,7 +1745,7 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
     }
     *out = nullptr;
     const qva_plan_desc &d = *desc;
-    if (d.dim == 0 || d.world < 1 || d.rank < 0 || d.rank >= d.world || d.mixer < 0 || d.mixer > 2) {
+    if (d.dim == 0 || d.world < 1 || d.rank < 0 || d.rank >= d.world || d.mixer < 0 || d.mixer > 3) {
         set_error("qva_plan_create: invalid dim/world/rank/mixer");
         return QVA_ERR_INVALID_ARGUMENT;
     }
@@ -1736,9 +1755,10 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
         set_error("virtual_shards requires world == 1");
         return QVA_ERR_INVALID_ARGUMENT;
     }
-    if (d.mixer == QVA_MIXER_X) {
-        if (d.n_qubits < 1 || d.n_qubits > 40 || d.dim != (1ull << d.n_qubits)) {
-            set_error("X mixer needs dim == 2^n_qubits (1 <= n <= 40)");
+    if (d.mixer == QVA_MIXER_X || d.mixer == QVA_MIXER_PARITY) {
+        if (d.n_qubits < 1 || d.n_qubits > 40 || d.dim != (1ull << d.n_qubits) ||
+            (d.mixer == QVA_MIXER_PARITY && d.n_qubits < 2)) {
+            set_error("X / parity mixer needs dim == 2^n_qubits (1 <= n <= 40; parity: n >= 2)");
             return QVA_ERR_UNSUPPORTED;
         }
     }
@@ -1752,7 +1772,7 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
     } else if (G > 1) {
         if (d.mixer != QVA_MIXER_X) {
             set_error("sharded state (world*virtual_shards > 1) is implemented for the X and circulant mixers; "
-                      "use the replicated mode (reserved[0]=1) for batches of sparse evolutions");
+                      "use the replicated mode (reserved[0]=1) for batches of sparse / parity evolutions");
             return QVA_ERR_UNSUPPORTED;
         }
         if (!is_pow2((uint64_t)G)) {
@@ -1779,10 +1799,12 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
     P->G = G;
     P->gbits = ilog2(G);
     P->max_batch = d.max_batch > 0 ? d.max_batch : 1;
-    if (d.mixer == QVA_MIXER_X) {
+    if (d.mixer == QVA_MIXER_X || d.mixer == QVA_MIXER_PARITY) {
         P->n = d.n_qubits;
         P->L = P->n - P->gbits;
     }
+    if (d.mixer == QVA_MIXER_PARITY)
+        for (int j = 0; j < d.n_qubits; ++j) P->parity_seq.push_back(j);
     if (replicated || d.world == 1) {
         P->local_n = P->N;
         P->offset = 0;
@@ -1908,8 +1930,8 @@ qva_status qva_set_qualities_device(qva_plan *P, const double *q, uint64_t offse
 
 qva_status qva_set_qualities_maxcut(qva_plan *P, int32_t m, const int32_t *u, const int32_t *v, const double *w) {
     if (!P || m < 0 || (m > 0 && (!u || !v))) return QVA_ERR_INVALID_ARGUMENT;
-    if (P->mixer != QVA_MIXER_X) {
-        set_error("qva_set_qualities_maxcut: X mixer plans only");
+    if (P->mixer != QVA_MIXER_X && P->mixer != QVA_MIXER_PARITY) {
+        set_error("qva_set_qualities_maxcut: qubit (X / parity mixer) plans only");
         return QVA_ERR_UNSUPPORTED;
     }
     for (int e = 0; e < m; ++e) {
@@ -1996,6 +2018,27 @@ qva_status qva_set_circulant_eigenvalues_const(qva_plan *P, double lambda0, doub
     P->lam_const = true;
     P->lam0 = lambda0;
     P->lamc = c;
+    return QVA_OK;
+}
+
+qva_status qva_set_parity_mixer(qva_plan *P, const int32_t *qubits, int32_t count) {
+    if (!P || !qubits || count < 2) {
+        set_error("qva_set_parity_mixer: need at least 2 qubits");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    if (P->mixer != QVA_MIXER_PARITY) {
+        set_error("not a parity-mixer plan");
+        return QVA_ERR_UNSUPPORTED;
+    }
+    std::vector<int> seen(P->n, 0), seq(count);
+    for (int i = 0; i < count; ++i) {
+        if (qubits[i] < 0 || qubits[i] >= P->n || seen[qubits[i]]++) {
+            set_error("qva_set_parity_mixer: qubit index outside [0, n) or repeated");
+            return QVA_ERR_INVALID_ARGUMENT;
+        }
+        seq[i] = qubits[i];
+    }
+    P->parity_seq = seq;
     return QVA_OK;
 }
 
@@ -2214,6 +2257,18 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
             QVA_TRY(fft_run(P->fft, r, P->stream, &obs));
         }
         *have_red = p > 0;
+        return QVA_OK;
+    }
+    if (P->mixer == QVA_MIXER_PARITY) {
+        QVA_TRY(ensure_q_dev(P));
+        QVA_TRY(reset_state(P));
+        for (int k = 0; k < p; ++k) {
+            {
+                ProfScope ps(P, K_OTHER, 40.0 * P->arr_n);
+                QVA_CUDA_TRY(launch_phase(P->psi, P->q, P->arr_n, theta[2 * k], P->stream));
+            }
+            QVA_TRY(parity_mix(P, theta[2 * k + 1]));
+        }
         return QVA_OK;
     }
     // sparse

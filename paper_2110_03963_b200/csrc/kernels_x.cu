@@ -359,6 +359,30 @@ template cudaError_t launch_block_transpose<double2>(double2 *, const double2 *,
 template cudaError_t launch_block_transpose<double>(double *, const double *, uint64_t, uint64_t, uint64_t,
                                                     cudaStream_t);
 
+// QAOAz parity mixer pair term exp(-i t (X_aX_b + Y_aY_b)) (PAPER.md Eq. parity_terms): a Givens
+// rotation by 2t on the {|..1_a..0_b..>, |..0_a..1_b..>} pairs; |00>, |11> untouched.  Thread k
+// of N/4 addresses the pair with bit a = 1, bit b = 0 (bits inserted into k at their positions).
+__global__ void parity_pair_kernel(double2 *__restrict__ psi, uint64_t quarter, int a, int b, double c, double s) {
+    const int lo = min(a, b), hi = max(a, b);
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < quarter;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t x = ((k >> lo) << (lo + 1)) | (k & ((1ull << lo) - 1));
+        x = ((x >> hi) << (hi + 1)) | (x & ((1ull << hi) - 1));
+        x |= 1ull << a;
+        const uint64_t y = (x ^ (1ull << a)) | (1ull << b);
+        const double2 u = psi[x], v = psi[y];
+        // u' = c u - i s v, v' = -i s u + c v
+        psi[x] = make_double2(fma(c, u.x, s * v.y), fma(c, u.y, -s * v.x));
+        psi[y] = make_double2(fma(c, v.x, s * u.y), fma(c, v.y, -s * u.x));
+    }
+}
+
+cudaError_t launch_parity_pair(double2 *psi, uint64_t n_amps, int a, int b, double t, cudaStream_t s) {
+    const uint64_t quarter = n_amps / 4;
+    parity_pair_kernel<<<grid_for(quarter, 256), 256, 0, s>>>(psi, quarter, a, b, cos(2.0 * t), sin(2.0 * t));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_chunk_transpose_bytes(void *out, const void *in, int G, uint64_t C, int elem_bytes, cudaStream_t s) {
     uint64_t total = (uint64_t)G * G * C;
     if (elem_bytes == 1)

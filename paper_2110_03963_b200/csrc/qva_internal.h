@@ -218,6 +218,8 @@ cudaError_t launch_chunk_transpose_bytes(void *out, const void *in, int G, uint6
 // fixed-order reduction of partials [batch][n][2] -> out [batch][2]
 cudaError_t launch_reduce_partials(const double *partials, uint64_t n, int batch, double *out,
                                    cudaStream_t s);
+// QAOAz parity-mixer pair term exp(-i t (X_aX_b + Y_aY_b)) on all n_amps amplitudes
+cudaError_t launch_parity_pair(double2 *psi, uint64_t n_amps, int a, int b, double t, cudaStream_t s);
 // elementwise phase (generic dims, any mixer): psi *= exp(-i gamma q)
 cudaError_t launch_phase(double2 *psi, const double *q, uint64_t n, double gamma, cudaStream_t s);
 // psi = 1/sqrt(N)

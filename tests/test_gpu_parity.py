@@ -346,6 +346,47 @@ def test_circulant_virtual_shards_random_spectrum(Q, N, G):
         _amp_close(P.get_state(), O.mixer_circulant_dense(psi0.copy(), lam, 0.7))
 
 
+# ---------------------------------------------------------------- QAOAz parity mixer ----
+def _weight_state(n, w, rng):
+    """Random normalised state supported on Hamming weight w (a parity-constrained psi0)."""
+    psi = np.zeros(1 << n, np.complex128)
+    idx = [x for x in range(1 << n) if bin(x).count("1") == w]
+    psi[idx] = rng.standard_normal(len(idx)) + 1j * rng.standard_normal(len(idx))
+    return psi / np.linalg.norm(psi)
+
+
+@pytest.mark.parametrize("n,seq,p", [(6, None, 2), (9, [0, 2, 4, 6, 8, 1, 3], 3), (14, None, 2),
+                                     (18, [17, 3, 9, 0, 12, 5], 2)])
+def test_qaoaz_parity_vs_oracle(Q, n, seq, p):
+    """QAOAz (PAPER.md Eq. qaoaz, parity mixer Eqs. parity_terms/qaoaz_mixers, reading R19) from a
+    weight-constrained initial state and from |+>; Hamming weight conserved on the GPU."""
+    rng = np.random.default_rng(500 + n)
+    u, v = random_regular_graph(n, 3 if n % 2 == 0 else 4, rng)
+    q = O.maxcut_q(n, u, v)
+    theta = rng.uniform(0, math.pi, 2 * p)
+    sq = list(range(n)) if seq is None else seq
+    psi0 = _weight_state(n, n // 2, rng) if seq is None else O.init_uniform(1 << n)
+    ref = O.evolve_parity(n, q, sq, theta, psi0)
+    with Q.Plan(1 << n, "parity", n_qubits=n) as P:
+        if seq is not None:
+            P.set_parity_mixer(seq)
+        P.set_qualities_maxcut(u, v)
+        P.set_initial_state(psi0)
+        P.evolve(theta)
+        got = P.get_state()
+        _amp_close(got, ref)
+        _f_close(P.expectation(), O.expectation(ref, q))
+        if seq is None:
+            w = np.array([bin(x).count("1") for x in range(1 << n)])
+            assert np.sum(np.abs(got[w != n // 2]) ** 2) < 1e-12
+        P.reset_state()
+        P.apply_mixer(0.41)
+        _amp_close(P.get_state(), O.mixer_parity(psi0.copy(), sq, 0.41))
+        f = P.evolve_batch(np.stack([theta, theta[::-1]]))
+        _f_close(f[0], O.expectation(ref, q))
+        _f_close(f[1], O.expectation(O.evolve_parity(n, q, sq, theta[::-1], psi0), q))
+
+
 # ---------------------------------------------------------------- cfg4 full size ----
 def test_cfg4_full_size_vs_golden(Q):
     g = json.load(open(os.path.join(GOLD, "cfg4_n30.json")))
