@@ -449,6 +449,7 @@ struct qva_plan {
         std::vector<int> key;  // (sharded layout, tile bits, permuted layout)
         int group, qbytes;
         void *buf;
+        size_t bytes;
     };
     std::vector<QtEntry> qt_cache;
     int layout = 0;
@@ -464,8 +465,18 @@ struct qva_plan {
         std::vector<int> key;
         int group, mode;
         void *rec, *thr, *G;
+        size_t rec_bytes;
+        std::vector<double> thr_h, G_h;   // host staging (kept alive with the entry)
+        std::vector<int> thr_hi, G_hi;
     };
     std::vector<GenEntry> gen_cache;
+    // device buffers of dropped q copies / records, reused by size (a new q every step must not
+    // pay cudaFree's device synchronisation and cudaMalloc's mapping cost)
+    std::vector<std::pair<size_t, void *>> pool;
+    // pinned host ring for small per-step uploads (angles, tables, generator records): a copy from
+    // pageable memory would synchronise the stream before it starts
+    unsigned char *ring = nullptr;
+    size_t ring_size = 0, ring_pos = 0;
     // permuted layout of the single-shard state (physical bit -> logical qubit); empty = natural
     std::vector<int> perm;
     bool perm_failed = false;
@@ -760,13 +771,58 @@ qva_status to_layout_A(qva_plan *P) {
     return exchange_state(P);
 }
 
+void pool_put(qva_plan *P, void *p, size_t bytes) {
+    if (p) P->pool.push_back({bytes, p});
+}
+// smallest pooled buffer of at least `bytes` (exact-size reuse is the common case), else cudaMalloc
+cudaError_t pool_get(qva_plan *P, void **p, size_t bytes) {
+    int best = -1;
+    for (int i = 0; i < (int)P->pool.size(); ++i)
+        if (P->pool[i].first >= bytes && (best < 0 || P->pool[i].first < P->pool[best].first)) best = i;
+    if (best >= 0 && P->pool[best].first <= 2 * bytes + 4096) {
+        *p = P->pool[best].second;
+        P->pool.erase(P->pool.begin() + best);
+        return cudaSuccess;
+    }
+    return cudaMalloc(p, bytes);
+}
+
+// H2D copy of a small host buffer through the pinned ring (falls back to a pageable copy when
+// larger than the ring); the ring restarts after a stream synchronisation when full
+constexpr size_t kRingBytes = 4 << 20;
+qva_status upload(qva_plan *P, void *dst, const void *src, size_t bytes) {
+    if (!bytes) return QVA_OK;
+    if (!P->ring) {
+        if (cudaMallocHost((void **)&P->ring, kRingBytes) != cudaSuccess) {
+            cudaGetLastError();
+            P->ring = nullptr;
+        } else {
+            P->ring_size = kRingBytes;
+        }
+    }
+    if (!P->ring || bytes > P->ring_size) {
+        QVA_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, P->stream));
+        return QVA_OK;
+    }
+    const size_t off = (P->ring_pos + 15) & ~(size_t)15;
+    if (off + bytes > P->ring_size) {
+        QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));  // earlier copies out of the ring are done
+        P->ring_pos = 0;
+        return upload(P, dst, src, bytes);
+    }
+    memcpy(P->ring + off, src, bytes);
+    QVA_CUDA_TRY(cudaMemcpyAsync(dst, P->ring + off, bytes, cudaMemcpyHostToDevice, P->stream));
+    P->ring_pos = off + bytes;
+    return QVA_OK;
+}
+
 void drop_qt(qva_plan *P) {
-    for (auto &e : P->qt_cache) cudaFree(e.buf);
+    for (auto &e : P->qt_cache) pool_put(P, e.buf, e.bytes);
     P->qt_cache.clear();
     for (auto &e : P->gen_cache) {
-        cudaFree(e.rec);
-        cudaFree(e.thr);
-        cudaFree(e.G);
+        pool_put(P, e.rec, e.rec_bytes);
+        pool_put(P, e.thr, 128 * 8 * sizeof(double));
+        pool_put(P, e.G, 32 * sizeof(double));
     }
     P->gen_cache.clear();
 }
@@ -848,13 +904,13 @@ qva_status ensure_qt(qva_plan *P, const std::vector<int> &key, const std::vector
         return QVA_ERR_UNSUPPORTED;
     }
     void *buf = nullptr;
-    QVA_CUDA_TRY(cudaMalloc(&buf, P->arr_n * (size_t)qbytes));
+    QVA_CUDA_TRY(pool_get(P, &buf, P->arr_n * (size_t)qbytes));
     {
         ProfScope ps(P, K_OTHER, 2.0 * qbytes * (double)P->arr_n);
         QVA_CUDA_TRY(
             launch_qt_gather(buf, src, qbytes, tp, kGroups[g], P->arr_n >> kTileBits, P->qmin, R, P->stream));
     }
-    P->qt_cache.push_back({key, g, qbytes, buf});
+    P->qt_cache.push_back({key, g, qbytes, buf, P->arr_n * (size_t)qbytes});
     *out = buf;
     return QVA_OK;
 }
@@ -997,9 +1053,10 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
     ent.group = gq;
     ent.mode = mode;
     ent.rec = ent.thr = ent.G = nullptr;
-    QVA_CUDA_TRY(cudaMalloc(&ent.rec, n_tiles * rec_bytes));
-    QVA_CUDA_TRY(cudaMalloc(&ent.thr, 128 * 8 * sizeof(double)));
-    QVA_CUDA_TRY(cudaMalloc(&ent.G, 32 * sizeof(double)));
+    ent.rec_bytes = n_tiles * rec_bytes;
+    QVA_CUDA_TRY(pool_get(P, &ent.rec, ent.rec_bytes));
+    QVA_CUDA_TRY(pool_get(P, &ent.thr, 128 * 8 * sizeof(double)));
+    QVA_CUDA_TRY(pool_get(P, &ent.G, 32 * sizeof(double)));
     void *d_edges = nullptr;
     const size_t eb = (tt.size() + tb.size()) * (sizeof(int2) + sizeof(double)) + 16;
     QVA_CUDA_TRY(cudaMallocAsync(&d_edges, eb, P->stream));
@@ -1020,7 +1077,7 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
         gp.tb_ab = (const int2 *)(d + tt.size() * sizeof(int2));
         gp.tt_w = (const double *)(d + woff);
         gp.tb_w = (const double *)(d + woff + ttw.size() * sizeof(double));
-        QVA_CUDA_TRY(cudaMemcpyAsync(d_edges, hb.data(), eb, cudaMemcpyHostToDevice, P->stream));
+        QVA_TRY(upload(P, d_edges, hb.data(), eb));
         ProfScope ps(P, K_OTHER, (double)n_tiles * rec_bytes);
         QVA_CUDA_TRY(launch_gen_records(ent.rec, n_tiles, f64 ? 1 : 0, gp, P->stream));
         QVA_CUDA_TRY(cudaFreeAsync(d_edges, P->stream));
@@ -1029,8 +1086,12 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
         int role[kTileBits], ridx[kTileBits];  // 0: thread bit, 1: register bit
         for (int j = 0; j < kCT_BITS; ++j) role[g.tbit[j]] = 0, ridx[g.tbit[j]] = j;
         for (int j = 0; j < kGroupBits; ++j) role[g.ebit[j]] = 1, ridx[g.ebit[j]] = j;
-        std::vector<double> thr(128 * 8, 0.0), G(32, 0.0);
-        std::vector<int> thr_i(128 * 8, 0), G_i(32, 0);
+        std::vector<double> &thr = ent.thr_h, &G = ent.G_h;
+        std::vector<int> &thr_i = ent.thr_hi, &G_i = ent.G_hi;
+        thr.assign(128 * 8, 0.0);
+        G.assign(32, 0.0);
+        thr_i.assign(128 * 8, 0);
+        G_i.assign(32, 0);
         for (int c = 0; c < 128; ++c) {
             double C = 0.0, beta[kGroupBits] = {0, 0, 0, 0, 0};
             auto xv = [&](int k) { return (c >> ridx[k]) & 1; };
@@ -1058,15 +1119,12 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
             G_i[e] = (int)s;
         }
         if (f64) {
-            QVA_CUDA_TRY(cudaMemcpyAsync(ent.thr, thr.data(), thr.size() * sizeof(double), cudaMemcpyHostToDevice,
-                                         P->stream));
-            QVA_CUDA_TRY(cudaMemcpyAsync(ent.G, G.data(), G.size() * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+            QVA_TRY(upload(P, ent.thr, thr.data(), thr.size() * sizeof(double)));
+            QVA_TRY(upload(P, ent.G, G.data(), G.size() * sizeof(double)));
         } else {
-            QVA_CUDA_TRY(cudaMemcpyAsync(ent.thr, thr_i.data(), thr_i.size() * sizeof(int), cudaMemcpyHostToDevice,
-                                         P->stream));
-            QVA_CUDA_TRY(cudaMemcpyAsync(ent.G, G_i.data(), G_i.size() * sizeof(int), cudaMemcpyHostToDevice, P->stream));
+            QVA_TRY(upload(P, ent.thr, thr_i.data(), thr_i.size() * sizeof(int)));
+            QVA_TRY(upload(P, ent.G, G_i.data(), G_i.size() * sizeof(int)));
         }
-        QVA_TRY(sync(P));  // host staging vectors go out of scope
     }
     P->gen_cache.push_back(ent);
     *out = &P->gen_cache.back();
@@ -1167,8 +1225,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             ++j;
         }
     }
-    QVA_CUDA_TRY(cudaMemcpyAsync(P->d_angles, ang.data(), ang.size() * sizeof(PassAngles), cudaMemcpyHostToDevice,
-                                 P->stream));
+    QVA_TRY(upload(P, P->d_angles, ang.data(), ang.size() * sizeof(PassAngles)));
     const int ntab = gen == kQGenInt ? P->g_m + 1 : (int_table ? (P->qmax - P->qmin + 1) : 0);
     if (!gam.empty()) {
         if (P->gam_cap < gam.size()) {
@@ -1183,12 +1240,10 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             QVA_CUDA_TRY(cudaMalloc(&P->d_tab, gam.size() * ntab * sizeof(double2)));
             P->tab_cap = gam.size() * ntab;
         }
-        QVA_CUDA_TRY(cudaMemcpyAsync(P->d_gam, gam.data(), gam.size() * sizeof(double), cudaMemcpyHostToDevice,
-                                     P->stream));
+        QVA_TRY(upload(P, P->d_gam, gam.data(), gam.size() * sizeof(double)));
         double2 *d_mult = nullptr;
         QVA_CUDA_TRY(cudaMallocAsync((void **)&d_mult, gam.size() * sizeof(double2), P->stream));
-        QVA_CUDA_TRY(cudaMemcpyAsync(d_mult, tab_mult.data(), gam.size() * sizeof(double2), cudaMemcpyHostToDevice,
-                                     P->stream));
+        QVA_TRY(upload(P, d_mult, tab_mult.data(), gam.size() * sizeof(double2)));
         {
             ProfScope ps(P, K_OTHER, 16.0 * gam.size() * ntab);
             QVA_CUDA_TRY(launch_phase_table(P->d_tab, P->d_gam, d_mult, (int)gam.size(), tab_qmin, ntab, P->stream));
@@ -1716,7 +1771,9 @@ qva_status qva_plan_destroy(qva_plan *P) {
     cudaFree(P->qcB);
     cudaFree(P->d_tab);
     cudaFree(P->d_gam);
-    for (auto &e : P->qt_cache) cudaFree(e.buf);
+    drop_qt(P);
+    for (auto &e : P->pool) cudaFree(e.second);
+    if (P->ring) cudaFreeHost(P->ring);
     cudaFree(P->partials);
     cudaFree(P->red);
     cudaFree(P->d_angles);
@@ -2186,7 +2243,7 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
             sp.p = p;
             sp.mode = 0;
             sp.out = P->red;
-            QVA_CUDA_TRY(cudaMemcpyAsync(P->d_thetas, theta, 2 * p * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+            QVA_TRY(upload(P, P->d_thetas, theta, 2 * p * sizeof(double)));
             sp.thetas = P->d_thetas;
             {
                 ProfScope ps(P, K_SMALL, 24.0 * P->arr_n);
