@@ -303,14 +303,52 @@ __device__ __forceinline__ typename QGenT<QB>::V gen_cut(typename QGenT<QB>::V S
     if (E & 16) x += al[4];
     return x;
 }
+// fp64 weights, one member: exp(i gamma cut) factorised as e^{i gamma S} prod_j (e^{i gamma al_j})^{e_j}
+// e^{i gamma G(e)}: 6 sincos per thread and tile instead of one per element, the 32 products
+// walked in Gray-code order (one complex multiply per element; |z| = 1 so a removed factor is
+// its conjugate), G factors from a per-pass smem table gf_s[32]
+template <int E>
+__device__ __forceinline__ constexpr int gray_flip() {
+    return E == 0 ? -1 : __builtin_ctz((unsigned)E);
+}
+__device__ __forceinline__ void apply_phase_gen_f64_fact(double2 (&v)[kAPT], double S, const double (&al)[5],
+                                                         const double2 *gf_s, double gamma) {
+    double sn, cs;
+    sincos(gamma * S, &sn, &cs);
+    double2 run = make_double2(cs, sn);
+    double2 z[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        sincos(gamma * al[j], &sn, &cs);
+        z[j] = make_double2(cs, sn);
+    }
+    static_for<kAPT>([&](auto gc) {
+        constexpr int Gk = decltype(gc)::value;
+        constexpr int E = Gk ^ (Gk >> 1);
+        if constexpr (Gk > 0) {
+            constexpr int J = gray_flip<Gk>();
+            if constexpr ((E >> J) & 1) run = cmul(run, z[J]);
+            else run = cmul(run, make_double2(z[J].x, -z[J].y));
+        }
+        v[E] = cmul(v[E], cmul(run, gf_s[E]));
+    });
+}
+
 template <int QB>
 __device__ __forceinline__ void apply_phase_gen(double2 (&v)[kAPT], const unsigned char *rec, const TileGroup &g,
                                                 int c, int lane, const typename QGenT<QB>::V (&cst)[6],
                                                 const typename QGenT<QB>::V *G_s, int m_edges, double gamma,
-                                                const double2 *tab_s, const double2 *tab_g) {
+                                                const double2 *tab_s, const double2 *tab_g,
+                                                const double2 *gf_s = nullptr) {
     using V = typename QGenT<QB>::V;
     V S, al[5];
     gen_coeffs<QB>(rec, g, c, cst, S, al);
+    if constexpr (QB == kQGenF64) {
+        if (gf_s) {
+            apply_phase_gen_f64_fact(v, S, al, gf_s, gamma);
+            return;
+        }
+    }
     const double2 *tab_l = tab_s + (lane & (kTabRep - 1));
     static_for<kAPT>([&](auto ec) {
         constexpr int E = decltype(ec)::value;
@@ -350,7 +388,8 @@ template <int STAGES, int QB>
 constexpr size_t tile_smem_bytes() {
     return (size_t)STAGES * (kTile * sizeof(double2) + (size_t)q_stage_bytes<QB>()) +
            (q_table<QB>() ? (size_t)kTabSmemMax * kTabRep * sizeof(double2) : 0) +
-           (q_gen<QB>() ? 32 * sizeof(double) : 0) + 2 * STAGES * sizeof(uint64_t) +
+           (q_gen<QB>() ? 32 * sizeof(double) : 0) + (QB == kQGenF64 ? 32 * sizeof(double2) : 0) +
+           2 * STAGES * sizeof(uint64_t) +
            (size_t)kMaxBatchSmem * sizeof(PassAngles);
 }
 
@@ -413,8 +452,10 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     double2 *tab_s = reinterpret_cast<double2 *>(q_s + (size_t)STAGES * QSB);
     GV *G_s = reinterpret_cast<GV *>(reinterpret_cast<unsigned char *>(tab_s) +
                                      (q_table<QB>() ? kTabSmemMax * kTabRep * sizeof(double2) : 0));
-    uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(G_s) +
-                                                  (q_gen<QB>() ? 32 * sizeof(double) : 0));
+    double2 *gf_s = reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(G_s) +
+                                                (q_gen<QB>() ? 32 * sizeof(double) : 0));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(gf_s) +
+                                                  (QB == kQGenF64 ? 32 * sizeof(double2) : 0));
     PassAngles *ang_s = reinterpret_cast<PassAngles *>(bars + 2 * STAGES);  // [batch]
     // full[round & 1][stage]: item `it` is round it / STAGES of stage it % STAGES.  Rounds r and
     // r - 2 of a stage belong to the same warpgroup, so each barrier is waited by one warpgroup
@@ -481,7 +522,14 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     if constexpr (q_gen<QB>()) {
         if (load_q) {
             const GV *Gg = reinterpret_cast<const GV *>(P.gen_G);
-            for (int k = tid; k < 32; k += kThreads) G_s[k] = Gg[k];
+            for (int k = tid; k < 32; k += kThreads) {
+                G_s[k] = Gg[k];
+                if constexpr (QB == kQGenF64) {  // G factors e^{i gamma G(e)} (one member)
+                    double sn, cs;
+                    sincos(P.angles[0].gamma * (double)Gg[k], &sn, &cs);
+                    gf_s[k] = make_double2(cs, sn);
+                }
+            }
             const GV *cg = reinterpret_cast<const GV *>(P.gen_thr) + (size_t)(tid % kCT) * 8;
 #pragma unroll
             for (int k = 0; k < 6; ++k) gcst[k] = cg[k];
@@ -553,7 +601,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                     if (QB > 0 && st.phase) {
                         if constexpr (q_gen<QB>())
                             apply_phase_gen<QB>(v, qs, P.groups[P.gq], c, lane, gcst, G_s, P.gen_m, ang->gamma,
-                                                use_tab_s ? tab_s : nullptr, tab_g);
+                                                use_tab_s ? tab_s : nullptr, tab_g, P.batch == 1 ? gf_s : nullptr);
                         else
                             apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
                     }
@@ -583,7 +631,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                 if constexpr (QB > 0 && K == prog_def<PROG>().phase_k) {
                     if constexpr (q_gen<QB>())
                         apply_phase_gen<QB>(v, qs, P.groups[P.gq], c, lane, gcst, G_s, P.gen_m, ang->gamma,
-                                            use_tab_s ? tab_s : nullptr, tab_g);
+                                            use_tab_s ? tab_s : nullptr, tab_g, P.batch == 1 ? gf_s : nullptr);
                     else
                         apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
                 }

@@ -404,6 +404,20 @@ def test_cfg4_full_size_vs_golden(Q):
         _amp_close(got, ref)
 
 
+def test_cfg5_family_n30_vs_lightcone_golden(Q):
+    """Weighted 4-regular MaxCut at n = 30 (cfg5 family, 16 GiB, one GPU): generated fp64 qualities
+    with the factorised phase, permuted schedule; <Q> against the oracle's exact light-cone value
+    (tests/golden/cfg5_n30.json, written by oracle/make_golden.py)."""
+    g = json.load(open(os.path.join(GOLD, "cfg5_n30.json")))
+    wl = make_config("cfg5", n_override=30)
+    assert np.allclose(g["theta"], wl.theta, rtol=0, atol=0)
+    with Q.Plan(wl.dim, "x", n_qubits=30) as P:
+        P.set_qualities_maxcut(wl.edges_u, wl.edges_v, wl.weights)
+        P.evolve(wl.theta)
+        _f_close(P.expectation(), g["expectation_lightcone"])
+        assert abs(P.norm2() - 1) < 1e-12
+
+
 # ---------------------------------------------------------------- sharded schedule ----
 @pytest.mark.parametrize("n,G,p", [(14, 2, 1), (15, 4, 2), (16, 8, 3), (20, 8, 2), (21, 2, 3)])
 def test_virtual_shards_vs_oracle(Q, n, G, p):
