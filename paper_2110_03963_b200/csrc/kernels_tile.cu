@@ -38,6 +38,7 @@ constexpr int kAPT = kTile / kCT;           // 32 amplitudes per consumer thread
 constexpr int kThreads = kWG * kCT;         // no producer warp: each warpgroup refills what it frees
 constexpr int kTabRep = 8;                  // smem phase-table replicas (one per 16-B bank group)
 constexpr int kTabSmemMax = 64;             // entries held in smem (int8 codes, batch == 1)
+constexpr int kGfMembers = 24;              // weighted generated q: factorised phase for batches <= 24
 
 static_assert(kAPT == 1 << kGroupBits, "group width");
 static_assert(kCT == 1 << kCT_BITS, "warpgroup width");
@@ -388,7 +389,7 @@ template <int STAGES, int QB>
 constexpr size_t tile_smem_bytes() {
     return (size_t)STAGES * (kTile * sizeof(double2) + (size_t)q_stage_bytes<QB>()) +
            (q_table<QB>() ? (size_t)kTabSmemMax * kTabRep * sizeof(double2) : 0) +
-           (q_gen<QB>() ? 32 * sizeof(double) : 0) + (QB == kQGenF64 ? 32 * sizeof(double2) : 0) +
+           (q_gen<QB>() ? 32 * sizeof(double) : 0) + (QB == kQGenF64 ? kGfMembers * 32 * sizeof(double2) : 0) +
            2 * STAGES * sizeof(uint64_t) +
            (size_t)kMaxBatchSmem * sizeof(PassAngles);
 }
@@ -455,7 +456,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     double2 *gf_s = reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(G_s) +
                                                 (q_gen<QB>() ? 32 * sizeof(double) : 0));
     uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(gf_s) +
-                                                  (QB == kQGenF64 ? 32 * sizeof(double2) : 0));
+                                                  (QB == kQGenF64 ? kGfMembers * 32 * sizeof(double2) : 0));
     PassAngles *ang_s = reinterpret_cast<PassAngles *>(bars + 2 * STAGES);  // [batch]
     // full[round & 1][stage]: item `it` is round it / STAGES of stage it % STAGES.  Rounds r and
     // r - 2 of a stage belong to the same warpgroup, so each barrier is waited by one warpgroup
@@ -522,13 +523,14 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     if constexpr (q_gen<QB>()) {
         if (load_q) {
             const GV *Gg = reinterpret_cast<const GV *>(P.gen_G);
-            for (int k = tid; k < 32; k += kThreads) {
-                G_s[k] = Gg[k];
-                if constexpr (QB == kQGenF64) {  // G factors e^{i gamma G(e)} (one member)
-                    double sn, cs;
-                    sincos(P.angles[0].gamma * (double)Gg[k], &sn, &cs);
-                    gf_s[k] = make_double2(cs, sn);
-                }
+            for (int k = tid; k < 32; k += kThreads) G_s[k] = Gg[k];
+            if constexpr (QB == kQGenF64) {  // G factors e^{i gamma_b G(e)} per member b
+                if (P.batch <= kGfMembers)
+                    for (int k = tid; k < 32 * P.batch; k += kThreads) {
+                        double sn, cs;
+                        sincos(P.angles[k >> 5].gamma * (double)Gg[k & 31], &sn, &cs);
+                        gf_s[k] = make_double2(cs, sn);
+                    }
             }
             const GV *cg = reinterpret_cast<const GV *>(P.gen_thr) + (size_t)(tid % kCT) * 8;
 #pragma unroll
@@ -601,7 +603,8 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                     if (QB > 0 && st.phase) {
                         if constexpr (q_gen<QB>())
                             apply_phase_gen<QB>(v, qs, P.groups[P.gq], c, lane, gcst, G_s, P.gen_m, ang->gamma,
-                                                use_tab_s ? tab_s : nullptr, tab_g, P.batch == 1 ? gf_s : nullptr);
+                                                use_tab_s ? tab_s : nullptr, tab_g,
+                                                P.batch <= kGfMembers ? gf_s + 32 * member : nullptr);
                         else
                             apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
                     }
@@ -631,7 +634,8 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                 if constexpr (QB > 0 && K == prog_def<PROG>().phase_k) {
                     if constexpr (q_gen<QB>())
                         apply_phase_gen<QB>(v, qs, P.groups[P.gq], c, lane, gcst, G_s, P.gen_m, ang->gamma,
-                                            use_tab_s ? tab_s : nullptr, tab_g, P.batch == 1 ? gf_s : nullptr);
+                                            use_tab_s ? tab_s : nullptr, tab_g,
+                                                P.batch <= kGfMembers ? gf_s + 32 * member : nullptr);
                     else
                         apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
                 }
