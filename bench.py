@@ -78,10 +78,13 @@ class ClockSampler:
         self.thread = None
 
     def start(self):
+        if os.environ.get("QVA_BENCH_NO_SMI"):  # diagnostics only: no clock sampling
+            self.proc = None
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
             return
@@ -291,7 +294,6 @@ def main():
     clocks.start()
     time.sleep(0.3)
     plan.reset_kernel_stats()
-    plan.set_profiling(True)
     l0 = plan.launch_count()
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -303,8 +305,15 @@ def main():
     barrier()
     ms = ev0.elapsed_time(ev1)
     launches = plan.launch_count() - l0
-    plan.set_profiling(False)
     clk = clocks.stop()
+    # per-kernel device times for the roofline: a separate profiled run of the same steps (CUDA
+    # events around every launch on the plan's stream), so the timed region above has no event gaps
+    plan.reset_kernel_stats()
+    plan.set_profiling(True)
+    for _ in range(args.steps):
+        step()
+    barrier()
+    plan.set_profiling(False)
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -479,6 +480,12 @@ struct qva_plan {
     size_t ring_size = 0, ring_pos = 0;
     // permuted layout of the single-shard state (physical bit -> logical qubit); empty = natural
     std::vector<int> perm;
+    std::map<int, std::pair<std::vector<PassPlan>, std::vector<int>>> perm_sched;  // p -> (passes, final layout)
+    struct TmEntry {
+        CUtensorMap in, out;
+        int dim_src[5], dim_w[5], member_dim;
+    };
+    std::map<std::vector<int64_t>, TmEntry> tmap_cache;
     bool perm_failed = false;
     double *partials = nullptr;
     uint64_t partials_n = 0;
@@ -1372,8 +1379,28 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
                 tp.pf_nblocks = 1ull << (n_phys - top - 1);
             }
         }
-        QVA_TRY(make_tile_tensor_maps(psi_in, tp.psi_out, n_phys, batch, tp, pp.permuted ? pp.obit.data() : nullptr,
-                                      &map, &map_out));
+        {
+            // tensor maps depend on (tile bits, store permutation, buffers, sizes): encoded once
+            std::vector<int64_t> key = {(int64_t)(uintptr_t)psi_in, (int64_t)(uintptr_t)tp.psi_out, n_phys, batch};
+            key.insert(key.end(), s.begin(), s.end());
+            if (pp.permuted) key.insert(key.end(), pp.obit.begin(), pp.obit.end());
+            auto it = P->tmap_cache.find(key);
+            if (it == P->tmap_cache.end()) {
+                qva_plan::TmEntry te;
+                QVA_TRY(make_tile_tensor_maps(psi_in, tp.psi_out, n_phys, batch, tp,
+                                              pp.permuted ? pp.obit.data() : nullptr, &te.in, &te.out));
+                memcpy(te.dim_src, tp.dim_src, sizeof(te.dim_src));
+                memcpy(te.dim_w, tp.dim_w, sizeof(te.dim_w));
+                te.member_dim = tp.member_dim;
+                if (P->tmap_cache.size() > 256) P->tmap_cache.clear();
+                it = P->tmap_cache.emplace(std::move(key), te).first;
+            }
+            map = it->second.in;
+            map_out = it->second.out;
+            memcpy(tp.dim_src, it->second.dim_src, sizeof(tp.dim_src));
+            memcpy(tp.dim_w, it->second.dim_w, sizeof(tp.dim_w));
+            tp.member_dim = it->second.member_dim;
+        }
         if (g_trace > 1) {
             fprintf(stderr, "[qva] pass set %d prog %d init %d gq %d expect %d release %d steps:", pp.set, prog, tp.init,
                     tp.gq, tp.expect, tp.release_step);
@@ -2267,14 +2294,19 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
             }
         }
         if (use_permuted(P)) {
-            std::vector<int> fin;
-            auto passes = perm_passes(P->L, p, &fin);
-            if (passes.empty() || !passes.back().expect) {
-                set_error("internal: permuted schedule did not complete");
-                return QVA_ERR_UNSUPPORTED;
+            // the schedule depends on (L, p) only: planned once per p (host planning off the step path)
+            auto it = P->perm_sched.find(p);
+            if (it == P->perm_sched.end()) {
+                std::vector<int> fin;
+                auto passes = perm_passes(P->L, p, &fin);
+                if (passes.empty() || !passes.back().expect) {
+                    set_error("internal: permuted schedule did not complete");
+                    return QVA_ERR_UNSUPPORTED;
+                }
+                it = P->perm_sched.emplace(p, std::make_pair(std::move(passes), std::move(fin))).first;
             }
-            QVA_TRY(run_passes(P, passes, theta, p, 1, P->psi, 0, P->has_psi0 ? 2 : 1, nullptr));
-            P->perm = fin;
+            QVA_TRY(run_passes(P, it->second.first, theta, p, 1, P->psi, 0, P->has_psi0 ? 2 : 1, nullptr));
+            P->perm = it->second.second;
             *have_red = true;
             return QVA_OK;
         }
