@@ -294,6 +294,7 @@ def main():
     clocks.start()
     time.sleep(0.3)
     plan.reset_kernel_stats()
+    plan.set_profiling(True)  # CUDA events around every launch, on the plan's stream, in the timed region
     l0 = plan.launch_count()
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -306,13 +307,6 @@ def main():
     ms = ev0.elapsed_time(ev1)
     launches = plan.launch_count() - l0
     clk = clocks.stop()
-    # per-kernel device times for the roofline: a separate profiled run of the same steps (CUDA
-    # events around every launch on the plan's stream), so the timed region above has no event gaps
-    plan.reset_kernel_stats()
-    plan.set_profiling(True)
-    for _ in range(args.steps):
-        step()
-    barrier()
     plan.set_profiling(False)
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
