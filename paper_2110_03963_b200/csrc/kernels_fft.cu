@@ -390,7 +390,8 @@ struct ColArgs {
     SubFft sf;
 };
 
-__global__ void __launch_bounds__(kFftThreads, 1) fft_col_kernel(const ColArgs a) {
+template <int NT>
+__global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const ColArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     load_roots();
     __shared__ double red[2 * (kFftThreads / 32)];
@@ -847,7 +848,8 @@ qva_status fft_plan_create(uint64_t N, int device, int G, FftPlan **out) {
     cudaMemcpy(fp->d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
     qva_status st = upload_roots();
     if (st != QVA_OK) return fail(st, "");
-    cudaFuncSetAttribute(fft_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
+    cudaFuncSetAttribute(fft_col_kernel<kFftThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
+    cudaFuncSetAttribute(fft_col_kernel<kFftThreads / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
     cudaFuncSetAttribute(fft_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSub * (int)sizeof(double2));
     cudaFuncSetAttribute(fft_whole_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * (int)sizeof(double2));
     if (fp->bluestein) {
@@ -872,7 +874,7 @@ qva_status fft_plan_create(uint64_t N, int device, int G, FftPlan **out) {
         c.out_len = M;
         c.N = M;
         c.do_fwd = 1;
-        fft_col_kernel<<<col_grid(fp), kFftThreads, col_smem(fp)>>>(c);
+        fft_col_kernel<kFftThreads><<<col_grid(fp), kFftThreads, col_smem(fp)>>>(c);
         RowArgs w = row_args(fp, fp->bhat);
         w.fwd_only = 1;
         fft_row_kernel<<<row_grid(fp), kFftThreads, row_smem(fp)>>>(w);
@@ -950,6 +952,15 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
     c.lam = blu ? r.lambda_perm : nullptr;
     const size_t smem_c = col_smem(fp), smem_r = row_smem(fp);
     const int gc = col_grid(fp), gr = row_grid(fp);
+    // column pass with 256-thread CTAs, two per SM (their barrier stalls overlap), when every
+    // stage's butterflies of one column fit a 256-thread round and two column blocks fit smem
+    static int half_env = [] {
+        const char *e = getenv("QVA_FFT_COL256");
+        return e ? atoi(e) : 1;
+    }();
+    bool col_half = half_env != 0 && smem_c <= 110 * 1024;
+    for (int st = 0; st < fp->col.ns && col_half; ++st)
+        if (fp->col.n / fp->col.r[st] > nb_of(fp->col.r[st]) * (kFftThreads / 2)) col_half = false;
 
     // in/out: nullptr -> W; the state (r.psi, length N) is named explicitly
     auto launch_col = [&](const double2 *in, uint64_t in_len, double2 *out, uint64_t out_len, int init, int inv,
@@ -968,7 +979,8 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
                              16.0 * (double)std::min<uint64_t>(out_len, Mi) +
                              ((ops & (OP_PHASE | OP_EXPECT)) ? q_bytes : 0.0) + ((ops & OP_SPEC) && c.lam ? 8.0 * N : 0.0);
         obs->begin(K_FFT_COL, bytes);
-        fft_col_kernel<<<gc, kFftThreads, smem_c, s>>>(c);
+        if (col_half) fft_col_kernel<kFftThreads / 2><<<gc, kFftThreads / 2, smem_c, s>>>(c);
+        else fft_col_kernel<kFftThreads><<<gc, kFftThreads, smem_c, s>>>(c);
         cudaError_t e = cudaGetLastError();
         obs->end();
         if (e != cudaSuccess) {
@@ -1114,7 +1126,7 @@ qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStr
             c.ops = ops;
             c.gamma = gamma;
             obs->begin(K_FFT_COL, 16.0 * NG * (init ? 1 : 2) + ((ops & (OP_PHASE | OP_EXPECT)) ? 8.0 * NG : 0.0));
-            fft_col_kernel<<<gc, kFftThreads, smem_c, s>>>(c);
+            fft_col_kernel<kFftThreads><<<gc, kFftThreads, smem_c, s>>>(c);
             cudaError_t e = cudaGetLastError();
             obs->end();
             if (e != cudaSuccess) {
