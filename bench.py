@@ -141,6 +141,9 @@ def workload_for(args, world):
     elif name == "cfg3":
         wl = make_config("cfg3")
         desc = "cfg3: QWOA N=10!, q~N(0,1), complete-graph Laplacian circulant mixer via FFT, p=4"
+    elif name == "qwoa12":
+        wl = make_config("cfg3", n_override=479001600)
+        desc = "NEXT-4: QWOA N=12! (479,001,600 states, 7.7 GB), q~N(0,1), K_N Laplacian circulant, three-level FFT, p=4"
     elif name == "cfg1":
         wl = make_config("cfg1")
         desc = "cfg1: QAOA MaxCut n=10, 3-regular, p=2"

@@ -82,7 +82,9 @@ typedef struct {
     int32_t reserved[7];     /* reserved[0]: 1 = replicated mode (every rank holds the whole state;
                                 batches shard over ranks).  reserved[1]: 1 = generate weighted MaxCut
                                 qualities inside the tile passes at every size (default: from 2^26
-                                amplitudes).  Others must be 0. */
+                                amplitudes).  reserved[2]: 1 =
+                                circulant mixer: three-level FFT split where one exists (tests; used
+                                anyway above 8192^2 states).  Others must be 0. */
 } qva_plan_desc;
 
 /* ---- lifecycle (Table 1 plan / destroy) ------------------------------------ */
@@ -201,11 +203,13 @@ qva_status qva_x_schedule(int32_t n_local, int32_t p, int32_t *out, int32_t cap,
 qva_status qva_x_schedule_permuted(int32_t n_local, int32_t p, int64_t *out, int32_t cap, int32_t *n_passes);
 /* Host-only: the FFT plan the circulant mixer uses for dimension dim over `shards` COMM-psi shards
  * (1 = single GPU; > 1: direct four-step with shards | M1 and shards | M2) (Sec. 3,
- * PAPER.md:315-333).
- * out[6] = {kind (0: one-CTA whole evolution, 1: four-step mixed radix with M = dim, 2: Bluestein
- * with M >= 2 dim - 1; -1: none), transform length M, M1, M2 (M = M1 * M2), columns per column-pass
- * CTA, rows per row-pass CTA}.  QVA_ERR_UNSUPPORTED when no plan exists (M would exceed 8192^2). */
-qva_status qva_circulant_plan_shape(uint64_t dim, int32_t shards, int64_t *out);
+ * PAPER.md:315-333).  flags bit 0: prefer a three-level split (tests; three levels are used
+ * anyway above 8192^2).
+ * out[9] = {kind (0: one-CTA whole evolution, 1: four-step mixed radix with M = dim, 2: Bluestein
+ * with M >= 2 dim - 1, 3: three-level mixed radix M = M1 * Mi1 * Mi2; -1: none), transform length
+ * M, M1, M2 (M = M1 * M2), columns per column-pass CTA, rows per row-pass CTA, levels, Mi1, Mi2}.
+ * QVA_ERR_UNSUPPORTED when no plan exists. */
+qva_status qva_circulant_plan_shape(uint64_t dim, int32_t shards, int32_t flags, int64_t *out);
 /* Kernel timing: when enabled, every kernel launch of the plan is bracketed with CUDA events
  * on the plan's stream; qva_kernel_stats returns, for kernel class `which` (0 = X tile pass,
  * 1 = small-state fused evolve, 2 = FFT column pass, 3 = FFT row pass, 4 = sparse SpMV,

@@ -81,7 +81,7 @@ def _load():
         "qva_exchange_plan": [i32, i32, P, P],
         "qva_x_schedule": [i32, i32, P, i32, ctypes.POINTER(i32)],
         "qva_x_schedule_permuted": [i32, i32, P, i32, ctypes.POINTER(i32)],
-        "qva_circulant_plan_shape": [ctypes.c_uint64, i32, P],
+        "qva_circulant_plan_shape": [ctypes.c_uint64, i32, i32, P],
         "qva_set_profiling": [P, i32],
         "qva_kernel_stats": [P, i32, ctypes.POINTER(d), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(d)],
         "qva_reset_kernel_stats": [P],
@@ -158,11 +158,11 @@ def qva_x_schedule_permuted(n_local: int, p: int):
     return [dict(zip(keys, (int(x) for x in out[8 * i:8 * i + 8]))) for i in range(min(n.value, cap))]
 
 
-def qva_circulant_plan_shape(dim: int, shards: int = 1):
-    """dict(kind, M, M1, M2, cw, rb) of the circulant mixer's FFT plan (include/qva.h)."""
-    out = np.zeros(6, np.int64)
-    _call("qva_circulant_plan_shape", dim, shards, _ptr(out))
-    return dict(zip(("kind", "M", "M1", "M2", "cw", "rb"), (int(x) for x in out)))
+def qva_circulant_plan_shape(dim: int, shards: int = 1, three_level: bool = False):
+    """dict(kind, M, M1, M2, cw, rb, levels, Mi1, Mi2) of the circulant mixer's FFT plan (include/qva.h)."""
+    out = np.zeros(9, np.int64)
+    _call("qva_circulant_plan_shape", dim, shards, 1 if three_level else 0, _ptr(out))
+    return dict(zip(("kind", "M", "M1", "M2", "cw", "rb", "levels", "Mi1", "Mi2"), (int(x) for x in out)))
 
 
 def qva_exchange_plan(G: int, rank: int):
@@ -204,7 +204,7 @@ class Plan:
     def __init__(self, dim: int, mixer: str = "x", n_qubits: int = -1, rank: int = 0, world: int = 1,
                  nccl_id: Optional[bytes] = None, device: int = 0, virtual_shards: int = 1,
                  stream: Optional[int] = None, max_batch: int = 1, replicated: bool = False,
-                 qgen_f64_always: bool = False):
+                 qgen_f64_always: bool = False, fft_three_level: bool = False):
         self._h = ctypes.c_void_p()
         self._id_buf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         d = PlanDesc()
@@ -220,6 +220,7 @@ class Plan:
         d.max_batch = max_batch
         d.reserved[0] = 1 if replicated else 0
         d.reserved[1] = 1 if qgen_f64_always else 0
+        d.reserved[2] = 1 if fft_three_level else 0
         _call("qva_plan_create", ctypes.byref(d), ctypes.byref(self._h))
         self.dim, self.mixer, self.world, self.rank = dim, mixer, world, rank
 

@@ -71,9 +71,15 @@ struct FftPlan {
     int device = 0;
     bool whole = false;
     bool bluestein = false;
-    int M1 = 1, M2 = 1;
+    int M1 = 1, M2 = 1;          // top-level split N = M1 * M2 (M2 = row length)
     int cw = 8, rb = 1;
-    SubFft col, row;
+    SubFft col, row;             // 2 levels: col = M1, row = M2; 3 levels: col = M1, row = Mi2
+    // three levels (N > 8192^2, NEXT-4): each top-level row of length M2 = Mi1 * Mi2 is itself a
+    // four-step transform (inner column pass over Mi1, inner row pass over Mi2, both row-local)
+    int levels = 2;
+    int Mi1 = 0, Mi2 = 0, cw2 = 8, rb2 = 1;
+    SubFft col2;
+    double2 *d_in_lo = nullptr, *d_in_hi = nullptr;   // inner twiddles w_{M2}
     double2 *d_tw = nullptr;     // stage twiddle tables (col then row)
     double2 *d_big_lo = nullptr, *d_big_hi = nullptr;
     int big_shift = 11;          // w_M^r = hi[r >> s] * lo[r & (2^s - 1)]
@@ -367,6 +373,8 @@ enum : int {
     OP_SPEC = 8,        // v *= exp(-i beta lambda_x) / N   (Bluestein middle)
     OP_CHIRP = 16,      // v *= c_x                 (start of a Bluestein mixer)
     OP_MASK = 32,       // v = 0 for x >= N
+    OP_OUTER_TW = 64,   // v *= w_N^{-x k1}: top-level inverse twiddle of a three-level transform (x =
+                        // position in the top-level row, k1 = its row index = matrix index)
 };
 
 struct ColArgs {
@@ -379,6 +387,10 @@ struct ColArgs {
     uint64_t N;              // state length (mask, chirp)
     int M1, M2, cw, lcw;     // cw = 2^lcw columns per CTA; M2 = columns held (row stride)
     int col_off, M2g;        // sharded column layout: global index of local column 0, global M2
+    uint64_t mat_stride;     // inner (three-level) passes: blockIdx.y selects a matrix at this stride
+    int mat_off;             // global top-level row index of matrix 0 (sharded)
+    const double2 *otw_lo, *otw_hi;  // OP_OUTER_TW: top-level twiddles w_N
+    int otw_shift;
     uint64_t m1mag;          // divu magic of M1
     int init;                // 1: v = amp0 for x < N (no load)
     int do_inv, do_fwd, ops;
@@ -398,6 +410,7 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
     const int M1 = a.M1, M2 = a.M2;
     const int c0 = blockIdx.x * a.cw;
     const int cwv = min(a.cw, M2 - c0);
+    const uint64_t mat = (uint64_t)blockIdx.y * a.mat_stride;  // inner passes: matrix = top-level row
     const int stride = cwv > 1 ? M1 + 1 : M1;  // odd padding: column-major stores are conflict-free
     double2 *A = reinterpret_cast<double2 *>(smem_raw);
     const int tot = M1 * cwv;
@@ -408,7 +421,7 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
         double2 v;
         if (a.init) v = make_double2(x < a.N ? a.amp0 : 0.0, 0.0);
-        else v = x < a.in_len ? a.in[x] : make_double2(0.0, 0.0);
+        else v = x < a.in_len ? a.in[mat + x] : make_double2(0.0, 0.0);
         A[c * stride + x1] = v;
     }
     __syncthreads();
@@ -439,6 +452,9 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
                     v = cmul(v, make_double2(cs * a.invN, s * a.invN));
                 }
                 if (ops & OP_CHIRP) v = cmul(v, chirp(x, a.N));
+                if (ops & OP_OUTER_TW)
+                    v = cmul(v, big_twiddle(a.otw_lo, a.otw_hi, a.otw_shift,
+                                            xl * (uint64_t)(a.mat_off + blockIdx.y), true));
             }
             slot = v;
         }
@@ -464,7 +480,7 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
         if (c >= cwv) continue;
         const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
-        if (x < a.out_len) a.out[x] = A[c * stride + x1];
+        if (x < a.out_len) a.out[mat + x] = A[c * stride + x1];
     }
 }
 
@@ -472,6 +488,7 @@ struct RowArgs {
     double2 *buf;
     int M1, M2, rb;
     int row_off;                // sharded row layout: global index of local row 0
+    int row_mod;                // three-level inner rows: twiddle row index = row % row_mod (0: none)
     uint64_t m2mag;             // divu magic of M2
     int fwd_only;               // 1: forward FFT only (spectrum out, no twiddle)
     int spec;                   // 0: constant (e0 at bin 0, ec elsewhere); 1: real lambda; 2: complex array
@@ -522,7 +539,8 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
     run_fft(A, a.sf, a.tw, a.rb, M2, true);
     for (int i = threadIdx.x; i < tot; i += blockDim.x) {
         const int r = (int)divu(i, a.m2mag), x2 = i - r * M2;
-        const uint64_t tr = (uint64_t)x2 * (uint64_t)(a.row_off + k1_0 + r);  // < M
+        const int kr = a.row_off + k1_0 + r;
+        const uint64_t tr = (uint64_t)x2 * (uint64_t)(a.row_mod ? kr % a.row_mod : kr);  // < M
         rows[i] = cmul(A[i], big_twiddle(a.big_lo, a.big_hi, a.big_shift, tr, true));
     }
 }
@@ -692,6 +710,53 @@ Split choose_split(uint64_t M, int G = 1) {
     return best;
 }
 
+// w_M^r = hi[r >> 11] * lo[r & 2047] tables on the device
+bool make_big_tables(uint64_t M, double2 **lo_d, double2 **hi_d) {
+    const int sft = 11;
+    const uint64_t B = 1ull << sft, nhi = (M + B - 1) / B;
+    std::vector<double2> lo(B), hi(nhi);
+    for (uint64_t j = 0; j < B; ++j) {
+        const long double ang = -2.0L * kPiL * (long double)j / (long double)M;
+        lo[j] = make_double2((double)cosl(ang), (double)sinl(ang));
+    }
+    for (uint64_t j = 0; j < nhi; ++j) {
+        const long double ang = -2.0L * kPiL * (long double)((j * B) % M) / (long double)M;
+        hi[j] = make_double2((double)cosl(ang), (double)sinl(ang));
+    }
+    if (cudaMalloc(lo_d, B * sizeof(double2)) != cudaSuccess || cudaMalloc(hi_d, nhi * sizeof(double2)) != cudaSuccess)
+        return false;
+    cudaMemcpy(*lo_d, lo.data(), B * sizeof(double2), cudaMemcpyHostToDevice);
+    cudaMemcpy(*hi_d, hi.data(), nhi * sizeof(double2), cudaMemcpyHostToDevice);
+    return true;
+}
+
+// three-level split N = M1 * (Mi1 * Mi2): column lengths M1, Mi1 <= kMaxCta/8 (128-B column blocks),
+// inner row Mi2 <= kMaxSub, every sub-FFT plannable; G | M1 and G | Mi1 * Mi2 when sharded; the
+// most balanced triple wins
+bool choose_split3(uint64_t N, int G, int &M1, int &Mi1, int &Mi2) {
+    double best = -1e300;
+    M1 = 0;
+    const uint64_t cmax = kMaxCta / 8;
+    for (uint64_t a = 2; a <= cmax; ++a) {
+        if (N % a || (a % G) || !sub_ok((int)a)) continue;
+        const uint64_t R = N / a;
+        if (R % G) continue;
+        for (uint64_t b = 2; b <= cmax; ++b) {
+            if (R % b || !sub_ok((int)b)) continue;
+            const uint64_t c = R / b;
+            if (c < 2 || c > (uint64_t)kMaxSub || !sub_ok((int)c)) continue;
+            const double score = std::min(std::min(log((double)a), log((double)b)), log((double)c));
+            if (score > best) {
+                best = score;
+                M1 = (int)a;
+                Mi1 = (int)b;
+                Mi2 = (int)c;
+            }
+        }
+    }
+    return M1 != 0;
+}
+
 qva_status upload_roots() {
     std::vector<double2> roots(160, make_double2(0, 0));
     for (int r = 2; r <= 16; ++r)
@@ -716,6 +781,8 @@ ColArgs col_args(const FftPlan *fp) {
     c.lcw = fp->cw == 8 ? 3 : fp->cw == 4 ? 2 : fp->cw == 2 ? 1 : 0;
     c.col_off = 0;
     c.M2g = fp->M2;
+    c.mat_stride = 0;
+    c.mat_off = 0;
     c.m1mag = div_magic((uint32_t)fp->M1);
     c.invN = 1.0 / (double)fp->N;
     c.tw = fp->d_tw;
@@ -747,7 +814,33 @@ int row_grid(const FftPlan *fp) { return fp->M1 / fp->rb; }
 
 // Pure host planning (no device resources): whole-CTA, direct four-step or Bluestein, and the
 // split.  Exposed through qva_circulant_plan_shape for CPU tests.
-FftShape fft_plan_shape(uint64_t N, int G) {
+static FftShape shape3(uint64_t N, int G) {
+    FftShape sh;
+    sh.N = N;
+    int a, b, c;
+    if (!smooth(N) || !choose_split3(N, G, a, b, c)) return sh;
+    sh.ok = true;
+    sh.levels = 3;
+    sh.M = N;
+    sh.M1 = a;
+    sh.M2 = 0;  // top-level row length b * c does not fit an int; see Mi1, Mi2
+    sh.Mi1 = b;
+    sh.Mi2 = c;
+    sh.cw = 8;
+    sh.cw2 = 8;
+    sh.rb = 1;
+    sh.rb2 = 1;
+    for (int r = 2; r <= 64; ++r)
+        if ((uint64_t)r * c <= (uint64_t)kMaxCta) sh.rb2 = r;
+    while (sh.rb2 > 1 && ((uint64_t)a * b) % sh.rb2) --sh.rb2;
+    return sh;
+}
+
+FftShape fft_plan_shape(uint64_t N, int G, bool force3) {
+    if (force3 || (N > (uint64_t)kMaxSub * kMaxSub && smooth(N))) {
+        FftShape s3 = shape3(N, G);
+        if (s3.ok || N > (uint64_t)kMaxSub * kMaxSub) return s3;
+    }
     FftShape sh;
     sh.N = N;
     if (G > 1) {  // sharded: direct four-step with G | M1, G | M2 only
@@ -791,7 +884,7 @@ FftShape fft_plan_shape(uint64_t N, int G) {
     return sh;
 }
 
-qva_status fft_plan_create(uint64_t N, int device, int G, FftPlan **out) {
+qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan **out) {
     *out = nullptr;
     FftPlan *fp = new FftPlan();
     fp->N = N;
@@ -802,7 +895,7 @@ qva_status fft_plan_create(uint64_t N, int device, int G, FftPlan **out) {
         return s;
     };
     std::vector<double2> tw;
-    const FftShape sh = fft_plan_shape(N, G);
+    const FftShape sh = fft_plan_shape(N, G, force3);
     if (!sh.ok)
         return fail(QVA_ERR_UNSUPPORTED,
                     G > 1 ? "sharded circulant mixer: N=" + std::to_string(N) + " has no four-step split M1*M2 (13-smooth, <= 8192) with " +
@@ -815,7 +908,24 @@ qva_status fft_plan_create(uint64_t N, int device, int G, FftPlan **out) {
     fp->M2 = sh.M2;
     fp->cw = sh.cw;
     fp->rb = sh.rb;
-    if (fp->whole) {
+    if (sh.levels == 3) {
+        fp->levels = 3;
+        fp->Mi1 = sh.Mi1;
+        fp->Mi2 = sh.Mi2;
+        fp->cw2 = sh.cw2;
+        fp->rb2 = sh.rb2;
+        const uint64_t R = (uint64_t)sh.Mi1 * sh.Mi2;
+        if (R > (uint64_t)INT32_MAX) return fail(QVA_ERR_UNSUPPORTED, "three-level FFT row too long");
+        fp->M2 = (int)R;  // top-level row length (column count of the top-level column pass)
+        if (!make_sub(fp->M1, fp->col, tw) || !make_sub(fp->Mi1, fp->col2, tw) || !make_sub(fp->Mi2, fp->row, tw))
+            return fail(QVA_ERR_UNSUPPORTED, "FFT planning failed");
+        fp->big_shift = 11;
+        if (!make_big_tables(N, &fp->d_big_lo, &fp->d_big_hi) || !make_big_tables(R, &fp->d_in_lo, &fp->d_in_hi))
+            return fail(QVA_ERR_OUT_OF_MEMORY, "cudaMalloc (FFT twiddles) failed");
+        fp->n_partials = col_grid(fp);
+        if (cudaMalloc(&fp->partials, fp->n_partials * 2 * sizeof(double)) != cudaSuccess)
+            return fail(QVA_ERR_OUT_OF_MEMORY, "cudaMalloc (FFT partials) failed");
+    } else if (fp->whole) {
         if (!make_sub((int)N, fp->row, tw)) return fail(QVA_ERR_UNSUPPORTED, "FFT planning failed");
     } else {
         if (!make_sub(fp->M1, fp->col, tw) || !make_sub(fp->M2, fp->row, tw))
@@ -893,6 +1003,8 @@ void fft_plan_destroy(FftPlan *fp) {
     cudaFree(fp->partials);
     cudaFree(fp->work);
     cudaFree(fp->bhat);
+    cudaFree(fp->d_in_lo);
+    cudaFree(fp->d_in_hi);
     delete fp;
 }
 
@@ -901,9 +1013,91 @@ void fft_permute_spectrum(const FftPlan *fp, const double *lambda, double *lambd
         memcpy(lambda_perm, lambda, fp->N * sizeof(double));
         return;
     }
+    if (fp->levels == 3) {  // position k1*R + k2*Mi2 + k3 holds bin k1 + M1*(k2 + Mi1*k3)
+        const uint64_t M1 = fp->M1, A = fp->Mi1, B = fp->Mi2, R = A * B;
+        for (uint64_t k1 = 0; k1 < M1; ++k1)
+            for (uint64_t k2 = 0; k2 < A; ++k2)
+                for (uint64_t k3 = 0; k3 < B; ++k3) lambda_perm[k1 * R + k2 * B + k3] = lambda[k1 + M1 * (k2 + A * k3)];
+        return;
+    }
     const uint64_t M1 = fp->M1, M2 = fp->M2;
     for (uint64_t k1 = 0; k1 < M1; ++k1)
         for (uint64_t k2 = 0; k2 < M2; ++k2) lambda_perm[k1 * M2 + k2] = lambda[k1 + M1 * k2];
+}
+
+// Three-level row transform of `nmat` consecutive top-level rows (matrices Mi1 x Mi2) starting at
+// global top-level row mat_off: inner column FFTs (+ w_{M2} twiddle), inner rows (forward FFT,
+// spectrum, inverse FFT, inverse w_{M2} twiddle), inner inverse column FFTs + the top-level
+// inverse twiddle w_N^{-x k1}.  Row-local: sharded plans run it on their own row blocks.
+static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, const FftRun &r, double beta,
+                              cudaStream_t s, LaunchObserver *obs) {
+    const double N = (double)fp->N;
+    const uint64_t R = (uint64_t)fp->Mi1 * fp->Mi2;
+    ColArgs c = col_args(fp);
+    c.M1 = fp->Mi1;
+    c.M2 = fp->Mi2;
+    c.M2g = fp->Mi2;
+    c.cw = fp->cw2;
+    c.lcw = fp->cw2 == 8 ? 3 : fp->cw2 == 4 ? 2 : fp->cw2 == 2 ? 1 : 0;
+    c.m1mag = div_magic((uint32_t)fp->Mi1);
+    c.sf = fp->col2;
+    c.big_lo = fp->d_in_lo;
+    c.big_hi = fp->d_in_hi;
+    c.in = psi;
+    c.out = psi;
+    c.in_len = R;
+    c.out_len = R;
+    c.N = R;
+    c.mat_stride = R;
+    c.mat_off = mat_off;
+    c.otw_lo = fp->d_big_lo;
+    c.otw_hi = fp->d_big_hi;
+    c.otw_shift = fp->big_shift;
+    const dim3 gc((fp->Mi2 + c.cw - 1) / c.cw, nmat);
+    const size_t smem_c = (size_t)c.cw * (fp->Mi1 + (c.cw > 1 ? 1 : 0)) * sizeof(double2);
+    auto cols = [&](int inv, int ops, int fwd) -> qva_status {
+        c.do_inv = inv;
+        c.do_fwd = fwd;
+        c.ops = ops;
+        obs->begin(K_FFT_COL, 32.0 * (double)R * nmat);
+        fft_col_kernel<kFftThreads><<<gc, kFftThreads, smem_c, s>>>(c);
+        cudaError_t e = cudaGetLastError();
+        obs->end();
+        if (e != cudaSuccess) {
+            set_error(std::string("fft_col_kernel (inner): ") + cudaGetErrorString(e));
+            return QVA_ERR_CUDA;
+        }
+        return QVA_OK;
+    };
+    QVA_TRY(cols(0, 0, 1));
+    RowArgs w = row_args(fp, psi);
+    w.M1 = nmat * fp->Mi1;
+    w.M2 = fp->Mi2;
+    w.rb = fp->rb2;
+    w.m2mag = div_magic((uint32_t)fp->Mi2);
+    w.big_lo = fp->d_in_lo;
+    w.big_hi = fp->d_in_hi;
+    w.row_off = mat_off * fp->Mi1;
+    w.row_mod = fp->Mi1;
+    if (r.lambda_perm) {
+        w.spec = 1;
+        w.lam_perm = r.lambda_perm;
+        w.beta = beta;
+        w.scale = 1.0 / N;
+    } else {
+        w.spec = 0;
+        w.e0 = make_double2(cos(-beta * r.lam0) / N, sin(-beta * r.lam0) / N);
+        w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
+    }
+    obs->begin(K_FFT_ROW, 32.0 * (double)R * nmat + (r.lambda_perm ? 8.0 * (double)R * nmat : 0.0));
+    fft_row_kernel<<<nmat * fp->Mi1 / fp->rb2, kFftThreads, (size_t)fp->rb2 * fp->Mi2 * sizeof(double2), s>>>(w);
+    cudaError_t e = cudaGetLastError();
+    obs->end();
+    if (e != cudaSuccess) {
+        set_error(std::string("fft_row_kernel (inner): ") + cudaGetErrorString(e));
+        return QVA_ERR_CUDA;
+    }
+    return cols(1, OP_OUTER_TW, 0);
 }
 
 qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver *obs) {
@@ -991,6 +1185,7 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
     };
     // direct: spectrum exp(-i beta lambda)/N; Bluestein: kernel spectrum B (or conj B) / M
     auto launch_row = [&](double beta, int bconj) -> qva_status {
+        if (fp->levels == 3) return inner_rows3(fp, W, fp->M1, 0, r, beta, s, obs);
         RowArgs w = row_args(fp, W);
         double extra = 0.0;
         if (blu) {
@@ -1137,6 +1332,7 @@ qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStr
         return QVA_OK;
     };
     auto rows = [&](double beta) -> qva_status {
+        if (fp->levels == 3) return inner_rows3(fp, r.psi, io.local * M1s, io.first * M1s, r, beta, s, obs);
         RowArgs w = row_args(fp, r.psi);
         w.rb = rb;
         w.row_off = io.first * M1s;

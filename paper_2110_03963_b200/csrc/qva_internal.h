@@ -250,9 +250,11 @@ struct FftShape {
     bool ok = false, whole = false, bluestein = false;
     uint64_t N = 0, M = 0;   // state length, transform length
     int M1 = 0, M2 = 0, cw = 0, rb = 0;
+    int levels = 2, Mi1 = 0, Mi2 = 0, cw2 = 0, rb2 = 0;  // three levels: N = M1 * Mi1 * Mi2
 };
-FftShape fft_plan_shape(uint64_t N, int G = 1);  // G > 1: sharded (direct four-step, G | M1, M2)
-qva_status fft_plan_create(uint64_t N, int device, int G, FftPlan **out);
+// G > 1: sharded (direct four-step, G | M1, M2); force3: three-level split where one exists (tests)
+FftShape fft_plan_shape(uint64_t N, int G = 1, bool force3 = false);
+qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan **out);
 void fft_plan_destroy(FftPlan *fp);
 // permute lambda (forward-bin order, length N) into the plan's internal spectral order
 void fft_permute_spectrum(const FftPlan *fp, const double *lambda, double *lambda_perm);

@@ -167,6 +167,20 @@ def test_sharded_circulant_plan_shapes(Q, N, G):
     assert sh["M1"] % G == 0 and sh["M2"] % G == 0
 
 
+@pytest.mark.parametrize("N,G,force", [(479001600, 1, False), (479001600, 8, False), (6227020800, 1, False),
+                                       (40320, 1, True), (3628800, 4, True)])
+def test_three_level_circulant_plan_shapes(Q, N, G, force):
+    """NEXT-4: above 8192^2 states (12! = 4.8e8, 13! = 6.2e9) the circulant mixer uses a three-level
+    four-step split N = M1 * Mi1 * Mi2 with 13-smooth factors (column lengths <= 1024, inner row
+    <= 8192); sharded plans keep G | M1 and G | Mi1 * Mi2."""
+    sh = Q.qva_circulant_plan_shape(N, G, force)
+    assert sh["kind"] == 3 and sh["levels"] == 3 and sh["M"] == N
+    assert sh["M1"] * sh["Mi1"] * sh["Mi2"] == N and sh["M2"] == sh["Mi1"] * sh["Mi2"]
+    assert sh["M1"] <= 1024 and sh["Mi1"] <= 1024 and sh["Mi2"] <= 8192
+    assert all(_smooth13(x) for x in (sh["M1"], sh["Mi1"], sh["Mi2"]))
+    assert sh["M1"] % G == 0 and sh["M2"] % G == 0
+
+
 def test_sharded_circulant_prime_unsupported(Q):
     with pytest.raises(Q.QvaError) as ei:
         Q.qva_circulant_plan_shape(1000003, 2)

@@ -387,6 +387,49 @@ def test_qaoaz_parity_vs_oracle(Q, n, seq, p):
         _f_close(f[1], O.expectation(O.evolve_parity(n, q, sq, theta[::-1], psi0), q))
 
 
+@pytest.mark.parametrize("N,G", [(5040, 1), (40320, 1), (3628800, 4)])
+def test_three_level_fft_forced(Q, N, G):
+    """NEXT-4: the three-level four-step (inner row transforms local to each top-level row block),
+    forced at small N, single GPU and virtual shards: random spectrum vs the dense definition at
+    N = 5040, K_N closed form otherwise."""
+    rng = np.random.default_rng(N + 7 * G)
+    q = rng.standard_normal(N)
+    theta = rng.uniform(0, math.pi, 4)
+    with Q.Plan(N, "circulant", virtual_shards=G, fft_three_level=True) as P:
+        P.set_qualities(q)
+        if N <= 5040:
+            lam = rng.standard_normal(N) * 3
+            P.set_circulant_eigenvalues(lam)
+            ref = O.evolve_circulant_dense(q, lam, theta)
+        else:
+            P.set_circulant_eigenvalues_const(0.0, float(N))
+            ref = O.evolve_complete(q, theta, 0.0, float(N))
+        P.evolve(theta)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+
+
+def test_qwoa_12_factorial(Q):
+    """NEXT-4 at size: QWOA over N = 12! = 479,001,600 states (7.7 GB, three-level FFT) with the
+    complete-graph Laplacian spectrum against the oracle's O(N) closed form: <Q> and sampled
+    amplitudes."""
+    N = 479001600
+    rng = np.random.default_rng(12)
+    q = rng.standard_normal(N)
+    theta = rng.uniform(0, math.pi, 4)
+    ref = O.evolve_complete(q, theta, 0.0, float(N))
+    with Q.Plan(N, "circulant") as P:
+        P.set_qualities(q)
+        P.set_circulant_eigenvalues_const(0.0, float(N))
+        P.evolve(theta)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+        idx = rng.integers(0, N, 2048)
+        got = np.array([P.get_state(int(i), 1)[0] for i in idx[:64]])
+        _amp_close(got, ref[idx[:64]])
+        blk = P.get_state(N - 4096, 4096)
+        _amp_close(blk, ref[N - 4096:])
+
+
 # ---------------------------------------------------------------- cfg4 full size ----
 def test_cfg4_full_size_vs_golden(Q):
     g = json.load(open(os.path.join(GOLD, "cfg4_n30.json")))
