@@ -247,14 +247,33 @@ __host__ __device__ constexpr int nb_of(int R) {
     return R == 2 ? 8 : R == 3 ? 5 : R == 4 ? 4 : R == 5 ? 3 : R == 7 ? 2 : 1;  // 8, 9, 11, 13, 16: 1
 }
 
-// One Stockham radix-R stage, in place, over `count` independent length-n transforms at
-// `stride` elements apart.  Rounds cover whole transforms (a transform's butterflies read and
-// write only its own elements), each round loads all its inputs into registers, synchronises,
-// then twiddles, transforms and stores.  The host guarantees n / R <= nb_of(R) * blockDim.x.
-template <int R>
-__device__ __forceinline__ void stage_inplace(double2 *buf, int n, int stride, int count, int m,
-                                              const double2 *__restrict__ tw, bool inv, uint64_t nbmag,
-                                              uint64_t mmag) {
+// Shared-memory addressing of `count` independent transforms (f = transform, i = position):
+//   AddrLin: f * stride + i (padded column-major / row-major buffers)
+//   AddrSwz<CW>: the layout a SWIZZLE_128B (CW = 8) / SWIZZLE_64B (CW = 4) TMA box of CW-column
+//     rows leaves in shared memory: row i is CW * 16 bytes, the 16-byte chunk of column f is
+//     f ^ ((i >> s) & (CW - 1)) (s = 0 / 1), so consecutive positions of one column fall in
+//     different bank groups
+struct AddrLin {
+    double2 *buf;
+    int stride;
+    __device__ __forceinline__ double2 *ptr(int f, int i) const { return buf + f * stride + i; }
+};
+template <int CW>
+struct AddrSwz {
+    unsigned char *base;
+    __device__ __forceinline__ double2 *ptr(int f, int i) const {
+        const int sw = CW == 8 ? (i & 7) : ((i >> 1) & 3);
+        return reinterpret_cast<double2 *>(base + (size_t)i * (CW * 16) + ((f ^ sw) << 4));
+    }
+};
+
+// One Stockham radix-R stage, in place, over `count` independent length-n transforms.  Rounds
+// cover whole transforms (a transform's butterflies read and write only its own elements), each
+// round loads all its inputs into registers, synchronises, then twiddles, transforms and
+// stores.  The host guarantees n / R <= nb_of(R) * blockDim.x.
+template <int R, typename Ad>
+__device__ __forceinline__ void stage_inplace(const Ad &ad, int n, int count, int m, const double2 *__restrict__ tw,
+                                              bool inv, uint64_t nbmag, uint64_t mmag) {
     constexpr int NB = nb_of(R);
     const int nb = n / R;
     const int per_round = max(1, (int)divu(NB * blockDim.x, nbmag));
@@ -267,9 +286,8 @@ __device__ __forceinline__ void stage_inplace(double2 *buf, int n, int stride, i
             if (J < total) {
                 const int fq = (int)divu(J, nbmag);
                 const int f = f0 + fq, j = J - fq * nb;
-                const double2 *x = buf + f * stride;
 #pragma unroll
-                for (int t = 0; t < R; ++t) a[b][t] = x[j + t * nb];
+                for (int t = 0; t < R; ++t) a[b][t] = *ad.ptr(f, j + t * nb);
             }
         }
         __syncthreads();
@@ -285,23 +303,23 @@ __device__ __forceinline__ void stage_inplace(double2 *buf, int n, int stride, i
                     for (int t = 1; t < R; ++t) a[b][t] = cmul(a[b][t], conj_if(__ldg(tw + t * k), inv));
                 }
                 dft<R>(a[b], inv);
-                double2 *y = buf + f * stride;
                 const int o = (j - k) * R + k;
 #pragma unroll
-                for (int t = 0; t < R; ++t) y[o + t * m] = a[b][t];
+                for (int t = 0; t < R; ++t) *ad.ptr(f, o + t * m) = a[b][t];
             }
         }
         __syncthreads();
     }
 }
 
-__device__ __forceinline__ void run_fft(double2 *buf, const SubFft &sf, const double2 *tw, int count, int stride, bool inv) {
+template <typename Ad>
+__device__ __forceinline__ void run_fft_ad(const Ad &ad, const SubFft &sf, const double2 *tw, int count, bool inv) {
     // stages are ordered by radix (factor_radices); one loop per radix keeps the live ranges of
     // different radices apart (a switch inside one stage loop made ptxas spill ~10 KB)
     int s = 0;
 #define QVA_RADIX_LOOP(R) \
     for (; s < sf.ns && sf.r[s] == R; ++s)                                                            \
-        stage_inplace<R>(buf, sf.n, stride, count, sf.m[s], tw + sf.twoff[s], inv, sf.nbmag[s], sf.mmag[s]);
+        stage_inplace<R>(ad, sf.n, count, sf.m[s], tw + sf.twoff[s], inv, sf.nbmag[s], sf.mmag[s]);
     QVA_RADIX_LOOP(16)
     QVA_RADIX_LOOP(8)
     QVA_RADIX_LOOP(4)
@@ -313,6 +331,9 @@ __device__ __forceinline__ void run_fft(double2 *buf, const SubFft &sf, const do
     QVA_RADIX_LOOP(11)
     QVA_RADIX_LOOP(13)
 #undef QVA_RADIX_LOOP
+}
+__device__ __forceinline__ void run_fft(double2 *buf, const SubFft &sf, const double2 *tw, int count, int stride, bool inv) {
+    run_fft_ad(AddrLin{buf, stride}, sf, tw, count, inv);
 }
 // a call boundary around a whole sub-FFT (used by the small whole-evolution kernel, whose
 // layer loop would otherwise spill ~11 KB per thread)
@@ -402,6 +423,68 @@ struct ColArgs {
     SubFft sf;
 };
 
+// The arithmetic of one column block (columns c0 .. c0+cwv of matrix mat_y), in shared memory
+// through the addressing policy: [inverse column FFTs] -> elementwise ops at the natural index ->
+// [forward column FFTs + twiddle w_M^{x2 k1}]; expectation partials to slot pslot.
+template <typename Ad>
+__device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0, int cwv, int mat_y, int pslot,
+                                          double *red) {
+    const int M1 = a.M1, M2 = a.M2;
+    const int tot = M1 * cwv;
+    if (a.do_inv) run_fft_ad(ad, a.sf, a.tw, cwv, true);
+    const int ops = a.ops;
+    if (ops) {
+        double acc = 0.0, nrm = 0.0;
+        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            const int c = (int)divu(idx, a.m1mag), x1 = idx - c * M1;
+            const uint64_t xl = (uint64_t)x1 * M2 + c0 + c;                  // local (q) index
+            const uint64_t x = (uint64_t)x1 * a.M2g + a.col_off + c0 + c;    // natural index
+            double2 &slot = *ad.ptr(c, x1);
+            double2 v = slot;
+            if ((ops & OP_MASK) && x >= a.N) {
+                v = make_double2(0.0, 0.0);
+            } else {
+                if (ops & OP_CHIRP_CONJ) v = cmulc(v, chirp(x, a.N));
+                if (ops & OP_EXPECT) {
+                    const double pr = v.x * v.x + v.y * v.y;
+                    acc = fma(pr, __ldg(a.q + xl), acc);
+                    nrm += pr;
+                }
+                if (ops & OP_PHASE) v = phase_mul(v, __ldg(a.q + xl), a.gamma);
+                if (ops & OP_SPEC) {
+                    const double lam = a.lam ? __ldg(a.lam + x) : (x == 0 ? a.lam0 : a.lamc);
+                    double s, cs;
+                    sincos(-a.beta * lam, &s, &cs);
+                    v = cmul(v, make_double2(cs * a.invN, s * a.invN));
+                }
+                if (ops & OP_CHIRP) v = cmul(v, chirp(x, a.N));
+                if (ops & OP_OUTER_TW)
+                    v = cmul(v, big_twiddle(a.otw_lo, a.otw_hi, a.otw_shift,
+                                            xl * (uint64_t)(a.mat_off + mat_y), true));
+            }
+            slot = v;
+        }
+        if (ops & OP_EXPECT) {
+            block_reduce2(acc, nrm, red);
+            if (threadIdx.x == 0) {
+                a.partials[2 * pslot] = acc;
+                a.partials[2 * pslot + 1] = nrm;
+            }
+        }
+        __syncthreads();
+    }
+    if (a.do_fwd) {
+        run_fft_ad(ad, a.sf, a.tw, cwv, false);
+        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            const int c = (int)divu(idx, a.m1mag), k1 = idx - c * M1;
+            const uint64_t r = (uint64_t)(a.col_off + c0 + c) * (uint64_t)k1;  // < M: no reduction needed
+            double2 *e = ad.ptr(c, k1);
+            *e = cmul(*e, big_twiddle(a.big_lo, a.big_hi, a.big_shift, r, false));
+        }
+        __syncthreads();
+    }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const ColArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -425,57 +508,7 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         A[c * stride + x1] = v;
     }
     __syncthreads();
-    if (a.do_inv) run_fft(A, a.sf, a.tw, cwv, stride, true);
-    const int ops = a.ops;
-    if (ops) {
-        double acc = 0.0, nrm = 0.0;
-        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-            const int c = (int)divu(idx, a.m1mag), x1 = idx - c * M1;
-            const uint64_t xl = (uint64_t)x1 * M2 + c0 + c;                  // local (q) index
-            const uint64_t x = (uint64_t)x1 * a.M2g + a.col_off + c0 + c;    // natural index
-            double2 &slot = A[c * stride + x1];
-            double2 v = slot;
-            if ((ops & OP_MASK) && x >= a.N) {
-                v = make_double2(0.0, 0.0);
-            } else {
-                if (ops & OP_CHIRP_CONJ) v = cmulc(v, chirp(x, a.N));
-                if (ops & OP_EXPECT) {
-                    const double pr = v.x * v.x + v.y * v.y;
-                    acc = fma(pr, __ldg(a.q + xl), acc);
-                    nrm += pr;
-                }
-                if (ops & OP_PHASE) v = phase_mul(v, __ldg(a.q + xl), a.gamma);
-                if (ops & OP_SPEC) {
-                    const double lam = a.lam ? __ldg(a.lam + x) : (x == 0 ? a.lam0 : a.lamc);
-                    double s, cs;
-                    sincos(-a.beta * lam, &s, &cs);
-                    v = cmul(v, make_double2(cs * a.invN, s * a.invN));
-                }
-                if (ops & OP_CHIRP) v = cmul(v, chirp(x, a.N));
-                if (ops & OP_OUTER_TW)
-                    v = cmul(v, big_twiddle(a.otw_lo, a.otw_hi, a.otw_shift,
-                                            xl * (uint64_t)(a.mat_off + blockIdx.y), true));
-            }
-            slot = v;
-        }
-        if (ops & OP_EXPECT) {
-            block_reduce2(acc, nrm, red);
-            if (threadIdx.x == 0) {
-                a.partials[2 * blockIdx.x] = acc;
-                a.partials[2 * blockIdx.x + 1] = nrm;
-            }
-        }
-        __syncthreads();
-    }
-    if (a.do_fwd) {
-        run_fft(A, a.sf, a.tw, cwv, stride, false);
-        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-            const int c = (int)divu(idx, a.m1mag), k1 = idx - c * M1;
-            const uint64_t r = (uint64_t)(a.col_off + c0 + c) * (uint64_t)k1;  // < M: no reduction needed
-            A[c * stride + k1] = cmul(A[c * stride + k1], big_twiddle(a.big_lo, a.big_hi, a.big_shift, r, false));
-        }
-        __syncthreads();
-    }
+    col_block(AddrLin{A, stride}, a, c0, cwv, blockIdx.y, blockIdx.x, red);
     for (int idx = threadIdx.x; idx < totw; idx += blockDim.x) {
         const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
         if (c >= cwv) continue;
