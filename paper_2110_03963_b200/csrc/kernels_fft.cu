@@ -119,14 +119,20 @@ __device__ __forceinline__ double2 mul_mi(double2 a, bool inv) {
 // cos / sin (2 pi j / N) for the two-level radix-16 and radix-9 butterflies (compile-time
 // constants: indices are unrolled, so they fold into immediates)
 __host__ __device__ constexpr double tw_cos(int N, int j) {
-    constexpr double c16[16] = {1.0, 0.9238795325112867, 0.7071067811865476, 0.38268343236508984, 6.123233995736766e-17, -0.3826834323650897, -0.7071067811865475, -0.9238795325112867, -1.0, -0.9238795325112868, -0.7071067811865477, -0.38268343236509034, -1.8369701987210297e-16, 0.38268343236509, 0.7071067811865474, 0.9238795325112865};
+    constexpr double c7[7] = {1.0, 0.6234898018587336, -0.22252093395631434, -0.900968867902419, -0.9009688679024191, -0.2225209339563146, 0.6234898018587334};
     constexpr double c9[9] = {1.0, 0.766044443118978, 0.17364817766693041, -0.4999999999999998, -0.9396926207859083, -0.9396926207859084, -0.5000000000000004, 0.17364817766692997, 0.7660444431189778};
-    return N == 16 ? c16[j] : c9[j];
+    constexpr double c11[11] = {1.0, 0.8412535328311812, 0.41541501300188644, -0.142314838273285, -0.654860733945285, -0.9594929736144974, -0.9594929736144975, -0.6548607339452852, -0.14231483827328523, 0.41541501300188605, 0.8412535328311812};
+    constexpr double c13[13] = {1.0, 0.8854560256532099, 0.5680647467311559, 0.120536680255323, -0.35460488704253545, -0.7485107481711012, -0.970941817426052, -0.9709418174260521, -0.7485107481711013, -0.3546048870425359, 0.1205366802553232, 0.5680647467311548, 0.88545602565321};
+    constexpr double c16[16] = {1.0, 0.9238795325112867, 0.7071067811865476, 0.38268343236508984, 6.123233995736766e-17, -0.3826834323650897, -0.7071067811865475, -0.9238795325112867, -1.0, -0.9238795325112868, -0.7071067811865477, -0.38268343236509034, -1.8369701987210297e-16, 0.38268343236509, 0.7071067811865474, 0.9238795325112865};
+    return N == 16 ? c16[j] : N == 13 ? c13[j] : N == 11 ? c11[j] : N == 9 ? c9[j] : c7[j];
 }
 __host__ __device__ constexpr double tw_sin(int N, int j) {
-    constexpr double s16[16] = {0.0, 0.3826834323650898, 0.7071067811865475, 0.9238795325112867, 1.0, 0.9238795325112867, 0.7071067811865476, 0.3826834323650899, 1.2246467991473532e-16, -0.38268343236508967, -0.7071067811865475, -0.9238795325112865, -1.0, -0.9238795325112866, -0.7071067811865477, -0.3826834323650904};
+    constexpr double s7[7] = {0.0, 0.7818314824680298, 0.9749279121818236, 0.43388373911755823, -0.433883739117558, -0.9749279121818236, -0.7818314824680299};
     constexpr double s9[9] = {0.0, 0.6427876096865393, 0.984807753012208, 0.8660254037844387, 0.3420201433256689, -0.34202014332566866, -0.8660254037844384, -0.9848077530122081, -0.6427876096865396};
-    return N == 16 ? s16[j] : s9[j];
+    constexpr double s11[11] = {0.0, 0.5406408174555976, 0.9096319953545183, 0.9898214418809328, 0.7557495743542583, 0.28173255684142967, -0.2817325568414294, -0.7557495743542582, -0.9898214418809327, -0.9096319953545186, -0.5406408174555974};
+    constexpr double s13[13] = {0.0, 0.4647231720437685, 0.8229838658936564, 0.992708874098054, 0.9350162426854148, 0.6631226582407952, 0.23931566428755768, -0.23931566428755743, -0.663122658240795, -0.9350162426854147, -0.992708874098054, -0.822983865893657, -0.4647231720437684};
+    constexpr double s16[16] = {0.0, 0.3826834323650898, 0.7071067811865475, 0.9238795325112867, 1.0, 0.9238795325112867, 0.7071067811865476, 0.3826834323650899, 1.2246467991473532e-16, -0.38268343236508967, -0.7071067811865475, -0.9238795325112865, -1.0, -0.9238795325112866, -0.7071067811865477, -0.3826834323650904};
+    return N == 16 ? s16[j] : N == 13 ? s13[j] : N == 11 ? s11[j] : N == 9 ? s9[j] : s7[j];
 }
 
 template <int R>
@@ -203,6 +209,33 @@ __device__ __forceinline__ void dft(double2 (&a)[R], bool inv) {
         a[4] = csub(b1, d1);
         a[2] = cadd(b2, d2);
         a[3] = csub(b2, d2);
+    } else if constexpr (R == 7 || R == 11 || R == 13) {
+        // odd prime: pairs (u, R-u) give y_t = a0 + sum_u c_tu (a_u + a_{R-u}) -/+ i sum_u s_tu
+        // (a_u - a_{R-u}) for (t, R-t): (R-1) real-coefficient FMAs per output instead of 2(R-1)
+        constexpr int H = (R - 1) / 2;
+        double2 sp[H], sm[H];
+#pragma unroll
+        for (int u = 1; u <= H; ++u) {
+            sp[u - 1] = cadd(a[u], a[R - u]);
+            sm[u - 1] = csub(a[u], a[R - u]);
+        }
+        double2 y0 = a[0];
+#pragma unroll
+        for (int u = 0; u < H; ++u) y0 = cadd(y0, sp[u]);
+#pragma unroll
+        for (int t = 1; t <= H; ++t) {
+            double2 re = a[0], im = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 1; u <= H; ++u) {
+                const double c = tw_cos(R, (t * u) % R), sn = tw_sin(R, (t * u) % R);
+                re = make_double2(fma(c, sp[u - 1].x, re.x), fma(c, sp[u - 1].y, re.y));
+                im = make_double2(fma(sn, sm[u - 1].x, im.x), fma(sn, sm[u - 1].y, im.y));
+            }
+            const double2 mi = mul_mi(im, inv);  // -i im (forward), +i im (inverse)
+            a[t] = cadd(re, mi);
+            a[R - t] = csub(re, mi);
+        }
+        a[0] = y0;
     } else if constexpr (R == 16) {
         dft_pq<4, 4>(a, inv);
     } else if constexpr (R == 9) {
@@ -515,6 +548,108 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
         if (x < a.out_len) a.out[mat + x] = A[c * stride + x1];
     }
+}
+
+// ---- TMA-pipelined column pass ------------------------------------------------------------
+// Persistent CTAs (one per SM) loop over column blocks of CW adjacent columns (CW * 16 bytes per
+// row).  A block arrives by TMA as nbox boxes of box_rows rows into one of two shared-memory
+// stages (SWIZZLE_128B / 64B: AddrSwz<CW>), so the load of block i+1 overlaps the FFTs of block i;
+// the result leaves by TMA store from the same stage.  Rows beyond M1 / columns beyond M2 are
+// zero-filled on load and clipped on store.  In-place passes of the direct path (not the first
+// pass from |+>, not Bluestein's padded / masked passes).
+struct ColTmaArgs {
+    ColArgs a;
+    int nblk_x, nmat;        // column blocks per matrix, matrices (three-level inner passes)
+    int box_rows, nbox;      // nbox boxes of box_rows rows cover M1 (box_rows % 16 == 0)
+    uint32_t stage_bytes;
+};
+
+__device__ __forceinline__ uint32_t smem_u32f(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// one call per column block: keeps the register allocation of the FFT stages independent of the
+// persistent loop around it (inlined, the loop made ptxas spill 16 KB per thread)
+template <int CW>
+__device__ __noinline__ void col_block_swz(unsigned char *stage, const ColArgs &a, int c0, int cwv, int my, int pslot,
+                                           double *red) {
+    col_block(AddrSwz<CW>{stage}, a, c0, cwv, my, pslot, red);
+}
+
+template <int CW>
+__global__ void __launch_bounds__(kFftThreads, 1)
+fft_col_tma_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ ColTmaArgs g) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    __shared__ double red[2 * (kFftThreads / 32)];
+    __shared__ __align__(8) uint64_t full[2];
+    load_roots();
+    const ColArgs &a = g.a;
+    const int total = g.nblk_x * g.nmat;
+    const int my_n = total > (int)blockIdx.x ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    if (threadIdx.x == 0) {
+        if (smem_u32f(smem_raw) & 1023) __trap();
+        for (int k = 0; k < 2; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32f(&full[k])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto coords = [&](int i, int &bx, int &my) {
+        const int b = (int)blockIdx.x + i * (int)gridDim.x;
+        bx = b % g.nblk_x;
+        my = b / g.nblk_x;
+    };
+    auto issue = [&](int i) {  // thread 0
+        int bx, my;
+        coords(i, bx, my);
+        const int s = i & 1;
+        const uint32_t bar = smem_u32f(&full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(g.stage_bytes) : "memory");
+        for (int k = 0; k < g.nbox; ++k) {
+            const uint32_t dst = smem_u32f(smem_raw + (size_t)s * g.stage_bytes + (size_t)k * g.box_rows * CW * 16);
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+                "l"(reinterpret_cast<uint64_t>(&tm)), "r"(bx * CW * 2), "r"(k * g.box_rows), "r"(my), "r"(bar)
+                : "memory");
+        }
+    };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2 && i < my_n; ++i) issue(i);
+    }
+    for (int i = 0; i < my_n; ++i) {
+        const int s = i & 1;
+        int bx, my;
+        coords(i, bx, my);
+        {
+            const uint32_t bar = smem_u32f(&full[s]);
+            uint32_t ok = 0;
+            const uint32_t par = (uint32_t)((i >> 1) & 1);
+            while (!ok)
+                asm volatile(
+                    "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                    : "=r"(ok)
+                    : "r"(bar), "r"(par)
+                    : "memory");
+        }
+        unsigned char *stage = smem_raw + (size_t)s * g.stage_bytes;
+        const int c0 = bx * CW;
+        col_block_swz<CW>(stage, a, c0, min(CW, a.M2 - c0), my, (int)blockIdx.x + i * (int)gridDim.x, red);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our smem writes -> TMA store
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < g.nbox; ++k) {
+                const uint32_t src = smem_u32f(stage + (size_t)k * g.box_rows * CW * 16);
+                asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                                 reinterpret_cast<uint64_t>(&tm)),
+                             "r"(bx * CW * 2), "r"(k * g.box_rows), "r"(my), "r"(src)
+                             : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            if (i + 2 < my_n) {
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // stage s read by the store
+                issue(i + 2);
+            }
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 struct RowArgs {
@@ -993,6 +1128,8 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
     if (st != QVA_OK) return fail(st, "");
     cudaFuncSetAttribute(fft_col_kernel<kFftThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
     cudaFuncSetAttribute(fft_col_kernel<kFftThreads / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
+    cudaFuncSetAttribute(fft_col_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    cudaFuncSetAttribute(fft_col_tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(fft_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSub * (int)sizeof(double2));
     cudaFuncSetAttribute(fft_whole_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * (int)sizeof(double2));
     if (fp->bluestein) {
@@ -1058,6 +1195,63 @@ void fft_permute_spectrum(const FftPlan *fp, const double *lambda, double *lambd
         for (uint64_t k2 = 0; k2 < M2; ++k2) lambda_perm[k1 * M2 + k2] = lambda[k1 + M1 * k2];
 }
 
+// TMA column pass over `arr` (nmat matrices of M1 rows x M2h columns at mat_stride elements) when
+// the blocks fit two stages; *launched = false leaves the pass to fft_col_kernel.  Expectation
+// partials go to slots [0, blocks) (returned in *slots).
+static qva_status launch_col_tma(FftPlan *fp, const ColArgs &c0, double2 *arr, int M1, int M2h, int nmat,
+                                 uint64_t mat_stride, cudaStream_t s, bool *launched, int *slots) {
+    *launched = false;
+    static int env = [] {
+        const char *e = getenv("QVA_FFT_TMA");
+        return e ? atoi(e) : 0;  // off: the persistent loop makes ptxas spill ~16 KB per thread
+    }();
+    if (!env) return QVA_OK;
+    const int nbox = (M1 + 255) / 256;
+    const int box_rows = ((M1 + nbox - 1) / nbox + 15) / 16 * 16;
+    const size_t budget = 200 * 1024;
+    int CW = 0;
+    if (2ull * nbox * box_rows * 128 <= budget) CW = 8;
+    else if (2ull * nbox * box_rows * 64 <= budget) CW = 4;
+    if (!CW || M2h < CW) return QVA_OK;
+    ColTmaArgs g;
+    memset(&g, 0, sizeof(g));
+    g.a = c0;
+    g.a.M1 = M1;
+    g.a.M2 = M2h;
+    g.a.cw = CW;
+    g.a.lcw = CW == 8 ? 3 : 2;
+    g.a.m1mag = div_magic((uint32_t)M1);
+    g.nblk_x = (M2h + CW - 1) / CW;
+    g.nmat = nmat;
+    g.box_rows = box_rows;
+    g.nbox = nbox;
+    g.stage_bytes = (uint32_t)(nbox * box_rows * CW * 16);
+    const int blocks = g.nblk_x * nmat;
+    if ((c0.ops & OP_EXPECT) && blocks > fp->n_partials) {
+        cudaFree(fp->partials);
+        fp->n_partials = blocks;
+        QVA_CUDA_TRY(cudaMalloc(&fp->partials, (size_t)blocks * 2 * sizeof(double)));
+    }
+    g.a.partials = fp->partials;
+    CUtensorMap tm;
+    const uint64_t dims[3] = {(uint64_t)M2h * 2, (uint64_t)M1, (uint64_t)nmat};
+    const uint64_t strides[2] = {(uint64_t)M2h * 16, (nmat > 1 ? mat_stride : (uint64_t)M1 * M2h) * 16};
+    const uint32_t box[3] = {(uint32_t)(CW * 2), (uint32_t)box_rows, 1};
+    QVA_TRY(encode_f64_tensor_map(&tm, arr, 3, dims, strides, box, CW * 16));
+    const int grid = std::min(blocks, 148);
+    const size_t smem = 2 * (size_t)g.stage_bytes;
+    if (CW == 8) fft_col_tma_kernel<8><<<grid, kFftThreads, smem, s>>>(tm, g);
+    else fft_col_tma_kernel<4><<<grid, kFftThreads, smem, s>>>(tm, g);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string("fft_col_tma_kernel: ") + cudaGetErrorString(e));
+        return QVA_ERR_CUDA;
+    }
+    *launched = true;
+    if (slots) *slots = blocks;
+    return QVA_OK;
+}
+
 // Three-level row transform of `nmat` consecutive top-level rows (matrices Mi1 x Mi2) starting at
 // global top-level row mat_off: inner column FFTs (+ w_{M2} twiddle), inner rows (forward FFT,
 // spectrum, inverse FFT, inverse w_{M2} twiddle), inner inverse column FFTs + the top-level
@@ -1093,6 +1287,12 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
         c.do_fwd = fwd;
         c.ops = ops;
         obs->begin(K_FFT_COL, 32.0 * (double)R * nmat);
+        bool tma = false;
+        QVA_TRY(launch_col_tma(fp, c, psi, fp->Mi1, fp->Mi2, nmat, R, s, &tma, nullptr));
+        if (tma) {
+            obs->end();
+            return QVA_OK;
+        }
         fft_col_kernel<kFftThreads><<<gc, kFftThreads, smem_c, s>>>(c);
         cudaError_t e = cudaGetLastError();
         obs->end();
@@ -1179,6 +1379,7 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
     c.lam = blu ? r.lambda_perm : nullptr;
     const size_t smem_c = col_smem(fp), smem_r = row_smem(fp);
     const int gc = col_grid(fp), gr = row_grid(fp);
+    int expect_slots = gc;  // partial slots written by the last column pass
     // column pass with 256-thread CTAs, two per SM (their barrier stalls overlap), when every
     // stage's butterflies of one column fit a 256-thread round and two column blocks fit smem
     static int half_env = [] {
@@ -1206,6 +1407,15 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
                              16.0 * (double)std::min<uint64_t>(out_len, Mi) +
                              ((ops & (OP_PHASE | OP_EXPECT)) ? q_bytes : 0.0) + ((ops & OP_SPEC) && c.lam ? 8.0 * N : 0.0);
         obs->begin(K_FFT_COL, bytes);
+        if (!blu && !init && in == out) {
+            bool tma = false;
+            QVA_TRY(launch_col_tma(fp, c, out, fp->M1, fp->M2, 1, 0, s, &tma, &expect_slots));
+            if (tma) {
+                obs->end();
+                return QVA_OK;
+            }
+        }
+        expect_slots = gc;
         if (col_half) fft_col_kernel<kFftThreads / 2><<<gc, kFftThreads / 2, smem_c, s>>>(c);
         else fft_col_kernel<kFftThreads><<<gc, kFftThreads, smem_c, s>>>(c);
         cudaError_t e = cudaGetLastError();
@@ -1249,8 +1459,8 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
         return QVA_OK;
     };
     auto reduce = [&]() -> qva_status {
-        obs->begin(K_REDUCE, 16.0 * fp->n_partials);
-        cudaError_t e = launch_reduce_partials(fp->partials, fp->n_partials, 1, r.red_out, s);
+        obs->begin(K_REDUCE, 16.0 * expect_slots);
+        cudaError_t e = launch_reduce_partials(fp->partials, expect_slots, 1, r.red_out, s);
         obs->end();
         if (e != cudaSuccess) {
             set_error(std::string("reduce: ") + cudaGetErrorString(e));
