@@ -281,23 +281,11 @@ __host__ __device__ constexpr int nb_of(int R) {
 }
 
 // Shared-memory addressing of `count` independent transforms (f = transform, i = position):
-//   AddrLin: f * stride + i (padded column-major / row-major buffers)
-//   AddrSwz<CW>: the layout a SWIZZLE_128B (CW = 8) / SWIZZLE_64B (CW = 4) TMA box of CW-column
-//     rows leaves in shared memory: row i is CW * 16 bytes, the 16-byte chunk of column f is
-//     f ^ ((i >> s) & (CW - 1)) (s = 0 / 1), so consecutive positions of one column fall in
-//     different bank groups
+// AddrLin: f * stride + i (padded column-major / row-major buffers)
 struct AddrLin {
     double2 *buf;
     int stride;
     __device__ __forceinline__ double2 *ptr(int f, int i) const { return buf + f * stride + i; }
-};
-template <int CW>
-struct AddrSwz {
-    unsigned char *base;
-    __device__ __forceinline__ double2 *ptr(int f, int i) const {
-        const int sw = CW == 8 ? (i & 7) : ((i >> 1) & 3);
-        return reinterpret_cast<double2 *>(base + (size_t)i * (CW * 16) + ((f ^ sw) << 4));
-    }
 };
 
 // One Stockham radix-R stage, in place, over `count` independent length-n transforms.  Rounds
@@ -548,108 +536,6 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
         if (x < a.out_len) a.out[mat + x] = A[c * stride + x1];
     }
-}
-
-// ---- TMA-pipelined column pass ------------------------------------------------------------
-// Persistent CTAs (one per SM) loop over column blocks of CW adjacent columns (CW * 16 bytes per
-// row).  A block arrives by TMA as nbox boxes of box_rows rows into one of two shared-memory
-// stages (SWIZZLE_128B / 64B: AddrSwz<CW>), so the load of block i+1 overlaps the FFTs of block i;
-// the result leaves by TMA store from the same stage.  Rows beyond M1 / columns beyond M2 are
-// zero-filled on load and clipped on store.  In-place passes of the direct path (not the first
-// pass from |+>, not Bluestein's padded / masked passes).
-struct ColTmaArgs {
-    ColArgs a;
-    int nblk_x, nmat;        // column blocks per matrix, matrices (three-level inner passes)
-    int box_rows, nbox;      // nbox boxes of box_rows rows cover M1 (box_rows % 16 == 0)
-    uint32_t stage_bytes;
-};
-
-__device__ __forceinline__ uint32_t smem_u32f(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-// one call per column block: keeps the register allocation of the FFT stages independent of the
-// persistent loop around it (inlined, the loop made ptxas spill 16 KB per thread)
-template <int CW>
-__device__ __noinline__ void col_block_swz(unsigned char *stage, const ColArgs &a, int c0, int cwv, int my, int pslot,
-                                           double *red) {
-    col_block(AddrSwz<CW>{stage}, a, c0, cwv, my, pslot, red);
-}
-
-template <int CW>
-__global__ void __launch_bounds__(kFftThreads, 1)
-fft_col_tma_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ ColTmaArgs g) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    __shared__ double red[2 * (kFftThreads / 32)];
-    __shared__ __align__(8) uint64_t full[2];
-    load_roots();
-    const ColArgs &a = g.a;
-    const int total = g.nblk_x * g.nmat;
-    const int my_n = total > (int)blockIdx.x ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-    if (threadIdx.x == 0) {
-        if (smem_u32f(smem_raw) & 1023) __trap();
-        for (int k = 0; k < 2; ++k)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32f(&full[k])) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    auto coords = [&](int i, int &bx, int &my) {
-        const int b = (int)blockIdx.x + i * (int)gridDim.x;
-        bx = b % g.nblk_x;
-        my = b / g.nblk_x;
-    };
-    auto issue = [&](int i) {  // thread 0
-        int bx, my;
-        coords(i, bx, my);
-        const int s = i & 1;
-        const uint32_t bar = smem_u32f(&full[s]);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(g.stage_bytes) : "memory");
-        for (int k = 0; k < g.nbox; ++k) {
-            const uint32_t dst = smem_u32f(smem_raw + (size_t)s * g.stage_bytes + (size_t)k * g.box_rows * CW * 16);
-            asm volatile(
-                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-                "l"(reinterpret_cast<uint64_t>(&tm)), "r"(bx * CW * 2), "r"(k * g.box_rows), "r"(my), "r"(bar)
-                : "memory");
-        }
-    };
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < 2 && i < my_n; ++i) issue(i);
-    }
-    for (int i = 0; i < my_n; ++i) {
-        const int s = i & 1;
-        int bx, my;
-        coords(i, bx, my);
-        {
-            const uint32_t bar = smem_u32f(&full[s]);
-            uint32_t ok = 0;
-            const uint32_t par = (uint32_t)((i >> 1) & 1);
-            while (!ok)
-                asm volatile(
-                    "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                    : "=r"(ok)
-                    : "r"(bar), "r"(par)
-                    : "memory");
-        }
-        unsigned char *stage = smem_raw + (size_t)s * g.stage_bytes;
-        const int c0 = bx * CW;
-        col_block_swz<CW>(stage, a, c0, min(CW, a.M2 - c0), my, (int)blockIdx.x + i * (int)gridDim.x, red);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our smem writes -> TMA store
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            for (int k = 0; k < g.nbox; ++k) {
-                const uint32_t src = smem_u32f(stage + (size_t)k * g.box_rows * CW * 16);
-                asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                                 reinterpret_cast<uint64_t>(&tm)),
-                             "r"(bx * CW * 2), "r"(k * g.box_rows), "r"(my), "r"(src)
-                             : "memory");
-            }
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            if (i + 2 < my_n) {
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // stage s read by the store
-                issue(i + 2);
-            }
-        }
-    }
-    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 struct RowArgs {
@@ -1128,8 +1014,6 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
     if (st != QVA_OK) return fail(st, "");
     cudaFuncSetAttribute(fft_col_kernel<kFftThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
     cudaFuncSetAttribute(fft_col_kernel<kFftThreads / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
-    cudaFuncSetAttribute(fft_col_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-    cudaFuncSetAttribute(fft_col_tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(fft_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSub * (int)sizeof(double2));
     cudaFuncSetAttribute(fft_whole_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * (int)sizeof(double2));
     if (fp->bluestein) {
@@ -1195,63 +1079,6 @@ void fft_permute_spectrum(const FftPlan *fp, const double *lambda, double *lambd
         for (uint64_t k2 = 0; k2 < M2; ++k2) lambda_perm[k1 * M2 + k2] = lambda[k1 + M1 * k2];
 }
 
-// TMA column pass over `arr` (nmat matrices of M1 rows x M2h columns at mat_stride elements) when
-// the blocks fit two stages; *launched = false leaves the pass to fft_col_kernel.  Expectation
-// partials go to slots [0, blocks) (returned in *slots).
-static qva_status launch_col_tma(FftPlan *fp, const ColArgs &c0, double2 *arr, int M1, int M2h, int nmat,
-                                 uint64_t mat_stride, cudaStream_t s, bool *launched, int *slots) {
-    *launched = false;
-    static int env = [] {
-        const char *e = getenv("QVA_FFT_TMA");
-        return e ? atoi(e) : 0;  // off: the persistent loop makes ptxas spill ~16 KB per thread
-    }();
-    if (!env) return QVA_OK;
-    const int nbox = (M1 + 255) / 256;
-    const int box_rows = ((M1 + nbox - 1) / nbox + 15) / 16 * 16;
-    const size_t budget = 200 * 1024;
-    int CW = 0;
-    if (2ull * nbox * box_rows * 128 <= budget) CW = 8;
-    else if (2ull * nbox * box_rows * 64 <= budget) CW = 4;
-    if (!CW || M2h < CW) return QVA_OK;
-    ColTmaArgs g;
-    memset(&g, 0, sizeof(g));
-    g.a = c0;
-    g.a.M1 = M1;
-    g.a.M2 = M2h;
-    g.a.cw = CW;
-    g.a.lcw = CW == 8 ? 3 : 2;
-    g.a.m1mag = div_magic((uint32_t)M1);
-    g.nblk_x = (M2h + CW - 1) / CW;
-    g.nmat = nmat;
-    g.box_rows = box_rows;
-    g.nbox = nbox;
-    g.stage_bytes = (uint32_t)(nbox * box_rows * CW * 16);
-    const int blocks = g.nblk_x * nmat;
-    if ((c0.ops & OP_EXPECT) && blocks > fp->n_partials) {
-        cudaFree(fp->partials);
-        fp->n_partials = blocks;
-        QVA_CUDA_TRY(cudaMalloc(&fp->partials, (size_t)blocks * 2 * sizeof(double)));
-    }
-    g.a.partials = fp->partials;
-    CUtensorMap tm;
-    const uint64_t dims[3] = {(uint64_t)M2h * 2, (uint64_t)M1, (uint64_t)nmat};
-    const uint64_t strides[2] = {(uint64_t)M2h * 16, (nmat > 1 ? mat_stride : (uint64_t)M1 * M2h) * 16};
-    const uint32_t box[3] = {(uint32_t)(CW * 2), (uint32_t)box_rows, 1};
-    QVA_TRY(encode_f64_tensor_map(&tm, arr, 3, dims, strides, box, CW * 16));
-    const int grid = std::min(blocks, 148);
-    const size_t smem = 2 * (size_t)g.stage_bytes;
-    if (CW == 8) fft_col_tma_kernel<8><<<grid, kFftThreads, smem, s>>>(tm, g);
-    else fft_col_tma_kernel<4><<<grid, kFftThreads, smem, s>>>(tm, g);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) {
-        set_error(std::string("fft_col_tma_kernel: ") + cudaGetErrorString(e));
-        return QVA_ERR_CUDA;
-    }
-    *launched = true;
-    if (slots) *slots = blocks;
-    return QVA_OK;
-}
-
 // Three-level row transform of `nmat` consecutive top-level rows (matrices Mi1 x Mi2) starting at
 // global top-level row mat_off: inner column FFTs (+ w_{M2} twiddle), inner rows (forward FFT,
 // spectrum, inverse FFT, inverse w_{M2} twiddle), inner inverse column FFTs + the top-level
@@ -1287,12 +1114,6 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
         c.do_fwd = fwd;
         c.ops = ops;
         obs->begin(K_FFT_COL, 32.0 * (double)R * nmat);
-        bool tma = false;
-        QVA_TRY(launch_col_tma(fp, c, psi, fp->Mi1, fp->Mi2, nmat, R, s, &tma, nullptr));
-        if (tma) {
-            obs->end();
-            return QVA_OK;
-        }
         fft_col_kernel<kFftThreads><<<gc, kFftThreads, smem_c, s>>>(c);
         cudaError_t e = cudaGetLastError();
         obs->end();
@@ -1407,14 +1228,6 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
                              16.0 * (double)std::min<uint64_t>(out_len, Mi) +
                              ((ops & (OP_PHASE | OP_EXPECT)) ? q_bytes : 0.0) + ((ops & OP_SPEC) && c.lam ? 8.0 * N : 0.0);
         obs->begin(K_FFT_COL, bytes);
-        if (!blu && !init && in == out) {
-            bool tma = false;
-            QVA_TRY(launch_col_tma(fp, c, out, fp->M1, fp->M2, 1, 0, s, &tma, &expect_slots));
-            if (tma) {
-                obs->end();
-                return QVA_OK;
-            }
-        }
         expect_slots = gc;
         if (col_half) fft_col_kernel<kFftThreads / 2><<<gc, kFftThreads / 2, smem_c, s>>>(c);
         else fft_col_kernel<kFftThreads><<<gc, kFftThreads, smem_c, s>>>(c);

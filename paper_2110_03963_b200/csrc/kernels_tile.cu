@@ -831,35 +831,6 @@ EncodeTiledFn encode_fn() {
 
 }  // namespace
 
-// generic tiled tensor map (fp64 elements) for the other TMA kernels (kernels_fft.cu)
-qva_status encode_f64_tensor_map(CUtensorMap *map, void *base, int rank, const uint64_t *dims,
-                                 const uint64_t *strides_bytes, const uint32_t *box, int swizzle_bytes) {
-    EncodeTiledFn enc = encode_fn();
-    if (!enc) {
-        set_error("cuTensorMapEncodeTiled entry point unavailable");
-        return QVA_ERR_CUDA;
-    }
-    cuuint64_t gd[5], gs[4];
-    cuuint32_t bx[5], es[5];
-    for (int d = 0; d < rank; ++d) {
-        gd[d] = dims[d];
-        bx[d] = box[d];
-        es[d] = 1;
-        if (d > 0) gs[d - 1] = strides_bytes[d - 1];
-    }
-    const CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                  : swizzle_bytes == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                         : CU_TENSOR_MAP_SWIZZLE_NONE;
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, base, gd, gs, bx, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-        return QVA_ERR_CUDA;
-    }
-    return QVA_OK;
-}
-
 int tile_pass_grid(uint64_t items) {
     static int sms = 0;
     if (!sms) {

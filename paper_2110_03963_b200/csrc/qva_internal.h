@@ -155,9 +155,6 @@ int tile_pass_grid(uint64_t items);
 int tile_consumer_warps();
 // builds the 5-D load map of psi_in seen through P.tile_bits and the store map of the same box
 // into psi_out through the bit permutation obit (nullptr: identity); fills P.dim_*, P.member_dim
-// generic tiled fp64 tensor map: dims[0] innermost (elements), strides of dims 1.. in bytes
-qva_status encode_f64_tensor_map(CUtensorMap *map, void *base, int rank, const uint64_t *dims,
-                                 const uint64_t *strides_bytes, const uint32_t *box, int swizzle_bytes);
 // number of TMA dims the maps of (tile_bits, obit) need (must be <= 5; batch 1)
 int tile_tma_dims(const int *tile_bits, int L, const int *obit);
 qva_status make_tile_tensor_maps(const double2 *psi_in, double2 *psi_out, int L, int batch, TilePassParams &P,
