@@ -475,6 +475,25 @@ struct qva_plan {
     // device buffers of dropped q copies / records, reused by size (a new q every step must not
     // pay cudaFree's device synchronisation and cudaMalloc's mapping cost)
     std::vector<std::pair<size_t, void *>> pool;
+    // CUDA graphs of the single-shard evolution: one per (p, buffers,
+    // q generation, half-angle pattern); capture staging and per-graph upload offsets
+    struct GraphEntry {
+        std::vector<int64_t> key;
+        cudaGraphExec_t exec;
+        int64_t kernels;                   // kernel launches per replay
+        unsigned char *stage;
+        size_t off[3];
+        int n_up;
+        double2 *psi_after, *alt_after;
+    };
+    std::vector<GraphEntry> graphs;
+    std::vector<int64_t> graph_warm_key;
+    unsigned char *graph_stage = nullptr;
+    size_t graph_pos = 0, graph_cap = 0;
+    std::vector<size_t> graph_offs;
+    int64_t q_gen_id = 0;                 // bumped whenever q copies / records are dropped
+    double2 *d_mult = nullptr;
+    size_t mult_cap = 0;
     // pinned host ring for small per-step uploads (angles, tables, generator records): a copy from
     // pageable memory would synchronise the stream before it starts
     unsigned char *ring = nullptr;
@@ -800,6 +819,18 @@ cudaError_t pool_get(qva_plan *P, void **p, size_t bytes) {
 constexpr size_t kRingBytes = 4 << 20;
 qva_status upload(qva_plan *P, void *dst, const void *src, size_t bytes) {
     if (!bytes) return QVA_OK;
+    if (P->graph_stage) {  // graph capture: the copy node reads this fixed pinned slot on every replay
+        const size_t off = (P->graph_pos + 15) & ~(size_t)15;
+        if (off + bytes > P->graph_cap) {
+            set_error("internal: graph staging overflow");
+            return QVA_ERR_INVALID_ARGUMENT;
+        }
+        memcpy(P->graph_stage + off, src, bytes);
+        QVA_CUDA_TRY(cudaMemcpyAsync(dst, P->graph_stage + off, bytes, cudaMemcpyHostToDevice, P->stream));
+        P->graph_offs.push_back(off);
+        P->graph_pos = off + bytes;
+        return QVA_OK;
+    }
     if (!P->ring) {
         if (cudaMallocHost((void **)&P->ring, kRingBytes) != cudaSuccess) {
             cudaGetLastError();
@@ -825,6 +856,7 @@ qva_status upload(qva_plan *P, void *dst, const void *src, size_t bytes) {
 }
 
 void drop_qt(qva_plan *P) {
+    ++P->q_gen_id;
     for (auto &e : P->qt_cache) pool_put(P, e.buf, e.bytes);
     P->qt_cache.clear();
     for (auto &e : P->gen_cache) {
@@ -951,6 +983,13 @@ bool use_qgen(const qva_plan *P) {
         return e ? atoi(e) : 1;
     }();
     return env != 0 && P->q_graph && P->mixer == QVA_MIXER_X;
+}
+
+// q path of a tile-pass sequence: generated integer / fp64 records, or 0 (stored q)
+int qgen_mode(const qva_plan *P, int batch) {
+    const bool gen_int = P->g_unit && P->g_m <= kGenIntMaxEdges;
+    const bool f64_ok = batch <= kGfMembersHost || P->L >= kGenF64MinQubits || P->d.reserved[1] != 0;
+    return use_qgen(P) && (gen_int || f64_ok) ? (gen_int ? kQGenInt : kQGenF64) : 0;
 }
 
 // logical qubit of every physical bit of the arrays a pass reads (n_phys bits) and the logical
@@ -1142,38 +1181,23 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
 
 // ---- tile-pass execution of a pass list -----------------------------------------------------
 // thetas: [batch][2p]; psi_base/stride: states of the batch members
-static int g_hostprof = [] {
-    const char *e = getenv("QVA_HOSTPROF");
-    return e ? atoi(e) : 0;
-}();
-static double host_ms() {
-    timespec ts;
-    clock_gettime(CLOCK_MONOTONIC, &ts);
-    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
-}
-
-qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const double *thetas, int p, int batch,
-                      double2 *psi_base, uint64_t stride, int init_mode, double *expect_out /*[batch][2] host*/) {
-    const double hp0 = g_hostprof ? host_ms() : 0.0;
-    double hp_first = -1.0;
-    int n_tile_passes = 0;
-    for (auto &pp : passes) n_tile_passes += !pp.exchange;
-    // graph-defined q: generated inside the passes (integer table path for unit weights)
-    // (weighted graphs: the factorised phase needs a per-member G table, held in smem for batches
-    // <= kGfMembers (cfg2: 1.17 vs 1.63 ms stored); larger batches pay one sincos per amplitude
-    // plus the record arithmetic, which only pays where HBM bounds the pass)
-    const bool gen_int = P->g_unit && P->g_m <= kGenIntMaxEdges;
-    const bool f64_ok = batch <= kGfMembersHost || P->L >= kGenF64MinQubits || P->d.reserved[1] != 0;
-    const int gen = use_qgen(P) && (gen_int || f64_ok) ? (gen_int ? kQGenInt : kQGenF64) : 0;
-    if (!gen && P->q_set && !P->q_classified) {
-        QVA_TRY(classify_q(P));
-        P->q_classified = true;
-    }
-    const bool int_table = gen == kQGenInt || (!gen && P->q_mode != 0);
-    const int tab_qmin = gen == kQGenInt ? -P->g_m : P->qmin;
-    QVA_TRY(ensure_angles(P, (size_t)n_tile_passes * batch));
-    std::vector<PassAngles> ang((size_t)n_tile_passes * batch);
-    std::vector<char> half1(n_tile_passes, 0), half2(n_tile_passes, 0);
+// Host data of one pass sequence for one theta set: per-pass angle records, half-angle flags,
+// phase-table rows (gammas + deferred scalar factors) and which passes apply the carried scale.
+// The structure (flags) decides the step programs; the values are what a replayed graph uploads.
+struct PassHostData {
+    std::vector<PassAngles> ang;
+    std::vector<char> half1, half2, apply_scale;
+    std::vector<double> gam;
+    std::vector<double2> tab_mult;
+    std::vector<int> tab_index;
+};
+static void pass_host_data(const std::vector<PassPlan> &passes, const double *thetas, int p, int batch,
+                           bool int_table, int n_tile_passes, PassHostData &H) {
+    std::vector<PassAngles> &ang = H.ang;
+    ang.assign((size_t)n_tile_passes * batch, PassAngles{});
+    std::vector<char> &half1 = H.half1, &half2 = H.half2;
+    half1.assign(n_tile_passes, 0);
+    half2.assign(n_tile_passes, 0);
     {
         int j = 0;
         for (const PassPlan &pp : passes) {
@@ -1186,8 +1210,10 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             ++j;
         }
     }
-    std::vector<double> gam;  // [phase pass][batch]
-    std::vector<int> tab_index(passes.size(), -1);
+    std::vector<double> &gam = H.gam;  // [phase pass][batch]
+    gam.clear();
+    std::vector<int> &tab_index = H.tab_index;
+    tab_index.assign(passes.size(), -1);
     {
         int j = 0, np = 0;
         for (size_t pi = 0; pi < passes.size(); ++pi) {
@@ -1223,8 +1249,10 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
     // The dropped rotation factors are scalars per member, so they commute with every pass: carry
     // them forward and fold them into the next integer phase table (free) or apply them at the
     // next fp64 phase / the last pass, instead of a complex multiply per amplitude in every pass.
-    std::vector<char> apply_scale(n_tile_passes, 0);
-    std::vector<double2> tab_mult;  // [phase table row][batch]
+    std::vector<char> &apply_scale = H.apply_scale;
+    apply_scale.assign(n_tile_passes, 0);
+    std::vector<double2> &tab_mult = H.tab_mult;  // [phase table row][batch]
+    tab_mult.clear();
     {
         std::vector<double2> carry(batch, make_double2(1.0, 0.0));
         int j = 0;
@@ -1246,6 +1274,43 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             ++j;
         }
     }
+}
+
+static int g_hostprof = [] {
+    const char *e = getenv("QVA_HOSTPROF");
+    return e ? atoi(e) : 0;
+}();
+static double host_ms() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+}
+
+qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const double *thetas, int p, int batch,
+                      double2 *psi_base, uint64_t stride, int init_mode, double *expect_out /*[batch][2] host*/) {
+    const double hp0 = g_hostprof ? host_ms() : 0.0;
+    double hp_first = -1.0;
+    int n_tile_passes = 0;
+    for (auto &pp : passes) n_tile_passes += !pp.exchange;
+    // graph-defined q: generated inside the passes (integer table path for unit weights)
+    // (weighted graphs: the factorised phase needs a per-member G table, held in smem for batches
+    // <= kGfMembers (cfg2: 1.17 vs 1.63 ms stored); larger batches pay one sincos per amplitude
+    // plus the record arithmetic, which only pays where HBM bounds the pass)
+    const int gen = qgen_mode(P, batch);
+    if (!gen && P->q_set && !P->q_classified) {
+        QVA_TRY(classify_q(P));
+        P->q_classified = true;
+    }
+    const bool int_table = gen == kQGenInt || (!gen && P->q_mode != 0);
+    const int tab_qmin = gen == kQGenInt ? -P->g_m : P->qmin;
+    QVA_TRY(ensure_angles(P, (size_t)n_tile_passes * batch));
+    PassHostData H;
+    pass_host_data(passes, thetas, p, batch, int_table, n_tile_passes, H);
+    const std::vector<PassAngles> &ang = H.ang;
+    const std::vector<char> &half1 = H.half1, &half2 = H.half2, &apply_scale = H.apply_scale;
+    const std::vector<double> &gam = H.gam;
+    const std::vector<double2> &tab_mult = H.tab_mult;
+    const std::vector<int> &tab_index = H.tab_index;
     QVA_TRY(upload(P, P->d_angles, ang.data(), ang.size() * sizeof(PassAngles)));
     const int ntab = gen == kQGenInt ? P->g_m + 1 : (int_table ? (P->qmax - P->qmin + 1) : 0);
     if (!gam.empty()) {
@@ -1262,14 +1327,17 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             P->tab_cap = gam.size() * ntab;
         }
         QVA_TRY(upload(P, P->d_gam, gam.data(), gam.size() * sizeof(double)));
-        double2 *d_mult = nullptr;
-        QVA_CUDA_TRY(cudaMallocAsync((void **)&d_mult, gam.size() * sizeof(double2), P->stream));
-        QVA_TRY(upload(P, d_mult, tab_mult.data(), gam.size() * sizeof(double2)));
+        if (P->mult_cap < gam.size()) {
+            cudaFree(P->d_mult);
+            P->d_mult = nullptr;
+            QVA_CUDA_TRY(cudaMalloc(&P->d_mult, gam.size() * sizeof(double2)));
+            P->mult_cap = gam.size();
+        }
+        QVA_TRY(upload(P, P->d_mult, tab_mult.data(), gam.size() * sizeof(double2)));
         {
             ProfScope ps(P, K_OTHER, 16.0 * gam.size() * ntab);
-            QVA_CUDA_TRY(launch_phase_table(P->d_tab, P->d_gam, d_mult, (int)gam.size(), tab_qmin, ntab, P->stream));
+            QVA_CUDA_TRY(launch_phase_table(P->d_tab, P->d_gam, P->d_mult, (int)gam.size(), tab_qmin, ntab, P->stream));
         }
-        QVA_CUDA_TRY(cudaFreeAsync(d_mult, P->stream));
     }
     uint64_t n_tiles = P->arr_n >> kTileBits;
     bool any_expect = false;
@@ -1453,6 +1521,99 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
     if (g_hostprof)
         fprintf(stderr, "[qva host] run_passes: %.3f ms to the first launch, %.3f ms total enqueue\n", hp_first,
                 host_ms() - hp0);
+    return QVA_OK;
+}
+
+// ---- graph replay of the single-shard evolution ------------------
+// The launch sequence of an evolution depends only on (p, schedule, buffers, q copies /
+// records, half-angle pattern); the theta-dependent data are three uploads (angle records,
+// phase-table gammas and scalar factors).  The first call with a new key runs normally (warming
+// every cache); the second captures run_passes into a CUDA graph whose copy nodes read a fixed
+// pinned staging block; later calls refill that block and launch the graph: one launch per
+// evaluation instead of ~10 launches and their host-side preparation.
+qva_status run_passes_graph(qva_plan *P, const std::vector<PassPlan> &passes, const double *theta, int p,
+                            int init_mode) {
+    static int env = [] {
+        const char *e = getenv("QVA_GRAPH");
+        return e ? atoi(e) : 1;
+    }();
+    if (!env || P->prof || g_trace || g_hostprof)
+        return run_passes(P, passes, theta, p, 1, P->psi, 0, init_mode, nullptr);
+    int n_tile_passes = 0;
+    for (auto &pp : passes) n_tile_passes += !pp.exchange;
+    const int gen = qgen_mode(P, 1);
+    const bool int_table = gen == kQGenInt || (!gen && P->q_mode != 0);
+    PassHostData H;
+    pass_host_data(passes, theta, p, 1, int_table, n_tile_passes, H);
+    std::vector<int64_t> key = {p, (int64_t)(uintptr_t)P->psi, (int64_t)(uintptr_t)P->psi_alt, init_mode,
+                                P->q_gen_id, gen, (int64_t)P->q_classified, (int64_t)P->q_mode,
+                                (int64_t)(uintptr_t)&passes};
+    for (int j = 0; j < n_tile_passes; ++j) key.push_back(H.half1[j] * 2 + H.half2[j]);
+    const void *srcs[3] = {H.ang.data(), H.gam.data(), H.tab_mult.data()};
+    const size_t sizes[3] = {H.ang.size() * sizeof(PassAngles), H.gam.size() * sizeof(double),
+                             H.gam.size() * sizeof(double2)};
+    for (auto &g : P->graphs)
+        if (g.key == key) {
+            for (int k = 0; k < g.n_up; ++k) memcpy(g.stage + g.off[k], srcs[k], sizes[k]);
+            QVA_CUDA_TRY(cudaGraphLaunch(g.exec, P->stream));
+            P->launches += g.kernels;
+            P->psi = g.psi_after;
+            P->psi_alt = g.alt_after;
+            return QVA_OK;
+        }
+    if (key != P->graph_warm_key) {  // first call with this key: run normally, warming the caches
+        P->graph_warm_key = key;
+        return run_passes(P, passes, theta, p, 1, P->psi, 0, init_mode, nullptr);
+    }
+    // second call: capture
+    qva_plan::GraphEntry g;
+    g.key = key;
+    const size_t cap = sizes[0] + sizes[1] + sizes[2] + 64;
+    QVA_CUDA_TRY(cudaMallocHost((void **)&g.stage, cap));
+    double2 *psi0 = P->psi, *alt0 = P->psi_alt;
+    P->graph_stage = g.stage;
+    P->graph_pos = 0;
+    P->graph_cap = cap;
+    P->graph_offs.clear();
+    cudaGraph_t graph = nullptr;
+    QVA_CUDA_TRY(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
+    const int64_t launches0 = P->launches;
+    qva_status st = run_passes(P, passes, theta, p, 1, P->psi, 0, init_mode, nullptr);
+    cudaError_t ce = cudaStreamEndCapture(P->stream, &graph);
+    P->graph_stage = nullptr;
+    g.kernels = P->launches - launches0;
+    P->launches = launches0;
+    g.psi_after = P->psi;
+    g.alt_after = P->psi_alt;
+    P->psi = psi0;
+    P->psi_alt = alt0;
+    if (st != QVA_OK || ce != cudaSuccess || P->graph_offs.size() > 3) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaFreeHost(g.stage);
+        cudaGetLastError();
+        P->graph_warm_key.clear();
+        if (st != QVA_OK) return st;
+        return run_passes(P, passes, theta, p, 1, P->psi, 0, init_mode, nullptr);
+    }
+    g.n_up = (int)P->graph_offs.size();
+    for (int k = 0; k < g.n_up; ++k) g.off[k] = P->graph_offs[k];
+    ce = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) {
+        cudaFreeHost(g.stage);
+        set_error(std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ce));
+        return QVA_ERR_CUDA;
+    }
+    if (P->graphs.size() >= 8) {
+        cudaGraphExecDestroy(P->graphs.front().exec);
+        cudaFreeHost(P->graphs.front().stage);
+        P->graphs.erase(P->graphs.begin());
+    }
+    P->graphs.push_back(g);
+    QVA_CUDA_TRY(cudaGraphLaunch(g.exec, P->stream));
+    P->launches += g.kernels;
+    P->psi = g.psi_after;
+    P->psi_alt = g.alt_after;
     return QVA_OK;
 }
 
@@ -1820,6 +1981,11 @@ qva_status qva_plan_destroy(qva_plan *P) {
     cudaFree(P->d_tab);
     cudaFree(P->d_gam);
     drop_qt(P);
+    for (auto &g : P->graphs) {
+        cudaGraphExecDestroy(g.exec);
+        cudaFreeHost(g.stage);
+    }
+    cudaFree(P->d_mult);
     for (auto &e : P->pool) cudaFree(e.second);
     if (P->ring) cudaFreeHost(P->ring);
     cudaFree(P->partials);
@@ -2326,7 +2492,7 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
                 }
                 it = P->perm_sched.emplace(p, std::make_pair(std::move(passes), std::move(fin))).first;
             }
-            QVA_TRY(run_passes(P, it->second.first, theta, p, 1, P->psi, 0, P->has_psi0 ? 2 : 1, nullptr));
+            QVA_TRY(run_passes_graph(P, it->second.first, theta, p, P->has_psi0 ? 2 : 1));
             P->perm = it->second.second;
             *have_red = true;
             return QVA_OK;

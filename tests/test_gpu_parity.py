@@ -136,6 +136,35 @@ def test_generated_qualities_batch_and_shards(Q):
         _amp_close(P.get_state(), O.evolve_x(n, q, thetas[0]))
 
 
+def test_repeated_evolutions_graph_replay(Q):
+    """Repeated evaluations of one plan (the optimiser's pattern): from the third call with the same
+    launch structure the evolution replays a captured CUDA graph with freshly uploaded angles; every
+    call must match the oracle, including after a q change, a get_state (layout back to natural)
+    and an angle with |cos beta| < 2^-10 (half-angle steps: another structure)."""
+    n, p = 22, 3
+    rng = np.random.default_rng(4242)
+    u, v = random_regular_graph(n, 3, rng)
+    q = O.maxcut_q(n, u, v)
+    with Q.Plan(1 << n, "x", n_qubits=n) as P:
+        P.set_qualities_maxcut(u, v)
+        for i in range(6):
+            th = rng.uniform(0, math.pi, 2 * p)
+            if i == 4:
+                th[3] = math.pi / 2  # beta_2 = pi/2: half-angle steps
+            P.evolve(th)
+            ref = O.evolve_x(n, q, th)
+            _f_close(P.expectation(), O.expectation(ref, q))
+            if i in (2, 5):
+                _amp_close(P.get_state(), ref)
+        w = rng.uniform(0, 1, len(u))
+        q2 = O.maxcut_q(n, u, v, w)
+        P.set_qualities_maxcut(u, v, w)
+        for i in range(4):
+            th = rng.uniform(0, math.pi, 2 * p)
+            P.evolve(th)
+            _f_close(P.expectation(), O.expectation(O.evolve_x(n, q2, th), q2))
+
+
 def test_tile_path_p0_and_norm(Q):
     n = 14
     q = np.linspace(-1, 1, 1 << n)
