@@ -494,6 +494,8 @@ struct qva_plan {
     int64_t q_gen_id = 0;                 // bumped whenever q copies / records are dropped
     double2 *d_mult = nullptr;
     size_t mult_cap = 0;
+    void *d_edges = nullptr;              // on-demand q generation: edge list
+    size_t edge_cap = 0;
     // pinned host ring for small per-step uploads (angles, tables, generator records): a copy from
     // pageable memory would synchronise the stream before it starts
     unsigned char *ring = nullptr;
@@ -867,29 +869,32 @@ void drop_qt(qva_plan *P) {
     P->gen_cache.clear();
 }
 
-// fp64 q of a graph-defined plan, generated on demand (maxcut_q_kernel, 8 B per amplitude)
+// fp64 q of a graph-defined plan, generated on demand (maxcut_q_kernel, 8 B per amplitude); the
+// edge list goes through the pinned upload ring into a persistent buffer, and the stream orders
+// the kernel before every consumer (no host synchronisation)
 qva_status ensure_q_dev(qva_plan *P) {
     if (!P->q_graph || P->q_dev_valid) return QVA_OK;
     const int m = P->g_m;
-    int32_t *du = nullptr, *dv = nullptr;
-    double *dw = nullptr;
-    const size_t me = m > 0 ? m : 1;
-    QVA_CUDA_TRY(cudaMallocAsync((void **)&du, me * sizeof(int32_t), P->stream));
-    QVA_CUDA_TRY(cudaMallocAsync((void **)&dv, me * sizeof(int32_t), P->stream));
-    if (m) QVA_CUDA_TRY(cudaMemcpyAsync(du, P->g_u.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice, P->stream));
-    if (m) QVA_CUDA_TRY(cudaMemcpyAsync(dv, P->g_v.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice, P->stream));
-    if (!P->g_unit) {
-        QVA_CUDA_TRY(cudaMallocAsync((void **)&dw, me * sizeof(double), P->stream));
-        QVA_CUDA_TRY(cudaMemcpyAsync(dw, P->g_w.data(), m * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+    const size_t need = (size_t)std::max(m, 1) * (2 * sizeof(int32_t) + sizeof(double));
+    if (P->edge_cap < need) {
+        cudaFree(P->d_edges);
+        P->d_edges = nullptr;
+        QVA_CUDA_TRY(cudaMalloc(&P->d_edges, need));
+        P->edge_cap = need;
+    }
+    int32_t *du = reinterpret_cast<int32_t *>(P->d_edges);
+    int32_t *dv = du + std::max(m, 1);
+    double *dw = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(P->d_edges) +
+                                            (size_t)std::max(m, 1) * 2 * sizeof(int32_t));
+    if (m) {
+        QVA_TRY(upload(P, du, P->g_u.data(), m * sizeof(int32_t)));
+        QVA_TRY(upload(P, dv, P->g_v.data(), m * sizeof(int32_t)));
+        if (!P->g_unit) QVA_TRY(upload(P, dw, P->g_w.data(), m * sizeof(double)));
     }
     {
         ProfScope ps(P, K_OTHER, 8.0 * P->arr_n);
-        QVA_CUDA_TRY(launch_maxcut_q(P->q, P->arr_n, P->offset, m, du, dv, dw, P->stream));
+        QVA_CUDA_TRY(launch_maxcut_q(P->q, P->arr_n, P->offset, m, du, dv, P->g_unit ? nullptr : dw, P->stream));
     }
-    cudaFreeAsync(du, P->stream);
-    cudaFreeAsync(dv, P->stream);
-    if (dw) cudaFreeAsync(dw, P->stream);
-    QVA_TRY(sync(P));
     P->q_dev_valid = true;
     return QVA_OK;
 }
@@ -1986,6 +1991,7 @@ qva_status qva_plan_destroy(qva_plan *P) {
         cudaFreeHost(g.stage);
     }
     cudaFree(P->d_mult);
+    cudaFree(P->d_edges);
     for (auto &e : P->pool) cudaFree(e.second);
     if (P->ring) cudaFreeHost(P->ring);
     cudaFree(P->partials);
