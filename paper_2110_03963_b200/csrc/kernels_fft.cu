@@ -356,6 +356,72 @@ __device__ __forceinline__ void run_fft_ad(const Ad &ad, const SubFft &sf, const
 __device__ __forceinline__ void run_fft(double2 *buf, const SubFft &sf, const double2 *tw, int count, int stride, bool inv) {
     run_fft_ad(AddrLin{buf, stride}, sf, tw, count, inv);
 }
+// ---- compile-time codelets ----------------------------------------------------------------
+// The same Stockham stages with the sub-FFT length, the radix list and hence every stage's m, nb
+// and twiddle offset known at compile time: the butterfly index division, the k = j mod m and
+// the shared-memory offsets fold into constants (the generic engine spends about half of its
+// instructions on that integer work).  The radix order must equal factor_radices'.
+template <int R, int N, int M, typename Ad>
+__device__ __forceinline__ void stage_ct(const Ad &ad, int count, const double2 *__restrict__ tw, bool inv) {
+    constexpr int NB = nb_of(R);
+    constexpr int nb = N / R;
+    const int per_round = max(1, (int)(NB * blockDim.x) / nb);
+    for (int f0 = 0; f0 < count; f0 += per_round) {
+        const int total = nb * min(per_round, count - f0);
+        double2 a[NB][R];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const int J = threadIdx.x + b * blockDim.x;
+            if (J < total) {
+                const int f = f0 + J / nb, j = J % nb;
+#pragma unroll
+                for (int t = 0; t < R; ++t) a[b][t] = *ad.ptr(f, j + t * nb);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const int J = threadIdx.x + b * blockDim.x;
+            if (J < total) {
+                const int f = f0 + J / nb, j = J % nb;
+                const int k = j % M;
+                if (M > 1) {
+#pragma unroll
+                    for (int t = 1; t < R; ++t) a[b][t] = cmul(a[b][t], conj_if(__ldg(tw + t * k), inv));
+                }
+                dft<R>(a[b], inv);
+                const int o = (j - k) * R + k;
+#pragma unroll
+                for (int t = 0; t < R; ++t) *ad.ptr(f, o + t * M) = a[b][t];
+            }
+        }
+        __syncthreads();
+    }
+}
+template <int N, int M, int OFF, typename Ad>
+__device__ __forceinline__ void stages_ct(const Ad &, const double2 *, int, bool) {}
+template <int N, int M, int OFF, typename Ad, int R, int... Rest>
+__device__ __forceinline__ void stages_ct(const Ad &ad, const double2 *tw, int count, bool inv) {
+    stage_ct<R, N, M>(ad, count, tw + OFF, inv);
+    stages_ct<N, M * R, OFF + M * R, Ad, Rest...>(ad, tw, count, inv);
+}
+template <int N, int... Rs>
+struct Codelet {
+    static constexpr int n = N;
+    template <typename Ad>
+    __device__ __forceinline__ static void run(const Ad &ad, const SubFft &sf, const double2 *tw, int count, bool inv) {
+        stages_ct<N, 1, 0, Ad, Rs...>(ad, tw + sf.twoff[0], count, inv);  // stage tables follow make_sub's
+    }
+};
+// runtime-planned transforms
+struct GenericFft {
+    static constexpr int n = 0;
+    template <typename Ad>
+    __device__ __forceinline__ static void run(const Ad &ad, const SubFft &sf, const double2 *tw, int count, bool inv) {
+        run_fft_ad(ad, sf, tw, count, inv);
+    }
+};
+
 // a call boundary around a whole sub-FFT (used by the small whole-evolution kernel, whose
 // layer loop would otherwise spill ~11 KB per thread)
 __device__ __noinline__ void run_fft_call(double2 *buf, const SubFft &sf, const double2 *tw, int count, int stride,
@@ -447,12 +513,12 @@ struct ColArgs {
 // The arithmetic of one column block (columns c0 .. c0+cwv of matrix mat_y), in shared memory
 // through the addressing policy: [inverse column FFTs] -> elementwise ops at the natural index ->
 // [forward column FFTs + twiddle w_M^{x2 k1}]; expectation partials to slot pslot.
-template <typename Ad>
+template <typename F, typename Ad>
 __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0, int cwv, int mat_y, int pslot,
                                           double *red) {
     const int M1 = a.M1, M2 = a.M2;
     const int tot = M1 * cwv;
-    if (a.do_inv) run_fft_ad(ad, a.sf, a.tw, cwv, true);
+    if (a.do_inv) F::run(ad, a.sf, a.tw, cwv, true);
     const int ops = a.ops;
     if (ops) {
         double acc = 0.0, nrm = 0.0;
@@ -495,7 +561,7 @@ __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0
         __syncthreads();
     }
     if (a.do_fwd) {
-        run_fft_ad(ad, a.sf, a.tw, cwv, false);
+        F::run(ad, a.sf, a.tw, cwv, false);
         for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
             const int c = (int)divu(idx, a.m1mag), k1 = idx - c * M1;
             const uint64_t r = (uint64_t)(a.col_off + c0 + c) * (uint64_t)k1;  // < M: no reduction needed
@@ -506,7 +572,7 @@ __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0
     }
 }
 
-template <int NT>
+template <int NT, typename F = GenericFft>
 __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const ColArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     load_roots();
@@ -529,7 +595,7 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         A[c * stride + x1] = v;
     }
     __syncthreads();
-    col_block(AddrLin{A, stride}, a, c0, cwv, blockIdx.y, blockIdx.x, red);
+    col_block<F>(AddrLin{A, stride}, a, c0, cwv, blockIdx.y, blockIdx.x, red);
     for (int idx = threadIdx.x; idx < totw; idx += blockDim.x) {
         const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
         if (c >= cwv) continue;
@@ -557,6 +623,7 @@ struct RowArgs {
     SubFft sf;
 };
 
+template <typename F = GenericFft>
 __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     load_roots();
@@ -567,7 +634,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
     const int tot = a.rb * M2;
     for (int i = threadIdx.x; i < tot; i += blockDim.x) A[i] = rows[i];
     __syncthreads();
-    run_fft(A, a.sf, a.tw, a.rb, M2, false);
+    F::run(AddrLin{A, M2}, a.sf, a.tw, a.rb, false);
     if (a.fwd_only) {
         for (int i = threadIdx.x; i < tot; i += blockDim.x) rows[i] = A[i];
         return;
@@ -590,7 +657,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
         A[i] = cmul(A[i], e);
     }
     __syncthreads();
-    run_fft(A, a.sf, a.tw, a.rb, M2, true);
+    F::run(AddrLin{A, M2}, a.sf, a.tw, a.rb, true);
     for (int i = threadIdx.x; i < tot; i += blockDim.x) {
         const int r = (int)divu(i, a.m2mag), x2 = i - r * M2;
         const int kr = a.row_off + k1_0 + r;
@@ -659,6 +726,45 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_whole_kernel(const WholeAr
             a.red_out[1] = nrm;
         }
     }
+}
+
+// Codelets compiled in (sizes of the cfg3 / 12! plans and powers of two); the planner prefers
+// splits whose sub-FFT lengths have one (kernels_fft.cu "compile-time codelets")
+using ColKernelFn = void (*)(ColArgs);
+using RowKernelFn = void (*)(RowArgs);
+struct CodeletEntry {
+    int n;
+    ColKernelFn col, col_half;
+    RowKernelFn row;
+};
+const CodeletEntry kCodelets[] = {
+    {768, fft_col_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_col_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>, fft_row_kernel<Codelet<768, 16, 16, 3>>},
+    {770, fft_col_kernel<kFftThreads, Codelet<770, 2, 5, 7, 11>>, fft_col_kernel<kFftThreads / 2, Codelet<770, 2, 5, 7, 11>>, fft_row_kernel<Codelet<770, 2, 5, 7, 11>>},
+    {810, fft_col_kernel<kFftThreads, Codelet<810, 2, 9, 9, 5>>, fft_col_kernel<kFftThreads / 2, Codelet<810, 2, 9, 9, 5>>, fft_row_kernel<Codelet<810, 2, 9, 9, 5>>},
+    {840, fft_col_kernel<kFftThreads, Codelet<840, 8, 3, 5, 7>>, fft_col_kernel<kFftThreads / 2, Codelet<840, 8, 3, 5, 7>>, fft_row_kernel<Codelet<840, 8, 3, 5, 7>>},
+    {1024, fft_col_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_col_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>, fft_row_kernel<Codelet<1024, 16, 16, 4>>},
+    {2048, fft_col_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_col_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>, fft_row_kernel<Codelet<2048, 16, 16, 8>>},
+    {4096, fft_col_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_col_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>, fft_row_kernel<Codelet<4096, 16, 16, 16>>},
+    {4320, fft_col_kernel<kFftThreads, Codelet<4320, 16, 2, 9, 3, 5>>, fft_col_kernel<kFftThreads / 2, Codelet<4320, 16, 2, 9, 3, 5>>, fft_row_kernel<Codelet<4320, 16, 2, 9, 3, 5>>},
+};
+const CodeletEntry *codelet_for(int n) {
+    static int env = [] {
+        const char *e = getenv("QVA_FFT_CODELETS");
+        return e ? atoi(e) : 1;
+    }();
+    if (!env) return nullptr;
+    for (const auto &c : kCodelets)
+        if (c.n == n) return &c;
+    return nullptr;
+}
+ColKernelFn col_kernel_for(int n, bool half) {
+    const CodeletEntry *c = codelet_for(n);
+    if (c) return half ? c->col_half : c->col;
+    return half ? fft_col_kernel<kFftThreads / 2> : fft_col_kernel<kFftThreads>;
+}
+RowKernelFn row_kernel_for(int n) {
+    const CodeletEntry *c = codelet_for(n);
+    return c ? c->row : fft_row_kernel<>;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1014,7 +1120,12 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
     if (st != QVA_OK) return fail(st, "");
     cudaFuncSetAttribute(fft_col_kernel<kFftThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
     cudaFuncSetAttribute(fft_col_kernel<kFftThreads / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
-    cudaFuncSetAttribute(fft_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSub * (int)sizeof(double2));
+    cudaFuncSetAttribute(fft_row_kernel<>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSub * (int)sizeof(double2));
+    for (const auto &cl : kCodelets) {
+        cudaFuncSetAttribute(cl.col, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
+        cudaFuncSetAttribute(cl.col_half, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
+        cudaFuncSetAttribute(cl.row, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSub * (int)sizeof(double2));
+    }
     cudaFuncSetAttribute(fft_whole_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * (int)sizeof(double2));
     if (fp->bluestein) {
         // kernel b_m = conj(c_m) for |m| < N on the length-M circle (b is even), then B = F_M b
@@ -1038,10 +1149,10 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
         c.out_len = M;
         c.N = M;
         c.do_fwd = 1;
-        fft_col_kernel<kFftThreads><<<col_grid(fp), kFftThreads, col_smem(fp)>>>(c);
+        col_kernel_for(fp->M1, false)<<<col_grid(fp), kFftThreads, col_smem(fp)>>>(c);
         RowArgs w = row_args(fp, fp->bhat);
         w.fwd_only = 1;
-        fft_row_kernel<<<row_grid(fp), kFftThreads, row_smem(fp)>>>(w);
+        row_kernel_for(fp->M2)<<<row_grid(fp), kFftThreads, row_smem(fp)>>>(w);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return fail(QVA_ERR_CUDA, std::string("Bluestein setup: ") + cudaGetErrorString(e));
     }
@@ -1114,7 +1225,7 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
         c.do_fwd = fwd;
         c.ops = ops;
         obs->begin(K_FFT_COL, 32.0 * (double)R * nmat);
-        fft_col_kernel<kFftThreads><<<gc, kFftThreads, smem_c, s>>>(c);
+        col_kernel_for(fp->Mi1, false)<<<gc, kFftThreads, smem_c, s>>>(c);
         cudaError_t e = cudaGetLastError();
         obs->end();
         if (e != cudaSuccess) {
@@ -1144,7 +1255,7 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
         w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
     }
     obs->begin(K_FFT_ROW, 32.0 * (double)R * nmat + (r.lambda_perm ? 8.0 * (double)R * nmat : 0.0));
-    fft_row_kernel<<<nmat * fp->Mi1 / fp->rb2, kFftThreads, (size_t)fp->rb2 * fp->Mi2 * sizeof(double2), s>>>(w);
+    row_kernel_for(fp->Mi2)<<<nmat * fp->Mi1 / fp->rb2, kFftThreads, (size_t)fp->rb2 * fp->Mi2 * sizeof(double2), s>>>(w);
     cudaError_t e = cudaGetLastError();
     obs->end();
     if (e != cudaSuccess) {
@@ -1229,8 +1340,7 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
                              ((ops & (OP_PHASE | OP_EXPECT)) ? q_bytes : 0.0) + ((ops & OP_SPEC) && c.lam ? 8.0 * N : 0.0);
         obs->begin(K_FFT_COL, bytes);
         expect_slots = gc;
-        if (col_half) fft_col_kernel<kFftThreads / 2><<<gc, kFftThreads / 2, smem_c, s>>>(c);
-        else fft_col_kernel<kFftThreads><<<gc, kFftThreads, smem_c, s>>>(c);
+        col_kernel_for(fp->M1, col_half)<<<gc, col_half ? kFftThreads / 2 : kFftThreads, smem_c, s>>>(c);
         cudaError_t e = cudaGetLastError();
         obs->end();
         if (e != cudaSuccess) {
@@ -1262,7 +1372,7 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
             w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
         }
         obs->begin(K_FFT_ROW, 32.0 * M + extra);
-        fft_row_kernel<<<gr, kFftThreads, smem_r, s>>>(w);
+        row_kernel_for(fp->M2)<<<gr, kFftThreads, smem_r, s>>>(w);
         cudaError_t e = cudaGetLastError();
         obs->end();
         if (e != cudaSuccess) {
@@ -1377,7 +1487,7 @@ qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStr
             c.ops = ops;
             c.gamma = gamma;
             obs->begin(K_FFT_COL, 16.0 * NG * (init ? 1 : 2) + ((ops & (OP_PHASE | OP_EXPECT)) ? 8.0 * NG : 0.0));
-            fft_col_kernel<kFftThreads><<<gc, kFftThreads, smem_c, s>>>(c);
+            col_kernel_for(fp->M1, false)<<<gc, kFftThreads, smem_c, s>>>(c);
             cudaError_t e = cudaGetLastError();
             obs->end();
             if (e != cudaSuccess) {
@@ -1403,7 +1513,7 @@ qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStr
             w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
         }
         obs->begin(K_FFT_ROW, 32.0 * NG * io.local + (r.lambda_perm ? 8.0 * NG * io.local : 0.0));
-        fft_row_kernel<<<io.local * M1s / rb, kFftThreads, smem_r, s>>>(w);
+        row_kernel_for(fp->M2)<<<io.local * M1s / rb, kFftThreads, smem_r, s>>>(w);
         cudaError_t e = cudaGetLastError();
         obs->end();
         if (e != cudaSuccess) {
