@@ -496,6 +496,12 @@ struct qva_plan {
     size_t mult_cap = 0;
     void *d_edges = nullptr;              // on-demand q generation: edge list
     size_t edge_cap = 0;
+    void *d_gen_edges = nullptr;          // generator records: classified edge lists
+    size_t gen_edge_cap = 0;
+    void *scratch = nullptr;              // scratch_get
+    size_t scratch_cap = 0;
+    double2 *small_batch = nullptr;       // batched small-state evolutions
+    size_t small_batch_cap = 0;
     // pinned host ring for small per-step uploads (angles, tables, generator records): a copy from
     // pageable memory would synchronise the stream before it starts
     unsigned char *ring = nullptr;
@@ -734,6 +740,7 @@ qva_status ensure_qB(qva_plan *P) {
 // tables (exact: the table entry for k is the same fp64 sincos of fl(gamma*k)).
 void drop_qt(qva_plan *P);
 qva_status ensure_q_dev(qva_plan *P);
+cudaError_t scratch_get(qva_plan *P, void **p, size_t bytes);
 qva_status classify_q(qva_plan *P) {
     drop_qt(P);
     P->q_mode = 0;
@@ -742,7 +749,7 @@ qva_status classify_q(qva_plan *P) {
     QVA_TRY(ensure_q_dev(P));
     int blocks = q_range_blocks(P->arr_n);
     double *mm = nullptr;
-    QVA_CUDA_TRY(cudaMallocAsync((void **)&mm, 2 * blocks * sizeof(double), P->stream));
+    QVA_CUDA_TRY(scratch_get(P, (void **)&mm, 2 * blocks * sizeof(double)));
     QVA_CUDA_TRY(cudaMemsetAsync(P->d_flag, 0, sizeof(int), P->stream));
     {
         ProfScope ps(P, K_OTHER, 8.0 * P->arr_n);
@@ -752,7 +759,6 @@ qva_status classify_q(qva_plan *P) {
     int flag = 0;
     QVA_CUDA_TRY(cudaMemcpyAsync(h.data(), mm, h.size() * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
     QVA_CUDA_TRY(cudaMemcpyAsync(&flag, P->d_flag, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
-    QVA_CUDA_TRY(cudaFreeAsync(mm, P->stream));
     QVA_TRY(sync(P));
     double lo = INFINITY, hi = -INFINITY;
     for (int b = 0; b < blocks; ++b) {
@@ -763,11 +769,10 @@ qva_status classify_q(qva_plan *P) {
         double v[3] = {(double)flag, -lo, hi};
         // max-reduce via NCCL
         double *d;
-        QVA_CUDA_TRY(cudaMallocAsync((void **)&d, sizeof(v), P->stream));
+        QVA_CUDA_TRY(scratch_get(P, (void **)&d, sizeof(v)));
         QVA_CUDA_TRY(cudaMemcpyAsync(d, v, sizeof(v), cudaMemcpyHostToDevice, P->stream));
         QVA_NCCL_TRY(ncclAllReduce(d, d, 3, ncclDouble, ncclMax, P->comm, P->stream));
         QVA_CUDA_TRY(cudaMemcpyAsync(v, d, sizeof(v), cudaMemcpyDeviceToHost, P->stream));
-        QVA_CUDA_TRY(cudaFreeAsync(d, P->stream));
         QVA_TRY(sync(P));
         flag = v[0] != 0.0;
         lo = -v[1];
@@ -855,6 +860,21 @@ qva_status upload(qva_plan *P, void *dst, const void *src, size_t bytes) {
     QVA_CUDA_TRY(cudaMemcpyAsync(dst, P->ring + off, bytes, cudaMemcpyHostToDevice, P->stream));
     P->ring_pos = off + bytes;
     return QVA_OK;
+}
+
+// persistent device scratch for short-lived buffers of one call (each use completes before the
+// call returns); stream-ordered allocation measured host stalls of up to 100+ ms per call
+cudaError_t scratch_get(qva_plan *P, void **p, size_t bytes) {
+    if (P->scratch_cap < bytes) {
+        cudaFree(P->scratch);
+        P->scratch = nullptr;
+        P->scratch_cap = 0;
+        cudaError_t e = cudaMalloc(&P->scratch, bytes);
+        if (e != cudaSuccess) return e;
+        P->scratch_cap = bytes;
+    }
+    *p = P->scratch;
+    return cudaSuccess;
 }
 
 void drop_qt(qva_plan *P) {
@@ -1110,9 +1130,14 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
     QVA_CUDA_TRY(pool_get(P, &ent.rec, ent.rec_bytes));
     QVA_CUDA_TRY(pool_get(P, &ent.thr, 128 * 8 * sizeof(double)));
     QVA_CUDA_TRY(pool_get(P, &ent.G, 32 * sizeof(double)));
-    void *d_edges = nullptr;
     const size_t eb = (tt.size() + tb.size()) * (sizeof(int2) + sizeof(double)) + 16;
-    QVA_CUDA_TRY(cudaMallocAsync(&d_edges, eb, P->stream));
+    if (P->gen_edge_cap < eb) {  // stream order keeps one staging buffer safe across entries
+        cudaFree(P->d_gen_edges);
+        P->d_gen_edges = nullptr;
+        QVA_CUDA_TRY(cudaMalloc(&P->d_gen_edges, eb));
+        P->gen_edge_cap = eb;
+    }
+    void *d_edges = P->d_gen_edges;
     {
         std::vector<unsigned char> hb(eb, 0);
         size_t off = 0;
@@ -1133,7 +1158,6 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
         QVA_TRY(upload(P, d_edges, hb.data(), eb));
         ProfScope ps(P, K_OTHER, (double)n_tiles * rec_bytes);
         QVA_CUDA_TRY(launch_gen_records(ent.rec, n_tiles, f64 ? 1 : 0, gp, P->stream));
-        QVA_CUDA_TRY(cudaFreeAsync(d_edges, P->stream));
         // host per-thread constants of group gq: C(c), beta_j(c), and G(e)
         const TileGroup &g = kGroups[gq];
         int role[kTileBits], ridx[kTileBits];  // 0: thread bit, 1: register bit
@@ -1448,23 +1472,8 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         // tiles go back through a TMA tensor store (measured faster than st.global from registers for
         // every tile shape; env QVA_TSTORE=0 selects the register stores for comparison)
         tp.tma_store = (g_tstore >= 0) ? g_tstore : 1;
-        static int order_env = [] { const char *e = getenv("QVA_ORDER"); return e ? atoi(e) : 0; }();
-        tp.order = order_env;
         CUtensorMap map, map_out;
         if (pp.permuted) tp.tma_store = 1;  // the permuted store is a TMA store map
-        // L2 block prefetch for strided sets: the block is everything below the highest tile bit;
-        // tiles per block = 2^(coordinate bits below it) (one 64-KiB chunk each)
-        static int pf_env = [] { const char *e = getenv("QVA_PF"); return e ? atoi(e) : 0; }();  // measured slower (8.3 vs 6.2 ms per pass): off by default
-        tp.psi_in = psi_in;
-        if (pf_env && batch == 1 && tp.init != 1) {
-            const int top = s[kTileBits - 1];
-            const int low = top + 1 - kTileBits;  // coordinate bits below the top tile bit
-            if (low > 0 && top + 1 < n_phys) {
-                tp.pf_shift = top + 1;
-                tp.pf_lowbits = low;
-                tp.pf_nblocks = 1ull << (n_phys - top - 1);
-            }
-        }
         {
             // tensor maps depend on (tile bits, store permutation, buffers, sizes): encoded once
             std::vector<int64_t> key = {(int64_t)(uintptr_t)psi_in, (int64_t)(uintptr_t)tp.psi_out, n_phys, batch};
@@ -1625,11 +1634,10 @@ qva_status run_passes_graph(qva_plan *P, const std::vector<PassPlan> &passes, co
 qva_status allreduce_host(qva_plan *P, double *vals, int n) {
     if (P->world == 1) return QVA_OK;
     double *d;
-    QVA_CUDA_TRY(cudaMallocAsync((void **)&d, n * sizeof(double), P->stream));
+    QVA_CUDA_TRY(scratch_get(P, (void **)&d, n * sizeof(double)));
     QVA_CUDA_TRY(cudaMemcpyAsync(d, vals, n * sizeof(double), cudaMemcpyHostToDevice, P->stream));
     QVA_NCCL_TRY(ncclAllReduce(d, d, n, ncclDouble, ncclSum, P->comm, P->stream));
     QVA_CUDA_TRY(cudaMemcpyAsync(vals, d, n * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
-    QVA_CUDA_TRY(cudaFreeAsync(d, P->stream));
     QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
     return QVA_OK;
 }
@@ -1992,6 +2000,9 @@ qva_status qva_plan_destroy(qva_plan *P) {
     }
     cudaFree(P->d_mult);
     cudaFree(P->d_edges);
+    cudaFree(P->d_gen_edges);
+    cudaFree(P->scratch);
+    cudaFree(P->small_batch);
     for (auto &e : P->pool) cudaFree(e.second);
     if (P->ring) cudaFreeHost(P->ring);
     cudaFree(P->partials);
@@ -2669,13 +2680,12 @@ qva_status qva_get_probabilities(qva_plan *P, double *out, uint64_t offset, uint
         P->expect_valid = ev;
     }
     double *d;
-    QVA_CUDA_TRY(cudaMallocAsync((void **)&d, count * sizeof(double), P->stream));
+    QVA_CUDA_TRY(scratch_get(P, (void **)&d, count * sizeof(double)));
     {
         ProfScope ps(P, K_OTHER, 24.0 * count);
         QVA_CUDA_TRY(launch_probabilities(P->psi + lo, d, count, P->stream));
     }
     QVA_CUDA_TRY(cudaMemcpyAsync(out, d, count * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
-    QVA_CUDA_TRY(cudaFreeAsync(d, P->stream));
     return sync(P);
 }
 
@@ -2703,8 +2713,13 @@ static qva_status batch_local(qva_plan *P, const double *thetas, int first, int 
                     QVA_CUDA_TRY(cudaMalloc(&P->red, (size_t)nb * 2 * sizeof(double)));
                     P->max_batch = nb;
                 }
-                double2 *bpsi = nullptr;
-                QVA_CUDA_TRY(cudaMallocAsync((void **)&bpsi, (size_t)nb * P->arr_n * sizeof(double2), P->stream));
+                if (P->small_batch_cap < (size_t)nb * P->arr_n) {
+                    cudaFree(P->small_batch);
+                    P->small_batch = nullptr;
+                    QVA_CUDA_TRY(cudaMalloc(&P->small_batch, (size_t)nb * P->arr_n * sizeof(double2)));
+                    P->small_batch_cap = (size_t)nb * P->arr_n;
+                }
+                double2 *bpsi = P->small_batch;
                 QVA_CUDA_TRY(cudaMemcpyAsync(P->d_thetas, th + (size_t)b0 * 2 * p, need * sizeof(double),
                                              cudaMemcpyHostToDevice, P->stream));
                 SmallEvolveParams sp{};
@@ -2722,7 +2737,6 @@ static qva_status batch_local(qva_plan *P, const double *thetas, int first, int 
                 }
                 QVA_CUDA_TRY(cudaMemcpyAsync(pairs.data(), P->red, pairs.size() * sizeof(double),
                                              cudaMemcpyDeviceToHost, P->stream));
-                QVA_CUDA_TRY(cudaFreeAsync(bpsi, P->stream));
                 QVA_TRY(sync(P));
             } else {
                 auto passes = cut_passes(evolve_tokens(P->L, 0, p), P->sets, true);

@@ -87,6 +87,8 @@ struct FftPlan {
     double2 *bhat = nullptr;     // Bluestein: F_M b in transposed order
     double *partials = nullptr;
     int n_partials = 0;
+    double *d_theta = nullptr;   // whole-kernel path: angles (host-to-device each evolution)
+    int theta_cap = 0;
 };
 
 namespace {
@@ -1170,6 +1172,7 @@ void fft_plan_destroy(FftPlan *fp) {
     cudaFree(fp->bhat);
     cudaFree(fp->d_in_lo);
     cudaFree(fp->d_in_hi);
+    cudaFree(fp->d_theta);
     delete fp;
 }
 
@@ -1285,15 +1288,19 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
         a.tw = fp->d_tw;
         a.sf = fp->row;
         const int nth = r.mode == 0 ? 2 * r.p : 1;
-        double *dth = nullptr;
-        QVA_CUDA_TRY(cudaMallocAsync((void **)&dth, std::max(nth, 1) * sizeof(double), s));
+        if (fp->theta_cap < nth || !fp->d_theta) {
+            cudaFree(fp->d_theta);
+            fp->d_theta = nullptr;
+            QVA_CUDA_TRY(cudaMalloc(&fp->d_theta, std::max(nth, 1) * sizeof(double)));
+            fp->theta_cap = std::max(nth, 1);
+        }
+        double *dth = fp->d_theta;
         if (nth) QVA_CUDA_TRY(cudaMemcpyAsync(dth, r.theta, nth * sizeof(double), cudaMemcpyHostToDevice, s));
         a.theta = dth;
         obs->begin(K_FFT_ROW, state_bytes * (r.init ? 1 : 2) + q_bytes * (r.mode == 0 ? 1 : 0));
         fft_whole_kernel<<<1, kFftThreads, (size_t)fp->N * sizeof(double2), s>>>(a);
         cudaError_t e = cudaGetLastError();
         obs->end();
-        cudaFreeAsync(dth, s);
         if (e != cudaSuccess) {
             set_error(std::string("fft_whole_kernel: ") + cudaGetErrorString(e));
             return QVA_ERR_CUDA;

@@ -94,9 +94,6 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
-__device__ __forceinline__ void l2_prefetch(const void *src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void wg_sync(int wg) { asm volatile("bar.sync %0, %1;" ::"r"(1 + wg), "n"(kCT) : "memory"); }
 
@@ -470,15 +467,10 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const uint64_t n_items = P.n_tiles * (uint64_t)P.batch;
-    // item order: interleaved (CTA b takes b, b + grid, ...) or blocked (CTA b takes a contiguous
-    // range of items, so its in-flight stages hold neighbouring tiles)
-    const uint64_t per_cta = (n_items + gridDim.x - 1) / gridDim.x;
-    const uint64_t blk_lo = min(n_items, (uint64_t)blockIdx.x * per_cta);
-    const uint32_t n_it = P.order ? (uint32_t)(min(n_items, blk_lo + per_cta) - blk_lo)
-                                  : (uint32_t)((n_items > blockIdx.x) ? (n_items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
-    auto item_of = [&](uint32_t j) -> uint64_t {
-        return P.order ? blk_lo + j : blockIdx.x + (uint64_t)j * gridDim.x;
-    };
+    // item order: interleaved over CTAs (CTA b takes b, b + grid, ...: the in-flight tiles of the
+    // whole grid are neighbours; contiguous per-CTA ranges measured no different)
+    const uint32_t n_it = (uint32_t)((n_items > blockIdx.x) ? (n_items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
+    auto item_of = [&](uint32_t j) -> uint64_t { return blockIdx.x + (uint64_t)j * gridDim.x; };
     const bool load_psi = (P.init != 1);
     const bool tstore = P.tma_store != 0;  // output through a TMA store of the final smem tile
     const bool load_q = (QB > 0) && (P.gq >= 0);
@@ -500,14 +492,6 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             tma_load_5d(smem_u32(psi_s + (size_t)s * kTile), &tmap, bar, cc);
         }
         if (qbytes) bulk_load(smem_u32(q_s + (size_t)s * QSB), qt + t * (uint64_t)qbytes, qbytes, bar);
-        // strided tile sets: tile (block b, index c) prefetches the contiguous 64-KiB chunk c of
-        // block b + 1 into L2, so the next block's 128-B rows are L2 hits and DRAM sees
-        // sequential reads
-        if (P.pf_shift) {
-            const uint64_t b = t >> P.pf_lowbits, cidx = t & ((1ull << P.pf_lowbits) - 1);
-            if (b + 1 < P.pf_nblocks)
-                l2_prefetch(P.psi_in + ((b + 1) << P.pf_shift) + (cidx << kTileBits), kTile * sizeof(double2));
-        }
     };
 
     if (tid == 0) {

@@ -117,17 +117,10 @@ struct TilePassParams {
     int release_step;        // step after whose smem accesses the stage is released (n_steps: after
                              // the expectation; -1: before any step, i.e. init passes without q)
     double amp0;
-    int order;               // tile order: 0 interleaved over CTAs, 1 contiguous range per CTA
-    // L2 block prefetch (strided tile sets, batch 1): tile t = (block t >> pf_lowbits, chunk
-    // c = low bits) prefetches psi_in[((block + 1) << pf_shift) + c * 4096 ...] (64 KiB)
     // generated MaxCut qualities (qbytes kQGenInt / kQGenF64): qt points at the per-tile records
     const void *gen_thr;     // [128][8] int / double: per consumer thread {C, beta[5]} of group gq
     const void *gen_G;       // [32] int / double: G(e) over the 5 register bits of group gq
     int gen_m;               // number of edges (integer mode: qmin = -gen_m)
-    const double2 *psi_in;
-    int pf_shift;            // 0: off; else log2(elements per block)
-    int pf_lowbits;
-    uint64_t pf_nblocks;
 };
 
 // Compile-time pass programs (kernels_tile.cu): group sequence g[0..n), which steps rotate,

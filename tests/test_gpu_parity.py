@@ -466,8 +466,9 @@ def test_cfg4_full_size_vs_golden(Q):
     assert np.allclose(g["theta"], wl.theta, rtol=0, atol=0)
     with Q.Plan(wl.dim, "x", n_qubits=wl.n_qubits) as P:
         P.set_qualities_maxcut(wl.edges_u, wl.edges_v)
-        P.evolve(wl.theta)
-        _f_close(P.expectation(), g["expectation_full_state"])
+        for _ in range(4):  # as bench.py runs it: the third call on replays the captured graph
+            P.evolve(wl.theta)
+            _f_close(P.expectation(), g["expectation_full_state"])
         _f_close(P.expectation(), g["expectation_lightcone"])
         assert abs(P.norm2() - 1) < 1e-12
         idx = np.asarray(g["sample_index"], np.int64)
