@@ -46,6 +46,7 @@ constexpr int kFftThreads = 512;
 constexpr int kMaxCta = 8192;                     // points per CTA transform set
 constexpr int kMaxSub = 8192;                     // longest sub-FFT
 constexpr int kColSmemMax = 200 * 1024;
+constexpr int kLoadU = 8;                         // independent global loads per thread per batch
 
 struct SubFft {
     int n = 1;
@@ -587,14 +588,27 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
     double2 *A = reinterpret_cast<double2 *>(smem_raw);
     const int tot = M1 * cwv;
     const int totw = M1 << a.lcw;  // (x1, c) over the full column width; c >= cwv skipped
-    for (int idx = threadIdx.x; idx < totw; idx += blockDim.x) {
-        const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
-        if (c >= cwv) continue;
-        const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
-        double2 v;
-        if (a.init) v = make_double2(x < a.N ? a.amp0 : 0.0, 0.0);
-        else v = x < a.in_len ? a.in[mat + x] : make_double2(0.0, 0.0);
-        A[c * stride + x1] = v;
+    // the column block arrives in batches of kLoadU independent loads per thread (one load per
+    // iteration would wait a full memory latency for each element before its smem store)
+    for (int base = threadIdx.x; base < totw; base += kLoadU * blockDim.x) {
+        double2 v[kLoadU];
+#pragma unroll
+        for (int u = 0; u < kLoadU; ++u) {
+            const int idx = base + u * blockDim.x;
+            const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
+            const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
+            v[u] = make_double2(0.0, 0.0);
+            if (idx < totw && c < cwv) {
+                if (a.init) v[u] = make_double2(x < a.N ? a.amp0 : 0.0, 0.0);
+                else if (x < a.in_len) v[u] = a.in[mat + x];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kLoadU; ++u) {
+            const int idx = base + u * blockDim.x;
+            const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
+            if (idx < totw && c < cwv) A[c * stride + x1] = v[u];
+        }
     }
     __syncthreads();
     col_block<F>(AddrLin{A, stride}, a, c0, cwv, blockIdx.y, blockIdx.x, red);
@@ -634,7 +648,19 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
     double2 *A = reinterpret_cast<double2 *>(smem_raw);
     double2 *rows = a.buf + (uint64_t)k1_0 * M2;
     const int tot = a.rb * M2;
-    for (int i = threadIdx.x; i < tot; i += blockDim.x) A[i] = rows[i];
+    for (int base = threadIdx.x; base < tot; base += kLoadU * blockDim.x) {
+        double2 v[kLoadU];
+#pragma unroll
+        for (int u = 0; u < kLoadU; ++u) {
+            const int i = base + u * blockDim.x;
+            if (i < tot) v[u] = rows[i];
+        }
+#pragma unroll
+        for (int u = 0; u < kLoadU; ++u) {
+            const int i = base + u * blockDim.x;
+            if (i < tot) A[i] = v[u];
+        }
+    }
     __syncthreads();
     F::run(AddrLin{A, M2}, a.sf, a.tw, a.rb, false);
     if (a.fwd_only) {
