@@ -6,6 +6,7 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Citations are to
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 from functools import lru_cache
@@ -22,6 +23,8 @@ __all__ = [
     "evolve_x", "evolve_complete", "evolve_circulant_dense", "lightcone_maxcut",
     "dense_sum_x", "mixer_sparse_dense", "evolve_sparse_dense", "c128",
     "mixer_parity", "evolve_parity", "parity_pairs",
+    "kperm_count", "kperm_unrank", "kperm_cost", "kperm_qualities",
+    "maxcut_term_q", "evolve_ex",
 ]
 
 
@@ -244,4 +247,78 @@ def evolve_sparse_dense(q: np.ndarray, W_dense: np.ndarray, theta,
     for k in range(len(theta) // 2):
         phase(psi, q, theta[2 * k])
         psi = np.ascontiguousarray(mixer_sparse_dense(psi, W_dense, theta[2 * k + 1]))
+    return psi
+
+
+# ---------------------------------------------------------------------------------------
+# Permutation-encoded subspaces (QWOA).
+# A solution s is a k-permutation of the m elements zeta = {0..m-1}; the
+# indexed state |i> holds the i-th k-permutation in lexicographic order (reading R23: the
+# indexing id_chi of Eq. qwoa_index is the Lehmer code / factorial number system).
+# ---------------------------------------------------------------------------------------
+
+def kperm_count(m: int, k: int) -> int:
+    """|S'| = m! / (m - k)! (number of k-permutations of m elements)."""
+    return math.perm(m, k)
+
+
+def kperm_unrank(m: int, k: int, r: int) -> list:
+    """The r-th k-permutation of range(m) in lexicographic order: digit a of the mixed-radix
+    (Lehmer) code of r is r // ((m-a-1)!/(m-k)!), and it picks that many-th smallest unused
+    element (R23)."""
+    avail = list(range(m))
+    out = []
+    for a in range(k):
+        c = math.perm(m - a - 1, k - a - 1)
+        d, r = divmod(r, c)
+        out.append(avail.pop(d))
+    return out
+
+
+def kperm_cost(pi, F, D, C=None) -> float:
+    """C(s) = sum_a ( C[a, s_a] + sum_b F[a, b] D[s_a, s_b] ) (reading R24: the quadratic-
+    assignment form; TSP is F = the directed cycle).  Summed in this order, a-major."""
+    k = len(pi)
+    s = 0.0
+    for a in range(k):
+        if C is not None:
+            s += float(C[a][pi[a]])
+        for b in range(k):
+            s += float(F[a][b]) * float(D[pi[a]][pi[b]])
+    return s
+
+
+def kperm_qualities(m: int, k: int, F, D, C=None, ranks=None) -> np.ndarray:
+    """q_i = C(s_i) for every rank i (or the given ranks): diag(Q) of the permutation subspace
+    ("diag(Q) = C(s_i)").  Plain loops: small subspaces / samples only."""
+    if ranks is None:
+        ranks = range(kperm_count(m, k))
+    return np.array([kperm_cost(kperm_unrank(m, k, int(r)), F, D, C) for r in ranks], np.float64)
+
+
+# ---------------------------------------------------------------------------------------
+# Extended QAOA (PAPER.md:190-207, Eqs. phase_shift_qaoa_ex / qaoa_ex; SURVEY NEXT-4).
+# ---------------------------------------------------------------------------------------
+
+def maxcut_term_q(n: int, u: int, v: int, w: float = 1.0) -> np.ndarray:
+    """Diagonal of one summation term of the max-cut quality (reading R25): Sigma_e(x) =
+    -w_e [x_u != x_v], so that sum_e Sigma_e = q = -cut_w (R10)."""
+    x = np.arange(1 << n, dtype=np.int64)
+    return -float(w) * (((x >> u) ^ (x >> v)) & 1).astype(np.float64)
+
+
+def evolve_ex(n: int, u, v, w, theta) -> np.ndarray:
+    """ex-QAOA state (PAPER.md Eq. qaoa_ex): theta = per layer [gamma_{i,1..m}, t_i]
+    (|theta| = (1 + m) D); layer i applies prod_e exp(-i gamma_{i,e} Sigma_e)
+    (Eq. phase_shift_qaoa_ex: the terms commute) then U_X(t_i); layer 1 acts first (R6)."""
+    m = len(u)
+    theta = np.asarray(theta, np.float64)
+    assert theta.size % (m + 1) == 0
+    p = theta.size // (m + 1)
+    psi = init_uniform(1 << n)
+    for i in range(p):
+        th = theta[i * (m + 1):(i + 1) * (m + 1)]
+        for e in range(m):
+            phase(psi, maxcut_term_q(n, int(u[e]), int(v[e]), 1.0 if w is None else float(w[e])), th[e])
+        mixer_x(psi, th[m])
     return psi

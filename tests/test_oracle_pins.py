@@ -178,10 +178,13 @@ def test_P7_ring_closed_form(n):
         assert f == pytest.approx(-n / 2 + (n / 4) * math.sin(4 * b) * math.sin(2 * g), abs=1e-12)
 
 
-def _p1_weighted_closed_form(n, u, v, w, g, b):
-    """P8: weighted p=1 max-cut closed form (Heisenberg picture), q = -cut_w."""
+def _p1_weighted_closed_form(n, u, v, w, g, b, gw=None):
+    """P8: weighted p=1 max-cut closed form (Heisenberg picture), q = -cut_w.  gw: per-edge
+    phase angles gamma_e * w_e (ex-QAOA, P18); default g * w."""
+    if gw is None:
+        gw = [g * x for x in w]
     W = {}
-    for a, c, x in zip(u, v, w):
+    for a, c, x in zip(u, v, gw):
         W[(int(a), int(c))] = x
         W[(int(c), int(a))] = x
     nbr = {i: set() for i in range(n)}
@@ -191,16 +194,16 @@ def _p1_weighted_closed_form(n, u, v, w, g, b):
     total = 0.0
     for a, c, wuv in zip(u, v, w):
         a, c = int(a), int(c)
-        Pu = np.prod([math.cos(g * W[(a, k)]) for k in nbr[a] - {c}])
-        Pv = np.prod([math.cos(g * W[(c, k)]) for k in nbr[c] - {a}])
+        Pu = np.prod([math.cos(W[(a, k)]) for k in nbr[a] - {c}])
+        Pv = np.prod([math.cos(W[(c, k)]) for k in nbr[c] - {a}])
         T = (nbr[a] & nbr[c])
         U = nbr[a] - T - {c}
         V = nbr[c] - T - {a}
-        t1 = 0.5 * math.sin(4 * b) * math.sin(g * wuv) * (Pu + Pv)
-        pu = np.prod([math.cos(g * W[(a, k)]) for k in U])
-        pv = np.prod([math.cos(g * W[(c, k)]) for k in V])
-        tm = np.prod([math.cos(g * (W[(a, k)] - W[(c, k)])) for k in T])
-        tp = np.prod([math.cos(g * (W[(a, k)] + W[(c, k)])) for k in T])
+        t1 = 0.5 * math.sin(4 * b) * math.sin(W[(a, c)]) * (Pu + Pv)
+        pu = np.prod([math.cos(W[(a, k)]) for k in U])
+        pv = np.prod([math.cos(W[(c, k)]) for k in V])
+        tm = np.prod([math.cos(W[(a, k)] - W[(c, k)]) for k in T])
+        tp = np.prod([math.cos(W[(a, k)] + W[(c, k)]) for k in T])
         t2 = 0.5 * math.sin(2 * b) ** 2 * pu * pv * (tm - tp)
         zz = t1 + t2
         total += wuv / 2 * (zz - 1)
@@ -433,3 +436,139 @@ def test_P16_parity_conservation_and_special_angle():
     for a, b in odd + even + last:
         sign *= np.array([(-1.0) ** (((x >> a) ^ (x >> b)) & 1) for x in range(1 << n)])
     assert np.max(np.abs(O.mixer_parity(phi.copy(), seq, math.pi / 2) - sign * phi)) < 1e-12
+
+
+# ---------------------------------------------------------------- permutation subspaces (P17) ----
+@pytest.mark.parametrize("m,k", [(1, 1), (3, 3), (4, 2), (5, 5), (6, 3), (7, 7), (8, 1)])
+def test_P17_kperm_unrank_is_itertools_order(m, k):
+    """P17: rank r <-> the r-th k-permutation in lexicographic order (R23): kperm_unrank against
+    itertools.permutations (library order), over every rank; the count is m!/(m-k)!."""
+    import itertools
+    ref = list(itertools.permutations(range(m), k))
+    assert O.kperm_count(m, k) == len(ref)
+    for r, pi in enumerate(ref):
+        assert tuple(O.kperm_unrank(m, k, r)) == pi
+
+
+def test_P17_kperm_lehmer_code_definition():
+    """P17: the Lehmer code d_a = #{unused elements < s_a} read as a mixed-radix number with
+    radices (m-a)... gives back the rank (Knuth's definition of the factorial number system)."""
+    m, k = 9, 5
+    for r in [0, 1, 2, 1000, 7777, O.kperm_count(m, k) - 1]:
+        pi = O.kperm_unrank(m, k, r)
+        rank = 0
+        for a in range(k):
+            d = sum(1 for x in pi[a + 1:] if x < pi[a]) + sum(
+                1 for x in range(m) if x not in pi and x < pi[a])
+            rank = rank * (m - a) + d
+        assert rank == r
+
+
+def test_P17_tsp_worked_example():
+    """P17 worked example, by hand: m = k = 3, directed 3-cycle F (F[a][(a+1)%3] = 1),
+    D = [[0,1,2],[4,0,8],[16,32,0]] (asymmetric).  Lexicographic tours and their costs:
+    012: D01+D12+D20 = 1+8+16 = 25; 021: D02+D21+D10 = 2+32+4 = 38; 102: D10+D02+D21 = 38;
+    120: D12+D20+D01 = 25; 201: D20+D01+D12 = 25; 210: D21+D10+D02 = 38."""
+    F = [[0, 1, 0], [0, 0, 1], [1, 0, 0]]
+    D = [[0, 1, 2], [4, 0, 8], [16, 32, 0]]
+    assert list(O.kperm_qualities(3, 3, F, D)) == [25.0, 38.0, 38.0, 25.0, 25.0, 38.0]
+    # a linear (assignment) term: C[a][s_a]
+    C = [[100, 200, 300], [0, 0, 0], [0, 0, 7]]
+    assert list(O.kperm_qualities(3, 3, F, D, C)) == [25 + 100 + 7, 38 + 100, 38 + 200 + 7,
+                                                      25 + 200, 25 + 300, 38 + 300]
+
+
+@pytest.mark.parametrize("m,k", [(6, 6), (7, 4), (5, 2)])
+def test_P17_kperm_sum_closed_form(m, k):
+    """P17: sum over all k-permutations of sum_ab F_ab D_{s_a s_b} + C_{a s_a} equals
+    sum_{a!=b} F_ab * sum_{i!=j} D_ij * (m-2)!/(m-k)! + sum_a F_aa * tr D * (m-1)!/(m-k)!
+    + sum_a sum_i C_ai * (m-1)!/(m-k)! (each ordered pair / element is equally often used)."""
+    rng = np.random.default_rng(m * 10 + k)
+    F = rng.uniform(-1, 1, (k, k))
+    D = rng.uniform(-1, 1, (m, m))
+    C = rng.uniform(-1, 1, (k, m))
+    q = O.kperm_qualities(m, k, F, D, C)
+    off = F.sum() - np.trace(F)
+    ref = off * (D.sum() - np.trace(D)) * (math.perm(m - 2, k - 2) if k >= 2 else 0)
+    ref += np.trace(F) * np.trace(D) * math.perm(m - 1, k - 1)
+    ref += C.sum() * math.perm(m - 1, k - 1)
+    assert q.sum() == pytest.approx(ref, rel=1e-12, abs=1e-9)
+
+
+def test_P17_tsp_rotation_invariance():
+    """P17: a closed tour's cost does not depend on its starting city: with F the directed
+    m-cycle, q(s) = q(rotate(s)) for every s (catches a transposed F or D index)."""
+    m = 6
+    rng = np.random.default_rng(17)
+    D = rng.uniform(0, 1, (m, m))
+    F = np.zeros((m, m))
+    for a in range(m):
+        F[a, (a + 1) % m] = 1
+    import itertools
+    perms = list(itertools.permutations(range(m)))
+    q = O.kperm_qualities(m, m, F, D)
+    index = {p: i for i, p in enumerate(perms)}
+    for i, pi in enumerate(perms):
+        rot = pi[1:] + pi[:1]
+        assert q[index[rot]] == pytest.approx(q[i], abs=1e-14)
+        rev = tuple(reversed(pi))  # the reversed tour costs sum D^T: differs for asymmetric D
+        assert abs(q[index[rev]] - sum(D[pi[(a + 1) % m], pi[a]] for a in range(m))) < 1e-12
+
+
+# ---------------------------------------------------------------- ex-QAOA (P18) ----
+def test_P18_ex_qaoa_equal_gammas_is_qaoa():
+    """P18: with gamma_{i,e} = gamma_i for every term, Eq. phase_shift_qaoa_ex is exp(-i gamma_i Q)
+    (R25: the terms sum to q), so ex-QAOA reduces to QAOA (Eq. qaoa) amplitude by amplitude."""
+    rng = np.random.default_rng(18)
+    n = 8
+    u, v = erdos_renyi_graph(n, 0.5, rng)
+    w = rng.uniform(0, 1, len(u))
+    m = len(u)
+    theta = rng.uniform(0, math.pi, 4)
+    tex = np.concatenate([np.r_[np.full(m, theta[2 * i]), theta[2 * i + 1]] for i in range(2)])
+    a = O.evolve_ex(n, u, v, w, tex)
+    b = O.evolve_x(n, O.maxcut_q(n, u, v, w), theta)
+    assert np.max(np.abs(a - b)) < 1e-13
+
+
+def test_P18_ex_qaoa_vs_dense_pauli_expm():
+    """P18: ex-QAOA against dense matrices built from Pauli Z / X Kronecker products:
+    Sigma_e = -w_e (I - Z_u Z_v) / 2, layer = expm(-i t sum_j X_j) expm(-i sum_e gamma_e Sigma_e)."""
+    rng = np.random.default_rng(181)
+    n = 5
+    u, v = erdos_renyi_graph(n, 0.7, rng)
+    w = rng.uniform(0.2, 1, len(u))
+    m = len(u)
+    I2, Z = np.eye(2), np.diag([1.0, -1.0])
+
+    def op(j, P):  # qubit j = bit j of the index (R8): kron order puts qubit n-1 first
+        out = np.array([[1.0]])
+        for b in reversed(range(n)):
+            out = np.kron(out, P if b == j else I2)
+        return out
+
+    Sig = [-w[e] * (np.eye(1 << n) - op(u[e], Z) @ op(v[e], Z)) / 2 for e in range(m)]
+    Xs = O.dense_sum_x(n)
+    theta = rng.uniform(0, math.pi, 2 * (m + 1))
+    psi = np.full(1 << n, (1 << n) ** -0.5, np.complex128)
+    for i in range(2):
+        th = theta[i * (m + 1):(i + 1) * (m + 1)]
+        H = sum(th[e] * Sig[e] for e in range(m))
+        psi = expm(-1j * Xs * th[m]) @ (expm(-1j * H) @ psi)
+    assert np.max(np.abs(O.evolve_ex(n, u, v, w, theta) - psi)) < 1e-12
+
+
+def test_P18_ex_qaoa_p1_closed_form():
+    """P18: at p = 1 the P8 closed form holds with the per-edge phase angles gamma_e w_e in place
+    of gamma w (the Heisenberg-picture derivation only uses the products); <Q> keeps w."""
+    rng = np.random.default_rng(182)
+    n = 9
+    u, v = erdos_renyi_graph(n, 0.5, rng)
+    w = rng.uniform(0, 1, len(u))
+    m = len(u)
+    q = O.maxcut_q(n, u, v, w)
+    for _ in range(2):
+        th = rng.uniform(0, math.pi, m + 1)
+        f = O.expectation(O.evolve_ex(n, u, v, w, th), q)
+        ref = _p1_weighted_closed_form(n, u, v, w, 0.0, th[m], gw=list(th[:m] * w))
+        assert f == pytest.approx(ref, abs=1e-12)
