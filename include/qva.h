@@ -114,6 +114,18 @@ qva_status qva_set_qualities_device(qva_plan *plan, const double *q_device, uint
  * indices in [0, n_qubits); w: m weights or NULL for unit weights.  X mixer only. */
 qva_status qva_set_qualities_maxcut(qva_plan *plan, int32_t m, const int32_t *u, const int32_t *v,
                                     const double *w);
+/* On-device generation of the qualities of a permutation-encoded subspace (QWOA, PAPER.md:98-120,
+ * :255-300; readings R23, R24).  Index i of the state holds s_i, the i-th k-permutation of the
+ * elements {0..m-1} in lexicographic order (Lehmer code: digit a has radix m-a), so the plan's dim
+ * must be m!/(m-k)! (else QVA_ERR_SIZE_MISMATCH); and
+ *     q_i = C(s_i) = sum_{a<k} ( lin[a*m + s_a] + sum_{b<k} F[a*k + b] * D[s_a*m + s_b] )
+ * (quadratic assignment; TSP: F = directed cycle; summed a-major in this order, F's zero entries
+ * skipped).  F: k*k row-major or NULL (no quadratic term), at most 400 nonzeros; D: m*m row-major
+ * (required when F is given); lin: k*m or NULL.  1 <= k <= m <= 20, else
+ * QVA_ERR_INVALID_ARGUMENT.  Host arrays, copied.  Any mixer; each rank generates its own
+ * partition.  QVA_ERR_NUMERIC on a non-finite input or result. */
+qva_status qva_set_qualities_permutation(qva_plan *plan, int32_t m, int32_t k, const double *F, const double *D,
+                                         const double *lin);
 
 /* Copy diag(Q) entries [offset, offset+count) (global, this rank's partition, layout of the
  * partition) back to q_out[count]. */

@@ -60,6 +60,7 @@ def _load():
         "qva_set_qualities": [P, P, u64, u64],
         "qva_set_qualities_device": [P, P, u64, u64],
         "qva_set_qualities_maxcut": [P, i32, P, P, P],
+        "qva_set_qualities_permutation": [P, i32, i32, P, P, P],
         "qva_get_qualities": [P, P, u64, u64],
         "qva_set_circulant_eigenvalues": [P, P, u64, u64],
         "qva_set_circulant_eigenvalues_const": [P, d, d],
@@ -260,6 +261,15 @@ class Plan:
         v = np.ascontiguousarray(v, np.int32)
         w = None if w is None else _f64(w)
         _call("qva_set_qualities_maxcut", self._h, len(u), _ptr(u), _ptr(v), _ptr(w))
+
+    def set_qualities_permutation(self, m: int, k: int, F=None, D=None, lin=None):
+        """q_i = C(s_i), s_i the i-th k-permutation of range(m) in lexicographic order,
+        C(s) = sum_a (lin[a, s_a] + sum_b F[a, b] D[s_a, s_b]) (readings R23, R24); generated on
+        the device.  F: (k, k), D: (m, m), lin: (k, m), each optional (D required with F)."""
+        F = None if F is None else _f64(np.asarray(F, np.float64).reshape(k, k))
+        D = None if D is None else _f64(np.asarray(D, np.float64).reshape(m, m))
+        lin = None if lin is None else _f64(np.asarray(lin, np.float64).reshape(k, m))
+        _call("qva_set_qualities_permutation", self._h, int(m), int(k), _ptr(F), _ptr(D), _ptr(lin))
 
     def get_qualities(self, offset: int = 0, count: Optional[int] = None, out: Optional[np.ndarray] = None):
         if count is None:

@@ -2252,6 +2252,93 @@ qva_status qva_set_qualities_maxcut(qva_plan *P, int32_t m, const int32_t *u, co
     return QVA_OK;
 }
 
+qva_status qva_set_qualities_permutation(qva_plan *P, int32_t m, int32_t k, const double *F, const double *D,
+                                         const double *lin) {
+    if (!P || m < 1 || m > kKpermMaxMHost || k < 1 || k > m || (F && !D)) {
+        set_error("qva_set_qualities_permutation: need 1 <= k <= m <= 20 (and D with F)");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    uint64_t total = 1;
+    for (int a = 0; a < k; ++a) total *= (uint64_t)(m - a);  // m!/(m-k)! <= 20! < 2^64
+    if (total != P->N) {
+        set_error("qva_set_qualities_permutation: plan dim " + std::to_string(P->N) + " != m!/(m-k)! = " +
+                  std::to_string(total));
+        return QVA_ERR_SIZE_MISMATCH;
+    }
+    auto finite = [](const double *x, size_t n) {
+        for (size_t i = 0; i < n; ++i)
+            if (!std::isfinite(x[i])) return false;
+        return true;
+    };
+    if ((F && !finite(F, (size_t)k * k)) || (D && !finite(D, (size_t)m * m)) || (lin && !finite(lin, (size_t)k * m))) {
+        set_error("non-finite permutation cost data");
+        return QVA_ERR_NUMERIC;
+    }
+    // pack: cnt[k] u64, D[m*m], lin[k*m], fv[nf] f64, frow[k+1], fab[nf] int
+    std::vector<uint64_t> cnt(k);
+    for (int a = 0; a < k; ++a) {
+        uint64_t c = 1;
+        for (int t = a + 1; t < k; ++t) c *= (uint64_t)(m - t);  // (m-a-1)!/(m-k)!
+        cnt[a] = c;
+    }
+    std::vector<double> fv;
+    std::vector<int> frow(k + 1, 0), fab;
+    for (int a = 0; a < k; ++a) {
+        frow[a] = (int)fv.size();
+        if (F)
+            for (int b = 0; b < k; ++b)
+                if (F[(size_t)a * k + b] != 0.0) {
+                    fv.push_back(F[(size_t)a * k + b]);
+                    fab.push_back(a << 8 | b);
+                }
+    }
+    frow[k] = (int)fv.size();
+    const int nf = (int)fv.size();
+    if (nf > kKpermMaxNfHost) {
+        set_error("qva_set_qualities_permutation: more than 400 nonzero F entries");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    std::vector<unsigned char> pack;
+    auto put = [&](const void *src, size_t n) {
+        const unsigned char *c = (const unsigned char *)src;
+        pack.insert(pack.end(), c, c + n);
+    };
+    put(cnt.data(), cnt.size() * sizeof(uint64_t));
+    std::vector<double> Dv(D ? D : nullptr, D ? D + (size_t)m * m : nullptr);
+    Dv.resize((size_t)m * m, 0.0);
+    put(Dv.data(), Dv.size() * sizeof(double));
+    if (lin) put(lin, (size_t)k * m * sizeof(double));
+    put(fv.data(), fv.size() * sizeof(double));
+    put(frow.data(), frow.size() * sizeof(int));
+    put(fab.data(), fab.size() * sizeof(int));
+    DeviceGuard dg(P->device);
+    void *dpack = nullptr;
+    QVA_CUDA_TRY(scratch_get(P, &dpack, pack.size()));
+    QVA_TRY(upload(P, dpack, pack.data(), pack.size()));
+    {
+        ProfScope ps(P, K_OTHER, 8.0 * P->local_n);
+        QVA_CUDA_TRY(launch_kperm_q(P->q, P->local_n, P->offset, m, k, dpack, nf, lin != nullptr, P->stream));
+    }
+    P->q_graph = false;  // the whole partition is overwritten
+    P->q_dev_valid = true;
+    QVA_CUDA_TRY(cudaMemsetAsync(P->d_flag, 0, sizeof(int), P->stream));
+    QVA_CUDA_TRY(launch_check_finite(P->q, P->local_n, P->d_flag, P->stream));
+    int flag = 0;
+    QVA_CUDA_TRY(cudaMemcpyAsync(&flag, P->d_flag, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
+    QVA_TRY(sync(P));
+    P->qB_valid = false;
+    P->q_classified = false;
+    P->q_mode = 0;
+    drop_qt(P);
+    if (flag) {
+        P->q_set = false;
+        set_error("non-finite permutation quality (overflow)");
+        return QVA_ERR_NUMERIC;
+    }
+    P->q_set = true;
+    return QVA_OK;
+}
+
 
 qva_status qva_get_qualities(qva_plan *P, double *q_out, uint64_t offset, uint64_t count) {
     if (!P || (!q_out && count)) return QVA_ERR_INVALID_ARGUMENT;

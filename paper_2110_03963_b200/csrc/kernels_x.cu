@@ -209,6 +209,70 @@ __global__ void maxcut_q_kernel(double *q, uint64_t count, uint64_t offset, int 
     }
 }
 
+// Permutation-subspace qualities (readings R23, R24): rank r -> the r-th
+// k-permutation s of {0..m-1} in lexicographic order (Lehmer digits d_a = r / cnt[a] with
+// cnt[a] = (m-a-1)!/(m-k)!, each picking the d_a-th smallest unused element), then
+// q_r = sum_a ( Cl[a][s_a] + sum_b F[a][b] D[s_a][s_b] ) in that order (zero F terms skipped:
+// adding +0.0 is exact).  s lives in two 64-bit words, 5 bits per slot (k <= 24), so the thread
+// stays in registers.  A one-off setup kernel: integer-division bound, not on the step path.
+struct KpermArgs {
+    int m, k, nf;            // elements, slots, nonzero F entries
+    const uint64_t *cnt;     // [k]
+    const double *D;         // [m][m]
+    const double *Cl;        // [k][m] or nullptr
+    const int *fab;          // [nf] (a << 8 | b), a-major
+    const double *fv;        // [nf]
+    const int *frow;         // [k + 1] start of row a in (fab, fv)
+};
+constexpr int kKpermMaxM = 20, kKpermMaxNf = 400;
+__global__ void kperm_q_kernel(double *q, uint64_t count, uint64_t offset, KpermArgs a) {
+    __shared__ double sD[kKpermMaxM * kKpermMaxM], sC[kKpermMaxM * kKpermMaxM], sF[kKpermMaxNf];
+    __shared__ unsigned short sFab[kKpermMaxNf];
+    __shared__ uint64_t sCnt[kKpermMaxM];
+    __shared__ int sRow[kKpermMaxM + 1];
+    for (int i = threadIdx.x; i < a.m * a.m; i += blockDim.x) sD[i] = a.D[i];
+    for (int i = threadIdx.x; i < a.k * a.m; i += blockDim.x) sC[i] = a.Cl ? a.Cl[i] : 0.0;
+    for (int i = threadIdx.x; i < a.nf; i += blockDim.x) {
+        sF[i] = a.fv[i];
+        sFab[i] = (unsigned short)a.fab[i];
+    }
+    for (int i = threadIdx.x; i < a.k; i += blockDim.x) sCnt[i] = a.cnt[i];
+    for (int i = threadIdx.x; i <= a.k; i += blockDim.x) sRow[i] = a.frow[i];
+    __syncthreads();
+    const bool lin = a.Cl != nullptr;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t r = offset + i;
+        uint32_t used = 0;
+        uint64_t w0 = 0, w1 = 0;  // slot a < 12 in w0, else w1 (5 bits each)
+        for (int s = 0; s < a.k; ++s) {
+            const uint64_t c = sCnt[s];
+            const uint64_t d = r / c;
+            r -= d * c;
+            // the d-th (0-based) element of {0..m-1} not yet used
+            uint32_t free = ~used & ((1u << a.m) - 1u);
+            for (uint64_t t = 0; t < d; ++t) free &= free - 1u;
+            const int e = __ffs(free) - 1;
+            used |= 1u << e;
+            if (s < 12) w0 |= (uint64_t)e << (5 * s);
+            else w1 |= (uint64_t)e << (5 * (s - 12));
+        }
+        auto slot = [&](int s) -> int {
+            return (int)(((s < 12 ? w0 >> (5 * s) : w1 >> (5 * (s - 12)))) & 31u);
+        };
+        double acc = 0.0;
+        for (int s = 0; s < a.k; ++s) {
+            const int ea = slot(s);
+            if (lin) acc += sC[s * a.m + ea];
+            for (int f = sRow[s]; f < sRow[s + 1]; ++f) {
+                const int b = sFab[f] & 255;
+                acc += sF[f] * sD[ea * a.m + slot(b)];
+            }
+        }
+        q[i] = acc;
+    }
+}
+
 template <typename T>
 __global__ void chunk_transpose_kernel(T *out, const T *in, int G, uint64_t C) {
     uint64_t total = (uint64_t)G * G * C;
@@ -327,6 +391,31 @@ cudaError_t launch_small_evolve(const SmallEvolveParams &p, int batch, cudaStrea
 cudaError_t launch_maxcut_q(double *q, uint64_t count, uint64_t offset, int m, const int32_t *u,
                             const int32_t *v, const double *w, cudaStream_t s) {
     maxcut_q_kernel<<<grid_for(count, 256), 256, 0, s>>>(q, count, offset, m, u, v, w);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_kperm_q(double *q, uint64_t count, uint64_t offset, int m, int k, const void *dev_pack, int nf,
+                           bool linear, cudaStream_t s) {
+    // dev_pack layout (packed by qva_set_qualities_permutation): cnt[k] u64, D[m*m], Cl[k*m] (if
+    // linear), fv[nf] doubles, then frow[k+1], fab[nf] ints
+    if (m < 1 || m > kKpermMaxM || k < 1 || k > m || nf > kKpermMaxNf) return cudaErrorInvalidValue;
+    const unsigned char *b = (const unsigned char *)dev_pack;
+    KpermArgs a;
+    a.m = m;
+    a.k = k;
+    a.nf = nf;
+    a.cnt = (const uint64_t *)b;
+    const double *d = (const double *)(b + sizeof(uint64_t) * k);
+    a.D = d;
+    d += m * m;
+    a.Cl = linear ? d : nullptr;
+    if (linear) d += k * m;
+    a.fv = d;
+    d += nf;
+    a.frow = (const int *)d;
+    a.fab = a.frow + k + 1;
+    if (count == 0) return cudaSuccess;
+    kperm_q_kernel<<<grid_for(count, 256), 256, 0, s>>>(q, count, offset, a);
     return cudaGetLastError();
 }
 

@@ -202,6 +202,11 @@ cudaError_t launch_small_evolve(const SmallEvolveParams &p, int batch, cudaStrea
 // qualities generator q_x = -cut_w(x) over [0, count) with global index offset + i
 cudaError_t launch_maxcut_q(double *q, uint64_t count, uint64_t offset, int m, const int32_t *u,
                             const int32_t *v, const double *w, cudaStream_t s);
+// permutation-subspace qualities (R23, R24) over [0, count) with global rank offset + i;
+// dev_pack: cnt[k] u64, D[m*m], Cl[k*m] (linear), fv[nf] f64, frow[k+1], fab[nf] int (a << 8 | b)
+constexpr int kKpermMaxMHost = 20, kKpermMaxNfHost = 400;
+cudaError_t launch_kperm_q(double *q, uint64_t count, uint64_t offset, int m, int k, const void *dev_pack, int nf,
+                           bool linear, cudaStream_t s);
 // block transpose of G x G chunks of C elements: out[t][r] = in[r][t]
 template <typename T>
 cudaError_t launch_chunk_transpose(T *out, const T *in, int G, uint64_t C, cudaStream_t s);

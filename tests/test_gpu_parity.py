@@ -597,3 +597,87 @@ def test_error_paths(Q):
         with pytest.raises(Q.QvaError) as ei:
             P.evolve([0.1, float("inf")])
         assert ei.value.status == 4
+
+
+# ---------------------------------------------------------------- permutation subspaces (NEXT-1) ----
+def _kperm_inputs(m, k, seed, tsp=False, linear=True):
+    rng = np.random.default_rng(seed)
+    D = rng.uniform(0, 10, (m, m))
+    if tsp:
+        F = np.zeros((k, k))
+        for a in range(k):
+            F[a, (a + 1) % k] = 1.0
+    else:
+        F = rng.uniform(-1, 1, (k, k)) * (rng.uniform(0, 1, (k, k)) < 0.5)
+    C = rng.uniform(-5, 5, (k, m)) if linear else None
+    return F, D, C
+
+
+@pytest.mark.parametrize("m,k,tsp,linear,sample", [(3, 3, True, False, None), (8, 8, True, False, None),
+                                                   (9, 6, False, True, None), (7, 2, False, True, None),
+                                                   (10, 10, True, True, 3000), (12, 12, True, False, 400),
+                                                   (14, 7, False, True, 1500)])
+def test_kperm_qualities_vs_oracle(Q, m, k, tsp, linear, sample):
+    """On-device permutation-subspace qualities (R23, R24) against the oracle's unranking + cost,
+    every rank for small subspaces, else sampled ranks (first, last and random)."""
+    F, D, C = _kperm_inputs(m, k, 100 * m + k, tsp, linear)
+    N = math.perm(m, k)
+    with Q.Plan(N, "circulant") as P:
+        P.set_qualities_permutation(m, k, F, D, C)
+        q = P.get_qualities()
+    if sample is None:
+        ranks = np.arange(N)
+    else:
+        rng = np.random.default_rng(7)
+        ranks = np.unique(np.r_[0, 1, N - 1, N // 2, rng.integers(0, N, sample)])
+    ref = O.kperm_qualities(m, k, F, D, C, ranks=ranks)
+    scale = np.abs(F).sum() * np.abs(D).max() + (np.abs(C).sum() if C is not None else 0.0)
+    assert np.max(np.abs(q[ranks] - ref)) <= 1e-13 * scale
+
+
+def test_kperm_qwoa_evolve_vs_oracle(Q):
+    """QWOA over the 8! tours of a random asymmetric TSP: generated q, complete-graph mixer, the
+    whole state against the oracle (q from the oracle's own unranking)."""
+    m = k = 8
+    F, D, C = _kperm_inputs(m, k, 808, tsp=True, linear=False)
+    N = math.perm(m, k)
+    q = O.kperm_qualities(m, k, F, D, C)
+    theta = np.random.default_rng(9).uniform(0, math.pi, 6) * np.array([0.05, 1, 0.05, 1, 0.05, 1])
+    ref = O.evolve_complete(q, theta, 0.0, float(N))
+    for G in (1, 4):
+        with Q.Plan(N, "circulant", virtual_shards=G) as P:
+            P.set_qualities_permutation(m, k, F, D)
+            P.set_circulant_eigenvalues_const(0.0, float(N))
+            P.evolve(theta)
+            _amp_close(P.get_state(), ref)
+            _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+
+
+def test_kperm_errors(Q):
+    """Argument checks of qva_set_qualities_permutation; 120 = 5!/0! = 5!/1! = 6*5*4 all fit."""
+    F, D, C = _kperm_inputs(5, 5, 1)
+    with Q.Plan(120, "circulant") as P:
+        with pytest.raises(Q.QvaError) as ei:
+            P.evolve([0.1, 0.2])  # no qualities yet
+        assert ei.value.status == 3  # NOT_READY
+        with pytest.raises(Q.QvaError) as ei:
+            P.set_qualities_permutation(4, 4, np.zeros((4, 4)), np.zeros((4, 4)))  # 24 != 120
+        assert ei.value.status == 2  # SIZE_MISMATCH
+        with pytest.raises(Q.QvaError) as ei:
+            P.set_qualities_permutation(5, 6, np.zeros((6, 6)), D)
+        assert ei.value.status == 1  # INVALID_ARGUMENT (k > m)
+        with pytest.raises(Q.QvaError) as ei:
+            P.set_qualities_permutation(21, 1, None, None, np.zeros((1, 21)))
+        assert ei.value.status == 1  # m > 20
+        Dn = D.copy()
+        Dn[1, 2] = np.inf
+        with pytest.raises(Q.QvaError) as ei:
+            P.set_qualities_permutation(5, 5, F, Dn)
+        assert ei.value.status == 4  # NUMERIC
+        for (m, k) in [(5, 5), (5, 4), (6, 3)]:
+            F2, D2, C2 = _kperm_inputs(m, k, m + k)
+            P.set_qualities_permutation(m, k, F2, D2, C2)
+            np.testing.assert_allclose(P.get_qualities(), O.kperm_qualities(m, k, F2, D2, C2), rtol=0, atol=1e-12)
+        P.set_qualities_permutation(5, 5, None, None, C)  # assignment problem: linear term only
+        np.testing.assert_allclose(P.get_qualities(), O.kperm_qualities(5, 5, np.zeros((5, 5)), D, C), rtol=0,
+                                   atol=1e-12)
