@@ -183,6 +183,18 @@ qva_status qva_get_probabilities(qva_plan *plan, double *out, uint64_t offset, u
  * all B values.  The current state afterwards is unspecified.  B <= desc.max_batch. */
 qva_status qva_evolve_batch(qva_plan *plan, const double *thetas, int32_t B, int32_t p, double *f_out);
 
+/* ex-QAOA (Eqs. phase_shift_qaoa_ex and qaoa_ex; reading R25) on a plan whose
+ * qualities are a max-cut graph (qva_set_qualities_maxcut, m edges; X or parity mixer):
+ * theta[(m+1)*p] = per layer [gamma_{i,1}, ..., gamma_{i,m}, t_i]; layer i applies
+ * prod_e exp(-i gamma_{i,e} Sigma_e), Sigma_e(x) = -w_e [bit_u(x) != bit_v(x)] (the edge terms of
+ * q = -cut_w, so equal gammas give qva_evolve), then the mixer U(t_i); layer 1 first.  Restarts from
+ * psi0; <Q> (the plan's q) as after qva_evolve.  QVA_ERR_NOT_READY without a max-cut graph. */
+qva_status qva_evolve_ex(qva_plan *plan, const double *theta, int32_t p);
+/* B ex-QAOA parameter sets thetas[B][(m+1)*p] -> f_out[B] (members one after another; with world
+ * > 1 in replicated mode the members are split across ranks).  The state afterwards is
+ * unspecified. */
+qva_status qva_evolve_ex_batch(qva_plan *plan, const double *thetas, int32_t B, int32_t p, double *f_out);
+
 /* ---- NCCL bootstrap (multi-process) ------------------------------------------------------------- */
 
 /* Writes a 128-byte ncclUniqueId into id_out (call on rank 0, broadcast to the other ranks). */

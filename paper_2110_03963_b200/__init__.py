@@ -77,6 +77,8 @@ def _load():
         "qva_get_state": [P, P, u64, u64],
         "qva_get_probabilities": [P, P, u64, u64],
         "qva_evolve_batch": [P, P, i32, i32, P],
+        "qva_evolve_ex": [P, P, i32],
+        "qva_evolve_ex_batch": [P, P, i32, i32, P],
         "qva_nccl_unique_id": [P],
         "qva_batch_partition": [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)],
         "qva_exchange_plan": [i32, i32, P, P],
@@ -261,6 +263,7 @@ class Plan:
         v = np.ascontiguousarray(v, np.int32)
         w = None if w is None else _f64(w)
         _call("qva_set_qualities_maxcut", self._h, len(u), _ptr(u), _ptr(v), _ptr(w))
+        self._n_edges = len(u)
 
     def set_qualities_permutation(self, m: int, k: int, F=None, D=None, lin=None):
         """q_i = C(s_i), s_i the i-th k-permutation of range(m) in lexicographic order,
@@ -351,6 +354,25 @@ class Plan:
         B, P2 = thetas.shape
         out = np.empty(B, np.float64)
         _call("qva_evolve_batch", self._h, _ptr(thetas), B, P2 // 2, _ptr(out))
+        return out
+
+    def evolve_ex(self, theta):
+        """ex-QAOA (PAPER.md Eq. qaoa_ex, R25): theta = per layer [gamma_{i,1..m}, t_i] over the
+        m edges of the max-cut graph set by set_qualities_maxcut."""
+        theta = _f64(theta)
+        m1 = getattr(self, "_n_edges", 0) + 1
+        if theta.size % m1:
+            raise ValueError(f"ex-QAOA theta length {theta.size} is not a multiple of m + 1 = {m1}")
+        _call("qva_evolve_ex", self._h, _ptr(theta), theta.size // m1)
+
+    def evolve_ex_batch(self, thetas) -> np.ndarray:
+        thetas = np.ascontiguousarray(thetas, np.float64)
+        B, T = thetas.shape
+        m1 = getattr(self, "_n_edges", 0) + 1
+        if T % m1:
+            raise ValueError(f"ex-QAOA theta length {T} is not a multiple of m + 1 = {m1}")
+        out = np.empty(B, np.float64)
+        _call("qva_evolve_ex_batch", self._h, _ptr(thetas), B, T // m1, _ptr(out))
         return out
 
     # ---- introspection

@@ -463,9 +463,17 @@ struct qva_plan {
     bool g_unit = true;
     std::vector<int> g_u, g_v;
     std::vector<double> g_w;
+    // ex-QAOA (R25): during one tile-path evolution, the per-layer phase weights
+    // gamma_{i,e} w_e ([p][g_m], host); phase passes then use records of those weights
+    const double *ex_w = nullptr;
+    double *q_ex = nullptr;                // step path: per-layer generated term sum
+    void *d_ex_edges = nullptr;            // step path: u, v, per-layer weights
+    size_t ex_edge_cap = 0;
     struct GenEntry {
         std::vector<int> key;
         int group, mode;
+        int wset = -1;                     // -1: the plan's weights; i: ex-QAOA layer i
+        std::vector<double> wsig;          // ex-QAOA: the weights the records were built from
         void *rec, *thr, *G;
         size_t rec_bytes;
         std::vector<double> thr_h, G_h;   // host staging (kept alive with the entry)
@@ -1012,7 +1020,7 @@ bool use_qgen(const qva_plan *P) {
 
 // q path of a tile-pass sequence: generated integer / fp64 records, or 0 (stored q)
 int qgen_mode(const qva_plan *P, int batch) {
-    const bool gen_int = P->g_unit && P->g_m <= kGenIntMaxEdges;
+    const bool gen_int = P->g_unit && P->g_m <= kGenIntMaxEdges && !P->ex_w;  // ex weights are real
     const bool f64_ok = batch <= kGfMembersHost || P->L >= kGenF64MinQubits || P->d.reserved[1] != 0;
     return use_qgen(P) && (gen_int || f64_ok) ? (gen_int ? kQGenInt : kQGenF64) : 0;
 }
@@ -1050,12 +1058,24 @@ void pass_layout(const qva_plan *P, const PassPlan &pp, int n_phys, std::vector<
 
 // per-tile records + per-thread constants of the generated q for one pass shape (cached)
 qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan &pp, int n_phys, int gq, int mode,
-                      const TilePassParams &tp, const qva_plan::GenEntry **out) {
-    for (auto &e : P->gen_cache)
-        if (e.key == qkey && e.group == gq && e.mode == mode) {
-            *out = &e;
-            return QVA_OK;
+                      const TilePassParams &tp, int wset, const qva_plan::GenEntry **out) {
+    // wset >= 0: ex-QAOA layer wset, whose weights change with theta (entries are rebuilt when
+    // they differ; stream order makes reusing the buffers safe)
+    const double *wts = (wset >= 0 && P->ex_w) ? P->ex_w + (size_t)wset * P->g_m : nullptr;
+    for (size_t i = 0; i < P->gen_cache.size(); ++i) {
+        auto &e = P->gen_cache[i];
+        if (e.key == qkey && e.group == gq && e.mode == mode && e.wset == (wts ? wset : -1)) {
+            if (!wts || std::equal(e.wsig.begin(), e.wsig.end(), wts)) {
+                *out = &e;
+                return QVA_OK;
+            }
+            pool_put(P, e.rec, e.rec_bytes);
+            pool_put(P, e.thr, 128 * 8 * sizeof(double));
+            pool_put(P, e.G, 32 * sizeof(double));
+            P->gen_cache.erase(P->gen_cache.begin() + i);
+            break;
         }
+    }
     std::vector<int> lay;
     uint64_t cmask, cval;
     pass_layout(P, pp, n_phys, lay, cmask, cval);
@@ -1091,7 +1111,7 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
         }
     }
     gp.const_val = cval;
-    gp.w_unit = P->g_unit ? 1 : 0;
+    gp.w_unit = (P->g_unit && !wts) ? 1 : 0;
     // classify the edges (self-loops never cut)
     std::vector<int2> tt, tb;
     std::vector<double> ttw, tbw;
@@ -1103,7 +1123,7 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
     for (int e = 0; e < P->g_m; ++e) {
         const int u = P->g_u[e], v = P->g_v[e];
         if (u == v) continue;
-        const double w = P->g_unit ? 1.0 : P->g_w[e];
+        const double w = wts ? wts[e] : (P->g_unit ? 1.0 : P->g_w[e]);
         const int ku = in_tile[u], kv = in_tile[v];
         if (ku < 0 && kv < 0) {
             tt.push_back(make_int2(u, v));
@@ -1125,6 +1145,8 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
     ent.key = qkey;
     ent.group = gq;
     ent.mode = mode;
+    ent.wset = wts ? wset : -1;
+    if (wts) ent.wsig.assign(wts, wts + P->g_m);
     ent.rec = ent.thr = ent.G = nullptr;
     ent.rec_bytes = n_tiles * rec_bytes;
     QVA_CUDA_TRY(pool_get(P, &ent.rec, ent.rec_bytes));
@@ -1133,6 +1155,8 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
     const size_t eb = (tt.size() + tb.size()) * (sizeof(int2) + sizeof(double)) + 16;
     if (P->gen_edge_cap < eb) {  // stream order keeps one staging buffer safe across entries
         cudaFree(P->d_gen_edges);
+    cudaFree(P->q_ex);
+    cudaFree(P->d_ex_edges);
         P->d_gen_edges = nullptr;
         QVA_CUDA_TRY(cudaMalloc(&P->d_gen_edges, eb));
         P->gen_edge_cap = eb;
@@ -1440,7 +1464,11 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         build_steps(pp, tp, pref, half1[j], half2[j]);
         if (needs_q && gen) {
             const qva_plan::GenEntry *ge = nullptr;
-            QVA_TRY(ensure_gen(P, qkey, pp, n_phys, tp.gq, gen, tp, &ge));
+            if (P->ex_w && pp.phase >= 0 && pp.expect) {
+                set_error("internal: ex-QAOA phase and <Q> in one pass");
+                return QVA_ERR_UNSUPPORTED;
+            }
+            QVA_TRY(ensure_gen(P, qkey, pp, n_phys, tp.gq, gen, tp, (P->ex_w && pp.phase >= 0) ? pp.phase : -1, &ge));
             tp.qt = ge->rec;
             tp.gen_thr = ge->thr;
             tp.gen_G = ge->G;
@@ -2001,6 +2029,8 @@ qva_status qva_plan_destroy(qva_plan *P) {
     cudaFree(P->d_mult);
     cudaFree(P->d_edges);
     cudaFree(P->d_gen_edges);
+    cudaFree(P->q_ex);
+    cudaFree(P->d_ex_edges);
     cudaFree(P->scratch);
     cudaFree(P->small_batch);
     for (auto &e : P->pool) cudaFree(e.second);
@@ -2548,6 +2578,45 @@ qva_status qva_apply_mixer(qva_plan *P, double beta) {
     return sync(P);
 }
 
+// X-mixer evolution through the tile passes (permuted or in-place schedule); graph: allow CUDA
+// graph replay of the single-shard sequence
+static qva_status x_tile_evolve(qva_plan *P, const double *theta, int p, bool graph, bool *have_red) {
+    P->layout = 0;
+    P->perm.clear();
+    if (p == 0) {
+        QVA_TRY(reset_state(P));
+        return QVA_OK;
+    }
+    if (use_permuted(P)) {
+        if (!P->psi_alt && cudaMalloc(&P->psi_alt, P->arr_n * sizeof(double2)) != cudaSuccess) {
+            cudaGetLastError();
+            P->perm_failed = true;  // no room for the ping-pong buffer: in-place schedule
+        }
+    }
+    if (use_permuted(P)) {
+        // the schedule depends on (L, p) only: planned once per p (host planning off the step path)
+        auto it = P->perm_sched.find(p);
+        if (it == P->perm_sched.end()) {
+            std::vector<int> fin;
+            auto passes = perm_passes(P->L, p, &fin);
+            if (passes.empty() || !passes.back().expect) {
+                set_error("internal: permuted schedule did not complete");
+                return QVA_ERR_UNSUPPORTED;
+            }
+            it = P->perm_sched.emplace(p, std::make_pair(std::move(passes), std::move(fin))).first;
+        }
+        QVA_TRY(graph ? run_passes_graph(P, it->second.first, theta, p, P->has_psi0 ? 2 : 1)
+                      : run_passes(P, it->second.first, theta, p, 1, P->psi, 0, P->has_psi0 ? 2 : 1, nullptr));
+        P->perm = it->second.second;
+        *have_red = true;
+        return QVA_OK;
+    }
+    auto passes = cut_passes(evolve_tokens(P->L, P->gbits, p), P->sets, true);
+    QVA_TRY(run_passes(P, passes, theta, p, 1, P->psi, 0, P->has_psi0 ? 2 : 1, nullptr));
+    *have_red = true;
+    return QVA_OK;
+}
+
 // one full evolution of the plan's own state; on return P->red holds (f, norm) (local sums)
 static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *have_red) {
     *have_red = false;
@@ -2572,38 +2641,7 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
             *have_red = true;
             return QVA_OK;
         }
-        P->layout = 0;
-        P->perm.clear();
-        if (p == 0) {
-            QVA_TRY(reset_state(P));
-            return QVA_OK;
-        }
-        if (use_permuted(P)) {
-            if (!P->psi_alt && cudaMalloc(&P->psi_alt, P->arr_n * sizeof(double2)) != cudaSuccess) {
-                cudaGetLastError();
-                P->perm_failed = true;  // no room for the ping-pong buffer: in-place schedule
-            }
-        }
-        if (use_permuted(P)) {
-            // the schedule depends on (L, p) only: planned once per p (host planning off the step path)
-            auto it = P->perm_sched.find(p);
-            if (it == P->perm_sched.end()) {
-                std::vector<int> fin;
-                auto passes = perm_passes(P->L, p, &fin);
-                if (passes.empty() || !passes.back().expect) {
-                    set_error("internal: permuted schedule did not complete");
-                    return QVA_ERR_UNSUPPORTED;
-                }
-                it = P->perm_sched.emplace(p, std::make_pair(std::move(passes), std::move(fin))).first;
-            }
-            QVA_TRY(run_passes_graph(P, it->second.first, theta, p, P->has_psi0 ? 2 : 1));
-            P->perm = it->second.second;
-            *have_red = true;
-            return QVA_OK;
-        }
-        auto passes = cut_passes(evolve_tokens(P->L, P->gbits, p), P->sets, true);
-        QVA_TRY(run_passes(P, passes, theta, p, 1, P->psi, 0, P->has_psi0 ? 2 : 1, nullptr));
-        *have_red = true;
+        QVA_TRY(x_tile_evolve(P, theta, p, true, have_red));
         return QVA_OK;
     }
     if (P->mixer == QVA_MIXER_CIRCULANT) {
@@ -2696,6 +2734,78 @@ qva_status qva_evolve(qva_plan *P, const double *theta, int32_t p) {
         return QVA_OK;
     }
     return sync(P);
+}
+
+// ---- ex-QAOA (Eqs. phase_shift_qaoa_ex / qaoa_ex; reading R25) -------------
+// theta = per layer [gamma_{i,1..m}, t_i].  Layer i's phase prod_e exp(-i gamma_{i,e} Sigma_e) with
+// Sigma_e = -w_e [x_u != x_v] is exp(+i cut_{w'}) for the per-layer weights w'_e = gamma_{i,e} w_e,
+// i.e. the generated max-cut phase with gamma = 1: the tile passes build per-layer records of w'
+// (the <Q> pass keeps the plan's w).  Other plans (small, parity mixer, shards whose phase and <Q>
+// share a pass) take the step path: generate -cut_{w'} per layer, phase with gamma = 1, mixer.
+static qva_status ex_impl(qva_plan *P, const double *theta, int p, bool *have_red) {
+    *have_red = false;
+    const int m = P->g_m;
+    std::vector<double> wx((size_t)p * m), th2(2 * (size_t)p);
+    for (int i = 0; i < p; ++i) {
+        const double *t = theta + (size_t)i * (m + 1);
+        for (int e = 0; e < m; ++e) wx[(size_t)i * m + e] = t[e] * (P->g_unit ? 1.0 : P->g_w[e]);
+        th2[2 * i] = 1.0;
+        th2[2 * i + 1] = t[m];
+    }
+    bool tile = P->mixer == QVA_MIXER_X && !use_small(P) && use_qgen(P) && p > 0;
+    if (tile && !use_permuted(P)) {
+        auto passes = cut_passes(evolve_tokens(P->L, P->gbits, p), P->sets, true);
+        for (auto &pp : passes)
+            if (pp.phase >= 0 && pp.expect) tile = false;
+    }
+    if (tile) {
+        P->ex_w = wx.data();
+        qva_status st = x_tile_evolve(P, th2.data(), p, false, have_red);
+        P->ex_w = nullptr;
+        return st;
+    }
+    QVA_TRY(reset_state(P));
+    if (p == 0) return QVA_OK;
+    const size_t need = (size_t)std::max(m, 1) * 2 * sizeof(int32_t) + wx.size() * sizeof(double) + 16;
+    if (P->ex_edge_cap < need) {
+        cudaFree(P->d_ex_edges);
+        P->d_ex_edges = nullptr;
+        QVA_CUDA_TRY(cudaMalloc(&P->d_ex_edges, need));
+        P->ex_edge_cap = need;
+    }
+    if (!P->q_ex) QVA_CUDA_TRY(cudaMalloc(&P->q_ex, P->arr_n * sizeof(double)));
+    int32_t *du = (int32_t *)P->d_ex_edges, *dv = du + std::max(m, 1);
+    double *dw = (double *)((unsigned char *)P->d_ex_edges + (((size_t)std::max(m, 1) * 2 * sizeof(int32_t) + 15) & ~15ull));
+    if (m) {
+        QVA_TRY(upload(P, du, P->g_u.data(), m * sizeof(int32_t)));
+        QVA_TRY(upload(P, dv, P->g_v.data(), m * sizeof(int32_t)));
+        QVA_TRY(upload(P, dw, wx.data(), wx.size() * sizeof(double)));
+    }
+    for (int i = 0; i < p; ++i) {
+        QVA_TRY(to_layout_A(P));  // the generated term sum is in natural (partition) order
+        {
+            ProfScope ps(P, K_OTHER, 8.0 * P->arr_n);
+            QVA_CUDA_TRY(launch_maxcut_q(P->q_ex, P->arr_n, P->offset, m, du, dv, dw + (size_t)i * m, P->stream));
+        }
+        {
+            ProfScope ps(P, K_OTHER, 40.0 * P->arr_n);
+            QVA_CUDA_TRY(launch_phase(P->psi, P->q_ex, P->arr_n, 1.0, P->stream));
+        }
+        QVA_TRY(apply_mixer_impl(P, th2[2 * i + 1]));
+    }
+    return QVA_OK;
+}
+
+static qva_status ex_check(qva_plan *P, const double *theta, size_t n_theta) {
+    if (!P->q_set || !P->q_graph) {
+        set_error("ex-QAOA needs the max-cut graph (qva_set_qualities_maxcut): its terms are the edges");
+        return QVA_ERR_NOT_READY;
+    }
+    if (P->mixer != QVA_MIXER_X && P->mixer != QVA_MIXER_PARITY) {
+        set_error("ex-QAOA: qubit (X / parity mixer) plans only");
+        return QVA_ERR_UNSUPPORTED;
+    }
+    return check_theta(theta, n_theta);
 }
 
 static qva_status expect_now(qva_plan *P) {
@@ -2850,6 +2960,55 @@ static qva_status batch_local(qva_plan *P, const double *thetas, int first, int 
         }
         f_out[i] = pair[0];
     }
+    return QVA_OK;
+}
+
+qva_status qva_evolve_ex(qva_plan *P, const double *theta, int32_t p) {
+    if (!P || p < 0 || (p > 0 && !theta)) return QVA_ERR_INVALID_ARGUMENT;
+    QVA_TRY(ex_check(P, theta, (size_t)p * (P->g_m + 1)));
+    DeviceGuard dg(P->device);
+    P->expect_valid = false;
+    bool have = false;
+    QVA_TRY(ex_impl(P, theta, p, &have));
+    if (have) {
+        double pair[2];
+        QVA_CUDA_TRY(cudaMemcpyAsync(pair, P->red, sizeof(pair), cudaMemcpyDeviceToHost, P->stream));
+        QVA_TRY(sync(P));
+        if (!P->replicated) QVA_TRY(allreduce_host(P, pair, 2));
+        P->expect_val = pair[0];
+        P->norm_val = pair[1];
+        P->expect_valid = true;
+        return QVA_OK;
+    }
+    return sync(P);
+}
+
+qva_status qva_evolve_ex_batch(qva_plan *P, const double *thetas, int32_t B, int32_t p, double *f_out) {
+    if (!P || B < 0 || p < 0 || (B > 0 && (!thetas || !f_out))) return QVA_ERR_INVALID_ARGUMENT;
+    const size_t per = (size_t)p * (P->g_m + 1);
+    QVA_TRY(ex_check(P, thetas, (size_t)B * per));
+    DeviceGuard dg(P->device);
+    P->expect_valid = false;
+    std::vector<double> f((size_t)B, 0.0);
+    int32_t first = 0, cnt = B;
+    if (P->replicated && P->world > 1) QVA_TRY(qva_batch_partition(B, P->world, P->rank, &first, &cnt));
+    for (int i = first; i < first + cnt; ++i) {  // members one after another on the plan's state
+        bool have = false;
+        QVA_TRY(ex_impl(P, thetas + (size_t)i * per, p, &have));
+        double pair[2];
+        if (have) {
+            QVA_CUDA_TRY(cudaMemcpyAsync(pair, P->red, sizeof(pair), cudaMemcpyDeviceToHost, P->stream));
+            QVA_TRY(sync(P));
+        } else {
+            QVA_TRY(to_natural_perm(P));
+            QVA_TRY(ensure_q_dev(P));
+            if (P->layout == 1) QVA_TRY(ensure_qB(P));
+            QVA_TRY(expect_generic(P, P->psi, P->arr_n, q_current(P), pair));
+        }
+        f[i] = pair[0];
+    }
+    if (P->world > 1) QVA_TRY(allreduce_host(P, f.data(), B));  // replicated: disjoint members; sharded: partial sums
+    std::copy(f.begin(), f.end(), f_out);
     return QVA_OK;
 }
 

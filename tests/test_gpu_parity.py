@@ -681,3 +681,90 @@ def test_kperm_errors(Q):
         P.set_qualities_permutation(5, 5, None, None, C)  # assignment problem: linear term only
         np.testing.assert_allclose(P.get_qualities(), O.kperm_qualities(5, 5, np.zeros((5, 5)), D, C), rtol=0,
                                    atol=1e-12)
+
+
+# ---------------------------------------------------------------- ex-QAOA (NEXT-4 item) ----
+def _ex_theta(m, p, rng):
+    return rng.uniform(0, math.pi, (m + 1) * p)
+
+
+@pytest.mark.parametrize("n,p,weighted,G", [(8, 2, True, 1), (12, 1, False, 1), (16, 2, True, 1), (16, 3, False, 1),
+                                            (22, 2, False, 1), (22, 2, True, 1), (16, 2, True, 4), (13, 2, False, 2)])
+def test_ex_qaoa_vs_oracle(Q, n, p, weighted, G):
+    """ex-QAOA (PAPER.md Eq. qaoa_ex, R25) against the oracle's term-by-term phases: small-state
+    step path (n <= 12), tile passes with per-layer records of the weights gamma_{i,e} w_e
+    (in-place n = 16, permuted n = 22), virtual shards (G = 4 tile path with exchanges; n = 13,
+    G = 2: phase and <Q> share a pass, so the step path)."""
+    rng = np.random.default_rng(1000 + n + p + G)
+    u, v = random_regular_graph(n, 3, rng) if n % 2 == 0 else erdos_renyi_graph(n, 0.3, rng)
+    w = rng.uniform(0, 1, len(u)) if weighted else None
+    theta = _ex_theta(len(u), p, rng)
+    ref = O.evolve_ex(n, u, v, w, theta)
+    q = O.maxcut_q(n, u, v, w)
+    with Q.Plan(1 << n, "x", n_qubits=n, virtual_shards=G) as P:
+        P.set_qualities_maxcut(u, v, w)
+        P.evolve_ex(theta)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+        _amp_close(P.get_state(), ref)
+        # a second theta rebuilds the per-layer records
+        theta2 = _ex_theta(len(u), p, rng)
+        P.evolve_ex(theta2)
+        ref2 = O.evolve_ex(n, u, v, w, theta2)
+        _amp_close(P.get_state(), ref2)
+
+
+def test_ex_qaoa_equal_gammas_is_qaoa_and_batch(Q):
+    """Equal per-edge angles reproduce qva_evolve (R25) at n = 24 (permuted tile path, weighted);
+    evolve_ex_batch members equal single evolutions."""
+    n, p = 24, 2
+    rng = np.random.default_rng(24)
+    u, v = random_regular_graph(n, 3, rng)
+    w = rng.uniform(0, 1, len(u))
+    m = len(u)
+    theta = rng.uniform(0, math.pi, 2 * p)
+    tex = np.concatenate([np.r_[np.full(m, theta[2 * i]), theta[2 * i + 1]] for i in range(p)])
+    with Q.Plan(1 << n, "x", n_qubits=n) as P:
+        P.set_qualities_maxcut(u, v, w)
+        P.evolve(theta)
+        a, fa = P.get_state(), P.expectation()
+        P.evolve_ex(tex)
+        assert np.max(np.abs(P.get_state() - a)) < 1e-12
+        assert abs(P.expectation() - fa) < 1e-10
+        sets = np.stack([tex, _ex_theta(m, p, rng), _ex_theta(m, p, rng)])
+        fb = P.evolve_ex_batch(sets)
+        for b in range(3):
+            P.evolve_ex(sets[b])
+            assert abs(P.expectation() - fb[b]) <= 1e-12 * max(1.0, abs(fb[b]))
+        assert abs(fb[0] - fa) < 1e-10
+
+
+def test_ex_qaoa_parity_mixer_and_errors(Q):
+    """ex phases with the QAOAz parity mixer (step path) against oracle primitives; errors."""
+    n, p = 10, 2
+    rng = np.random.default_rng(77)
+    u, v = erdos_renyi_graph(n, 0.4, rng)
+    m = len(u)
+    theta = _ex_theta(m, p, rng)
+    psi0 = np.zeros(1 << n, np.complex128)
+    psi0[0b0101010101] = 1.0
+    ref = psi0.copy()
+    for i in range(p):
+        th = theta[i * (m + 1):(i + 1) * (m + 1)]
+        for e in range(m):
+            O.phase(ref, O.maxcut_term_q(n, int(u[e]), int(v[e])), th[e])
+        O.mixer_parity(ref, list(range(n)), th[m])
+    with Q.Plan(1 << n, "parity", n_qubits=n) as P:
+        P.set_parity_mixer(list(range(n)))
+        P.set_initial_state(psi0)
+        with pytest.raises(Q.QvaError) as ei:
+            P.evolve_ex(theta)
+        assert ei.value.status == 3  # NOT_READY: no graph
+        P.set_qualities(O.maxcut_q(n, u, v))
+        with pytest.raises(Q.QvaError) as ei:
+            P.evolve_ex(theta)  # a q vector has no edge terms
+        assert ei.value.status == 3
+        P.set_qualities_maxcut(u, v)
+        P.evolve_ex(theta)
+        _amp_close(P.get_state(), ref)
+        with pytest.raises(ValueError):
+            P.evolve_ex(theta[:-1])
