@@ -29,10 +29,13 @@ def central_difference_sets(theta, h: float = 1e-6) -> np.ndarray:
     return out
 
 
-def objective_and_gradient(plan, theta, h: float = 1e-6):
-    """(f(theta), central-difference gradient) from one batched evolution."""
+def objective_and_gradient(plan, theta, h: float = 1e-6, ansatz: str = "qaoa"):
+    """(f(theta), central-difference gradient) from one batched evolution.
+    ansatz "ex": theta is the ex-QAOA vector (|theta| = (1 + |Sigma|) D) and the
+    sets go through evolve_ex_batch."""
     theta = np.asarray(theta, np.float64)
-    f = np.asarray(plan.evolve_batch(central_difference_sets(theta, h)), np.float64)
+    sets = central_difference_sets(theta, h)
+    f = np.asarray(plan.evolve_ex_batch(sets) if ansatz == "ex" else plan.evolve_batch(sets), np.float64)
     g = (f[1::2] - f[2::2]) / (2.0 * h)
     return float(f[0]), g
 
@@ -49,17 +52,19 @@ class OptimizeResult:
 
 
 def minimize(plan, theta0, method: str = "L-BFGS-B", h: float = 1e-6, maxiter: int = 200,
-             gtol: float = 1e-7, bounds=None, callback: Optional[Callable] = None) -> OptimizeResult:
+             gtol: float = 1e-7, bounds=None, callback: Optional[Callable] = None,
+             ansatz: str = "qaoa") -> OptimizeResult:
     """Minimise <Q> over theta = [gamma_1, beta_1, ..., gamma_p, beta_p] (reading R7) with a
     quasi-Newton method (BFGS / L-BFGS-B as in PAPER.md:341) and batched central-difference
     gradients. `plan` needs qualities (and the mixer data) set; create it with
-    max_batch >= 2 * len(theta0) + 1 so that a gradient is one launch sequence."""
+    max_batch >= 2 * len(theta0) + 1 so that a gradient is one launch sequence.  ansatz "ex":
+    ex-QAOA parameters (per layer one angle per edge term, then t_i)."""
     from scipy.optimize import minimize as sp_minimize
 
     history: List[float] = []
 
     def fg(th):
-        f, g = objective_and_gradient(plan, th, h)
+        f, g = objective_and_gradient(plan, th, h, ansatz)
         history.append(f)
         return f, g
 

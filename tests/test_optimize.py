@@ -14,11 +14,14 @@ from paper_2110_03963_b200.optimize import central_difference_sets, minimize, ob
 
 
 class _OraclePlan:
-    def __init__(self, n, q):
-        self.n, self.q = n, q
+    def __init__(self, n, q, u=None, v=None):
+        self.n, self.q, self.u, self.v = n, q, u, v
 
     def evolve_batch(self, thetas):
         return np.array([O.expectation(O.evolve_x(self.n, self.q, th), self.q) for th in thetas])
+
+    def evolve_ex_batch(self, thetas):
+        return np.array([O.expectation(O.evolve_ex(self.n, self.u, self.v, None, th), self.q) for th in thetas])
 
 
 def _ring(n):
@@ -64,6 +67,31 @@ def test_minimize_ring_reaches_three_quarters(method):
     res = minimize(_OraclePlan(n, q), [0.5, 0.4], method=method, maxiter=100)
     assert res.fun <= -0.75 * n + 1e-7, res
     assert res.history[0] > res.fun
+
+
+def test_minimize_ex_qaoa_ring():
+    """ex-QAOA contains QAOA (equal angles, R25), so its p = 1 optimum on the
+    ring is at least as good: <= -3n/4."""
+    n = 8
+    u, v = _ring(n)
+    q = O.maxcut_q(n, u, v)
+    th0 = np.r_[np.full(n, 0.5), 0.4]
+    res = minimize(_OraclePlan(n, q, u, v), th0, maxiter=100, ansatz="ex")
+    assert res.fun <= -0.75 * n + 1e-7, res
+
+
+@pytest.mark.gpu
+def test_minimize_ex_on_gpu_plan():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2110_03963_b200 as Q
+    n = 14
+    u, v = _ring(n)
+    with Q.Plan(1 << n, "x", n_qubits=n) as P:
+        P.set_qualities_maxcut(u, v)
+        res = minimize(P, np.r_[np.full(n, 0.5), 0.4], maxiter=100, ansatz="ex")
+    assert res.fun <= -0.75 * n + 1e-7, res
 
 
 @pytest.mark.gpu
