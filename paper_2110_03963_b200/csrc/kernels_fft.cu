@@ -47,6 +47,18 @@ constexpr int kMaxCta = 8192;                     // points per CTA transform se
 constexpr int kMaxSub = 8192;                     // longest sub-FFT
 constexpr int kColSmemMax = 200 * 1024;
 constexpr int kLoadU = 8;                         // independent global loads per thread per batch
+// per-CTA twiddle tables: w^{C k} for k < n as
+// A[k >> 5] * B[k & 31], i.e. ceil(n/32) + 32 entries per C
+__host__ __device__ constexpr int tw_split_entries(int n) { return ((n + 31) >> 5) + 32; }
+// column passes: forward tables cw * E; three-level inner passes also the outer twiddle M1 + cw
+__host__ __device__ constexpr int col_tw_entries(int cw, int M1, bool outer) {
+    return (outer && M1 + cw > cw * tw_split_entries(M1)) ? M1 + cw : cw * tw_split_entries(M1);
+}
+inline size_t col_smem_bytes(int cw, int M1, bool outer = false) {
+    return ((size_t)cw * (M1 + (cw > 1 ? 1 : 0)) + (size_t)col_tw_entries(cw, M1, outer)) * 16;
+}
+inline size_t row_smem_bytes(int rb, int M2) { return ((size_t)rb * M2 + (size_t)rb * tw_split_entries(M2)) * 16; }
+constexpr int kRowSmemMax = 200 * 1024;
 
 struct SubFft {
     int n = 1;
@@ -518,7 +530,7 @@ struct ColArgs {
 // [forward column FFTs + twiddle w_M^{x2 k1}]; expectation partials to slot pslot.
 template <typename F, typename Ad>
 __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0, int cwv, int mat_y, int pslot,
-                                          double *red) {
+                                          double *red, const double2 *Tw) {
     const int M1 = a.M1, M2 = a.M2;
     const int tot = M1 * cwv;
     if (a.do_inv) F::run(ad, a.sf, a.tw, cwv, true);
@@ -548,9 +560,7 @@ __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0
                     v = cmul(v, make_double2(cs * a.invN, s * a.invN));
                 }
                 if (ops & OP_CHIRP) v = cmul(v, chirp(x, a.N));
-                if (ops & OP_OUTER_TW)
-                    v = cmul(v, big_twiddle(a.otw_lo, a.otw_hi, a.otw_shift,
-                                            xl * (uint64_t)(a.mat_off + mat_y), true));
+                if (ops & OP_OUTER_TW) v = cmul(v, cmul(Tw[x1], Tw[M1 + c]));  // w_N^{-xl K}, table
             }
             slot = v;
         }
@@ -563,16 +573,7 @@ __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0
         }
         __syncthreads();
     }
-    if (a.do_fwd) {
-        F::run(ad, a.sf, a.tw, cwv, false);
-        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-            const int c = (int)divu(idx, a.m1mag), k1 = idx - c * M1;
-            const uint64_t r = (uint64_t)(a.col_off + c0 + c) * (uint64_t)k1;  // < M: no reduction needed
-            double2 *e = ad.ptr(c, k1);
-            *e = cmul(*e, big_twiddle(a.big_lo, a.big_hi, a.big_shift, r, false));
-        }
-        __syncthreads();
-    }
+    if (a.do_fwd) F::run(ad, a.sf, a.tw, cwv, false);  // the twiddle w_M^{x2 k1} is applied by the store
 }
 
 template <int NT, typename F = GenericFft>
@@ -586,8 +587,25 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
     const uint64_t mat = (uint64_t)blockIdx.y * a.mat_stride;  // inner passes: matrix = top-level row
     const int stride = cwv > 1 ? M1 + 1 : M1;  // odd padding: column-major stores are conflict-free
     double2 *A = reinterpret_cast<double2 *>(smem_raw);
-    const int tot = M1 * cwv;
     const int totw = M1 << a.lcw;  // (x1, c) over the full column width; c >= cwv skipped
+    // twiddle tables (their global loads go out with the column block's): forward pass
+    // w_M^{C k1} = Tw[c*E + (k1 >> 5)] * Tw[c*E + nh + (k1 & 31)] (C = global column); outer
+    // (three-level inverse) w_N^{-xl K} = Tw[x1] * Tw[M1 + c] (xl = x1*M2 + c0 + c, K = matrix)
+    double2 *Tw = A + (size_t)a.cw * (M1 + (a.cw > 1 ? 1 : 0));
+    const int nh = (M1 + 31) >> 5, E = nh + 32;
+    if (a.do_fwd) {
+        for (int i = threadIdx.x; i < cwv * E; i += blockDim.x) {
+            const int c = i / E, j = i - c * E;
+            const uint64_t C = (uint64_t)(a.col_off + c0 + c);
+            const int k = j < nh ? (j << 5) : j - nh;  // every k < M1 (entries past M1 are never read)
+            Tw[i] = k < M1 ? big_twiddle(a.big_lo, a.big_hi, a.big_shift, C * (uint64_t)k, false) : make_double2(1.0, 0.0);
+        }
+    } else if (a.ops & OP_OUTER_TW) {
+        const uint64_t K = (uint64_t)(a.mat_off + blockIdx.y);
+        for (int i = threadIdx.x; i < M1 + cwv; i += blockDim.x)
+            Tw[i] = big_twiddle(a.otw_lo, a.otw_hi, a.otw_shift,
+                                i < M1 ? (uint64_t)i * (uint64_t)M2 * K : (uint64_t)(c0 + i - M1) * K, true);
+    }
     // the column block arrives in batches of kLoadU independent loads per thread (one load per
     // iteration would wait a full memory latency for each element before its smem store)
     for (int base = threadIdx.x; base < totw; base += kLoadU * blockDim.x) {
@@ -611,12 +629,14 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         }
     }
     __syncthreads();
-    col_block<F>(AddrLin{A, stride}, a, c0, cwv, blockIdx.y, blockIdx.x, red);
+    col_block<F>(AddrLin{A, stride}, a, c0, cwv, blockIdx.y, blockIdx.x, red, Tw);
     for (int idx = threadIdx.x; idx < totw; idx += blockDim.x) {
         const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
         if (c >= cwv) continue;
         const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
-        if (x < a.out_len) a.out[mat + x] = A[c * stride + x1];
+        double2 v = A[c * stride + x1];
+        if (a.do_fwd) v = cmul(v, cmul(Tw[c * E + (x1 >> 5)], Tw[c * E + nh + (x1 & 31)]));
+        if (x < a.out_len) a.out[mat + x] = v;
     }
 }
 
@@ -684,13 +704,31 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
         }
         A[i] = cmul(A[i], e);
     }
+    // final twiddle w^{-x2 kr} = Tr[r*E + (x2 >> 5)] * Tr[r*E + nh + (x2 & 31)] per row r (after
+    // the block: its loads overlap the inverse FFT's first stage)
+    double2 *Tr = A + tot;
+    const int nh = (M2 + 31) >> 5, E = nh + 32;
+    for (int i = threadIdx.x; i < a.rb * E; i += blockDim.x) {
+        const int r = i / E, j = i - r * E;
+        const int kr = a.row_off + k1_0 + r;
+        const uint64_t K = (uint64_t)(a.row_mod ? kr % a.row_mod : kr);
+        const int k = j < nh ? (j << 5) : j - nh;  // every k < M2 (entries past M2 are never read)
+        Tr[i] = k < M2 ? big_twiddle(a.big_lo, a.big_hi, a.big_shift, K * (uint64_t)k, true) : make_double2(1.0, 0.0);
+    }
     __syncthreads();
     F::run(AddrLin{A, M2}, a.sf, a.tw, a.rb, true);
+    // (row, column) of i carried incrementally: the multiply-high divu here made ptxas emit code
+    // that indexed Tr out of range (reproducible on B200; plain division or this form is correct)
+    int r = threadIdx.x / M2, x2 = threadIdx.x - r * M2;
+    const int step_r = blockDim.x / M2, step_x = blockDim.x - step_r * M2;
     for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-        const int r = (int)divu(i, a.m2mag), x2 = i - r * M2;
-        const int kr = a.row_off + k1_0 + r;
-        const uint64_t tr = (uint64_t)x2 * (uint64_t)(a.row_mod ? kr % a.row_mod : kr);  // < M
-        rows[i] = cmul(A[i], big_twiddle(a.big_lo, a.big_hi, a.big_shift, tr, true));
+        rows[i] = cmul(A[i], cmul(Tr[r * E + (x2 >> 5)], Tr[r * E + nh + (x2 & 31)]));
+        r += step_r;
+        x2 += step_x;
+        if (x2 >= M2) {
+            x2 -= M2;
+            ++r;
+        }
     }
 }
 
@@ -867,7 +905,7 @@ Split choose_split(uint64_t M, int G = 1) {
         if (m1 % G || m2 % G) continue;  // sharded: whole row / column blocks per shard
         int cw = 0;
         for (int c : {8, 4, 2, 1})
-            if ((uint64_t)c * m1 <= (uint64_t)kMaxCta && (size_t)c * (m1 + 1) * sizeof(double2) <= kColSmemMax) {
+            if ((uint64_t)c * m1 <= (uint64_t)kMaxCta && col_smem_bytes(c, (int)m1) <= (size_t)kColSmemMax) {
                 cw = c;
                 break;
             }
@@ -956,8 +994,8 @@ qva_status upload_roots() {
     return QVA_OK;
 }
 
-size_t col_smem(const FftPlan *fp) { return (size_t)fp->cw * (fp->M1 + (fp->cw > 1 ? 1 : 0)) * sizeof(double2); }
-size_t row_smem(const FftPlan *fp) { return (size_t)fp->rb * fp->M2 * sizeof(double2); }
+size_t col_smem(const FftPlan *fp) { return col_smem_bytes(fp->cw, fp->M1); }
+size_t row_smem(const FftPlan *fp) { return row_smem_bytes(fp->rb, fp->M2); }
 
 // launch helpers shared by planning (Bluestein kernel spectrum) and fft_run
 ColArgs col_args(const FftPlan *fp) {
@@ -1148,11 +1186,11 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
     if (st != QVA_OK) return fail(st, "");
     cudaFuncSetAttribute(fft_col_kernel<kFftThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
     cudaFuncSetAttribute(fft_col_kernel<kFftThreads / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
-    cudaFuncSetAttribute(fft_row_kernel<>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSub * (int)sizeof(double2));
+    cudaFuncSetAttribute(fft_row_kernel<>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmemMax);
     for (const auto &cl : kCodelets) {
         cudaFuncSetAttribute(cl.col, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
         cudaFuncSetAttribute(cl.col_half, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
-        cudaFuncSetAttribute(cl.row, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSub * (int)sizeof(double2));
+        cudaFuncSetAttribute(cl.row, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmemMax);
     }
     cudaFuncSetAttribute(fft_whole_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * (int)sizeof(double2));
     if (fp->bluestein) {
@@ -1248,7 +1286,7 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
     c.otw_hi = fp->d_big_hi;
     c.otw_shift = fp->big_shift;
     const dim3 gc((fp->Mi2 + c.cw - 1) / c.cw, nmat);
-    const size_t smem_c = (size_t)c.cw * (fp->Mi1 + (c.cw > 1 ? 1 : 0)) * sizeof(double2);
+    const size_t smem_c = col_smem_bytes(c.cw, fp->Mi1, true);
     auto cols = [&](int inv, int ops, int fwd) -> qva_status {
         c.do_inv = inv;
         c.do_fwd = fwd;
@@ -1284,7 +1322,7 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
         w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
     }
     obs->begin(K_FFT_ROW, 32.0 * (double)R * nmat + (r.lambda_perm ? 8.0 * (double)R * nmat : 0.0));
-    row_kernel_for(fp->Mi2)<<<nmat * fp->Mi1 / fp->rb2, kFftThreads, (size_t)fp->rb2 * fp->Mi2 * sizeof(double2), s>>>(w);
+    row_kernel_for(fp->Mi2)<<<nmat * fp->Mi1 / fp->rb2, kFftThreads, row_smem_bytes(fp->rb2, fp->Mi2), s>>>(w);
     cudaError_t e = cudaGetLastError();
     obs->end();
     if (e != cudaSuccess) {
@@ -1495,11 +1533,11 @@ qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStr
     while (c.cw > 1 && M2s % c.cw) c.cw >>= 1;  // keep whole column blocks inside a shard
     c.lcw = c.cw == 8 ? 3 : c.cw == 4 ? 2 : c.cw == 2 ? 1 : 0;
     const int gc = (M2s + c.cw - 1) / c.cw;
-    const size_t smem_c = (size_t)c.cw * (fp->M1 + (c.cw > 1 ? 1 : 0)) * sizeof(double2);
+    const size_t smem_c = col_smem_bytes(c.cw, fp->M1);
     int rb = 1;
     for (int x = 2; x <= 64; ++x)
         if (M1s % x == 0 && x * fp->M2 <= kMaxCta) rb = x;
-    const size_t smem_r = (size_t)rb * fp->M2 * sizeof(double2);
+    const size_t smem_r = row_smem_bytes(rb, fp->M2);
     if ((size_t)gc * io.local > (size_t)fp->n_partials) {
         cudaFree(fp->partials);
         fp->n_partials = gc * io.local;
