@@ -49,7 +49,8 @@ constexpr int kColSmemMax = 200 * 1024;
 constexpr int kLoadU = 8;                         // independent global loads per thread per batch
 // per-CTA twiddle tables: w^{C k} for k < n as
 // A[k >> 5] * B[k & 31], i.e. ceil(n/32) + 32 entries per C
-__host__ __device__ constexpr int tw_split_entries(int n) { return ((n + 31) >> 5) + 32; }
+// (odd, so that the 8 columns' tables of a column block start in distinct bank groups)
+__host__ __device__ constexpr int tw_split_entries(int n) { return (((n + 31) >> 5) + 32) | 1; }
 // column passes: forward tables cw * E; three-level inner passes also the outer twiddle M1 + cw
 __host__ __device__ constexpr int col_tw_entries(int cw, int M1, bool outer) {
     return (outer && M1 + cw > cw * tw_split_entries(M1)) ? M1 + cw : cw * tw_split_entries(M1);
@@ -302,6 +303,18 @@ struct AddrLin {
     int stride;
     __device__ __forceinline__ double2 *ptr(int f, int i) const { return buf + f * stride + i; }
 };
+// AddrSw<S>: the same with the low 3 index bits XORed with bits S..S+2 (S = 0: identity).  A
+// radix-R first stage (R = 2^S or 2^(S+1)) stores at stride R, which without the swizzle puts 8
+// lanes of a 16-B access phase in one bank group; with it they spread over all 8.  Contiguous
+// 8-aligned runs map onto themselves, so every other access stays conflict-free.  Needs the
+// transform length to be a multiple of 8.
+template <int S>
+struct AddrSw {
+    double2 *buf;
+    int stride;
+    __device__ __forceinline__ static int sw(int i) { return S ? (i ^ ((i >> S) & 7)) : i; }
+    __device__ __forceinline__ double2 *ptr(int f, int i) const { return buf + f * stride + sw(i); }
+};
 
 // One Stockham radix-R stage, in place, over `count` independent length-n transforms.  Rounds
 // cover whole transforms (a transform's butterflies read and write only its own elements), each
@@ -420,9 +433,13 @@ __device__ __forceinline__ void stages_ct(const Ad &ad, const double2 *tw, int c
     stage_ct<R, N, M>(ad, count, tw + OFF, inv);
     stages_ct<N, M * R, OFF + M * R, Ad, Rest...>(ad, tw, count, inv);
 }
+template <int R1, int... Rest>
+constexpr int first_radix() { return R1; }
 template <int N, int... Rs>
 struct Codelet {
     static constexpr int n = N;
+    static constexpr int kR1 = first_radix<Rs...>();
+    static constexpr int kSwz = kR1 == 16 ? 4 : ((kR1 == 8 || kR1 == 4 || kR1 == 2) && N % 8 == 0) ? 3 : 0;
     template <typename Ad>
     __device__ __forceinline__ static void run(const Ad &ad, const SubFft &sf, const double2 *tw, int count, bool inv) {
         stages_ct<N, 1, 0, Ad, Rs...>(ad, tw + sf.twoff[0], count, inv);  // stage tables follow make_sub's
@@ -431,6 +448,7 @@ struct Codelet {
 // runtime-planned transforms
 struct GenericFft {
     static constexpr int n = 0;
+    static constexpr int kSwz = 0;
     template <typename Ad>
     __device__ __forceinline__ static void run(const Ad &ad, const SubFft &sf, const double2 *tw, int count, bool inv) {
         run_fft_ad(ad, sf, tw, count, inv);
@@ -532,11 +550,13 @@ template <typename F, typename Ad>
 __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0, int cwv, int mat_y, int pslot,
                                           double *red, const double2 *Tw) {
     const int M1 = a.M1, M2 = a.M2;
-    const int tot = M1 * cwv;
     if (a.do_inv) F::run(ad, a.sf, a.tw, cwv, true);
     const int ops = a.ops;
     if (ops) {
         double acc = 0.0, nrm = 0.0;
+        // column fastest across the threads: q is read in 8-column runs (64 B per row) instead
+        // of one 8-B word per M2-strided row; the odd smem stride keeps the 8 columns conflict-free
+        const int tot = M1 * cwv;
         for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
             const int c = (int)divu(idx, a.m1mag), x1 = idx - c * M1;
             const uint64_t xl = (uint64_t)x1 * M2 + c0 + c;                  // local (q) index
@@ -587,12 +607,13 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
     const uint64_t mat = (uint64_t)blockIdx.y * a.mat_stride;  // inner passes: matrix = top-level row
     const int stride = cwv > 1 ? M1 + 1 : M1;  // odd padding: column-major stores are conflict-free
     double2 *A = reinterpret_cast<double2 *>(smem_raw);
+    const AddrSw<F::kSwz> ad{A, stride};
     const int totw = M1 << a.lcw;  // (x1, c) over the full column width; c >= cwv skipped
     // twiddle tables (their global loads go out with the column block's): forward pass
     // w_M^{C k1} = Tw[c*E + (k1 >> 5)] * Tw[c*E + nh + (k1 & 31)] (C = global column); outer
     // (three-level inverse) w_N^{-xl K} = Tw[x1] * Tw[M1 + c] (xl = x1*M2 + c0 + c, K = matrix)
     double2 *Tw = A + (size_t)a.cw * (M1 + (a.cw > 1 ? 1 : 0));
-    const int nh = (M1 + 31) >> 5, E = nh + 32;
+    const int nh = (M1 + 31) >> 5, E = tw_split_entries(M1);
     if (a.do_fwd) {
         for (int i = threadIdx.x; i < cwv * E; i += blockDim.x) {
             const int c = i / E, j = i - c * E;
@@ -625,16 +646,16 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         for (int u = 0; u < kLoadU; ++u) {
             const int idx = base + u * blockDim.x;
             const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
-            if (idx < totw && c < cwv) A[c * stride + x1] = v[u];
+            if (idx < totw && c < cwv) *ad.ptr(c, x1) = v[u];
         }
     }
     __syncthreads();
-    col_block<F>(AddrLin{A, stride}, a, c0, cwv, blockIdx.y, blockIdx.x, red, Tw);
+    col_block<F>(ad, a, c0, cwv, blockIdx.y, blockIdx.x, red, Tw);
     for (int idx = threadIdx.x; idx < totw; idx += blockDim.x) {
         const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
         if (c >= cwv) continue;
         const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
-        double2 v = A[c * stride + x1];
+        double2 v = *ad.ptr(c, x1);
         if (a.do_fwd) v = cmul(v, cmul(Tw[c * E + (x1 >> 5)], Tw[c * E + nh + (x1 & 31)]));
         if (x < a.out_len) a.out[mat + x] = v;
     }
@@ -666,48 +687,68 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
     const int M2 = a.M2;
     const int k1_0 = blockIdx.x * a.rb;  // local row; global row = row_off + local
     double2 *A = reinterpret_cast<double2 *>(smem_raw);
+    const AddrSw<F::kSwz> ad{A, M2};
     double2 *rows = a.buf + (uint64_t)k1_0 * M2;
     const int tot = a.rb * M2;
-    for (int base = threadIdx.x; base < tot; base += kLoadU * blockDim.x) {
-        double2 v[kLoadU];
-#pragma unroll
-        for (int u = 0; u < kLoadU; ++u) {
-            const int i = base + u * blockDim.x;
-            if (i < tot) v[u] = rows[i];
+    // (row, column) of the flat index i = threadIdx.x + n * blockDim.x, carried incrementally
+    const int r0 = threadIdx.x / M2, x0 = threadIdx.x - r0 * M2;
+    const int step_r = blockDim.x / M2, step_x = blockDim.x - step_r * M2;
+    auto adv = [&](int &r, int &x) {
+        r += step_r;
+        x += step_x;
+        if (x >= M2) {
+            x -= M2;
+            ++r;
         }
+    };
+    {
+        int r = r0, x = x0;
+        for (int base = threadIdx.x; base < tot; base += kLoadU * blockDim.x) {
+            double2 v[kLoadU];
 #pragma unroll
-        for (int u = 0; u < kLoadU; ++u) {
-            const int i = base + u * blockDim.x;
-            if (i < tot) A[i] = v[u];
+            for (int u = 0; u < kLoadU; ++u) {
+                const int i = base + u * blockDim.x;
+                if (i < tot) v[u] = rows[i];
+            }
+#pragma unroll
+            for (int u = 0; u < kLoadU; ++u) {
+                const int i = base + u * blockDim.x;
+                if (i < tot) *ad.ptr(r, x) = v[u];
+                adv(r, x);
+            }
         }
     }
     __syncthreads();
-    F::run(AddrLin{A, M2}, a.sf, a.tw, a.rb, false);
+    F::run(ad, a.sf, a.tw, a.rb, false);
     if (a.fwd_only) {
-        for (int i = threadIdx.x; i < tot; i += blockDim.x) rows[i] = A[i];
+        int r = r0, x = x0;
+        for (int i = threadIdx.x; i < tot; i += blockDim.x, adv(r, x)) rows[i] = *ad.ptr(r, x);
         return;
     }
-    for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-        const int r = (int)divu(i, a.m2mag), k2 = i - r * M2;
-        const int k1 = a.row_off + k1_0 + r;
-        const uint64_t pos = (uint64_t)k1 * M2 + k2;
-        double2 e;
-        if (a.spec == 1) {
-            double s, c;
-            sincos(-a.beta * __ldg(a.lam_perm + pos), &s, &c);
-            e = make_double2(c * a.scale, s * a.scale);
-        } else if (a.spec == 2) {
-            double2 b = __ldg(a.bhat + pos);
-            e = make_double2(b.x * a.scale, (a.conj_b ? -b.y : b.y) * a.scale);
-        } else {
-            e = (k1 == 0 && k2 == 0) ? a.e0 : a.ec;
+    {
+        int r = r0, k2 = x0;
+        for (int i = threadIdx.x; i < tot; i += blockDim.x, adv(r, k2)) {
+            const int k1 = a.row_off + k1_0 + r;
+            const uint64_t pos = (uint64_t)k1 * M2 + k2;
+            double2 e;
+            if (a.spec == 1) {
+                double s, c;
+                sincos(-a.beta * __ldg(a.lam_perm + pos), &s, &c);
+                e = make_double2(c * a.scale, s * a.scale);
+            } else if (a.spec == 2) {
+                double2 b = __ldg(a.bhat + pos);
+                e = make_double2(b.x * a.scale, (a.conj_b ? -b.y : b.y) * a.scale);
+            } else {
+                e = (k1 == 0 && k2 == 0) ? a.e0 : a.ec;
+            }
+            double2 *p = ad.ptr(r, k2);
+            *p = cmul(*p, e);
         }
-        A[i] = cmul(A[i], e);
     }
     // final twiddle w^{-x2 kr} = Tr[r*E + (x2 >> 5)] * Tr[r*E + nh + (x2 & 31)] per row r (after
     // the block: its loads overlap the inverse FFT's first stage)
     double2 *Tr = A + tot;
-    const int nh = (M2 + 31) >> 5, E = nh + 32;
+    const int nh = (M2 + 31) >> 5, E = tw_split_entries(M2);
     for (int i = threadIdx.x; i < a.rb * E; i += blockDim.x) {
         const int r = i / E, j = i - r * E;
         const int kr = a.row_off + k1_0 + r;
@@ -716,20 +757,12 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
         Tr[i] = k < M2 ? big_twiddle(a.big_lo, a.big_hi, a.big_shift, K * (uint64_t)k, true) : make_double2(1.0, 0.0);
     }
     __syncthreads();
-    F::run(AddrLin{A, M2}, a.sf, a.tw, a.rb, true);
-    // (row, column) of i carried incrementally: the multiply-high divu here made ptxas emit code
-    // that indexed Tr out of range (reproducible on B200; plain division or this form is correct)
-    int r = threadIdx.x / M2, x2 = threadIdx.x - r * M2;
-    const int step_r = blockDim.x / M2, step_x = blockDim.x - step_r * M2;
-    for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-        rows[i] = cmul(A[i], cmul(Tr[r * E + (x2 >> 5)], Tr[r * E + nh + (x2 & 31)]));
-        r += step_r;
-        x2 += step_x;
-        if (x2 >= M2) {
-            x2 -= M2;
-            ++r;
-        }
-    }
+    F::run(ad, a.sf, a.tw, a.rb, true);
+    // (a multiply-high divu for (r, x2) here made ptxas emit code that indexed Tr out of range on
+    // B200; the incremental form is correct)
+    int r = r0, x2 = x0;
+    for (int i = threadIdx.x; i < tot; i += blockDim.x, adv(r, x2))
+        rows[i] = cmul(*ad.ptr(r, x2), cmul(Tr[r * E + (x2 >> 5)], Tr[r * E + nh + (x2 & 31)]));
 }
 
 // whole evolution of a (direct, 13-smooth) N <= 4096 state in one CTA
