@@ -60,6 +60,7 @@ inline size_t col_smem_bytes(int cw, int M1, bool outer = false) {
 }
 inline size_t row_smem_bytes(int rb, int M2) { return ((size_t)rb * M2 + (size_t)rb * tw_split_entries(M2)) * 16; }
 constexpr int kRowSmemMax = 200 * 1024;
+constexpr size_t kColHalfSmemMax = 110 * 1024;  // two 256-thread column CTAs per SM
 
 struct SubFft {
     int n = 1;
@@ -349,7 +350,7 @@ __device__ __forceinline__ void stage_inplace(const Ad &ad, int n, int count, in
                 const int k = j - (int)divu(j, mmag) * m;
                 if (m > 1) {
 #pragma unroll
-                    for (int t = 1; t < R; ++t) a[b][t] = cmul(a[b][t], conj_if(__ldg(tw + t * k), inv));
+                    for (int t = 1; t < R; ++t) a[b][t] = cmul(a[b][t], conj_if(tw[t * k], inv));
                 }
                 dft<R>(a[b], inv);
                 const int o = (j - k) * R + k;
@@ -415,7 +416,7 @@ __device__ __forceinline__ void stage_ct(const Ad &ad, int count, const double2 
                 const int k = j % M;
                 if (M > 1) {
 #pragma unroll
-                    for (int t = 1; t < R; ++t) a[b][t] = cmul(a[b][t], conj_if(__ldg(tw + t * k), inv));
+                    for (int t = 1; t < R; ++t) a[b][t] = cmul(a[b][t], conj_if(tw[t * k], inv));
                 }
                 dft<R>(a[b], inv);
                 const int o = (j - k) * R + k;
@@ -540,6 +541,7 @@ struct ColArgs {
     const double2 *big_lo, *big_hi;
     int big_shift;
     double *partials;
+    int tws, ts_off;         // stage twiddles copied to smem at A + ts_off (tws entries; 0: global)
     SubFft sf;
 };
 
@@ -548,9 +550,9 @@ struct ColArgs {
 // [forward column FFTs + twiddle w_M^{x2 k1}]; expectation partials to slot pslot.
 template <typename F, typename Ad>
 __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0, int cwv, int mat_y, int pslot,
-                                          double *red, const double2 *Tw) {
+                                          double *red, const double2 *Tw, const double2 *twp) {
     const int M1 = a.M1, M2 = a.M2;
-    if (a.do_inv) F::run(ad, a.sf, a.tw, cwv, true);
+    if (a.do_inv) F::run(ad, a.sf, twp, cwv, true);
     const int ops = a.ops;
     if (ops) {
         double acc = 0.0, nrm = 0.0;
@@ -593,7 +595,16 @@ __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0
         }
         __syncthreads();
     }
-    if (a.do_fwd) F::run(ad, a.sf, a.tw, cwv, false);  // the twiddle w_M^{x2 k1} is applied by the store
+    if (a.do_fwd) F::run(ad, a.sf, twp, cwv, false);  // the twiddle w_M^{x2 k1} is applied by the store
+}
+
+// the sub-FFT's stage twiddle tables (tws entries from tw + twoff[0]) into shared memory at Ts;
+// returns the base to hand to F::run (its offsets are relative to the global table)
+__device__ __forceinline__ const double2 *stage_twiddles(const double2 *tw, const SubFft &sf, int tws, double2 *Ts) {
+    if (!tws) return tw;
+    const double2 *src = tw + sf.twoff[0];
+    for (int i = threadIdx.x; i < tws; i += blockDim.x) Ts[i] = src[i];
+    return Ts - sf.twoff[0];  // generic address: only Ts[0..tws) is ever dereferenced
 }
 
 template <int NT, typename F = GenericFft>
@@ -627,6 +638,7 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
             Tw[i] = big_twiddle(a.otw_lo, a.otw_hi, a.otw_shift,
                                 i < M1 ? (uint64_t)i * (uint64_t)M2 * K : (uint64_t)(c0 + i - M1) * K, true);
     }
+    const double2 *twp = stage_twiddles(a.tw, a.sf, a.tws, A + a.ts_off);
     // the column block arrives in batches of kLoadU independent loads per thread (one load per
     // iteration would wait a full memory latency for each element before its smem store)
     for (int base = threadIdx.x; base < totw; base += kLoadU * blockDim.x) {
@@ -650,7 +662,7 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         }
     }
     __syncthreads();
-    col_block<F>(ad, a, c0, cwv, blockIdx.y, blockIdx.x, red, Tw);
+    col_block<F>(ad, a, c0, cwv, blockIdx.y, blockIdx.x, red, Tw, twp);
     for (int idx = threadIdx.x; idx < totw; idx += blockDim.x) {
         const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
         if (c >= cwv) continue;
@@ -677,6 +689,7 @@ struct RowArgs {
     const double2 *tw;
     const double2 *big_lo, *big_hi;
     int big_shift;
+    int tws, ts_off;            // stage twiddles copied to smem at A + ts_off (tws entries; 0: global)
     SubFft sf;
 };
 
@@ -701,6 +714,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
             ++r;
         }
     };
+    const double2 *twp = stage_twiddles(a.tw, a.sf, a.tws, A + a.ts_off);
     {
         int r = r0, x = x0;
         for (int base = threadIdx.x; base < tot; base += kLoadU * blockDim.x) {
@@ -719,7 +733,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
         }
     }
     __syncthreads();
-    F::run(ad, a.sf, a.tw, a.rb, false);
+    F::run(ad, a.sf, twp, a.rb, false);
     if (a.fwd_only) {
         int r = r0, x = x0;
         for (int i = threadIdx.x; i < tot; i += blockDim.x, adv(r, x)) rows[i] = *ad.ptr(r, x);
@@ -757,7 +771,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a
         Tr[i] = k < M2 ? big_twiddle(a.big_lo, a.big_hi, a.big_shift, K * (uint64_t)k, true) : make_double2(1.0, 0.0);
     }
     __syncthreads();
-    F::run(ad, a.sf, a.tw, a.rb, true);
+    F::run(ad, a.sf, twp, a.rb, true);
     // (a multiply-high divu for (r, x2) here made ptxas emit code that indexed Tr out of range on
     // B200; the incremental form is correct)
     int r = r0, x2 = x0;
@@ -1029,6 +1043,21 @@ qva_status upload_roots() {
 
 size_t col_smem(const FftPlan *fp) { return col_smem_bytes(fp->cw, fp->M1); }
 size_t row_smem(const FftPlan *fp) { return row_smem_bytes(fp->rb, fp->M2); }
+// stage twiddle entries of a sub-FFT (its tables are contiguous from twoff[0])
+int stage_tw_entries(const SubFft &sf) {
+    return sf.ns ? sf.twoff[sf.ns - 1] + sf.m[sf.ns - 1] * sf.r[sf.ns - 1] - sf.twoff[0] : 0;
+}
+// adds the stage tables behind a launch's shared-memory block when they fit under cap and the
+// copy is small next to the CTA's elements (a 4320-point row CTA would copy 5504 entries)
+template <typename Args>
+size_t with_stage_tw(Args &a, size_t base_bytes, size_t cap, int elements) {
+    a.ts_off = (int)(base_bytes / sizeof(double2));
+    a.tws = stage_tw_entries(a.sf);
+    if (4 * a.tws <= elements && base_bytes + (size_t)a.tws * sizeof(double2) <= cap)
+        return base_bytes + (size_t)a.tws * sizeof(double2);
+    a.tws = 0;
+    return base_bytes;
+}
 
 // launch helpers shared by planning (Bluestein kernel spectrum) and fft_run
 ColArgs col_args(const FftPlan *fp) {
@@ -1248,10 +1277,12 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
         c.out_len = M;
         c.N = M;
         c.do_fwd = 1;
-        col_kernel_for(fp->M1, false)<<<col_grid(fp), kFftThreads, col_smem(fp)>>>(c);
+        const size_t sc = with_stage_tw(c, col_smem(fp), kColSmemMax, fp->cw * fp->M1);
+        col_kernel_for(fp->M1, false)<<<col_grid(fp), kFftThreads, sc>>>(c);
         RowArgs w = row_args(fp, fp->bhat);
         w.fwd_only = 1;
-        row_kernel_for(fp->M2)<<<row_grid(fp), kFftThreads, row_smem(fp)>>>(w);
+        const size_t sr = with_stage_tw(w, row_smem(fp), kRowSmemMax, fp->rb * fp->M2);
+        row_kernel_for(fp->M2)<<<row_grid(fp), kFftThreads, sr>>>(w);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return fail(QVA_ERR_CUDA, std::string("Bluestein setup: ") + cudaGetErrorString(e));
     }
@@ -1319,7 +1350,7 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
     c.otw_hi = fp->d_big_hi;
     c.otw_shift = fp->big_shift;
     const dim3 gc((fp->Mi2 + c.cw - 1) / c.cw, nmat);
-    const size_t smem_c = col_smem_bytes(c.cw, fp->Mi1, true);
+    const size_t smem_c = with_stage_tw(c, col_smem_bytes(c.cw, fp->Mi1, true), kColSmemMax, c.cw * fp->Mi1);
     auto cols = [&](int inv, int ops, int fwd) -> qva_status {
         c.do_inv = inv;
         c.do_fwd = fwd;
@@ -1355,7 +1386,8 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
         w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
     }
     obs->begin(K_FFT_ROW, 32.0 * (double)R * nmat + (r.lambda_perm ? 8.0 * (double)R * nmat : 0.0));
-    row_kernel_for(fp->Mi2)<<<nmat * fp->Mi1 / fp->rb2, kFftThreads, row_smem_bytes(fp->rb2, fp->Mi2), s>>>(w);
+    const size_t smem_r3 = with_stage_tw(w, row_smem_bytes(fp->rb2, fp->Mi2), kRowSmemMax, fp->rb2 * fp->Mi2);
+    row_kernel_for(fp->Mi2)<<<nmat * fp->Mi1 / fp->rb2, kFftThreads, smem_r3, s>>>(w);
     cudaError_t e = cudaGetLastError();
     obs->end();
     if (e != cudaSuccess) {
@@ -1413,7 +1445,7 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
     c.lam0 = r.lam0;
     c.lamc = r.lamc;
     c.lam = blu ? r.lambda_perm : nullptr;
-    const size_t smem_c = col_smem(fp), smem_r = row_smem(fp);
+    size_t smem_c = col_smem(fp);
     const int gc = col_grid(fp), gr = row_grid(fp);
     int expect_slots = gc;  // partial slots written by the last column pass
     // column pass with 256-thread CTAs, two per SM (their barrier stalls overlap), when every
@@ -1422,9 +1454,10 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
         const char *e = getenv("QVA_FFT_COL256");
         return e ? atoi(e) : 1;
     }();
-    bool col_half = half_env != 0 && smem_c <= 110 * 1024;
+    bool col_half = half_env != 0 && smem_c <= kColHalfSmemMax;
     for (int st = 0; st < fp->col.ns && col_half; ++st)
         if (fp->col.n / fp->col.r[st] > nb_of(fp->col.r[st]) * (kFftThreads / 2)) col_half = false;
+    smem_c = with_stage_tw(c, smem_c, col_half ? kColHalfSmemMax : (size_t)kColSmemMax, fp->cw * fp->M1);
 
     // in/out: nullptr -> W; the state (r.psi, length N) is named explicitly
     auto launch_col = [&](const double2 *in, uint64_t in_len, double2 *out, uint64_t out_len, int init, int inv,
@@ -1476,6 +1509,7 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
             w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
         }
         obs->begin(K_FFT_ROW, 32.0 * M + extra);
+        const size_t smem_r = with_stage_tw(w, row_smem(fp), kRowSmemMax, fp->rb * fp->M2);
         row_kernel_for(fp->M2)<<<gr, kFftThreads, smem_r, s>>>(w);
         cudaError_t e = cudaGetLastError();
         obs->end();
@@ -1566,7 +1600,7 @@ qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStr
     while (c.cw > 1 && M2s % c.cw) c.cw >>= 1;  // keep whole column blocks inside a shard
     c.lcw = c.cw == 8 ? 3 : c.cw == 4 ? 2 : c.cw == 2 ? 1 : 0;
     const int gc = (M2s + c.cw - 1) / c.cw;
-    const size_t smem_c = col_smem_bytes(c.cw, fp->M1);
+    const size_t smem_c = with_stage_tw(c, col_smem_bytes(c.cw, fp->M1), kColSmemMax, c.cw * fp->M1);
     int rb = 1;
     for (int x = 2; x <= 64; ++x)
         if (M1s % x == 0 && x * fp->M2 <= kMaxCta) rb = x;
@@ -1617,7 +1651,8 @@ qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStr
             w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
         }
         obs->begin(K_FFT_ROW, 32.0 * NG * io.local + (r.lambda_perm ? 8.0 * NG * io.local : 0.0));
-        row_kernel_for(fp->M2)<<<io.local * M1s / rb, kFftThreads, smem_r, s>>>(w);
+        const size_t smem_rs = with_stage_tw(w, smem_r, kRowSmemMax, rb * fp->M2);
+        row_kernel_for(fp->M2)<<<io.local * M1s / rb, kFftThreads, smem_rs, s>>>(w);
         cudaError_t e = cudaGetLastError();
         obs->end();
         if (e != cudaSuccess) {
