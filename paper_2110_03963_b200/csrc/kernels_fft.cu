@@ -542,6 +542,7 @@ struct ColArgs {
     int big_shift;
     double *partials;
     int tws, ts_off;         // stage twiddles copied to smem at A + ts_off (tws entries; 0: global)
+    int ops_cfast;           // elementwise ops column-fastest with batched q loads (q not L2-resident)
     SubFft sf;
 };
 
@@ -556,27 +557,24 @@ __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0
     const int ops = a.ops;
     if (ops) {
         double acc = 0.0, nrm = 0.0;
-        // column fastest across the threads: q is read in 8-column runs (64 B per row) instead
-        // of one 8-B word per M2-strided row; the odd smem stride keeps the 8 columns conflict-free
-        const int tot = M1 * cwv;
-        for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-            const int c = (int)divu(idx, a.m1mag), x1 = idx - c * M1;
-            const uint64_t xl = (uint64_t)x1 * M2 + c0 + c;                  // local (q) index
-            const uint64_t x = (uint64_t)x1 * a.M2g + a.col_off + c0 + c;    // natural index
-            double2 &slot = *ad.ptr(c, x1);
-            double2 v = slot;
+        // one element (c, x1); qv / lv: its q and lambda when loaded ahead (need_q / need_lam)
+        const bool need_q = (ops & (OP_EXPECT | OP_PHASE)) != 0, need_lam = (ops & OP_SPEC) && a.lam;
+        auto op = [&](int c, int x1, double qv, double lv) {
+            const uint64_t x = (uint64_t)x1 * a.M2g + a.col_off + c0 + c;  // natural index
+            double2 *slot = ad.ptr(c, x1);
+            double2 v = *slot;
             if ((ops & OP_MASK) && x >= a.N) {
                 v = make_double2(0.0, 0.0);
             } else {
                 if (ops & OP_CHIRP_CONJ) v = cmulc(v, chirp(x, a.N));
                 if (ops & OP_EXPECT) {
                     const double pr = v.x * v.x + v.y * v.y;
-                    acc = fma(pr, __ldg(a.q + xl), acc);
+                    acc = fma(pr, qv, acc);
                     nrm += pr;
                 }
-                if (ops & OP_PHASE) v = phase_mul(v, __ldg(a.q + xl), a.gamma);
+                if (ops & OP_PHASE) v = phase_mul(v, qv, a.gamma);
                 if (ops & OP_SPEC) {
-                    const double lam = a.lam ? __ldg(a.lam + x) : (x == 0 ? a.lam0 : a.lamc);
+                    const double lam = a.lam ? lv : (x == 0 ? a.lam0 : a.lamc);
                     double s, cs;
                     sincos(-a.beta * lam, &s, &cs);
                     v = cmul(v, make_double2(cs * a.invN, s * a.invN));
@@ -584,7 +582,63 @@ __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0
                 if (ops & OP_CHIRP) v = cmul(v, chirp(x, a.N));
                 if (ops & OP_OUTER_TW) v = cmul(v, cmul(Tw[x1], Tw[M1 + c]));  // w_N^{-xl K}, table
             }
-            slot = v;
+            *slot = v;
+        };
+        auto live = [&](int c, int x1) {  // element holds data and is not masked off
+            return c < cwv && !((ops & OP_MASK) && (uint64_t)x1 * a.M2g + a.col_off + c0 + c >= a.N);
+        };
+        if (a.ops_cfast) {
+            // HBM-resident q (large N): column fastest across the threads, so q arrives in 8-column
+            // runs (64 B per row) instead of one 8-B word per M2-strided row, and kLoadU loads per
+            // thread are in flight before the first is used
+            const int totw = M1 << a.lcw;
+            for (int base = threadIdx.x; base < totw; base += kLoadU * blockDim.x) {
+                double qv[kLoadU], lv[kLoadU];
+#pragma unroll
+                for (int u = 0; u < kLoadU; ++u) {
+                    const int idx = base + u * blockDim.x, x1 = idx >> a.lcw, c = idx & (a.cw - 1);
+                    qv[u] = lv[u] = 0.0;
+                    if (idx < totw && live(c, x1)) {
+                        if (need_q) qv[u] = __ldg(a.q + (uint64_t)x1 * M2 + c0 + c);
+                        if (need_lam) lv[u] = __ldg(a.lam + (uint64_t)x1 * a.M2g + a.col_off + c0 + c);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kLoadU; ++u) {
+                    const int idx = base + u * blockDim.x, x1 = idx >> a.lcw, c = idx & (a.cw - 1);
+                    if (idx < totw && c < cwv) op(c, x1, qv[u], lv[u]);
+                }
+            }
+        } else {
+            // L2-resident q: row fastest (measured faster at cfg3)
+            const int tot = M1 * cwv;
+            for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+                const int c = (int)divu(idx, a.m1mag), x1 = idx - c * M1;
+                const uint64_t xl = (uint64_t)x1 * M2 + c0 + c;                  // local (q) index
+                const uint64_t x = (uint64_t)x1 * a.M2g + a.col_off + c0 + c;    // natural index
+                double2 &slot = *ad.ptr(c, x1);
+                double2 v = slot;
+                if ((ops & OP_MASK) && x >= a.N) {
+                    v = make_double2(0.0, 0.0);
+                } else {
+                    if (ops & OP_CHIRP_CONJ) v = cmulc(v, chirp(x, a.N));
+                    if (ops & OP_EXPECT) {
+                        const double pr = v.x * v.x + v.y * v.y;
+                        acc = fma(pr, __ldg(a.q + xl), acc);
+                        nrm += pr;
+                    }
+                    if (ops & OP_PHASE) v = phase_mul(v, __ldg(a.q + xl), a.gamma);
+                    if (ops & OP_SPEC) {
+                        const double lam = a.lam ? __ldg(a.lam + x) : (x == 0 ? a.lam0 : a.lamc);
+                        double s, cs;
+                        sincos(-a.beta * lam, &s, &cs);
+                        v = cmul(v, make_double2(cs * a.invN, s * a.invN));
+                    }
+                    if (ops & OP_CHIRP) v = cmul(v, chirp(x, a.N));
+                    if (ops & OP_OUTER_TW) v = cmul(v, cmul(Tw[x1], Tw[M1 + c]));  // w_N^{-xl K}, table
+                }
+                slot = v;
+            }
         }
         if (ops & OP_EXPECT) {
             block_reduce2(acc, nrm, red);
@@ -1079,6 +1133,11 @@ ColArgs col_args(const FftPlan *fp) {
     c.big_shift = fp->big_shift;
     c.partials = fp->partials;
     c.sf = fp->col;
+    static int cfast_env = [] {
+        const char *e = getenv("QVA_FFT_CFAST");
+        return e ? atoi(e) : -1;
+    }();
+    c.ops_cfast = cfast_env >= 0 ? cfast_env : (fp->M * 24 > (uint64_t)96 << 20 ? 1 : 0);  // q beyond ~3/4 of L2
     return c;
 }
 RowArgs row_args(const FftPlan *fp, double2 *buf) {
