@@ -51,9 +51,11 @@ constexpr int kLoadU = 8;                         // independent global loads pe
 // A[k >> 5] * B[k & 31], i.e. ceil(n/32) + 32 entries per C
 // (odd, so that the 8 columns' tables of a column block start in distinct bank groups)
 __host__ __device__ constexpr int tw_split_entries(int n) { return (((n + 31) >> 5) + 32) | 1; }
-// column passes: forward tables cw * E; three-level inner passes also the outer twiddle M1 + cw
+// column passes: forward tables cw * E; three-level inner passes also the outer twiddle
+// w^{(x1 M2 + c) K} = A[x1 >> 5] * B[x1 & 31] * C[c]: E + cw entries
 __host__ __device__ constexpr int col_tw_entries(int cw, int M1, bool outer) {
-    return (outer && M1 + cw > cw * tw_split_entries(M1)) ? M1 + cw : cw * tw_split_entries(M1);
+    return (outer && tw_split_entries(M1) + cw > cw * tw_split_entries(M1)) ? tw_split_entries(M1) + cw
+                                                                             : cw * tw_split_entries(M1);
 }
 inline size_t col_smem_bytes(int cw, int M1, bool outer = false) {
     return ((size_t)cw * (M1 + (cw > 1 ? 1 : 0)) + (size_t)col_tw_entries(cw, M1, outer)) * 16;
@@ -549,6 +551,10 @@ struct ColArgs {
 // The arithmetic of one column block (columns c0 .. c0+cwv of matrix mat_y), in shared memory
 // through the addressing policy: [inverse column FFTs] -> elementwise ops at the natural index ->
 // [forward column FFTs + twiddle w_M^{x2 k1}]; expectation partials to slot pslot.
+__device__ __forceinline__ double2 outer_tw(const double2 *Tw, int M1, int x1, int c) {
+    const int nh = (M1 + 31) >> 5, E = tw_split_entries(M1);
+    return cmul(cmul(Tw[x1 >> 5], Tw[nh + (x1 & 31)]), Tw[E + c]);
+}
 template <typename F, typename Ad>
 __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0, int cwv, int mat_y, int pslot,
                                           double *red, const double2 *Tw, const double2 *twp) {
@@ -580,7 +586,7 @@ __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0
                     v = cmul(v, make_double2(cs * a.invN, s * a.invN));
                 }
                 if (ops & OP_CHIRP) v = cmul(v, chirp(x, a.N));
-                if (ops & OP_OUTER_TW) v = cmul(v, cmul(Tw[x1], Tw[M1 + c]));  // w_N^{-xl K}, table
+                if (ops & OP_OUTER_TW) v = cmul(v, outer_tw(Tw, M1, x1, c));  // w_N^{-xl K}, tables
             }
             *slot = v;
         };
@@ -635,7 +641,7 @@ __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0
                         v = cmul(v, make_double2(cs * a.invN, s * a.invN));
                     }
                     if (ops & OP_CHIRP) v = cmul(v, chirp(x, a.N));
-                    if (ops & OP_OUTER_TW) v = cmul(v, cmul(Tw[x1], Tw[M1 + c]));  // w_N^{-xl K}, table
+                    if (ops & OP_OUTER_TW) v = cmul(v, outer_tw(Tw, M1, x1, c));  // w_N^{-xl K}, tables
                 }
                 slot = v;
             }
@@ -676,7 +682,8 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
     const int totw = M1 << a.lcw;  // (x1, c) over the full column width; c >= cwv skipped
     // twiddle tables (their global loads go out with the column block's): forward pass
     // w_M^{C k1} = Tw[c*E + (k1 >> 5)] * Tw[c*E + nh + (k1 & 31)] (C = global column); outer
-    // (three-level inverse) w_N^{-xl K} = Tw[x1] * Tw[M1 + c] (xl = x1*M2 + c0 + c, K = matrix)
+    // (three-level inverse) w_N^{-xl K} = Tw[x1 >> 5] * Tw[nh + (x1 & 31)] * Tw[E + c]
+    // (xl = x1*M2 + c0 + c, K = matrix)
     double2 *Tw = A + (size_t)a.cw * (M1 + (a.cw > 1 ? 1 : 0));
     const int nh = (M1 + 31) >> 5, E = tw_split_entries(M1);
     if (a.do_fwd) {
@@ -688,9 +695,13 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         }
     } else if (a.ops & OP_OUTER_TW) {
         const uint64_t K = (uint64_t)(a.mat_off + blockIdx.y);
-        for (int i = threadIdx.x; i < M1 + cwv; i += blockDim.x)
-            Tw[i] = big_twiddle(a.otw_lo, a.otw_hi, a.otw_shift,
-                                i < M1 ? (uint64_t)i * (uint64_t)M2 * K : (uint64_t)(c0 + i - M1) * K, true);
+        for (int i = threadIdx.x; i < E + cwv; i += blockDim.x) {
+            const int k = i < nh ? (i << 5) : i - nh;  // x1 split (i < E), then the column (i >= E)
+            Tw[i] = (i >= E || k < M1)
+                        ? big_twiddle(a.otw_lo, a.otw_hi, a.otw_shift,
+                                      i < E ? (uint64_t)k * (uint64_t)M2 * K : (uint64_t)(c0 + i - E) * K, true)
+                        : make_double2(1.0, 0.0);
+        }
     }
     const double2 *twp = stage_twiddles(a.tw, a.sf, a.tws, A + a.ts_off);
     // the column block arrives in batches of kLoadU independent loads per thread (one load per
@@ -747,8 +758,8 @@ struct RowArgs {
     SubFft sf;
 };
 
-template <typename F = GenericFft>
-__global__ void __launch_bounds__(kFftThreads, 1) fft_row_kernel(const RowArgs a) {
+template <int NT = kFftThreads, typename F = GenericFft>
+__global__ void __launch_bounds__(NT, kFftThreads / NT) fft_row_kernel(const RowArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     load_roots();
     const int M2 = a.M2;
@@ -902,17 +913,17 @@ using RowKernelFn = void (*)(RowArgs);
 struct CodeletEntry {
     int n;
     ColKernelFn col, col_half;
-    RowKernelFn row;
+    RowKernelFn row, row_half;
 };
 const CodeletEntry kCodelets[] = {
-    {768, fft_col_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_col_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>, fft_row_kernel<Codelet<768, 16, 16, 3>>},
-    {770, fft_col_kernel<kFftThreads, Codelet<770, 2, 5, 7, 11>>, fft_col_kernel<kFftThreads / 2, Codelet<770, 2, 5, 7, 11>>, fft_row_kernel<Codelet<770, 2, 5, 7, 11>>},
-    {810, fft_col_kernel<kFftThreads, Codelet<810, 2, 9, 9, 5>>, fft_col_kernel<kFftThreads / 2, Codelet<810, 2, 9, 9, 5>>, fft_row_kernel<Codelet<810, 2, 9, 9, 5>>},
-    {840, fft_col_kernel<kFftThreads, Codelet<840, 8, 3, 5, 7>>, fft_col_kernel<kFftThreads / 2, Codelet<840, 8, 3, 5, 7>>, fft_row_kernel<Codelet<840, 8, 3, 5, 7>>},
-    {1024, fft_col_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_col_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>, fft_row_kernel<Codelet<1024, 16, 16, 4>>},
-    {2048, fft_col_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_col_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>, fft_row_kernel<Codelet<2048, 16, 16, 8>>},
-    {4096, fft_col_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_col_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>, fft_row_kernel<Codelet<4096, 16, 16, 16>>},
-    {4320, fft_col_kernel<kFftThreads, Codelet<4320, 16, 2, 9, 3, 5>>, fft_col_kernel<kFftThreads / 2, Codelet<4320, 16, 2, 9, 3, 5>>, fft_row_kernel<Codelet<4320, 16, 2, 9, 3, 5>>},
+    {768, fft_col_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_col_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>, fft_row_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_row_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>},
+    {770, fft_col_kernel<kFftThreads, Codelet<770, 2, 5, 7, 11>>, fft_col_kernel<kFftThreads / 2, Codelet<770, 2, 5, 7, 11>>, fft_row_kernel<kFftThreads, Codelet<770, 2, 5, 7, 11>>, fft_row_kernel<kFftThreads / 2, Codelet<770, 2, 5, 7, 11>>},
+    {810, fft_col_kernel<kFftThreads, Codelet<810, 2, 9, 9, 5>>, fft_col_kernel<kFftThreads / 2, Codelet<810, 2, 9, 9, 5>>, fft_row_kernel<kFftThreads, Codelet<810, 2, 9, 9, 5>>, fft_row_kernel<kFftThreads / 2, Codelet<810, 2, 9, 9, 5>>},
+    {840, fft_col_kernel<kFftThreads, Codelet<840, 8, 3, 5, 7>>, fft_col_kernel<kFftThreads / 2, Codelet<840, 8, 3, 5, 7>>, fft_row_kernel<kFftThreads, Codelet<840, 8, 3, 5, 7>>, fft_row_kernel<kFftThreads / 2, Codelet<840, 8, 3, 5, 7>>},
+    {1024, fft_col_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_col_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>, fft_row_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_row_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>},
+    {2048, fft_col_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_col_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>, fft_row_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_row_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>},
+    {4096, fft_col_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_col_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>, fft_row_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_row_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>},
+    {4320, fft_col_kernel<kFftThreads, Codelet<4320, 16, 2, 9, 3, 5>>, fft_col_kernel<kFftThreads / 2, Codelet<4320, 16, 2, 9, 3, 5>>, fft_row_kernel<kFftThreads, Codelet<4320, 16, 2, 9, 3, 5>>, fft_row_kernel<kFftThreads / 2, Codelet<4320, 16, 2, 9, 3, 5>>},
 };
 const CodeletEntry *codelet_for(int n) {
     static int env = [] {
@@ -929,9 +940,10 @@ ColKernelFn col_kernel_for(int n, bool half) {
     if (c) return half ? c->col_half : c->col;
     return half ? fft_col_kernel<kFftThreads / 2> : fft_col_kernel<kFftThreads>;
 }
-RowKernelFn row_kernel_for(int n) {
+RowKernelFn row_kernel_for(int n, bool half = false) {
     const CodeletEntry *c = codelet_for(n);
-    return c ? c->row : fft_row_kernel<>;
+    if (c) return half ? c->row_half : c->row;
+    return half ? fft_row_kernel<kFftThreads / 2> : fft_row_kernel<>;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1308,10 +1320,12 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
     cudaFuncSetAttribute(fft_col_kernel<kFftThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
     cudaFuncSetAttribute(fft_col_kernel<kFftThreads / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
     cudaFuncSetAttribute(fft_row_kernel<>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmemMax);
+    cudaFuncSetAttribute(fft_row_kernel<kFftThreads / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmemMax);
     for (const auto &cl : kCodelets) {
         cudaFuncSetAttribute(cl.col, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
         cudaFuncSetAttribute(cl.col_half, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmemMax);
         cudaFuncSetAttribute(cl.row, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmemMax);
+        cudaFuncSetAttribute(cl.row_half, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmemMax);
     }
     cudaFuncSetAttribute(fft_whole_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * (int)sizeof(double2));
     if (fp->bluestein) {
@@ -1409,13 +1423,23 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
     c.otw_hi = fp->d_big_hi;
     c.otw_shift = fp->big_shift;
     const dim3 gc((fp->Mi2 + c.cw - 1) / c.cw, nmat);
-    const size_t smem_c = with_stage_tw(c, col_smem_bytes(c.cw, fp->Mi1, true), kColSmemMax, c.cw * fp->Mi1);
+    // 256-thread CTAs, two per SM, when the block fits (as for the top-level column pass)
+    bool half = col_smem_bytes(c.cw, fp->Mi1, true) <= kColHalfSmemMax;
+    for (int st = 0; st < fp->col2.ns && half; ++st)
+        if (fp->col2.n / fp->col2.r[st] > nb_of(fp->col2.r[st]) * (kFftThreads / 2)) half = false;
+    static int half_env3 = [] {
+        const char *e = getenv("QVA_FFT_COL256");
+        return e ? atoi(e) : 1;
+    }();
+    half = half && half_env3 != 0;
+    const size_t smem_c = with_stage_tw(c, col_smem_bytes(c.cw, fp->Mi1, true), half ? kColHalfSmemMax : kColSmemMax,
+                                        c.cw * fp->Mi1);
     auto cols = [&](int inv, int ops, int fwd) -> qva_status {
         c.do_inv = inv;
         c.do_fwd = fwd;
         c.ops = ops;
         obs->begin(K_FFT_COL, 32.0 * (double)R * nmat);
-        col_kernel_for(fp->Mi1, false)<<<gc, kFftThreads, smem_c, s>>>(c);
+        col_kernel_for(fp->Mi1, half)<<<gc, half ? kFftThreads / 2 : kFftThreads, smem_c, s>>>(c);
         cudaError_t e = cudaGetLastError();
         obs->end();
         if (e != cudaSuccess) {
@@ -1445,8 +1469,17 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
         w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
     }
     obs->begin(K_FFT_ROW, 32.0 * (double)R * nmat + (r.lambda_perm ? 8.0 * (double)R * nmat : 0.0));
-    const size_t smem_r3 = with_stage_tw(w, row_smem_bytes(fp->rb2, fp->Mi2), kRowSmemMax, fp->rb2 * fp->Mi2);
-    row_kernel_for(fp->Mi2)<<<nmat * fp->Mi1 / fp->rb2, kFftThreads, smem_r3, s>>>(w);
+    // 256-thread CTAs over half the rows, two or more per SM, when the stages fit 256 threads
+    int rbh = 0;
+    for (int x = fp->rb2 / 2; x >= 1 && !rbh; --x)
+        if (((uint64_t)nmat * fp->Mi1) % x == 0) rbh = x;
+    bool rhalf = half_env3 != 0 && rbh >= 1 && row_smem_bytes(rbh, fp->Mi2) <= kColHalfSmemMax;
+    for (int st = 0; st < fp->row.ns && rhalf; ++st)
+        if (fp->row.n / fp->row.r[st] > nb_of(fp->row.r[st]) * (kFftThreads / 2)) rhalf = false;
+    if (rhalf) w.rb = rbh;
+    const size_t smem_r3 = with_stage_tw(w, row_smem_bytes(w.rb, fp->Mi2), rhalf ? kColHalfSmemMax : kRowSmemMax,
+                                         w.rb * fp->Mi2);
+    row_kernel_for(fp->Mi2, rhalf)<<<nmat * fp->Mi1 / w.rb, rhalf ? kFftThreads / 2 : kFftThreads, smem_r3, s>>>(w);
     cudaError_t e = cudaGetLastError();
     obs->end();
     if (e != cudaSuccess) {
