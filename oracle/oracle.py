@@ -23,7 +23,7 @@ __all__ = [
     "evolve_x", "evolve_complete", "evolve_circulant_dense", "lightcone_maxcut",
     "dense_sum_x", "mixer_sparse_dense", "evolve_sparse_dense", "c128",
     "mixer_parity", "evolve_parity", "parity_pairs",
-    "kperm_count", "kperm_unrank", "kperm_cost", "kperm_qualities",
+    "maxcut_q_at", "kperm_count", "kperm_unrank", "kperm_cost", "kperm_qualities",
     "maxcut_term_q", "evolve_ex",
 ]
 
@@ -89,6 +89,20 @@ def maxcut_q(n: int, u, v, w=None) -> np.ndarray:
         wp = _ptr(w)
     lib().or_maxcut_q(n, len(u), _ptr(u), _ptr(v), wp, _ptr(q))
     return q
+
+
+def maxcut_q_at(u, v, w, xs) -> np.ndarray:
+    """q_x = -cut_w(x) at the given indices only (R10; vertex j = bit j of x, R8), for samples of
+    states too large to enumerate.  Edge order summation, like maxcut_q."""
+    out = []
+    for x in xs:
+        x = int(x)
+        c = 0.0
+        for k in range(len(u)):
+            if ((x >> int(u[k])) ^ (x >> int(v[k]))) & 1:
+                c += 1.0 if w is None else float(w[k])
+        out.append(-c)
+    return np.array(out, np.float64)
 
 
 def init_uniform(N: int) -> np.ndarray:

@@ -703,6 +703,7 @@ qva_status exchange_buffers(qva_plan *P, T *src, T *dst) {
 }
 
 qva_status ensure_q_dev(qva_plan *P);
+qva_status ensure_q_alloc(qva_plan *P);
 qva_status exchange_state(qva_plan *P) {
     QVA_TRY(exchange_buffers<double2>(P, P->psi, P->psi_alt));
     std::swap(P->psi, P->psi_alt);
@@ -897,10 +898,24 @@ void drop_qt(qva_plan *P) {
     P->gen_cache.clear();
 }
 
+// q (8 B per amplitude) is allocated on first use: a max-cut plan on the tile path never needs
+// it, which is what lets an n = 33 state (128 GiB) fit one GPU without a 64 GiB q beside it
+qva_status ensure_q_alloc(qva_plan *P) {
+    if (P->q) return QVA_OK;
+    if (cudaMalloc(&P->q, P->arr_n * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("cudaMalloc of the quality vector (" + std::to_string(P->arr_n * sizeof(double)) + " bytes) failed");
+        return QVA_ERR_OUT_OF_MEMORY;
+    }
+    QVA_CUDA_TRY(cudaMemsetAsync(P->q, 0, P->arr_n * sizeof(double), P->stream));
+    return QVA_OK;
+}
+
 // fp64 q of a graph-defined plan, generated on demand (maxcut_q_kernel, 8 B per amplitude); the
 // edge list goes through the pinned upload ring into a persistent buffer, and the stream orders
 // the kernel before every consumer (no host synchronisation)
 qva_status ensure_q_dev(qva_plan *P) {
+    QVA_TRY(ensure_q_alloc(P));
     if (!P->q_graph || P->q_dev_valid) return QVA_OK;
     const int m = P->g_m;
     const size_t need = (size_t)std::max(m, 1) * (2 * sizeof(int32_t) + sizeof(double));
@@ -1798,6 +1813,7 @@ qva_status parity_mix(qva_plan *P, double t) {
 qva_status apply_mixer_impl(qva_plan *P, double beta) {
     if (P->mixer == QVA_MIXER_X) {
         if (use_small(P)) {
+            QVA_TRY(ensure_q_alloc(P));  // the small-state kernel stages q even when it only mixes
             SmallEvolveParams sp{};
             sp.psi = P->psi;
             sp.q = P->q;
@@ -2152,7 +2168,6 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
         return true;
     };
     if (!alloc((void **)&P->psi, P->arr_n * sizeof(double2))) return fail(QVA_ERR_OUT_OF_MEMORY);
-    if (!alloc((void **)&P->q, P->arr_n * sizeof(double))) return fail(QVA_ERR_OUT_OF_MEMORY);
     if (G > 1 && !alloc((void **)&P->psi_alt, P->arr_n * sizeof(double2))) return fail(QVA_ERR_OUT_OF_MEMORY);
     if (!alloc((void **)&P->red, (size_t)P->max_batch * 2 * sizeof(double))) return fail(QVA_ERR_OUT_OF_MEMORY);
     if (!alloc((void **)&P->d_flag, sizeof(int))) return fail(QVA_ERR_OUT_OF_MEMORY);
@@ -2192,7 +2207,6 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
         }
     }
     if (reset_state(P) != QVA_OK) return fail(QVA_ERR_CUDA);
-    if (cudaMemsetAsync(P->q, 0, P->arr_n * sizeof(double), P->stream) != cudaSuccess) return fail(QVA_ERR_CUDA);
     if (cudaStreamSynchronize(P->stream) != cudaSuccess) {
         set_error("plan init failed");
         return fail(QVA_ERR_CUDA);
@@ -2212,6 +2226,7 @@ static qva_status set_q_common(qva_plan *P, const double *src, bool device, uint
     uint64_t lo;
     QVA_TRY(check_range(P, offset, count, &lo));
     if (count == 0) return QVA_OK;
+    QVA_TRY(ensure_q_alloc(P));
     if (P->q_graph) {  // a partial upload overwrites part of the graph's q: materialise it first
         QVA_TRY(ensure_q_dev(P));
         P->q_graph = false;
@@ -2342,6 +2357,7 @@ qva_status qva_set_qualities_permutation(qva_plan *P, int32_t m, int32_t k, cons
     put(frow.data(), frow.size() * sizeof(int));
     put(fab.data(), fab.size() * sizeof(int));
     DeviceGuard dg(P->device);
+    QVA_TRY(ensure_q_alloc(P));
     void *dpack = nullptr;
     QVA_CUDA_TRY(scratch_get(P, &dpack, pack.size()));
     QVA_TRY(upload(P, dpack, pack.data(), pack.size()));

@@ -768,3 +768,33 @@ def test_ex_qaoa_parity_mixer_and_errors(Q):
         _amp_close(P.get_state(), ref)
         with pytest.raises(ValueError):
             P.evolve_ex(theta[:-1])
+
+
+# ---------------------------------------------------------------- maximum single-GPU size ----
+def test_cfg5_family_n33_one_gpu_vs_lightcone_golden(Q):
+    """Maximum size on one B200: n = 33 (2^33 amplitudes, 128 GiB state).  Generated qualities
+    need no 64 GiB q vector (allocated lazily), and with no room for the permuted schedule's
+    second state the plan takes the in-place schedule; <Q> and the norm against the oracle's
+    exact light-cone value (tests/golden/cfg5_n33.json, written by oracle/make_golden.py)."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    if free < 140e9:
+        pytest.skip(f"needs ~140 GB free device memory, have {free / 1e9:.0f} GB")
+    g = json.load(open(os.path.join(GOLD, "cfg5_n33.json")))
+    wl = make_config("cfg5", n_override=33)
+    assert np.allclose(g["theta"], wl.theta, rtol=0, atol=0)
+    with Q.Plan(wl.dim, "x", n_qubits=33) as P:
+        P.set_qualities_maxcut(wl.edges_u, wl.edges_v, wl.weights)
+        P.evolve(wl.theta)
+        _f_close(P.expectation(), g["expectation_lightcone"])
+        assert abs(P.norm2() - 1) < 1e-12
+        # P3 at the largest size: with beta = pi/2, U_M = (-i)^n X^{(x)n}, so after one layer
+        # psi_x = (-i)^33 e^{-i gamma q(~x)} / sqrt(N) and q(~x) = q(x) for a cut; sampled x
+        gam = 0.37
+        P.evolve([gam, math.pi / 2])
+        xs = np.random.default_rng(33).integers(0, 1 << 33, 16)
+        qx = O.maxcut_q_at(wl.edges_u, wl.edges_v, wl.weights, xs)
+        for x, qv in zip(xs, qx):
+            ref = (-1j) ** 33 * np.exp(-1j * gam * qv) / math.sqrt(2.0 ** 33)
+            got = P.get_state(int(x), 1)[0]
+            assert abs(got - ref) <= 1e-10 * abs(ref), (x, got, ref)

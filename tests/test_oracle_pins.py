@@ -39,6 +39,24 @@ def test_maxcut_q_vs_networkx(weighted):
         assert q[x] == pytest.approx(-ref, abs=1e-13)
 
 
+@pytest.mark.parametrize("weighted", [False, True])
+def test_maxcut_q_at_vs_networkx(weighted):
+    """maxcut_q_at (sampled q for huge n) against networkx.cut_size at n = 33 sampled states."""
+    rng = np.random.default_rng(12)
+    n = 33
+    u, v = erdos_renyi_graph(n, 0.15, rng)
+    w = rng.uniform(0, 1, len(u)) if weighted else None
+    G = nx.Graph()
+    G.add_nodes_from(range(n))
+    for k in range(len(u)):
+        G.add_edge(int(u[k]), int(v[k]), weight=float(w[k]) if weighted else 1.0)
+    xs = rng.integers(0, 1 << n, 20)
+    q = O.maxcut_q_at(u, v, w, xs)
+    for x, qv in zip(xs, q):
+        S = [j for j in range(n) if (int(x) >> j) & 1]
+        assert qv == pytest.approx(-nx.cut_size(G, S, weight="weight"), abs=1e-12)
+
+
 def test_maxcut_q_single_edge_spec_example():
     """SPEC.md:446 single edge (0,1), n=2: equal-bit states are uncut -> q = -(0,1,1,0)."""
     q = O.maxcut_q(2, [0], [1])
