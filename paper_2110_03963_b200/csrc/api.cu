@@ -1417,6 +1417,11 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
     const int qbytes = gen ? gen : (P->q_mode == 1 ? 1 : (P->q_mode == 2 ? 2 : 8));
     int j = 0;
     bool first = true;
+    bool exchanged = false;  // the previous pass already wrote the exchanged layout (fused exchange)
+    static int g_fuse_x = [] {
+        const char *e = getenv("QVA_FUSE_EXCHANGE");
+        return e ? atoi(e) : 1;
+    }();
     for (size_t pi = 0; pi < passes.size(); ++pi) {
         const PassPlan &pp = passes[pi];
         if (pp.exchange) {
@@ -1424,9 +1429,28 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
                 set_error("internal: exchange in batched pass list");
                 return QVA_ERR_INVALID_ARGUMENT;
             }
+            if (exchanged) {
+                exchanged = false;
+                continue;
+            }
             QVA_TRY(exchange_state(P));
             psi_base = P->psi;
             continue;
+        }
+        // global <-> local exchange fused into the store of the pass before it (virtual shards):
+        // the exchange swaps the physical bit fields [L-g, L) and [L, L+g), which the tile's TMA
+        // store applies as an output bit permutation into psi_alt -- no transpose pass
+        std::vector<int> xbit;
+        if (g_fuse_x && !pp.permuted && batch == 1 && P->G > 1 && P->world == 1 && pi + 1 < passes.size() &&
+            passes[pi + 1].exchange && P->psi_alt) {
+            xbit.resize(n_phys);
+            for (int b = 0; b < n_phys; ++b) xbit[b] = b;
+            for (int i = 0; i < P->gbits; ++i) {
+                xbit[P->L - P->gbits + i] = P->L + i;
+                xbit[P->L + i] = P->L - P->gbits + i;
+            }
+            // the permuted store must stay one <= 5-D TMA box (else the transpose pass runs)
+            if (tile_tma_dims(P->sets[pp.set].data(), n_phys, xbit.data()) > 5) xbit.clear();
         }
         TilePassParams tp;
         memset(&tp, 0, sizeof(tp));
@@ -1464,7 +1488,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         const double2 *psi_in = (first && init_mode == 2) ? P->psi0 : psi_base;
         tp.init = (first && init_mode == 1) ? 1 : 0;
         // permuted passes write out of place (except a first pass, whose input is not psi_base)
-        const bool swap_after = pp.permuted && !(first && init_mode != 0);
+        const bool swap_after = (pp.permuted && !(first && init_mode != 0)) || !xbit.empty();
         if (swap_after) tp.psi_out = P->psi_alt;
         tp.amp0 = 1.0 / sqrt((double)P->N);
         const bool needs_q = pp.phase >= 0 || pp.expect;
@@ -1516,17 +1540,17 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         // every tile shape; env QVA_TSTORE=0 selects the register stores for comparison)
         tp.tma_store = (g_tstore >= 0) ? g_tstore : 1;
         CUtensorMap map, map_out;
-        if (pp.permuted) tp.tma_store = 1;  // the permuted store is a TMA store map
+        if (pp.permuted || !xbit.empty()) tp.tma_store = 1;  // the permuted store is a TMA store map
+        const int *obit = pp.permuted ? pp.obit.data() : (xbit.empty() ? nullptr : xbit.data());
         {
             // tensor maps depend on (tile bits, store permutation, buffers, sizes): encoded once
             std::vector<int64_t> key = {(int64_t)(uintptr_t)psi_in, (int64_t)(uintptr_t)tp.psi_out, n_phys, batch};
             key.insert(key.end(), s.begin(), s.end());
-            if (pp.permuted) key.insert(key.end(), pp.obit.begin(), pp.obit.end());
+            if (obit) key.insert(key.end(), obit, obit + n_phys);
             auto it = P->tmap_cache.find(key);
             if (it == P->tmap_cache.end()) {
                 qva_plan::TmEntry te;
-                QVA_TRY(make_tile_tensor_maps(psi_in, tp.psi_out, n_phys, batch, tp,
-                                              pp.permuted ? pp.obit.data() : nullptr, &te.in, &te.out));
+                QVA_TRY(make_tile_tensor_maps(psi_in, tp.psi_out, n_phys, batch, tp, obit, &te.in, &te.out));
                 memcpy(te.dim_src, tp.dim_src, sizeof(te.dim_src));
                 memcpy(te.dim_w, tp.dim_w, sizeof(te.dim_w));
                 te.member_dim = tp.member_dim;
@@ -1565,6 +1589,10 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         if (swap_after) {
             std::swap(P->psi, P->psi_alt);
             psi_base = P->psi;
+        }
+        if (!xbit.empty()) {
+            P->layout ^= 1;  // what exchange_state would have done
+            exchanged = true;
         }
         if (pp.expect) {
             ProfScope ps(P, K_REDUCE, 16.0 * nslot * batch);
