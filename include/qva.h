@@ -84,7 +84,10 @@ typedef struct {
                                 qualities inside the tile passes at every size (default: from 2^26
                                 amplitudes).  reserved[2]: 1 =
                                 circulant mixer: three-level FFT split where one exists (tests; used
-                                anyway above 8192^2 states).  Others must be 0. */
+                                anyway above 8192^2 states).  reserved[3]: 1 = virtual shards run
+                                the global<->local exchange through the peer-store path of real
+                                shards (each virtual shard's buffer as its "peer"; tests the code
+                                multi-GPU plans use).  Others must be 0. */
 } qva_plan_desc;
 
 /* ---- lifecycle (Table 1 plan / destroy) ------------------------------------ */

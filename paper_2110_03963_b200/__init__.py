@@ -207,7 +207,8 @@ class Plan:
     def __init__(self, dim: int, mixer: str = "x", n_qubits: int = -1, rank: int = 0, world: int = 1,
                  nccl_id: Optional[bytes] = None, device: int = 0, virtual_shards: int = 1,
                  stream: Optional[int] = None, max_batch: int = 1, replicated: bool = False,
-                 qgen_f64_always: bool = False, fft_three_level: bool = False):
+                 qgen_f64_always: bool = False, fft_three_level: bool = False,
+                 peer_store_exchange: bool = False):
         self._h = ctypes.c_void_p()
         self._id_buf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         d = PlanDesc()
@@ -224,6 +225,7 @@ class Plan:
         d.reserved[0] = 1 if replicated else 0
         d.reserved[1] = 1 if qgen_f64_always else 0
         d.reserved[2] = 1 if fft_three_level else 0
+        d.reserved[3] = 1 if peer_store_exchange else 0
         _call("qva_plan_create", ctypes.byref(d), ctypes.byref(self._h))
         self.dim, self.mixer, self.world, self.rank = dim, mixer, world, rank
 

@@ -466,6 +466,12 @@ struct qva_plan {
     // ex-QAOA (R25): during one tile-path evolution, the per-layer phase weights
     // gamma_{i,e} w_e ([p][g_m], host); phase passes then use records of those weights
     const double *ex_w = nullptr;
+    // fused peer-store exchange (world > 1): both state buffers of every rank, IPC-mapped
+    // (index 0: the buffer that was psi at creation, 1: psi_alt); d_bar: barrier word
+    bool ipc_ok = false;
+    double2 *ipc_own[2] = {nullptr, nullptr};
+    double2 *ipc_peer[2][kMaxPeers] = {};
+    int *d_bar = nullptr;
     double *q_ex = nullptr;                // step path: per-layer generated term sum
     void *d_ex_edges = nullptr;            // step path: u, v, per-layer weights
     size_t ex_edge_cap = 0;
@@ -1172,6 +1178,10 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
         cudaFree(P->d_gen_edges);
     cudaFree(P->q_ex);
     cudaFree(P->d_ex_edges);
+    for (int k = 0; k < 2; ++k)
+        for (int t = 0; t < kMaxPeers; ++t)
+            if (P->ipc_peer[k][t] && P->ipc_peer[k][t] != P->ipc_own[k]) cudaIpcCloseMemHandle(P->ipc_peer[k][t]);
+    cudaFree(P->d_bar);
         P->d_gen_edges = nullptr;
         QVA_CUDA_TRY(cudaMalloc(&P->d_gen_edges, eb));
         P->gen_edge_cap = eb;
@@ -1452,6 +1462,17 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             // the permuted store must stay one <= 5-D TMA box (else the transpose pass runs)
             if (tile_tma_dims(P->sets[pp.set].data(), n_phys, xbit.data()) > 5) xbit.clear();
         }
+        // real shards: the same exchange done by stores into the receiving ranks' buffers (peer
+        // memory); needs the chunk bits [L-g, L) outside the tile (they name the receiver)
+        bool xpeer = false;
+        const bool xvirt = P->world == 1 && P->d.reserved[3] != 0;  // test mode: virtual shards as peers
+        if (xvirt) xbit.clear();
+        if (g_fuse_x && (P->ipc_ok || xvirt) && !pp.permuted && batch == 1 && P->G > 1 && P->G <= kMaxPeers &&
+            pi + 1 < passes.size() && passes[pi + 1].exchange) {
+            xpeer = true;
+            for (int k = 0; k < kTileBits; ++k)
+                if (P->sets[pp.set][k] >= P->L - P->gbits) xpeer = false;
+        }
         TilePassParams tp;
         memset(&tp, 0, sizeof(tp));
         const std::vector<int> &s = pp.permuted ? pp.tbits : P->sets[pp.set];
@@ -1488,7 +1509,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         const double2 *psi_in = (first && init_mode == 2) ? P->psi0 : psi_base;
         tp.init = (first && init_mode == 1) ? 1 : 0;
         // permuted passes write out of place (except a first pass, whose input is not psi_base)
-        const bool swap_after = (pp.permuted && !(first && init_mode != 0)) || !xbit.empty();
+        const bool swap_after = (pp.permuted && !(first && init_mode != 0)) || !xbit.empty() || xpeer;
         if (swap_after) tp.psi_out = P->psi_alt;
         tp.amp0 = 1.0 / sqrt((double)P->N);
         const bool needs_q = pp.phase >= 0 || pp.expect;
@@ -1542,6 +1563,19 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         CUtensorMap map, map_out;
         if (pp.permuted || !xbit.empty()) tp.tma_store = 1;  // the permuted store is a TMA store map
         const int *obit = pp.permuted ? pp.obit.data() : (xbit.empty() ? nullptr : xbit.data());
+        if (xpeer) {
+            tp.tma_store = 0;  // register stores: each tile's destination is a peer pointer
+            if (xvirt) {  // shard t's buffer is psi_alt's t-th 2^L block
+                for (int t = 0; t < P->G; ++t) tp.xpeer[t] = P->psi_alt + ((uint64_t)t << P->L);
+                tp.xvirt = 1;
+            } else {
+                const int k = (P->psi_alt == P->ipc_own[0]) ? 0 : 1;  // every rank swaps in lockstep
+                for (int t = 0; t < P->world; ++t) tp.xpeer[t] = P->ipc_peer[k][t];
+            }
+            tp.xg = P->G;
+            tp.xrank = P->rank;
+            tp.xshift = P->L - P->gbits;
+        }
         {
             // tensor maps depend on (tile bits, store permutation, buffers, sizes): encoded once
             std::vector<int64_t> key = {(int64_t)(uintptr_t)psi_in, (int64_t)(uintptr_t)tp.psi_out, n_phys, batch};
@@ -1590,7 +1624,13 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             std::swap(P->psi, P->psi_alt);
             psi_base = P->psi;
         }
-        if (!xbit.empty()) {
+        if (xpeer && !xvirt) {
+            // every rank's stores into our buffer are done once every rank's pass has finished:
+            // a one-word all-reduce on the stream is that barrier
+            QVA_CUDA_TRY(cudaMemsetAsync(P->d_bar, 0, sizeof(int), P->stream));
+            QVA_NCCL_TRY(ncclAllReduce(P->d_bar, P->d_bar, 1, ncclInt32, ncclSum, P->comm, P->stream));
+        }
+        if (!xbit.empty() || xpeer) {
             P->layout ^= 1;  // what exchange_state would have done
             exchanged = true;
         }
@@ -1700,6 +1740,65 @@ qva_status run_passes_graph(qva_plan *P, const std::vector<PassPlan> &passes, co
     P->psi = g.psi_after;
     P->psi_alt = g.alt_after;
     return QVA_OK;
+}
+
+// Fused exchange over peer memory: every rank's two state buffers are exported as CUDA IPC
+// handles, all-gathered over the plan's NCCL communicator and mapped (NVLink P2P), so the pass
+// before a global<->local exchange can store each tile straight into its receiving rank's
+// buffer.  Any failure leaves ipc_ok = false and the exchange runs as NCCL send/recv.
+void setup_peer_exchange(qva_plan *P) {
+    static int env = [] {
+        const char *e = getenv("QVA_FUSE_EXCHANGE");
+        return e ? atoi(e) : 1;
+    }();
+    if (!env || P->world > kMaxPeers || !P->psi || !P->psi_alt || !P->comm) return;
+    P->ipc_own[0] = P->psi;
+    P->ipc_own[1] = P->psi_alt;
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    std::vector<unsigned char> mine(2 * hb), all(2 * hb * P->world);
+    if (cudaIpcGetMemHandle((cudaIpcMemHandle_t *)mine.data(), P->psi) != cudaSuccess ||
+        cudaIpcGetMemHandle((cudaIpcMemHandle_t *)(mine.data() + hb), P->psi_alt) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    unsigned char *dbuf = nullptr;
+    if (cudaMalloc(&dbuf, 2 * hb * (P->world + 1)) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    bool ok = cudaMemcpy(dbuf, mine.data(), 2 * hb, cudaMemcpyHostToDevice) == cudaSuccess &&
+              ncclAllGather(dbuf, dbuf + 2 * hb, 2 * hb, ncclChar, P->comm, P->stream) == ncclSuccess &&
+              cudaStreamSynchronize(P->stream) == cudaSuccess &&
+              cudaMemcpy(all.data(), dbuf + 2 * hb, all.size(), cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(dbuf);
+    for (int t = 0; ok && t < P->world; ++t)
+        for (int k = 0; ok && k < 2; ++k) {
+            if (t == P->rank) {
+                P->ipc_peer[k][t] = P->ipc_own[k];
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            memcpy(&h, all.data() + (2 * t + k) * hb, hb);
+            void *ptr = nullptr;
+            ok = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+            P->ipc_peer[k][t] = (double2 *)ptr;
+        }
+    if (ok) ok = cudaMalloc(&P->d_bar, sizeof(int)) == cudaSuccess;
+    // every rank must agree, or the ranks would run different exchange code
+    int flag = ok ? 1 : 0, *dflag = nullptr;
+    if (cudaMalloc(&dflag, sizeof(int)) == cudaSuccess) {
+        cudaMemcpy(dflag, &flag, sizeof(int), cudaMemcpyHostToDevice);
+        if (ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, P->comm, P->stream) != ncclSuccess ||
+            cudaStreamSynchronize(P->stream) != cudaSuccess)
+            flag = 0;
+        else
+            cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost);
+        cudaFree(dflag);
+    } else {
+        flag = 0;
+    }
+    cudaGetLastError();
+    P->ipc_ok = flag == 1;
 }
 
 qva_status allreduce_host(qva_plan *P, double *vals, int n) {
@@ -2234,6 +2333,7 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
             return fail(QVA_ERR_NCCL);
         }
     }
+    if (d.world > 1 && d.mixer == QVA_MIXER_X) setup_peer_exchange(P);  // falls back to NCCL on failure
     if (reset_state(P) != QVA_OK) return fail(QVA_ERR_CUDA);
     if (cudaStreamSynchronize(P->stream) != cudaSuccess) {
         set_error("plan init failed");

@@ -671,7 +671,19 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
         uint64_t base = member * P.member_stride;
 #pragma unroll
         for (int r = 0; r < kMaxRuns; ++r) base |= ((t >> P.run_src[r]) & P.run_mask[r]) << P.run_dst[r];
-        double2 *dst = P.psi_out + base + tbase;
+        double2 *out = P.psi_out;
+        if (P.xg) {  // fused exchange: the tile's chunk (never a tile bit) names the receiving rank
+            const uint64_t m = (uint64_t)(P.xg - 1) << P.xshift;
+            uint64_t src = (uint64_t)P.xrank;
+            if (P.xvirt) {
+                const int hs = P.xshift + __ffs(P.xg) - 1;  // = L: the virtual shard bits
+                src = (base >> hs) & (uint64_t)(P.xg - 1);
+                base &= (1ull << hs) - 1;
+            }
+            out = P.xpeer[(base & m) >> P.xshift];
+            base = (base & ~m) | (src << P.xshift);
+        }
+        double2 *dst = out + base + tbase;
 #pragma unroll
         for (int e = 0; e < kAPT; ++e) {
             uint64_t o = 0;
@@ -682,6 +694,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
         }
     }
     if (tstore && c == 0) bulk_wait_all();
+    if (P.xg) __threadfence_system();  // peer stores visible before the host-side barrier
     if (QB > 0 && kExpect && P.expect && acc_member >= 0) flush_partial(P, acc_member, warp, lane, acc, nrm);
 }
 

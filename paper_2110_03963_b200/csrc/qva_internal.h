@@ -54,6 +54,7 @@ constexpr int kMaxGroups = 3;
 constexpr int kSmallMaxQubits = 12;           // whole-state-in-one-CTA path
 constexpr int kQGenInt = 3;                   // tile-pass q mode: generated MaxCut q, unit weights
 constexpr int kQGenF64 = 9;                   // tile-pass q mode: generated MaxCut q, fp64 weights
+constexpr int kMaxPeers = 8;                  // fused peer-store exchange: ranks per plan
 
 // Register group: which tile-local bits the 5 register-index bits (ebit) and the 7 consumer
 // thread-index bits (tbit) address.  Chosen on the host so that every 8-lane phase of a
@@ -121,6 +122,15 @@ struct TilePassParams {
     const void *gen_thr;     // [128][8] int / double: per consumer thread {C, beta[5]} of group gq
     const void *gen_G;       // [32] int / double: G(e) over the 5 register bits of group gq
     int gen_m;               // number of edges (integer mode: qmin = -gen_m)
+    // global <-> local exchange fused into this pass's stores (world > 1, register-store path):
+    // an element whose output local index has chunk t = bits [xshift, xshift + log2 xg) goes to
+    // rank t's receive buffer xpeer[t] (peer memory over NVLink, IPC-mapped) at the same index
+    // with those bits replaced by xrank -- the all-to-all of COMM-psi done by
+    // the stores themselves.  xg = 0: ordinary local stores.
+    double2 *xpeer[kMaxPeers];
+    int xg, xrank, xshift;
+    int xvirt;               // virtual shards: the sending shard is physical bits [xshift + log2 xg,
+                             // + log2 xg) (stripped from the index) instead of xrank
 };
 
 // Compile-time pass programs (kernels_tile.cu): group sequence g[0..n), which steps rotate,

@@ -492,17 +492,22 @@ def test_cfg5_family_n30_vs_lightcone_golden(Q):
 
 
 # ---------------------------------------------------------------- sharded schedule ----
-@pytest.mark.parametrize("n,G,p", [(14, 2, 1), (15, 4, 2), (16, 8, 3), (20, 8, 2), (21, 2, 3)])
-def test_virtual_shards_vs_oracle(Q, n, G, p):
-    """COMM-psi sharding with G shards on one GPU (loopback exchange):
-    same schedule, layouts and exchange mapping as the multi-GPU path."""
+@pytest.mark.parametrize("n,G,p,peer", [(14, 2, 1, False), (15, 4, 2, False), (16, 8, 3, False), (20, 8, 2, False),
+                                        (21, 2, 3, False), (14, 2, 1, True), (16, 8, 3, True), (20, 4, 2, True),
+                                        (22, 8, 2, True)])
+def test_virtual_shards_vs_oracle(Q, n, G, p, peer):
+    """COMM-psi sharding with G shards on one GPU: same schedule, layouts and
+    exchange mapping as the multi-GPU path.  The exchange is fused into the preceding pass's
+    store -- as an output bit permutation (peer=False), or (peer=True) through the register
+    peer-store path real shards use, each virtual shard's block of psi_alt standing in for the
+    receiving rank's buffer."""
     rng = np.random.default_rng(n * G)
     u, v = random_regular_graph(n, 4, rng)
     w = rng.uniform(0, 1, len(u))
     theta = rng.uniform(0, math.pi, 2 * p)
     q = O.maxcut_q(n, u, v, w)
     ref = O.evolve_x(n, q, theta)
-    with Q.Plan(1 << n, "x", n_qubits=n, virtual_shards=G) as P:
+    with Q.Plan(1 << n, "x", n_qubits=n, virtual_shards=G, peer_store_exchange=peer) as P:
         P.set_qualities(q)  # generic path: layout-B q is built by the exchange (C7)
         P.evolve(theta)
         _f_close(P.expectation(), O.expectation(ref, q))
