@@ -472,6 +472,8 @@ struct qva_plan {
     double2 *ipc_own[2] = {nullptr, nullptr};
     double2 *ipc_peer[2][kMaxPeers] = {};
     int *d_bar = nullptr;
+    unsigned long long *d_ctr = nullptr;  // per-pass tile claim counters (dynamic tile order)
+    int ctr_cap = 0;
     double *q_ex = nullptr;                // step path: per-layer generated term sum
     void *d_ex_edges = nullptr;            // step path: u, v, per-layer weights
     size_t ex_edge_cap = 0;
@@ -1176,12 +1178,6 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
     const size_t eb = (tt.size() + tb.size()) * (sizeof(int2) + sizeof(double)) + 16;
     if (P->gen_edge_cap < eb) {  // stream order keeps one staging buffer safe across entries
         cudaFree(P->d_gen_edges);
-    cudaFree(P->q_ex);
-    cudaFree(P->d_ex_edges);
-    for (int k = 0; k < 2; ++k)
-        for (int t = 0; t < kMaxPeers; ++t)
-            if (P->ipc_peer[k][t] && P->ipc_peer[k][t] != P->ipc_own[k]) cudaIpcCloseMemHandle(P->ipc_peer[k][t]);
-    cudaFree(P->d_bar);
         P->d_gen_edges = nullptr;
         QVA_CUDA_TRY(cudaMalloc(&P->d_gen_edges, eb));
         P->gen_edge_cap = eb;
@@ -1425,6 +1421,21 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
     if (any_expect) QVA_TRY(ensure_partials(P, (uint64_t)nslot * batch));
     const int n_phys = ilog2(P->arr_n);
     const int qbytes = gen ? gen : (P->q_mode == 1 ? 1 : (P->q_mode == 2 ? 2 : 8));
+    // dynamic tile claiming: one zeroed counter per tile pass (one memset for the sequence)
+    static int g_dyn = [] {
+        const char *e = getenv("QVA_DYN");
+        return e ? atoi(e) : 1;
+    }();
+    if (g_dyn) {
+        if (P->ctr_cap < n_tile_passes) {
+            cudaFree(P->d_ctr);
+            P->d_ctr = nullptr;
+            const int cap = std::max(n_tile_passes, 64);
+            QVA_CUDA_TRY(cudaMalloc(&P->d_ctr, cap * sizeof(unsigned long long)));
+            P->ctr_cap = cap;
+        }
+        QVA_CUDA_TRY(cudaMemsetAsync(P->d_ctr, 0, n_tile_passes * sizeof(unsigned long long), P->stream));
+    }
     int j = 0;
     bool first = true;
     bool exchanged = false;  // the previous pass already wrote the exchanged layout (fused exchange)
@@ -1548,6 +1559,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             tp.gq = -1;
         }
         tp.angles = P->d_angles + (size_t)j * batch;
+        tp.work_ctr = (g_dyn == 1 || (g_dyn > 1 && ((g_dyn >> 1) >> j) & 1)) ? P->d_ctr + j : nullptr;
         tp.expect = pp.expect ? 1 : 0;
         tp.partials = P->partials;
         tp.apply_scale = apply_scale[j];
@@ -2174,6 +2186,11 @@ qva_status qva_plan_destroy(qva_plan *P) {
     cudaFree(P->d_gen_edges);
     cudaFree(P->q_ex);
     cudaFree(P->d_ex_edges);
+    for (int k = 0; k < 2; ++k)
+        for (int t = 0; t < kMaxPeers; ++t)
+            if (P->ipc_peer[k][t] && P->ipc_peer[k][t] != P->ipc_own[k]) cudaIpcCloseMemHandle(P->ipc_peer[k][t]);
+    cudaFree(P->d_bar);
+    cudaFree(P->d_ctr);
     cudaFree(P->scratch);
     cudaFree(P->small_batch);
     for (auto &e : P->pool) cudaFree(e.second);

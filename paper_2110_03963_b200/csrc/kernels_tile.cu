@@ -387,7 +387,7 @@ constexpr size_t tile_smem_bytes() {
     return (size_t)STAGES * (kTile * sizeof(double2) + (size_t)q_stage_bytes<QB>()) +
            (q_table<QB>() ? (size_t)kTabSmemMax * kTabRep * sizeof(double2) : 0) +
            (q_gen<QB>() ? 32 * sizeof(double) : 0) + (QB == kQGenF64 ? kGfMembers * 32 * sizeof(double2) : 0) +
-           2 * STAGES * sizeof(uint64_t) +
+           4 * STAGES * sizeof(uint64_t) +  // barriers + claimed items
            (size_t)kMaxBatchSmem * sizeof(PassAngles);
 }
 
@@ -454,12 +454,14 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                                                 (q_gen<QB>() ? 32 * sizeof(double) : 0));
     uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(gf_s) +
                                                   (QB == kQGenF64 ? kGfMembers * 32 * sizeof(double2) : 0));
-    PassAngles *ang_s = reinterpret_cast<PassAngles *>(bars + 2 * STAGES);  // [batch]
+    uint64_t *items_s = bars + 2 * STAGES;  // item claimed for each barrier slot
+    PassAngles *ang_s = reinterpret_cast<PassAngles *>(items_s + 2 * STAGES);  // [batch]
     // full[round & 1][stage]: item `it` is round it / STAGES of stage it % STAGES.  Rounds r and
     // r - 2 of a stage belong to the same warpgroup, so each barrier is waited by one warpgroup
     // at most one phase ahead (no parity aliasing).
     const uint32_t full0 = smem_u32(bars);
-    auto full_bar = [&](uint32_t it) { return full0 + 8 * (((it / STAGES) & 1) * STAGES + it % STAGES); };
+    auto slot_of = [&](uint32_t it) { return ((it / STAGES) & 1) * STAGES + it % STAGES; };
+    auto full_bar = [&](uint32_t it) { return full0 + 8 * slot_of(it); };
 
     constexpr TileProg D = prog_def<PROG>();
     constexpr bool kPhase = PROG == 0 ? QB > 0 : D.phase_k >= 0;
@@ -467,8 +469,11 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const uint64_t n_items = P.n_tiles * (uint64_t)P.batch;
-    // item order: interleaved over CTAs (CTA b takes b, b + grid, ...: the in-flight tiles of the
-    // whole grid are neighbours; contiguous per-CTA ranges measured no different)
+    // item order: claimed dynamically from P.work_ctr when set (CTA iteration j takes the next
+    // free tile, so the in-flight tiles of the grid stay neighbours and SMs that stream faster
+    // take more: static shares left some SMs idle for up to 20 % of a window pass); else
+    // interleaved over CTAs (CTA b takes b, b + grid, ...)
+    const bool dyn = P.work_ctr != nullptr;
     const uint32_t n_it = (uint32_t)((n_items > blockIdx.x) ? (n_items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
     auto item_of = [&](uint32_t j) -> uint64_t { return blockIdx.x + (uint64_t)j * gridDim.x; };
     const bool load_psi = (P.init != 1);
@@ -480,11 +485,21 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     const unsigned char *qt = reinterpret_cast<const unsigned char *>(P.qt);
 
     // TMA traffic for CTA iteration j (item blockIdx.x + j * gridDim.x)
+    // A claimed item past the end is a sentinel: the barrier completes with no data and the
+    // consumer stops.  Per warpgroup (iteration parity) the claims happen in iteration order, so
+    // once a warpgroup meets a sentinel every later iteration of it is one too.
     auto issue = [&](uint32_t j) {
-        const uint64_t item = item_of(j);
+        const uint64_t item = dyn ? atomicAdd(P.work_ctr, 1ull) : item_of(j);
         const uint64_t member = item >> P.log2_tiles, t = item & (P.n_tiles - 1);
         const int s = j % STAGES;
         const uint32_t bar = full_bar(j);
+        if (dyn) {
+            items_s[slot_of(j)] = item;
+            if (item >= n_items) {
+                mbar_expect_tx(bar, 0);
+                return;
+            }
+        }
         mbar_expect_tx(bar, bytes);
         if (load_psi) {
             int cc[5];
@@ -524,7 +539,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     __syncthreads();
     if (tid == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-        for (uint32_t j = 0; j < (uint32_t)STAGES && j < n_it; ++j) issue(j);
+        for (uint32_t j = 0; j < (uint32_t)STAGES && (dyn || j < n_it); ++j) issue(j);
     }
 
     // ---------------- warpgroup wg takes CTA iterations wg, wg + 2, ... ----------------
@@ -539,9 +554,19 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     double acc = 0.0, nrm = 0.0;
     int64_t acc_member = -1;
 
-    for (uint32_t it = wg; it < n_it; it += kWG) {
-        const uint64_t item = item_of(it);
+    for (uint32_t it = wg; dyn || it < n_it; it += kWG) {
         const int s = it % STAGES;
+        uint64_t item;
+        if (dyn) {
+            mbar_wait(full_bar(it), ((it / STAGES) >> 1) & 1);
+            item = items_s[slot_of(it)];
+            if (item >= n_items) {  // keep the claim chain going for the other warpgroup, then stop
+                if (c == 0) issue(it + STAGES);
+                break;
+            }
+        } else {
+            item = item_of(it);
+        }
         const uint64_t member = item >> P.log2_tiles;
         const uint64_t t = item & (P.n_tiles - 1);
         const PassAngles *ang = ang_s + member;
@@ -553,14 +578,14 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
 
         const uint32_t buf = smem_u32(psi_s + (size_t)s * kTile);
         const unsigned char *qs = q_s + (size_t)s * QSB;
-        mbar_wait(full_bar(it), ((it / STAGES) >> 1) & 1);
+        if (!dyn) mbar_wait(full_bar(it), ((it / STAGES) >> 1) & 1);
 
         // hand stage s back: the whole warpgroup is done with it, so one thread refills it with
         // iteration it + STAGES (the async-proxy write must follow our generic-proxy accesses)
         auto release = [&]() {
             fence_proxy_async();
             wg_sync(wg);
-            if (c == 0 && it + STAGES < n_it) issue(it + STAGES);
+            if (c == 0 && (dyn || it + STAGES < n_it)) issue(it + STAGES);
         };
         double2 v[kAPT];
         if (!load_psi) {
@@ -658,7 +683,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                 tma_coords(P, member, t, cc);
                 tma_store_5d(&tmap_out, buf, cc);
                 bulk_wait_read_all();
-                if (it + STAGES < n_it) issue(it + STAGES);
+                if (dyn || it + STAGES < n_it) issue(it + STAGES);
             }
             continue;
         }

@@ -127,6 +127,8 @@ struct TilePassParams {
     // rank t's receive buffer xpeer[t] (peer memory over NVLink, IPC-mapped) at the same index
     // with those bits replaced by xrank -- the all-to-all of COMM-psi done by
     // the stores themselves.  xg = 0: ordinary local stores.
+    unsigned long long *work_ctr;  // zeroed per launch: tiles are claimed dynamically (atomicAdd), so
+                                   // SMs that stream faster take more tiles (no end-of-pass tail)
     double2 *xpeer[kMaxPeers];
     int xg, xrank, xshift;
     int xvirt;               // virtual shards: the sending shard is physical bits [xshift + log2 xg,
