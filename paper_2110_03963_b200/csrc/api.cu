@@ -1766,23 +1766,22 @@ void setup_peer_exchange(qva_plan *P) {
     if (!env || P->world > kMaxPeers || !P->psi || !P->psi_alt || !P->comm) return;
     P->ipc_own[0] = P->psi;
     P->ipc_own[1] = P->psi_alt;
+    // every rank takes part in both collectives below whatever happens locally (a rank that
+    // skipped one would leave the others blocked in it); the final min-reduce decides
     const size_t hb = sizeof(cudaIpcMemHandle_t);
-    std::vector<unsigned char> mine(2 * hb), all(2 * hb * P->world);
-    if (cudaIpcGetMemHandle((cudaIpcMemHandle_t *)mine.data(), P->psi) != cudaSuccess ||
-        cudaIpcGetMemHandle((cudaIpcMemHandle_t *)(mine.data() + hb), P->psi_alt) != cudaSuccess) {
-        cudaGetLastError();
-        return;
-    }
-    unsigned char *dbuf = nullptr;
-    if (cudaMalloc(&dbuf, 2 * hb * (P->world + 1)) != cudaSuccess) {
-        cudaGetLastError();
-        return;
-    }
-    bool ok = cudaMemcpy(dbuf, mine.data(), 2 * hb, cudaMemcpyHostToDevice) == cudaSuccess &&
-              ncclAllGather(dbuf, dbuf + 2 * hb, 2 * hb, ncclChar, P->comm, P->stream) == ncclSuccess &&
-              cudaStreamSynchronize(P->stream) == cudaSuccess &&
-              cudaMemcpy(all.data(), dbuf + 2 * hb, all.size(), cudaMemcpyDeviceToHost) == cudaSuccess;
-    cudaFree(dbuf);
+    std::vector<unsigned char> mine(2 * hb, 0), all(2 * hb * P->world, 0);
+    bool ok = cudaIpcGetMemHandle((cudaIpcMemHandle_t *)mine.data(), P->psi) == cudaSuccess &&
+              cudaIpcGetMemHandle((cudaIpcMemHandle_t *)(mine.data() + hb), P->psi_alt) == cudaSuccess;
+    cudaGetLastError();
+    // staging in the (not yet used) receive buffer: no allocation that could fail on one rank only
+    unsigned char *dbuf = reinterpret_cast<unsigned char *>(P->psi_alt);
+    const bool g = cudaMemcpy(dbuf, mine.data(), 2 * hb, cudaMemcpyHostToDevice) == cudaSuccess &&
+                   ncclAllGather(dbuf, dbuf + 2 * hb, 2 * hb, ncclChar, P->comm, P->stream) == ncclSuccess &&
+                   cudaStreamSynchronize(P->stream) == cudaSuccess &&
+                   cudaMemcpy(all.data(), dbuf + 2 * hb, all.size(), cudaMemcpyDeviceToHost) == cudaSuccess;
+    ok = ok && g;
+    // a rank whose handles failed sent zeros: opening those fails here, and the vote below
+    // turns the fused path off everywhere
     for (int t = 0; ok && t < P->world; ++t)
         for (int k = 0; ok && k < 2; ++k) {
             if (t == P->rank) {
@@ -1797,18 +1796,13 @@ void setup_peer_exchange(qva_plan *P) {
         }
     if (ok) ok = cudaMalloc(&P->d_bar, sizeof(int)) == cudaSuccess;
     // every rank must agree, or the ranks would run different exchange code
-    int flag = ok ? 1 : 0, *dflag = nullptr;
-    if (cudaMalloc(&dflag, sizeof(int)) == cudaSuccess) {
-        cudaMemcpy(dflag, &flag, sizeof(int), cudaMemcpyHostToDevice);
-        if (ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, P->comm, P->stream) != ncclSuccess ||
-            cudaStreamSynchronize(P->stream) != cudaSuccess)
-            flag = 0;
-        else
-            cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost);
-        cudaFree(dflag);
-    } else {
+    int flag = ok ? 1 : 0;
+    int *dflag = reinterpret_cast<int *>(P->psi_alt);
+    if (cudaMemcpy(dflag, &flag, sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+        ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, P->comm, P->stream) != ncclSuccess ||
+        cudaStreamSynchronize(P->stream) != cudaSuccess ||
+        cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
         flag = 0;
-    }
     cudaGetLastError();
     P->ipc_ok = flag == 1;
 }
