@@ -1754,16 +1754,20 @@ qva_status run_passes_graph(qva_plan *P, const std::vector<PassPlan> &passes, co
     return QVA_OK;
 }
 
+bool fuse_exchange_enabled() {
+    static int env = [] {
+        const char *e = getenv("QVA_FUSE_EXCHANGE");
+        return e ? atoi(e) : 1;
+    }();
+    return env != 0;
+}
+
 // Fused exchange over peer memory: every rank's two state buffers are exported as CUDA IPC
 // handles, all-gathered over the plan's NCCL communicator and mapped (NVLink P2P), so the pass
 // before a global<->local exchange can store each tile straight into its receiving rank's
 // buffer.  Any failure leaves ipc_ok = false and the exchange runs as NCCL send/recv.
 void setup_peer_exchange(qva_plan *P) {
-    static int env = [] {
-        const char *e = getenv("QVA_FUSE_EXCHANGE");
-        return e ? atoi(e) : 1;
-    }();
-    if (!env || P->world > kMaxPeers || !P->psi || !P->psi_alt || !P->comm) return;
+    if (!fuse_exchange_enabled() || P->world > kMaxPeers || !P->psi || !P->psi_alt || !P->comm) return;
     P->ipc_own[0] = P->psi;
     P->ipc_own[1] = P->psi_alt;
     // every rank takes part in both collectives below whatever happens locally (a rank that
@@ -1905,6 +1909,12 @@ struct PlanShardIO : FftShardIO {
     explicit PlanShardIO(qva_plan *P_) : P(P_) {}
     qva_status to_col(const double2 *row, double2 *col) override { return shard_to_col<double2>(P, row, col); }
     qva_status to_row(const double2 *col, double2 *row) override { return shard_to_row<double2>(P, col, row); }
+    qva_status barrier() override {
+        if (P->world == 1) return QVA_OK;  // virtual shards: stream order
+        QVA_CUDA_TRY(cudaMemsetAsync(P->d_bar, 0, sizeof(int), P->stream));
+        QVA_NCCL_TRY(ncclAllReduce(P->d_bar, P->d_bar, 1, ncclInt32, ncclSum, P->comm, P->stream));
+        return QVA_OK;
+    }
 };
 
 // buffers of the sharded circulant path: column-layout work array (psi_alt), q in the column
@@ -1923,6 +1933,19 @@ qva_status circ_shard_setup(qva_plan *P, PlanShardIO &io) {
     io.first = P->world == 1 ? 0 : P->rank;
     io.col = P->psi_alt;
     io.q_col = P->qB;
+    // transposes fused into the pass stores: virtual shards address blocks of psi / psi_alt, real
+    // shards the IPC-mapped peer buffers (psi and psi_alt never swap on the circulant path)
+    // (virtual shards only with peer_store_exchange: on one GPU the L2-resident block transposes
+    // measured faster, cfg3 G = 2: 1.33 vs 1.41 ms; the flag runs the multi-GPU store path)
+    io.fused = fuse_exchange_enabled() && P->G <= kMaxPeers &&
+               (P->world == 1 ? P->d.reserved[3] != 0 : P->ipc_ok);
+    if (io.fused) {
+        const uint64_t NG = P->N / P->G;
+        for (int t = 0; t < P->G; ++t) {
+            io.row_dst[t] = P->world == 1 ? P->psi + t * NG : P->ipc_peer[0][t];
+            io.col_dst[t] = P->world == 1 ? P->psi_alt + t * NG : P->ipc_peer[1][t];
+        }
+    }
     return QVA_OK;
 }
 
@@ -2344,7 +2367,8 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
             return fail(QVA_ERR_NCCL);
         }
     }
-    if (d.world > 1 && d.mixer == QVA_MIXER_X) setup_peer_exchange(P);  // falls back to NCCL on failure
+    if (d.world > 1 && (d.mixer == QVA_MIXER_X || d.mixer == QVA_MIXER_CIRCULANT))
+        setup_peer_exchange(P);  // falls back to NCCL on failure
     if (reset_state(P) != QVA_OK) return fail(QVA_ERR_CUDA);
     if (cudaStreamSynchronize(P->stream) != cudaSuccess) {
         set_error("plan init failed");

@@ -545,6 +545,8 @@ struct ColArgs {
     double *partials;
     int tws, ts_off;         // stage twiddles copied to smem at A + ts_off (tws entries; 0: global)
     int ops_cfast;           // elementwise ops column-fastest with batched q loads (q not L2-resident)
+    int xg;                  // > 0: sharded to-row transpose fused into the store (xg shards):
+    double2 *xout[kMaxPeers];//   row x1 goes to xout[x1 / (M1 / xg)] at (x1 mod M1/xg) * M2g + column
     SubFft sf;
 };
 
@@ -734,8 +736,14 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
         double2 v = *ad.ptr(c, x1);
         if (a.do_fwd) v = cmul(v, cmul(Tw[c * E + (x1 >> 5)], Tw[c * E + nh + (x1 & 31)]));
-        if (x < a.out_len) a.out[mat + x] = v;
+        if (a.xg) {  // fused to-row transpose: row x1 belongs to shard d
+            const int m1s = M1 / a.xg, d = x1 / m1s;
+            a.xout[d][(uint64_t)(x1 - d * m1s) * a.M2g + a.col_off + c0 + c] = v;
+        } else if (x < a.out_len) {
+            a.out[mat + x] = v;
+        }
     }
+    if (a.xg) __threadfence_system();  // peer stores visible before the host-side barrier
 }
 
 struct RowArgs {
@@ -755,6 +763,8 @@ struct RowArgs {
     const double2 *big_lo, *big_hi;
     int big_shift;
     int tws, ts_off;            // stage twiddles copied to smem at A + ts_off (tws entries; 0: global)
+    int xg, M2s;                // > 0: sharded to-column transpose fused into the store: column x2
+    double2 *xout[kMaxPeers];   //   goes to xout[x2 / M2s] at global row * M2s + (x2 mod M2s)
     SubFft sf;
 };
 
@@ -840,8 +850,16 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_row_kernel(const Row
     // (a multiply-high divu for (r, x2) here made ptxas emit code that indexed Tr out of range on
     // B200; the incremental form is correct)
     int r = r0, x2 = x0;
-    for (int i = threadIdx.x; i < tot; i += blockDim.x, adv(r, x2))
-        rows[i] = cmul(*ad.ptr(r, x2), cmul(Tr[r * E + (x2 >> 5)], Tr[r * E + nh + (x2 & 31)]));
+    for (int i = threadIdx.x; i < tot; i += blockDim.x, adv(r, x2)) {
+        const double2 v = cmul(*ad.ptr(r, x2), cmul(Tr[r * E + (x2 >> 5)], Tr[r * E + nh + (x2 & 31)]));
+        if (a.xg) {  // fused to-column transpose: column x2 belongs to shard s
+            const int sh = x2 / a.M2s;
+            a.xout[sh][(uint64_t)(a.row_off + k1_0 + r) * a.M2s + (x2 - sh * a.M2s)] = v;
+        } else {
+            rows[i] = v;
+        }
+    }
+    if (a.xg) __threadfence_system();  // peer stores visible before the host-side barrier
 }
 
 // whole evolution of a (direct, 13-smooth) N <= 4096 state in one CTA
@@ -1702,7 +1720,12 @@ qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStr
         fp->n_partials = gc * io.local;
         QVA_CUDA_TRY(cudaMalloc(&fp->partials, fp->n_partials * 2 * sizeof(double)));
     }
+    // transposes fused into the pass stores (two-level plans; the three-level inner passes keep
+    // the separate transposes)
+    const bool fused = io.fused && fp->levels == 2 && G <= kMaxPeers;
     auto cols = [&](int init, int inv, int ops, double gamma, int fwd) -> qva_status {
+        c.xg = fused ? G : 0;
+        for (int t = 0; t < G && fused; ++t) c.xout[t] = io.row_dst[t];
         for (int ls = 0; ls < io.local; ++ls) {
             c.in = io.col + ls * NG;
             c.in_len = NG;
@@ -1732,6 +1755,9 @@ qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStr
         RowArgs w = row_args(fp, r.psi);
         w.rb = rb;
         w.row_off = io.first * M1s;
+        w.xg = fused ? G : 0;
+        w.M2s = M2s;
+        for (int t = 0; t < G && fused; ++t) w.xout[t] = io.col_dst[t];
         if (r.lambda_perm) {
             w.spec = 1;
             w.lam_perm = r.lambda_perm;
@@ -1753,21 +1779,24 @@ qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStr
         }
         return QVA_OK;
     };
+    // after a pass: the data is in the other layout already (fused) or gets there by a transpose
+    auto after_cols = [&]() { return fused ? io.barrier() : io.to_row(io.col, r.psi); };
+    auto after_rows = [&]() { return fused ? io.barrier() : io.to_col(r.psi, io.col); };
     if (r.mode == 1) {
         QVA_TRY(io.to_col(r.psi, io.col));
         QVA_TRY(cols(0, 0, 0, 0.0, 1));
-        QVA_TRY(io.to_row(io.col, r.psi));
+        QVA_TRY(after_cols());
         QVA_TRY(rows(r.theta[0]));
-        QVA_TRY(io.to_col(r.psi, io.col));
+        QVA_TRY(after_rows());
         QVA_TRY(cols(0, 1, 0, 0.0, 0));
-        return io.to_row(io.col, r.psi);
+        return after_cols();
     }
     if (!r.init) QVA_TRY(io.to_col(r.psi, io.col));
     for (int k = 0; k < r.p; ++k) {
         QVA_TRY(cols(k == 0 ? r.init : 0, k > 0, OP_PHASE, r.theta[2 * k], 1));
-        QVA_TRY(io.to_row(io.col, r.psi));
+        QVA_TRY(after_cols());
         QVA_TRY(rows(r.theta[2 * k + 1]));
-        QVA_TRY(io.to_col(r.psi, io.col));
+        QVA_TRY(after_rows());
     }
     if (r.p > 0) {
         QVA_TRY(cols(0, 1, r.expect ? OP_EXPECT : 0, 0.0, 0));
@@ -1781,7 +1810,7 @@ qva_status fft_run_sharded(FftPlan *fp, const FftRun &r, FftShardIO &io, cudaStr
             }
         }
     }
-    return io.to_row(io.col, r.psi);
+    return after_cols();
 }
 
 }  // namespace qva

@@ -290,6 +290,14 @@ struct FftShardIO {
     const double *q_col = nullptr;    // q in the column layout
     virtual qva_status to_col(const double2 *row, double2 *col) = 0;  // all-to-all transposes
     virtual qva_status to_row(const double2 *col, double2 *row) = 0;
+    // transposes fused into the passes' stores: the row pass writes shard s's columns straight
+    // into col_dst[s] (its column-layout buffer), the column pass writes shard d's rows into
+    // row_dst[d]; peer memory (IPC, NVLink) on real shards, blocks of this process's arrays on
+    // virtual ones.  barrier(): every shard's stores into ours are complete.
+    bool fused = false;
+    double2 *row_dst[kMaxPeers] = {};
+    double2 *col_dst[kMaxPeers] = {};
+    virtual qva_status barrier() { return QVA_OK; }
     virtual ~FftShardIO() {}
 };
 bool fft_shardable(const FftPlan *fp, int G);

@@ -338,13 +338,15 @@ def test_bluestein_complete_graph_vs_closed_form(Q, N):
         _amp_close(P.get_state(), ref)
 
 
-@pytest.mark.parametrize("G", [2, 4, 8])
-def test_cfg3_virtual_shards(Q, G):
+@pytest.mark.parametrize("G,peer", [(2, False), (4, False), (8, False), (2, True), (8, True)])
+def test_cfg3_virtual_shards(Q, G, peer):
     """Sharded QWOA: G row-block shards on one GPU, the column pass in the
-    column layout reached by all-to-all transposes; same state as the unsharded oracle."""
+    column layout reached by all-to-all transposes (peer=False) or by the passes' own stores into
+    the other layout's shard buffers (peer=True, the multi-GPU path); same state as the
+    unsharded oracle."""
     wl = make_config("cfg3")
     ref = O.evolve_complete(wl.q, wl.theta, wl.lam0, wl.lam_rest)
-    with Q.Plan(wl.dim, "circulant", virtual_shards=G) as P:
+    with Q.Plan(wl.dim, "circulant", virtual_shards=G, peer_store_exchange=peer) as P:
         P.set_qualities(wl.q)
         P.set_circulant_eigenvalues_const(wl.lam0, wl.lam_rest)
         P.evolve(wl.theta)
@@ -352,15 +354,16 @@ def test_cfg3_virtual_shards(Q, G):
         _amp_close(P.get_state(), ref)
 
 
-@pytest.mark.parametrize("N,G", [(6144, 2), (6144, 8), (40320, 4)])
-def test_circulant_virtual_shards_random_spectrum(Q, N, G):
+@pytest.mark.parametrize("N,G,peer", [(6144, 2, False), (6144, 8, False), (40320, 4, False), (6144, 8, True),
+                                      (40320, 4, True)])
+def test_circulant_virtual_shards_random_spectrum(Q, N, G, peer):
     rng = np.random.default_rng(N + G)
     q = rng.standard_normal(N)
     lam = rng.standard_normal(N) * 3
     theta = rng.uniform(0, math.pi, 6)
     psi0 = rng.standard_normal(N) + 1j * rng.standard_normal(N)
     psi0 /= np.linalg.norm(psi0)
-    with Q.Plan(N, "circulant", virtual_shards=G) as P:
+    with Q.Plan(N, "circulant", virtual_shards=G, peer_store_exchange=peer) as P:
         P.set_qualities(q)
         P.set_circulant_eigenvalues(lam)
         P.evolve(theta)
