@@ -155,6 +155,9 @@ def workload_for(args, world):
 # ---------------------------------------------------------------------------------------------
 # CPU oracle arm (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------------------------
+ONE_THREAD = {}  # filled by oracle_sample for the X-mixer recipes: the oracle on one OpenMP thread
+
+
 def oracle_sample(name, wl, budget_s=20.0):
     """Time the CPU oracle, as it stands, on a bounded sample of the same workload.
     Returns (amp-layers/s, seconds, cores, sample description)."""
@@ -180,6 +183,16 @@ def oracle_sample(name, wl, budget_s=20.0):
         dt, f = run(swl)
         desc = (f"oracle full p={swl.p} evolution + <Q> of the {fam} recipe at n={n} (2^{n} amplitudes; "
                 f"the full workload has 2^{wl.n_qubits}), {cores} OpenMP threads, f={f:.6f}")
+        # the same oracle on one thread (both core counts), on a smaller sample
+        n1 = max(n0, n - 4 if fam == "cfg4" else n - 4)
+        O.set_num_threads(1)
+        try:
+            s1 = make_config(fam, n_override=n1)
+            dt1, _ = run(s1)
+        finally:
+            O.set_num_threads(cores)
+        ONE_THREAD.update({"value": (1 << n1) * s1.p / dt1, "cores": 1, "sample": f"n={n1}, 1 thread",
+                           "seconds": dt1})
         return (1 << n) * swl.p / dt, dt, cores, desc
     if wl.mixer == "x":
         B = len(wl.batch_thetas) if wl.batch_thetas is not None else 1
@@ -404,6 +417,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt, cores, sdesc = oracle_sample(name, wl, budget_s=20.0)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sdesc, "seconds": dt}
+        if ONE_THREAD:
+            cpu["single_thread"] = dict(ONE_THREAD, unit=UNIT)
 
     if rank == 0:
         line = {

@@ -18,7 +18,7 @@ _SRC = os.path.join(_HERE, "qva_oracle.c")
 _LIB = os.path.join(_HERE, "libqva_oracle.so")
 
 __all__ = [
-    "build_oracle", "lib", "num_threads", "maxcut_q", "init_uniform", "phase", "mixer_x",
+    "build_oracle", "lib", "num_threads", "set_num_threads", "maxcut_q", "init_uniform", "phase", "mixer_x",
     "mixer_circulant_dense", "mixer_complete", "expectation", "norm2", "probabilities",
     "evolve_x", "evolve_complete", "evolve_circulant_dense", "lightcone_maxcut",
     "dense_sum_x", "mixer_sparse_dense", "evolve_sparse_dense", "c128",
@@ -44,6 +44,7 @@ def lib():
     d, i, u64 = ctypes.c_double, ctypes.c_int, ctypes.c_uint64
     P = ctypes.c_void_p
     L.or_num_threads.restype = i
+    L.or_set_num_threads.argtypes = [i]
     L.or_maxcut_q.argtypes = [i, i, P, P, P, P]
     L.or_init_uniform.argtypes = [u64, P]
     L.or_phase.argtypes = [u64, P, P, d]
@@ -76,6 +77,11 @@ def c128(psi) -> np.ndarray:
 
 def num_threads() -> int:
     return int(lib().or_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP thread count of the oracle's loops (timing only; results do not depend on it)."""
+    lib().or_set_num_threads(int(n))
 
 
 def maxcut_q(n: int, u, v, w=None) -> np.ndarray:

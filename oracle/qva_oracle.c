@@ -33,6 +33,14 @@ OR_API int or_num_threads(void) {
     return 1;
 #endif
 }
+/* thread count of the OpenMP loops (timing only: SURVEY 8(d) reports 1 thread and all cores) */
+OR_API void or_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
 
 /* Max-cut qualities.  PAPER.md:721-726 (Eq. maxcut-cost) counts UNCUT edges,
  * C = sum_E 1/2 (1 + Z_i Z_j); the configs (BASELINE.json) fix q_x = -cut_w(x)
