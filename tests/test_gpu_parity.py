@@ -419,6 +419,57 @@ def test_qaoaz_parity_vs_oracle(Q, n, seq, p):
         _f_close(f[1], O.expectation(O.evolve_parity(n, q, sq, theta[::-1], psi0), q))
 
 
+def _pair_group_csr(n, pairs):
+    """CSR of sum over the pairs (a, b) of (X_a X_b + Y_a Y_b) = 2 (|01><10| + |10><01|) on (a, b):
+    built from the definition, independently of the parity kernel."""
+    N = 1 << n
+    rows = [[] for _ in range(N)]
+    for a, b in pairs:
+        for x in range(N):
+            if ((x >> a) ^ (x >> b)) & 1:
+                rows[x].append((x ^ (1 << a) ^ (1 << b), 2.0))
+    row_ptr = np.zeros(N + 1, np.int64)
+    col, val = [], []
+    for x in range(N):
+        r = sorted(rows[x])
+        row_ptr[x + 1] = row_ptr[x] + len(r)
+        col += [c for c, _ in r]
+        val += [w for _, w in r]
+    return row_ptr, np.array(col, np.int32), np.array(val, np.float64)
+
+
+@pytest.mark.parametrize("n,seq", [(8, None), (9, [0, 3, 6, 1, 4, 7, 2])])
+def test_qaoaz_parity_vs_sparse_taylor(Q, n, seq):
+    """SURVEY NEXT-2 cross-check: the structured parity mixer (one step) equals the generic CSR
+    Taylor mixer applied group by group, exp(-it B_last) exp(-it B_even) exp(-it B_odd) (R19), on
+    the GPU, from a random state."""
+    rng = np.random.default_rng(900 + n)
+    psi0 = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi0 /= np.linalg.norm(psi0)
+    sq = list(range(n)) if seq is None else seq
+    odd, even, last = O.parity_pairs(sq)
+    t = 0.37
+    with Q.Plan(1 << n, "parity", n_qubits=n) as P:
+        if seq is not None:
+            P.set_parity_mixer(seq)
+        P.set_qualities(np.zeros(1 << n))
+        P.set_initial_state(psi0)
+        P.reset_state()
+        P.apply_mixer(t)
+        got = P.get_state()
+    with Q.Plan(1 << n, "sparse") as S:
+        S.set_qualities(np.zeros(1 << n))
+        S.set_initial_state(psi0)
+        S.reset_state()
+        for group in (odd, even, last):
+            if group:
+                S.set_sparse_mixer(*_pair_group_csr(n, group))
+                S.apply_mixer(t)
+        ref = S.get_state()
+    assert np.max(np.abs(got - ref)) < 1e-10
+    _amp_close(got, O.mixer_parity(psi0.copy(), sq, t))
+
+
 @pytest.mark.parametrize("N,G", [(5040, 1), (40320, 1), (3628800, 4)])
 def test_three_level_fft_forced(Q, N, G):
     """NEXT-4: the three-level four-step (inner row transforms local to each top-level row block),
