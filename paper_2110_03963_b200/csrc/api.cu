@@ -552,6 +552,8 @@ struct qva_plan {
     std::vector<double> lambda_host;   // natural (forward-bin) order mirror
     // parity (QAOAz): ordered qubit subsequence
     std::vector<int> parity_seq;
+    std::vector<ParityWindow> parity_win;  // window passes of the current sequence (built lazily)
+    std::vector<int> parity_win_seq;       // the sequence they were built for
     // sparse
     SparseMixer sm;
     bool sparse_set = false;
@@ -1949,11 +1951,124 @@ qva_status circ_shard_setup(qva_plan *P, PlanShardIO &io) {
     return QVA_OK;
 }
 
-// QAOAz parity mixer U(t) = e^{-itB_last} e^{-itB_even} e^{-itB_odd} (reading R19): pair terms in
-// that order, one coalesced pass over the |01>/|10> halves per pair
-qva_status parity_mix(qva_plan *P, double t) {
+// QAOAz parity mixer U(t) = e^{-itB_last} e^{-itB_even} e^{-itB_odd} (reading R19).  The pair
+// terms of one group act on disjoint qubits and commute; a term only has to follow the terms of
+// earlier groups it shares a qubit with.  Windows of <= 12 physical bits (0..2 always, for
+// 128-B rows) each take, greedily in group order, every term whose qubits fit and whose
+// predecessors are done or earlier in the same window: one HBM round trip per window instead of
+// one per term (default sequence, n = 28: 5 windows for 27 terms).
+static std::vector<ParityWindow> parity_windows(int n, const std::vector<int> &s) {
+    const int K = (int)s.size();
+    std::vector<std::pair<int, int>> terms;
+    std::vector<int> grp;
+    for (int m = 0; m + 1 < K; m += 2) terms.push_back({s[m], s[m + 1]}), grp.push_back(0);
+    for (int m = 1; m + 1 < K; m += 2) terms.push_back({s[m], s[m + 1]}), grp.push_back(1);
+    if (K >= 3 && (K & 1)) terms.push_back({s[K - 1], s[0]}), grp.push_back(2);
+    const int T = (int)terms.size();
+    std::vector<std::vector<int>> deps(T);
+    for (int k = 0; k < T; ++k)
+        for (int j = 0; j < k; ++j)
+            if (grp[j] < grp[k] && (terms[j].first == terms[k].first || terms[j].first == terms[k].second ||
+                                    terms[j].second == terms[k].first || terms[j].second == terms[k].second))
+                deps[k].push_back(j);
+    std::vector<char> done(T, 0);
+    std::vector<ParityWindow> out;
+    const int wmax = std::min(n, kWinMaxBits);
+    for (int left = T; left > 0;) {
+        std::vector<char> inw(n, 0), placed(T, 0);
+        int w = 0;
+        for (int b = 0; b < std::min(3, n); ++b) inw[b] = 1, ++w;
+        std::vector<int> plan;
+        for (int k = 0; k < T && (int)plan.size() < kWinMaxPairs; ++k) {
+            if (done[k]) continue;
+            bool ready = true;
+            for (int j : deps[k]) ready = ready && (done[j] || placed[j]);
+            if (!ready) continue;
+            const int need = !inw[terms[k].first] + !inw[terms[k].second];
+            if (w + need > wmax) continue;
+            inw[terms[k].first] = inw[terms[k].second] = 1;
+            w += need;
+            placed[k] = 1;
+            plan.push_back(k);
+        }
+        // pad the window to wmax bits with the lowest free bits (longer rows, fewer tiles)
+        for (int b = 0; b < n && w < wmax; ++b)
+            if (!inw[b]) inw[b] = 1, ++w;
+        ParityWindow W;
+        memset(&W, 0, sizeof(W));
+        W.n = n;
+        W.w = w;
+        std::vector<int> bits, local(n, -1);
+        for (int b = 0; b < n; ++b)
+            if (inw[b]) local[b] = (int)bits.size(), bits.push_back(b);
+        auto runs = [&](bool in_window, int *src, int *wd, int *dst, int cap, int &nr) {
+            nr = 0;
+            int idx = 0;  // running index in the window (or the tile number)
+            for (int b = 0; b < n;) {
+                if ((bool)inw[b] != in_window) { ++b; continue; }
+                int st = b;
+                while (b < n && (bool)inw[b] == in_window) ++b;
+                if (nr == cap) return false;
+                src[nr] = idx;
+                wd[nr] = b - st;
+                dst[nr] = st;
+                idx += b - st;
+                ++nr;
+            }
+            return true;
+        };
+        if (!runs(true, W.in_src, W.in_w, W.in_dst, kWinMaxRuns, W.n_in) ||
+            !runs(false, W.out_src, W.out_w, W.out_dst, kWinMaxRuns + 1, W.n_out))
+            return {};  // too fragmented for the run tables: the caller takes the per-term passes
+        W.np = (int)plan.size();
+        for (int i = 0; i < W.np; ++i) {
+            W.pa[i] = (int8_t)local[terms[plan[i]].first];
+            W.pb[i] = (int8_t)local[terms[plan[i]].second];
+            done[plan[i]] = 1;
+        }
+        left -= W.np;
+        out.push_back(W);
+    }
+    return out;
+}
+
+// one mixer step; q != nullptr also applies the phase exp(-i gamma q) first (fused into the
+// first window's loads)
+qva_status reset_state(qva_plan *P);
+qva_status parity_mix(qva_plan *P, double t, const double *q = nullptr, double gamma = 0.0, bool from_psi0 = false) {
     const std::vector<int> &s = P->parity_seq;
     const int K = (int)s.size();
+    static int win_env = [] {
+        const char *e = getenv("QVA_PARITY_WINDOWS");
+        return e ? atoi(e) : 1;
+    }();
+    if (win_env && P->arr_n == (1ull << P->n)) {
+        if (P->parity_win_seq != s) {
+            P->parity_win = parity_windows(P->n, s);
+            P->parity_win_seq = s;
+        }
+        if (!P->parity_win.empty()) {
+            for (size_t i = 0; i < P->parity_win.size(); ++i) {
+                ParityWindow W = P->parity_win[i];
+                W.c = cos(2.0 * t);
+                W.s = sin(2.0 * t);
+                W.q = (i == 0) ? q : nullptr;
+                W.gamma = gamma;
+                if (i == 0 && from_psi0) {  // the first window also stands in for reset_state
+                    if (P->has_psi0) W.src = P->psi0;
+                    else W.init_amp = 1.0 / sqrt((double)P->N);
+                }
+                ProfScope ps(P, K_OTHER, (32.0 + (W.q ? 8.0 : 0.0)) * P->arr_n);
+                QVA_CUDA_TRY(launch_parity_window(P->psi, W, P->stream));
+            }
+            return QVA_OK;
+        }
+    }
+    if (from_psi0) QVA_TRY(reset_state(P));
+    if (q) {
+        ProfScope ps(P, K_OTHER, 40.0 * P->arr_n);
+        QVA_CUDA_TRY(launch_phase(P->psi, q, P->arr_n, gamma, P->stream));
+    }
     auto pair = [&](int a, int b) -> qva_status {
         ProfScope ps(P, K_OTHER, 16.0 * P->arr_n);
         QVA_CUDA_TRY(launch_parity_pair(P->psi, P->arr_n, a, b, t, P->stream));
@@ -2859,14 +2974,10 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
     }
     if (P->mixer == QVA_MIXER_PARITY) {
         QVA_TRY(ensure_q_dev(P));
-        QVA_TRY(reset_state(P));
-        for (int k = 0; k < p; ++k) {
-            {
-                ProfScope ps(P, K_OTHER, 40.0 * P->arr_n);
-                QVA_CUDA_TRY(launch_phase(P->psi, P->q, P->arr_n, theta[2 * k], P->stream));
-            }
-            QVA_TRY(parity_mix(P, theta[2 * k + 1]));
-        }
+        if (p == 0) return reset_state(P);
+        P->layout = 0;
+        P->perm.clear();
+        for (int k = 0; k < p; ++k) QVA_TRY(parity_mix(P, theta[2 * k + 1], P->q, theta[2 * k], k == 0));
         return QVA_OK;
     }
     // sparse

@@ -466,6 +466,88 @@ __global__ void parity_pair_kernel(double2 *__restrict__ psi, uint64_t quarter, 
     }
 }
 
+// Several parity pair terms in one HBM round trip: each CTA stages a window of 2^w amplitudes (the
+// physical bits P.bits, given as runs; bits 0..2 lead, so loads and stores move 128-B rows),
+// optionally applies the phase exp(-i gamma q_x) as it loads, then the listed pair rotations in
+// order (each a Givens rotation by 2t on the window's 01/10 pairs, a barrier between pairs),
+// and writes the window back.  The host orders the pairs so that every term that shares a qubit
+// with an earlier-group term comes after it (reading R19).
+__global__ void __launch_bounds__(256) parity_window_kernel(double2 *__restrict__ psi, const __grid_constant__ ParityWindow P) {
+    extern __shared__ double2 win[];
+    const int W = 1 << P.w;
+    const uint64_t n_tiles = 1ull << (P.n - P.w);
+    for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        // tile number -> the non-window bits (as runs)
+        uint64_t base = 0;
+        for (int r = 0; r < P.n_out; ++r) base |= ((t >> P.out_src[r]) & ((1ull << P.out_w[r]) - 1)) << P.out_dst[r];
+        __syncthreads();  // the previous tile's stores have read the window
+        // batches of kWinU independent loads per thread before any is used (one load per
+        // iteration would expose a full memory latency per element)
+        constexpr int kWinU = 8;
+        for (int e0 = threadIdx.x; e0 < W; e0 += kWinU * blockDim.x) {
+            double2 v[kWinU];
+            double qv[kWinU];
+            uint64_t offs[kWinU];
+#pragma unroll
+            for (int u = 0; u < kWinU; ++u) {
+                const int e = e0 + u * blockDim.x;
+                uint64_t off = 0;
+                for (int r = 0; r < P.n_in; ++r) off |= (uint64_t)((e >> P.in_src[r]) & ((1 << P.in_w[r]) - 1)) << P.in_dst[r];
+                offs[u] = off;
+                if (e < W) {
+                    v[u] = P.init_amp > 0.0 ? make_double2(P.init_amp, 0.0) : (P.src ? P.src : psi)[base + off];
+                    qv[u] = P.q ? P.q[base + off] : 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kWinU; ++u) {
+                const int e = e0 + u * blockDim.x;
+                if (e >= W) break;
+                double2 x = v[u];
+                if (P.q) {
+                    double sn, cs;
+                    sincos(P.gamma * qv[u], &sn, &cs);
+                    x = make_double2(fma(cs, x.x, sn * x.y), fma(cs, x.y, -sn * x.x));
+                }
+                win[e] = x;
+            }
+        }
+        __syncthreads();
+        for (int k = 0; k < P.np; ++k) {
+            const int a = P.pa[k], b = P.pb[k];
+            const int lo = min(a, b), hi = max(a, b);
+            for (int m = threadIdx.x; m < W / 4; m += blockDim.x) {
+                int x = ((m >> lo) << (lo + 1)) | (m & ((1 << lo) - 1));
+                x = ((x >> hi) << (hi + 1)) | (x & ((1 << hi) - 1));
+                x |= 1 << a;
+                const int y = (x ^ (1 << a)) | (1 << b);
+                const double2 u = win[x], v = win[y];
+                win[x] = make_double2(fma(P.c, u.x, P.s * v.y), fma(P.c, u.y, -P.s * v.x));
+                win[y] = make_double2(fma(P.c, v.x, P.s * u.y), fma(P.c, v.y, -P.s * u.x));
+            }
+            __syncthreads();
+        }
+        for (int e = threadIdx.x; e < W; e += blockDim.x) {
+            uint64_t off = 0;
+            for (int r = 0; r < P.n_in; ++r) off |= (uint64_t)((e >> P.in_src[r]) & ((1 << P.in_w[r]) - 1)) << P.in_dst[r];
+            psi[base + off] = win[e];
+        }
+    }
+}
+
+cudaError_t launch_parity_window(double2 *psi, const ParityWindow &p, cudaStream_t s) {
+    static bool configured = false;
+    const size_t smem = ((size_t)1 << p.w) * sizeof(double2);
+    if (!configured) {
+        cudaFuncSetAttribute(parity_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        configured = true;
+    }
+    const uint64_t tiles = 1ull << (p.n - p.w);
+    const int grid = (int)std::min<uint64_t>(tiles, 148ull * 3);
+    parity_window_kernel<<<grid, 256, smem, s>>>(psi, p);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_parity_pair(double2 *psi, uint64_t n_amps, int a, int b, double t, cudaStream_t s) {
     const uint64_t quarter = n_amps / 4;
     parity_pair_kernel<<<grid_for(quarter, 256), 256, 0, s>>>(psi, quarter, a, b, cos(2.0 * t), sin(2.0 * t));

@@ -230,6 +230,21 @@ cudaError_t launch_reduce_partials(const double *partials, uint64_t n, int batch
                                    cudaStream_t s);
 // QAOAz parity-mixer pair term exp(-i t (X_aX_b + Y_aY_b)) on all n_amps amplitudes
 cudaError_t launch_parity_pair(double2 *psi, uint64_t n_amps, int a, int b, double t, cudaStream_t s);
+// several pair terms over one window of <= 12 physical bits per HBM round trip (parity_window_kernel)
+constexpr int kWinMaxBits = 12, kWinMaxPairs = 64, kWinMaxRuns = 12;
+struct ParityWindow {
+    int n, w;                                 // state bits, window bits
+    int n_in, in_src[kWinMaxRuns], in_w[kWinMaxRuns], in_dst[kWinMaxRuns];     // window e -> phys
+    int n_out, out_src[kWinMaxRuns + 1], out_w[kWinMaxRuns + 1], out_dst[kWinMaxRuns + 1];  // tile -> phys
+    int np;
+    int8_t pa[kWinMaxPairs], pb[kWinMaxPairs];  // window-local bits of each pair, in order
+    double c, s;                              // cos 2t, sin 2t
+    const double *q;                          // phase on load (nullptr: none)
+    double gamma;
+    const double2 *src;                       // load from here instead of psi (the initial state)
+    double init_amp;                          // > 0: the window starts as init_amp (|+>, no load)
+};
+cudaError_t launch_parity_window(double2 *psi, const ParityWindow &p, cudaStream_t s);
 // elementwise phase (generic dims, any mixer): psi *= exp(-i gamma q)
 cudaError_t launch_phase(double2 *psi, const double *q, uint64_t n, double gamma, cudaStream_t s);
 // psi = 1/sqrt(N)
