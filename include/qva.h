@@ -218,6 +218,14 @@ qva_status qva_exchange_plan(int32_t G, int32_t rank, int32_t *peer_of_chunk, in
 
 /* ---- introspection ---------------------------------------------------------------------------- */
 
+/* Host-only (no GPU): the window passes of the QAOAz parity mixer over `seq` (reading R19,
+ * PAPER.md:213-248) for an n-qubit state.  out receives, per window, [w, np, the w physical bits
+ * of the window (ascending), then np pairs (a, b) in application order]; *n_windows the count.
+ * Entries beyond cap are not written.  Every pair term of B_odd, B_even, B_last appears once, after
+ * every earlier-group term it shares a qubit with. */
+qva_status qva_parity_schedule(int32_t n, const int32_t *seq, int32_t count, int32_t *out, int32_t cap,
+                               int32_t *n_windows);
+
 /* Pass schedule the X-mixer path uses for (n_local, p): writes up to cap entries of
  * (tile_set_index, n_rot_before_phase, has_phase, n_rot_after_phase) as 4 int32 per pass and
  * returns the pass count in *n_passes.  Host-only. */

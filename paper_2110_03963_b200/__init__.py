@@ -66,6 +66,7 @@ def _load():
         "qva_set_circulant_eigenvalues_const": [P, d, d],
         "qva_set_sparse_mixer": [P, P, P, P, u64],
         "qva_set_parity_mixer": [P, P, i32],
+        "qva_parity_schedule": [i32, P, i32, P, i32, ctypes.POINTER(i32)],
         "qva_set_initial_state": [P, P, u64, u64],
         "qva_clear_initial_state": [P],
         "qva_reset_state": [P],
@@ -159,6 +160,23 @@ def qva_x_schedule_permuted(n_local: int, p: int):
     _call("qva_x_schedule_permuted", n_local, p, _ptr(out), cap, ctypes.byref(n))
     keys = ("window", "a1", "a2", "phase", "expect", "r1", "r2", "dims")
     return [dict(zip(keys, (int(x) for x in out[8 * i:8 * i + 8]))) for i in range(min(n.value, cap))]
+
+
+def qva_parity_schedule(n: int, seq):
+    """Window passes of the QAOAz parity mixer (host-only): list of (window bits, [(a, b), ...])."""
+    sq = np.ascontiguousarray(seq, np.int32)
+    cap = 4096
+    out = np.zeros(cap, np.int32)
+    nw = ctypes.c_int32()
+    _call("qva_parity_schedule", int(n), _ptr(sq), len(sq), _ptr(out), cap, ctypes.byref(nw))
+    res, pos = [], 0
+    for _ in range(nw.value):
+        w, npairs = int(out[pos]), int(out[pos + 1])
+        bits = [int(b) for b in out[pos + 2:pos + 2 + w]]
+        pr = out[pos + 2 + w:pos + 2 + w + 2 * npairs].reshape(-1, 2)
+        res.append((bits, [(int(a), int(b)) for a, b in pr]))
+        pos += 2 + w + 2 * npairs
+    return res
 
 
 def qva_circulant_plan_shape(dim: int, shards: int = 1, three_level: bool = False):

@@ -2266,6 +2266,41 @@ qva_status qva_x_schedule_permuted(int32_t n_local, int32_t p, int64_t *out, int
     return QVA_OK;
 }
 
+qva_status qva_parity_schedule(int32_t n, const int32_t *seq, int32_t count, int32_t *out, int32_t cap,
+                               int32_t *n_windows) {
+    if (n < 1 || n > 62 || !seq || count < 2 || !n_windows) {
+        set_error("qva_parity_schedule: need 1 <= n <= 62 and a sequence of >= 2 qubits");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    std::vector<int> s(seq, seq + count);
+    for (int q : s)
+        if (q < 0 || q >= n) {
+            set_error("qva_parity_schedule: qubit outside [0, n)");
+            return QVA_ERR_INVALID_ARGUMENT;
+        }
+    const std::vector<ParityWindow> wins = parity_windows(n, s);
+    *n_windows = (int32_t)wins.size();
+    // per window: [w, np, bits of the window (w entries, ascending), (a, b) physical per pair]
+    int32_t pos = 0;
+    for (const ParityWindow &W : wins) {
+        std::vector<int> bits;
+        for (int r = 0; r < W.n_in; ++r)
+            for (int j = 0; j < W.in_w[r]; ++j) bits.push_back(W.in_dst[r] + j);
+        const int32_t need = 2 + W.w + 2 * W.np;
+        if (pos + need <= cap) {
+            out[pos] = W.w;
+            out[pos + 1] = W.np;
+            for (int j = 0; j < W.w; ++j) out[pos + 2 + j] = bits[j];
+            for (int i = 0; i < W.np; ++i) {
+                out[pos + 2 + W.w + 2 * i] = bits[W.pa[i]];
+                out[pos + 3 + W.w + 2 * i] = bits[W.pb[i]];
+            }
+        }
+        pos += need;
+    }
+    return QVA_OK;
+}
+
 qva_status qva_circulant_plan_shape(uint64_t dim, int32_t shards, int32_t flags, int64_t *out) {
     if (!out || shards < 1) return QVA_ERR_INVALID_ARGUMENT;
     const FftShape sh = fft_plan_shape(dim, shards, (flags & 1) != 0);

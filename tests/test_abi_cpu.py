@@ -209,3 +209,39 @@ def test_plan_argument_errors(Q):
     with pytest.raises(Q.QvaError) as ei:
         Q.Plan(720, "sparse", world=2, rank=0)  # sharded sparse mixer: replicated mode only
     assert ei.value.status == 5
+
+
+# ---------------------------------------------------------------- QAOAz window schedule (host) ----
+@pytest.mark.parametrize("n,seed", [(6, 0), (12, 1), (20, 2), (28, 3), (33, 4), (40, 5)])
+def test_parity_window_schedule(Q, n, seed):
+    """The parity mixer's window passes (qva_parity_schedule, host-only): every term of B_odd,
+    B_even and B_last (reading R19; the oracle's parity_pairs) applied exactly once, inside its
+    window (<= 12 bits, bits 0..2 included), after every earlier-group term it shares a qubit with."""
+    import oracle as O
+    rng = np.random.default_rng(seed)
+    for trial in range(4):
+        if trial == 0:
+            seq = list(range(n))
+        else:
+            K = int(rng.integers(2, n + 1))
+            seq = [int(x) for x in rng.permutation(n)[:K]]
+        odd, even, last = O.parity_pairs(seq)
+        groups = [(0, t) for t in odd] + [(1, t) for t in even] + [(2, t) for t in last]
+        wins = Q.qva_parity_schedule(n, seq)
+        order = []
+        for bits, pairs in wins:
+            assert len(bits) <= 12 and bits == sorted(bits) and len(set(bits)) == len(bits)
+            assert all(b in bits for b in range(min(3, n)))
+            for a, b in pairs:
+                assert a in bits and b in bits
+                order.append((a, b))
+        assert len(order) == len(groups)
+        pos = {}
+        for i, (a, b) in enumerate(order):
+            pos[frozenset((a, b))] = i
+        for g, (a, b) in groups:
+            key = frozenset((a, b))
+            assert key in pos
+            for g2, (c, d) in groups:
+                if g2 < g and {c, d} & {a, b}:
+                    assert pos[frozenset((c, d))] < pos[key]
