@@ -857,3 +857,72 @@ def test_cfg5_family_n33_one_gpu_vs_lightcone_golden(Q):
             ref = (-1j) ** 33 * np.exp(-1j * gam * qv) / math.sqrt(2.0 ** 33)
             got = P.get_state(int(x), 1)[0]
             assert abs(got - ref) <= 1e-10 * abs(ref), (x, got, ref)
+
+
+# ---------------------------------------------------------------- randomized sweep ----
+@pytest.mark.parametrize("seed", range(30))
+def test_random_configurations_vs_oracle(Q, seed):
+    """Breadth sweep over the size boundaries of the X path (small-state kernel n <= 12, in-place
+    tiles 13..20, permuted schedule >= 21), p = 0..4, stored / generated (unit, weighted) q, batch
+    members and virtual shards: state and <Q> against the oracle."""
+    rng = np.random.default_rng(7000 + seed)
+    n = int(rng.choice([2, 3, 5, 8, 11, 12, 13, 14, 17, 20, 21, 22]))
+    p = int(rng.integers(0, 5))
+    mode = ["stored", "unit", "weighted"][seed % 3]
+    G = int(rng.choice([1, 2, 4])) if n >= 14 and mode != "stored" else 1
+    u, v = erdos_renyi_graph(n, 0.4, rng)
+    if len(u) == 0:
+        u, v = np.array([0]), np.array([n - 1])
+    w = rng.uniform(0, 1, len(u)) if mode == "weighted" else None
+    q = O.maxcut_q(n, u, v, w)
+    theta = rng.uniform(0, math.pi, 2 * p)
+    ref = O.evolve_x(n, q, theta)
+    with Q.Plan(1 << n, "x", n_qubits=n, virtual_shards=G, max_batch=3 if G == 1 else 1,
+                peer_store_exchange=bool(seed % 2)) as P:
+        if mode == "stored":
+            P.set_qualities(q)
+        else:
+            P.set_qualities_maxcut(u, v, w)
+        P.evolve(theta)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+        if G == 1 and p > 0:
+            sets = np.stack([theta, theta[::-1], rng.uniform(0, math.pi, 2 * p)])
+            f = P.evolve_batch(sets)
+            for b in range(3):
+                rb = O.evolve_x(n, q, sets[b])
+                _f_close(f[b], O.expectation(rb, q), O.expectation(rb, np.abs(q)))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_circulant_configurations_vs_oracle(Q, seed):
+    """Breadth sweep of the circulant path: random N (whole-CTA, four-step, Bluestein sizes), random
+    real spectrum, p = 0..3, virtual shards where the split allows, against the dense oracle."""
+    rng = np.random.default_rng(8000 + seed)
+    N = int(rng.choice([1, 2, 3, 6, 30, 97, 360, 1024, 2310, 4097, 5040, 9240, 11520, 40320]))
+    p = int(rng.integers(0, 4))
+    q = rng.standard_normal(N)
+    lam = rng.standard_normal(N) * 2
+    theta = rng.uniform(0, math.pi, 2 * p)
+    G = 1
+    for g in (8, 4, 2):
+        try:
+            shp = Q.qva_circulant_plan_shape(N, g)
+        except Q.QvaError:
+            continue  # no direct split with g | M1, M2 (e.g. Bluestein sizes): unsharded
+        if N >= 5040 and shp["kind"] == 1 and shp["M1"] % g == 0 and shp["M2"] % g == 0:
+            G = int(rng.choice([1, g]))
+            break
+    if N > 12000:
+        ref = None  # dense oracle too large: the complete-graph spectrum and its closed form
+        lam = np.full(N, float(N))
+        lam[0] = 0.0
+        ref = O.evolve_complete(q, theta, 0.0, float(N))
+    else:
+        ref = O.evolve_circulant_dense(q, lam, theta)
+    with Q.Plan(N, "circulant", virtual_shards=G, peer_store_exchange=bool(seed % 2)) as P:
+        P.set_qualities(q)
+        P.set_circulant_eigenvalues(lam)
+        P.evolve(theta)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
