@@ -926,3 +926,29 @@ def test_random_circulant_configurations_vs_oracle(Q, seed):
         P.evolve(theta)
         _amp_close(P.get_state(), ref)
         _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_parity_configurations_vs_oracle(Q, seed):
+    """Breadth sweep of the QAOAz window schedule: random n, random qubit subsequences (odd and
+    even lengths), p = 1..3, from a random state, against the oracle."""
+    rng = np.random.default_rng(9000 + seed)
+    n = int(rng.choice([3, 4, 7, 12, 13, 15, 18]))
+    K = int(rng.integers(2, n + 1))
+    seq = [int(x) for x in rng.permutation(n)[:K]]
+    p = int(rng.integers(1, 4))
+    u, v = erdos_renyi_graph(n, 0.5, rng)
+    if len(u) == 0:
+        u, v = np.array([0]), np.array([n - 1])
+    q = O.maxcut_q(n, u, v)
+    theta = rng.uniform(0, math.pi, 2 * p)
+    psi0 = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi0 /= np.linalg.norm(psi0)
+    ref = O.evolve_parity(n, q, seq, theta, psi0)
+    with Q.Plan(1 << n, "parity", n_qubits=n) as P:
+        P.set_parity_mixer(seq)
+        P.set_qualities_maxcut(u, v)
+        P.set_initial_state(psi0)
+        P.evolve(theta)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
