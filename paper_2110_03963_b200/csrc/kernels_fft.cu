@@ -143,10 +143,10 @@ __host__ __device__ constexpr double tw_cos(int N, int j) {
     constexpr double c11[11] = {1.0, 0.8412535328311812, 0.41541501300188644, -0.142314838273285, -0.654860733945285, -0.9594929736144974, -0.9594929736144975, -0.6548607339452852, -0.14231483827328523, 0.41541501300188605, 0.8412535328311812};
     constexpr double c13[13] = {1.0, 0.8854560256532099, 0.5680647467311559, 0.120536680255323, -0.35460488704253545, -0.7485107481711012, -0.970941817426052, -0.9709418174260521, -0.7485107481711013, -0.3546048870425359, 0.1205366802553232, 0.5680647467311548, 0.88545602565321};
     constexpr double c16[16] = {1.0, 0.9238795325112867, 0.7071067811865476, 0.38268343236508984, 6.123233995736766e-17, -0.3826834323650897, -0.7071067811865475, -0.9238795325112867, -1.0, -0.9238795325112868, -0.7071067811865477, -0.38268343236509034, -1.8369701987210297e-16, 0.38268343236509, 0.7071067811865474, 0.9238795325112865};
-    constexpr double c10[10] = {1.0, 0.8090169943749475, 0.30901699437494745, -0.30901699437494745, -0.8090169943749475,
-                                -1.0, -0.8090169943749475, -0.30901699437494745, 0.30901699437494745, 0.8090169943749475};
+    constexpr double c10[10] = {1.0, 0.8090169943749475, 0.30901699437494745, -0.30901699437494745, -0.8090169943749475, -1.0, -0.8090169943749475, -0.30901699437494745, 0.30901699437494745, 0.8090169943749475};
     constexpr double c6[6] = {1.0, 0.5, -0.5, -1.0, -0.5, 0.5};
-    return N == 16 ? c16[j] : N == 13 ? c13[j] : N == 11 ? c11[j] : N == 10 ? c10[j] : N == 9 ? c9[j] : N == 6 ? c6[j] : c7[j];
+    constexpr double c15[15] = {1.0, 0.9135454576426009, 0.6691306063588582, 0.30901699437494745, -0.10452846326765347, -0.5, -0.8090169943749475, -0.9781476007338057, -0.9781476007338057, -0.8090169943749475, -0.5, -0.10452846326765347, 0.30901699437494745, 0.6691306063588582, 0.9135454576426009};
+    return N == 16 ? c16[j] : N == 15 ? c15[j] : N == 13 ? c13[j] : N == 11 ? c11[j] : N == 10 ? c10[j] : N == 9 ? c9[j] : N == 6 ? c6[j] : c7[j];
 }
 __host__ __device__ constexpr double tw_sin(int N, int j) {
     constexpr double s7[7] = {0.0, 0.7818314824680298, 0.9749279121818236, 0.43388373911755823, -0.433883739117558, -0.9749279121818236, -0.7818314824680299};
@@ -154,10 +154,10 @@ __host__ __device__ constexpr double tw_sin(int N, int j) {
     constexpr double s11[11] = {0.0, 0.5406408174555976, 0.9096319953545183, 0.9898214418809328, 0.7557495743542583, 0.28173255684142967, -0.2817325568414294, -0.7557495743542582, -0.9898214418809327, -0.9096319953545186, -0.5406408174555974};
     constexpr double s13[13] = {0.0, 0.4647231720437685, 0.8229838658936564, 0.992708874098054, 0.9350162426854148, 0.6631226582407952, 0.23931566428755768, -0.23931566428755743, -0.663122658240795, -0.9350162426854147, -0.992708874098054, -0.822983865893657, -0.4647231720437684};
     constexpr double s16[16] = {0.0, 0.3826834323650898, 0.7071067811865475, 0.9238795325112867, 1.0, 0.9238795325112867, 0.7071067811865476, 0.3826834323650899, 1.2246467991473532e-16, -0.38268343236508967, -0.7071067811865475, -0.9238795325112865, -1.0, -0.9238795325112866, -0.7071067811865477, -0.3826834323650904};
-    constexpr double s10[10] = {0.0, 0.5877852522924731, 0.9510565162951536, 0.9510565162951536, 0.5877852522924731,
-                                0.0, -0.5877852522924731, -0.9510565162951536, -0.9510565162951536, -0.5877852522924731};
+    constexpr double s10[10] = {0.0, 0.5877852522924731, 0.9510565162951535, 0.9510565162951535, 0.5877852522924731, 0.0, -0.5877852522924731, -0.9510565162951535, -0.9510565162951535, -0.5877852522924731};
     constexpr double s6[6] = {0.0, 0.8660254037844386, 0.8660254037844386, 0.0, -0.8660254037844386, -0.8660254037844386};
-    return N == 16 ? s16[j] : N == 13 ? s13[j] : N == 11 ? s11[j] : N == 10 ? s10[j] : N == 9 ? s9[j] : N == 6 ? s6[j] : s7[j];
+    constexpr double s15[15] = {0.0, 0.4067366430758002, 0.7431448254773942, 0.9510565162951535, 0.9945218953682733, 0.8660254037844386, 0.5877852522924731, 0.20791169081775934, -0.20791169081775934, -0.5877852522924731, -0.8660254037844386, -0.9945218953682733, -0.9510565162951535, -0.7431448254773942, -0.4067366430758002};
+    return N == 16 ? s16[j] : N == 15 ? s15[j] : N == 13 ? s13[j] : N == 11 ? s11[j] : N == 10 ? s10[j] : N == 9 ? s9[j] : N == 6 ? s6[j] : s7[j];
 }
 
 template <int R>
@@ -269,6 +269,8 @@ __device__ __forceinline__ void dft(double2 (&a)[R], bool inv) {
         dft_pq<2, 5>(a, inv);
     } else if constexpr (R == 6) {
         dft_pq<2, 3>(a, inv);
+    } else if constexpr (R == 15) {
+        dft_pq<3, 5>(a, inv);
     } else if constexpr (R == 8) {
         // radix-2 split into two length-4 DFTs: X_k = E_k + w8^k O_k, X_{k+4} = E_k - w8^k O_k
         double2 e[4] = {a[0], a[2], a[4], a[6]}, o[4] = {a[1], a[3], a[5], a[7]};
@@ -386,6 +388,7 @@ __device__ __forceinline__ void run_fft_ad(const Ad &ad, const SubFft &sf, const
     QVA_RADIX_LOOP(8)
     QVA_RADIX_LOOP(10)
     QVA_RADIX_LOOP(6)
+    QVA_RADIX_LOOP(15)
     QVA_RADIX_LOOP(4)
     QVA_RADIX_LOOP(2)
     QVA_RADIX_LOOP(9)
@@ -949,7 +952,7 @@ const CodeletEntry kCodelets[] = {
     {768, fft_col_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_col_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>, fft_row_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_row_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>},
     {770, fft_col_kernel<kFftThreads, Codelet<770, 10, 7, 11>>, fft_col_kernel<kFftThreads / 2, Codelet<770, 10, 7, 11>>, fft_row_kernel<kFftThreads, Codelet<770, 10, 7, 11>>, fft_row_kernel<kFftThreads / 2, Codelet<770, 10, 7, 11>>},
     {810, fft_col_kernel<kFftThreads, Codelet<810, 10, 9, 9>>, fft_col_kernel<kFftThreads / 2, Codelet<810, 10, 9, 9>>, fft_row_kernel<kFftThreads, Codelet<810, 10, 9, 9>>, fft_row_kernel<kFftThreads / 2, Codelet<810, 10, 9, 9>>},
-    {840, fft_col_kernel<kFftThreads, Codelet<840, 8, 3, 5, 7>>, fft_col_kernel<kFftThreads / 2, Codelet<840, 8, 3, 5, 7>>, fft_row_kernel<kFftThreads, Codelet<840, 8, 3, 5, 7>>, fft_row_kernel<kFftThreads / 2, Codelet<840, 8, 3, 5, 7>>},
+    {840, fft_col_kernel<kFftThreads, Codelet<840, 8, 15, 7>>, fft_col_kernel<kFftThreads / 2, Codelet<840, 8, 15, 7>>, fft_row_kernel<kFftThreads, Codelet<840, 8, 15, 7>>, fft_row_kernel<kFftThreads / 2, Codelet<840, 8, 15, 7>>},
     {1024, fft_col_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_col_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>, fft_row_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_row_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>},
     {2048, fft_col_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_col_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>, fft_row_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_row_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>},
     {4096, fft_col_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_col_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>, fft_row_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_row_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>},
@@ -983,10 +986,10 @@ const long double kPiL = 3.141592653589793238462643383279502884L;
 
 bool factor_radices(int n, std::vector<int> &rs) {
     rs.clear();
-    // order must match run_fft's radix loops: 16, 8, 10, 6, 4, 2, 9, 3, 5, 7, 11, 13 (a 2 goes into
-    // a radix-10 or radix-6 stage where it can: one stage fewer)
+    // order must match run_fft's radix loops: 16, 8, 10, 6, 15, 4, 2, 9, 3, 5, 7, 11, 13 (a 2 goes
+    // into a radix-10 or radix-6 stage, a 3 with a 5 into radix 15, where they can: fewer stages)
     int x = n;
-    for (int p : {16, 8, 10, 6, 4, 2, 9, 3, 5, 7, 11, 13})
+    for (int p : {16, 8, 10, 6, 15, 4, 2, 9, 3, 5, 7, 11, 13})
         while (x % p == 0) { rs.push_back(p); x /= p; }
     return x == 1;
 }
