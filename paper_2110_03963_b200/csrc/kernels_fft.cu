@@ -1057,10 +1057,11 @@ Split choose_split(uint64_t M, int G = 1) {
                 break;
             }
         if (!cw) continue;
-        // wave quantisation on 148 SMs (one 512-thread CTA per SM): fraction of CTA slots used
+        // wave quantisation on the SMs (one 512-thread CTA per SM): fraction of CTA slots used
         auto wave_eff = [](uint64_t blocks) {
-            const uint64_t w = (blocks + 147) / 148;
-            return (double)blocks / (double)(w * 148);
+            const uint64_t sms = (uint64_t)num_sms();
+            const uint64_t w = (blocks + sms - 1) / sms;
+            return (double)blocks / (double)(w * sms);
         };
         int rb = 1;
         for (int r = 2; r <= 64; ++r)

@@ -110,7 +110,7 @@ qva_status sparse_apply_mixer(SparseMixer &sm, double2 *psi, double beta, cudaSt
     *terms_used = 0;
     if (beta == 0.0 || sm.rows == 0) return QVA_OK;
     const uint64_t rows = sm.rows;
-    int blocks = (int)std::min<uint64_t>((rows + kSpmvThreads - 1) / kSpmvThreads, 148ull * 8);
+    int blocks = (int)std::min<uint64_t>((rows + kSpmvThreads - 1) / kSpmvThreads, (uint64_t)num_sms() * 8);
     if (blocks < 1) blocks = 1;
     if (sm.scratch_blocks < blocks) {
         cudaFree(sm.scratch);

@@ -853,14 +853,19 @@ EncodeTiledFn encode_fn() {
 
 }  // namespace
 
-int tile_pass_grid(uint64_t items) {
+int num_sms() {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+        if (sms <= 0) sms = 148;  // B200
     }
+    return sms;
+}
+
+int tile_pass_grid(uint64_t items) {
+    const int sms = num_sms();
     uint64_t g = std::min<uint64_t>(items, (uint64_t)sms);
     return (int)std::max<uint64_t>(g, 1);
 }
@@ -1022,7 +1027,7 @@ cudaError_t launch_tile_pass(const CUtensorMap &map, const CUtensorMap &map_out,
 cudaError_t launch_qt_gather(void *dst, const void *src, int qbytes, const TilePassParams &p, const TileGroup &g,
                              uint64_t n_tiles, int qmin, const LayoutRuns &lay, cudaStream_t s) {
     const uint64_t total = n_tiles * (uint64_t)kTile;
-    int blocks = (int)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+    int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)num_sms() * 16);
     if (qbytes == 8)
         qt_gather_kernel<double><<<blocks, 256, 0, s>>>((double *)dst, (const double *)src, p, g, n_tiles, 0, lay);
     else if (qbytes == 2)
@@ -1033,14 +1038,14 @@ cudaError_t launch_qt_gather(void *dst, const void *src, int qbytes, const TileP
 }
 
 cudaError_t launch_gen_records(void *rec, uint64_t n_tiles, int fp64, const GenPrep &g, cudaStream_t s) {
-    int blocks = (int)std::min<uint64_t>((n_tiles + 255) / 256, 148ull * 8);
+    int blocks = (int)std::min<uint64_t>((n_tiles + 255) / 256, (uint64_t)num_sms() * 8);
     if (fp64) gen_records_kernel<double><<<blocks, 256, 0, s>>>((unsigned char *)rec, n_tiles, 112, g);
     else gen_records_kernel<int><<<blocks, 256, 0, s>>>((unsigned char *)rec, n_tiles, 16, g);
     return cudaGetLastError();
 }
 
 cudaError_t launch_permute_copy(double2 *out, const double2 *in, uint64_t n, const LayoutRuns &lay, cudaStream_t s) {
-    int blocks = (int)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    int blocks = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms() * 16);
     permute_copy_kernel<<<blocks, 256, 0, s>>>(out, in, n, lay);
     return cudaGetLastError();
 }

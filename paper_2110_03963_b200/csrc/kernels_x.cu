@@ -348,7 +348,7 @@ __global__ void check_finite_kernel(const double *x, uint64_t n, int *flag) {
 
 inline int grid_for(uint64_t n, int threads) {
     uint64_t b = (n + threads - 1) / threads;
-    uint64_t cap = 148ull * 16;
+    uint64_t cap = (uint64_t)num_sms() * 16;
     if (b > cap) b = cap;
     if (b < 1) b = 1;
     return (int)b;
@@ -543,7 +543,7 @@ cudaError_t launch_parity_window(double2 *psi, const ParityWindow &p, cudaStream
         configured = true;
     }
     const uint64_t tiles = 1ull << (p.n - p.w);
-    const int grid = (int)std::min<uint64_t>(tiles, 148ull * 3);
+    const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms() * 3);
     parity_window_kernel<<<grid, 256, smem, s>>>(psi, p);
     return cudaGetLastError();
 }

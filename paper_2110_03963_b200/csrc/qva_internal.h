@@ -157,6 +157,8 @@ constexpr TileProg kTileProgs[kNumTileProgs] = {
 };
 
 int tile_pass_grid(uint64_t items);
+// SM count of the current device (cached; grids are sized in multiples of it)
+int num_sms();
 int tile_consumer_warps();
 // builds the 5-D load map of psi_in seen through P.tile_bits and the store map of the same box
 // into psi_out through the bit permutation obit (nullptr: identity); fills P.dim_*, P.member_dim
