@@ -140,12 +140,12 @@ struct TilePassParams {
 // accumulated.  Program 0 = the generic interpreter of TilePassParams::steps.
 struct TileProg {
     int n;
-    int g[5];
-    bool rot[5];
+    int g[6];
+    bool rot[6];
     int phase_k;
     bool expect;
 };
-constexpr int kNumTileProgs = 7;
+constexpr int kNumTileProgs = 8;
 constexpr TileProg kTileProgs[kNumTileProgs] = {
     {0, {0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}, -1, false},  // 0: generic
     {2, {0, 1, 0, 0, 0}, {1, 1, 0, 0, 0}, -1, false},  // 1: X Y            (B/C pass)
@@ -154,6 +154,8 @@ constexpr TileProg kTileProgs[kNumTileProgs] = {
     {2, {0, 1, 0, 0, 0}, {1, 1, 0, 0, 0}, -1, true},   // 4: X Y + <Q>      (last pass)
     {4, {0, 0, 2, 1, 0}, {0, 1, 1, 1, 0}, 0, false},   // 5: P | X W Y      (first pass, from |+>)
     {3, {0, 0, 1, 0, 0}, {0, 1, 1, 0, 0}, 0, false},   // 6: P | X Y        (first pass, row bits deferred)
+    {6, {0, 1, 2, 2, 0, 1}, {1, 1, 1, 1, 1, 1}, 2, false},  // 7: X Y W | P | W X Y (in-place layer boundary
+                                                            //    on the contiguous set: batches, n <= 20)
 };
 
 int tile_pass_grid(uint64_t items);
