@@ -832,6 +832,9 @@ cudaError_t launch_prog(const CUtensorMap &map, const CUtensorMap &mo, const Til
         case 5: return launch_one<STAGES, QB, 5>(map, mo, p, grid, s);
         case 6: return launch_one<STAGES, QB, 6>(map, mo, p, grid, s);
         case 7: return launch_one<STAGES, QB, 7>(map, mo, p, grid, s);
+        case 8: return launch_one<STAGES, QB, 8>(map, mo, p, grid, s);
+        case 9: return launch_one<STAGES, QB, 9>(map, mo, p, grid, s);
+        case 10: return launch_one<STAGES, QB, 10>(map, mo, p, grid, s);
         default: return launch_one<STAGES, QB, 0>(map, mo, p, grid, s);
     }
 }

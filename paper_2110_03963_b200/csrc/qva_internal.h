@@ -145,7 +145,7 @@ struct TileProg {
     int phase_k;
     bool expect;
 };
-constexpr int kNumTileProgs = 8;
+constexpr int kNumTileProgs = 11;
 constexpr TileProg kTileProgs[kNumTileProgs] = {
     {0, {0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}, -1, false},  // 0: generic
     {2, {0, 1, 0, 0, 0}, {1, 1, 0, 0, 0}, -1, false},  // 1: X Y            (B/C pass)
@@ -156,6 +156,9 @@ constexpr TileProg kTileProgs[kNumTileProgs] = {
     {3, {0, 0, 1, 0, 0}, {0, 1, 1, 0, 0}, 0, false},   // 6: P | X Y        (first pass, row bits deferred)
     {6, {0, 1, 2, 2, 0, 1}, {1, 1, 1, 1, 1, 1}, 2, false},  // 7: X Y W | P | W X Y (in-place layer boundary
                                                             //    on the contiguous set: batches, n <= 20)
+    {1, {1, 0, 0, 0, 0, 0}, {1, 0, 0, 0, 0, 0}, -1, false}, // 8: Y            (short sets: shards, n < 24)
+    {1, {1, 0, 0, 0, 0, 0}, {1, 0, 0, 0, 0, 0}, -1, true},  // 9: Y + <Q>
+    {2, {1, 1, 0, 0, 0, 0}, {1, 1, 0, 0, 0, 0}, 0, false},  // 10: Y | P | Y
 };
 
 int tile_pass_grid(uint64_t items);
