@@ -952,3 +952,42 @@ def test_random_parity_configurations_vs_oracle(Q, seed):
         P.evolve(theta)
         _amp_close(P.get_state(), ref)
         _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+
+
+def test_degenerate_and_ragged_inputs(Q):
+    """Edge cases of the boundary: zero-length set/get calls, B = 0 batches, p = 0 evolutions
+    (state = psi0, <Q> = its expectation), chunked ragged q uploads equal to one upload, ragged
+    partial state / probability reads, N = 1 and N = 2 circulant plans, n = 1 qubit plans."""
+    n = 13
+    rng = np.random.default_rng(31)
+    q = rng.standard_normal(1 << n)
+    with Q.Plan(1 << n, "x", n_qubits=n, max_batch=4) as P:
+        P.set_qualities(q[:0], 0)                                  # empty upload: no-op
+        for a, b in [(0, 1), (1, 1000), (1000, 1001), (1001, 8192)]:  # ragged chunks
+            P.set_qualities(q[a:b], a)
+        np.testing.assert_array_equal(P.get_qualities(), q)
+        assert len(P.get_state(17, 0)) == 0
+        assert len(P.evolve_batch(np.zeros((0, 4)))) == 0          # B = 0
+        P.evolve([])                                               # p = 0: |+>
+        _amp_close(P.get_state(), O.init_uniform(1 << n))
+        _f_close(P.expectation(), float(np.mean(q)), float(np.mean(np.abs(q))))
+        theta = rng.uniform(0, math.pi, 4)
+        P.evolve(theta)
+        ref = O.evolve_x(n, q, theta)
+        for off, cnt in [(0, 1), (3, 5), (4095, 3), (8191, 1), (100, 4000)]:
+            _amp_close(P.get_state(off, cnt), ref[off:off + cnt])
+            np.testing.assert_allclose(P.get_probabilities(off, cnt), np.abs(ref[off:off + cnt]) ** 2, atol=1e-13)
+    for N in (1, 2):
+        qs = rng.standard_normal(N)
+        lam = rng.standard_normal(N)
+        th = rng.uniform(0, math.pi, 4)
+        with Q.Plan(N, "circulant") as P:
+            P.set_qualities(qs)
+            P.set_circulant_eigenvalues(lam)
+            P.evolve(th)
+            _amp_close(P.get_state(), O.evolve_circulant_dense(qs, lam, th))
+    with Q.Plan(2, "x", n_qubits=1) as P:
+        P.set_qualities(np.array([0.3, -1.2]))
+        th = [0.7, 0.4, 1.9, 2.2]
+        P.evolve(th)
+        _amp_close(P.get_state(), O.evolve_x(1, np.array([0.3, -1.2]), th))
