@@ -54,7 +54,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = sorted(glob.glob(os.path.join(CSRC, "*.h"))) + [
         os.path.join(os.path.dirname(HERE), "include", "qva.h")]
-    objs = []
+    objs, jobs = [], []
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
@@ -62,7 +62,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
             cmd = [NVCC] + CFLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd), flush=True)
-            subprocess.check_call(cmd)
+            jobs.append(cmd)
+    # the translation units compile independently: run them side by side
+    procs = [subprocess.Popen(cmd) for cmd in jobs]
+    failed = [cmd for cmd, pr in zip(jobs, procs) if pr.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
     if force or _stale(LIB, objs):
         cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + NCCL_LINK
         if verbose:
