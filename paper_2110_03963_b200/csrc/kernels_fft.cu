@@ -1110,6 +1110,15 @@ bool make_big_tables(uint64_t M, double2 **lo_d, double2 **hi_d) {
 bool choose_split3(uint64_t N, int G, int &M1, int &Mi1, int &Mi2) {
     double best = -1e300;
     M1 = 0;
+    if (const char *e = getenv("QVA_FFT3")) {  // measurement override "a,b,c" (must multiply to N)
+        int a = 0, b = 0, c = 0;
+        if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && (uint64_t)a * b * c == N && sub_ok(a) && sub_ok(b) && sub_ok(c)) {
+            M1 = a;
+            Mi1 = b;
+            Mi2 = c;
+            return true;
+        }
+    }
     const uint64_t cmax = kMaxCta / 8;
     for (uint64_t a = 2; a <= cmax; ++a) {
         if (N % a || (a % G) || !sub_ok((int)a)) continue;
@@ -1119,7 +1128,12 @@ bool choose_split3(uint64_t N, int G, int &M1, int &Mi1, int &Mi2) {
             if (R % b || !sub_ok((int)b)) continue;
             const uint64_t c = R / b;
             if (c < 2 || c > (uint64_t)kMaxSub || !sub_ok((int)c)) continue;
-            const double score = std::min(std::min(log((double)a), log((double)b)), log((double)c));
+            // most balanced triple; among equally balanced ones the inner row length with the most
+            // factors of 2 (radix-16 codelet stages, swizzled smem: 12! with rows of 768 = 16*16*3
+            // measured 143 ms vs 154 ms with rows of 810)
+            int twos = 0;
+            for (uint64_t x = c; x % 2 == 0; x /= 2) ++twos;
+            const double score = std::min(std::min(log((double)a), log((double)b)), log((double)c)) + 1e-3 * twos;
             if (score > best) {
                 best = score;
                 M1 = (int)a;
