@@ -1045,11 +1045,13 @@ struct Split {
 Split choose_split(uint64_t M, int G = 1) {
     Split best;
     double best_score = -1e300;
+    static const char *force2 = getenv("QVA_FFT2");  // measurement override "M1" (column length)
     for (uint64_t m1 = 2; m1 <= (uint64_t)kMaxSub && m1 <= M; ++m1) {
         if (M % m1) continue;
         const uint64_t m2 = M / m1;
         if (m2 < 2 || m2 > (uint64_t)kMaxSub || !sub_ok((int)m1) || !sub_ok((int)m2)) continue;
         if (m1 % G || m2 % G) continue;  // sharded: whole row / column blocks per shard
+        if (force2 && (uint64_t)atoi(force2) != m1) continue;
         int cw = 0;
         for (int c : {8, 4, 2, 1})
             if ((uint64_t)c * m1 <= (uint64_t)kMaxCta && col_smem_bytes(c, (int)m1) <= (size_t)kColSmemMax) {
