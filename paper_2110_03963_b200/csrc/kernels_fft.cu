@@ -384,6 +384,9 @@ __device__ __forceinline__ void run_fft_ad(const Ad &ad, const SubFft &sf, const
 #define QVA_RADIX_LOOP(R) \
     for (; s < sf.ns && sf.r[s] == R; ++s)                                                            \
         stage_inplace<R>(ad, sf.n, count, sf.m[s], tw + sf.twoff[s], inv, sf.nbmag[s], sf.mmag[s]);
+    QVA_RADIX_LOOP(7)
+    QVA_RADIX_LOOP(11)
+    QVA_RADIX_LOOP(13)
     QVA_RADIX_LOOP(16)
     QVA_RADIX_LOOP(8)
     QVA_RADIX_LOOP(10)
@@ -394,9 +397,6 @@ __device__ __forceinline__ void run_fft_ad(const Ad &ad, const SubFft &sf, const
     QVA_RADIX_LOOP(9)
     QVA_RADIX_LOOP(3)
     QVA_RADIX_LOOP(5)
-    QVA_RADIX_LOOP(7)
-    QVA_RADIX_LOOP(11)
-    QVA_RADIX_LOOP(13)
 #undef QVA_RADIX_LOOP
 }
 __device__ __forceinline__ void run_fft(double2 *buf, const SubFft &sf, const double2 *tw, int count, int stride, bool inv) {
@@ -950,9 +950,9 @@ struct CodeletEntry {
 };
 const CodeletEntry kCodelets[] = {
     {768, fft_col_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_col_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>, fft_row_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_row_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>},
-    {770, fft_col_kernel<kFftThreads, Codelet<770, 10, 7, 11>>, fft_col_kernel<kFftThreads / 2, Codelet<770, 10, 7, 11>>, fft_row_kernel<kFftThreads, Codelet<770, 10, 7, 11>>, fft_row_kernel<kFftThreads / 2, Codelet<770, 10, 7, 11>>},
+    {770, fft_col_kernel<kFftThreads, Codelet<770, 7, 11, 10>>, fft_col_kernel<kFftThreads / 2, Codelet<770, 7, 11, 10>>, fft_row_kernel<kFftThreads, Codelet<770, 7, 11, 10>>, fft_row_kernel<kFftThreads / 2, Codelet<770, 7, 11, 10>>},
     {810, fft_col_kernel<kFftThreads, Codelet<810, 10, 9, 9>>, fft_col_kernel<kFftThreads / 2, Codelet<810, 10, 9, 9>>, fft_row_kernel<kFftThreads, Codelet<810, 10, 9, 9>>, fft_row_kernel<kFftThreads / 2, Codelet<810, 10, 9, 9>>},
-    {840, fft_col_kernel<kFftThreads, Codelet<840, 8, 15, 7>>, fft_col_kernel<kFftThreads / 2, Codelet<840, 8, 15, 7>>, fft_row_kernel<kFftThreads, Codelet<840, 8, 15, 7>>, fft_row_kernel<kFftThreads / 2, Codelet<840, 8, 15, 7>>},
+    {840, fft_col_kernel<kFftThreads, Codelet<840, 7, 8, 15>>, fft_col_kernel<kFftThreads / 2, Codelet<840, 7, 8, 15>>, fft_row_kernel<kFftThreads, Codelet<840, 7, 8, 15>>, fft_row_kernel<kFftThreads / 2, Codelet<840, 7, 8, 15>>},
     {1024, fft_col_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_col_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>, fft_row_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_row_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>},
     {2048, fft_col_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_col_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>, fft_row_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_row_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>},
     {4096, fft_col_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_col_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>, fft_row_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_row_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>},
@@ -991,6 +991,9 @@ bool factor_radices(int n, std::vector<int> &rs) {
     int x = n;
     for (int p : {16, 8, 10, 6, 15, 4, 2, 9, 3, 5, 7, 11, 13})
         while (x % p == 0) { rs.push_back(p); x /= p; }
+    // execution order: the large odd primes first (their stride-7/11/13 first-stage stores are
+    // bank-conflict free), then the rest in extraction order
+    std::stable_partition(rs.begin(), rs.end(), [](int r) { return r == 7 || r == 11 || r == 13; });
     return x == 1;
 }
 
