@@ -947,16 +947,17 @@ struct CodeletEntry {
     int n;
     ColKernelFn col, col_half;
     RowKernelFn row, row_half;
+    int rad[6];  // the codelet's stage order (0-terminated); make_sub builds its tables in it
 };
 const CodeletEntry kCodelets[] = {
-    {768, fft_col_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_col_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>, fft_row_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_row_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>},
-    {770, fft_col_kernel<kFftThreads, Codelet<770, 7, 11, 10>>, fft_col_kernel<kFftThreads / 2, Codelet<770, 7, 11, 10>>, fft_row_kernel<kFftThreads, Codelet<770, 7, 11, 10>>, fft_row_kernel<kFftThreads / 2, Codelet<770, 7, 11, 10>>},
-    {810, fft_col_kernel<kFftThreads, Codelet<810, 10, 9, 9>>, fft_col_kernel<kFftThreads / 2, Codelet<810, 10, 9, 9>>, fft_row_kernel<kFftThreads, Codelet<810, 10, 9, 9>>, fft_row_kernel<kFftThreads / 2, Codelet<810, 10, 9, 9>>},
-    {840, fft_col_kernel<kFftThreads, Codelet<840, 7, 8, 15>>, fft_col_kernel<kFftThreads / 2, Codelet<840, 7, 8, 15>>, fft_row_kernel<kFftThreads, Codelet<840, 7, 8, 15>>, fft_row_kernel<kFftThreads / 2, Codelet<840, 7, 8, 15>>},
-    {1024, fft_col_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_col_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>, fft_row_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_row_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>},
-    {2048, fft_col_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_col_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>, fft_row_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_row_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>},
-    {4096, fft_col_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_col_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>, fft_row_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_row_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>},
-    {4320, fft_col_kernel<kFftThreads, Codelet<4320, 16, 10, 9, 3>>, fft_col_kernel<kFftThreads / 2, Codelet<4320, 16, 10, 9, 3>>, fft_row_kernel<kFftThreads, Codelet<4320, 16, 10, 9, 3>>, fft_row_kernel<kFftThreads / 2, Codelet<4320, 16, 10, 9, 3>>},
+    {768, fft_col_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_col_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>, fft_row_kernel<kFftThreads, Codelet<768, 16, 16, 3>>, fft_row_kernel<kFftThreads / 2, Codelet<768, 16, 16, 3>>, {16, 16, 3}},
+    {770, fft_col_kernel<kFftThreads, Codelet<770, 7, 11, 10>>, fft_col_kernel<kFftThreads / 2, Codelet<770, 7, 11, 10>>, fft_row_kernel<kFftThreads, Codelet<770, 7, 11, 10>>, fft_row_kernel<kFftThreads / 2, Codelet<770, 7, 11, 10>>, {7, 11, 10}},
+    {810, fft_col_kernel<kFftThreads, Codelet<810, 9, 9, 10>>, fft_col_kernel<kFftThreads / 2, Codelet<810, 9, 9, 10>>, fft_row_kernel<kFftThreads, Codelet<810, 9, 9, 10>>, fft_row_kernel<kFftThreads / 2, Codelet<810, 9, 9, 10>>, {9, 9, 10}},
+    {840, fft_col_kernel<kFftThreads, Codelet<840, 7, 8, 15>>, fft_col_kernel<kFftThreads / 2, Codelet<840, 7, 8, 15>>, fft_row_kernel<kFftThreads, Codelet<840, 7, 8, 15>>, fft_row_kernel<kFftThreads / 2, Codelet<840, 7, 8, 15>>, {7, 8, 15}},
+    {1024, fft_col_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_col_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>, fft_row_kernel<kFftThreads, Codelet<1024, 16, 16, 4>>, fft_row_kernel<kFftThreads / 2, Codelet<1024, 16, 16, 4>>, {16, 16, 4}},
+    {2048, fft_col_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_col_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>, fft_row_kernel<kFftThreads, Codelet<2048, 16, 16, 8>>, fft_row_kernel<kFftThreads / 2, Codelet<2048, 16, 16, 8>>, {16, 16, 8}},
+    {4096, fft_col_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_col_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>, fft_row_kernel<kFftThreads, Codelet<4096, 16, 16, 16>>, fft_row_kernel<kFftThreads / 2, Codelet<4096, 16, 16, 16>>, {16, 16, 16}},
+    {4320, fft_col_kernel<kFftThreads, Codelet<4320, 9, 3, 16, 10>>, fft_col_kernel<kFftThreads / 2, Codelet<4320, 9, 3, 16, 10>>, fft_row_kernel<kFftThreads, Codelet<4320, 9, 3, 16, 10>>, fft_row_kernel<kFftThreads / 2, Codelet<4320, 9, 3, 16, 10>>, {9, 3, 16, 10}},
 };
 const CodeletEntry *codelet_for(int n) {
     static int env = [] {
@@ -984,8 +985,17 @@ RowKernelFn row_kernel_for(int n, bool half = false) {
 // ------------------------------------------------------------------------------------------
 const long double kPiL = 3.141592653589793238462643383279502884L;
 
-bool factor_radices(int n, std::vector<int> &rs) {
+const CodeletEntry *codelet_for(int n);
+bool factor_radices(int n, std::vector<int> &rs, bool codelet_order = true) {
     rs.clear();
+    // a compiled codelet fixes its own stage order (chosen per size: a conflict-free first stage);
+    // the runtime engine (codelet_order = false: the single-CTA kernel) needs the loops' order
+    if (const CodeletEntry *c = codelet_order ? codelet_for(n) : nullptr) {
+        int prod = 1;
+        for (int i = 0; i < 6 && c->rad[i]; ++i) rs.push_back(c->rad[i]), prod *= c->rad[i];
+        if (prod == n) return true;
+        rs.clear();
+    }
     // order must match run_fft's radix loops: 16, 8, 10, 6, 15, 4, 2, 9, 3, 5, 7, 11, 13 (a 2 goes
     // into a radix-10 or radix-6 stage, a 3 with a 5 into radix 15, where they can: fewer stages)
     int x = n;
@@ -1007,9 +1017,9 @@ bool sub_ok(int n) {
     return true;
 }
 
-bool make_sub(int n, SubFft &sf, std::vector<double2> &tw) {
+bool make_sub(int n, SubFft &sf, std::vector<double2> &tw, bool codelet_order = true) {
     std::vector<int> rs;
-    if (n < 1 || n > kMaxSub || !factor_radices(n, rs) || (int)rs.size() > kMaxStages) return false;
+    if (n < 1 || n > kMaxSub || !factor_radices(n, rs, codelet_order) || (int)rs.size() > kMaxStages) return false;
     for (int r : rs)
         if (n / r > nb_of(r) * kFftThreads) return false;  // one transform per stage round
     sf.n = n;
@@ -1339,7 +1349,7 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
         if (cudaMalloc(&fp->partials, fp->n_partials * 2 * sizeof(double)) != cudaSuccess)
             return fail(QVA_ERR_OUT_OF_MEMORY, "cudaMalloc (FFT partials) failed");
     } else if (fp->whole) {
-        if (!make_sub((int)N, fp->row, tw)) return fail(QVA_ERR_UNSUPPORTED, "FFT planning failed");
+        if (!make_sub((int)N, fp->row, tw, false)) return fail(QVA_ERR_UNSUPPORTED, "FFT planning failed");
     } else {
         if (!make_sub(fp->M1, fp->col, tw) || !make_sub(fp->M2, fp->row, tw))
             return fail(QVA_ERR_UNSUPPORTED, "FFT planning failed");
