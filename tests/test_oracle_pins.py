@@ -590,3 +590,120 @@ def test_P18_ex_qaoa_p1_closed_form():
         f = O.expectation(O.evolve_ex(n, u, v, w, th), q)
         ref = _p1_weighted_closed_form(n, u, v, w, 0.0, th[m], gw=list(th[:m] * w))
         assert f == pytest.approx(ref, abs=1e-12)
+
+
+# ---------------------------------------------------------------- evolution loops (P19) ----
+# The p-layer products of the QWOA, QAOAz and generic-sparse oracles, each pinned against a
+# product of dense unitaries built by a route the oracle does not use (closed-form matrices,
+# Pauli Kronecker products, numpy.linalg.eigh).  PAPER.md:46-51 (Eq. 1): layer k applies
+# U_Q(gamma_k) then U_M(beta_k); layer 1 acts first (R6); theta = [g1, b1, ...] (R7).
+# Each test also checks that the plausible mistakes -- mixer before phase, gamma/beta swapped,
+# layers in reverse order -- would NOT pass, so the pin is sensitive to the loop structure.
+
+def _dense_product(psi0, q, mixer_u, theta, order="pm", swap=False, reverse=False):
+    """Dense reference: for k = 1..p, psi <- U_M(b_k) U_Q(g_k) psi with U_Q = expm(-i g diag q)
+    written as the diagonal exp(-i g q_x) (Eq. 3) and U_M = mixer_u(b)."""
+    psi = np.array(psi0, np.complex128)
+    p = len(theta) // 2
+    layers = list(range(p))[::-1] if reverse else range(p)
+    for k in layers:
+        g, b = theta[2 * k], theta[2 * k + 1]
+        if swap:
+            g, b = b, g
+        UQ = np.exp(-1j * g * np.asarray(q))
+        if order == "pm":
+            psi = mixer_u(b) @ (UQ * psi)
+        else:
+            psi = UQ * (mixer_u(b) @ psi)
+    return psi
+
+
+def _assert_loop_pinned(got, psi0, q, mixer_u, theta, tol=1e-12):
+    ref = _dense_product(psi0, q, mixer_u, theta)
+    assert np.max(np.abs(got - ref)) < tol
+    for kw in ({"order": "mp"}, {"swap": True}, {"reverse": True}):
+        bad = _dense_product(psi0, q, mixer_u, theta, **kw)
+        assert np.max(np.abs(bad - ref)) > 1e-4, kw  # the pin distinguishes this mistake
+
+
+def _expm_hermitian(H, t):
+    """exp(-i t H) for a real symmetric / Hermitian H by numpy.linalg.eigh (not scipy expm)."""
+    lam, V = np.linalg.eigh(H)
+    return (V * np.exp(-1j * t * lam)) @ V.conj().T
+
+
+@pytest.mark.parametrize("N,lam0,lam_rest", [(24, 0.0, 24.0), (120, 0.0, 120.0), (37, 1.5, -0.4)])
+def test_P19_qwoa_evolve_complete_vs_dense_product(N, lam0, lam_rest):
+    """QWOA (PAPER.md:298 Eq. qwoa) with the complete-graph-family spectrum: the circulant with
+    lambda = (lam0, c, ..., c) is the matrix c I + (lam0 - c)/N J (J = all ones: the j = 0 mode is
+    the uniform vector).  cfg3's Laplacian (R5) is lam0 = 0, c = N, i.e. N I - J."""
+    rng = np.random.default_rng(N)
+    q = rng.standard_normal(N)
+    theta = rng.uniform(0, math.pi, 8)
+    C = lam_rest * np.eye(N) + (lam0 - lam_rest) / N * np.ones((N, N))
+    psi0 = np.full(N, 1 / math.sqrt(N), np.complex128)
+    psi0 = psi0 * np.exp(1j * rng.uniform(0, 2 * math.pi, N))  # a non-uniform start exercises the mixer
+    got = O.evolve_complete(q, theta, lam0, lam_rest, psi0=psi0)
+    _assert_loop_pinned(got, psi0, q, lambda b: _expm_hermitian(C, b), theta)
+    # default psi0 = |+> (a1)
+    got = O.evolve_complete(q, theta, lam0, lam_rest)
+    ref = _dense_product(np.full(N, 1 / math.sqrt(N), np.complex128), q, lambda b: _expm_hermitian(C, b), theta)
+    assert np.max(np.abs(got - ref)) < 1e-12
+
+
+@pytest.mark.parametrize("N", [16, 45, 64])
+def test_P19_qwoa_evolve_circulant_dense_vs_dense_product(N):
+    """QWOA with an arbitrary symmetric circulant mixer: the dense matrix is
+    scipy's circulant(c) of a random symmetric first column c (c_k = c_{N-k}); its spectrum by
+    forward-DFT bin is lambda_j = sum_k c_k cos(2 pi j k / N), written out here (R4)."""
+    rng = np.random.default_rng(500 + N)
+    c = rng.standard_normal(N)
+    c = 0.5 * (c + np.roll(c[::-1], 1))
+    k = np.arange(N)
+    lam = np.array([np.sum(c * np.cos(2 * math.pi * ((j * k) % N) / N)) for j in range(N)])
+    C = circulant(c)
+    assert np.allclose(C, C.T)
+    q = rng.standard_normal(N)
+    theta = rng.uniform(0, math.pi, 6)
+    psi0 = _rand_state(N, rng)
+    got = O.evolve_circulant_dense(q, lam, theta, psi0=psi0)
+    _assert_loop_pinned(got, psi0, q, lambda b: _expm_hermitian(C, b), theta)
+
+
+@pytest.mark.parametrize("n,seq", [(3, [0, 1, 2]), (5, [4, 0, 2, 1, 3]), (6, [1, 3, 5, 0]), (7, [6, 0, 3, 1, 5, 2, 4])])
+def test_P19_qaoaz_evolve_parity_vs_dense_product(n, seq):
+    """QAOAz (PAPER.md:213-248 Eqs. parity_terms / qaoaz_mixers / qaoaz): per layer the phase, then
+    e^{-itB_odd}, e^{-itB_even}, e^{-itB_last} with each B a sum of dense X_aX_b + Y_aY_b Pauli
+    Kronecker products (R19), exponentiated by eigh."""
+    rng = np.random.default_rng(n * 10 + len(seq))
+    odd, even, last = O.parity_pairs(seq)
+    Bs = [_dense_B(n, pr) for pr in (odd, even, last)]
+
+    def U(t):
+        M = np.eye(1 << n, dtype=complex)
+        for B in Bs:
+            M = _expm_hermitian(B, t) @ M
+        return M
+    q = rng.standard_normal(1 << n)
+    theta = rng.uniform(0, math.pi, 6)
+    psi0 = _rand_state(1 << n, rng)
+    got = O.evolve_parity(n, q, seq, theta, psi0)
+    _assert_loop_pinned(got, psi0, q, U, theta)
+
+
+@pytest.mark.parametrize("N,density", [(12, 0.3), (64, 0.08)])
+def test_P19_generic_sparse_evolve_vs_dense_product(N, density):
+    """Generic QVA with a sparse symmetric mixer W (PAPER.md:46-51 Eq. 1, :72-77 Eq. 4, :333): the
+    oracle's evolve_sparse_dense (scipy expm per layer) against exp(-i beta W) by eigh."""
+    rng = np.random.default_rng(N)
+    W = np.where(rng.uniform(size=(N, N)) < density, rng.uniform(-1, 1, (N, N)), 0.0)
+    W = np.triu(W, 1)
+    W = W + W.T + np.diag(rng.uniform(-0.5, 0.5, N) * (rng.uniform(size=N) < 0.5))
+    q = rng.standard_normal(N)
+    theta = rng.uniform(0, math.pi, 8)
+    psi0 = _rand_state(N, rng)
+    got = O.evolve_sparse_dense(q, W, theta, psi0=psi0)
+    _assert_loop_pinned(got, psi0, q, lambda b: _expm_hermitian(W, b), theta)
+    got = O.evolve_sparse_dense(q, W, theta)
+    ref = _dense_product(np.full(N, 1 / math.sqrt(N), np.complex128), q, lambda b: _expm_hermitian(W, b), theta)
+    assert np.max(np.abs(got - ref)) < 1e-12
