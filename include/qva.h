@@ -94,10 +94,42 @@ typedef struct {
 /* ---- lifecycle (Table 1 plan / destroy) ------------------------------------ */
 
 /* Allocates device memory for the state (and the sharding receive buffer / batch states).
- * QVA_ERR_UNSUPPORTED: X mixer with dim != 2^n_qubits, world not a power of two for the X
- * mixer, world > 1 for the circulant or sparse mixer (not implemented yet). */
+ * world > 1 creates the plan's NCCL communicator from desc->nccl_unique_id (collective: every
+ * rank calls it) and, for sharded X / circulant plans, exports both state buffers as CUDA IPC
+ * handles and maps every peer's (the fused peer-store exchange); if any rank
+ * fails to map, all ranks fall back to NCCL send/recv (decided by a min-vote).
+ * QVA_ERR_UNSUPPORTED: X mixer with dim != 2^n_qubits, world / shard count not a power of two
+ * for the X mixer, sharded sparse or parity mixers (use the replicated mode for their batches),
+ * a sharded circulant dim with no split M1*M2 that the shard count divides. */
 qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out);
-/* NULL-safe; frees everything the plan owns. */
+
+/* Host transport of a world > 1 plan: the caller's own process group (e.g. torch.distributed over
+ * gloo) carries the plan's collectives instead of NCCL.  Every buffer argument is a host buffer
+ * valid for the duration of the call; every rank calls each function in the same order with the
+ * same sizes.  Return 0 on success, non-zero on failure (mapped to QVA_ERR_NCCL).
+ *   allgather(ctx, in, out, bytes): out[r*bytes .. (r+1)*bytes) = rank r's `in` (rank-major).
+ *   allreduce_f64(ctx, vals, n, op): in place element-wise over ranks; op 0 = sum, 1 = max, 2 = min.
+ *   alltoall(ctx, send, recv, chunk_bytes): chunk t of `send` (world chunks) goes to rank t; chunk s
+ *     of `recv` is the one rank s sent to us.
+ * What uses it (COMM-psi; COMM-grad_f, :374-389): the IPC-handle all-gather and
+ * min-vote at plan creation, the one-word barrier after a fused peer-store pass (the library
+ * synchronises its stream first, so every rank's stores into our buffer have landed when the
+ * barrier returns), the <Q> / batch / q-range all-reduces, and the exchange / transpose fallbacks
+ * when IPC is unavailable (device data staged through host memory: slow; tests).  The data path
+ * of the fused exchange stays device-to-device over IPC-mapped peer memory.  This is how the
+ * multi-rank code path runs when several ranks share one GPU (NCCL refuses two ranks per device).
+ * The struct is copied; ctx must outlive the plan. */
+typedef struct {
+    void *ctx;
+    int (*allgather)(void *ctx, const void *in, void *out, uint64_t bytes);
+    int (*allreduce_f64)(void *ctx, double *vals, uint64_t n, int32_t op);
+    int (*alltoall)(void *ctx, const void *send, void *recv, uint64_t chunk_bytes);
+} qva_transport;
+/* qva_plan_create with an optional host transport (NULL = NCCL as in qva_plan_create; non-NULL:
+ * world > 1 and desc->nccl_unique_id is ignored).  QVA_ERR_INVALID_ARGUMENT if a function is NULL. */
+qva_status qva_plan_create_ex(const qva_plan_desc *desc, const qva_transport *transport, qva_plan **out);
+/* NULL-safe; frees everything the plan owns.  For world > 1 it is collective: every rank unmaps
+ * the peers' IPC buffers, then all ranks pass a barrier before any exported buffer is freed. */
 qva_status qva_plan_destroy(qva_plan *plan);
 /* COMM-psi partition of this rank: local_n = local_i, offset = local_i_offset
  * (Eqs. local_i, offset).  Contiguous equal blocks for power-of-two N
@@ -256,6 +288,12 @@ qva_status qva_kernel_stats(qva_plan *plan, int32_t which, double *ms, int64_t *
 qva_status qva_reset_kernel_stats(qva_plan *plan);
 /* Number of kernel launches issued by the plan since the last reset (all classes). */
 qva_status qva_launch_count(qva_plan *plan, int64_t *launches);
+/* Plan introspection (host only, no device work): what = 0: 1 if the global<->local exchange and
+ * the circulant transposes run fused into the pass stores over IPC-mapped peer memory (world > 1)
+ * or over virtual-shard peers, else 0; 1: shard count G (world x virtual shards); 2: 1 if the plan's
+ * collectives run over a host transport (qva_plan_create_ex), else 0; 3: world; 4: rank.
+ * QVA_ERR_INVALID_ARGUMENT for another `what`. */
+qva_status qva_plan_query(const qva_plan *plan, int32_t what, int64_t *out);
 
 const char *qva_status_string(qva_status s);
 const char *qva_last_error(void);

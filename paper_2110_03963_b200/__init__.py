@@ -46,6 +46,64 @@ class PlanDesc(ctypes.Structure):
     ]
 
 
+_AG_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64)
+_AR_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32)
+_A2A_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64)
+
+
+class Transport(ctypes.Structure):
+    """qva_transport (include/qva.h): host collectives of a world > 1 plan."""
+    _fields_ = [("ctx", ctypes.c_void_p), ("allgather", _AG_FN), ("allreduce_f64", _AR_FN), ("alltoall", _A2A_FN)]
+
+
+class TorchHostTransport:
+    """qva_transport over an initialised torch.distributed CPU process group (gloo): the plan's
+    collectives (IPC-handle all-gather, min-vote, barrier, <Q> / batch all-reduce, fallback
+    all-to-all) run as torch collectives on host tensors.  Plumbing only: no arithmetic of the
+    method.  Keep the object alive as long as the plan (Plan does)."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self._torch, self._dist, self._group = torch, dist, group
+        self.world = dist.get_world_size(group)
+
+        def _view(addr, nbytes):
+            return self._torch.frombuffer((ctypes.c_char * nbytes).from_address(addr), dtype=self._torch.uint8)
+
+        def allgather(_ctx, inp, out, nbytes):
+            try:
+                src = _view(inp, nbytes).clone()
+                dst = self._torch.empty(self.world * nbytes, dtype=self._torch.uint8)
+                self._dist.all_gather_into_tensor(dst, src, group=self._group)
+                ctypes.memmove(out, dst.data_ptr(), self.world * nbytes)
+                return 0
+            except Exception:
+                return 1
+
+        def allreduce(_ctx, vals, n, op):
+            try:
+                t = self._torch.frombuffer((ctypes.c_double * n).from_address(vals), dtype=self._torch.float64)
+                ops = {0: self._dist.ReduceOp.SUM, 1: self._dist.ReduceOp.MAX, 2: self._dist.ReduceOp.MIN}
+                self._dist.all_reduce(t, op=ops[int(op)], group=self._group)
+                return 0
+            except Exception:
+                return 1
+
+        def alltoall(_ctx, send, recv, chunk):
+            try:
+                src = _view(send, self.world * chunk).clone()
+                dst = self._torch.empty(self.world * chunk, dtype=self._torch.uint8)
+                self._dist.all_to_all_single(dst, src, group=self._group)
+                ctypes.memmove(recv, dst.data_ptr(), self.world * chunk)
+                return 0
+            except Exception:
+                return 1
+
+        self._fns = (_AG_FN(allgather), _AR_FN(allreduce), _A2A_FN(alltoall))
+        self.struct = Transport(None, *self._fns)
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2110_03963_b200.build` "
@@ -54,6 +112,7 @@ def _load():
     P, u64, i32, d = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double
     sig = {
         "qva_plan_create": [ctypes.POINTER(PlanDesc), ctypes.POINTER(P)],
+        "qva_plan_create_ex": [ctypes.POINTER(PlanDesc), ctypes.POINTER(Transport), ctypes.POINTER(P)],
         "qva_plan_destroy": [P],
         "qva_plan_get_partition": [P, ctypes.POINTER(u64), ctypes.POINTER(u64)],
         "qva_partition": [u64, i32, i32, ctypes.POINTER(u64), ctypes.POINTER(u64)],
@@ -90,6 +149,7 @@ def _load():
         "qva_kernel_stats": [P, i32, ctypes.POINTER(d), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(d)],
         "qva_reset_kernel_stats": [P],
         "qva_launch_count": [P, ctypes.POINTER(ctypes.c_int64)],
+        "qva_plan_query": [P, i32, ctypes.POINTER(ctypes.c_int64)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -226,8 +286,11 @@ class Plan:
                  nccl_id: Optional[bytes] = None, device: int = 0, virtual_shards: int = 1,
                  stream: Optional[int] = None, max_batch: int = 1, replicated: bool = False,
                  qgen_f64_always: bool = False, fft_three_level: bool = False,
-                 peer_store_exchange: bool = False):
+                 peer_store_exchange: bool = False, transport: Optional[TorchHostTransport] = None):
+        """transport: a TorchHostTransport (world > 1) to run the plan's collectives over a torch
+        host process group instead of NCCL (include/qva.h qva_plan_create_ex)."""
         self._h = ctypes.c_void_p()
+        self._transport = transport
         self._id_buf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
         d = PlanDesc()
         d.dim = dim
@@ -244,7 +307,10 @@ class Plan:
         d.reserved[1] = 1 if qgen_f64_always else 0
         d.reserved[2] = 1 if fft_three_level else 0
         d.reserved[3] = 1 if peer_store_exchange else 0
-        _call("qva_plan_create", ctypes.byref(d), ctypes.byref(self._h))
+        if transport is not None:
+            _call("qva_plan_create_ex", ctypes.byref(d), ctypes.byref(transport.struct), ctypes.byref(self._h))
+        else:
+            _call("qva_plan_create", ctypes.byref(d), ctypes.byref(self._h))
         self.dim, self.mixer, self.world, self.rank = dim, mixer, world, rank
 
     # ---- lifecycle
@@ -407,6 +473,13 @@ class Plan:
 
     def reset_kernel_stats(self):
         _call("qva_reset_kernel_stats", self._h)
+
+    def query(self, what) -> int:
+        """qva_plan_query: 'fused_exchange', 'shards', 'host_transport', 'world', 'rank' (or 0..4)."""
+        keys = {"fused_exchange": 0, "shards": 1, "host_transport": 2, "world": 3, "rank": 4}
+        out = ctypes.c_int64()
+        _call("qva_plan_query", self._h, keys.get(what, what), ctypes.byref(out))
+        return out.value
 
     def launch_count(self) -> int:
         n = ctypes.c_int64()

@@ -507,6 +507,7 @@ struct qva_plan {
     unsigned char *graph_stage = nullptr;
     size_t graph_pos = 0, graph_cap = 0;
     std::vector<size_t> graph_offs;
+    bool graph_capture_dirty = false;     // a graph-referenced buffer was dropped during capture
     int64_t q_gen_id = 0;                 // bumped whenever q copies / records are dropped
     double2 *d_mult = nullptr;
     size_t mult_cap = 0;
@@ -557,8 +558,12 @@ struct qva_plan {
     // sparse
     SparseMixer sm;
     bool sparse_set = false;
-    // nccl
+    // collectives of a world > 1 plan: the NCCL communicator, or the caller's host transport
+    // (qva_plan_create_ex); see "multi-process collectives" below
     ncclComm_t comm = nullptr;
+    bool host_tp = false;
+    qva_transport tp = {};
+    bool created = false;                 // qva_plan_create completed (collective teardown allowed)
     // profiling
     bool prof = false;
     KernelStat stats[8];
@@ -655,9 +660,36 @@ int ilog2(uint64_t x) {
     return r;
 }
 
+// Every captured CUDA graph bakes in the raw addresses of the plan's scratch buffers
+// (partials, angle records, phase tables, claim counters, q copies / records).  Any path that
+// frees or recycles one of them first drops the graphs (a replay after a grow would
+// read and write freed memory).  A drop during a capture marks the capture dirty; it is then
+// discarded and the passes run uncaptured.
+void invalidate_graphs(qva_plan *P) {
+    if (P->graph_stage) {
+        P->graph_capture_dirty = true;
+        return;
+    }
+    if (!P->graphs.empty()) {
+        cudaStreamSynchronize(P->stream);  // a replay in flight still reads its staging block
+        for (auto &g : P->graphs) {
+            cudaGraphExecDestroy(g.exec);
+            cudaFreeHost(g.stage);
+        }
+        P->graphs.clear();
+    }
+    P->graph_warm_key.clear();
+}
+// cudaFree of a plan-owned buffer that a captured graph may reference
+void plan_free(qva_plan *P, void *p) {
+    if (!p) return;
+    invalidate_graphs(P);
+    cudaFree(p);
+}
+
 qva_status ensure_partials(qva_plan *P, uint64_t n) {
     if (P->partials_n >= n) return QVA_OK;
-    if (P->partials) cudaFree(P->partials);
+    plan_free(P, P->partials);
     P->partials = nullptr;
     QVA_CUDA_TRY(cudaMalloc(&P->partials, n * 2 * sizeof(double)));
     P->partials_n = n;
@@ -666,7 +698,7 @@ qva_status ensure_partials(qva_plan *P, uint64_t n) {
 
 qva_status ensure_angles(qva_plan *P, size_t n) {
     if (P->angles_cap >= n) return QVA_OK;
-    if (P->d_angles) cudaFree(P->d_angles);
+    plan_free(P, P->d_angles);
     P->d_angles = nullptr;
     QVA_CUDA_TRY(cudaMalloc(&P->d_angles, n * sizeof(PassAngles)));
     P->angles_cap = n;
@@ -679,6 +711,90 @@ qva_status check_theta(const double *theta, size_t n) {
             set_error("non-finite theta");
             return QVA_ERR_NUMERIC;
         }
+    return QVA_OK;
+}
+
+// ---- multi-process collectives (world > 1) -------------------------------------------------------
+// Every collective of a multi-process plan goes through these four calls.  NCCL runs them on the
+// plan's stream (stream-ordered with the kernels around them); a host transport (qva_transport,
+// include/qva.h) runs them on host buffers after synchronising the stream.
+enum { kCollSum = 0, kCollMax = 1, kCollMin = 2 };
+
+qva_status tp_check(int rc, const char *what) {
+    if (rc == 0) return QVA_OK;
+    set_error(std::string("host transport ") + what + " failed (" + std::to_string(rc) + ")");
+    return QVA_ERR_NCCL;
+}
+cudaError_t scratch_get(qva_plan *P, void **p, size_t bytes);
+
+// element-wise reduction of n host doubles over ranks, in place.  NCCL stages through `dev` (n
+// doubles of device memory; NULL -> the plan's scratch) with stream-ordered copies.
+qva_status coll_allreduce_host(qva_plan *P, double *vals, int n, int op, double *dev = nullptr) {
+    if (P->world == 1 || n <= 0) return QVA_OK;
+    if (P->host_tp) return tp_check(P->tp.allreduce_f64(P->tp.ctx, vals, (uint64_t)n, op), "allreduce");
+    double *d = dev;
+    if (!d) QVA_CUDA_TRY(scratch_get(P, (void **)&d, n * sizeof(double)));
+    const ncclRedOp_t nop = op == kCollMax ? ncclMax : (op == kCollMin ? ncclMin : ncclSum);
+    QVA_CUDA_TRY(cudaMemcpyAsync(d, vals, n * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+    QVA_NCCL_TRY(ncclAllReduce(d, d, n, ncclDouble, nop, P->comm, P->stream));
+    QVA_CUDA_TRY(cudaMemcpyAsync(vals, d, n * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
+    QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
+    return QVA_OK;
+}
+
+// all-gather of `bytes` host bytes per rank into out[world * bytes] (rank-major).  NCCL stages
+// through `dev` ((world + 1) * bytes of device memory).  Every copy is on the plan's stream, so
+// the staging is ordered before the collective (a synchronous cudaMemcpy on the legacy
+// stream is not ordered with a non-blocking stream's NCCL kernel).
+qva_status coll_allgather_host(qva_plan *P, const void *in, void *out, size_t bytes, unsigned char *dev) {
+    if (P->host_tp) return tp_check(P->tp.allgather(P->tp.ctx, in, out, bytes), "allgather");
+    QVA_CUDA_TRY(cudaMemcpyAsync(dev, in, bytes, cudaMemcpyHostToDevice, P->stream));
+    QVA_NCCL_TRY(ncclAllGather(dev, dev + bytes, bytes, ncclChar, P->comm, P->stream));
+    QVA_CUDA_TRY(cudaMemcpyAsync(out, dev + bytes, bytes * P->world, cudaMemcpyDeviceToHost, P->stream));
+    QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
+    return QVA_OK;
+}
+
+// barrier ordered after this rank's stream work: once it completes on every rank, every rank's
+// kernels enqueued before it (e.g. stores into our buffers over peer memory, which end with
+// __threadfence_system) are done.  NCCL: a one-word all-reduce on the stream (no host wait); host
+// transport: synchronise the stream, then a one-value all-reduce.
+qva_status coll_stream_barrier(qva_plan *P) {
+    if (P->world == 1) return QVA_OK;
+    if (P->host_tp) {
+        QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
+        double z = 0.0;
+        return tp_check(P->tp.allreduce_f64(P->tp.ctx, &z, 1, kCollSum), "barrier");
+    }
+    QVA_CUDA_TRY(cudaMemsetAsync(P->d_bar, 0, sizeof(int), P->stream));
+    QVA_NCCL_TRY(ncclAllReduce(P->d_bar, P->d_bar, 1, ncclInt32, ncclSum, P->comm, P->stream));
+    return QVA_OK;
+}
+
+// all-to-all of device chunks: chunk t of src (chunk_bytes each) goes to rank t, chunk s of dst
+// comes from rank s; our own chunk is a local copy.  NCCL: grouped send/recv on the stream.  Host
+// transport: the whole src through host memory (fallback / tests only).
+qva_status coll_alltoall_dev(qva_plan *P, const void *src, void *dst, size_t chunk_bytes) {
+    const char *s = (const char *)src;
+    char *d = (char *)dst;
+    if (P->host_tp) {
+        std::vector<char> hs(chunk_bytes * P->world), hr(chunk_bytes * P->world);
+        QVA_CUDA_TRY(cudaMemcpyAsync(hs.data(), s, hs.size(), cudaMemcpyDeviceToHost, P->stream));
+        QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
+        QVA_TRY(tp_check(P->tp.alltoall(P->tp.ctx, hs.data(), hr.data(), chunk_bytes), "alltoall"));
+        QVA_CUDA_TRY(cudaMemcpyAsync(d, hr.data(), hr.size(), cudaMemcpyHostToDevice, P->stream));
+        QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
+        return QVA_OK;
+    }
+    QVA_NCCL_TRY(ncclGroupStart());
+    for (int t = 0; t < P->world; ++t) {
+        if (t == P->rank) continue;
+        QVA_NCCL_TRY(ncclSend(s + t * chunk_bytes, chunk_bytes, ncclChar, t, P->comm, P->stream));
+        QVA_NCCL_TRY(ncclRecv(d + t * chunk_bytes, chunk_bytes, ncclChar, t, P->comm, P->stream));
+    }
+    QVA_NCCL_TRY(ncclGroupEnd());
+    QVA_CUDA_TRY(cudaMemcpyAsync(d + P->rank * chunk_bytes, s + P->rank * chunk_bytes, chunk_bytes,
+                                 cudaMemcpyDeviceToDevice, P->stream));
     return QVA_OK;
 }
 
@@ -695,21 +811,8 @@ qva_status exchange_buffers(qva_plan *P, T *src, T *dst) {
         return QVA_OK;
     }
     ProfScope ps(P, K_EXCHANGE, 2.0 * sizeof(T) * (double)P->arr_n);
-    size_t cnt = C * sizeof(T) / sizeof(double);
-    std::vector<int32_t> peer(P->world), pchunk(P->world);
-    QVA_TRY(qva_exchange_plan(P->world, P->rank, peer.data(), pchunk.data()));
-    QVA_NCCL_TRY(ncclGroupStart());
-    for (int t = 0; t < P->world; ++t) {
-        if (peer[t] == P->rank) continue;
-        // send our chunk t to peer[t]; receive the peer's chunk pchunk into our chunk t (the plan is
-        // symmetric: the peer sends us its chunk `rank`, which lands in our chunk t)
-        QVA_NCCL_TRY(ncclSend((const double *)(src + t * C), cnt, ncclDouble, peer[t], P->comm, P->stream));
-        QVA_NCCL_TRY(ncclRecv((double *)(dst + t * C), cnt, ncclDouble, peer[t], P->comm, P->stream));
-    }
-    QVA_NCCL_TRY(ncclGroupEnd());
-    QVA_CUDA_TRY(cudaMemcpyAsync(dst + P->rank * C, src + P->rank * C, C * sizeof(T), cudaMemcpyDeviceToDevice,
-                                 P->stream));
-    return QVA_OK;
+    // chunk t (top local bits = t) goes to rank t, where it becomes chunk `rank` (qva_exchange_plan)
+    return coll_alltoall_dev(P, src, dst, C * sizeof(T));
 }
 
 qva_status ensure_q_dev(qva_plan *P);
@@ -738,17 +841,7 @@ qva_status ensure_qB(qva_plan *P) {
             QVA_CUDA_TRY(launch_chunk_transpose_bytes(P->qcB, P->qc, P->G, C, eb, P->stream));
         } else {
             ProfScope ps(P, K_EXCHANGE, 2.0 * eb * (double)P->arr_n);
-            const char *src = (const char *)P->qc;
-            char *dst = (char *)P->qcB;
-            QVA_NCCL_TRY(ncclGroupStart());
-            for (int t = 0; t < P->world; ++t) {
-                if (t == P->rank) continue;
-                QVA_NCCL_TRY(ncclSend(src + t * C * eb, C * eb, ncclInt8, t, P->comm, P->stream));
-                QVA_NCCL_TRY(ncclRecv(dst + t * C * eb, C * eb, ncclInt8, t, P->comm, P->stream));
-            }
-            QVA_NCCL_TRY(ncclGroupEnd());
-            QVA_CUDA_TRY(cudaMemcpyAsync(dst + P->rank * C * eb, src + P->rank * C * eb, C * eb,
-                                         cudaMemcpyDeviceToDevice, P->stream));
+            QVA_TRY(coll_alltoall_dev(P, P->qc, P->qcB, C * eb));
         }
         P->qcB_valid = true;
     }
@@ -786,13 +879,7 @@ qva_status classify_q(qva_plan *P) {
     }
     if (P->world > 1) {
         double v[3] = {(double)flag, -lo, hi};
-        // max-reduce via NCCL
-        double *d;
-        QVA_CUDA_TRY(scratch_get(P, (void **)&d, sizeof(v)));
-        QVA_CUDA_TRY(cudaMemcpyAsync(d, v, sizeof(v), cudaMemcpyHostToDevice, P->stream));
-        QVA_NCCL_TRY(ncclAllReduce(d, d, 3, ncclDouble, ncclMax, P->comm, P->stream));
-        QVA_CUDA_TRY(cudaMemcpyAsync(v, d, sizeof(v), cudaMemcpyDeviceToHost, P->stream));
-        QVA_TRY(sync(P));
+        QVA_TRY(coll_allreduce_host(P, v, 3, kCollMax));
         flag = v[0] != 0.0;
         lo = -v[1];
         hi = v[2];
@@ -802,10 +889,10 @@ qva_status classify_q(qva_plan *P) {
     if (lo >= -128 && hi <= 127) eb = 1;
     else if (lo >= -32768 && hi <= 32767) eb = 2;
     if (!eb) return QVA_OK;
-    if (P->qc) cudaFree(P->qc);
+    plan_free(P, P->qc);
     P->qc = nullptr;
     QVA_CUDA_TRY(cudaMalloc(&P->qc, P->arr_n * eb));
-    if (P->qcB) cudaFree(P->qcB);
+    plan_free(P, P->qcB);
     P->qcB = nullptr;
     {
         ProfScope ps(P, K_OTHER, (8.0 + eb) * P->arr_n);
@@ -825,7 +912,9 @@ qva_status to_layout_A(qva_plan *P) {
 }
 
 void pool_put(qva_plan *P, void *p, size_t bytes) {
-    if (p) P->pool.push_back({bytes, p});
+    if (!p) return;
+    invalidate_graphs(P);  // the buffer may be handed to another use by pool_get
+    P->pool.push_back({bytes, p});
 }
 // smallest pooled buffer of at least `bytes` (exact-size reuse is the common case), else cudaMalloc
 cudaError_t pool_get(qva_plan *P, void **p, size_t bytes) {
@@ -885,7 +974,7 @@ qva_status upload(qva_plan *P, void *dst, const void *src, size_t bytes) {
 // call returns); stream-ordered allocation measured host stalls of up to 100+ ms per call
 cudaError_t scratch_get(qva_plan *P, void **p, size_t bytes) {
     if (P->scratch_cap < bytes) {
-        cudaFree(P->scratch);
+        plan_free(P, P->scratch);
         P->scratch = nullptr;
         P->scratch_cap = 0;
         cudaError_t e = cudaMalloc(&P->scratch, bytes);
@@ -930,7 +1019,7 @@ qva_status ensure_q_dev(qva_plan *P) {
     const int m = P->g_m;
     const size_t need = (size_t)std::max(m, 1) * (2 * sizeof(int32_t) + sizeof(double));
     if (P->edge_cap < need) {
-        cudaFree(P->d_edges);
+        plan_free(P, P->d_edges);
         P->d_edges = nullptr;
         QVA_CUDA_TRY(cudaMalloc(&P->d_edges, need));
         P->edge_cap = need;
@@ -1179,7 +1268,7 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
     QVA_CUDA_TRY(pool_get(P, &ent.G, 32 * sizeof(double)));
     const size_t eb = (tt.size() + tb.size()) * (sizeof(int2) + sizeof(double)) + 16;
     if (P->gen_edge_cap < eb) {  // stream order keeps one staging buffer safe across entries
-        cudaFree(P->d_gen_edges);
+        plan_free(P, P->d_gen_edges);
         P->d_gen_edges = nullptr;
         QVA_CUDA_TRY(cudaMalloc(&P->d_gen_edges, eb));
         P->gen_edge_cap = eb;
@@ -1391,20 +1480,20 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
     const int ntab = gen == kQGenInt ? P->g_m + 1 : (int_table ? (P->qmax - P->qmin + 1) : 0);
     if (!gam.empty()) {
         if (P->gam_cap < gam.size()) {
-            cudaFree(P->d_gam);
+            plan_free(P, P->d_gam);
             P->d_gam = nullptr;
             QVA_CUDA_TRY(cudaMalloc(&P->d_gam, gam.size() * sizeof(double)));
             P->gam_cap = gam.size();
         }
         if (P->tab_cap < gam.size() * ntab) {
-            cudaFree(P->d_tab);
+            plan_free(P, P->d_tab);
             P->d_tab = nullptr;
             QVA_CUDA_TRY(cudaMalloc(&P->d_tab, gam.size() * ntab * sizeof(double2)));
             P->tab_cap = gam.size() * ntab;
         }
         QVA_TRY(upload(P, P->d_gam, gam.data(), gam.size() * sizeof(double)));
         if (P->mult_cap < gam.size()) {
-            cudaFree(P->d_mult);
+            plan_free(P, P->d_mult);
             P->d_mult = nullptr;
             QVA_CUDA_TRY(cudaMalloc(&P->d_mult, gam.size() * sizeof(double2)));
             P->mult_cap = gam.size();
@@ -1430,7 +1519,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
     }();
     if (g_dyn) {
         if (P->ctr_cap < n_tile_passes) {
-            cudaFree(P->d_ctr);
+            plan_free(P, P->d_ctr);
             P->d_ctr = nullptr;
             const int cap = std::max(n_tile_passes, 64);
             QVA_CUDA_TRY(cudaMalloc(&P->d_ctr, cap * sizeof(unsigned long long)));
@@ -1641,8 +1730,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         if (xpeer && !xvirt) {
             // every rank's stores into our buffer are done once every rank's pass has finished:
             // a one-word all-reduce on the stream is that barrier
-            QVA_CUDA_TRY(cudaMemsetAsync(P->d_bar, 0, sizeof(int), P->stream));
-            QVA_NCCL_TRY(ncclAllReduce(P->d_bar, P->d_bar, 1, ncclInt32, ncclSum, P->comm, P->stream));
+            QVA_TRY(coll_stream_barrier(P));
         }
         if (!xbit.empty() || xpeer) {
             P->layout ^= 1;  // what exchange_state would have done
@@ -1714,6 +1802,7 @@ qva_status run_passes_graph(qva_plan *P, const std::vector<PassPlan> &passes, co
     P->graph_pos = 0;
     P->graph_cap = cap;
     P->graph_offs.clear();
+    P->graph_capture_dirty = false;
     cudaGraph_t graph = nullptr;
     QVA_CUDA_TRY(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
     const int64_t launches0 = P->launches;
@@ -1726,7 +1815,8 @@ qva_status run_passes_graph(qva_plan *P, const std::vector<PassPlan> &passes, co
     g.alt_after = P->psi_alt;
     P->psi = psi0;
     P->psi_alt = alt0;
-    if (st != QVA_OK || ce != cudaSuccess || P->graph_offs.size() > 3) {
+    if (st != QVA_OK || ce != cudaSuccess || P->graph_offs.size() > 3 || P->graph_capture_dirty) {
+        P->graph_capture_dirty = false;
         if (graph) cudaGraphDestroy(graph);
         cudaFreeHost(g.stage);
         cudaGetLastError();
@@ -1768,8 +1858,20 @@ bool fuse_exchange_enabled() {
 // handles, all-gathered over the plan's NCCL communicator and mapped (NVLink P2P), so the pass
 // before a global<->local exchange can store each tile straight into its receiving rank's
 // buffer.  Any failure leaves ipc_ok = false and the exchange runs as NCCL send/recv.
+// unmap every peer buffer this rank opened (ours are not IPC mappings)
+void close_peer_maps(qva_plan *P) {
+    for (int k = 0; k < 2; ++k)
+        for (int t = 0; t < kMaxPeers; ++t) {
+            double2 *ptr = P->ipc_peer[k][t];
+            if (ptr && ptr != P->ipc_own[k]) cudaIpcCloseMemHandle(ptr);
+            P->ipc_peer[k][t] = nullptr;
+        }
+    cudaGetLastError();
+}
+
 void setup_peer_exchange(qva_plan *P) {
-    if (!fuse_exchange_enabled() || P->world > kMaxPeers || !P->psi || !P->psi_alt || !P->comm) return;
+    if (!fuse_exchange_enabled() || P->world > kMaxPeers || !P->psi || !P->psi_alt || (!P->comm && !P->host_tp))
+        return;
     P->ipc_own[0] = P->psi;
     P->ipc_own[1] = P->psi_alt;
     // every rank takes part in both collectives below whatever happens locally (a rank that
@@ -1779,12 +1881,9 @@ void setup_peer_exchange(qva_plan *P) {
     bool ok = cudaIpcGetMemHandle((cudaIpcMemHandle_t *)mine.data(), P->psi) == cudaSuccess &&
               cudaIpcGetMemHandle((cudaIpcMemHandle_t *)(mine.data() + hb), P->psi_alt) == cudaSuccess;
     cudaGetLastError();
-    // staging in the (not yet used) receive buffer: no allocation that could fail on one rank only
+    // NCCL staging in the (not yet used) receive buffer: no allocation that could fail on one rank
     unsigned char *dbuf = reinterpret_cast<unsigned char *>(P->psi_alt);
-    const bool g = cudaMemcpy(dbuf, mine.data(), 2 * hb, cudaMemcpyHostToDevice) == cudaSuccess &&
-                   ncclAllGather(dbuf, dbuf + 2 * hb, 2 * hb, ncclChar, P->comm, P->stream) == ncclSuccess &&
-                   cudaStreamSynchronize(P->stream) == cudaSuccess &&
-                   cudaMemcpy(all.data(), dbuf + 2 * hb, all.size(), cudaMemcpyDeviceToHost) == cudaSuccess;
+    const bool g = coll_allgather_host(P, mine.data(), all.data(), 2 * hb, dbuf) == QVA_OK;
     ok = ok && g;
     // a rank whose handles failed sent zeros: opening those fails here, and the vote below
     // turns the fused path off everywhere
@@ -1800,29 +1899,17 @@ void setup_peer_exchange(qva_plan *P) {
             ok = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
             P->ipc_peer[k][t] = (double2 *)ptr;
         }
-    if (ok) ok = cudaMalloc(&P->d_bar, sizeof(int)) == cudaSuccess;
-    // every rank must agree, or the ranks would run different exchange code
-    int flag = ok ? 1 : 0;
-    int *dflag = reinterpret_cast<int *>(P->psi_alt);
-    if (cudaMemcpy(dflag, &flag, sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
-        ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, P->comm, P->stream) != ncclSuccess ||
-        cudaStreamSynchronize(P->stream) != cudaSuccess ||
-        cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
-        flag = 0;
+    if (ok && !P->host_tp) ok = cudaMalloc(&P->d_bar, sizeof(int)) == cudaSuccess;
     cudaGetLastError();
-    P->ipc_ok = flag == 1;
+    // every rank must agree, or the ranks would run different exchange code
+    double flag = ok ? 1.0 : 0.0;
+    if (coll_allreduce_host(P, &flag, 1, kCollMin, reinterpret_cast<double *>(P->psi_alt)) != QVA_OK) flag = 0.0;
+    cudaGetLastError();
+    P->ipc_ok = flag == 1.0;
+    if (!P->ipc_ok) close_peer_maps(P);
 }
 
-qva_status allreduce_host(qva_plan *P, double *vals, int n) {
-    if (P->world == 1) return QVA_OK;
-    double *d;
-    QVA_CUDA_TRY(scratch_get(P, (void **)&d, n * sizeof(double)));
-    QVA_CUDA_TRY(cudaMemcpyAsync(d, vals, n * sizeof(double), cudaMemcpyHostToDevice, P->stream));
-    QVA_NCCL_TRY(ncclAllReduce(d, d, n, ncclDouble, ncclSum, P->comm, P->stream));
-    QVA_CUDA_TRY(cudaMemcpyAsync(vals, d, n * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
-    QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
-    return QVA_OK;
-}
+qva_status allreduce_host(qva_plan *P, double *vals, int n) { return coll_allreduce_host(P, vals, n, kCollSum); }
 
 // generic (non-tile) expectation over this process's arrays
 qva_status expect_generic(qva_plan *P, const double2 *psi, uint64_t n, const double *q, double *out2) {
@@ -1868,18 +1955,7 @@ qva_status shard_to_col(qva_plan *P, const T *row, T *col) {
     }
     T *snd = reinterpret_cast<T *>(P->xfer);
     QVA_CUDA_TRY(launch_block_transpose<T>(snd, row, M1s, (uint64_t)G, M2s, P->stream));
-    const uint64_t chunk = M1s * M2s;
-    const size_t cnt = chunk * sizeof(T) / sizeof(double);
-    QVA_NCCL_TRY(ncclGroupStart());
-    for (int s = 0; s < G; ++s) {
-        if (s == P->rank) continue;
-        QVA_NCCL_TRY(ncclSend((const double *)(snd + s * chunk), cnt, ncclDouble, s, P->comm, P->stream));
-        QVA_NCCL_TRY(ncclRecv((double *)(col + s * chunk), cnt, ncclDouble, s, P->comm, P->stream));
-    }
-    QVA_NCCL_TRY(ncclGroupEnd());
-    QVA_CUDA_TRY(cudaMemcpyAsync(col + P->rank * chunk, snd + P->rank * chunk, chunk * sizeof(T),
-                                 cudaMemcpyDeviceToDevice, P->stream));
-    return QVA_OK;
+    return coll_alltoall_dev(P, snd, col, M1s * M2s * sizeof(T));
 }
 template <typename T>
 qva_status shard_to_row(qva_plan *P, const T *col, T *row) {
@@ -1891,17 +1967,7 @@ qva_status shard_to_row(qva_plan *P, const T *col, T *row) {
         return QVA_OK;
     }
     T *rcv = reinterpret_cast<T *>(P->xfer);
-    const uint64_t chunk = M1s * M2s;
-    const size_t cnt = chunk * sizeof(T) / sizeof(double);
-    QVA_NCCL_TRY(ncclGroupStart());
-    for (int s = 0; s < G; ++s) {
-        if (s == P->rank) continue;
-        QVA_NCCL_TRY(ncclSend((const double *)(col + s * chunk), cnt, ncclDouble, s, P->comm, P->stream));
-        QVA_NCCL_TRY(ncclRecv((double *)(rcv + s * chunk), cnt, ncclDouble, s, P->comm, P->stream));
-    }
-    QVA_NCCL_TRY(ncclGroupEnd());
-    QVA_CUDA_TRY(cudaMemcpyAsync(rcv + P->rank * chunk, col + P->rank * chunk, chunk * sizeof(T),
-                                 cudaMemcpyDeviceToDevice, P->stream));
+    QVA_TRY(coll_alltoall_dev(P, col, rcv, M1s * M2s * sizeof(T)));
     QVA_CUDA_TRY(launch_block_transpose<T>(row, rcv, (uint64_t)G, M1s, M2s, P->stream));
     return QVA_OK;
 }
@@ -1913,9 +1979,7 @@ struct PlanShardIO : FftShardIO {
     qva_status to_row(const double2 *col, double2 *row) override { return shard_to_row<double2>(P, col, row); }
     qva_status barrier() override {
         if (P->world == 1) return QVA_OK;  // virtual shards: stream order
-        QVA_CUDA_TRY(cudaMemsetAsync(P->d_bar, 0, sizeof(int), P->stream));
-        QVA_NCCL_TRY(ncclAllReduce(P->d_bar, P->d_bar, 1, ncclInt32, ncclSum, P->comm, P->stream));
-        return QVA_OK;
+        return coll_stream_barrier(P);
     }
 };
 
@@ -2333,6 +2397,16 @@ qva_status qva_plan_destroy(qva_plan *P) {
     DeviceGuard dg(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     harvest(P);
+    if (P->ipc_ok) {
+        // collective teardown: unmap the peers' buffers, then wait until every rank has unmapped
+        // ours before freeing them (freeing exported memory that a peer still maps is undefined)
+        close_peer_maps(P);
+        if (P->created) {
+            if (coll_stream_barrier(P) != QVA_OK) fprintf(stderr, "[qva] destroy: barrier failed: %s\n", qva_last_error());
+            cudaStreamSynchronize(P->stream);
+        }
+        P->ipc_ok = false;
+    }
     cudaFree(P->psi);
     cudaFree(P->psi_alt);
     cudaFree(P->xfer);
@@ -2383,9 +2457,15 @@ qva_status qva_plan_destroy(qva_plan *P) {
     return QVA_OK;
 }
 
-qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
+qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) { return qva_plan_create_ex(desc, nullptr, out); }
+
+qva_status qva_plan_create_ex(const qva_plan_desc *desc, const qva_transport *transport, qva_plan **out) {
     if (!desc || !out) {
         set_error("qva_plan_create: NULL argument");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    if (transport && (!transport->allgather || !transport->allreduce_f64 || !transport->alltoall)) {
+        set_error("qva_plan_create_ex: every transport function must be non-NULL");
         return QVA_ERR_INVALID_ARGUMENT;
     }
     *out = nullptr;
@@ -2504,7 +2584,10 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
             return fail(QVA_ERR_UNSUPPORTED);
         }
     }
-    if (d.world > 1) {
+    if (d.world > 1 && transport) {
+        P->host_tp = true;
+        P->tp = *transport;
+    } else if (d.world > 1) {
         if (!d.nccl_unique_id) {
             set_error("world > 1 needs nccl_unique_id");
             return fail(QVA_ERR_INVALID_ARGUMENT);
@@ -2524,6 +2607,7 @@ qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out) {
         set_error("plan init failed");
         return fail(QVA_ERR_CUDA);
     }
+    P->created = true;
     *out = P;
     return QVA_OK;
 }
@@ -3093,7 +3177,7 @@ static qva_status ex_impl(qva_plan *P, const double *theta, int p, bool *have_re
     if (p == 0) return QVA_OK;
     const size_t need = (size_t)std::max(m, 1) * 2 * sizeof(int32_t) + wx.size() * sizeof(double) + 16;
     if (P->ex_edge_cap < need) {
-        cudaFree(P->d_ex_edges);
+        plan_free(P, P->d_ex_edges);
         P->d_ex_edges = nullptr;
         QVA_CUDA_TRY(cudaMalloc(&P->d_ex_edges, need));
         P->ex_edge_cap = need;
@@ -3224,19 +3308,19 @@ static qva_status batch_local(qva_plan *P, const double *thetas, int first, int 
                 QVA_TRY(ensure_q_dev(P));
                 size_t need = (size_t)nb * 2 * p;
                 if (need > P->thetas_cap) {
-                    cudaFree(P->d_thetas);
+                    plan_free(P, P->d_thetas);
                     P->d_thetas = nullptr;
                     QVA_CUDA_TRY(cudaMalloc(&P->d_thetas, need * sizeof(double)));
                     P->thetas_cap = need;
                 }
                 if ((size_t)nb > (size_t)P->max_batch) {
-                    cudaFree(P->red);
+                    plan_free(P, P->red);
                     P->red = nullptr;
                     QVA_CUDA_TRY(cudaMalloc(&P->red, (size_t)nb * 2 * sizeof(double)));
                     P->max_batch = nb;
                 }
                 if (P->small_batch_cap < (size_t)nb * P->arr_n) {
-                    cudaFree(P->small_batch);
+                    plan_free(P, P->small_batch);
                     P->small_batch = nullptr;
                     QVA_CUDA_TRY(cudaMalloc(&P->small_batch, (size_t)nb * P->arr_n * sizeof(double2)));
                     P->small_batch_cap = (size_t)nb * P->arr_n;
@@ -3396,6 +3480,21 @@ qva_status qva_launch_count(qva_plan *P, int64_t *launches) {
     if (!P || !launches) return QVA_ERR_INVALID_ARGUMENT;
     *launches = P->launches;
     return QVA_OK;
+}
+
+qva_status qva_plan_query(const qva_plan *P, int32_t what, int64_t *out) {
+    if (!P || !out) return QVA_ERR_INVALID_ARGUMENT;
+    switch (what) {
+        case 0:
+            *out = P->world > 1 ? (P->ipc_ok ? 1 : 0)
+                                : ((P->G > 1 && fuse_exchange_enabled() && P->d.reserved[3] != 0) ? 1 : 0);
+            return QVA_OK;
+        case 1: *out = P->G; return QVA_OK;
+        case 2: *out = P->host_tp ? 1 : 0; return QVA_OK;
+        case 3: *out = P->world; return QVA_OK;
+        case 4: *out = P->rank; return QVA_OK;
+        default: set_error("qva_plan_query: unknown query"); return QVA_ERR_INVALID_ARGUMENT;
+    }
 }
 
 }  // extern "C"

@@ -808,15 +808,14 @@ __global__ void gen_records_kernel(unsigned char *rec, uint64_t n_tiles, uint32_
 template <int STAGES, int QB, int PROG>
 cudaError_t launch_one(const CUtensorMap &map, const CUtensorMap &map_out, const TilePassParams &p, int grid,
                        cudaStream_t s) {
-    static bool configured = false;
+    static DeviceOnce configured;
     constexpr size_t smem = tile_smem_bytes<STAGES, QB>();
     static_assert(smem <= 232448, "shared memory budget");
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tile_pass_kernel<STAGES, QB, PROG>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = once_per_device(configured, [] {
+        return cudaFuncSetAttribute(tile_pass_kernel<STAGES, QB, PROG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem);
+    });
+    if (e != cudaSuccess) return e;
     tile_pass_kernel<STAGES, QB, PROG><<<grid, kThreads, smem, s>>>(map, map_out, p);
     return cudaGetLastError();
 }

@@ -376,14 +376,13 @@ cudaError_t launch_q_encode(const double *q, uint64_t n, void *codes, int bytes,
 }
 
 cudaError_t launch_small_evolve(const SmallEvolveParams &p, int batch, cudaStream_t s) {
-    static bool configured = false;
+    static DeviceOnce configured;
     size_t smem = ((size_t)1 << p.n) * sizeof(double2);
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(small_evolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(((size_t)1 << kSmallMaxQubits) * sizeof(double2)));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = once_per_device(configured, [] {
+        return cudaFuncSetAttribute(small_evolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(((size_t)1 << kSmallMaxQubits) * sizeof(double2)));
+    });
+    if (e != cudaSuccess) return e;
     small_evolve_kernel<<<batch, kSmallThreads, smem, s>>>(p);
     return cudaGetLastError();
 }
@@ -536,12 +535,12 @@ __global__ void __launch_bounds__(256) parity_window_kernel(double2 *__restrict_
 }
 
 cudaError_t launch_parity_window(double2 *psi, const ParityWindow &p, cudaStream_t s) {
-    static bool configured = false;
+    static DeviceOnce configured;
     const size_t smem = ((size_t)1 << p.w) * sizeof(double2);
-    if (!configured) {
-        cudaFuncSetAttribute(parity_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        configured = true;
-    }
+    cudaError_t e = once_per_device(configured, [] {
+        return cudaFuncSetAttribute(parity_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    });
+    if (e != cudaSuccess) return e;
     const uint64_t tiles = 1ull << (p.n - p.w);
     const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms() * 3);
     parity_window_kernel<<<grid, 256, smem, s>>>(psi, p);

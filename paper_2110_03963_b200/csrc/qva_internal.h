@@ -7,6 +7,7 @@
 #include <nccl.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -164,6 +165,25 @@ constexpr TileProg kTileProgs[kNumTileProgs] = {
 int tile_pass_grid(uint64_t items);
 // SM count of the current device (cached; grids are sized in multiples of it)
 int num_sms();
+
+// Function attributes (the >48 KiB dynamic shared-memory opt-in) belong to a device context, so
+// a kernel's attribute is set once per (kernel, device): a device bit mask under a mutex (plans
+// on several devices, or on several threads, may coexist).
+struct DeviceOnce {
+    std::mutex m;
+    uint64_t mask = 0;
+};
+template <class F>
+cudaError_t once_per_device(DeviceOnce &o, F &&f) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(o.m);
+    if ((o.mask >> dev) & 1ull) return cudaSuccess;
+    e = f();
+    if (e == cudaSuccess) o.mask |= 1ull << dev;
+    return e;
+}
 int tile_consumer_warps();
 // builds the 5-D load map of psi_in seen through P.tile_bits and the store map of the same box
 // into psi_out through the bit permutation obit (nullptr: identity); fills P.dim_*, P.member_dim

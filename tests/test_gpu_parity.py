@@ -165,6 +165,51 @@ def test_repeated_evolutions_graph_replay(Q):
             _f_close(P.expectation(), O.expectation(O.evolve_x(n, q2, th), q2))
 
 
+def test_graph_replay_survives_buffer_growth(Q):
+    """a captured evolution graph bakes in the addresses of the plan's scratch
+    buffers; a later call that grows one of them (a larger p, a batch, a step-level expectation,
+    a new q) must not leave a replay on freed memory.  Pattern: p=2 (warm, capture, replay), p=3,
+    a batch, a non-fused expectation, then p=2 again -- every result against the oracle."""
+    n = 22
+    rng = np.random.default_rng(99)
+    u, v = random_regular_graph(n, 3, rng)
+    q = O.maxcut_q(n, u, v)
+    with Q.Plan(1 << n, "x", n_qubits=n, max_batch=3) as P:
+        P.set_qualities_maxcut(u, v)
+        for _ in range(3):  # warm, capture, replay
+            th = rng.uniform(0, math.pi, 4)
+            P.evolve(th)
+            _f_close(P.expectation(), O.expectation(O.evolve_x(n, q, th), q))
+        th3 = rng.uniform(0, math.pi, 6)
+        for _ in range(3):  # p = 3: more passes, more angle records / tables
+            P.evolve(th3)
+        _f_close(P.expectation(), O.expectation(O.evolve_x(n, q, th3), q))
+        ths = rng.uniform(0, math.pi, (3, 8))
+        f = P.evolve_batch(ths)  # p = 4 batch: partials / angles for 3 members
+        for b in range(3):
+            _f_close(f[b], O.expectation(O.evolve_x(n, q, ths[b]), q))
+        P.reset_state()
+        P.apply_phase(0.4)
+        P.apply_mixer(0.9)
+        r = O.init_uniform(1 << n)
+        O.phase(r, q, 0.4)
+        O.mixer_x(r, 0.9)
+        _f_close(P.expectation(), O.expectation(r, q))  # generic expectation: more partial slots
+        w = rng.uniform(0, 1, len(u))
+        qw = O.maxcut_q(n, u, v, w)
+        P.set_qualities_maxcut(u, v, w)  # new records (pooled buffers recycled)
+        thw = rng.uniform(0, math.pi, 4)
+        P.evolve(thw)
+        _f_close(P.expectation(), O.expectation(O.evolve_x(n, qw, thw), qw))
+        P.set_qualities_maxcut(u, v)
+        for _ in range(3):  # back to the first key: must re-capture, not replay stale buffers
+            th = rng.uniform(0, math.pi, 4)
+            P.evolve(th)
+            ref = O.evolve_x(n, q, th)
+            _f_close(P.expectation(), O.expectation(ref, q))
+        _amp_close(P.get_state(), ref)
+
+
 def test_tile_path_p0_and_norm(Q):
     n = 14
     q = np.linspace(-1, 1, 1 << n)

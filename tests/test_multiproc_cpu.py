@@ -9,8 +9,11 @@ here with real processes (SURVEY §4 tier 3-4):
     g local bits are swapped (the layout the sharded schedule assumes), and a second exchange
     restores layout A;
   * the COMM-grad-f batch split: members split by qva_batch_partition,
-    evaluated per rank (here by the CPU oracle, at n = 8), zero-filled and sum-all-reduced,
-    equal the serial evaluation.
+    evaluated per rank (here by the CPU oracle, at n = 8, because this file runs without a
+    GPU), zero-filled and sum-all-reduced, equal the serial evaluation.
+The library's own world > 1 path (plan creation with world = 2/4, IPC peer stores, the
+barrier, its batch and <Q> all-reduces, the send/recv fallbacks) runs in
+tests/test_multiproc_gpu.py: real ranks as processes on one GPU over a gloo host transport.
 """
 import os
 import socket
