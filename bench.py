@@ -120,6 +120,40 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def total_bytes_step_gpu(plan, Q, steps):
+    """implemented bytes of every kernel class per step (this GPU)"""
+    return sum(plan.kernel_stats(c)["bytes"] for c in Q.KERNEL_CLASSES) / steps
+
+
+def host_info():
+    """nproc, CPU model and MemTotal of the box the oracle is timed on."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal"):
+                    info["mem_total_gib"] = round(int(line.split()[1]) / 1048576.0, 1)
+                    break
+    except Exception:
+        pass
+    return info
+
+
+# SURVEY 8(d) algorithmic floor of the X-mixer path: two HBM round trips (2 x 32 B) per
+# amplitude-layer, q generated inside the passes (NEXT-1) so no q bytes
+FLOOR_X_BYTES = 64.0
+# NVLink per direction per GPU: measured peer copy on this pool (B200_PROFILING.md); nominal 900
+NVL_GBS, NVL_NOMINAL_GBS = 770.0, 900.0
+
+
 def workload_for(args, world):
     if args.workload:
         name = args.workload
@@ -235,7 +269,8 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": desc},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info[0], "kind": "oracle", "sample": info[1]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info[0], "kind": "oracle", "sample": info[1],
+                         "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -254,6 +289,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--virtual-shards", type=int, default=1,
+                    help="run the sharded schedule with G virtual shards on one GPU (format check of the "
+                         "sharded roofline fields before a multi-GPU node exists)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -280,8 +318,11 @@ def main():
     nccl_id = Q.nccl_id_broadcast() if world > 1 else None
 
     batch = wl.batch_thetas if name == "cfg2" else None
+    vshards = max(1, args.virtual_shards) if world == 1 else 1
     plan = Q.Plan(wl.dim, wl.mixer, n_qubits=wl.n_qubits, rank=rank, world=world, nccl_id=nccl_id,
-                  device=local_rank, stream=stream.cuda_stream, max_batch=len(batch) if batch is not None else 1)
+                  device=local_rank, stream=stream.cuda_stream, max_batch=len(batch) if batch is not None else 1,
+                  virtual_shards=vshards, peer_store_exchange=vshards > 1)
+    G = world * vshards
     if wl.mixer == "x":
         plan.set_qualities_maxcut(wl.edges_u, wl.edges_v, wl.weights)
     else:
@@ -341,14 +382,56 @@ def main():
         kernel_share = st["ms"] / total_kernel_ms
     peak, peak_src = _peaks()
     roof = None
+    per_gpu = vshards if world == 1 else 1  # shards whose work one GPU does
     if st["launches"] > 0 and st["ms"] > 0:
-        per_launch_bytes = st["bytes"] / st["launches"]
+        impl_bytes = st["bytes"] / st["launches"]
         per_launch_s = st["ms"] * 1e-3 / st["launches"]
+        if cls == "tile" and local_n >= (1 << 24):
+            # algorithmic bytes per launch = the SURVEY 8(d) floor (64 B per amplitude-layer) x the
+            # amplitude-layers one launch processes (this GPU's amp-layers of the timed steps over its
+            # tile-pass launches)
+            amp_layers_per_launch = amp_layers / G * per_gpu * args.steps / st["launches"]
+            per_launch_bytes = FLOOR_X_BYTES * amp_layers_per_launch
+            basis = (f"SURVEY 8(d) floor {FLOOR_X_BYTES:.0f} B/amp-layer x {amp_layers_per_launch:.6g} amp-layers "
+                     "per launch")
+        else:
+            per_launch_bytes = impl_bytes
+            basis = ("bytes of the implemented schedule (state round trip + q/spectrum reads) per launch"
+                     + (" (the SURVEY 8(d) 64 B floor is stated for n >= 24; below it fewer passes per layer "
+                        "suffice)" if cls == "tile" else ""))
         achieved = per_launch_bytes / per_launch_s / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": _ncu_traffic(cls), "kernel": f"{cls} pass", "algorithmic_bytes_per_launch": per_launch_bytes,
+                "algorithmic_basis": basis, "implemented_bytes_per_launch": impl_bytes,
+                "frac_implemented": impl_bytes / per_launch_s / 1e9 / peak,
                 "mean_launch_ms": st["ms"] / st["launches"], "launches": st["launches"],
                 "share_of_kernel_time": kernel_share, "peak_source": peak_src}
+        if cls == "tile" and local_n >= (1 << 24):
+            # the whole step against the floor (every kernel and gap of the step included)
+            roof["frac_step_vs_floor"] = FLOOR_X_BYTES * amp_layers / G * per_gpu / (ms_step * 1e-3) / 1e9 / peak
+    # sharded runs: combined HBM / NVLink roofline per layer:
+    # T_roof = max(T_HBM, T_NVL), frac = T_roof / T_layer
+    sharded = None
+    if G > 1:
+        xfer = plan.query("xfer_bytes") / args.steps  # bytes one shard sends to the others, per step
+        layers = wl.p * B
+        t_nvl = xfer / (NVL_GBS * 1e9)
+        if wl.mixer == "x":
+            hbm_bytes = FLOOR_X_BYTES * float(wl.dim) * wl.p * B / G * per_gpu
+        else:
+            hbm_bytes = total_bytes_step_gpu(plan, Q, args.steps)
+        t_hbm = hbm_bytes / (peak * 1e9)
+        t_roof = max(t_hbm, t_nvl)
+        sharded = {"shards": G, "virtual": world == 1, "nvlink_bytes_per_gpu_step": xfer,
+                   "nvlink_bytes_per_gpu_layer": xfer / layers, "t_nvl_ms_per_layer": 1e3 * t_nvl / layers,
+                   "t_hbm_ms_per_layer": 1e3 * t_hbm / layers, "t_layer_ms": ms_step / layers,
+                   "bound": "nvlink" if t_nvl > t_hbm else "hbm", "frac": 1e3 * t_roof / ms_step,
+                   "nvlink_gbs": NVL_GBS, "nvlink_nominal_gbs": NVL_NOMINAL_GBS,
+                   "nvlink_source": "measured peer copy per direction per GPU (B200_PROFILING.md)",
+                   "hbm_basis": ("SURVEY 8(d) floor 64 B/amp-layer" if wl.mixer == "x" else
+                                 "implemented bytes of every kernel"),
+                   "note": ("virtual shards on one GPU: the NVLink bytes are the traffic each shard would send "
+                            "on a real node; t_hbm covers all shards of the one GPU") if world == 1 else None}
     # whole-step model bytes (all kernels' algorithmic bytes) / step time
     total_bytes = sum(plan.kernel_stats(c)["bytes"] for c in Q.KERNEL_CLASSES)
     achieved_step_gbs = total_bytes / args.steps / (ms_step * 1e-3) / 1e9 / max(1, 1)
@@ -416,10 +499,18 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt, cores, sdesc = oracle_sample(name, wl, budget_s=20.0)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sdesc, "seconds": dt}
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sdesc, "seconds": dt,
+               "host": host_info()}
         if ONE_THREAD:
             cpu["single_thread"] = dict(ONE_THREAD, unit=UNIT)
 
+    # working set of the timed step vs this device's L2 (cudaDevAttrL2CacheSize)
+    l2_bytes = torch.cuda.get_device_properties(local_rank).L2_cache_size
+    ws = local_n * B * 16
+    l2_label = (f"inputs larger than L2: {ws / 2**30:.2f} GiB of state per GPU vs {l2_bytes / 2**20:.0f} MiB L2, no flush"
+                if ws > 2 * l2_bytes else
+                f"working set {ws / 2**20:.0f} MiB of state vs {l2_bytes / 2**20:.0f} MiB L2: L2-resident or near it, "
+                "no flush (the workload's own size)")
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -427,12 +518,13 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "dim": wl.dim, "p": wl.p, "batch": B,
                        "amplitudes_per_gpu": local_n,
-                       "l2": "inputs larger than L2: 16 GiB state per GPU, no flush" if local_n >= (1 << 26)
-                       else "state fits in L2 (126 MB); no flush (L2-resident workload)",
-                       "parallelism": f"state sharded over {world} GPUs" if world > 1 else "1 GPU"},
+                       "l2": l2_label,
+                       "parallelism": (f"state sharded over {world} GPUs" if world > 1 else
+                                       (f"1 GPU, {vshards} virtual shards" if vshards > 1 else "1 GPU"))},
             "achieved_hbm_gbs_step": achieved_step_gbs,
             "objective": f if batch is None else float(np.asarray(f)[0]),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roof, "sharded_roofline": sharded, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

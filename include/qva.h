@@ -291,7 +291,10 @@ qva_status qva_launch_count(qva_plan *plan, int64_t *launches);
 /* Plan introspection (host only, no device work): what = 0: 1 if the global<->local exchange and
  * the circulant transposes run fused into the pass stores over IPC-mapped peer memory (world > 1)
  * or over virtual-shard peers, else 0; 1: shard count G (world x virtual shards); 2: 1 if the plan's
- * collectives run over a host transport (qva_plan_create_ex), else 0; 3: world; 4: rank.
+ * collectives run over a host transport (qva_plan_create_ex), else 0; 3: world; 4: rank; 5: state
+ * bytes one shard has sent to the other shards (global<->local exchanges, circulant transposes:
+ * (G-1)/G of a shard's slice each) since the last qva_reset_kernel_stats -- the NVLink traffic of
+ * a real shard, the notional one of a virtual shard.
  * QVA_ERR_INVALID_ARGUMENT for another `what`. */
 qva_status qva_plan_query(const qva_plan *plan, int32_t what, int64_t *out);
 

@@ -475,8 +475,8 @@ class Plan:
         _call("qva_reset_kernel_stats", self._h)
 
     def query(self, what) -> int:
-        """qva_plan_query: 'fused_exchange', 'shards', 'host_transport', 'world', 'rank' (or 0..4)."""
-        keys = {"fused_exchange": 0, "shards": 1, "host_transport": 2, "world": 3, "rank": 4}
+        """qva_plan_query: 'fused_exchange', 'shards', 'host_transport', 'world', 'rank', 'xfer_bytes' (0..5)."""
+        keys = {"fused_exchange": 0, "shards": 1, "host_transport": 2, "world": 3, "rank": 4, "xfer_bytes": 5}
         out = ctypes.c_int64()
         _call("qva_plan_query", self._h, keys.get(what, what), ctypes.byref(out))
         return out.value

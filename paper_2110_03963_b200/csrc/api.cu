@@ -564,6 +564,8 @@ struct qva_plan {
     bool host_tp = false;
     qva_transport tp = {};
     bool created = false;                 // qva_plan_create completed (collective teardown allowed)
+    double xfer_bytes = 0.0;              // state bytes one shard sent to the other shards since the
+                                          // last stats reset (NVLink traffic of a real shard)
     // profiling
     bool prof = false;
     KernelStat stats[8];
@@ -801,10 +803,19 @@ qva_status coll_alltoall_dev(qva_plan *P, const void *src, void *dst, size_t chu
 // ---- exchange (global <-> local qubit swap; COMM-psi) ----------------------
 // Every shard r sends chunk t (local index top-g bits = t) to shard t, which stores it as its
 // chunk r: a block transpose of the G x G chunk matrix.  The layout flips between A and B.
+// cross-shard traffic of one all-to-all of `elem_bytes`-byte elements over the whole (local) array:
+// each shard keeps 1/G of its slice and sends the rest, (G-1)/G x slice bytes
+void count_xfer(qva_plan *P, double elem_bytes) {
+    if (P->G <= 1) return;
+    const double slice = (double)P->arr_n / (P->world == 1 ? P->G : 1) * elem_bytes;
+    P->xfer_bytes += slice * (P->G - 1) / P->G;
+}
+
 template <typename T>
 qva_status exchange_buffers(qva_plan *P, T *src, T *dst) {
     uint64_t per_shard = 1ull << P->L;
     uint64_t C = per_shard / P->G;
+    count_xfer(P, sizeof(T));
     if (P->world == 1) {
         ProfScope ps(P, K_EXCHANGE, 2.0 * sizeof(T) * (double)P->arr_n);
         QVA_CUDA_TRY(launch_chunk_transpose<T>(dst, src, P->G, C, P->stream));
@@ -1735,6 +1746,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         if (!xbit.empty() || xpeer) {
             P->layout ^= 1;  // what exchange_state would have done
             exchanged = true;
+            count_xfer(P, sizeof(double2) * batch);
         }
         if (pp.expect) {
             ProfScope ps(P, K_REDUCE, 16.0 * nslot * batch);
@@ -1975,9 +1987,16 @@ qva_status shard_to_row(qva_plan *P, const T *col, T *row) {
 struct PlanShardIO : FftShardIO {
     qva_plan *P;
     explicit PlanShardIO(qva_plan *P_) : P(P_) {}
-    qva_status to_col(const double2 *row, double2 *col) override { return shard_to_col<double2>(P, row, col); }
-    qva_status to_row(const double2 *col, double2 *row) override { return shard_to_row<double2>(P, col, row); }
-    qva_status barrier() override {
+    qva_status to_col(const double2 *row, double2 *col) override {
+        count_xfer(P, sizeof(double2));
+        return shard_to_col<double2>(P, row, col);
+    }
+    qva_status to_row(const double2 *col, double2 *row) override {
+        count_xfer(P, sizeof(double2));
+        return shard_to_row<double2>(P, col, row);
+    }
+    qva_status barrier() override {  // ends a transpose fused into the pass stores
+        count_xfer(P, sizeof(double2));
         if (P->world == 1) return QVA_OK;  // virtual shards: stream order
         return coll_stream_barrier(P);
     }
@@ -3473,6 +3492,7 @@ qva_status qva_reset_kernel_stats(qva_plan *P) {
     QVA_TRY(sync(P));
     for (auto &s : P->stats) s = KernelStat();
     P->launches = 0;
+    P->xfer_bytes = 0.0;
     return QVA_OK;
 }
 
@@ -3493,6 +3513,7 @@ qva_status qva_plan_query(const qva_plan *P, int32_t what, int64_t *out) {
         case 2: *out = P->host_tp ? 1 : 0; return QVA_OK;
         case 3: *out = P->world; return QVA_OK;
         case 4: *out = P->rank; return QVA_OK;
+        case 5: *out = (int64_t)P->xfer_bytes; return QVA_OK;
         default: set_error("qva_plan_query: unknown query"); return QVA_ERR_INVALID_ARGUMENT;
     }
 }
