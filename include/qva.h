@@ -88,7 +88,13 @@ typedef struct {
                                 the exchanges through the peer-store paths of real shards (X
                                 mixer: global<->local exchange; circulant: row/column transposes
                                 fused into the FFT pass stores), each virtual shard's buffer as
-                                its "peer"; tests the code multi-GPU plans use.  Others must be 0. */
+                                its "peer"; tests the code multi-GPU plans use.  reserved[4]: 1 =
+                                circulant mixer with a spectrum set by
+                                qva_set_circulant_eigenvalues_const (lambda_0, c, ..., c): apply it
+                                in closed form, U psi = e^{-i beta c} psi + (e^{-i beta lambda_0} -
+                                e^{-i beta c}) mean(psi) (one 40-B pass per layer, single shard;
+                                an O(N) speed-of-light reference for the FFT path; the
+                                FFT stays the default).  Others must be 0. */
 } qva_plan_desc;
 
 /* ---- lifecycle (Table 1 plan / destroy) ------------------------------------ */

@@ -286,7 +286,8 @@ class Plan:
                  nccl_id: Optional[bytes] = None, device: int = 0, virtual_shards: int = 1,
                  stream: Optional[int] = None, max_batch: int = 1, replicated: bool = False,
                  qgen_f64_always: bool = False, fft_three_level: bool = False,
-                 peer_store_exchange: bool = False, transport: Optional[TorchHostTransport] = None):
+                 peer_store_exchange: bool = False, transport: Optional[TorchHostTransport] = None,
+                 complete_closed_form: bool = False):
         """transport: a TorchHostTransport (world > 1) to run the plan's collectives over a torch
         host process group instead of NCCL (include/qva.h qva_plan_create_ex)."""
         self._h = ctypes.c_void_p()
@@ -307,6 +308,7 @@ class Plan:
         d.reserved[1] = 1 if qgen_f64_always else 0
         d.reserved[2] = 1 if fft_three_level else 0
         d.reserved[3] = 1 if peer_store_exchange else 0
+        d.reserved[4] = 1 if complete_closed_form else 0
         if transport is not None:
             _call("qva_plan_create_ex", ctypes.byref(d), ctypes.byref(transport.struct), ctypes.byref(self._h))
         else:

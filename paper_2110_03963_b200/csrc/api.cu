@@ -1939,6 +1939,12 @@ qva_status expect_generic(qva_plan *P, const double2 *psi, uint64_t n, const dou
     return sync(P);
 }
 
+// opt-in closed form of the complete-graph-family circulant (desc.reserved[4], kernels_complete.cu):
+// single shard, spectrum given as (lambda_0, c) by qva_set_circulant_eigenvalues_const
+bool use_complete_closed_form(const qva_plan *P) {
+    return P->mixer == QVA_MIXER_CIRCULANT && P->d.reserved[4] != 0 && P->lam_const && P->G == 1;
+}
+
 bool use_small(const qva_plan *P) { return P->mixer == QVA_MIXER_X && P->n <= kSmallMaxQubits && P->G == 1; }
 
 // permuted out-of-place schedule: single shard, >= 21 qubits
@@ -2201,6 +2207,11 @@ qva_status apply_mixer_impl(qva_plan *P, double beta) {
         r.theta = &beta;
         r.mode = 1;
         PlanObserver obs(P);
+        if (use_complete_closed_form(P)) {
+            double *scr = nullptr;
+            QVA_CUDA_TRY(scratch_get(P, (void **)&scr, complete_scratch_doubles(P->N) * sizeof(double)));
+            return complete_run(r, P->N, scr, P->stream, &obs);
+        }
         if (P->G > 1) {
             PlanShardIO io(P);
             QVA_TRY(circ_shard_setup(P, io));
@@ -3100,7 +3111,11 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
         r.expect = p > 0;
         r.red_out = P->red;
         PlanObserver obs(P);
-        if (P->G > 1) {
+        if (use_complete_closed_form(P)) {
+            double *scr = nullptr;
+            QVA_CUDA_TRY(scratch_get(P, (void **)&scr, complete_scratch_doubles(P->N) * sizeof(double)));
+            QVA_TRY(complete_run(r, P->N, scr, P->stream, &obs));
+        } else if (P->G > 1) {
             PlanShardIO io(P);
             QVA_TRY(circ_shard_setup(P, io));
             QVA_TRY(fft_run_sharded(P->fft, r, io, P->stream, &obs));

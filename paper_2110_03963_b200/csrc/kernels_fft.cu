@@ -135,6 +135,25 @@ __device__ __forceinline__ double2 mul_mi(double2 a, bool inv) {
     return inv ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
 }
 
+// 16-byte global -> shared copies that bypass the registers (LDGSTS): a thread issues all of its
+// block's copies back to back, so a whole column / row block is in flight at once and the
+// twiddle-table set-up below overlaps it (the register-staged loads kept at most kLoadU per
+// thread in flight and waited a memory latency per batch)
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ bool fft_async_loads() {
+#ifdef QVA_FFT_SYNC_LOADS
+    return false;
+#else
+    return true;
+#endif
+}
+
 // cos / sin (2 pi j / N) for the two-level radix-16 and radix-9 butterflies (compile-time
 // constants: indices are unrolled, so they fold into immediates)
 __host__ __device__ constexpr double tw_cos(int N, int j) {
@@ -701,6 +720,15 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
     // w_M^{C k1} = Tw[c*E + (k1 >> 5)] * Tw[c*E + nh + (k1 & 31)] (C = global column); outer
     // (three-level inverse) w_N^{-xl K} = Tw[x1 >> 5] * Tw[nh + (x1 & 31)] * Tw[E + c]
     // (xl = x1*M2 + c0 + c, K = matrix)
+    if (!a.init && fft_async_loads()) {  // the whole column block in flight before the table set-up
+        for (int idx = threadIdx.x; idx < totw; idx += blockDim.x) {
+            const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
+            if (c >= cwv) continue;
+            const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
+            if (x < a.in_len) cp_async16(ad.ptr(c, x1), a.in + mat + x);
+            else *ad.ptr(c, x1) = make_double2(0.0, 0.0);
+        }
+    }
     double2 *Tw = A + (size_t)a.cw * (M1 + (a.cw > 1 ? 1 : 0));
     const int nh = (M1 + 31) >> 5, E = tw_split_entries(M1);
     if (a.do_fwd) {
@@ -721,27 +749,31 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         }
     }
     const double2 *twp = stage_twiddles(a.tw, a.sf, a.tws, A + a.ts_off);
-    // the column block arrives in batches of kLoadU independent loads per thread (one load per
-    // iteration would wait a full memory latency for each element before its smem store)
-    for (int base = threadIdx.x; base < totw; base += kLoadU * blockDim.x) {
-        double2 v[kLoadU];
+    if (a.init || !fft_async_loads()) {
+        // the column block arrives in batches of kLoadU independent loads per thread (one load
+        // per iteration would wait a full memory latency for each element before its smem store)
+        for (int base = threadIdx.x; base < totw; base += kLoadU * blockDim.x) {
+            double2 v[kLoadU];
 #pragma unroll
-        for (int u = 0; u < kLoadU; ++u) {
-            const int idx = base + u * blockDim.x;
-            const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
-            const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
-            v[u] = make_double2(0.0, 0.0);
-            if (idx < totw && c < cwv) {
-                if (a.init) v[u] = make_double2(x < a.N ? a.amp0 : 0.0, 0.0);
-                else if (x < a.in_len) v[u] = a.in[mat + x];
+            for (int u = 0; u < kLoadU; ++u) {
+                const int idx = base + u * blockDim.x;
+                const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
+                const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
+                v[u] = make_double2(0.0, 0.0);
+                if (idx < totw && c < cwv) {
+                    if (a.init) v[u] = make_double2(x < a.N ? a.amp0 : 0.0, 0.0);
+                    else if (x < a.in_len) v[u] = a.in[mat + x];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kLoadU; ++u) {
+                const int idx = base + u * blockDim.x;
+                const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
+                if (idx < totw && c < cwv) *ad.ptr(c, x1) = v[u];
             }
         }
-#pragma unroll
-        for (int u = 0; u < kLoadU; ++u) {
-            const int idx = base + u * blockDim.x;
-            const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
-            if (idx < totw && c < cwv) *ad.ptr(c, x1) = v[u];
-        }
+    } else {
+        cp_async_wait_all();
     }
     __syncthreads();
     col_block<F>(ad, a, c0, cwv, blockIdx.y, blockIdx.x, red, Tw, twp);
@@ -804,8 +836,14 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_row_kernel(const Row
             ++r;
         }
     };
+    if (fft_async_loads()) {  // the whole row block in flight before the stage-table copy
+        int r = r0, x = x0;
+        for (int i = threadIdx.x; i < tot; i += blockDim.x, adv(r, x)) cp_async16(ad.ptr(r, x), rows + i);
+    }
     const double2 *twp = stage_twiddles(a.tw, a.sf, a.tws, A + a.ts_off);
-    {
+    if (fft_async_loads()) {
+        cp_async_wait_all();
+    } else {
         int r = r0, x = x0;
         for (int base = threadIdx.x; base < tot; base += kLoadU * blockDim.x) {
             double2 v[kLoadU];

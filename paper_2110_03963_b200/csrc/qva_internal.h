@@ -325,6 +325,10 @@ struct FftRun {
     double *red_out = nullptr;         // device [2] receives the reduced pair when expect
 };
 qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver *obs);
+// complete-graph-family spectrum (lambda_0, c, ..., c) in closed form (kernels_complete.cu; opt-in
+// ablation, desc.reserved[4]): p + 1 passes of 40 B per amplitude; scratch: complete_scratch_doubles(n)
+size_t complete_scratch_doubles(uint64_t n);
+qva_status complete_run(const FftRun &r, uint64_t n, double *scratch, cudaStream_t s, LaunchObserver *obs);
 // sharded four-step: r.psi is this process's row block(s) in natural order (local * N/G)
 struct FftShardIO {
     int G = 1, local = 1, first = 0;  // shards, shards held by this process, global index of local 0

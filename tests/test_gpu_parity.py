@@ -624,6 +624,31 @@ def test_virtual_shards_vs_oracle(Q, n, G, p, peer):
         _amp_close(P.get_state(), r2)
 
 
+# ---------------------------------------------------------------- K_N closed form ----
+@pytest.mark.parametrize("N,lam0,c", [(720, 0.0, 720.0), (3628800, 0.0, 3628800.0), (1000, 1.5, -0.7)])
+def test_complete_closed_form_vs_oracle(Q, N, lam0, c):
+    """The opt-in closed form of the complete-graph-family circulant (desc.reserved[4]): p-layer
+    evolution, a single step-level mixer and a non-uniform initial state against the oracle's
+    closed form (pinned by P10 / P19 against expm / the dense matrix c I + (lam0 - c) J / N)."""
+    rng = np.random.default_rng(N)
+    q = rng.standard_normal(N)
+    th = rng.uniform(0, math.pi, 8)
+    ref = O.evolve_complete(q, th, lam0, c)
+    with Q.Plan(N, "circulant", complete_closed_form=True) as P:
+        P.set_qualities(q)
+        P.set_circulant_eigenvalues_const(lam0, c)
+        P.evolve(th)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+        P.apply_mixer(0.8)
+        _amp_close(P.get_state(), O.mixer_complete(ref.copy(), 0.8, lam0, c))
+        psi0 = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+        psi0 /= np.linalg.norm(psi0)
+        P.set_initial_state(psi0)
+        P.evolve(th[:4])
+        _amp_close(P.get_state(), O.evolve_complete(q, th[:4], lam0, c, psi0=psi0))
+
+
 # ---------------------------------------------------------------- sparse (Taylor) ----
 def _csr(W):
     rows, cols = np.nonzero(W)
