@@ -300,7 +300,8 @@ qva_status qva_launch_count(qva_plan *plan, int64_t *launches);
  * collectives run over a host transport (qva_plan_create_ex), else 0; 3: world; 4: rank; 5: state
  * bytes one shard has sent to the other shards (global<->local exchanges, circulant transposes:
  * (G-1)/G of a shard's slice each) since the last qva_reset_kernel_stats -- the NVLink traffic of
- * a real shard, the notional one of a virtual shard.
+ * a real shard, the notional one of a virtual shard; 6: 1 if the last QAOAz (parity) evolution ran
+ * as TMA tile passes with the pair terms on register groups, 0 if it took the window kernel.
  * QVA_ERR_INVALID_ARGUMENT for another `what`. */
 qva_status qva_plan_query(const qva_plan *plan, int32_t what, int64_t *out);
 

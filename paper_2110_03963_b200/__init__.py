@@ -478,7 +478,8 @@ class Plan:
 
     def query(self, what) -> int:
         """qva_plan_query: 'fused_exchange', 'shards', 'host_transport', 'world', 'rank', 'xfer_bytes' (0..5)."""
-        keys = {"fused_exchange": 0, "shards": 1, "host_transport": 2, "world": 3, "rank": 4, "xfer_bytes": 5}
+        keys = {"fused_exchange": 0, "shards": 1, "host_transport": 2, "world": 3, "rank": 4, "xfer_bytes": 5,
+                "parity_tile": 6}
         out = ctypes.c_int64()
         _call("qva_plan_query", self._h, keys.get(what, what), ctypes.byref(out))
         return out.value

@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <cmath>
 #include <cstdio>
@@ -57,6 +58,11 @@ struct PassPlan {
     // (input physical bit -> output physical bit)
     bool permuted = false;
     std::vector<int> tbits, lay_in, obit;
+    // QAOAz parity window pass (parity_tile_passes): in place over tile bits `tbits`, the step list
+    // (register groups + pair terms) planned on the host, pair angle of layer `play`
+    bool parity = false;
+    int play = -1;
+    std::vector<PassStep> psteps;
 };
 
 static std::vector<std::vector<int>> make_tile_sets(int L) {
@@ -309,6 +315,8 @@ static const TileGroup kGroups[kMaxGroups] = {
     {{3, 4, 5, 6, 7}, {0, 1, 2, 8, 9, 10, 11}},   // X
     {{8, 9, 10, 11, 3}, {0, 1, 2, 4, 5, 6, 7}},   // Y
     {{0, 1, 2, 6, 7}, {3, 4, 5, 8, 9, 10, 11}},   // W
+    {{6, 7, 8, 9, 10}, {0, 1, 2, 3, 4, 5, 11}},   // V (parity pair terms; kernels_tile.cu dev_ebit)
+    {{1, 2, 3, 10, 11}, {0, 4, 5, 6, 7, 8, 9}},   // Z
 };
 static int group_of_bit(int b) { return b >= 8 ? 1 : (b >= 3 ? 0 : 2); }
 static int ebit_index(int g, int b) {
@@ -341,7 +349,7 @@ static void build_steps(const PassPlan &pp, TilePassParams &tp, int pref_gq, boo
         std::vector<int> o2 = G2;
         std::sort(o2.begin(), o2.end());
         do {
-            for (int gp_choice = 0; gp_choice < kMaxGroups; ++gp_choice) {
+            for (int gp_choice = 0; gp_choice < 3; ++gp_choice) {  // X-mixer passes use groups X, Y, W
                 std::vector<PassStep> st;
                 for (int g : o1) {
                     st.push_back({(int8_t)g, (int8_t)m1[g], 0, 0});
@@ -386,12 +394,33 @@ static void build_steps(const PassPlan &pp, TilePassParams &tp, int pref_gq, boo
     for (int j = 0; j < kCT_BITS; ++j) tp.st_tphys[j] = tp.tile_bits[gf.tbit[j]];
 }
 
+// Step list of a parity window pass: the host-planned steps; q is consumed in the group of the
+// phase step (first step) or, for the expectation, the last step (build_parity_plan makes them one)
+static void build_parity_steps(const PassPlan &pp, TilePassParams &tp) {
+    tp.n_groups = kMaxGroups;
+    for (int g = 0; g < kMaxGroups; ++g) tp.groups[g] = kGroups[g];
+    tp.n_steps = (int)pp.psteps.size();
+    for (int i = 0; i < tp.n_steps; ++i) tp.steps[i] = pp.psteps[i];
+    tp.gq = -1;
+    for (int i = 0; i < tp.n_steps; ++i)
+        if (tp.steps[i].phase) tp.gq = tp.steps[i].group;
+    if (pp.expect) tp.gq = tp.steps[tp.n_steps - 1].group;
+    const TileGroup &gf = kGroups[tp.steps[tp.n_steps - 1].group];
+    for (int j = 0; j < kGroupBits; ++j) tp.st_estr[j] = 1ull << tp.tile_bits[gf.ebit[j]];
+    for (int j = 0; j < kCT_BITS; ++j) tp.st_tphys[j] = tp.tile_bits[gf.tbit[j]];
+}
+
 // the compile-time program (kTileProgs) whose shape equals this pass, or 0 (generic)
 static int match_prog(const TilePassParams &tp) {
     for (int q = 1; q < kNumTileProgs; ++q) {
         const TileProg &D = kTileProgs[q];
         if (D.n != tp.n_steps || D.expect != (tp.expect != 0)) continue;
-        if ((q == 5 || q == 6) != (tp.init == 1)) continue;  // programs 5, 6 start from |+> without a load
+        // programs 5, 6 start from |+> without a load; the QAOAz programs take either
+        if (q < kFirstParityProg && (q == 5 || q == 6) != (tp.init == 1)) continue;
+        // only the QAOAz programs apply pair terms, and they take no rotations
+        bool pairs = false;
+        for (int k = 0; k < tp.n_steps; ++k) pairs |= tp.steps[k].npair != 0;
+        if (pairs != (q >= kFirstParityProg)) continue;
         bool ok = true;
         for (int k = 0; k < D.n && ok; ++k) {
             const PassStep &st = tp.steps[k];
@@ -555,6 +584,9 @@ struct qva_plan {
     std::vector<int> parity_seq;
     std::vector<ParityWindow> parity_win;  // window passes of the current sequence (built lazily)
     std::vector<int> parity_win_seq;       // the sequence they were built for
+    std::map<int, std::vector<PassPlan>> parity_tile_sched;  // tile-pass schedule per p (parity_tile_passes)
+    std::vector<int> parity_tile_seq;      // the sequence it was built for
+    bool parity_tile_ran = false;          // the last parity evolution ran as tile passes
     // sparse
     SparseMixer sm;
     bool sparse_set = false;
@@ -868,7 +900,7 @@ qva_status classify_q(qva_plan *P) {
     drop_qt(P);
     P->q_mode = 0;
     P->qcB_valid = false;
-    if (P->mixer != QVA_MIXER_X || P->L < kTileBits) return QVA_OK;
+    if ((P->mixer != QVA_MIXER_X && P->mixer != QVA_MIXER_PARITY) || P->L < kTileBits) return QVA_OK;
     QVA_TRY(ensure_q_dev(P));
     int blocks = q_range_blocks(P->arr_n);
     double *mm = nullptr;
@@ -1140,7 +1172,7 @@ bool use_qgen(const qva_plan *P) {
         const char *e = getenv("QVA_QGEN");
         return e ? atoi(e) : 1;
     }();
-    return env != 0 && P->q_graph && P->mixer == QVA_MIXER_X;
+    return env != 0 && P->q_graph && (P->mixer == QVA_MIXER_X || P->mixer == QVA_MIXER_PARITY);
 }
 
 // q path of a tile-pass sequence: generated integer / fp64 records, or 0 (stored q)
@@ -1413,6 +1445,10 @@ static void pass_host_data(const std::vector<PassPlan> &passes, const double *th
                 };
                 if (pp.a1 >= 0) factor(pp.a1, n1, half1[j], a.t1);
                 if (pp.a2 >= 0) factor(pp.a2, n2, half2[j], a.t2);
+                if (pp.parity && pp.play >= 0) {  // Givens pair terms: cos 2t, sin 2t (R19)
+                    a.t1 = cos(2.0 * th[2 * pp.play + 1]);
+                    a.t2 = sin(2.0 * th[2 * pp.play + 1]);
+                }
                 a.scale = make_double2(sr, si);
                 if (pp.phase >= 0) {
                     a.gamma = th[2 * pp.phase];
@@ -1588,7 +1624,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         }
         TilePassParams tp;
         memset(&tp, 0, sizeof(tp));
-        const std::vector<int> &s = pp.permuted ? pp.tbits : P->sets[pp.set];
+        const std::vector<int> &s = (pp.permuted || pp.parity) ? pp.tbits : P->sets[pp.set];
         uint64_t tmask = 0;
         for (int k = 0; k < kTileBits; ++k) {
             tp.tile_bits[k] = s[k];
@@ -1634,7 +1670,8 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         if (needs_q)
             for (auto &e : P->qt_cache)
                 if (e.key == qkey && e.qbytes == qbytes) pref = e.group;
-        build_steps(pp, tp, pref, half1[j], half2[j]);
+        if (pp.parity) build_parity_steps(pp, tp);
+        else build_steps(pp, tp, pref, half1[j], half2[j]);
         if (needs_q && gen) {
             const qva_plan::GenEntry *ge = nullptr;
             if (P->ex_w && pp.phase >= 0 && pp.expect) {
@@ -2046,7 +2083,11 @@ qva_status circ_shard_setup(qva_plan *P, PlanShardIO &io) {
 // 128-B rows) each take, greedily in group order, every term whose qubits fit and whose
 // predecessors are done or earlier in the same window: one HBM round trip per window instead of
 // one per term (default sequence, n = 28: 5 windows for 27 terms).
-static std::vector<ParityWindow> parity_windows(int n, const std::vector<int> &s) {
+struct ParityWinPlan {
+    std::vector<int> bits;            // window bits (ascending, physical = logical here)
+    std::vector<int> ta, tb, cls;     // its pair terms in application order; cls 0 odd, 1 even, 2 last
+};
+static std::vector<ParityWinPlan> parity_window_plan(int n, const std::vector<int> &s) {
     const int K = (int)s.size();
     std::vector<std::pair<int, int>> terms;
     std::vector<int> grp;
@@ -2061,7 +2102,7 @@ static std::vector<ParityWindow> parity_windows(int n, const std::vector<int> &s
                                     terms[j].second == terms[k].first || terms[j].second == terms[k].second))
                 deps[k].push_back(j);
     std::vector<char> done(T, 0);
-    std::vector<ParityWindow> out;
+    std::vector<ParityWinPlan> out;
     const int wmax = std::min(n, kWinMaxBits);
     for (int left = T; left > 0;) {
         std::vector<char> inw(n, 0), placed(T, 0);
@@ -2083,13 +2124,33 @@ static std::vector<ParityWindow> parity_windows(int n, const std::vector<int> &s
         // pad the window to wmax bits with the lowest free bits (longer rows, fewer tiles)
         for (int b = 0; b < n && w < wmax; ++b)
             if (!inw[b]) inw[b] = 1, ++w;
+        ParityWinPlan W;
+        for (int b = 0; b < n; ++b)
+            if (inw[b]) W.bits.push_back(b);
+        for (int k : plan) {
+            W.ta.push_back(terms[k].first);
+            W.tb.push_back(terms[k].second);
+            W.cls.push_back(grp[k]);
+            done[k] = 1;
+        }
+        left -= (int)plan.size();
+        out.push_back(W);
+    }
+    return out;
+}
+
+// Windows of <= 12 physical bits for the register-free parity_window_kernel.
+static std::vector<ParityWindow> parity_windows(int n, const std::vector<int> &s) {
+    std::vector<ParityWindow> out;
+    for (const ParityWinPlan &P : parity_window_plan(n, s)) {
+        std::vector<char> inw(n, 0);
+        for (int b : P.bits) inw[b] = 1;
         ParityWindow W;
         memset(&W, 0, sizeof(W));
         W.n = n;
-        W.w = w;
-        std::vector<int> bits, local(n, -1);
-        for (int b = 0; b < n; ++b)
-            if (inw[b]) local[b] = (int)bits.size(), bits.push_back(b);
+        W.w = (int)P.bits.size();
+        std::vector<int> local(n, -1);
+        for (int i = 0; i < (int)P.bits.size(); ++i) local[P.bits[i]] = i;
         auto runs = [&](bool in_window, int *src, int *wd, int *dst, int cap, int &nr) {
             nr = 0;
             int idx = 0;  // running index in the window (or the tile number)
@@ -2109,16 +2170,130 @@ static std::vector<ParityWindow> parity_windows(int n, const std::vector<int> &s
         if (!runs(true, W.in_src, W.in_w, W.in_dst, kWinMaxRuns, W.n_in) ||
             !runs(false, W.out_src, W.out_w, W.out_dst, kWinMaxRuns + 1, W.n_out))
             return {};  // too fragmented for the run tables: the caller takes the per-term passes
-        W.np = (int)plan.size();
+        W.np = (int)P.ta.size();
         for (int i = 0; i < W.np; ++i) {
-            W.pa[i] = (int8_t)local[terms[plan[i]].first];
-            W.pb[i] = (int8_t)local[terms[plan[i]].second];
-            done[plan[i]] = 1;
+            W.pa[i] = (int8_t)local[P.ta[i]];
+            W.pb[i] = (int8_t)local[P.tb[i]];
         }
-        left -= W.np;
         out.push_back(W);
     }
     return out;
+}
+
+// The window's pair terms as register-group steps of a tile pass (window bit i = tile bit i): at
+// each step the group (X, Y, W, V, Z) that can apply the most remaining terms -- both qubits among
+// its register bits, every earlier-class term of the window sharing a qubit already applied --
+// takes them in window order (ties: stay in the current group, i.e. no smem transpose).
+// false if some term fits no group (the caller keeps the register-free window kernel).
+static bool parity_group_steps(const ParityWinPlan &W, std::vector<PassStep> &steps) {
+    const int T = (int)W.ta.size();
+    if (T > 64) return false;
+    std::vector<int> tbit(64, -1);
+    for (int i = 0; i < (int)W.bits.size(); ++i) tbit[W.bits[i]] = i;
+    std::vector<uint64_t> dep(T, 0);  // earlier-class terms of the window sharing a qubit
+    for (int k = 0; k < T; ++k)
+        for (int j = 0; j < T; ++j)
+            if (W.cls[j] < W.cls[k] && (W.ta[j] == W.ta[k] || W.ta[j] == W.tb[k] || W.tb[j] == W.ta[k] ||
+                                        W.tb[j] == W.tb[k]))
+                dep[k] |= 1ull << j;
+    uint64_t fits[kMaxGroups] = {};  // terms whose two qubits are register bits of group g
+    for (int g = 0; g < kMaxGroups; ++g)
+        for (int k = 0; k < T; ++k)
+            if (ebit_index(g, tbit[W.ta[k]]) >= 0 && ebit_index(g, tbit[W.tb[k]]) >= 0) fits[g] |= 1ull << k;
+    const uint64_t all = T == 64 ? ~0ull : (1ull << T) - 1;
+    // a step in group g takes every applicable term in window order (taking a term never delays
+    // another), so a plan is a group sequence; iterative deepening finds the fewest steps
+    auto step = [&](uint64_t done, int g) {
+        for (int k = 0; k < T; ++k)
+            if (!((done >> k) & 1) && ((fits[g] >> k) & 1) && (dep[k] & ~done) == 0) done |= 1ull << k;
+        return done;
+    };
+    std::vector<int> seq;
+    std::function<bool(uint64_t, int)> dfs = [&](uint64_t done, int depth) -> bool {
+        if (done == all) return true;
+        if (depth == 0) return false;
+        for (int g = 0; g < kMaxGroups; ++g) {
+            if (!seq.empty() && seq.back() == g) continue;
+            const uint64_t nd = step(done, g);
+            if (nd == done) continue;
+            seq.push_back(g);
+            if (dfs(nd, depth - 1)) return true;
+            seq.pop_back();
+        }
+        return false;
+    };
+    bool found = false;
+    for (int depth = 1; depth <= 8 && !found; ++depth) {
+        seq.clear();
+        found = dfs(0, depth);
+    }
+    if (!found) return false;
+    uint64_t done = 0;
+    for (int g : seq) {
+        const uint64_t nd = step(done, g);
+        std::vector<int> take;
+        for (int k = 0; k < T; ++k)
+            if (((nd & ~done) >> k) & 1) take.push_back(k);
+        // within the step, a term follows the terms it depends on (window order already does)
+        for (size_t i = 0; i < take.size(); i += kMaxStepPairs) {
+            PassStep st;
+            memset(&st, 0, sizeof(st));
+            st.group = (int8_t)g;
+            for (size_t k = i; k < take.size() && k < i + kMaxStepPairs; ++k) {
+                int ja = ebit_index(g, tbit[W.ta[take[k]]]), jb = ebit_index(g, tbit[W.tb[take[k]]]);
+                if (ja > jb) std::swap(ja, jb);
+                st.pair[st.npair++] = (int8_t)(ja * 8 + jb);
+            }
+            steps.push_back(st);
+        }
+        done = nd;
+    }
+    return true;
+}
+
+// QAOAz evolution as tile passes (one HBM round trip per window, pair terms on register groups,
+// phase fused into the first window of each layer, <Q> into the last): single shard, n >= 12,
+// every window plannable.  Returns false when the sequence needs the register-free path.
+static bool parity_tile_passes(int n, int L, int G, const std::vector<int> &s, int p, std::vector<PassPlan> &out) {
+    out.clear();
+    if (G != 1 || L < kTileBits || n != L || p < 1) return false;
+    const std::vector<ParityWinPlan> wins = parity_window_plan(n, s);
+    if (wins.empty()) return false;
+    std::vector<std::vector<PassStep>> wsteps(wins.size());
+    for (size_t w = 0; w < wins.size(); ++w) {
+        if ((int)wins[w].bits.size() != kTileBits) return false;
+        if (!parity_group_steps(wins[w], wsteps[w]) || wsteps[w].empty()) return false;
+        if (tile_tma_dims(wins[w].bits.data(), n, nullptr) > 5) return false;
+        int runs = 0;  // non-tile runs (TilePassParams::run_*)
+        for (int b = 0; b < n;) {
+            if (std::find(wins[w].bits.begin(), wins[w].bits.end(), b) != wins[w].bits.end()) { ++b; continue; }
+            ++runs;
+            while (b < n && std::find(wins[w].bits.begin(), wins[w].bits.end(), b) == wins[w].bits.end()) ++b;
+        }
+        if (runs > kMaxRuns) return false;
+    }
+    for (int k = 0; k < p; ++k)
+        for (size_t w = 0; w < wins.size(); ++w) {
+            PassPlan pp;
+            pp.parity = true;
+            pp.tbits = wins[w].bits;
+            pp.play = k;
+            pp.phase = (w == 0) ? k : -1;
+            pp.expect = (k == p - 1 && w + 1 == wins.size());
+            pp.psteps = wsteps[w];
+            if (pp.phase >= 0) {  // the layer's phase on load: in a step, phase precedes its pair terms
+                pp.psteps.front().phase = 1;
+                if (pp.expect && pp.psteps.back().group != pp.psteps.front().group) {  // one q group per pass
+                    PassStep e;
+                    memset(&e, 0, sizeof(e));
+                    e.group = pp.psteps.front().group;
+                    pp.psteps.push_back(e);
+                }
+            }
+            if ((int)pp.psteps.size() > kMaxSteps) return false;
+            out.push_back(pp);
+        }
+    return true;
 }
 
 // one mixer step; q != nullptr also applies the phase exp(-i gamma q) first (fused into the
@@ -3126,10 +3301,32 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
         return QVA_OK;
     }
     if (P->mixer == QVA_MIXER_PARITY) {
-        QVA_TRY(ensure_q_dev(P));
         if (p == 0) return reset_state(P);
         P->layout = 0;
         P->perm.clear();
+        // tile passes (TMA pipeline, pair terms on register groups; QVA_PARITY_TILE=0: window kernel)
+        static int tile_env = [] {
+            const char *e = getenv("QVA_PARITY_TILE");
+            return e ? atoi(e) : 1;
+        }();
+        if (tile_env) {
+            auto it = P->parity_tile_sched.find(p);
+            if (it == P->parity_tile_sched.end() || P->parity_tile_seq != P->parity_seq) {
+                if (P->parity_tile_seq != P->parity_seq) P->parity_tile_sched.clear();
+                P->parity_tile_seq = P->parity_seq;
+                std::vector<PassPlan> passes;
+                if (!parity_tile_passes(P->n, P->L, P->G, P->parity_seq, p, passes)) passes.clear();
+                it = P->parity_tile_sched.emplace(p, std::move(passes)).first;
+            }
+            P->parity_tile_ran = !it->second.empty();
+            if (!it->second.empty()) {
+                if (!use_qgen(P)) QVA_TRY(ensure_q_dev(P));
+                QVA_TRY(run_passes(P, it->second, theta, p, 1, P->psi, 0, P->has_psi0 ? 2 : 1, nullptr));
+                *have_red = true;
+                return QVA_OK;
+            }
+        }
+        QVA_TRY(ensure_q_dev(P));
         for (int k = 0; k < p; ++k) QVA_TRY(parity_mix(P, theta[2 * k + 1], P->q, theta[2 * k], k == 0));
         return QVA_OK;
     }
@@ -3529,6 +3726,7 @@ qva_status qva_plan_query(const qva_plan *P, int32_t what, int64_t *out) {
         case 3: *out = P->world; return QVA_OK;
         case 4: *out = P->rank; return QVA_OK;
         case 5: *out = (int64_t)P->xfer_bytes; return QVA_OK;
+        case 6: *out = P->parity_tile_ran ? 1 : 0; return QVA_OK;
         default: set_error("qva_plan_query: unknown query"); return QVA_ERR_INVALID_ARGUMENT;
     }
 }

@@ -141,13 +141,43 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 // x(e) < 128 and k(e) a multiple of 128, so each access is one LOP3 + LDS/STS with an immediate.
 // A is laundered through a register move per item so ptxas cannot hoist the 8 XOR variants of
 // every stage out of the loop (they would not fit the register budget).
+// Groups 3 (V) and 4 (Z), added for the QAOAz parity pair terms, use the general form of the same
+// addressing: with T(c) / E(e) the tile indices of the thread bits / register bits (disjoint),
+// the swizzled 16-B slot is linear over GF(2): slot(T | E) = slot(T) ^ slot(E), slot(i) = i ^ ((i >> 3)
+// & 7), so addr = (A ^ x(e)) + k(e) with A = buf + 16 slot(T(c)), x(e) = 16 slot(E(e)) mod 1024 and
+// k(e) = the rest (bits >= 10 of A and of 16 slot(E(e)) are disjoint, and buf is 1024-B aligned).
+//   V: ebit {6,7,8,9,10}  tbit {0,1,2,3,4,5,11}
+//   Z: ebit {1,2,3,10,11} tbit {0,4,5,6,7,8,9}
+// (the first three thread bits of each group hit distinct bank-group bits, i0^i3, i1^i4, i2^i5).
+__host__ __device__ constexpr int dev_ebit(int G, int j) {
+    constexpr int V[5] = {6, 7, 8, 9, 10}, Z[5] = {1, 2, 3, 10, 11};
+    return G == 3 ? V[j] : Z[j];
+}
+__host__ __device__ constexpr int dev_tbit(int G, int j) {
+    constexpr int V[7] = {0, 1, 2, 3, 4, 5, 11}, Z[7] = {0, 4, 5, 6, 7, 8, 9};
+    return G == 3 ? V[j] : Z[j];
+}
+__host__ __device__ constexpr uint32_t swz_slot(uint32_t i) { return i ^ ((i >> 3) & 7); }
+template <int G>
+__device__ __forceinline__ constexpr uint32_t gen_e_index(int e) {
+    uint32_t i = 0;
+    for (int j = 0; j < kGroupBits; ++j)
+        if ((e >> j) & 1) i |= 1u << dev_ebit(G, j);
+    return i;
+}
 template <int G>
 __device__ __forceinline__ uint32_t group_base(uint32_t buf, int c) {
     const uint32_t l = c & 7, h = c >> 3;
     uint32_t a;
     if (G == 0) a = buf + (l << 4) + (h << 12);
     else if (G == 1) a = buf + ((l ^ ((h & 3) << 1)) << 4) + (h << 8);
-    else a = buf + (l << 4) + (l << 7) + (h << 12);
+    else if (G == 2) a = buf + (l << 4) + (l << 7) + (h << 12);
+    else {
+        uint32_t T = 0;
+#pragma unroll
+        for (int j = 0; j < kCT_BITS; ++j) T |= (uint32_t)((c >> j) & 1) << dev_tbit(G, j);
+        a = buf + (swz_slot(T) << 4);
+    }
     asm volatile("mov.b32 %0, %0;" : "+r"(a));
     return a;
 }
@@ -155,7 +185,41 @@ template <int G>
 __device__ __forceinline__ uint32_t group_addr(uint32_t A, int e) {
     if (G == 0) return (A ^ ((e & 7) << 4)) + (e << 7);
     if (G == 1) return (A ^ ((e >> 4) << 4)) + ((e >> 4) << 7) + ((e & 15) << 12);
-    return (A ^ ((e & 7) << 4)) + ((e >> 3) << 10);
+    if (G == 2) return (A ^ ((e & 7) << 4)) + ((e >> 3) << 10);
+    const uint32_t k = swz_slot(gen_e_index<G>(e)) << 4;
+    return (A ^ (k & 1023u)) + (k & ~1023u);
+}
+
+// QAOAz pair term exp(-i t (X_a X_b + Y_a Y_b)) on register bits (JA, JB): the Givens rotation by
+// 2t on the {01, 10} pairs (R19), u' = c u - i s v, v' = c v - i s u with c = cos 2t, s = sin 2t;
+// the {00, 11} elements are unchanged.  Same arithmetic as the oracle's or_pair_xy.
+template <int JA, int JB>
+__device__ __forceinline__ void givens_pair(double2 (&v)[kAPT], double c, double s) {
+#pragma unroll
+    for (int e = 0; e < kAPT; ++e)
+        if (((e >> JA) & 1) && !((e >> JB) & 1)) {
+            const int f = e ^ (1 << JA) ^ (1 << JB);
+            const double2 u = v[e], w = v[f];
+            v[e] = make_double2(fma(c, u.x, s * w.y), fma(c, u.y, -s * w.x));
+            v[f] = make_double2(fma(c, w.x, s * u.y), fma(c, w.y, -s * u.x));
+        }
+}
+__device__ __forceinline__ void apply_pairs(double2 (&v)[kAPT], const PassStep &st, double c, double s) {
+    for (int k = 0; k < st.npair; ++k) {
+        switch (st.pair[k]) {
+            case 0 * 8 + 1: givens_pair<0, 1>(v, c, s); break;
+            case 0 * 8 + 2: givens_pair<0, 2>(v, c, s); break;
+            case 0 * 8 + 3: givens_pair<0, 3>(v, c, s); break;
+            case 0 * 8 + 4: givens_pair<0, 4>(v, c, s); break;
+            case 1 * 8 + 2: givens_pair<1, 2>(v, c, s); break;
+            case 1 * 8 + 3: givens_pair<1, 3>(v, c, s); break;
+            case 1 * 8 + 4: givens_pair<1, 4>(v, c, s); break;
+            case 2 * 8 + 3: givens_pair<2, 3>(v, c, s); break;
+            case 2 * 8 + 4: givens_pair<2, 4>(v, c, s); break;
+            case 3 * 8 + 4: givens_pair<3, 4>(v, c, s); break;
+            default: break;
+        }
+    }
 }
 __device__ __forceinline__ double2 lds128(uint32_t a) {
     double2 v;
@@ -608,7 +672,9 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                         if (prev >= 0) wg_sync(wg);
                         smem_read_g<G>(v, buf, c);
                     }
-                    if (st.mask) rotate_group<G>(v, st.mask, tt);
+                    if constexpr (G <= 2) {
+                        if (st.mask) rotate_group<G>(v, st.mask, tt);
+                    }
                     if (QB > 0 && st.phase) {
                         if constexpr (q_gen<QB>())
                             apply_phase_gen<QB>(v, qs, P.groups[P.gq], c, lane, gcst, G_s, P.gen_m, ang->gamma,
@@ -617,11 +683,16 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                         else
                             apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
                     }
+                    if (st.npair) apply_pairs(v, st, ang->t1, ang->t2);  // QAOAz: after the step's phase
                     if (next != G) smem_write_g<G>(v, buf, c);
                 };
-                if (st.group == 0) body(std::integral_constant<int, 0>());
-                else if (st.group == 1) body(std::integral_constant<int, 1>());
-                else body(std::integral_constant<int, 2>());
+                switch (st.group) {
+                    case 0: body(std::integral_constant<int, 0>()); break;
+                    case 1: body(std::integral_constant<int, 1>()); break;
+                    case 2: body(std::integral_constant<int, 2>()); break;
+                    case 3: body(std::integral_constant<int, 3>()); break;
+                    default: body(std::integral_constant<int, 4>()); break;
+                }
                 prev = st.group;
                 if (k == P.release_step && !tstore) release();
             }
@@ -648,6 +719,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                     else
                         apply_phase_group<QB>(v, qs, c, lane, ang->gamma, use_tab_s ? tab_s : nullptr, tab_g);
                 }
+                if constexpr (PROG >= kFirstParityProg) apply_pairs(v, P.steps[K], ang->t1, ang->t2);  // QAOAz programs
                 if constexpr (K == REL) {
                     if (!tstore) release();
                 }
@@ -669,10 +741,13 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             // the tile goes back through shared memory in the load layout and out with one TMA
             // store; the stage is refilled once the store engine has read it
             if constexpr (PROG == 0) {
-                const int gf = P.steps[P.n_steps - 1].group;
-                if (gf == 0) smem_write_g<0>(v, buf, c);
-                else if (gf == 1) smem_write_g<1>(v, buf, c);
-                else smem_write_g<2>(v, buf, c);
+                switch (P.steps[P.n_steps - 1].group) {
+                    case 0: smem_write_g<0>(v, buf, c); break;
+                    case 1: smem_write_g<1>(v, buf, c); break;
+                    case 2: smem_write_g<2>(v, buf, c); break;
+                    case 3: smem_write_g<3>(v, buf, c); break;
+                    default: smem_write_g<4>(v, buf, c); break;
+                }
             } else {
                 smem_write_g<prog_def<PROG>().g[prog_def<PROG>().n - 1]>(v, buf, c);
             }
@@ -834,6 +909,14 @@ cudaError_t launch_prog(const CUtensorMap &map, const CUtensorMap &mo, const Til
         case 8: return launch_one<STAGES, QB, 8>(map, mo, p, grid, s);
         case 9: return launch_one<STAGES, QB, 9>(map, mo, p, grid, s);
         case 10: return launch_one<STAGES, QB, 10>(map, mo, p, grid, s);
+        case 11: return launch_one<STAGES, QB, 11>(map, mo, p, grid, s);
+        case 12: return launch_one<STAGES, QB, 12>(map, mo, p, grid, s);
+        case 13: return launch_one<STAGES, QB, 13>(map, mo, p, grid, s);
+        case 14: return launch_one<STAGES, QB, 14>(map, mo, p, grid, s);
+        case 15: return launch_one<STAGES, QB, 15>(map, mo, p, grid, s);
+        case 16: return launch_one<STAGES, QB, 16>(map, mo, p, grid, s);
+        case 17: return launch_one<STAGES, QB, 17>(map, mo, p, grid, s);
+        case 18: return launch_one<STAGES, QB, 18>(map, mo, p, grid, s);
         default: return launch_one<STAGES, QB, 0>(map, mo, p, grid, s);
     }
 }

@@ -51,7 +51,8 @@ constexpr int kTileBits = 12;                 // 2^12 amplitudes (64 KiB) per ti
 constexpr int kGroupBits = 5;                 // 32 amplitudes per consumer thread in registers
 constexpr int kCT_BITS = 7;                   // 128 consumer threads
 constexpr int kMaxSteps = 16;
-constexpr int kMaxGroups = 3;
+constexpr int kMaxGroups = 5;                // X, Y, W (X mixer) + V, Z (QAOAz parity pair terms)
+constexpr int kMaxStepPairs = 6;             // parity pair terms per register-group step
 constexpr int kSmallMaxQubits = 12;           // whole-state-in-one-CTA path
 constexpr int kQGenInt = 3;                   // tile-pass q mode: generated MaxCut q, unit weights
 constexpr int kQGenF64 = 9;                   // tile-pass q mode: generated MaxCut q, fp64 weights
@@ -70,6 +71,11 @@ struct PassStep {
     int8_t mask;       // 5-bit rotation mask over the group's register bits
     int8_t angle;      // 0: first beta slot (R1), 1: second (R2)
     int8_t phase;      // apply the phase after the rotations of this step (group must be gq)
+    // QAOAz parity mixer (R19): pair terms exp(-i t (X_aX_b + Y_aY_b)), in order,
+    // on register bits (ja, jb) of this group, encoded ja * 8 + jb (ja < jb); the pass's angle record
+    // holds t1 = cos 2t, t2 = sin 2t
+    int8_t npair;
+    int8_t pair[kMaxStepPairs];
 };
 
 // Per-member angle record for one pass (device array [batch]).  Rotations use the factored
@@ -146,7 +152,8 @@ struct TileProg {
     int phase_k;
     bool expect;
 };
-constexpr int kNumTileProgs = 11;
+constexpr int kNumTileProgs = 19;
+constexpr int kFirstParityProg = 11;  // programs >= this apply the steps' QAOAz pair terms
 constexpr TileProg kTileProgs[kNumTileProgs] = {
     {0, {0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}, -1, false},  // 0: generic
     {2, {0, 1, 0, 0, 0}, {1, 1, 0, 0, 0}, -1, false},  // 1: X Y            (B/C pass)
@@ -160,6 +167,16 @@ constexpr TileProg kTileProgs[kNumTileProgs] = {
     {1, {1, 0, 0, 0, 0, 0}, {1, 0, 0, 0, 0, 0}, -1, false}, // 8: Y            (short sets: shards, n < 24)
     {1, {1, 0, 0, 0, 0, 0}, {1, 0, 0, 0, 0, 0}, -1, true},  // 9: Y + <Q>
     {2, {1, 1, 0, 0, 0, 0}, {1, 1, 0, 0, 0, 0}, 0, false},  // 10: Y | P | Y
+    // QAOAz parity windows (pair terms in every step, runtime lists; groups V = 3, Z = 4): the shapes
+    // the window planner gives the default sequence (contiguous window W Z X V, strided X Y V / Y V)
+    {4, {2, 4, 0, 3, 0, 0}, {0, 0, 0, 0, 0, 0}, 0, false},  // 11: P | W Z X V
+    {4, {2, 4, 0, 3, 0, 0}, {0, 0, 0, 0, 0, 0}, -1, false}, // 12: W Z X V
+    {3, {0, 1, 3, 0, 0, 0}, {0, 0, 0, 0, 0, 0}, -1, false}, // 13: X Y V
+    {3, {0, 1, 3, 0, 0, 0}, {0, 0, 0, 0, 0, 0}, 0, false},  // 14: P | X Y V
+    {2, {1, 3, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0}, -1, false}, // 15: Y V
+    {2, {1, 3, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0}, -1, true},  // 16: Y V + <Q>
+    {3, {0, 1, 3, 0, 0, 0}, {0, 0, 0, 0, 0, 0}, -1, true},  // 17: X Y V + <Q>
+    {2, {1, 3, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0}, 0, false},  // 18: P | Y V
 };
 
 int tile_pass_grid(uint64_t items);

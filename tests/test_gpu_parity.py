@@ -464,6 +464,46 @@ def test_qaoaz_parity_vs_oracle(Q, n, seq, p):
         _f_close(f[1], O.expectation(O.evolve_parity(n, q, sq, theta[::-1], psi0), q))
 
 
+@pytest.mark.parametrize("n,p,mode", [(12, 1, "gen"), (16, 2, "stored"), (20, 2, "gen_w"), (22, 3, "gen"),
+                                      (24, 2, "stored_int")])
+def test_qaoaz_parity_tile_passes_vs_oracle(Q, n, p, mode):
+    """The QAOAz mixer as TMA tile passes (default qubit sequence): each window's pair terms run on
+    register groups X/Y/W/V/Z inside one HBM round trip, the phase fused into the first window of
+    a layer (generated max-cut q, unit or fp64 weights, or stored fp64 / integer q), <Q> into the
+    last; from |+>, from a weight-n/2 state and as a batch, against the oracle."""
+    rng = np.random.default_rng(700 + n)
+    u, v = random_regular_graph(n, 3, rng)
+    w = rng.uniform(0, 1, len(u)) if mode == "gen_w" else None
+    q = O.maxcut_q(n, u, v, w)
+    if mode == "stored":
+        q = rng.standard_normal(1 << n)
+    theta = rng.uniform(0, math.pi, 2 * p)
+    sq = list(range(n))
+    with Q.Plan(1 << n, "parity", n_qubits=n, max_batch=2) as P:
+        if mode.startswith("gen"):
+            P.set_qualities_maxcut(u, v, w)
+        else:
+            P.set_qualities(q)
+        ref = O.evolve_parity(n, q, sq, theta, O.init_uniform(1 << n))
+        P.evolve(theta)
+        assert P.query("parity_tile") == 1
+        _f_close(P.expectation(), O.expectation(ref, q), O.expectation(ref, np.abs(q)))
+        _amp_close(P.get_state(), ref)
+        psi0 = np.zeros(1 << n, np.complex128)
+        idx = rng.choice([x for x in range(1 << min(n, 16)) if bin(x).count("1") == min(n, 16) // 2], 64)
+        psi0[idx] = rng.standard_normal(64) + 1j * rng.standard_normal(64)
+        psi0 /= np.linalg.norm(psi0)
+        P.set_initial_state(psi0)
+        ref0 = O.evolve_parity(n, q, sq, theta, psi0)
+        P.evolve(theta)
+        assert P.query("parity_tile") == 1
+        _amp_close(P.get_state(), ref0)
+        th2 = np.stack([theta, rng.uniform(0, math.pi, 2 * p)])
+        f = P.evolve_batch(th2)
+        for b in range(2):
+            _f_close(f[b], O.expectation(O.evolve_parity(n, q, sq, th2[b], psi0), q), O.expectation(ref0, np.abs(q)))
+
+
 def _pair_group_csr(n, pairs):
     """CSR of sum over the pairs (a, b) of (X_a X_b + Y_a Y_b) = 2 (|01><10| + |10><01|) on (a, b):
     built from the definition, independently of the parity kernel."""
