@@ -1400,7 +1400,7 @@ struct PassHostData {
     std::vector<int> tab_index;
 };
 static void pass_host_data(const std::vector<PassPlan> &passes, const double *thetas, int p, int batch,
-                           bool int_table, int n_tile_passes, PassHostData &H) {
+                           bool int_table, int n_tile_passes, PassHostData &H, bool fold_gf = false) {
     std::vector<PassAngles> &ang = H.ang;
     ang.assign((size_t)n_tile_passes * batch, PassAngles{});
     std::vector<char> &half1 = H.half1, &half2 = H.half2;
@@ -1474,6 +1474,8 @@ static void pass_host_data(const std::vector<PassPlan> &passes, const double *th
             const bool last = (j == n_tile_passes - 1);
             const bool fold_tab = pp.phase >= 0 && int_table;
             const bool fold_here = (pp.phase >= 0 && !int_table) || last;
+            // factorised fp64 generated phase: the factor rides on the per-member G table (free)
+            const bool into_gf = fold_gf && pp.phase >= 0 && !int_table;
             for (int b = 0; b < batch; ++b) {
                 PassAngles &a = ang[(size_t)j * batch + b];
                 const double2 f = a.scale, c = carry[b];
@@ -1482,7 +1484,7 @@ static void pass_host_data(const std::vector<PassPlan> &passes, const double *th
                 if (fold_here) a.scale = carry[b];
                 if (fold_tab || fold_here) carry[b] = make_double2(1.0, 0.0);
             }
-            apply_scale[j] = fold_here ? 1 : 0;
+            apply_scale[j] = into_gf ? 2 : (fold_here ? 1 : 0);
             ++j;
         }
     }
@@ -1517,7 +1519,8 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
     const int tab_qmin = gen == kQGenInt ? -P->g_m : P->qmin;
     QVA_TRY(ensure_angles(P, (size_t)n_tile_passes * batch));
     PassHostData H;
-    pass_host_data(passes, thetas, p, batch, int_table, n_tile_passes, H);
+    pass_host_data(passes, thetas, p, batch, int_table, n_tile_passes, H,
+                   gen == kQGenF64 && batch <= kGfMembersHost);
     const std::vector<PassAngles> &ang = H.ang;
     const std::vector<char> &half1 = H.half1, &half2 = H.half2, &apply_scale = H.apply_scale;
     const std::vector<double> &gam = H.gam;
@@ -1701,7 +1704,8 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         tp.work_ctr = (g_dyn == 1 || (g_dyn > 1 && ((g_dyn >> 1) >> j) & 1)) ? P->d_ctr + j : nullptr;
         tp.expect = pp.expect ? 1 : 0;
         tp.partials = P->partials;
-        tp.apply_scale = apply_scale[j];
+        tp.apply_scale = apply_scale[j] == 1 ? 1 : 0;
+        tp.fold_scale_gf = apply_scale[j] == 2 ? 1 : 0;
         // last step touching shared memory: a group switch (smem transpose) or the phase (q stage)
         tp.release_step = (tp.init == 1 && tp.gq < 0) ? -1 : 0;
         for (int k = 0; k < tp.n_steps; ++k)
@@ -1820,7 +1824,7 @@ qva_status run_passes_graph(qva_plan *P, const std::vector<PassPlan> &passes, co
     const int gen = qgen_mode(P, 1);
     const bool int_table = gen == kQGenInt || (!gen && P->q_mode != 0);
     PassHostData H;
-    pass_host_data(passes, theta, p, 1, int_table, n_tile_passes, H);
+    pass_host_data(passes, theta, p, 1, int_table, n_tile_passes, H, gen == kQGenF64);
     std::vector<int64_t> key = {p, (int64_t)(uintptr_t)P->psi, (int64_t)(uintptr_t)P->psi_alt, init_mode,
                                 P->q_gen_id, gen, (int64_t)P->q_classified, (int64_t)P->q_mode,
                                 (int64_t)(uintptr_t)&passes};

@@ -384,15 +384,26 @@ __device__ __forceinline__ void apply_phase_gen_f64_fact(double2 (&v)[kAPT], dou
         sincos(gamma * al[j], &sn, &cs);
         z[j] = make_double2(cs, sn);
     }
-    static_for<kAPT>([&](auto gc) {
+    // four independent Gray-code chains over the low 3 register bits (one per value of bits 3, 4):
+    // the same 31 products as one chain, a quarter of its dependency depth
+    double2 r4[4];
+    r4[0] = run;
+    r4[1] = cmul(run, z[3]);
+    r4[2] = cmul(run, z[4]);
+    r4[3] = cmul(r4[1], z[4]);
+    static_for<8>([&](auto gc) {
         constexpr int Gk = decltype(gc)::value;
-        constexpr int E = Gk ^ (Gk >> 1);
+        constexpr int El = Gk ^ (Gk >> 1);
         if constexpr (Gk > 0) {
             constexpr int J = gray_flip<Gk>();
-            if constexpr ((E >> J) & 1) run = cmul(run, z[J]);
-            else run = cmul(run, make_double2(z[J].x, -z[J].y));
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                if constexpr ((El >> J) & 1) r4[h] = cmul(r4[h], z[J]);
+                else r4[h] = cmul(r4[h], make_double2(z[J].x, -z[J].y));
+            }
         }
-        v[E] = cmul(v[E], cmul(run, gf_s[E]));
+#pragma unroll
+        for (int h = 0; h < 4; ++h) v[El | (h << 3)] = cmul(v[El | (h << 3)], cmul(r4[h], gf_s[El | (h << 3)]));
     });
 }
 
@@ -592,7 +603,8 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                     for (int k = tid; k < 32 * P.batch; k += kThreads) {
                         double sn, cs;
                         sincos(P.angles[k >> 5].gamma * (double)Gg[k & 31], &sn, &cs);
-                        gf_s[k] = make_double2(cs, sn);
+                        gf_s[k] = P.fold_scale_gf ? cmul(make_double2(cs, sn), P.angles[k >> 5].scale)
+                                                  : make_double2(cs, sn);
                     }
             }
             const GV *cg = reinterpret_cast<const GV *>(P.gen_thr) + (size_t)(tid % kCT) * 8;

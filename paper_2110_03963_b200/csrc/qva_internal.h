@@ -121,6 +121,8 @@ struct TilePassParams {
     int expect;              // accumulate partial <Q> and norm in the final group (== gq)
     int qmin, ntab;
     int apply_scale;
+    int fold_scale_gf;       // fp64 factorised generated phase: multiply the per-member G factors by
+                             // angles[member].scale instead of every amplitude (apply_scale = 0)
     int tma_store;           // 1: write the tile back with a TMA tensor store (strided tile sets)
     int release_step;        // step after whose smem accesses the stage is released (n_steps: after
                              // the expectation; -1: before any step, i.e. init passes without q)
