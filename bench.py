@@ -125,6 +125,10 @@ def total_bytes_step_gpu(plan, Q, steps):
     return sum(plan.kernel_stats(c)["bytes"] for c in Q.KERNEL_CLASSES) / steps
 
 
+def local_n_of(plan):
+    return plan.get_partition()[0]
+
+
 def host_info():
     """nproc, CPU model and MemTotal of the box the oracle is timed on."""
     info = {"nproc": os.cpu_count()}
@@ -181,6 +185,15 @@ def workload_for(args, world):
     elif name == "cfg1":
         wl = make_config("cfg1")
         desc = "cfg1: QAOA MaxCut n=10, 3-regular, p=2"
+    elif name == "cfg3cf":
+        wl = make_config("cfg3")
+        desc = ("cfg3 with the K_N closed-form mixer (opt-in reference path, SURVEY K10): QWOA N=10!, "
+                "q~N(0,1), lambda=(0,N,...,N), p=4")
+    elif name == "qaoaz28":
+        wl = make_config("cfg4", n_override=28, p_override=2)
+        wl.mixer = "parity"
+        desc = ("NEXT-2: QAOAz, parity (XY) mixer over qubits 0..27 (B_odd, B_even), n=28, max-cut q of the "
+                "cfg4 recipe generated on the device, p=2, from a Hamming-weight-14 basis state")
     else:
         raise SystemExit(f"unknown workload {name}")
     return name, wl, desc
@@ -242,6 +255,17 @@ def oracle_sample(name, wl, budget_s=20.0):
         dt = time.perf_counter() - t0
         desc = f"oracle evolution + <Q> of {nb} of the {B} parameter sets of {name} (n={wl.n_qubits}), {cores} threads"
         return wl.dim * wl.p * nb / dt, dt, cores, desc
+    if wl.mixer == "parity":  # QAOAz: the oracle's pair-term loops on a smaller slice of the recipe
+        n = min(wl.n_qubits, 22)
+        swl = make_config("cfg4", n_override=n, p_override=wl.p)
+        q = O.maxcut_q(n, swl.edges_u, swl.edges_v)
+        psi0 = np.zeros(1 << n, np.complex128)
+        psi0[(1 << (n // 2)) - 1] = 1.0
+        t0 = time.perf_counter()
+        psi = O.evolve_parity(n, q, list(range(n)), swl.theta, psi0)
+        O.expectation(psi, q)
+        dt = time.perf_counter() - t0
+        return (1 << n) * wl.p / dt, dt, cores, f"oracle QAOAz evolution + <Q> at n={n} (the workload has n={wl.n_qubits}), {cores} threads"
     # circulant: closed-form oracle on the full cfg3 size
     t0 = time.perf_counter()
     psi = O.evolve_complete(wl.q, wl.theta, wl.lam0, wl.lam_rest)
@@ -321,10 +345,14 @@ def main():
     vshards = max(1, args.virtual_shards) if world == 1 else 1
     plan = Q.Plan(wl.dim, wl.mixer, n_qubits=wl.n_qubits, rank=rank, world=world, nccl_id=nccl_id,
                   device=local_rank, stream=stream.cuda_stream, max_batch=len(batch) if batch is not None else 1,
-                  virtual_shards=vshards, peer_store_exchange=vshards > 1)
+                  virtual_shards=vshards, peer_store_exchange=vshards > 1, complete_closed_form=name == "cfg3cf")
     G = world * vshards
-    if wl.mixer == "x":
+    if wl.mixer in ("x", "parity"):
         plan.set_qualities_maxcut(wl.edges_u, wl.edges_v, wl.weights)
+        if wl.mixer == "parity":
+            psi0 = np.zeros(local_n_of(plan), np.complex128)
+            psi0[(1 << (wl.n_qubits // 2)) - 1] = 1.0
+            plan.set_initial_state(psi0)
     else:
         plan.set_qualities(wl.q)
         plan.set_circulant_eigenvalues_const(wl.lam0, wl.lam_rest)
@@ -374,7 +402,10 @@ def main():
     value = amp_layers / (ms_step * 1e-3)
 
     # dominant kernel
-    cls = "tile" if wl.mixer == "x" and wl.n_qubits > 12 else ("small" if wl.mixer == "x" else "fft_col")
+    if wl.mixer in ("x", "parity"):
+        cls = "tile" if wl.n_qubits > 12 else "small"
+    else:
+        cls = "other" if name == "cfg3cf" else "fft_col"
     st = plan.kernel_stats(cls)
     kernel_share = None
     total_kernel_ms = sum(plan.kernel_stats(c)["ms"] for c in Q.KERNEL_CLASSES)
@@ -386,7 +417,7 @@ def main():
     if st["launches"] > 0 and st["ms"] > 0:
         impl_bytes = st["bytes"] / st["launches"]
         per_launch_s = st["ms"] * 1e-3 / st["launches"]
-        if cls == "tile" and local_n >= (1 << 24):
+        if cls == "tile" and wl.mixer == "x" and local_n >= (1 << 24):
             # algorithmic bytes per launch = the SURVEY 8(d) floor (64 B per amplitude-layer) x the
             # amplitude-layers one launch processes (this GPU's amp-layers of the timed steps over its
             # tile-pass launches)
@@ -406,7 +437,7 @@ def main():
                 "frac_implemented": impl_bytes / per_launch_s / 1e9 / peak,
                 "mean_launch_ms": st["ms"] / st["launches"], "launches": st["launches"],
                 "share_of_kernel_time": kernel_share, "peak_source": peak_src}
-        if cls == "tile" and local_n >= (1 << 24):
+        if cls == "tile" and wl.mixer == "x" and local_n >= (1 << 24):
             # the whole step against the floor (every kernel and gap of the step included)
             roof["frac_step_vs_floor"] = FLOOR_X_BYTES * amp_layers / G * per_gpu / (ms_step * 1e-3) / 1e9 / peak
     # sharded runs: combined HBM / NVLink roofline per layer:
