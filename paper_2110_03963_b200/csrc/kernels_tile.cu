@@ -6,16 +6,21 @@
 // <psi|Q|psi> = sum |psi_x|^2 q_x and of the norm (Eq. 2).
 //
 // sm_100a design:
-//  * persistent grid, one CTA per SM, 5 warps: warp 4 lane 0 is the TMA producer, warps 0-3
-//    (128 threads) are consumers holding 32 amplitudes each in registers;
+//  * persistent grid, one CTA per SM, 256 threads = two consumer warpgroups that take alternate
+//    tiles; there is no producer warp: the warpgroup that frees a stage refills it (one elected
+//    thread claims the next tile from a per-pass atomic counter and issues its TMA load);
 //  * a STAGES-deep ring of 64 KiB shared-memory tiles filled by cp.async.bulk.tensor (one 5-D
 //    box per tile: the tile bits are box dimensions, the other index bits are coordinates, so
 //    strided high-qubit tiles cost one instruction) with SWIZZLE_128B, completion on mbarriers;
-//  * the qualities (fp64 or compact integer codes) arrive in the same stage by a 1-D bulk copy
-//    from a copy of q pre-permuted into consumer order (conflict-free 16-byte smem reads);
-//  * rotations run on register groups of 5 tile bits; a group change is one in-place swizzled
-//    smem transpose (conflict-free LDS.128/STS.128); results are stored straight from
-//    registers with st.global.cs (full 128-B segments on the X/Y groups).
+//  * the qualities (fp64 or compact integer codes, or per-tile records of generated max-cut q)
+//    arrive in the same stage by a 1-D bulk copy from a copy pre-permuted into consumer order
+//    (conflict-free 16-byte smem reads);
+//  * each consumer thread holds 32 amplitudes; rotations (and the QAOAz pair terms) run on
+//    register groups of 5 tile bits; a group change is one in-place swizzled smem transpose
+//    (conflict-free LDS.128/STS.128);
+//  * the finished tile is written back to its stage in the load layout and leaves with one TMA
+//    tensor store (cp.async.bulk.tensor ... bulk_group), or, for the fused multi-GPU exchange,
+//    with register stores into the peers' IPC-mapped buffers.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
