@@ -105,8 +105,9 @@ typedef struct {
  * handles and maps every peer's (the fused peer-store exchange); if any rank
  * fails to map, all ranks fall back to NCCL send/recv (decided by a min-vote).
  * QVA_ERR_UNSUPPORTED: X mixer with dim != 2^n_qubits, world / shard count not a power of two
- * for the X mixer, sharded sparse or parity mixers (use the replicated mode for their batches),
- * a sharded circulant dim with no split M1*M2 that the shard count divides. */
+ * for the X mixer, sharded parity mixers or virtual shards of a sparse mixer (use the replicated
+ * mode for their batches), a sharded circulant dim with no split M1*M2 that the shard count
+ * divides.  A world > 1 sparse plan holds a row block of W (qva_set_sparse_mixer_rows). */
 qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out);
 
 /* Host transport of a world > 1 plan: the caller's own process group (e.g. torch.distributed over
@@ -185,6 +186,19 @@ qva_status qva_set_circulant_eigenvalues_const(qva_plan *plan, double lambda0, d
  * action uses s = max(1, ceil(|beta| ||W||_1 / 3)) sub-steps of degree <= 40 (reading R13). */
 qva_status qva_set_sparse_mixer(qva_plan *plan, const int64_t *row_ptr, const int32_t *col,
                                 const double *val, uint64_t nnz);
+/* Row-partitioned W for a world > 1 sparse plan (the paper's distributed SpMV, PAPER.md:333,
+ * :1099; COMM-psi partition, Eqs. local_i / offset, :356-366): this rank's rows [row_offset,
+ * row_offset + rows), which must be its partition (qva_plan_get_partition); row_ptr[rows + 1]
+ * local (row_ptr[0] = 0, row_ptr[rows] = nnz), col[nnz] GLOBAL column indices in [0, dim),
+ * val[nnz] or NULL.  Collective: every rank calls it; ||W||_1 is the global maximum row sum, and
+ * every rank's Taylor-term buffers are exported as CUDA IPC handles and mapped, so each SpMV reads
+ * the entries of remote columns straight from the owning rank's buffer over NVLink (if any rank
+ * cannot map them, every term vector is all-gathered instead); the per-term norm maximum is one
+ * all-reduce of two doubles, which also orders every rank's term k before any term k + 1.  With
+ * world = 1 it equals qva_set_sparse_mixer (row_offset 0, rows = dim).
+ * QVA_ERR_SIZE_MISMATCH: rows / row_offset not this rank's partition or row_ptr inconsistent. */
+qva_status qva_set_sparse_mixer_rows(qva_plan *plan, const int64_t *row_ptr, const int32_t *col,
+                                     const double *val, uint64_t row_offset, uint64_t rows, uint64_t nnz);
 
 /* QAOAz parity mixer (QVA_MIXER_PARITY plans; PAPER.md:213-248 Eqs. parity_terms, qaoaz_mixers):
  * the ordered qubit subsequence s[0..count) the mixing operators act on.
@@ -301,7 +315,9 @@ qva_status qva_launch_count(qva_plan *plan, int64_t *launches);
  * bytes one shard has sent to the other shards (global<->local exchanges, circulant transposes:
  * (G-1)/G of a shard's slice each) since the last qva_reset_kernel_stats -- the NVLink traffic of
  * a real shard, the notional one of a virtual shard; 6: 1 if the last QAOAz (parity) evolution ran
- * as TMA tile passes with the pair terms on register groups, 0 if it took the window kernel.
+ * as TMA tile passes with the pair terms on register groups, 0 if it took the window kernel; 7: 1 if
+ * a row-partitioned sparse mixer reads remote columns from the peers' IPC-mapped Taylor buffers,
+ * 0 (single shard, or the term-gather fallback).
  * QVA_ERR_INVALID_ARGUMENT for another `what`. */
 qva_status qva_plan_query(const qva_plan *plan, int32_t what, int64_t *out);
 

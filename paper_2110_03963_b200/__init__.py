@@ -124,6 +124,7 @@ def _load():
         "qva_set_circulant_eigenvalues": [P, P, u64, u64],
         "qva_set_circulant_eigenvalues_const": [P, d, d],
         "qva_set_sparse_mixer": [P, P, P, P, u64],
+        "qva_set_sparse_mixer_rows": [P, P, P, P, u64, u64, u64],
         "qva_set_parity_mixer": [P, P, i32],
         "qva_parity_schedule": [i32, P, i32, P, i32, ctypes.POINTER(i32)],
         "qva_set_initial_state": [P, P, u64, u64],
@@ -384,6 +385,15 @@ class Plan:
         val = None if val is None else _f64(val)
         _call("qva_set_sparse_mixer", self._h, _ptr(row_ptr), _ptr(col), _ptr(val), len(col))
 
+    def set_sparse_mixer_rows(self, row_ptr, col, val=None, row_offset: int = 0):
+        """This rank's rows of a row-partitioned W (world > 1; include/qva.h): local row_ptr,
+        global column indices.  Collective."""
+        row_ptr = np.ascontiguousarray(row_ptr, np.int64)
+        col = np.ascontiguousarray(col, np.int32)
+        val = None if val is None else _f64(val)
+        _call("qva_set_sparse_mixer_rows", self._h, _ptr(row_ptr), _ptr(col), _ptr(val), int(row_offset),
+              len(row_ptr) - 1, len(col))
+
     def set_parity_mixer(self, qubits):
         """Ordered qubit subsequence of the QAOAz parity mixer (include/qva.h)."""
         s = np.ascontiguousarray(qubits, np.int32)
@@ -479,7 +489,7 @@ class Plan:
     def query(self, what) -> int:
         """qva_plan_query: 'fused_exchange', 'shards', 'host_transport', 'world', 'rank', 'xfer_bytes' (0..5)."""
         keys = {"fused_exchange": 0, "shards": 1, "host_transport": 2, "world": 3, "rank": 4, "xfer_bytes": 5,
-                "parity_tile": 6}
+                "parity_tile": 6, "sparse_peer": 7}
         out = ctypes.c_int64()
         _call("qva_plan_query", self._h, keys.get(what, what), ctypes.byref(out))
         return out.value

@@ -835,6 +835,32 @@ qva_status coll_alltoall_dev(qva_plan *P, const void *src, void *dst, size_t chu
 // ---- exchange (global <-> local qubit swap; COMM-psi) ----------------------
 // Every shard r sends chunk t (local index top-g bits = t) to shard t, which stores it as its
 // chunk r: a block transpose of the G x G chunk matrix.  The layout flips between A and B.
+// all-gather of equal device slices: rank r's `bytes` at src land at dst + r * bytes (NCCL on the
+// stream; host transport through host memory)
+qva_status coll_allgather_dev(qva_plan *P, const void *src, void *dst, size_t bytes) {
+    if (P->host_tp) {
+        std::vector<char> hs(bytes), hr(bytes * P->world);
+        QVA_CUDA_TRY(cudaMemcpyAsync(hs.data(), src, bytes, cudaMemcpyDeviceToHost, P->stream));
+        QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
+        QVA_TRY(tp_check(P->tp.allgather(P->tp.ctx, hs.data(), hr.data(), bytes), "allgather"));
+        QVA_CUDA_TRY(cudaMemcpyAsync(dst, hr.data(), hr.size(), cudaMemcpyHostToDevice, P->stream));
+        QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
+        return QVA_OK;
+    }
+    QVA_NCCL_TRY(ncclAllGather(src, dst, bytes, ncclChar, P->comm, P->stream));
+    return QVA_OK;
+}
+
+// collectives of the row-partitioned sparse mixer (SparseComm, kernels_sparse.cu)
+struct PlanSparseComm : SparseComm {
+    qva_plan *P;
+    explicit PlanSparseComm(qva_plan *P_) : P(P_) {}
+    qva_status max2(double *v) override { return coll_allreduce_host(P, v, 2, kCollMax); }
+    qva_status gather(const double2 *local, double2 *all, uint64_t stride) override {
+        return coll_allgather_dev(P, local, all, stride * sizeof(double2));
+    }
+};
+
 // cross-shard traffic of one all-to-all of `elem_bytes`-byte elements over the whole (local) array:
 // each shard keeps 1/G of its slice and sends the rest, (G-1)/G x slice bytes
 void count_xfer(qva_plan *P, double elem_bytes) {
@@ -2406,7 +2432,9 @@ qva_status apply_mixer_impl(qva_plan *P, double beta) {
         }
         int terms = 0;
         PlanObserver obs(P);
-        return sparse_apply_mixer(P->sm, P->psi, beta, P->stream, &obs, &terms);
+        PlanSparseComm comm(P);
+        return sparse_apply_mixer(P->sm, P->psi, beta, P->stream, &obs, &terms,
+                                  (P->world > 1 && !P->replicated) ? &comm : nullptr);
     }
     return QVA_ERR_UNSUPPORTED;
 }
@@ -2606,10 +2634,17 @@ qva_status qva_plan_destroy(qva_plan *P) {
     DeviceGuard dg(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     harvest(P);
-    if (P->ipc_ok) {
+    if (P->ipc_ok || P->sm.peer_ok) {
         // collective teardown: unmap the peers' buffers, then wait until every rank has unmapped
         // ours before freeing them (freeing exported memory that a peer still maps is undefined)
         close_peer_maps(P);
+        if (P->sm.peer_ok) {
+            for (int k = 0; k < 2; ++k)
+                for (int t = 0; t < P->world; ++t)
+                    if (t != P->rank && P->sm.src.peer[k][t]) cudaIpcCloseMemHandle((void *)P->sm.src.peer[k][t]);
+            cudaGetLastError();
+            P->sm.peer_ok = false;
+        }
         if (P->created) {
             if (coll_stream_barrier(P) != QVA_OK) fprintf(stderr, "[qva] destroy: barrier failed: %s\n", qva_last_error());
             cudaStreamSynchronize(P->stream);
@@ -2659,6 +2694,7 @@ qva_status qva_plan_destroy(qva_plan *P) {
     cudaFree(P->sm.t0);
     cudaFree(P->sm.t1);
     cudaFree(P->sm.scratch);
+    cudaFree(P->sm.gather_buf);
     for (auto e : P->event_pool) cudaEventDestroy(e);
     if (P->comm) ncclCommDestroy(P->comm);
     if (P->own_stream && P->stream) cudaStreamDestroy(P->stream);
@@ -2701,6 +2737,12 @@ qva_status qva_plan_create_ex(const qva_plan_desc *desc, const qva_transport *tr
         // distributed four-step FFT: needs G | M1 and G | M2 (checked on the FFT plan)
         if (d.dim % (uint64_t)G) {
             set_error("sharded circulant mixer needs dim divisible by the shard count");
+            return QVA_ERR_UNSUPPORTED;
+        }
+    } else if (G > 1 && d.mixer == QVA_MIXER_SPARSE && vs == 1) {
+        // row-partitioned W over real ranks (qva_set_sparse_mixer_rows): any dim, COMM-psi blocks
+        if ((uint64_t)d.world > d.dim) {
+            set_error("sharded sparse mixer needs dim >= world");
             return QVA_ERR_UNSUPPORTED;
         }
     } else if (G > 1) {
@@ -2768,7 +2810,8 @@ qva_status qva_plan_create_ex(const qva_plan_desc *desc, const qva_transport *tr
         return true;
     };
     if (!alloc((void **)&P->psi, P->arr_n * sizeof(double2))) return fail(QVA_ERR_OUT_OF_MEMORY);
-    if (G > 1 && !alloc((void **)&P->psi_alt, P->arr_n * sizeof(double2))) return fail(QVA_ERR_OUT_OF_MEMORY);
+    if (G > 1 && d.mixer != QVA_MIXER_SPARSE && !alloc((void **)&P->psi_alt, P->arr_n * sizeof(double2)))
+        return fail(QVA_ERR_OUT_OF_MEMORY);
     if (!alloc((void **)&P->red, (size_t)P->max_batch * 2 * sizeof(double))) return fail(QVA_ERR_OUT_OF_MEMORY);
     if (!alloc((void **)&P->d_flag, sizeof(int))) return fail(QVA_ERR_OUT_OF_MEMORY);
     P->thetas_cap = 256;
@@ -3072,39 +3115,75 @@ qva_status qva_set_parity_mixer(qva_plan *P, const int32_t *qubits, int32_t coun
 
 qva_status qva_set_sparse_mixer(qva_plan *P, const int64_t *row_ptr, const int32_t *col, const double *val,
                                 uint64_t nnz) {
+    if (!P) return QVA_ERR_INVALID_ARGUMENT;
+    if (P->world > 1 && !P->replicated) {
+        set_error("world > 1: each rank passes its own rows with qva_set_sparse_mixer_rows");
+        return QVA_ERR_INVALID_ARGUMENT;
+    }
+    return qva_set_sparse_mixer_rows(P, row_ptr, col, val, 0, P->N, nnz);
+}
+
+// Row-partitioned W (the paper's distributed SpMV): this rank's rows
+// [row_offset, row_offset + rows) = its COMM-psi partition, global column indices.  Collective for
+// world > 1: the global ||W||_1 (max-allreduce) and the IPC handles of every rank's Taylor buffers
+// (the SpMV reads remote columns straight from the peers' buffers; if any rank cannot map them,
+// all fall back to gathering each term vector).
+qva_status qva_set_sparse_mixer_rows(qva_plan *P, const int64_t *row_ptr, const int32_t *col, const double *val,
+                                     uint64_t row_offset, uint64_t rows, uint64_t nnz) {
     if (!P || !row_ptr || (nnz && !col)) return QVA_ERR_INVALID_ARGUMENT;
     if (P->mixer != QVA_MIXER_SPARSE) {
         set_error("not a sparse-mixer plan");
         return QVA_ERR_UNSUPPORTED;
     }
-    uint64_t rows = P->N;
+    if (row_offset != P->offset || rows != P->local_n) {
+        set_error("qva_set_sparse_mixer_rows: rows must be this rank's partition [" + std::to_string(P->offset) + ", " +
+                  std::to_string(P->offset + P->local_n) + ")");
+        return QVA_ERR_SIZE_MISMATCH;
+    }
+    const bool sharded = P->world > 1 && !P->replicated;
     if (row_ptr[0] != 0 || (uint64_t)row_ptr[rows] != nnz) {
-        set_error("row_ptr[0] must be 0 and row_ptr[dim] == nnz");
+        set_error("row_ptr[0] must be 0 and row_ptr[rows] == nnz");
         return QVA_ERR_SIZE_MISMATCH;
     }
     // ||W||_1 = max_j sum_i |w_ij| = max row abs sum for symmetric W (reading R13); validate
     double norm1 = 0.0;
-    for (uint64_t r = 0; r < rows; ++r) {
+    qva_status bad = QVA_OK;
+    for (uint64_t r = 0; r < rows && bad == QVA_OK; ++r) {
         if (row_ptr[r + 1] < row_ptr[r]) {
             set_error("row_ptr not monotone");
-            return QVA_ERR_INVALID_ARGUMENT;
+            bad = QVA_ERR_INVALID_ARGUMENT;
+            break;
         }
-        double s = 0.0;
+        double sum = 0.0;
         for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
-            if (col[k] < 0 || (uint64_t)col[k] >= rows) {
+            if (col[k] < 0 || (uint64_t)col[k] >= P->N) {
                 set_error("column index out of range");
-                return QVA_ERR_INVALID_ARGUMENT;
+                bad = QVA_ERR_INVALID_ARGUMENT;
+                break;
             }
             double v = val ? val[k] : 1.0;
             if (!std::isfinite(v)) {
                 set_error("non-finite matrix entry");
-                return QVA_ERR_NUMERIC;
+                bad = QVA_ERR_NUMERIC;
+                break;
             }
-            s += fabs(v);
+            sum += fabs(v);
         }
-        norm1 = std::max(norm1, s);
+        norm1 = std::max(norm1, sum);
     }
     DeviceGuard dg(P->device);
+    if (sharded) {  // every rank joins the collectives below even when its own rows were rejected
+        double v[3] = {norm1, bad == QVA_OK ? 0.0 : 1.0, 0.0};
+        QVA_TRY(coll_allreduce_host(P, v, 3, kCollMax));
+        if (bad != QVA_OK) return bad;
+        if (v[1] != 0.0) {
+            set_error("another rank rejected its rows of W");
+            return QVA_ERR_INVALID_ARGUMENT;
+        }
+        norm1 = v[0];
+    } else if (bad != QVA_OK) {
+        return bad;
+    }
     SparseMixer &sm = P->sm;
     cudaFree(sm.row_ptr);
     cudaFree(sm.col);
@@ -3118,11 +3197,70 @@ qva_status qva_set_sparse_mixer(qva_plan *P, const int64_t *row_ptr, const int32
         QVA_CUDA_TRY(cudaMalloc(&sm.val, std::max<uint64_t>(nnz, 1) * sizeof(double)));
         if (nnz) QVA_CUDA_TRY(cudaMemcpyAsync(sm.val, val, nnz * sizeof(double), cudaMemcpyHostToDevice, P->stream));
     }
-    if (!sm.t0) QVA_CUDA_TRY(cudaMalloc(&sm.t0, rows * sizeof(double2)));
-    if (!sm.t1) QVA_CUDA_TRY(cudaMalloc(&sm.t1, rows * sizeof(double2)));
+    // Taylor buffers: the largest partition's length on every rank (the gather fallback moves
+    // equal slices)
+    uint64_t stride = rows;
+    if (sharded) {
+        uint64_t n0, o0;
+        qva_partition(P->N, P->world, 0, &n0, &o0);  // rank 0 holds the largest block (R16)
+        stride = n0;
+    }
+    if (!sm.t0) QVA_CUDA_TRY(cudaMalloc(&sm.t0, std::max<uint64_t>(stride, 1) * sizeof(double2)));
+    if (!sm.t1) QVA_CUDA_TRY(cudaMalloc(&sm.t1, std::max<uint64_t>(stride, 1) * sizeof(double2)));
     sm.nnz = nnz;
     sm.rows = rows;
     sm.norm1 = norm1;
+    if (sharded && sm.src.G == 1) {  // first call: map the peers' Taylor buffers (collective)
+        SpmvSource src;
+        src.G = P->world;
+        for (int r = 0; r <= P->world; ++r) {
+            uint64_t n_r, o_r;
+            if (r < P->world) {
+                qva_partition(P->N, P->world, r, &n_r, &o_r);
+                src.off[r] = o_r;
+            } else {
+                src.off[r] = P->N;
+            }
+        }
+        const size_t hb = sizeof(cudaIpcMemHandle_t);
+        std::vector<unsigned char> mine(2 * hb, 0), all(2 * hb * P->world, 0);
+        bool ok = fuse_exchange_enabled() && P->world <= kMaxPeers &&
+                  cudaIpcGetMemHandle((cudaIpcMemHandle_t *)mine.data(), sm.t0) == cudaSuccess &&
+                  cudaIpcGetMemHandle((cudaIpcMemHandle_t *)(mine.data() + hb), sm.t1) == cudaSuccess;
+        cudaGetLastError();
+        unsigned char *stage = nullptr;
+        QVA_CUDA_TRY(scratch_get(P, (void **)&stage, (P->world + 1) * 2 * hb));
+        ok = (coll_allgather_host(P, mine.data(), all.data(), 2 * hb, stage) == QVA_OK) && ok;
+        for (int t = 0; ok && t < P->world; ++t)
+            for (int k = 0; ok && k < 2; ++k) {
+                if (t == P->rank) {
+                    src.peer[k][t] = k ? sm.t1 : sm.t0;
+                    continue;
+                }
+                cudaIpcMemHandle_t h;
+                memcpy(&h, all.data() + (2 * t + k) * hb, hb);
+                void *ptr = nullptr;
+                ok = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+                src.peer[k][t] = (const double2 *)ptr;
+            }
+        cudaGetLastError();
+        double flag = ok ? 1.0 : 0.0;
+        if (coll_allreduce_host(P, &flag, 1, kCollMin) != QVA_OK) flag = 0.0;
+        if (flag == 1.0) {
+            sm.peer_ok = true;
+        } else {  // unmap what was mapped; gather each term instead
+            for (int k = 0; k < 2; ++k)
+                for (int t = 0; t < P->world; ++t)
+                    if (t != P->rank && src.peer[k][t]) cudaIpcCloseMemHandle((void *)src.peer[k][t]);
+            memset(src.peer, 0, sizeof(src.peer));
+            cudaGetLastError();
+            QVA_CUDA_TRY(cudaMalloc(&sm.gather_buf, (size_t)P->world * stride * sizeof(double2)));
+            src.gathered = sm.gather_buf;
+        }
+        src.stride = stride;
+        sm.src = src;
+        if (!P->host_tp && !P->d_bar) QVA_CUDA_TRY(cudaMalloc(&P->d_bar, sizeof(int)));
+    }
     QVA_TRY(sync(P));
     P->sparse_set = true;
     return QVA_OK;
@@ -3347,7 +3485,9 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
         }
         int terms = 0;
         PlanObserver obs(P);
-        QVA_TRY(sparse_apply_mixer(P->sm, P->psi, theta[2 * k + 1], P->stream, &obs, &terms));
+        PlanSparseComm comm(P);
+        QVA_TRY(sparse_apply_mixer(P->sm, P->psi, theta[2 * k + 1], P->stream, &obs, &terms,
+                                   (P->world > 1 && !P->replicated) ? &comm : nullptr));
     }
     return QVA_OK;
 }
@@ -3731,6 +3871,7 @@ qva_status qva_plan_query(const qva_plan *P, int32_t what, int64_t *out) {
         case 4: *out = P->rank; return QVA_OK;
         case 5: *out = (int64_t)P->xfer_bytes; return QVA_OK;
         case 6: *out = P->parity_tile_ran ? 1 : 0; return QVA_OK;
+        case 7: *out = P->sm.peer_ok ? 1 : 0; return QVA_OK;
         default: set_error("qva_plan_query: unknown query"); return QVA_ERR_INVALID_ARGUMENT;
     }
 }

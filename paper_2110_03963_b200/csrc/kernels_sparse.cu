@@ -43,11 +43,25 @@ __device__ __forceinline__ void block_max2(double &a, double &b, double *red) {
     }
 }
 
-// t_out = (-i h/k) W t_in ; F += t_out ; per-block (|t_out|_inf, |F|_inf)
+// entry c of the term vector: local (one shard), a peer's IPC-mapped slice, or the gathered copy
+__device__ __forceinline__ double2 term_entry(const double2 *__restrict__ t_in, const SpmvSource &S, int which,
+                                              uint64_t c) {
+    if (S.G == 1) return __ldg(t_in + c);
+    int r = 0;
+#pragma unroll
+    for (int k = 1; k < kMaxPeers; ++k) r += (k < S.G && c >= S.off[k]) ? 1 : 0;
+    const uint64_t l = c - S.off[r];
+    if (S.gathered) return __ldg(S.gathered + (uint64_t)r * S.stride + l);
+    return S.peer[which][r][l];  // NVLink / same-device peer read (not through the read-only path)
+}
+
+// t_out = (-i h/k) W t_in ; F += t_out ; per-block (|t_out|_inf, |F|_inf).  Rows are this rank's
+// rows; columns are global indices (row-partitioned W: remote entries read from the peers).
 __global__ void __launch_bounds__(kSpmvThreads)
 spmv_taylor_kernel(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                    const double *__restrict__ val, const double2 *__restrict__ t_in, double2 *__restrict__ t_out,
-                   double2 *__restrict__ F, uint64_t rows, double coef, double *__restrict__ scratch) {
+                   double2 *__restrict__ F, uint64_t rows, double coef, double *__restrict__ scratch,
+                   const __grid_constant__ SpmvSource S, int which) {
     __shared__ double red[2 * (kSpmvThreads / 32)];
     double mt = 0.0, mf = 0.0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
@@ -56,7 +70,7 @@ spmv_taylor_kernel(const int64_t *__restrict__ row_ptr, const int32_t *__restric
         const int64_t e = row_ptr[i + 1];
         for (int64_t k = row_ptr[i]; k < e; ++k) {
             double w = val ? __ldg(val + k) : 1.0;
-            double2 x = __ldg(t_in + __ldg(col + k));
+            double2 x = term_entry(t_in, S, which, (uint64_t)__ldg(col + k));
             ar = fma(w, x.x, ar);
             ai = fma(w, x.y, ai);
         }
@@ -106,9 +120,9 @@ __global__ void inf_norm_kernel(const double2 *v, uint64_t n, double *scratch) {
 }  // namespace
 
 qva_status sparse_apply_mixer(SparseMixer &sm, double2 *psi, double beta, cudaStream_t s, LaunchObserver *obs,
-                              int *terms_used) {
+                              int *terms_used, SparseComm *comm) {
     *terms_used = 0;
-    if (beta == 0.0 || sm.rows == 0) return QVA_OK;
+    if (beta == 0.0 || (sm.rows == 0 && !comm)) return QVA_OK;
     const uint64_t rows = sm.rows;
     int blocks = (int)std::min<uint64_t>((rows + kSpmvThreads - 1) / kSpmvThreads, (uint64_t)num_sms() * 8);
     if (blocks < 1) blocks = 1;
@@ -135,13 +149,18 @@ qva_status sparse_apply_mixer(SparseMixer &sm, double2 *psi, double beta, cudaSt
         double host[2];
         QVA_CUDA_TRY(cudaMemcpyAsync(host, d_out, sizeof(host), cudaMemcpyDeviceToHost, s));
         QVA_CUDA_TRY(cudaStreamSynchronize(s));
+        // row-partitioned W: the global maxima; the collective also orders every rank's T_0 copy
+        // before any rank's first SpMV reads it (and, below, term k's writes before term k+1's reads)
+        if (comm) QVA_TRY(comm->max2(host));
         double prev = host[0];
         bool converged = false;
         double2 *tin = sm.t0, *tout = sm.t1;
+        int which = 0;  // tin is buffer t0 (0) or t1 (1) on every rank
         for (int k = 1; k <= kMaxTerms; ++k) {
+            if (comm && sm.src.gathered) QVA_TRY(comm->gather(tin, sm.gather_buf, sm.src.stride));
             obs->begin(K_SPMV, bytes_per_spmv);
             spmv_taylor_kernel<<<blocks, kSpmvThreads, 0, s>>>(sm.row_ptr, sm.col, sm.val, tin, tout, psi, rows,
-                                                               h / k, sm.scratch);
+                                                               h / k, sm.scratch, sm.src, which);
             max_reduce_kernel<<<1, 1024, 0, s>>>(sm.scratch, blocks, d_out);
             obs->end();
             cudaError_t e = cudaGetLastError();
@@ -151,6 +170,7 @@ qva_status sparse_apply_mixer(SparseMixer &sm, double2 *psi, double beta, cudaSt
             }
             QVA_CUDA_TRY(cudaMemcpyAsync(host, d_out, sizeof(host), cudaMemcpyDeviceToHost, s));
             QVA_CUDA_TRY(cudaStreamSynchronize(s));
+            if (comm) QVA_TRY(comm->max2(host));
             ++*terms_used;
             if (!std::isfinite(host[0]) || !std::isfinite(host[1])) {
                 set_error("Taylor action produced non-finite values");
@@ -162,6 +182,7 @@ qva_status sparse_apply_mixer(SparseMixer &sm, double2 *psi, double beta, cudaSt
             }
             prev = host[0];
             std::swap(tin, tout);
+            which ^= 1;
         }
         if (!converged) {
             set_error("truncated Taylor action did not converge in 40 terms");

@@ -374,19 +374,42 @@ cudaError_t launch_block_transpose(T *out, const T *in, uint64_t A, uint64_t B, 
 // ---------------------------------------------------------------------------------------------
 // sparse (CSR truncated Taylor) mixer (kernels_sparse.cu)
 // ---------------------------------------------------------------------------------------------
+// Where the SpMV finds the entries of the Taylor term vector it multiplies: this process's own
+// buffer (one shard), the IPC-mapped buffers of every rank (row-partitioned W over world > 1
+// ranks: column c lives on the rank whose partition [off[r], off[r+1]) holds it), or a gathered
+// copy of the whole vector (fallback without IPC, rank r's slice at r * stride).
+struct SpmvSource {
+    int G = 1;                               // 1: local buffer only
+    uint64_t off[kMaxPeers + 1] = {};        // partition offsets (COMM-psi, qva_partition)
+    const double2 *peer[2][kMaxPeers] = {};  // [Taylor buffer t0 / t1][rank] (IPC-mapped)
+    const double2 *gathered = nullptr;       // fallback: all ranks' slices at rank * stride
+    uint64_t stride = 0;
+};
 struct SparseMixer {
     int64_t *row_ptr = nullptr;
     int32_t *col = nullptr;
     double *val = nullptr;   // nullptr: all ones
     uint64_t nnz = 0;
-    uint64_t rows = 0;
-    double norm1 = 0.0;      // ||W||_1 (W symmetric: max row abs sum)
-    double2 *t0 = nullptr, *t1 = nullptr;  // Taylor term buffers
+    uint64_t rows = 0;       // rows held here (this rank's partition of a row-partitioned W)
+    double norm1 = 0.0;      // ||W||_1 (W symmetric: max row abs sum; global over ranks)
+    double2 *t0 = nullptr, *t1 = nullptr;  // Taylor term buffers (rows elements)
     double *scratch = nullptr;             // per-block maxima
     int scratch_blocks = 0;
+    SpmvSource src;                        // world > 1: where remote columns are read
+    double2 *gather_buf = nullptr;         // fallback gather buffer (G * stride elements)
+    bool peer_ok = false;                  // src.peer holds IPC mappings (to close in destroy)
 };
-// psi <- exp(-i beta W) psi.  terms_used receives the total number of SpMVs.
+// Collectives a row-partitioned mixer needs between Taylor terms (api.cu implements them on the
+// plan's transport): the global max of two doubles (which also orders every rank's SpMV before
+// any next one) and, without IPC, the all-gather of a term vector.
+struct SparseComm {
+    virtual qva_status max2(double *v) = 0;
+    virtual qva_status gather(const double2 *local, double2 *all, uint64_t stride) = 0;
+    virtual ~SparseComm() {}
+};
+// psi <- exp(-i beta W) psi.  terms_used receives the total number of SpMVs.  comm == nullptr:
+// single shard.
 qva_status sparse_apply_mixer(SparseMixer &sm, double2 *psi, double beta, cudaStream_t s, LaunchObserver *obs,
-                              int *terms_used);
+                              int *terms_used, SparseComm *comm = nullptr);
 
 }  // namespace qva

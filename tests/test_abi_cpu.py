@@ -207,7 +207,10 @@ def test_plan_argument_errors(Q):
         Q.Plan(721, "circulant", world=2, rank=0)  # sharded QWOA needs shards | dim
     assert ei.value.status == 5
     with pytest.raises(Q.QvaError) as ei:
-        Q.Plan(720, "sparse", world=2, rank=0)  # sharded sparse mixer: replicated mode only
+        Q.Plan(720, "sparse", virtual_shards=2)  # sparse mixer: row blocks over real ranks only
+    assert ei.value.status == 5
+    with pytest.raises(Q.QvaError) as ei:
+        Q.Plan(1 << 12, "parity", n_qubits=12, world=2, rank=0)  # sharded QAOAz: replicated mode only
     assert ei.value.status == 5
 
 

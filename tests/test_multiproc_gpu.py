@@ -4,8 +4,10 @@ Each process is one rank of a real multi-process plan (qva_plan_create_ex with w
 every real-rank branch runs: the IPC-handle all-gather and min-vote at plan creation, the pass
 stores into the peers' IPC-mapped buffers (COMM-psi exchange fused into the preceding pass,
 PAPER.md:356-370), the barrier after it, the <Q> / batch all-reduces (COMM-grad_f,
-PAPER.md:374-389), the circulant row/column transposes fused into the FFT pass stores, and --
-with QVA_FUSE_EXCHANGE=0 -- the send/recv exchange and transpose fallbacks.  NCCL refuses two
+PAPER.md:374-389), the circulant row/column transposes fused into the FFT pass stores, the
+row-partitioned sparse mixer whose SpMV reads remote columns from the peers' IPC-mapped Taylor
+buffers (the paper's distributed SpMV), and -- with QVA_FUSE_EXCHANGE=0 --
+the send/recv exchange, transpose and term-gather fallbacks.  NCCL refuses two
 ranks on one device, so the plan's few collectives run over a host transport (torch gloo,
 TorchHostTransport); the data path stays device-to-device through CUDA IPC.  No kernel waits on
 another rank's kernel (every cross-rank ordering is a host-side barrier after a stream
@@ -147,6 +149,46 @@ def _rank_checks(rank, world):
         for b in range(len(ths)):
             _f_close(f[b], O.expectation(O.evolve_x(n2, q2, ths[b]), q2))
 
+    # ---- generic sparse mixer with W partitioned by rows (the paper's distributed SpMV) ----
+    def rows_csr(W, lo, hi):
+        rp, cols, vals = [0], [], []
+        for r in range(lo, hi):
+            nz = np.nonzero(W[r])[0]
+            cols += list(nz)
+            vals += list(W[r, nz])
+            rp.append(len(cols))
+        return np.array(rp, np.int64), np.array(cols, np.int32), np.array(vals, np.float64)
+
+    N4 = 1000  # not a power of two: the partition remainder goes to the lowest ranks (R16)
+    rng = np.random.default_rng(4242)
+    W = np.where(rng.uniform(size=(N4, N4)) < 0.01, rng.uniform(-1, 1, (N4, N4)), 0.0)
+    W = np.triu(W, 1)
+    W = W + W.T
+    q4 = rng.standard_normal(N4)
+    th4 = rng.uniform(0, math.pi, 4)
+    ref4 = O.evolve_sparse_dense(q4, W, th4)
+    with Q.Plan(N4, "sparse", rank=rank, world=world, transport=T) as P:
+        ln, off = P.get_partition()
+        rp, cc, vv = rows_csr(W, off, off + ln)
+        P.set_sparse_mixer_rows(rp, cc, vv, row_offset=off)
+        res["s_peer"] = P.query("sparse_peer")
+        P.set_qualities(q4[off:off + ln], offset=off)
+        P.evolve(th4)
+        res["s_damp"] = _amp_close(P.get_state(), ref4[off:off + ln])
+        _f_close(P.expectation(), O.expectation(ref4, q4), O.expectation(ref4, np.abs(q4)))
+    # the hypercube (sum_j X_j) as a row-partitioned CSR equals the X mixer (P12 cross-check)
+    n5 = 12
+    X = O.dense_sum_x(n5)
+    q5 = O.maxcut_q(n5, *random_regular_graph(n5, 3, rng))
+    th5 = rng.uniform(0, math.pi, 4)
+    with Q.Plan(1 << n5, "sparse", rank=rank, world=world, transport=T) as P:
+        ln, off = P.get_partition()
+        rp, cc, vv = rows_csr(X, off, off + ln)
+        P.set_sparse_mixer_rows(rp, cc, None, row_offset=off)
+        P.set_qualities(q5[off:off + ln], offset=off)
+        P.evolve(th5)
+        _amp_close(P.get_state(), O.evolve_x(n5, q5, th5)[off:off + ln])
+
     # ---- circulant (QWOA) sharded by rows: cfg3, N = 10!, two transposes per layer (C5) ----
     wl = make_config("cfg3")
     ref3 = O.evolve_complete(wl.q, wl.theta, wl.lam0, wl.lam_rest)
@@ -176,3 +218,4 @@ def test_world_gt1_plans_on_one_gpu(_gpu, world, fuse):
         # the fused path must really be the one that ran (IPC mapping succeeded on every rank)
         assert out[r]["x_fused"] == (1 if fuse else 0), out[r]
         assert out[r]["c_fused"] == (1 if fuse else 0), out[r]
+        assert out[r]["s_peer"] == (1 if fuse else 0), out[r]
