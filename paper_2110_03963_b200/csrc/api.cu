@@ -1730,6 +1730,11 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         tp.work_ctr = (g_dyn == 1 || (g_dyn > 1 && ((g_dyn >> 1) >> j) & 1)) ? P->d_ctr + j : nullptr;
         tp.expect = pp.expect ? 1 : 0;
         tp.partials = P->partials;
+        static int g_tail = [] {
+            const char *e = getenv("QVA_TAIL");
+            return e ? atoi(e) : 0;
+        }();
+        tp.tail_mode = g_tail;
         tp.apply_scale = apply_scale[j] == 1 ? 1 : 0;
         tp.fold_scale_gf = apply_scale[j] == 2 ? 1 : 0;
         // last step touching shared memory: a group switch (smem transpose) or the phase (q stage)

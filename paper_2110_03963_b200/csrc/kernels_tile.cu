@@ -568,8 +568,8 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     // A claimed item past the end is a sentinel: the barrier completes with no data and the
     // consumer stops.  Per warpgroup (iteration parity) the claims happen in iteration order, so
     // once a warpgroup meets a sentinel every later iteration of it is one too.
-    auto issue = [&](uint32_t j) {
-        const uint64_t item = dyn ? atomicAdd(P.work_ctr, 1ull) : item_of(j);
+    auto issue = [&](uint32_t j, uint64_t claim = ~0ull) {
+        const uint64_t item = dyn ? (claim != ~0ull ? claim : atomicAdd(P.work_ctr, 1ull)) : item_of(j);
         const uint64_t member = item >> P.log2_tiles, t = item & (P.n_tiles - 1);
         const int s = j % STAGES;
         const uint32_t bar = full_bar(j);
@@ -635,9 +635,20 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     double acc = 0.0, nrm = 0.0;
     int64_t acc_member = -1;
 
+    const bool preclaim = dyn && (P.tail_mode & 1), defer = (P.tail_mode & 2) != 0;
+    uint32_t pending = ~0u;
+    uint64_t pending_claim = ~0ull;
+    auto flush_pending = [&]() {
+        if (c == 0 && pending != ~0u) {
+            bulk_wait_read_all();
+            issue(pending, pending_claim);
+            pending = ~0u;
+        }
+    };
     for (uint32_t it = wg; dyn || it < n_it; it += kWG) {
         const int s = it % STAGES;
         uint64_t item;
+        flush_pending();
         if (dyn) {
             mbar_wait(full_bar(it), ((it / STAGES) >> 1) & 1);
             item = items_s[slot_of(it)];
@@ -660,13 +671,15 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
         const uint32_t buf = smem_u32(psi_s + (size_t)s * kTile);
         const unsigned char *qs = q_s + (size_t)s * QSB;
         if (!dyn) mbar_wait(full_bar(it), ((it / STAGES) >> 1) & 1);
+        uint64_t pre_claim = ~0ull;
+        if (preclaim && c == 0) pre_claim = atomicAdd(P.work_ctr, 1ull);
 
         // hand stage s back: the whole warpgroup is done with it, so one thread refills it with
         // iteration it + STAGES (the async-proxy write must follow our generic-proxy accesses)
         auto release = [&]() {
             fence_proxy_async();
             wg_sync(wg);
-            if (c == 0 && (dyn || it + STAGES < n_it)) issue(it + STAGES);
+            if (c == 0 && (dyn || it + STAGES < n_it)) issue(it + STAGES, pre_claim);
         };
         double2 v[kAPT];
         if (!load_psi) {
@@ -686,7 +699,10 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                 auto body = [&](auto gc) {
                     constexpr int G = decltype(gc)::value;
                     if (prev != G) {
-                        if (prev >= 0) wg_sync(wg);
+                        if (prev >= 0) {
+                            flush_pending();
+                            wg_sync(wg);
+                        }
                         smem_read_g<G>(v, buf, c);
                     }
                     if constexpr (G <= 2) {
@@ -721,6 +737,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
                 if constexpr (K == 0) {
                     if (load_psi) smem_read_g<G>(v, buf, c);
                 } else if constexpr (prog_def<PROG>().g[K - 1] != G) {
+                    flush_pending();
                     wg_sync(wg);
                     smem_read_g<G>(v, buf, c);
                 }
@@ -768,14 +785,22 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             } else {
                 smem_write_g<prog_def<PROG>().g[prog_def<PROG>().n - 1]>(v, buf, c);
             }
+            flush_pending();
             fence_proxy_async();
             wg_sync(wg);
             if (c == 0) {
                 int cc[5];
                 tma_coords(P, member, t, cc);
                 tma_store_5d(&tmap_out, buf, cc);
-                bulk_wait_read_all();
-                if (dyn || it + STAGES < n_it) issue(it + STAGES);
+                if (defer) {
+                    if (dyn || it + STAGES < n_it) {
+                        pending = it + STAGES;
+                        pending_claim = pre_claim;
+                    }
+                } else {
+                    bulk_wait_read_all();
+                    if (dyn || it + STAGES < n_it) issue(it + STAGES, pre_claim);
+                }
             }
             continue;
         }
@@ -810,6 +835,7 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
             __stcs(dst + o, v[e]);
         }
     }
+    flush_pending();
     if (tstore && c == 0) bulk_wait_all();
     if (P.xg) __threadfence_system();  // peer stores visible before the host-side barrier
     if (QB > 0 && kExpect && P.expect && acc_member >= 0) flush_partial(P, acc_member, warp, lane, acc, nrm);

@@ -121,6 +121,8 @@ struct TilePassParams {
     int expect;              // accumulate partial <Q> and norm in the final group (== gq)
     int qmin, ntab;
     int apply_scale;
+    int tail_mode;           // measurement switch QVA_TAIL (bit 0: claim the refill's tile at the start
+                             // of a tile; bit 1: defer the store-read wait + refill to the next barrier)
     int fold_scale_gf;       // fp64 factorised generated phase: multiply the per-member G factors by
                              // angles[member].scale instead of every amplitude (apply_scale = 0)
     int tma_store;           // 1: write the tile back with a TMA tensor store (strided tile sets)
