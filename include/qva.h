@@ -92,9 +92,10 @@ typedef struct {
                                 circulant mixer with a spectrum set by
                                 qva_set_circulant_eigenvalues_const (lambda_0, c, ..., c): apply it
                                 in closed form, U psi = e^{-i beta c} psi + (e^{-i beta lambda_0} -
-                                e^{-i beta c}) mean(psi) (one 40-B pass per layer, single shard;
-                                an O(N) speed-of-light reference for the FFT path; the
-                                FFT stays the default).  Others must be 0. */
+                                e^{-i beta c}) mean(psi) (one 40-B pass per layer; on a row-
+                                sharded state one 16-B all-reduce of sum(psi) per layer, SURVEY
+                                C6; an O(N) speed-of-light reference for the FFT path, SURVEY K10;
+                                the FFT stays the default).  Others must be 0. */
 } qva_plan_desc;
 
 /* ---- lifecycle (Table 1 plan / destroy) ------------------------------------ */

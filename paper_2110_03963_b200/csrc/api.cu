@@ -851,6 +851,27 @@ qva_status coll_allgather_dev(qva_plan *P, const void *src, void *dst, size_t by
     return QVA_OK;
 }
 
+// in-place sum over ranks of n device doubles (NCCL on the stream; host transport via host memory)
+qva_status coll_allreduce_dev(qva_plan *P, double *dev, int n) {
+    if (P->world == 1) return QVA_OK;
+    if (P->host_tp) {
+        std::vector<double> h(n);
+        QVA_CUDA_TRY(cudaMemcpyAsync(h.data(), dev, n * sizeof(double), cudaMemcpyDeviceToHost, P->stream));
+        QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
+        QVA_TRY(tp_check(P->tp.allreduce_f64(P->tp.ctx, h.data(), (uint64_t)n, kCollSum), "allreduce"));
+        QVA_CUDA_TRY(cudaMemcpyAsync(dev, h.data(), n * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+        QVA_CUDA_TRY(cudaStreamSynchronize(P->stream));
+        return QVA_OK;
+    }
+    QVA_NCCL_TRY(ncclAllReduce(dev, dev, n, ncclDouble, ncclSum, P->comm, P->stream));
+    return QVA_OK;
+}
+struct PlanCompleteComm : CompleteComm {
+    qva_plan *P;
+    explicit PlanCompleteComm(qva_plan *P_) : P(P_) {}
+    qva_status sum2_dev(double *dev2) override { return coll_allreduce_dev(P, dev2, 2); }
+};
+
 // collectives of the row-partitioned sparse mixer (SparseComm, kernels_sparse.cu)
 struct PlanSparseComm : SparseComm {
     qva_plan *P;
@@ -2014,7 +2035,7 @@ qva_status expect_generic(qva_plan *P, const double2 *psi, uint64_t n, const dou
 // opt-in closed form of the complete-graph-family circulant (desc.reserved[4], kernels_complete.cu):
 // single shard, spectrum given as (lambda_0, c) by qva_set_circulant_eigenvalues_const
 bool use_complete_closed_form(const qva_plan *P) {
-    return P->mixer == QVA_MIXER_CIRCULANT && P->d.reserved[4] != 0 && P->lam_const && P->G == 1;
+    return P->mixer == QVA_MIXER_CIRCULANT && P->d.reserved[4] != 0 && P->lam_const;
 }
 
 bool use_small(const qva_plan *P) { return P->mixer == QVA_MIXER_X && P->n <= kSmallMaxQubits && P->G == 1; }
@@ -2419,8 +2440,9 @@ qva_status apply_mixer_impl(qva_plan *P, double beta) {
         PlanObserver obs(P);
         if (use_complete_closed_form(P)) {
             double *scr = nullptr;
-            QVA_CUDA_TRY(scratch_get(P, (void **)&scr, complete_scratch_doubles(P->N) * sizeof(double)));
-            return complete_run(r, P->N, scr, P->stream, &obs);
+            QVA_CUDA_TRY(scratch_get(P, (void **)&scr, complete_scratch_doubles(P->arr_n) * sizeof(double)));
+            PlanCompleteComm cc(P);
+            return complete_run(r, P->arr_n, P->N, scr, P->stream, &obs, P->world > 1 ? &cc : nullptr);
         }
         if (P->G > 1) {
             PlanShardIO io(P);
@@ -3435,8 +3457,9 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
         PlanObserver obs(P);
         if (use_complete_closed_form(P)) {
             double *scr = nullptr;
-            QVA_CUDA_TRY(scratch_get(P, (void **)&scr, complete_scratch_doubles(P->N) * sizeof(double)));
-            QVA_TRY(complete_run(r, P->N, scr, P->stream, &obs));
+            QVA_CUDA_TRY(scratch_get(P, (void **)&scr, complete_scratch_doubles(P->arr_n) * sizeof(double)));
+            PlanCompleteComm cc(P);
+            QVA_TRY(complete_run(r, P->arr_n, P->N, scr, P->stream, &obs, P->world > 1 ? &cc : nullptr));
         } else if (P->G > 1) {
             PlanShardIO io(P);
             QVA_TRY(circ_shard_setup(P, io));

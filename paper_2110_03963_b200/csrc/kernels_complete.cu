@@ -88,17 +88,24 @@ __global__ void __launch_bounds__(kCThreads) complete_pass_kernel(double2 *psi, 
 }
 
 // (a, d) of U(beta) from the per-block sums of the state it acts on: a = e^{-i beta c},
-// d = (e^{-i beta lambda_0} - a) * sum / N.  One block, fixed summation order.
+// d = (e^{-i beta lambda_0} - a) * sum / N.  One block, fixed summation order.  mode 1: only the
+// sum, into ad[2] (sharded: reduced over ranks before mode 2); mode 2: (a, d) from ad[2].
 __global__ void complete_coef_kernel(const double *partials, int nblocks, double beta, double lam0, double lamc,
-                                     double invN, double2 *ad) {
+                                     double invN, double2 *ad, int mode) {
     __shared__ double red[2 * 32];
     double s0 = 0.0, s1 = 0.0;
-    for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
-        s0 += partials[2 * i];
-        s1 += partials[2 * i + 1];
+    if (mode == 2) {
+        s0 = ad[2].x;
+        s1 = ad[2].y;
+    } else {
+        for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
+            s0 += partials[2 * i];
+            s1 += partials[2 * i + 1];
+        }
+        creduce2(s0, s1, red);
     }
-    creduce2(s0, s1, red);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && mode == 1) ad[2] = make_double2(s0, s1);
+    if (threadIdx.x == 0 && mode != 1) {
         double sc, cc, s0l, c0l;
         sincos(-beta * lamc, &sc, &cc);
         sincos(-beta * lam0, &s0l, &c0l);
@@ -118,13 +125,14 @@ int complete_grid(uint64_t n) {
 
 }  // namespace
 
-size_t complete_scratch_doubles(uint64_t n) { return 2 * (size_t)complete_grid(n) + 4; }
+size_t complete_scratch_doubles(uint64_t n) { return 2 * (size_t)complete_grid(n) + 6; }
 
-qva_status complete_run(const FftRun &r, uint64_t n, double *scratch, cudaStream_t s, LaunchObserver *obs) {
+qva_status complete_run(const FftRun &r, uint64_t n, uint64_t n_global, double *scratch, cudaStream_t s,
+                        LaunchObserver *obs, CompleteComm *comm) {
     const int grid = complete_grid(n);
     double *partials = scratch;
     double2 *ad = reinterpret_cast<double2 *>(scratch + 2 * (size_t)grid);
-    const double invN = 1.0 / (double)n;
+    const double invN = 1.0 / (double)n_global;
     auto pass = [&](int init, const double2 *pend, int do_phase, double gamma, int mode) -> qva_status {
         const double bytes = (init ? 0.0 : 16.0 * n) + 16.0 * n + ((do_phase || mode == 1) ? 8.0 * n : 0.0);
         obs->begin(K_OTHER, bytes);
@@ -140,7 +148,17 @@ qva_status complete_run(const FftRun &r, uint64_t n, double *scratch, cudaStream
     };
     auto coef = [&](double beta) -> qva_status {
         obs->begin(K_REDUCE, 16.0 * grid);
-        complete_coef_kernel<<<1, 1024, 0, s>>>(partials, grid, beta, r.lam0, r.lamc, invN, ad);
+        if (!comm) {
+            complete_coef_kernel<<<1, 1024, 0, s>>>(partials, grid, beta, r.lam0, r.lamc, invN, ad, 0);
+        } else {  // row-sharded state: the sum of psi over every rank (16 B all-reduce)
+            complete_coef_kernel<<<1, 1024, 0, s>>>(partials, grid, beta, r.lam0, r.lamc, invN, ad, 1);
+            qva_status st = comm->sum2_dev(reinterpret_cast<double *>(ad + 2));
+            if (st != QVA_OK) {
+                obs->end();
+                return st;
+            }
+            complete_coef_kernel<<<1, 32, 0, s>>>(partials, grid, beta, r.lam0, r.lamc, invN, ad, 2);
+        }
         cudaError_t e = cudaGetLastError();
         obs->end();
         if (e != cudaSuccess) {

@@ -349,7 +349,13 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
 // complete-graph-family spectrum (lambda_0, c, ..., c) in closed form (kernels_complete.cu; opt-in
 // ablation, desc.reserved[4]): p + 1 passes of 40 B per amplitude; scratch: complete_scratch_doubles(n)
 size_t complete_scratch_doubles(uint64_t n);
-qva_status complete_run(const FftRun &r, uint64_t n, double *scratch, cudaStream_t s, LaunchObserver *obs);
+// sharded state: in-place sum over ranks of 2 doubles on the device, stream-ordered
+struct CompleteComm {
+    virtual qva_status sum2_dev(double *dev2) = 0;
+    virtual ~CompleteComm() {}
+};
+qva_status complete_run(const FftRun &r, uint64_t n, uint64_t n_global, double *scratch, cudaStream_t s,
+                        LaunchObserver *obs, CompleteComm *comm = nullptr);
 // sharded four-step: r.psi is this process's row block(s) in natural order (local * N/G)
 struct FftShardIO {
     int G = 1, local = 1, first = 0;  // shards, shards held by this process, global index of local 0

@@ -200,6 +200,14 @@ def _rank_checks(rank, world):
         P.evolve(wl.theta)
         res["c_damp"] = _amp_close(P.get_state(), ref3[off:off + ln])
         _f_close(P.expectation(), O.expectation(ref3, wl.q), scale=float(np.sum(np.abs(ref3) ** 2 * np.abs(wl.q))))
+    # the K_N closed form on the same row-sharded state: one 16-B all-reduce of sum(psi) per layer
+    with Q.Plan(wl.dim, "circulant", rank=rank, world=world, transport=T, complete_closed_form=True) as P:
+        ln, off = P.get_partition()
+        P.set_qualities(wl.q[off:off + ln], offset=off)
+        P.set_circulant_eigenvalues_const(wl.lam0, wl.lam_rest)
+        P.evolve(wl.theta)
+        _amp_close(P.get_state(), ref3[off:off + ln])
+        _f_close(P.expectation(), O.expectation(ref3, wl.q), scale=float(np.sum(np.abs(ref3) ** 2 * np.abs(wl.q))))
     return res
 
 
