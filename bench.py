@@ -371,6 +371,9 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # CUDA events around every launch, on the plan's stream, in the timed region; switched on before
+    # the warm-up so that the evaluation's replayed CUDA graph already carries them (event nodes)
+    plan.set_profiling(True)
     for _ in range(args.warmup):
         step()
     barrier()
@@ -379,7 +382,6 @@ def main():
     clocks.start()
     time.sleep(0.3)
     plan.reset_kernel_stats()
-    plan.set_profiling(True)  # CUDA events around every launch, on the plan's stream, in the timed region
     l0 = plan.launch_count()
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)

@@ -515,7 +515,10 @@ struct qva_plan {
         size_t rec_bytes;
         std::vector<double> thr_h, G_h;   // host staging (kept alive with the entry)
         std::vector<int> thr_hi, G_hi;
+        void *codes = nullptr;             // consumer-order uint8 codes built from the records (lazily)
+        int64_t born = 0;                  // run_passes call that created the entry
     };
+    int64_t pass_seq = 0;                  // run_passes calls so far (code copies: reused q only)
     std::vector<GenEntry> gen_cache;
     // device buffers of dropped q copies / records, reused by size (a new q every step must not
     // pay cudaFree's device synchronisation and cudaMalloc's mapping cost)
@@ -1083,6 +1086,7 @@ void drop_qt(qva_plan *P) {
         pool_put(P, e.rec, e.rec_bytes);
         pool_put(P, e.thr, 128 * 8 * sizeof(double));
         pool_put(P, e.G, 32 * sizeof(double));
+        pool_put(P, e.codes, P->arr_n);
     }
     P->gen_cache.clear();
 }
@@ -1229,6 +1233,18 @@ int qgen_mode(const qva_plan *P, int batch) {
     return use_qgen(P) && (gen_int || f64_ok) ? (gen_int ? kQGenInt : kQGenF64) : 0;
 }
 
+// unit-weight generated q read as consumer-order uint8 codes (m <= 255) built once per q and pass
+// shape from the records, instead of assembling cut(x) per element in every pass (QVA_QGEN_CODES=0:
+// in-pass generation); single members (batches keep the in-pass generator: one code copy would serve
+// them too, but their passes are compute-bound, not memory-bound)
+bool gen_codes_mode(const qva_plan *P, int gen, int batch) {
+    static int env = [] {
+        const char *e = getenv("QVA_QGEN_CODES");
+        return e ? atoi(e) : 1;
+    }();
+    return env != 0 && gen == kQGenInt && P->g_m <= 255 && batch == 1;
+}
+
 // logical qubit of every physical bit of the arrays a pass reads (n_phys bits) and the logical
 // bits that are constant on this process (global qubits of a real shard = its rank bits)
 void pass_layout(const qva_plan *P, const PassPlan &pp, int n_phys, std::vector<int> &lay, uint64_t &cmask,
@@ -1276,6 +1292,7 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
             pool_put(P, e.rec, e.rec_bytes);
             pool_put(P, e.thr, 128 * 8 * sizeof(double));
             pool_put(P, e.G, 32 * sizeof(double));
+            pool_put(P, e.codes, P->arr_n);
             P->gen_cache.erase(P->gen_cache.begin() + i);
             break;
         }
@@ -1352,6 +1369,7 @@ qva_status ensure_gen(qva_plan *P, const std::vector<int> &qkey, const PassPlan 
     ent.wset = wts ? wset : -1;
     if (wts) ent.wsig.assign(wts, wts + P->g_m);
     ent.rec = ent.thr = ent.G = nullptr;
+    ent.born = P->pass_seq;
     ent.rec_bytes = n_tiles * rec_bytes;
     QVA_CUDA_TRY(pool_get(P, &ent.rec, ent.rec_bytes));
     QVA_CUDA_TRY(pool_get(P, &ent.thr, 128 * 8 * sizeof(double)));
@@ -1549,6 +1567,7 @@ static double host_ms() {
 
 qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const double *thetas, int p, int batch,
                       double2 *psi_base, uint64_t stride, int init_mode, double *expect_out /*[batch][2] host*/) {
+    ++P->pass_seq;
     const double hp0 = g_hostprof ? host_ms() : 0.0;
     double hp_first = -1.0;
     int n_tile_passes = 0;
@@ -1722,6 +1741,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
                 if (e.key == qkey && e.qbytes == qbytes) pref = e.group;
         if (pp.parity) build_parity_steps(pp, tp);
         else build_steps(pp, tp, pref, half1[j], half2[j]);
+        int launch_qb = 0;  // q mode of this launch when it differs from the sequence's (generated codes)
         if (needs_q && gen) {
             const qva_plan::GenEntry *ge = nullptr;
             if (P->ex_w && pp.phase >= 0 && pp.expect) {
@@ -1730,6 +1750,28 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             }
             QVA_TRY(ensure_gen(P, qkey, pp, n_phys, tp.gq, gen, tp, (P->ex_w && pp.phase >= 0) ? pp.phase : -1, &ge));
             tp.qt = ge->rec;
+            // phase passes read 1-B codes built from the records (stored-code pass); an expectation-only
+            // pass keeps the in-pass generator (A/B, cfg4: 5.19 vs 5.34 ms -- it is memory-bound)
+            // (built only for a q that outlived the evolution that made its records: a q set anew for
+            // every evaluation keeps the in-pass generator, the cheaper one when used once)
+            if (pp.phase >= 0 && gen_codes_mode(P, gen, batch) && ge->born < P->pass_seq) {
+                qva_plan::GenEntry *gm = const_cast<qva_plan::GenEntry *>(ge);
+                if (!gm->codes && P->graph_stage) {
+                    // never built inside a graph capture (the replays would rebuild them): the capture
+                    // is dropped, the uncaptured rerun builds them and a later call captures the
+                    // code-reading passes
+                    P->graph_capture_dirty = true;
+                } else {
+                    if (!gm->codes) {
+                        QVA_CUDA_TRY(pool_get(P, &gm->codes, P->arr_n));
+                        ProfScope ps(P, K_OTHER, (double)P->arr_n);
+                        QVA_CUDA_TRY(launch_gen_codes(gm->codes, gm->rec, P->arr_n >> kTileBits, gm->thr, gm->G,
+                                                      kGroups[tp.gq], P->g_m, P->stream));
+                    }
+                    tp.qt = gm->codes;
+                    launch_qb = 1;
+                }
+            }
             tp.gen_thr = ge->thr;
             tp.gen_G = ge->G;
             tp.gen_m = P->g_m;
@@ -1822,7 +1864,8 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             QVA_CUDA_TRY(cudaMemsetAsync(P->partials, 0, (size_t)nslot * batch * 2 * sizeof(double), P->stream));
         {
             ProfScope ps(P, K_TILE, bytes);
-            QVA_CUDA_TRY(launch_tile_pass(map, map_out, tp, needs_q ? qbytes : 0, prog, grid, P->stream));
+            QVA_CUDA_TRY(launch_tile_pass(map, map_out, tp, needs_q ? (launch_qb ? launch_qb : qbytes) : 0, prog, grid,
+                                          P->stream));
             if (g_hostprof && hp_first < 0) hp_first = host_ms() - hp0;
         }
         first = false;

@@ -841,6 +841,39 @@ tile_pass_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant
     if (QB > 0 && kExpect && P.expect && acc_member >= 0) flush_partial(P, acc_member, warp, lane, acc, nrm);
 }
 
+// Consumer-order uint8 codes j = m - cut(x) of generated unit-weight MaxCut qualities (q = -cut,
+// qmin = -m), written once per (q, pass shape, register group) from the same per-tile records and
+// per-thread constants the in-pass generator uses: the passes then read 1 B per amplitude through
+// the stored-code path (QB = 1) instead of assembling cut(x) per element (A/B on one B200, cfg4:
+// the two phase passes 6.35 -> 5.80 ms each).  Layout as qt_gather_kernel: thread c's codes 16 per
+// 16-byte chunk at chunk index (e / 16) * kCT + c.
+__global__ void gen_codes_kernel(uint8_t *codes, const unsigned char *rec, uint64_t n_tiles, const int *thr,
+                                 const int *Gv, TileGroup g, int m) {
+    const uint64_t total = n_tiles * kCT;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = k / kCT;
+        const int c = (int)(k % kCT);
+        int cst[6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) cst[i] = thr[c * 8 + i];
+        int S, al[5];
+        gen_coeffs<kQGenInt>(rec + t * 16, g, c, cst, S, al);
+        uint4 out[2];
+        uint32_t *w = reinterpret_cast<uint32_t *>(out);
+        static_for<kAPT>([&](auto ec) {
+            constexpr int E = decltype(ec)::value;
+            const int cut = gen_cut<kQGenInt, E>(S, al, Gv);
+            const uint32_t j = (uint32_t)(m - cut) & 0xffu;
+            if constexpr ((E & 3) == 0) w[E >> 2] = j;
+            else w[E >> 2] |= j << (8 * (E & 3));
+        });
+        uint4 *dst = reinterpret_cast<uint4 *>(codes + t * (uint64_t)kTile);
+        dst[c] = out[0];
+        dst[kCT + c] = out[1];
+    }
+}
+
 // logical index of physical index x under a layout given as bit runs (LayoutRuns)
 __device__ __forceinline__ uint64_t layout_map(const LayoutRuns &R, uint64_t x) {
     uint64_t y = 0;
@@ -1163,6 +1196,15 @@ cudaError_t launch_qt_gather(void *dst, const void *src, int qbytes, const TileP
         qt_gather_kernel<int16_t>
             <<<blocks, 256, 0, s>>>((int16_t *)dst, (const int16_t *)src, p, g, n_tiles, qmin, lay);
     else qt_gather_kernel<int8_t><<<blocks, 256, 0, s>>>((int8_t *)dst, (const int8_t *)src, p, g, n_tiles, qmin, lay);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_codes(void *codes, const void *rec, uint64_t n_tiles, const void *thr, const void *G,
+                             const TileGroup &g, int m, cudaStream_t s) {
+    const uint64_t total = n_tiles * kCT;
+    int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)num_sms() * 16);
+    gen_codes_kernel<<<blocks, 256, 0, s>>>((uint8_t *)codes, (const unsigned char *)rec, n_tiles, (const int *)thr,
+                                            (const int *)G, g, m);
     return cudaGetLastError();
 }
 

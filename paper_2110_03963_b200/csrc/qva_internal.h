@@ -236,6 +236,9 @@ struct GenPrep {
     const double *tb_w;
 };
 cudaError_t launch_gen_records(void *rec, uint64_t n_tiles, int fp64, const GenPrep &g, cudaStream_t s);
+// consumer-order uint8 codes (m - cut) of a unit-weight generated q from its records (gen_codes_kernel)
+cudaError_t launch_gen_codes(void *codes, const void *rec, uint64_t n_tiles, const void *thr, const void *G,
+                             const TileGroup &g, int m, cudaStream_t s);
 // out[logical(x)] = in[x] (restores the natural layout of a permuted state)
 cudaError_t launch_permute_copy(double2 *out, const double2 *in, uint64_t n, const LayoutRuns &lay, cudaStream_t s);
 // phase tables tab[b][j] = exp(-i gammas[b] (qmin + j)) * mult[b], j < ntab (same fp64 sincos as

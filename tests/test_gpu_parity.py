@@ -176,6 +176,7 @@ def test_graph_replay_survives_buffer_growth(Q):
     q = O.maxcut_q(n, u, v)
     with Q.Plan(1 << n, "x", n_qubits=n, max_batch=3) as P:
         P.set_qualities_maxcut(u, v)
+        P.set_profiling(True)  # graphs then carry per-launch event nodes (bench.py's timed region)
         for _ in range(3):  # warm, capture, replay
             th = rng.uniform(0, math.pi, 4)
             P.evolve(th)
@@ -202,12 +203,15 @@ def test_graph_replay_survives_buffer_growth(Q):
         P.evolve(thw)
         _f_close(P.expectation(), O.expectation(O.evolve_x(n, qw, thw), qw))
         P.set_qualities_maxcut(u, v)
+        P.reset_kernel_stats()
         for _ in range(3):  # back to the first key: must re-capture, not replay stale buffers
             th = rng.uniform(0, math.pi, 4)
             P.evolve(th)
             ref = O.evolve_x(n, q, th)
             _f_close(P.expectation(), O.expectation(ref, q))
         _amp_close(P.get_state(), ref)
+        st = P.kernel_stats("tile")  # every launch timed, replayed or not: 5 tile passes per p=2 evolution
+        assert st["launches"] == 15 and st["ms"] > 0, st
 
 
 def test_tile_path_p0_and_norm(Q):
