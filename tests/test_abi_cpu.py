@@ -248,3 +248,27 @@ def test_parity_window_schedule(Q, n, seed):
             for g2, (c, d) in groups:
                 if g2 < g and {c, d} & {a, b}:
                     assert pos[frozenset((c, d))] < pos[key]
+
+
+def test_create_ex_transport_validation(Q):
+    """qva_plan_create_ex rejects a host transport with a missing function before touching a device
+    (include/qva.h); a complete one gets as far as the device (no GPU here: a CUDA error)."""
+    import ctypes
+    d = Q.PlanDesc()
+    d.dim, d.n_qubits, d.mixer, d.rank, d.world = 1 << 14, 14, 0, 0, 2
+    h = ctypes.c_void_p()
+    t = Q.Transport()  # all NULL
+    st = Q.lib().qva_plan_create_ex(ctypes.byref(d), ctypes.byref(t), ctypes.byref(h))
+    assert st == 1 and not h.value
+    assert b"transport" in Q.lib().qva_last_error()
+
+
+def test_sparse_rows_partition_rule(Q):
+    """qva_set_sparse_mixer_rows takes this rank's COMM-psi rows: the host partition rule gives
+    contiguous blocks covering [0, dim) with the remainder on the lowest ranks (R16)."""
+    for N, world in ((1000, 2), (1000, 4), (1000, 3), (7, 4)):
+        parts = [Q.qva_partition(N, world, r) for r in range(world)]
+        assert sum(n for n, _ in parts) == N
+        assert parts[0][1] == 0
+        for (n0, o0), (n1, o1) in zip(parts, parts[1:]):
+            assert o1 == o0 + n0 and n0 >= n1
