@@ -106,9 +106,11 @@ typedef struct {
  * handles and maps every peer's (the fused peer-store exchange); if any rank
  * fails to map, all ranks fall back to NCCL send/recv (decided by a min-vote).
  * QVA_ERR_UNSUPPORTED: X mixer with dim != 2^n_qubits, world / shard count not a power of two
- * for the X mixer, sharded parity mixers or virtual shards of a sparse mixer (use the replicated
- * mode for their batches), a sharded circulant dim with no split M1*M2 that the shard count
- * divides.  A world > 1 sparse plan holds a row block of W (qva_set_sparse_mixer_rows). */
+ * for the X mixer or a world > 1 parity mixer, fewer than 12 local qubits, virtual shards of a
+ * sparse or parity mixer, a sharded circulant dim with no split M1*M2 that the shard count
+ * divides.  A world > 1 sparse plan holds a row block of W (qva_set_sparse_mixer_rows); a world > 1
+ * parity (QAOAz) plan runs the pair terms that touch a rank qubit as peer passes over the other
+ * ranks' IPC-mapped state buffers (QVA_ERR_UNSUPPORTED at evolve if they could not be mapped). */
 qva_status qva_plan_create(const qva_plan_desc *desc, qva_plan **out);
 
 /* Host transport of a world > 1 plan: the caller's own process group (e.g. torch.distributed over

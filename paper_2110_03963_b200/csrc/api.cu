@@ -65,6 +65,16 @@ struct PassPlan {
     std::vector<PassStep> psteps;
 };
 
+struct ParityWinPlan {
+    std::vector<int> bits;            // window bits (ascending, physical = logical here)
+    std::vector<int> ta, tb, cls;     // its pair terms in application order; cls 0 odd, 1 even, 2 last
+};
+struct ParityItem {              // sharded QAOAz schedule: a window of local bits or one global term
+    bool global = false;
+    ParityWinPlan win;
+    int a = -1, b = -1;
+};
+
 static std::vector<std::vector<int>> make_tile_sets(int L) {
     std::vector<std::vector<int>> sets;
     std::vector<int> s0;
@@ -590,6 +600,9 @@ struct qva_plan {
     std::map<int, std::vector<PassPlan>> parity_tile_sched;  // tile-pass schedule per p (parity_tile_passes)
     std::vector<int> parity_tile_seq;      // the sequence it was built for
     bool parity_tile_ran = false;          // the last parity evolution ran as tile passes
+    std::vector<ParityItem> parity_shard_items;           // sharded QAOAz schedule (one layer)
+    std::vector<std::vector<PassStep>> parity_shard_steps;  // its window step lists
+    std::vector<int> parity_shard_seq;
     // sparse
     SparseMixer sm;
     bool sparse_set = false;
@@ -2018,7 +2031,8 @@ void close_peer_maps(qva_plan *P) {
 }
 
 void setup_peer_exchange(qva_plan *P) {
-    if (!fuse_exchange_enabled() || P->world > kMaxPeers || !P->psi || !P->psi_alt || (!P->comm && !P->host_tp))
+    if ((!fuse_exchange_enabled() && P->mixer != QVA_MIXER_PARITY) || P->world > kMaxPeers || !P->psi ||
+        !P->psi_alt || (!P->comm && !P->host_tp))
         return;
     P->ipc_own[0] = P->psi;
     P->ipc_own[1] = P->psi_alt;
@@ -2182,10 +2196,84 @@ qva_status circ_shard_setup(qva_plan *P, PlanShardIO &io) {
 // 128-B rows) each take, greedily in group order, every term whose qubits fit and whose
 // predecessors are done or earlier in the same window: one HBM round trip per window instead of
 // one per term (default sequence, n = 28: 5 windows for 27 terms).
-struct ParityWinPlan {
-    std::vector<int> bits;            // window bits (ascending, physical = logical here)
-    std::vector<int> ta, tb, cls;     // its pair terms in application order; cls 0 odd, 1 even, 2 last
-};
+static std::vector<ParityWinPlan> parity_window_plan(int n, const std::vector<int> &s);
+// Sharded state (qubits >= nl are rank bits): windows over local bits take the ready local terms
+// (as parity_window_plan); when no local term is ready, every ready term touching a rank qubit
+// becomes one peer pass.  One layer of the mixer.
+static std::vector<ParityItem> parity_shard_items(int n, int nl, const std::vector<int> &s) {
+    const int K = (int)s.size();
+    std::vector<std::pair<int, int>> terms;
+    std::vector<int> grp;
+    for (int m = 0; m + 1 < K; m += 2) terms.push_back({s[m], s[m + 1]}), grp.push_back(0);
+    for (int m = 1; m + 1 < K; m += 2) terms.push_back({s[m], s[m + 1]}), grp.push_back(1);
+    if (K >= 3 && (K & 1)) terms.push_back({s[K - 1], s[0]}), grp.push_back(2);
+    const int T = (int)terms.size();
+    std::vector<std::vector<int>> deps(T);
+    for (int k = 0; k < T; ++k)
+        for (int j = 0; j < k; ++j)
+            if (grp[j] < grp[k] && (terms[j].first == terms[k].first || terms[j].first == terms[k].second ||
+                                    terms[j].second == terms[k].first || terms[j].second == terms[k].second))
+                deps[k].push_back(j);
+    auto local = [&](int k) { return terms[k].first < nl && terms[k].second < nl; };
+    std::vector<char> done(T, 0);
+    std::vector<ParityItem> out;
+    const int wmax = std::min(nl, kWinMaxBits);
+    for (int left = T; left > 0;) {
+        std::vector<char> inw(n, 0), placed(T, 0);
+        int w = 0;
+        for (int b = 0; b < std::min(3, nl); ++b) inw[b] = 1, ++w;
+        std::vector<int> plan;
+        for (int k = 0; k < T && (int)plan.size() < kWinMaxPairs; ++k) {
+            if (done[k] || !local(k)) continue;
+            bool ready = true;
+            for (int j : deps[k]) ready = ready && (done[j] || placed[j]);
+            if (!ready) continue;
+            const int need = !inw[terms[k].first] + !inw[terms[k].second];
+            if (w + need > wmax) continue;
+            inw[terms[k].first] = inw[terms[k].second] = 1;
+            w += need;
+            placed[k] = 1;
+            plan.push_back(k);
+        }
+        if (!plan.empty()) {
+            for (int b = 0; b < nl && w < wmax; ++b)
+                if (!inw[b]) inw[b] = 1, ++w;
+            ParityItem it;
+            for (int b = 0; b < nl; ++b)
+                if (inw[b]) it.win.bits.push_back(b);
+            for (int k : plan) {
+                it.win.ta.push_back(terms[k].first);
+                it.win.tb.push_back(terms[k].second);
+                it.win.cls.push_back(grp[k]);
+                done[k] = 1;
+            }
+            left -= (int)plan.size();
+            out.push_back(it);
+            continue;
+        }
+        int got = 0;
+        std::vector<int> ready_g;
+        for (int k = 0; k < T; ++k) {
+            if (done[k] || local(k)) continue;
+            bool ready = true;
+            for (int j : deps[k]) ready = ready && done[j];
+            if (ready) ready_g.push_back(k);
+        }
+        for (int k : ready_g) {
+            ParityItem it;
+            it.global = true;
+            it.a = terms[k].first;
+            it.b = terms[k].second;
+            out.push_back(it);
+            done[k] = 1;
+            ++got;
+        }
+        left -= got;
+        if (!got) return {};  // cannot happen: some term is always ready
+    }
+    return out;
+}
+
 static std::vector<ParityWinPlan> parity_window_plan(int n, const std::vector<int> &s) {
     const int K = (int)s.size();
     std::vector<std::pair<int, int>> terms;
@@ -2238,42 +2326,49 @@ static std::vector<ParityWinPlan> parity_window_plan(int n, const std::vector<in
     return out;
 }
 
+// A window plan as run tables for the register-free parity_window_kernel on a state of n bits.
+// false if too fragmented for the run tables (the caller takes the per-term passes).
+static bool parity_window_of(int n, const ParityWinPlan &P, ParityWindow &W) {
+    std::vector<char> inw(n, 0);
+    for (int b : P.bits) inw[b] = 1;
+    memset(&W, 0, sizeof(W));
+    W.n = n;
+    W.w = (int)P.bits.size();
+    std::vector<int> local(n, -1);
+    for (int i = 0; i < (int)P.bits.size(); ++i) local[P.bits[i]] = i;
+    auto runs = [&](bool in_window, int *src, int *wd, int *dst, int cap, int &nr) {
+        nr = 0;
+        int idx = 0;  // running index in the window (or the tile number)
+        for (int b = 0; b < n;) {
+            if ((bool)inw[b] != in_window) { ++b; continue; }
+            int st = b;
+            while (b < n && (bool)inw[b] == in_window) ++b;
+            if (nr == cap) return false;
+            src[nr] = idx;
+            wd[nr] = b - st;
+            dst[nr] = st;
+            idx += b - st;
+            ++nr;
+        }
+        return true;
+    };
+    if (!runs(true, W.in_src, W.in_w, W.in_dst, kWinMaxRuns, W.n_in) ||
+        !runs(false, W.out_src, W.out_w, W.out_dst, kWinMaxRuns + 1, W.n_out))
+        return false;
+    W.np = (int)P.ta.size();
+    for (int i = 0; i < W.np; ++i) {
+        W.pa[i] = (int8_t)local[P.ta[i]];
+        W.pb[i] = (int8_t)local[P.tb[i]];
+    }
+    return true;
+}
+
 // Windows of <= 12 physical bits for the register-free parity_window_kernel.
 static std::vector<ParityWindow> parity_windows(int n, const std::vector<int> &s) {
     std::vector<ParityWindow> out;
     for (const ParityWinPlan &P : parity_window_plan(n, s)) {
-        std::vector<char> inw(n, 0);
-        for (int b : P.bits) inw[b] = 1;
         ParityWindow W;
-        memset(&W, 0, sizeof(W));
-        W.n = n;
-        W.w = (int)P.bits.size();
-        std::vector<int> local(n, -1);
-        for (int i = 0; i < (int)P.bits.size(); ++i) local[P.bits[i]] = i;
-        auto runs = [&](bool in_window, int *src, int *wd, int *dst, int cap, int &nr) {
-            nr = 0;
-            int idx = 0;  // running index in the window (or the tile number)
-            for (int b = 0; b < n;) {
-                if ((bool)inw[b] != in_window) { ++b; continue; }
-                int st = b;
-                while (b < n && (bool)inw[b] == in_window) ++b;
-                if (nr == cap) return false;
-                src[nr] = idx;
-                wd[nr] = b - st;
-                dst[nr] = st;
-                idx += b - st;
-                ++nr;
-            }
-            return true;
-        };
-        if (!runs(true, W.in_src, W.in_w, W.in_dst, kWinMaxRuns, W.n_in) ||
-            !runs(false, W.out_src, W.out_w, W.out_dst, kWinMaxRuns + 1, W.n_out))
-            return {};  // too fragmented for the run tables: the caller takes the per-term passes
-        W.np = (int)P.ta.size();
-        for (int i = 0; i < W.np; ++i) {
-            W.pa[i] = (int8_t)local[P.ta[i]];
-            W.pb[i] = (int8_t)local[P.tb[i]];
-        }
+        if (!parity_window_of(n, P, W)) return {};
         out.push_back(W);
     }
     return out;
@@ -2395,10 +2490,157 @@ static bool parity_tile_passes(int n, int L, int G, const std::vector<int> &s, i
     return true;
 }
 
+qva_status reset_state(qva_plan *P);
+qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const double *thetas, int p, int batch,
+                      double2 *psi_base, uint64_t stride, int init_mode, double *expect_out);
+// QAOAz on a sharded state (world > 1; rank = the top g qubits).  Per layer the items of
+// parity_shard_items: windows of local bits run as tile passes (pair terms on register groups,
+// phase fused into the layer's first window, <Q> into the last), and each term touching a rank
+// qubit runs as one peer pass that reads the partner rank's IPC-mapped buffer (parity_peer_kernel),
+// after a barrier (every rank's previous writes are done).  t_only != nullptr: one mixer step on the
+// current state (no phase, no expectation).
+static qva_status parity_sharded_run(qva_plan *P, const double *theta, int p, bool *have_red, const double *t_only) {
+    *have_red = false;
+    if (!P->ipc_ok) {
+        set_error("sharded QAOAz mixer needs the peers' buffers mapped (CUDA IPC)");
+        return QVA_ERR_UNSUPPORTED;
+    }
+    if (P->parity_shard_seq != P->parity_seq) {
+        P->parity_shard_items = parity_shard_items(P->n, P->L, P->parity_seq);
+        P->parity_shard_steps.assign(P->parity_shard_items.size(), {});
+        for (size_t i = 0; i < P->parity_shard_items.size(); ++i) {  // no steps: the register-free path
+            const ParityItem &it = P->parity_shard_items[i];
+            if (it.global) continue;
+            if ((int)it.win.bits.size() != kTileBits || tile_tma_dims(it.win.bits.data(), P->L, nullptr) > 5 ||
+                !parity_group_steps(it.win, P->parity_shard_steps[i]))
+                P->parity_shard_steps[i].clear();
+        }
+        P->parity_shard_seq = P->parity_seq;
+    }
+    const auto &items = P->parity_shard_items;
+    if (items.empty()) {
+        set_error("sharded QAOAz: no window plan for this qubit sequence");
+        return QVA_ERR_UNSUPPORTED;
+    }
+    std::vector<double> th1;
+    if (t_only) {
+        th1 = {0.0, *t_only};
+        theta = th1.data();
+        p = 1;
+    }
+    const bool evolving = t_only == nullptr;
+    bool first = evolving;  // the evolution's first pass starts from |+> / psi0
+    std::vector<PassPlan> run;
+    auto flush = [&]() -> qva_status {
+        if (run.empty()) return QVA_OK;
+        QVA_TRY(run_passes(P, run, theta, p, 1, P->psi, 0, first ? (P->has_psi0 ? 2 : 1) : 0, nullptr));
+        first = false;
+        run.clear();
+        return QVA_OK;
+    };
+    for (int k = 0; k < p; ++k) {
+        bool phase_pending = evolving;
+        for (size_t i = 0; i < items.size(); ++i) {
+            const ParityItem &it = items[i];
+            const bool last = evolving && k == p - 1 && i + 1 == items.size();
+            if (!it.global && !P->parity_shard_steps[i].empty()) {
+                PassPlan pp;
+                pp.parity = true;
+                pp.tbits = it.win.bits;
+                pp.play = k;
+                pp.psteps = P->parity_shard_steps[i];
+                if (phase_pending) {
+                    pp.phase = k;
+                    pp.psteps.front().phase = 1;
+                    phase_pending = false;
+                }
+                pp.expect = last;
+                if (pp.expect && pp.phase >= 0 && pp.psteps.back().group != pp.psteps.front().group) {
+                    PassStep e;
+                    memset(&e, 0, sizeof(e));
+                    e.group = pp.psteps.front().group;
+                    pp.psteps.push_back(e);
+                }
+                if ((int)pp.psteps.size() > kMaxSteps) {
+                    set_error("sharded QAOAz: window pass has too many steps");
+                    return QVA_ERR_UNSUPPORTED;
+                }
+                run.push_back(pp);
+                if (last) *have_red = true;
+                continue;
+            }
+            QVA_TRY(flush());
+            if (first) {
+                QVA_TRY(reset_state(P));
+                first = false;
+            }
+            if (!it.global) {  // a local window no tile plan covers: window kernel (phase fused), else per term
+                const double t = theta[2 * k + 1];
+                ParityWindow W;
+                if (parity_window_of(P->L, it.win, W)) {
+                    if (phase_pending) QVA_TRY(ensure_q_dev(P));
+                    W.c = cos(2.0 * t);
+                    W.s = sin(2.0 * t);
+                    W.q = phase_pending ? P->q : nullptr;
+                    W.gamma = theta[2 * k];
+                    phase_pending = false;
+                    ProfScope ps(P, K_OTHER, (32.0 + (W.q ? 8.0 : 0.0)) * P->arr_n);
+                    QVA_CUDA_TRY(launch_parity_window(P->psi, W, P->stream));
+                    continue;
+                }
+                if (phase_pending) {
+                    QVA_TRY(ensure_q_dev(P));
+                    ProfScope ps(P, K_OTHER, 40.0 * P->arr_n);
+                    QVA_CUDA_TRY(launch_phase(P->psi, P->q, P->arr_n, theta[2 * k], P->stream));
+                    phase_pending = false;
+                }
+                for (size_t m = 0; m < it.win.ta.size(); ++m) {
+                    ProfScope ps(P, K_OTHER, 32.0 * P->arr_n);
+                    QVA_CUDA_TRY(launch_parity_pair(P->psi, P->arr_n, it.win.ta[m], it.win.tb[m], t, P->stream));
+                }
+                continue;
+            }
+            if (phase_pending) {  // the layer opens with a rank-qubit term: a standalone phase
+                QVA_TRY(ensure_q_dev(P));
+                ProfScope ps(P, K_OTHER, 40.0 * P->arr_n);
+                QVA_CUDA_TRY(launch_phase(P->psi, P->q, P->arr_n, theta[2 * k], P->stream));  // layout A
+                phase_pending = false;
+            }
+            QVA_TRY(coll_stream_barrier(P));  // every rank's state is final before anyone reads it
+            ParityPeer pr{};
+            pr.L = P->L;
+            pr.rank = P->rank;
+            pr.a = it.a;
+            pr.b = it.b;
+            pr.c = cos(2.0 * theta[2 * k + 1]);
+            pr.s = sin(2.0 * theta[2 * k + 1]);
+            const int kb = (P->psi == P->ipc_own[0]) ? 0 : 1;  // every rank swaps in lockstep
+            for (int t = 0; t < P->world; ++t) pr.peer[t] = P->ipc_peer[kb][t];
+            {
+                ProfScope ps(P, K_EXCHANGE, 48.0 * P->arr_n);
+                QVA_CUDA_TRY(launch_parity_peer(P->psi_alt, P->psi, pr, P->stream));
+            }
+            std::swap(P->psi, P->psi_alt);
+            count_xfer(P, sizeof(double2) * 2);  // about half the elements read remotely
+        }
+    }
+    QVA_TRY(flush());
+    if (first) QVA_TRY(reset_state(P));  // p = 0: the initial state
+    return QVA_OK;
+}
+
 // one mixer step; q != nullptr also applies the phase exp(-i gamma q) first (fused into the
 // first window's loads)
-qva_status reset_state(qva_plan *P);
 qva_status parity_mix(qva_plan *P, double t, const double *q = nullptr, double gamma = 0.0, bool from_psi0 = false) {
+    if (P->world > 1 && !P->replicated) {  // sharded state
+        if (from_psi0) QVA_TRY(reset_state(P));
+        if (q) {
+            ProfScope ps(P, K_OTHER, 40.0 * P->arr_n);
+            QVA_CUDA_TRY(launch_phase(P->psi, q, P->arr_n, gamma, P->stream));
+        }
+        bool dummy = false;
+        return parity_sharded_run(P, nullptr, 1, &dummy, &t);
+    }
     const std::vector<int> &s = P->parity_seq;
     const int K = (int)s.size();
     static int win_env = [] {
@@ -2809,6 +3051,12 @@ qva_status qva_plan_create_ex(const qva_plan_desc *desc, const qva_transport *tr
             set_error("sharded circulant mixer needs dim divisible by the shard count");
             return QVA_ERR_UNSUPPORTED;
         }
+    } else if (G > 1 && d.mixer == QVA_MIXER_PARITY && vs == 1) {
+        // QAOAz over real ranks: windows of local bits + peer passes for rank-qubit terms
+        if (!is_pow2((uint64_t)G) || d.n_qubits - ilog2(G) < kTileBits) {
+            set_error("sharded QAOAz needs a power-of-two world and n_qubits - log2(world) >= 12");
+            return QVA_ERR_UNSUPPORTED;
+        }
     } else if (G > 1 && d.mixer == QVA_MIXER_SPARSE && vs == 1) {
         // row-partitioned W over real ranks (qva_set_sparse_mixer_rows): any dim, COMM-psi blocks
         if ((uint64_t)d.world > d.dim) {
@@ -2922,8 +3170,9 @@ qva_status qva_plan_create_ex(const qva_plan_desc *desc, const qva_transport *tr
             return fail(QVA_ERR_NCCL);
         }
     }
-    if (d.world > 1 && (d.mixer == QVA_MIXER_X || d.mixer == QVA_MIXER_CIRCULANT))
-        setup_peer_exchange(P);  // falls back to NCCL on failure
+    if (d.world > 1 && (d.mixer == QVA_MIXER_X || d.mixer == QVA_MIXER_CIRCULANT ||
+                        (d.mixer == QVA_MIXER_PARITY && !replicated)))
+        setup_peer_exchange(P);  // falls back to NCCL on failure (QAOAz: no fallback, see parity_sharded_run)
     if (reset_state(P) != QVA_OK) return fail(QVA_ERR_CUDA);
     if (cudaStreamSynchronize(P->stream) != cudaSuccess) {
         set_error("plan init failed");
@@ -3517,6 +3766,10 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
         if (p == 0) return reset_state(P);
         P->layout = 0;
         P->perm.clear();
+        if (P->world > 1 && !P->replicated) {
+            if (!use_qgen(P)) QVA_TRY(ensure_q_dev(P));
+            return parity_sharded_run(P, theta, p, have_red, nullptr);
+        }
         // tile passes (TMA pipeline, pair terms on register groups; QVA_PARITY_TILE=0: window kernel)
         static int tile_env = [] {
             const char *e = getenv("QVA_PARITY_TILE");

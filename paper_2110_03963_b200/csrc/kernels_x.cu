@@ -465,6 +465,36 @@ __global__ void parity_pair_kernel(double2 *__restrict__ psi, uint64_t quarter, 
     }
 }
 
+// A parity pair term exp(-i t (X_a X_b + Y_a Y_b)) whose qubits are not both local to the shard
+// (COMM-psi: rank = the top g index bits): element x of this rank pairs with
+// y = x ^ 2^a ^ 2^b when bits a and b of x differ, and y lives on rank y >> L.  Out of place (the
+// partner reads our old values too): out = c u - i s v with u = psi[x], v = the partner's value,
+// read straight from the owning rank's IPC-mapped buffer (NVLink) -- the pairwise half-slice
+// exchange of the paper done by the loads of the kernel itself.  00 / 11 elements copy through.
+__global__ void parity_peer_kernel(double2 *__restrict__ out, const double2 *__restrict__ in,
+                                   const __grid_constant__ ParityPeer P) {
+    const uint64_t nl = 1ull << P.L;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = ((uint64_t)P.rank << P.L) | i;
+        const double2 u = in[i];
+        if ((((x >> P.a) ^ (x >> P.b)) & 1) == 0) {
+            out[i] = u;
+            continue;
+        }
+        const uint64_t y = x ^ (1ull << P.a) ^ (1ull << P.b);
+        const int ry = (int)(y >> P.L);
+        const uint64_t j = y & (nl - 1);
+        const double2 v = ry == P.rank ? in[j] : P.peer[ry][j];
+        out[i] = make_double2(fma(P.c, u.x, P.s * v.y), fma(P.c, u.y, -P.s * v.x));
+    }
+}
+
+cudaError_t launch_parity_peer(double2 *out, const double2 *in, const ParityPeer &p, cudaStream_t s) {
+    const uint64_t nl = 1ull << p.L;
+    parity_peer_kernel<<<grid_for(nl, 256), 256, 0, s>>>(out, in, p);
+    return cudaGetLastError();
+}
+
 // Several parity pair terms in one HBM round trip: each CTA stages a window of 2^w amplitudes (the
 // physical bits P.bits, given as runs; bits 0..2 lead, so loads and stores move 128-B rows),
 // optionally applies the phase exp(-i gamma q_x) as it loads, then the listed pair rotations in

@@ -296,6 +296,14 @@ struct ParityWindow {
     double init_amp;                          // > 0: the window starts as init_amp (|+>, no load)
 };
 cudaError_t launch_parity_window(double2 *psi, const ParityWindow &p, cudaStream_t s);
+// a pair term with a global (rank) qubit on a sharded state: partner values read from the peers'
+// IPC-mapped buffers, out of place (parity_peer_kernel)
+struct ParityPeer {
+    int L, rank, a, b;                 // local bits; this rank; the pair's (logical = global index) bits
+    double c, s;                       // cos 2t, sin 2t
+    const double2 *peer[kMaxPeers];    // every rank's current state buffer (this rank's own included)
+};
+cudaError_t launch_parity_peer(double2 *out, const double2 *in, const ParityPeer &p, cudaStream_t s);
 // elementwise phase (generic dims, any mixer): psi *= exp(-i gamma q)
 cudaError_t launch_phase(double2 *psi, const double *q, uint64_t n, double gamma, cudaStream_t s);
 // psi = 1/sqrt(N)

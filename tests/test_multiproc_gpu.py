@@ -6,7 +6,9 @@ stores into the peers' IPC-mapped buffers (COMM-psi exchange fused into the prec
 PAPER.md:356-370), the barrier after it, the <Q> / batch all-reduces (COMM-grad_f,
 PAPER.md:374-389), the circulant row/column transposes fused into the FFT pass stores, the
 row-partitioned sparse mixer whose SpMV reads remote columns from the peers' IPC-mapped Taylor
-buffers (the paper's distributed SpMV), and -- with QVA_FUSE_EXCHANGE=0 --
+buffers (the paper's distributed SpMV), the QAOAz mixer on a sharded state
+(pair terms touching a rank qubit read the partner's IPC-mapped buffer), and -- with
+QVA_FUSE_EXCHANGE=0 --
 the send/recv exchange, transpose and term-gather fallbacks.  NCCL refuses two
 ranks on one device, so the plan's few collectives run over a host transport (torch gloo,
 TorchHostTransport); the data path stays device-to-device through CUDA IPC.  No kernel waits on
@@ -188,6 +190,34 @@ def _rank_checks(rank, world):
         P.set_qualities(q5[off:off + ln], offset=off)
         P.evolve(th5)
         _amp_close(P.get_state(), O.evolve_x(n5, q5, th5)[off:off + ln])
+
+    # ---- QAOAz (parity mixer) on a sharded state: windows of local bits as tile passes, every pair
+    # term touching a rank qubit as a peer pass reading the partner rank's IPC-mapped buffer ----
+    n6 = 16
+    rng = np.random.default_rng(606)
+    u6, v6 = random_regular_graph(n6, 3, rng)
+    q6 = O.maxcut_q(n6, u6, v6)
+    th6 = rng.uniform(0, math.pi, 4)
+    psi06 = np.zeros(1 << n6, np.complex128)
+    idx = [x for x in range(1 << n6) if bin(x).count("1") == 8][:200]
+    psi06[idx] = rng.standard_normal(len(idx)) + 1j * rng.standard_normal(len(idx))
+    psi06 /= np.linalg.norm(psi06)
+    for seq in (list(range(n6)), [15, 0, 7, 14, 3, 9, 12, 1, 13, 5]):
+        ref6 = O.evolve_parity(n6, q6, seq, th6, psi06)
+        with Q.Plan(1 << n6, "parity", n_qubits=n6, rank=rank, world=world, transport=T) as P:
+            ln, off = P.get_partition()
+            P.set_parity_mixer(seq)
+            P.set_qualities_maxcut(u6, v6)
+            P.set_initial_state(psi06[off:off + ln], offset=off)
+            P.evolve(th6)
+            _amp_close(P.get_state(), ref6[off:off + ln])
+            _f_close(P.expectation(), O.expectation(ref6, q6), O.expectation(ref6, np.abs(q6)))
+            P.set_qualities(q6[off:off + ln], offset=off)  # stored q
+            P.evolve(th6)
+            _amp_close(P.get_state(), ref6[off:off + ln])
+            P.reset_state()
+            P.apply_mixer(0.41)  # step-level mixer on the sharded state
+            _amp_close(P.get_state(), O.mixer_parity(psi06.copy(), seq, 0.41)[off:off + ln])
 
     # ---- circulant (QWOA) sharded by rows: cfg3, N = 10!, two transposes per layer (C5) ----
     wl = make_config("cfg3")
