@@ -522,6 +522,7 @@ def main():
             plan.evolve(th_host)
             return plan.expectation()
 
+        q_step()  # untimed warm-up: the graph -> stored q switch allocates q and its code buffers once
         ems2, wms2 = timed(q_step)
         e2e["host_q_variant"] = {"value": amp_layers / (ems2 * 1e-3), "unit": UNIT,
                                  "h2d_bytes_per_step": int(local_n * 8 + th_host.nbytes), "d2h_bytes_per_step": 8,

@@ -478,6 +478,7 @@ struct qva_plan {
     int q_mode = 0;                    // 0 fp64, 1 int8, 2 int16
     int qmin = 0, qmax = 0;
     void *qc = nullptr, *qcB = nullptr;
+    size_t qc_cap = 0, qcB_cap = 0;   // their sizes (reused across uploads: no free / malloc per q)
     bool qcB_valid = false;
     bool q_classified = false;
     double2 *d_tab = nullptr;
@@ -940,7 +941,13 @@ qva_status ensure_qB(qva_plan *P) {
     }
     if (P->q_mode && !P->qcB_valid) {
         int eb = P->q_mode == 1 ? 1 : 2;
-        if (!P->qcB) QVA_CUDA_TRY(cudaMalloc(&P->qcB, P->arr_n * eb));
+        if (P->qcB_cap < P->arr_n * eb) {
+            plan_free(P, P->qcB);
+            P->qcB = nullptr;
+            P->qcB_cap = 0;
+            QVA_CUDA_TRY(cudaMalloc(&P->qcB, P->arr_n * eb));
+            P->qcB_cap = P->arr_n * eb;
+        }
         uint64_t C = (1ull << P->L) / P->G;
         if (P->world == 1) {
             ProfScope ps(P, K_EXCHANGE, 2.0 * eb * (double)P->arr_n);
@@ -959,7 +966,16 @@ qva_status ensure_qB(qva_plan *P) {
 void drop_qt(qva_plan *P);
 qva_status ensure_q_dev(qva_plan *P);
 cudaError_t scratch_get(qva_plan *P, void **p, size_t bytes);
+static double host_ms();
+static int hostprof_env() {
+    static int v = [] {
+        const char *e = getenv("QVA_HOSTPROF");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
 qva_status classify_q(qva_plan *P) {
+    const double h0 = hostprof_env() ? host_ms() : 0.0;
     drop_qt(P);
     P->q_mode = 0;
     P->qcB_valid = false;
@@ -995,11 +1011,13 @@ qva_status classify_q(qva_plan *P) {
     if (lo >= -128 && hi <= 127) eb = 1;
     else if (lo >= -32768 && hi <= 32767) eb = 2;
     if (!eb) return QVA_OK;
-    plan_free(P, P->qc);
-    P->qc = nullptr;
-    QVA_CUDA_TRY(cudaMalloc(&P->qc, P->arr_n * eb));
-    plan_free(P, P->qcB);
-    P->qcB = nullptr;
+    if (P->qc_cap < P->arr_n * eb) {
+        plan_free(P, P->qc);
+        P->qc = nullptr;
+        P->qc_cap = 0;
+        QVA_CUDA_TRY(cudaMalloc(&P->qc, P->arr_n * eb));
+        P->qc_cap = P->arr_n * eb;
+    }
     {
         ProfScope ps(P, K_OTHER, (8.0 + eb) * P->arr_n);
         QVA_CUDA_TRY(launch_q_encode(P->q, P->arr_n, P->qc, eb, P->stream));
@@ -1007,7 +1025,9 @@ qva_status classify_q(qva_plan *P) {
     P->q_mode = eb == 1 ? 1 : 2;
     P->qmin = (int)lo;
     P->qmax = (int)hi;
-    return sync(P);
+    qva_status st = sync(P);
+    if (hostprof_env()) fprintf(stderr, "[qva] classify_q %.2f ms (host, incl. sync)\n", host_ms() - h0);
+    return st;
 }
 
 qva_status to_natural_perm(qva_plan *P);

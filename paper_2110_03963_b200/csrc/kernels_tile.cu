@@ -884,27 +884,46 @@ __device__ __forceinline__ uint64_t layout_map(const LayoutRuns &R, uint64_t x) 
 // q (fp64 or integer codes) permuted into the consumer order of register group G of tile set S:
 // dst[t][pos(tid, e)] = src[logical(phys(t, i(tid, e)))], pos as read by apply_phase_group /
 // accumulate_expect; `lay` maps the pass's physical layout to the logical index of q.
+// One thread per (tile t, consumer thread c) writes c's 32 values as whole 16-byte chunks.  Both
+// maps are bit maps (tile bit b -> physical bit tile_bits[b] -> logical bit), so the logical index
+// is the OR of the images of the set bits: the tile's coordinate part once per thread, the
+// thread's part once, and one OR per register element from five precomputed bit images (the
+// per-element bit loops this replaces made the 1-byte gathers compute-bound: ~10 ms per GiB).
 template <typename T>
 __global__ void qt_gather_kernel(T *dst, const T *src, const __grid_constant__ TilePassParams P, TileGroup G,
                                  uint64_t n_tiles, int qmin, const __grid_constant__ LayoutRuns lay) {
-    const uint64_t total = n_tiles * (uint64_t)kTile;
-    constexpr int PER = (sizeof(T) == 8) ? 2 : 16 / (int)sizeof(T);
+    constexpr int PER = 16 / (int)sizeof(T);  // values per 16-byte chunk
+    const uint64_t total = n_tiles * (uint64_t)kCT;
+    uint64_t eimg[kGroupBits];
+#pragma unroll
+    for (int j = 0; j < kGroupBits; ++j) eimg[j] = layout_map(lay, 1ull << P.tile_bits[G.ebit[j]]);
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
          k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t t = k >> kTileBits;
-        const int pos = (int)(k & (kTile - 1));
-        // invert pos = ((e / PER) * kCT + tid) * PER + e % PER
-        const int within = pos % PER, chunk = pos / PER;
-        const int tid = chunk % kCT, e = (chunk / kCT) * PER + within;
-        int i = 0;
-        for (int j = 0; j < kCT_BITS; ++j) i |= ((tid >> j) & 1) << G.tbit[j];
-        for (int j = 0; j < kGroupBits; ++j) i |= ((e >> j) & 1) << G.ebit[j];
+        const uint64_t t = k / kCT;
+        const int c = (int)(k % kCT);
         uint64_t phys = 0;
         for (int r = 0; r < P.n_runs; ++r) phys |= ((t >> P.run_src[r]) & ((1ull << P.run_w[r]) - 1)) << P.run_dst[r];
-        for (int b = 0; b < kTileBits; ++b) phys |= (uint64_t)((i >> b) & 1) << P.tile_bits[b];
-        const uint64_t x = layout_map(lay, phys);
-        if (sizeof(T) == 8) dst[k] = src[x];
-        else dst[k] = (T)((int)src[x] - qmin);  // integer codes stored as j = code - qmin
+        for (int j = 0; j < kCT_BITS; ++j) phys |= (uint64_t)((c >> j) & 1) << P.tile_bits[G.tbit[j]];
+        const uint64_t base = layout_map(lay, phys);
+        T *out = dst + t * (uint64_t)kTile;
+#pragma unroll
+        for (int ch = 0; ch < kAPT / PER; ++ch) {
+            union {
+                uint4 u;
+                T v[PER];
+            } w;
+#pragma unroll
+            for (int r = 0; r < PER; ++r) {
+                const int e = ch * PER + r;
+                uint64_t x = base;
+#pragma unroll
+                for (int j = 0; j < kGroupBits; ++j)
+                    if ((e >> j) & 1) x |= eimg[j];
+                if (sizeof(T) == 8) w.v[r] = src[x];
+                else w.v[r] = (T)((int)src[x] - qmin);  // integer codes stored as j = code - qmin
+            }
+            reinterpret_cast<uint4 *>(out)[ch * kCT + c] = w.u;
+        }
     }
 }
 
@@ -1188,7 +1207,7 @@ cudaError_t launch_tile_pass(const CUtensorMap &map, const CUtensorMap &map_out,
 
 cudaError_t launch_qt_gather(void *dst, const void *src, int qbytes, const TilePassParams &p, const TileGroup &g,
                              uint64_t n_tiles, int qmin, const LayoutRuns &lay, cudaStream_t s) {
-    const uint64_t total = n_tiles * (uint64_t)kTile;
+    const uint64_t total = n_tiles * (uint64_t)kCT;
     int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)num_sms() * 16);
     if (qbytes == 8)
         qt_gather_kernel<double><<<blocks, 256, 0, s>>>((double *)dst, (const double *)src, p, g, n_tiles, 0, lay);

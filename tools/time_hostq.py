@@ -9,6 +9,8 @@ wl = make_config("cfg4")
 stream = torch.cuda.Stream()
 with Q.Plan(wl.dim, "x", n_qubits=wl.n_qubits, stream=stream.cuda_stream) as P:
     P.set_qualities_maxcut(wl.edges_u, wl.edges_v)
+    if os.environ.get("PROF"):
+        P.set_profiling(True)   # with QVA_TRACE=1: per-launch device times on stderr
     qh = torch.empty(wl.dim, dtype=torch.float64, pin_memory=True)
     qn = qh.numpy()
     P.get_qualities(0, wl.dim, out=qn)
