@@ -593,10 +593,10 @@ __device__ __forceinline__ double2 outer_tw(const double2 *Tw, int M1, int x1, i
 }
 template <typename F, typename Ad>
 __device__ __forceinline__ void col_block(const Ad &ad, const ColArgs &a, int c0, int cwv, int mat_y, int pslot,
-                                          double *red, const double2 *Tw, const double2 *twp) {
+                                          double *red, const double2 *Tw, const double2 *twp, int ops_mask) {
     const int M1 = a.M1, M2 = a.M2;
     if (a.do_inv) F::run(ad, a.sf, twp, cwv, true);
-    const int ops = a.ops;
+    const int ops = a.ops & ops_mask;
     if (ops) {
         double acc = 0.0, nrm = 0.0;
         // one element (c, x1); qv / lv: its q and lambda when loaded ahead (need_q / need_lam)
@@ -729,6 +729,13 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
             else *ad.ptr(c, x1) = make_double2(0.0, 0.0);
         }
     }
+    // HBM-resident q of the elementwise phase / <Q>: its rows (cw columns, 64 B) are pulled into L2
+    // now, so the batched loads of the ops loop (after the inverse FFT) hit L2 instead of waiting a
+    // full DRAM latency per batch (12!: 8.10 -> 7.98 ms per column pass)
+    if (a.ops_cfast && (a.ops & (OP_EXPECT | OP_PHASE))) {
+        for (int x1 = threadIdx.x; x1 < M1; x1 += blockDim.x)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.q + (uint64_t)x1 * M2 + c0));
+    }
     double2 *Tw = A + (size_t)a.cw * (M1 + (a.cw > 1 ? 1 : 0));
     const int nh = (M1 + 31) >> 5, E = tw_split_entries(M1);
     if (a.do_fwd) {
@@ -776,13 +783,17 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_col_kernel(const Col
         cp_async_wait_all();
     }
     __syncthreads();
-    col_block<F>(ad, a, c0, cwv, blockIdx.y, blockIdx.x, red, Tw, twp);
+    // an inverse-only pass whose one elementwise op is the outer twiddle (three-level inner inverse
+    // column pass) applies it in the store loop instead of a separate shared-memory sweep
+    const bool otw_store = a.ops == OP_OUTER_TW && !a.do_fwd;
+    col_block<F>(ad, a, c0, cwv, blockIdx.y, blockIdx.x, red, Tw, twp, otw_store ? ~OP_OUTER_TW : ~0);
     for (int idx = threadIdx.x; idx < totw; idx += blockDim.x) {
         const int x1 = idx >> a.lcw, c = idx & (a.cw - 1);
         if (c >= cwv) continue;
         const uint64_t x = (uint64_t)x1 * M2 + c0 + c;
         double2 v = *ad.ptr(c, x1);
         if (a.do_fwd) v = cmul(v, cmul(Tw[c * E + (x1 >> 5)], Tw[c * E + nh + (x1 & 31)]));
+        else if (otw_store) v = cmul(v, outer_tw(Tw, M1, x1, c));  // w_N^{-xl K}
         if (a.xg) {  // fused to-row transpose: row x1 belongs to shard d
             const int m1s = M1 / a.xg, d = x1 / m1s;
             a.xout[d][(uint64_t)(x1 - d * m1s) * a.M2g + a.col_off + c0 + c] = v;
@@ -867,7 +878,14 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_row_kernel(const Row
         for (int i = threadIdx.x; i < tot; i += blockDim.x, adv(r, x)) rows[i] = *ad.ptr(r, x);
         return;
     }
-    {
+    // constant spectrum (spec 0: e0 at bin 0, ec elsewhere): F^-1(e X) = ec F^-1 X + (e0 - ec) X_0
+    // F^-1 delta_0, and F^-1 delta_0 = 1, so the spectrum is folded into the final store loop (one
+    // shared-memory sweep fewer); only the CTA holding global row 0 keeps X_0 for its row 0
+    const bool spec_fold = a.spec == 0;
+    const bool has0 = spec_fold && a.row_off + k1_0 == 0;
+    const double2 x00 = has0 ? *ad.ptr(0, 0) : make_double2(0.0, 0.0);
+    const double2 d00 = has0 ? cmul(csub(a.e0, a.ec), x00) : make_double2(0.0, 0.0);
+    if (!spec_fold) {
         int r = r0, k2 = x0;
         for (int i = threadIdx.x; i < tot; i += blockDim.x, adv(r, k2)) {
             const int k1 = a.row_off + k1_0 + r;
@@ -904,7 +922,12 @@ __global__ void __launch_bounds__(NT, kFftThreads / NT) fft_row_kernel(const Row
     // B200; the incremental form is correct)
     int r = r0, x2 = x0;
     for (int i = threadIdx.x; i < tot; i += blockDim.x, adv(r, x2)) {
-        const double2 v = cmul(*ad.ptr(r, x2), cmul(Tr[r * E + (x2 >> 5)], Tr[r * E + nh + (x2 & 31)]));
+        double2 u = *ad.ptr(r, x2);
+        if (spec_fold) {
+            u = cmul(u, a.ec);
+            if (has0 && r == 0) u = cadd(u, d00);
+        }
+        const double2 v = cmul(u, cmul(Tr[r * E + (x2 >> 5)], Tr[r * E + nh + (x2 & 31)]));
         if (a.xg) {  // fused to-column transpose: column x2 belongs to shard s
             const int sh = x2 / a.M2s;
             a.xout[sh][(uint64_t)(a.row_off + k1_0 + r) * a.M2s + (x2 - sh * a.M2s)] = v;

@@ -126,6 +126,9 @@ def _w_exchange(rank, world):
 
 
 def _w_batch(rank, world):
+    # host logic only (member partition + all-reduce of the members' values): libqva needs a GPU to
+    # create a plan; the library's own sharded batch and its all-reduce run in
+    # tests/test_multiproc_gpu.py (world = 2 / 4 plans on one B200, every member vs the oracle)
     import oracle as O
     import paper_2110_03963_b200 as Q
     rng = np.random.default_rng(7)
