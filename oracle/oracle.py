@@ -20,7 +20,8 @@ _LIB = os.path.join(_HERE, "libqva_oracle.so")
 __all__ = [
     "build_oracle", "lib", "num_threads", "set_num_threads", "maxcut_q", "init_uniform", "phase", "mixer_x",
     "mixer_circulant_dense", "mixer_complete", "expectation", "norm2", "probabilities",
-    "evolve_x", "evolve_complete", "evolve_circulant_dense", "lightcone_maxcut",
+    "evolve_x", "evolve_complete", "evolve_circulant_dense", "evolve_circulant_fft", "mixer_circulant_fft",
+    "lightcone_maxcut",
     "dense_sum_x", "mixer_sparse_dense", "evolve_sparse_dense", "c128",
     "mixer_parity", "evolve_parity", "parity_pairs",
     "maxcut_q_at", "kperm_count", "kperm_unrank", "kperm_cost", "kperm_qualities",
@@ -191,6 +192,28 @@ def evolve_circulant_dense(q: np.ndarray, lam: np.ndarray, theta,
     q = np.ascontiguousarray(q, np.float64)
     lam = np.ascontiguousarray(lam, np.float64)
     lib().or_evolve_circulant_dense(N, _ptr(psi), _ptr(q), _ptr(lam), _ptr(theta), len(theta) // 2)
+    return psi
+
+
+def mixer_circulant_fft(psi: np.ndarray, lam: np.ndarray, beta: float) -> np.ndarray:
+    """F^-1 diag(e^{-i beta lam}) F by the FFT the paper names for circulant mixers
+    (Sec. 3; readings R3, R4: numpy's forward-DFT bin order).  Library
+    primitive: numpy.fft (pocketfft).  Returns a new array."""
+    lam = np.asarray(lam, np.float64)
+    return np.fft.ifft(np.exp(-1j * beta * lam) * np.fft.fft(psi))
+
+
+def evolve_circulant_fft(q: np.ndarray, lam: np.ndarray, theta,
+                         psi0: np.ndarray | None = None) -> np.ndarray:
+    """QWOA state prod_k U_M(beta_k) U_Q(gamma_k) |psi0> (PAPER.md:298 Eq. qwoa; theta layout
+    R7) with the circulant mixer through mixer_circulant_fft: the large-N twin of
+    evolve_circulant_dense (same loop; pinned against it in tests/test_oracle_pins.py P20)."""
+    theta = np.asarray(theta, np.float64)
+    N = len(q)
+    psi = init_uniform(N) if psi0 is None else np.array(psi0, np.complex128, copy=True)
+    for k in range(len(theta) // 2):
+        phase(psi, q, float(theta[2 * k]))
+        psi = np.ascontiguousarray(mixer_circulant_fft(psi, lam, float(theta[2 * k + 1])), np.complex128)
     return psi
 
 

@@ -59,9 +59,9 @@ bool fs_stage_tables(int n, std::vector<double2> &tab);
 // final twiddle, in place
 int fs_row_block(int n);
 cudaError_t fs_row_launch(int n, const FsRowArgs &a, uint64_t n_rows, cudaStream_t s);
-// columns: n = column length, cols = columns per matrix (multiple of 8), nmat matrices;
+// columns: n = column length, cols = columns per matrix (multiple of fs_col_width(n)), nmat matrices;
 // inv / fwd select the transforms (inverse -> ops -> forward)
 cudaError_t fs_col_launch(int n, const FsColArgs &a, int cols, int nmat, bool inv, bool fwd, cudaStream_t s);
-int fs_col_width();
+int fs_col_width(int n);  // columns per CTA of the length-n column codelet (0: none)
 
 }  // namespace qva

@@ -1198,7 +1198,7 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
         fp->big_shift = 11;
         if (!make_big_tables(N, &fp->d_big_lo, &fp->d_big_hi) || !make_big_tables(R, &fp->d_in_lo, &fp->d_in_hi))
             return fail(QVA_ERR_OUT_OF_MEMORY, "cudaMalloc (FFT twiddles) failed");
-        fp->n_partials = col_grid(fp);
+        fp->n_partials = std::max(col_grid(fp), fp->M2 / 4);  // fused-stage column blocks may be 4 wide
         if (cudaMalloc(&fp->partials, fp->n_partials * 2 * sizeof(double)) != cudaSuccess)
             return fail(QVA_ERR_OUT_OF_MEMORY, "cudaMalloc (FFT partials) failed");
     } else if (fp->whole) {
@@ -1225,7 +1225,7 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
             return fail(QVA_ERR_OUT_OF_MEMORY, "cudaMalloc (FFT twiddles) failed");
         cudaMemcpy(fp->d_big_lo, lo.data(), B * sizeof(double2), cudaMemcpyHostToDevice);
         cudaMemcpy(fp->d_big_hi, hi.data(), nhi * sizeof(double2), cudaMemcpyHostToDevice);
-        fp->n_partials = col_grid(fp);
+        fp->n_partials = std::max(col_grid(fp), fp->M2 / 4);  // fused-stage column blocks may be 4 wide
         if (cudaMalloc(&fp->partials, fp->n_partials * 2 * sizeof(double)) != cudaSuccess)
             return fail(QVA_ERR_OUT_OF_MEMORY, "cudaMalloc (FFT partials) failed");
     }
@@ -1242,8 +1242,9 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
         };
         const int cols = fp->M2, rowlen = fp->levels == 3 ? fp->Mi2 : fp->M2;
         bool ok = true;
-        if (cols % fs_col_width() == 0) ok = ok && fs_tab(fp->M1, true, &fp->fs_col);
-        if (fp->levels == 3 && fp->Mi2 % fs_col_width() == 0) ok = ok && fs_tab(fp->Mi1, true, &fp->fs_col2);
+        if (fs_col_width(fp->M1) && cols % fs_col_width(fp->M1) == 0) ok = ok && fs_tab(fp->M1, true, &fp->fs_col);
+        if (fp->levels == 3 && fs_col_width(fp->Mi1) && fp->Mi2 % fs_col_width(fp->Mi1) == 0)
+            ok = ok && fs_tab(fp->Mi1, true, &fp->fs_col2);
         const uint64_t nrows = fp->levels == 3 ? (uint64_t)fp->M1 * fp->Mi1 : (uint64_t)fp->M1;
         const int rbk = fs_row_block(rowlen);
         if (rbk > 0 && nrows % rbk == 0)
@@ -1568,7 +1569,7 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
         if (fp->fs_col && !blu && !(ops & ~(OP_PHASE | OP_EXPECT)) && in_len == (uint64_t)fp->N &&
             out_len == (uint64_t)fp->N && (inv || fwd)) {
             FsColArgs f = fs_col_args(fp, fp->fs_col, c);
-            expect_slots = fp->M2 / fs_col_width();
+            expect_slots = fp->M2 / fs_col_width(fp->M1);
             e = fs_col_launch(fp->M1, f, fp->M2, 1, inv != 0, fwd != 0, s);
         } else {
             col_kernel_for(fp->M1, col_half)<<<gc, col_half ? kFftThreads / 2 : kFftThreads, smem_c, s>>>(c);

@@ -23,6 +23,7 @@
 // 128 B instead of 224 B, and 7 block barriers instead of 15.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <type_traits>
 #include <utility>
@@ -199,16 +200,15 @@ __device__ __forceinline__ void fs_first_store(const Ad &ad, double2 (&v)[NB][R]
 // row_mod for three-level inner rows), in place.  As fft_row_kernel with the spectrum folded:
 // spec 0 multiplies every bin by ec (carried in the final twiddle) and bin 0 of global row 0 by
 // e0 / ec on the registers.
-template <typename C, int T, int NT, int MINB>
-__global__ void __launch_bounds__(T, MINB) fs_row_kernel(const FsRowArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+// SM0: the block was copied into shared memory ahead (pipelined kernel) and stage 0 reads it there
+template <typename C, int T, int NT, bool SM0>
+__device__ __forceinline__ void fs_row_block(const FsRowArgs &a, double2 *A, uint64_t blk) {
     constexpr int N = C::N, S = C::S;
     static_assert(S >= 2 && C::r(0, S - 1) == C::r(1, 0), "reversed inverse order");
-    double2 *A = reinterpret_cast<double2 *>(smem_raw);
     const FsAddr<C::swz()> ad{A, N};
-    double2 *rows = a.buf + (uint64_t)blockIdx.x * NT * N;
-    const int grow0 = a.row_off + (int)blockIdx.x * NT;
-    // forward stage 0: global -> registers -> DFT -> shared memory
+    double2 *rows = a.buf + blk * NT * N;
+    const int grow0 = a.row_off + (int)blk * NT;
+    // forward stage 0: global (or the prefetched block) -> registers -> DFT -> shared memory
     {
         constexpr int R = C::r(0, 0), nb = N / R, tot = NT * nb, NB = (tot + T - 1) / T;
         double2 v[NB][R];
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(T, MINB) fs_row_kernel(const FsRowArgs a) {
                 fs_map<false, NT, nb>(J, f, j);
                 const double2 *src = rows + f * N + j;
 #pragma unroll
-                for (int t = 0; t < R; ++t) v[b][t] = src[t * nb];
+                for (int t = 0; t < R; ++t) v[b][t] = SM0 ? *ad.ptr(f, j + t * nb) : src[t * nb];
             }
         }
 #pragma unroll
@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(T, MINB) fs_row_kernel(const FsRowArgs a) {
             const int J = threadIdx.x + b * T;
             if (tot % T == 0 || J < tot) dft<R>(v[b], false);
         }
+        if constexpr (SM0) __syncthreads();
         fs_first_store<C, 0, T, NT, false>(ad, v);
     }
     __syncthreads();
@@ -289,22 +290,61 @@ __global__ void __launch_bounds__(T, MINB) fs_row_kernel(const FsRowArgs a) {
     }
 }
 
+__device__ __forceinline__ void fs_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void fs_cp_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <typename C, int T, int NT, int MINB>
+__global__ void __launch_bounds__(T, MINB) fs_row_kernel(const FsRowArgs a, uint64_t nblk) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    fs_row_block<C, T, NT, false>(a, reinterpret_cast<double2 *>(smem_raw), blockIdx.x);
+}
+// Persistent pipelined form: CTA b takes blocks b, b + grid, ...; while one block is transformed
+// the next one's rows are in flight into the second shared-memory buffer (cp.async), so the
+// first stage's loads no longer wait a memory latency per block.
+template <typename C, int T, int NT, int MINB>
+__global__ void __launch_bounds__(T, MINB) fs_row_pipe_kernel(const FsRowArgs a, uint64_t nblk) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int N = C::N, E = NT * N;
+    double2 *A0 = reinterpret_cast<double2 *>(smem_raw);
+    auto prefetch = [&](double2 *A, uint64_t blk) {
+        const FsAddr<C::swz()> ad{A, N};
+        const double2 *src = a.buf + blk * E;
+        for (int i = threadIdx.x; i < E; i += T) {
+            const int f = i / N;
+            cp_async16(ad.ptr(f, i - f * N), src + i);
+        }
+    };
+    uint64_t blk = blockIdx.x;
+    int cur = 0;
+    if (blk < nblk) prefetch(A0, blk);
+    fs_cp_commit();
+    for (; blk < nblk; blk += gridDim.x) {
+        const uint64_t nxt = blk + gridDim.x;
+        if (nxt < nblk) prefetch(A0 + (cur ^ 1) * E, nxt);
+        fs_cp_commit();
+        fs_cp_wait_prev();
+        __syncthreads();
+        fs_row_block<C, T, NT, true>(a, A0 + cur * E, blk);
+        __syncthreads();
+        cur ^= 1;
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Column pass: CW adjacent columns (c0 .. c0+CW) of a matrix with row stride M2, column length
 // N, column-fastest over the threads (CW * 16 B = 128-B rows per global access):
 // [inverse FFT] -> <Q> partials, phase exp(-i gamma q), outer twiddle (three-level) on the
 // registers -> [forward FFT -> twiddle w_M^{C k1}] -> global.  As fft_col_kernel.
-template <typename C, int T, int CW, int MINB, bool INV, bool FWD>
-__global__ void __launch_bounds__(T, MINB) fs_col_kernel(const FsColArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ double red[2 * (T / 32 + 1)];
+template <int N>
+constexpr int fs_col_stride() { return (N % 2 == 0) ? N + 1 : N; }  // odd: 8 columns, 8 bank groups
+template <typename C, int T, int CW, bool INV, bool FWD, bool SM0>
+__device__ __forceinline__ void fs_col_block(const FsColArgs &a, double2 *A, int bx, int by, double *red) {
     constexpr int N = C::N, S = C::S;
-    constexpr int CS = (N % 2 == 0) ? N + 1 : N;  // odd column stride: 8 columns, 8 bank groups
+    constexpr int CS = fs_col_stride<N>();
     static_assert(S >= 2 && C::r(0, 0) == C::r(1, S - 1), "reversed inverse order");
-    double2 *A = reinterpret_cast<double2 *>(smem_raw);
     const FsAddr<0> ad{A, CS};
-    const int c0 = (int)blockIdx.x * CW;
-    const uint64_t mat = (uint64_t)blockIdx.y * a.mat_stride;
+    const int c0 = bx * CW;
+    const uint64_t mat = (uint64_t)by * a.mat_stride;
     const uint64_t M2 = (uint64_t)a.M2;
     const double2 *in = a.in + mat + c0;
     double2 *out = a.out + mat + c0;
@@ -329,7 +369,7 @@ __global__ void __launch_bounds__(T, MINB) fs_col_kernel(const FsColArgs a) {
                     fs_map<true, CW, nb>(J, c, j);
                     const double2 *src = in + (uint64_t)j * M2 + c;
 #pragma unroll
-                    for (int t = 0; t < R; ++t) u[b][t] = src[(uint64_t)(t * nb) * M2];
+                    for (int t = 0; t < R; ++t) u[b][t] = SM0 ? *ad.ptr(c, j + t * nb) : src[(uint64_t)(t * nb) * M2];
                 }
             }
 #pragma unroll
@@ -337,6 +377,7 @@ __global__ void __launch_bounds__(T, MINB) fs_col_kernel(const FsColArgs a) {
                 const int J = threadIdx.x + b * T;
                 if (tot % T == 0 || J < tot) dft<R>(u[b], true);
             }
+            if constexpr (SM0) __syncthreads();
             fs_first_store<C, 1, T, CW, true>(ad, u);
         }
         __syncthreads();
@@ -352,7 +393,7 @@ __global__ void __launch_bounds__(T, MINB) fs_col_kernel(const FsColArgs a) {
                 const double2 *src = in + (uint64_t)j * M2 + c;
 #pragma unroll
                 for (int t = 0; t < Rm; ++t)
-                    v[b][t] = a.init ? make_double2(a.amp0, 0.0) : src[(uint64_t)(t * nbm) * M2];
+                    v[b][t] = a.init ? make_double2(a.amp0, 0.0) : SM0 ? *ad.ptr(c, j + t * nbm) : src[(uint64_t)(t * nbm) * M2];
             }
         }
     }
@@ -386,7 +427,7 @@ __global__ void __launch_bounds__(T, MINB) fs_col_kernel(const FsColArgs a) {
                     }
                 }
                 if (a.ops & OP_OTW) {
-                    const uint64_t K = (uint64_t)(a.mat_off + (int)blockIdx.y);
+                    const uint64_t K = (uint64_t)(a.mat_off + by);
                     const uint64_t xl0 = (uint64_t)j * M2 + (uint64_t)(c0 + c);
                     double2 w = conjd(fs_big(a.otw_lo, a.otw_hi, a.otw_shift, K * xl0));
                     const double2 st = conjd(fs_big(a.otw_lo, a.otw_hi, a.otw_shift, K * (uint64_t)nbm * M2));
@@ -405,7 +446,7 @@ __global__ void __launch_bounds__(T, MINB) fs_col_kernel(const FsColArgs a) {
             const int J = threadIdx.x + b * T;
             if (totm % T == 0 || J < totm) dft<Rm>(v[b], false);
         }
-        if constexpr (INV) __syncthreads();  // the inverse last stage's reads are done
+        if constexpr (INV || SM0) __syncthreads();  // the last reads of the block are done
         fs_first_store<C, 0, T, CW, true>(ad, v);
         __syncthreads();
         fs_static_for<S - 2>([&](auto sc) { fs_stage<C, 0, decltype(sc)::value + 1, T, CW, true>(ad, a.tw); });
@@ -460,27 +501,66 @@ __global__ void __launch_bounds__(T, MINB) fs_col_kernel(const FsColArgs a) {
                 sa += red[2 * w];
                 sb += red[2 * w + 1];
             }
-            a.partials[2 * blockIdx.x] = sa;
-            a.partials[2 * blockIdx.x + 1] = sb;
+            a.partials[2 * bx] = sa;
+            a.partials[2 * bx + 1] = sb;
         }
     }
 }
 
+template <typename C, int T, int CW, int MINB, bool INV, bool FWD>
+__global__ void __launch_bounds__(T, MINB) fs_col_kernel(const FsColArgs a, int nbx, uint64_t nblk) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double red[2 * (T / 32 + 1)];
+    fs_col_block<C, T, CW, INV, FWD, false>(a, reinterpret_cast<double2 *>(smem_raw), blockIdx.x, blockIdx.y, red);
+}
+// Persistent pipelined form (as fs_row_pipe_kernel): blocks (bx, by) = (b mod nbx, b / nbx),
+// the next block's columns copied into the second buffer while the current one is transformed.
+template <typename C, int T, int CW, int MINB, bool INV, bool FWD>
+__global__ void __launch_bounds__(T, MINB) fs_col_pipe_kernel(const FsColArgs a, int nbx, uint64_t nblk) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double red[2 * (T / 32 + 1)];
+    constexpr int N = C::N, CS = fs_col_stride<N>(), E = CW * CS;
+    double2 *A0 = reinterpret_cast<double2 *>(smem_raw);
+    const bool load = true;  // (init passes launch the one-shot kernel)
+    const uint64_t M2 = (uint64_t)a.M2;
+    auto prefetch = [&](double2 *A, uint64_t blk) {
+        const int bx = (int)(blk % (uint64_t)nbx), by = (int)(blk / (uint64_t)nbx);
+        const double2 *src = a.in + (uint64_t)by * a.mat_stride + bx * CW;
+        for (int i = threadIdx.x; i < N * CW; i += T) {
+            const int c = i & (CW - 1), x1 = i / CW;
+            cp_async16(A + c * CS + x1, src + (uint64_t)x1 * M2 + c);
+        }
+    };
+    uint64_t blk = blockIdx.x;
+    int cur = 0;
+    if (load && blk < nblk) prefetch(A0, blk);
+    fs_cp_commit();
+    for (; blk < nblk; blk += gridDim.x) {
+        const uint64_t nxt = blk + gridDim.x;
+        if (load && nxt < nblk) prefetch(A0 + (cur ^ 1) * E, nxt);
+        fs_cp_commit();
+        fs_cp_wait_prev();
+        __syncthreads();
+        const int bx = (int)(blk % (uint64_t)nbx), by = (int)(blk / (uint64_t)nbx);
+        fs_col_block<C, T, CW, INV, FWD, true>(a, A0 + cur * E, bx, by, red);
+        __syncthreads();
+        cur ^= 1;
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
-// compiled codelets and their launch shapes
-using FsRowFn = void (*)(FsRowArgs);
-using FsColFn = void (*)(FsColArgs);
-constexpr int kFsCW = 8;
+// compiled codelets and their launch shapes (several per length for measurement: QVA_FS_ROWV /
+// QVA_FS_COLV select the variant index, default 0)
+using FsRowFn = void (*)(FsRowArgs, uint64_t);
+using FsColFn = void (*)(FsColArgs, int, uint64_t);
 
 struct FsRowEntry {
-    int n, threads, rows;
+    int n, threads, rows, pipe;
     FsRowFn fn;
-    int rad[8];
 };
 struct FsColEntry {
-    int n, threads;
+    int n, threads, cw, pipe;
     FsColFn inv_fwd, fwd, inv;
-    int rad[8];
 };
 
 using C768 = FsC<16, 16, 3>;
@@ -489,49 +569,90 @@ using C770 = FsC<7, 11, 10>;
 using C810 = FsC<10, 9, 9>;
 using C840 = FsC<8, 15, 7>;
 
+#define QVA_FS_ROW(C, T, NT, MB) {C::N, T, NT, 0, fs_row_kernel<C, T, NT, MB>}
+#define QVA_FS_ROWP(C, T, NT, MB) {C::N, T, NT, 1, fs_row_pipe_kernel<C, T, NT, MB>}
+// index 0 of each length is the default (measured on one B200, tools/ab_fs.sh: 12! 768-point rows
+// pipelined 96 x 2 rows 105.0 ms vs one-shot 192 x 4 rows 109.8 ms per p=4 evolution; cfg3
+// 4320-point rows one-shot two CTAs per SM 0.622 ms vs 0.721 ms one per SM, 0.979 ms pipelined)
 const FsRowEntry kFsRows[] = {
-    {768, 192, 4, fs_row_kernel<C768, 192, 4, 3>, {16, 16, 3}},
-    {4320, 288, 1, fs_row_kernel<C4320, 288, 1, 1>, {9, 3, 16, 10}},
+    QVA_FS_ROWP(C768, 96, 2, 4),
+    QVA_FS_ROW(C768, 192, 4, 3),
+    QVA_FS_ROWP(C768, 192, 4, 2),
+    QVA_FS_ROW(C4320, 288, 1, 2),
+    QVA_FS_ROW(C4320, 288, 1, 1),
+    QVA_FS_ROWP(C4320, 288, 1, 1),
 };
-#define QVA_FS_COL(C, T)                                                                        \
-    fs_col_kernel<C, T, kFsCW, 1, true, true>, fs_col_kernel<C, T, kFsCW, 1, false, true>,      \
-        fs_col_kernel<C, T, kFsCW, 1, true, false>
+#undef QVA_FS_ROW
+#undef QVA_FS_ROWP
+#define QVA_FS_COL(K, C, T, CW, MB, P)                                                      \
+    {C::N, T, CW, P, K<C, T, CW, MB, true, true>, K<C, T, CW, MB, false, true>, K<C, T, CW, MB, true, false>}
+// column codelets: one-shot CTAs (the pipelined forms spill in the block loop and doubled the
+// DRAM write traffic at 12!: 162-205 ms; 840-point columns four wide, two CTAs per SM: cfg3 0.622
+// vs 0.653 ms eight wide)
 const FsColEntry kFsCols[] = {
-    {770, 640, QVA_FS_COL(C770, 640), {7, 11, 10}},
-    {810, 512, QVA_FS_COL(C810, 512), {10, 9, 9}},
-    {840, 480, QVA_FS_COL(C840, 480), {8, 15, 7}},
+    QVA_FS_COL(fs_col_kernel, C770, 640, 8, 1, 0),
+    QVA_FS_COL(fs_col_pipe_kernel, C770, 640, 8, 1, 1),
+    QVA_FS_COL(fs_col_kernel, C810, 512, 8, 1, 0),
+    QVA_FS_COL(fs_col_pipe_kernel, C810, 512, 8, 1, 1),
+    QVA_FS_COL(fs_col_kernel, C840, 256, 4, 2, 0),
+    QVA_FS_COL(fs_col_kernel, C840, 480, 8, 1, 0),
 };
 #undef QVA_FS_COL
 
+template <typename C>
+void fs_fill_rad(int n, int *rad) {
+    if (n != C::N) return;
+    constexpr Arr8 f = C::F;
+    for (int s = 0; s < C::S; ++s) rad[s] = f.v[s];
+}
+const int *fs_radices(int n) {
+    static int rad[8] = {};
+    for (int &r : rad) r = 0;
+    fs_fill_rad<C768>(n, rad);
+    fs_fill_rad<C4320>(n, rad);
+    fs_fill_rad<C770>(n, rad);
+    fs_fill_rad<C810>(n, rad);
+    fs_fill_rad<C840>(n, rad);
+    return rad[0] ? rad : nullptr;
+}
+int fs_env(const char *name) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : 0;
+}
 const FsRowEntry *fs_row_entry(int n) {
+    static const int v = fs_env("QVA_FS_ROWV");
+    int k = 0;
+    for (const auto &e : kFsRows)
+        if (e.n == n && k++ == v) return &e;
     for (const auto &e : kFsRows)
         if (e.n == n) return &e;
     return nullptr;
 }
 const FsColEntry *fs_col_entry(int n) {
+    static const int v = fs_env("QVA_FS_COLV");
+    int k = 0;
+    for (const auto &e : kFsCols)
+        if (e.n == n && k++ == v) return &e;
     for (const auto &e : kFsCols)
         if (e.n == n) return &e;
     return nullptr;
 }
-const int *fs_radices(int n) {
-    if (const FsRowEntry *e = fs_row_entry(n)) return e->rad;
-    if (const FsColEntry *e = fs_col_entry(n)) return e->rad;
-    return nullptr;
+size_t fs_col_smem(const FsColEntry &e) {
+    return (size_t)(e.pipe ? 2 : 1) * e.cw * ((e.n % 2 == 0) ? e.n + 1 : e.n) * sizeof(double2);
 }
+size_t fs_row_smem(const FsRowEntry &e) { return (size_t)(e.pipe ? 2 : 1) * e.rows * e.n * sizeof(double2); }
 
 DeviceOnce g_fs_attr;
 
 cudaError_t fs_set_attrs() {
     return once_per_device(g_fs_attr, [] {
         for (const auto &e : kFsRows) {
-            cudaError_t r = cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)(e.rows * e.n * sizeof(double2)));
+            cudaError_t r = cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs_row_smem(e));
             if (r != cudaSuccess) return r;
         }
         for (const auto &e : kFsCols) {
-            const int bytes = (int)(kFsCW * ((e.n % 2 == 0) ? e.n + 1 : e.n) * sizeof(double2));
             for (FsColFn f : {e.inv_fwd, e.fwd, e.inv}) {
-                cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+                cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs_col_smem(e));
                 if (r != cudaSuccess) return r;
             }
         }
@@ -553,7 +674,10 @@ int fs_row_block(int n) {
     const FsRowEntry *e = fs_row_entry(n);
     return e ? e->rows : 0;
 }
-int fs_col_width() { return kFsCW; }
+int fs_col_width(int n) {
+    const FsColEntry *e = fs_col_entry(n);
+    return e ? e->cw : 0;
+}
 
 bool fs_stage_tables(int n, std::vector<double2> &tab) {
     const int *rad = fs_radices(n);
@@ -578,25 +702,52 @@ bool fs_stage_tables(int n, std::vector<double2> &tab) {
     return true;
 }
 
+// persistent grid of the pipelined kernels: resident CTAs per SM x SMs
+template <typename Fn>
+static unsigned fs_pipe_grid(Fn f, int threads, size_t smem, uint64_t nblk) {
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, threads, smem) != cudaSuccess || per < 1) per = 1;
+    return (unsigned)std::min<uint64_t>(nblk, (uint64_t)per * (uint64_t)num_sms());
+}
+
 cudaError_t fs_row_launch(int n, const FsRowArgs &a, uint64_t n_rows, cudaStream_t s) {
     const FsRowEntry *e = fs_row_entry(n);
     if (!e || n_rows % e->rows) return cudaErrorInvalidValue;
     cudaError_t r = fs_set_attrs();
     if (r != cudaSuccess) return r;
     if (n_rows == 0) return cudaSuccess;
-    e->fn<<<(unsigned)(n_rows / e->rows), e->threads, e->rows * n * sizeof(double2), s>>>(a);
+    const uint64_t nblk = n_rows / e->rows;
+    const size_t smem = fs_row_smem(*e);
+    const unsigned grid = e->pipe ? fs_pipe_grid(e->fn, e->threads, smem, nblk) : (unsigned)nblk;
+    e->fn<<<grid, e->threads, smem, s>>>(a, nblk);
     return cudaGetLastError();
 }
 
 cudaError_t fs_col_launch(int n, const FsColArgs &a, int cols, int nmat, bool inv, bool fwd, cudaStream_t s) {
     const FsColEntry *e = fs_col_entry(n);
-    if (!e || cols % kFsCW || (!inv && !fwd)) return cudaErrorInvalidValue;
+    if (!e || cols % e->cw || (!inv && !fwd)) return cudaErrorInvalidValue;
     cudaError_t r = fs_set_attrs();
     if (r != cudaSuccess) return r;
     if (cols == 0 || nmat == 0) return cudaSuccess;
-    const size_t bytes = kFsCW * ((n % 2 == 0) ? n + 1 : n) * sizeof(double2);
     FsColFn f = inv ? (fwd ? e->inv_fwd : e->inv) : e->fwd;
-    f<<<dim3(cols / kFsCW, nmat), e->threads, bytes, s>>>(a);
+    const int nbx = cols / e->cw;
+    const uint64_t nblk = (uint64_t)nbx * nmat;
+    const size_t smem = fs_col_smem(*e);
+    const FsColEntry *o = nullptr;  // a pass that loads nothing (init) prefers a one-shot kernel
+    if (e->pipe && a.init && !inv)
+        for (const auto &x : kFsCols)
+            if (x.n == n && !x.pipe && x.cw == e->cw) {
+                o = &x;
+                break;
+            }
+    if (o) {
+        FsColFn g = fwd ? o->fwd : o->inv;
+        g<<<dim3(nbx, nmat), o->threads, fs_col_smem(*o), s>>>(a, nbx, nblk);
+    } else if (e->pipe) {
+        f<<<fs_pipe_grid(f, e->threads, smem, nblk), e->threads, smem, s>>>(a, nbx, nblk);
+    } else {
+        f<<<dim3(nbx, nmat), e->threads, smem, s>>>(a, nbx, nblk);
+    }
     return cudaGetLastError();
 }
 

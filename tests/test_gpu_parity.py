@@ -350,6 +350,39 @@ def test_cfg3_full(Q):
         _amp_close(P.get_state(), ref)
 
 
+def test_cfg3_random_spectrum_fused_stage(Q):
+    """cfg3 size (N = 10!, 840 x 4320 split: the fused-stage column and row passes of
+    kernels_fft_fs.cu) with an arbitrary real spectrum (row-pass spectrum from the lambda array,
+    transposed order) and an arbitrary initial state (column pass loads psi0 without an inverse
+    transform), against the numpy-FFT oracle; then single mixer / phase steps (forward-only and
+    inverse-only column passes)."""
+    wl = make_config("cfg3")
+    N = wl.dim
+    rng = np.random.default_rng(31)
+    lam = rng.standard_normal(N) * 2
+    theta = rng.uniform(0, math.pi, 6)
+    psi0 = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    psi0 /= np.linalg.norm(psi0)
+    with Q.Plan(N, "circulant") as P:
+        P.set_qualities(wl.q)
+        P.set_circulant_eigenvalues(lam)
+        P.evolve(theta)
+        ref = O.evolve_circulant_fft(wl.q, lam, theta)
+        _amp_close(P.get_state(), ref)
+        _f_close(P.expectation(), O.expectation(ref, wl.q), O.expectation(ref, np.abs(wl.q)))
+        P.set_initial_state(psi0)
+        P.evolve(theta)
+        _amp_close(P.get_state(), O.evolve_circulant_fft(wl.q, lam, theta, psi0))
+        P.clear_initial_state()
+        P.reset_state()
+        P.apply_mixer(0.7)
+        P.apply_phase(1.3)
+        P.apply_mixer(0.4)
+        ref = O.mixer_circulant_fft(O.init_uniform(N), lam, 0.7)
+        ref = O.phase(np.ascontiguousarray(ref), wl.q, 1.3)
+        _amp_close(P.get_state(), O.mixer_circulant_fft(ref, lam, 0.4))
+
+
 @pytest.mark.parametrize("N", [2, 7, 13, 17, 96, 97, 720, 1001, 1009, 4096, 4099, 5040, 6144, 8198, 10007])
 def test_circulant_random_spectrum_vs_dense(Q, N):
     """Generic real spectrum: whole-CTA kernel (13-smooth N <= 4096), four-step mixed radix

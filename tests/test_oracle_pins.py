@@ -707,3 +707,21 @@ def test_P19_generic_sparse_evolve_vs_dense_product(N, density):
     got = O.evolve_sparse_dense(q, W, theta)
     ref = _dense_product(np.full(N, 1 / math.sqrt(N), np.complex128), q, lambda b: _expm_hermitian(W, b), theta)
     assert np.max(np.abs(got - ref)) < 1e-12
+
+
+# ---------------------------------------------------------------- P20: FFT-route QWOA oracle ----
+@pytest.mark.parametrize("N", [12, 97, 720, 1001])
+def test_P20_evolve_circulant_fft_vs_dense(N):
+    """P20: the numpy-FFT QWOA evolution (large-N oracle of the circulant mixer)
+    equals the O(N^2) dense-definition evolution (itself pinned by P11 / P19) for a random real
+    spectrum and a random initial state; a swapped gamma/beta fails."""
+    rng = np.random.default_rng(900 + N)
+    q = rng.standard_normal(N)
+    lam = rng.standard_normal(N) * 3
+    theta = rng.uniform(0, math.pi, 6)
+    psi0 = _rand_state(N, rng)
+    ref = O.evolve_circulant_dense(q, lam, theta, psi0)
+    got = O.evolve_circulant_fft(q, lam, theta, psi0)
+    np.testing.assert_allclose(got, ref, atol=1e-11)
+    swapped = O.evolve_circulant_fft(q, lam, theta.reshape(-1, 2)[:, ::-1].ravel(), psi0)
+    assert np.max(np.abs(swapped - ref)) > 1e-3
