@@ -549,6 +549,214 @@ __global__ void __launch_bounds__(T, MINB) fs_col_pipe_kernel(const FsColArgs a,
 }
 
 // ---------------------------------------------------------------------------------------------
+// Ping-pong column pass: the same transforms with out-of-place stages between two shared-memory
+// buffers, so a stage needs one barrier and no thread has to hold all of its butterflies at once
+// (butterflies in rounds of T): small CTAs (two or more per SM) whose stage-0 loads overlap the
+// other CTAs' arithmetic.
+template <typename C, int D, int s, int T, int CW, typename Ad>
+__device__ __forceinline__ void fs_stage_pp(const Ad &src, const Ad &dst, const double2 *__restrict__ tw) {
+    constexpr int N = C::N, R = C::r(D, s), M = C::m(D, s), nb = N / R, tot = CW * nb, OFF = C::off(D, s);
+#pragma unroll
+    for (int J = threadIdx.x; J < tot; J += T) {
+        int c, j;
+        fs_map<true, CW, nb>(J, c, j);
+        double2 v[R];
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[t] = *src.ptr(c, j + t * nb);
+        const int k = j % M;
+#pragma unroll
+        for (int t = 1; t < R; ++t) v[t] = cmul(v[t], __ldg(tw + OFF + (t - 1) * M + k));
+        dft<R>(v, D != 0);
+        const int o = (j - k) * R + k;
+#pragma unroll
+        for (int t = 0; t < R; ++t) *dst.ptr(c, o + t * M) = v[t];
+    }
+    __syncthreads();
+}
+
+template <typename C, int T, int CW, int MINB, bool INV, bool FWD>
+__global__ void __launch_bounds__(T, MINB) fs_colpp_kernel(const FsColArgs a, int nbx, uint64_t nblk) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double red[2 * (T / 32 + 1)];
+    constexpr int N = C::N, S = C::S, CS = fs_col_stride<N>();
+    static_assert(S >= 2 && C::r(0, 0) == C::r(1, S - 1), "reversed inverse order");
+    double2 *A0 = reinterpret_cast<double2 *>(smem_raw);
+    const FsAddr<0> b0{A0, CS}, b1{A0 + CW * CS, CS};
+    const int c0 = (int)blockIdx.x * CW;
+    const uint64_t mat = (uint64_t)blockIdx.y * a.mat_stride;
+    const uint64_t M2 = (uint64_t)a.M2;
+    const double2 *in = a.in + mat + c0;
+    double2 *out = a.out + mat + c0;
+    constexpr int OP_EXP = 2, OP_PH = 4, OP_OTW = 64;
+    const bool need_q = (a.ops & (OP_EXP | OP_PH)) != 0;
+    if (need_q)
+        for (int x1 = threadIdx.x; x1 < N; x1 += T)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.q + (uint64_t)x1 * M2 + c0));
+    double acc = 0.0, nrm = 0.0;
+    // ops on one butterfly's middle elements (c, x1 = j + t*nbm)
+    constexpr int Rm = C::r(0, 0), nbm = N / Rm, totm = CW * nbm;
+    auto ops = [&](double2 (&v)[Rm], int c, int j) {
+        if (need_q) {
+            const double *qp = a.q + (uint64_t)j * M2 + c0 + c;
+            double qv[Rm];
+#pragma unroll
+            for (int t = 0; t < Rm; ++t) qv[t] = __ldg(qp + (uint64_t)(t * nbm) * M2);
+#pragma unroll
+            for (int t = 0; t < Rm; ++t) {
+                if (a.ops & OP_EXP) {
+                    const double pr = v[t].x * v[t].x + v[t].y * v[t].y;
+                    acc = fma(pr, qv[t], acc);
+                    nrm += pr;
+                }
+                if (a.ops & OP_PH) {
+                    double sn, cs;
+                    sincos(a.gamma * qv[t], &sn, &cs);
+                    v[t] = make_double2(fma(cs, v[t].x, sn * v[t].y), fma(cs, v[t].y, -sn * v[t].x));
+                }
+            }
+        }
+        if (a.ops & OP_OTW) {
+            const uint64_t K = (uint64_t)(a.mat_off + (int)blockIdx.y);
+            const uint64_t xl0 = (uint64_t)j * M2 + (uint64_t)(c0 + c);
+            double2 w = conjd(fs_big(a.otw_lo, a.otw_hi, a.otw_shift, K * xl0));
+            const double2 st = conjd(fs_big(a.otw_lo, a.otw_hi, a.otw_shift, K * (uint64_t)nbm * M2));
+#pragma unroll
+            for (int t = 0; t < Rm; ++t) {
+                v[t] = cmul(v[t], w);
+                if (t + 1 < Rm) w = cmul(w, st);
+            }
+        }
+    };
+    // after the middle: forward stage 0 to buffer `dst`, or the result straight to global
+    auto middle_out = [&](double2 (&v)[Rm], int c, int j, const FsAddr<0> &dst) {
+        if constexpr (FWD) {
+            dft<Rm>(v, false);
+#pragma unroll
+            for (int t = 0; t < Rm; ++t) *dst.ptr(c, j * Rm + t) = v[t];
+        } else {
+            double2 *o = out + (uint64_t)j * M2 + c;
+#pragma unroll
+            for (int t = 0; t < Rm; ++t) o[(uint64_t)(t * nbm) * M2] = v[t];
+        }
+    };
+    // the forward transform's stages after stage 0 (which wrote buffer `first`) and its store
+    auto forward_rest = [&](bool first_is_b0) {
+        const FsAddr<0> *bufs[2] = {first_is_b0 ? &b0 : &b1, first_is_b0 ? &b1 : &b0};
+        int cur = 0;
+        fs_static_for<S - 2>([&](auto sc) {
+            fs_stage_pp<C, 0, decltype(sc)::value + 1, T, CW>(*bufs[cur], *bufs[cur ^ 1], a.tw);
+            cur ^= 1;
+        });
+        constexpr int R = C::r(0, S - 1), M = C::m(0, S - 1), nb = N / R, tot = CW * nb, OFF = C::off(0, S - 1);
+        const FsAddr<0> &src = *bufs[cur];
+#pragma unroll
+        for (int J = threadIdx.x; J < tot; J += T) {
+            int c, j;
+            fs_map<true, CW, nb>(J, c, j);
+            double2 v[R];
+#pragma unroll
+            for (int t = 0; t < R; ++t) v[t] = *src.ptr(c, j + t * nb);
+#pragma unroll
+            for (int t = 1; t < R; ++t) v[t] = cmul(v[t], __ldg(a.tw + OFF + (t - 1) * M + j));
+            dft<R>(v, false);
+            const uint64_t Cg = (uint64_t)(a.col_off + c0 + c);
+            double2 w = fs_big(a.big_lo, a.big_hi, a.big_shift, Cg * (uint64_t)j);
+            const double2 st = fs_big(a.big_lo, a.big_hi, a.big_shift, Cg * (uint64_t)nb);
+            double2 *dd = out + (uint64_t)j * M2 + c;
+#pragma unroll
+            for (int t = 0; t < R; ++t) {
+                dd[(uint64_t)(t * nb) * M2] = cmul(v[t], w);
+                if (t + 1 < R) w = cmul(w, st);
+            }
+        }
+    };
+    if constexpr (INV) {
+        {  // inverse stage 0 from global into b0
+            constexpr int R = C::r(1, 0), nb = N / R, tot = CW * nb;
+#pragma unroll
+            for (int J = threadIdx.x; J < tot; J += T) {
+                int c, j;
+                fs_map<true, CW, nb>(J, c, j);
+                const double2 *src = in + (uint64_t)j * M2 + c;
+                double2 v[R];
+#pragma unroll
+                for (int t = 0; t < R; ++t) v[t] = src[(uint64_t)(t * nb) * M2];
+                dft<R>(v, true);
+#pragma unroll
+                for (int t = 0; t < R; ++t) *b0.ptr(c, j * R + t) = v[t];
+            }
+            __syncthreads();
+        }
+        const FsAddr<0> *bufs[2] = {&b0, &b1};
+        int cur = 0;
+        fs_static_for<S - 2>([&](auto sc) {
+            fs_stage_pp<C, 1, decltype(sc)::value + 1, T, CW>(*bufs[cur], *bufs[cur ^ 1], a.tw);
+            cur ^= 1;
+        });
+        {  // inverse last stage -> ops -> forward stage 0 (or global)
+            constexpr int R = C::r(1, S - 1), M = C::m(1, S - 1), nb = N / R, tot = CW * nb, OFF = C::off(1, S - 1);
+            static_assert(R == Rm && nb == nbm, "boundary");
+            const FsAddr<0> &src = *bufs[cur], &dst = *bufs[cur ^ 1];
+#pragma unroll
+            for (int J = threadIdx.x; J < tot; J += T) {
+                int c, j;
+                fs_map<true, CW, nb>(J, c, j);
+                double2 v[R];
+#pragma unroll
+                for (int t = 0; t < R; ++t) v[t] = *src.ptr(c, j + t * nb);
+#pragma unroll
+                for (int t = 1; t < R; ++t) v[t] = cmul(v[t], __ldg(a.tw + OFF + (t - 1) * M + j));
+                dft<R>(v, true);
+                if (a.ops) ops(v, c, j);
+                middle_out(v, c, j, dst);
+            }
+            if constexpr (FWD) {
+                __syncthreads();
+                forward_rest(cur == 1);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int J = threadIdx.x; J < totm; J += T) {
+            int c, j;
+            fs_map<true, CW, nbm>(J, c, j);
+            const double2 *src = in + (uint64_t)j * M2 + c;
+            double2 v[Rm];
+#pragma unroll
+            for (int t = 0; t < Rm; ++t) v[t] = a.init ? make_double2(a.amp0, 0.0) : src[(uint64_t)(t * nbm) * M2];
+            if (a.ops) ops(v, c, j);
+            middle_out(v, c, j, b0);
+        }
+        if constexpr (FWD) {
+            __syncthreads();
+            forward_rest(true);
+        }
+    }
+    if (a.ops & OP_EXP) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+        }
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane == 0) {
+            red[2 * warp] = acc;
+            red[2 * warp + 1] = nrm;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double sa = 0.0, sb = 0.0;
+            for (int w = 0; w < (T + 31) / 32; ++w) {
+                sa += red[2 * w];
+                sb += red[2 * w + 1];
+            }
+            a.partials[2 * blockIdx.x] = sa;
+            a.partials[2 * blockIdx.x + 1] = sb;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // compiled codelets and their launch shapes (several per length for measurement: QVA_FS_ROWV /
 // QVA_FS_COLV select the variant index, default 0)
 using FsRowFn = void (*)(FsRowArgs, uint64_t);
@@ -586,15 +794,23 @@ const FsRowEntry kFsRows[] = {
 #undef QVA_FS_ROWP
 #define QVA_FS_COL(K, C, T, CW, MB, P)                                                      \
     {C::N, T, CW, P, K<C, T, CW, MB, true, true>, K<C, T, CW, MB, false, true>, K<C, T, CW, MB, true, false>}
-// column codelets: one-shot CTAs (the pipelined forms spill in the block loop and doubled the
-// DRAM write traffic at 12!: 162-205 ms; 840-point columns four wide, two CTAs per SM: cfg3 0.622
-// vs 0.653 ms eight wide)
+// column codelets (index 0 = default; measured on one B200, tools/ab_fs.sh, p=4 evolutions):
+// 770 / 810 (12!): ping-pong 768 threads x 8 columns 102.4 ms, one-shot in place 640 / 512 x 8
+// 105.0 ms, ping-pong 384 x 4 111.5 ms, 256 x 4 117.0 ms, pipelined persistent 162-205 ms (its
+// block loop spills and doubled the DRAM write traffic); 840 (cfg3): one-shot 256 x 4, two CTAs
+// per SM 0.622 ms, ping-pong 768 x 8 0.622 ms, one-shot 480 x 8 0.653 ms.  Four-wide blocks (64-B
+// rows) cost at HBM-resident 12!, eight-wide blocks need ~100 KB of shared memory per buffer.
 const FsColEntry kFsCols[] = {
+    QVA_FS_COL(fs_colpp_kernel, C770, 768, 8, 1, 2),
     QVA_FS_COL(fs_col_kernel, C770, 640, 8, 1, 0),
     QVA_FS_COL(fs_col_pipe_kernel, C770, 640, 8, 1, 1),
+    QVA_FS_COL(fs_colpp_kernel, C770, 384, 4, 2, 2),
+    QVA_FS_COL(fs_colpp_kernel, C810, 768, 8, 1, 2),
     QVA_FS_COL(fs_col_kernel, C810, 512, 8, 1, 0),
     QVA_FS_COL(fs_col_pipe_kernel, C810, 512, 8, 1, 1),
+    QVA_FS_COL(fs_colpp_kernel, C810, 384, 4, 2, 2),
     QVA_FS_COL(fs_col_kernel, C840, 256, 4, 2, 0),
+    QVA_FS_COL(fs_colpp_kernel, C840, 768, 8, 1, 2),
     QVA_FS_COL(fs_col_kernel, C840, 480, 8, 1, 0),
 };
 #undef QVA_FS_COL
@@ -640,6 +856,7 @@ const FsColEntry *fs_col_entry(int n) {
 size_t fs_col_smem(const FsColEntry &e) {
     return (size_t)(e.pipe ? 2 : 1) * e.cw * ((e.n % 2 == 0) ? e.n + 1 : e.n) * sizeof(double2);
 }
+bool fs_col_persistent(const FsColEntry &e) { return e.pipe == 1; }
 size_t fs_row_smem(const FsRowEntry &e) { return (size_t)(e.pipe ? 2 : 1) * e.rows * e.n * sizeof(double2); }
 
 DeviceOnce g_fs_attr;
@@ -734,7 +951,7 @@ cudaError_t fs_col_launch(int n, const FsColArgs &a, int cols, int nmat, bool in
     const uint64_t nblk = (uint64_t)nbx * nmat;
     const size_t smem = fs_col_smem(*e);
     const FsColEntry *o = nullptr;  // a pass that loads nothing (init) prefers a one-shot kernel
-    if (e->pipe && a.init && !inv)
+    if (fs_col_persistent(*e) && a.init && !inv)
         for (const auto &x : kFsCols)
             if (x.n == n && !x.pipe && x.cw == e->cw) {
                 o = &x;
@@ -743,7 +960,7 @@ cudaError_t fs_col_launch(int n, const FsColArgs &a, int cols, int nmat, bool in
     if (o) {
         FsColFn g = fwd ? o->fwd : o->inv;
         g<<<dim3(nbx, nmat), o->threads, fs_col_smem(*o), s>>>(a, nbx, nblk);
-    } else if (e->pipe) {
+    } else if (fs_col_persistent(*e)) {
         f<<<fs_pipe_grid(f, e->threads, smem, nblk), e->threads, smem, s>>>(a, nbx, nblk);
     } else {
         f<<<dim3(nbx, nmat), e->threads, smem, s>>>(a, nbx, nblk);
