@@ -1666,6 +1666,7 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
         const char *e = getenv("QVA_DYN");
         return e ? atoi(e) : 1;
     }();
+    static const bool g_dyn_all = getenv("QVA_DYN") != nullptr;  // explicit QVA_DYN: as given
     if (g_dyn) {
         if (P->ctr_cap < n_tile_passes) {
             plan_free(P, P->d_ctr);
@@ -1823,7 +1824,12 @@ qva_status run_passes(qva_plan *P, const std::vector<PassPlan> &passes, const do
             tp.gq = -1;
         }
         tp.angles = P->d_angles + (size_t)j * batch;
-        tp.work_ctr = (g_dyn == 1 || (g_dyn > 1 && ((g_dyn >> 1) >> j) & 1)) ? P->d_ctr + j : nullptr;
+        // claimed tiles level the SMs of the load-bound passes; the write-only first pass (no state
+        // to load, uniform work per tile) keeps the static interleaved split, which spares its
+        // claiming thread an atomic round trip per tile (A/B on one box, cfg4 init pass: 3.93 ->
+        // 3.76 ms; QVA_DYN=1 claims in every pass)
+        const bool dyn_default = g_dyn == 1 && !(tp.init == 1 && !g_dyn_all);
+        tp.work_ctr = (dyn_default || (g_dyn > 1 && ((g_dyn >> 1) >> j) & 1)) ? P->d_ctr + j : nullptr;
         tp.expect = pp.expect ? 1 : 0;
         tp.partials = P->partials;
         // default 2: the thread that issued a tile's TMA store waits for its shared-memory read
