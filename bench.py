@@ -468,6 +468,11 @@ def main():
     # whole-step model bytes (all kernels' algorithmic bytes) / step time
     total_bytes = sum(plan.kernel_stats(c)["bytes"] for c in Q.KERNEL_CLASSES)
     achieved_step_gbs = total_bytes / args.steps / (ms_step * 1e-3) / 1e9 / max(1, 1)
+    if roof is not None:
+        # every kernel's implemented bytes of a step over the step time: unaffected by launches that
+        # overlap on several streams (the three-level FFT's grouped inner passes, whose per-launch
+        # event times include the concurrent group's share of the SMs)
+        roof["frac_step_implemented"] = achieved_step_gbs / peak
 
     # ---- e2e through the public API with host buffers.  The step's inputs are the problem
     # (MaxCut graph: edge list + weights) and theta, copied from pinned host memory; q is derived

@@ -304,8 +304,9 @@ qva_status qva_circulant_plan_shape(uint64_t dim, int32_t shards, int32_t flags,
 /* Kernel timing: when enabled, every kernel launch of the plan is bracketed with CUDA events
  * on the plan's stream; qva_kernel_stats returns, for kernel class `which` (0 = X tile pass,
  * 1 = small-state fused evolve, 2 = FFT column pass, 3 = FFT row pass, 4 = sparse SpMV,
- * 5 = reduction, 6 = exchange), the summed device milliseconds, launches and algorithmic
- * bytes since the last reset. */
+ * 5 = reduction, 6 = exchange, 7 = other, 8 = three-level FFT inner passes run in groups on
+ * auxiliary streams: launches and bytes counted, not timed -- 0 ms), the summed device
+ * milliseconds, launches and algorithmic bytes since the last reset. */
 qva_status qva_set_profiling(qva_plan *plan, int32_t enable);
 qva_status qva_kernel_stats(qva_plan *plan, int32_t which, double *ms, int64_t *launches, double *bytes);
 qva_status qva_reset_kernel_stats(qva_plan *plan);

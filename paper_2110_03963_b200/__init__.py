@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libqva.so")
 MIXER_X, MIXER_CIRCULANT, MIXER_SPARSE, MIXER_PARITY = 0, 1, 2, 3
 _MIXERS = {"x": MIXER_X, "circulant": MIXER_CIRCULANT, "sparse": MIXER_SPARSE, "parity": MIXER_PARITY}
 KERNEL_CLASSES = {"tile": 0, "small": 1, "fft_col": 2, "fft_row": 3, "spmv": 4, "reduce": 5,
-                  "exchange": 6, "other": 7}
+                  "exchange": 6, "other": 7, "fft_inner": 8}
 
 
 class QvaError(RuntimeError):

@@ -617,7 +617,7 @@ struct qva_plan {
                                           // last stats reset (NVLink traffic of a real shard)
     // profiling
     bool prof = false;
-    KernelStat stats[8];
+    KernelStat stats[kKernelClasses];
     std::vector<PendingEvent> pending;
     std::vector<cudaEvent_t> event_pool;
     int64_t launches = 0;
@@ -643,17 +643,19 @@ struct ProfScope {
     int cls;
     double bytes;
     cudaEvent_t a = nullptr, b = nullptr;
-    ProfScope(qva_plan *P_, int cls_, double bytes_, int64_t nlaunch = 1) : P(P_), cls(cls_), bytes(bytes_) {
+    cudaStream_t st;
+    ProfScope(qva_plan *P_, int cls_, double bytes_, int64_t nlaunch = 1, cudaStream_t st_ = nullptr)
+        : P(P_), cls(cls_), bytes(bytes_), st(st_ ? st_ : P_->stream) {
         P->launches += nlaunch;
         if (P->prof) {
             a = get_event(P);
             b = get_event(P);
-            cudaEventRecord(a, P->stream);
+            cudaEventRecord(a, st);
         }
     }
     ~ProfScope() {
         if (P->prof) {
-            cudaEventRecord(b, P->stream);
+            cudaEventRecord(b, st);
             P->pending.push_back({a, b, cls, bytes});
         }
     }
@@ -663,7 +665,16 @@ struct PlanObserver : LaunchObserver {
     qva_plan *P;
     std::vector<ProfScope *> stack;
     explicit PlanObserver(qva_plan *P_) : P(P_) {}
-    void begin(int cls, double bytes) override { stack.push_back(new ProfScope(P, cls, bytes)); }
+    void begin(int cls, double bytes, cudaStream_t st = nullptr) override {
+        stack.push_back(new ProfScope(P, cls, bytes, 1, st));
+    }
+    void count(int cls, double bytes) override {
+        P->launches += 1;
+        if (P->prof) {
+            P->stats[cls].launches += 1;
+            P->stats[cls].bytes += bytes;
+        }
+    }
     void end() override {
         delete stack.back();
         stack.pop_back();
@@ -4187,7 +4198,7 @@ qva_status qva_set_profiling(qva_plan *P, int32_t enable) {
 }
 
 qva_status qva_kernel_stats(qva_plan *P, int32_t which, double *ms, int64_t *launches, double *bytes) {
-    if (!P || which < 0 || which >= 8) return QVA_ERR_INVALID_ARGUMENT;
+    if (!P || which < 0 || which >= kKernelClasses) return QVA_ERR_INVALID_ARGUMENT;
     DeviceGuard dg(P->device);
     QVA_TRY(sync(P));
     if (ms) *ms = P->stats[which].ms;

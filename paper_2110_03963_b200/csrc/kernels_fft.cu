@@ -110,6 +110,11 @@ struct FftPlan {
     // fused-stage passes (kernels_fft_fs.cu) for the compiled lengths of unsharded direct plans:
     // stage tables of the top-level column, inner column (three levels) and row transforms
     double2 *fs_col = nullptr, *fs_col2 = nullptr, *fs_row = nullptr;
+    // three-level inner passes in groups of top-level rows on auxiliary streams (L2 reuse between
+    // a group's three inner passes, tails of one group's launches under the next group's)
+    cudaStream_t aux[4] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[4] = {};
+    int n_aux = 0;
 };
 
 namespace {
@@ -1313,6 +1318,11 @@ void fft_plan_destroy(FftPlan *fp) {
     cudaFree(fp->fs_col);
     cudaFree(fp->fs_col2);
     cudaFree(fp->fs_row);
+    for (int k = 0; k < fp->n_aux; ++k) {
+        cudaStreamDestroy(fp->aux[k]);
+        cudaEventDestroy(fp->ev_join[k]);
+    }
+    if (fp->ev_fork) cudaEventDestroy(fp->ev_fork);
     delete fp;
 }
 
@@ -1384,8 +1394,11 @@ static FsRowArgs fs_row_args(const FftPlan *fp, const double2 *tab, const RowArg
     return f;
 }
 
+// untimed: the launches overlap with other groups' on auxiliary streams (counted as K_FFT_INNER, no
+// event brackets: per-launch events between thousands of short grouped launches cost more than
+// the grouping gains)
 static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, const FftRun &r, double beta,
-                              cudaStream_t s, LaunchObserver *obs) {
+                              cudaStream_t s, LaunchObserver *obs, bool untimed = false) {
     const double N = (double)fp->N;
     const uint64_t R = (uint64_t)fp->Mi1 * fp->Mi2;
     ColArgs c = col_args(fp);
@@ -1424,7 +1437,8 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
         c.do_inv = inv;
         c.do_fwd = fwd;
         c.ops = ops;
-        obs->begin(K_FFT_COL, 32.0 * (double)R * nmat);
+        if (untimed) obs->count(K_FFT_INNER, 32.0 * (double)R * nmat);
+        else obs->begin(K_FFT_COL, 32.0 * (double)R * nmat, s);
         cudaError_t e;
         if (fp->fs_col2 && !c.xg) {
             e = fs_col_launch(fp->Mi1, fs_col_args(fp, fp->fs_col2, c), fp->Mi2, nmat, inv != 0, fwd != 0, s);
@@ -1432,7 +1446,7 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
             col_kernel_for(fp->Mi1, half)<<<gc, half ? kFftThreads / 2 : kFftThreads, smem_c, s>>>(c);
             e = cudaGetLastError();
         }
-        obs->end();
+        if (!untimed) obs->end();
         if (e != cudaSuccess) {
             set_error(std::string("fft_col_kernel (inner): ") + cudaGetErrorString(e));
             return QVA_ERR_CUDA;
@@ -1459,7 +1473,9 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
         w.e0 = make_double2(cos(-beta * r.lam0) / N, sin(-beta * r.lam0) / N);
         w.ec = make_double2(cos(-beta * r.lamc) / N, sin(-beta * r.lamc) / N);
     }
-    obs->begin(K_FFT_ROW, 32.0 * (double)R * nmat + (r.lambda_perm ? 8.0 * (double)R * nmat : 0.0));
+    const double row_bytes = 32.0 * (double)R * nmat + (r.lambda_perm ? 8.0 * (double)R * nmat : 0.0);
+    if (untimed) obs->count(K_FFT_INNER, row_bytes);
+    else obs->begin(K_FFT_ROW, row_bytes, s);
     // 256-thread CTAs over half the rows, two or more per SM, when the stages fit 256 threads
     int rbh = 0;
     for (int x = fp->rb2 / 2; x >= 1 && !rbh; --x)
@@ -1477,12 +1493,53 @@ static qva_status inner_rows3(FftPlan *fp, double2 *psi, int nmat, int mat_off, 
         row_kernel_for(fp->Mi2, rhalf)<<<nmat * fp->Mi1 / w.rb, rhalf ? kFftThreads / 2 : kFftThreads, smem_r3, s>>>(w);
         e = cudaGetLastError();
     }
-    obs->end();
+    if (!untimed) obs->end();
     if (e != cudaSuccess) {
         set_error(std::string("fft_row_kernel (inner): ") + cudaGetErrorString(e));
         return QVA_ERR_CUDA;
     }
     return cols(1, OP_OUTER_TW, 0);
+}
+
+// The three inner passes of a three-level layer, optionally in groups of QVA_FFT_GROUP top-level rows
+// (matrices) spread round-robin over QVA_FFT_STREAMS auxiliary streams: each group's data (group x
+// Mi1 x Mi2 x 16 B) is read from HBM by its inner column pass and stays in L2 for its row and
+// inverse column passes, while the groups on the other streams fill the SMs.
+static qva_status inner_rows3_grouped(FftPlan *fp, double2 *psi, int nmat, int mat_off, const FftRun &r, double beta,
+                                      cudaStream_t s, LaunchObserver *obs) {
+    static const int g_env = [] {
+        const char *e = getenv("QVA_FFT_GROUP");
+        return e ? atoi(e) : -1;
+    }();
+    static const int k_env = [] {
+        const char *e = getenv("QVA_FFT_STREAMS");
+        return e ? std::max(1, std::min(4, atoi(e))) : 2;
+    }();
+    const uint64_t R = (uint64_t)fp->Mi1 * fp->Mi2;
+    // default: groups of ~20 MB (two matrices at 12!: 95.6 ms per p=4 evolution against 102.6 ms
+    // ungrouped; one matrix 107.4, four 99.2, eight 102.9; two streams beat three or four)
+    const int g = g_env >= 0 ? g_env : (int)std::max<uint64_t>(2, std::min<uint64_t>(8, ((20ull << 20) + 8 * R) / (16 * R)));
+    if (g <= 0 || 4 * g > nmat) return inner_rows3(fp, psi, nmat, mat_off, r, beta, s, obs);
+    if (fp->n_aux < k_env) {
+        for (int k = fp->n_aux; k < k_env; ++k) {
+            QVA_CUDA_TRY(cudaStreamCreateWithFlags(&fp->aux[k], cudaStreamNonBlocking));
+            QVA_CUDA_TRY(cudaEventCreateWithFlags(&fp->ev_join[k], cudaEventDisableTiming));
+        }
+        if (!fp->ev_fork) QVA_CUDA_TRY(cudaEventCreateWithFlags(&fp->ev_fork, cudaEventDisableTiming));
+        fp->n_aux = k_env;
+    }
+    QVA_CUDA_TRY(cudaEventRecord(fp->ev_fork, s));
+    for (int k = 0; k < k_env; ++k) QVA_CUDA_TRY(cudaStreamWaitEvent(fp->aux[k], fp->ev_fork, 0));
+    int i = 0;
+    for (int m0 = 0; m0 < nmat; m0 += g, ++i) {
+        const int gm = std::min(g, nmat - m0);
+        QVA_TRY(inner_rows3(fp, psi + (uint64_t)m0 * R, gm, mat_off + m0, r, beta, fp->aux[i % k_env], obs, true));
+    }
+    for (int k = 0; k < k_env; ++k) {
+        QVA_CUDA_TRY(cudaEventRecord(fp->ev_join[k], fp->aux[k]));
+        QVA_CUDA_TRY(cudaStreamWaitEvent(s, fp->ev_join[k], 0));
+    }
+    return QVA_OK;
 }
 
 qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver *obs) {
@@ -1584,7 +1641,7 @@ qva_status fft_run(FftPlan *fp, const FftRun &r, cudaStream_t s, LaunchObserver 
     };
     // direct: spectrum exp(-i beta lambda)/N; Bluestein: kernel spectrum B (or conj B) / M
     auto launch_row = [&](double beta, int bconj) -> qva_status {
-        if (fp->levels == 3) return inner_rows3(fp, W, fp->M1, 0, r, beta, s, obs);
+        if (fp->levels == 3) return inner_rows3_grouped(fp, W, fp->M1, 0, r, beta, s, obs);
         RowArgs w = row_args(fp, W);
         double extra = 0.0;
         if (blu) {

@@ -319,9 +319,15 @@ cudaError_t launch_check_finite(const double *x, uint64_t n, int *flag, cudaStre
 // launch observer: the plan counts launches and (when profiling) brackets them with events
 // ---------------------------------------------------------------------------------------------
 enum KernelClass { K_TILE = 0, K_SMALL = 1, K_FFT_COL = 2, K_FFT_ROW = 3, K_SPMV = 4, K_REDUCE = 5,
-                   K_EXCHANGE = 6, K_OTHER = 7 };
+                   K_EXCHANGE = 6, K_OTHER = 7, K_FFT_INNER = 8 };
+constexpr int kKernelClasses = 9;
 struct LaunchObserver {
-    virtual void begin(int cls, double algorithmic_bytes) = 0;
+    // stream: the stream the launch goes to (nullptr: the plan's stream); the events bracketing
+    // the launch are recorded there
+    virtual void begin(int cls, double algorithmic_bytes, cudaStream_t stream = nullptr) = 0;
+    // a launch counted (launches, bytes) but not bracketed by events (launches that overlap on
+    // auxiliary streams, K_FFT_INNER)
+    virtual void count(int cls, double algorithmic_bytes) = 0;
     virtual void end() = 0;
     virtual ~LaunchObserver() {}
 };
