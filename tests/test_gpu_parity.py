@@ -381,6 +381,29 @@ def test_cfg3_random_spectrum_fused_stage(Q):
         ref = O.mixer_circulant_fft(O.init_uniform(N), lam, 0.7)
         ref = O.phase(np.ascontiguousarray(ref), wl.q, 1.3)
         _amp_close(P.get_state(), O.mixer_circulant_fft(ref, lam, 0.4))
+        # one layer (first column pass straight into the final inverse one) and p = 0
+        P.evolve(theta[:2])
+        ref1 = O.evolve_circulant_fft(wl.q, lam, theta[:2])
+        _amp_close(P.get_state(), ref1)
+        _f_close(P.expectation(), O.expectation(ref1, wl.q), O.expectation(ref1, np.abs(wl.q)))
+        P.evolve([])
+        _amp_close(P.get_state(), O.init_uniform(N))
+
+
+def test_cfg3_batch_fused_stage(Q):
+    """Finite-difference batch on the cfg3 circulant plan: every member's <Q>
+    against the numpy-FFT oracle."""
+    wl = make_config("cfg3")
+    rng = np.random.default_rng(37)
+    lam = rng.standard_normal(wl.dim)
+    sets = rng.uniform(0, math.pi, (3, 4))
+    with Q.Plan(wl.dim, "circulant", max_batch=3) as P:
+        P.set_qualities(wl.q)
+        P.set_circulant_eigenvalues(lam)
+        f = P.evolve_batch(sets)
+    for b in range(3):
+        rb = O.evolve_circulant_fft(wl.q, lam, sets[b])
+        _f_close(f[b], O.expectation(rb, wl.q), O.expectation(rb, np.abs(wl.q)))
 
 
 @pytest.mark.parametrize("N", [2, 7, 13, 17, 96, 97, 720, 1001, 1009, 4096, 4099, 5040, 6144, 8198, 10007])
@@ -633,6 +656,16 @@ def test_qwoa_12_factorial(Q):
         _amp_close(got, ref[idx[:64]])
         blk = P.get_state(N - 4096, 4096)
         _amp_close(blk, ref[N - 4096:])
+        # step level (fused-stage forward-only / inverse-only top-level column passes around the
+        # grouped inner passes): one phase then one mixer from |+>
+        del ref
+        P.reset_state()
+        P.apply_phase(0.9)
+        P.apply_mixer(0.37)
+        ref = O.mixer_complete(O.phase(O.init_uniform(N), q, 0.9), 0.37, 0.0, float(N))
+        got = np.array([P.get_state(int(i), 1)[0] for i in idx[64:128]])
+        _amp_close(got, ref[idx[64:128]])
+        _amp_close(P.get_state(0, 4096), ref[:4096])
 
 
 # ---------------------------------------------------------------- cfg4 full size ----
