@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(T, MINB) fs_row_pipe_kernel(const FsRowArgs a,
 // registers -> [forward FFT -> twiddle w_M^{C k1}] -> global.  As fft_col_kernel.
 template <int N>
 constexpr int fs_col_stride() { return (N % 2 == 0) ? N + 1 : N; }  // odd: 8 columns, 8 bank groups
-template <typename C, int T, int CW, bool INV, bool FWD, bool SM0>
+template <typename C, int T, int CW, bool INV, bool FWD>
 __device__ __forceinline__ void fs_col_block(const FsColArgs &a, double2 *A, int bx, int by, double *red) {
     constexpr int N = C::N, S = C::S;
     constexpr int CS = fs_col_stride<N>();
@@ -369,7 +369,7 @@ __device__ __forceinline__ void fs_col_block(const FsColArgs &a, double2 *A, int
                     fs_map<true, CW, nb>(J, c, j);
                     const double2 *src = in + (uint64_t)j * M2 + c;
 #pragma unroll
-                    for (int t = 0; t < R; ++t) u[b][t] = SM0 ? *ad.ptr(c, j + t * nb) : src[(uint64_t)(t * nb) * M2];
+                    for (int t = 0; t < R; ++t) u[b][t] = src[(uint64_t)(t * nb) * M2];
                 }
             }
 #pragma unroll
@@ -377,7 +377,6 @@ __device__ __forceinline__ void fs_col_block(const FsColArgs &a, double2 *A, int
                 const int J = threadIdx.x + b * T;
                 if (tot % T == 0 || J < tot) dft<R>(u[b], true);
             }
-            if constexpr (SM0) __syncthreads();
             fs_first_store<C, 1, T, CW, true>(ad, u);
         }
         __syncthreads();
@@ -393,7 +392,7 @@ __device__ __forceinline__ void fs_col_block(const FsColArgs &a, double2 *A, int
                 const double2 *src = in + (uint64_t)j * M2 + c;
 #pragma unroll
                 for (int t = 0; t < Rm; ++t)
-                    v[b][t] = a.init ? make_double2(a.amp0, 0.0) : SM0 ? *ad.ptr(c, j + t * nbm) : src[(uint64_t)(t * nbm) * M2];
+                    v[b][t] = a.init ? make_double2(a.amp0, 0.0) : src[(uint64_t)(t * nbm) * M2];
             }
         }
     }
@@ -446,7 +445,7 @@ __device__ __forceinline__ void fs_col_block(const FsColArgs &a, double2 *A, int
             const int J = threadIdx.x + b * T;
             if (totm % T == 0 || J < totm) dft<Rm>(v[b], false);
         }
-        if constexpr (INV || SM0) __syncthreads();  // the last reads of the block are done
+        if constexpr (INV) __syncthreads();  // the inverse last stage's reads are done
         fs_first_store<C, 0, T, CW, true>(ad, v);
         __syncthreads();
         fs_static_for<S - 2>([&](auto sc) { fs_stage<C, 0, decltype(sc)::value + 1, T, CW, true>(ad, a.tw); });
@@ -511,48 +510,13 @@ template <typename C, int T, int CW, int MINB, bool INV, bool FWD>
 __global__ void __launch_bounds__(T, MINB) fs_col_kernel(const FsColArgs a, int nbx, uint64_t nblk) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double red[2 * (T / 32 + 1)];
-    fs_col_block<C, T, CW, INV, FWD, false>(a, reinterpret_cast<double2 *>(smem_raw), blockIdx.x, blockIdx.y, red);
+    fs_col_block<C, T, CW, INV, FWD>(a, reinterpret_cast<double2 *>(smem_raw), blockIdx.x, blockIdx.y, red);
 }
-// Persistent pipelined form (as fs_row_pipe_kernel): blocks (bx, by) = (b mod nbx, b / nbx),
-// the next block's columns copied into the second buffer while the current one is transformed.
-template <typename C, int T, int CW, int MINB, bool INV, bool FWD>
-__global__ void __launch_bounds__(T, MINB) fs_col_pipe_kernel(const FsColArgs a, int nbx, uint64_t nblk) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ double red[2 * (T / 32 + 1)];
-    constexpr int N = C::N, CS = fs_col_stride<N>(), E = CW * CS;
-    double2 *A0 = reinterpret_cast<double2 *>(smem_raw);
-    const bool load = true;  // (init passes launch the one-shot kernel)
-    const uint64_t M2 = (uint64_t)a.M2;
-    auto prefetch = [&](double2 *A, uint64_t blk) {
-        const int bx = (int)(blk % (uint64_t)nbx), by = (int)(blk / (uint64_t)nbx);
-        const double2 *src = a.in + (uint64_t)by * a.mat_stride + bx * CW;
-        for (int i = threadIdx.x; i < N * CW; i += T) {
-            const int c = i & (CW - 1), x1 = i / CW;
-            cp_async16(A + c * CS + x1, src + (uint64_t)x1 * M2 + c);
-        }
-    };
-    uint64_t blk = blockIdx.x;
-    int cur = 0;
-    if (load && blk < nblk) prefetch(A0, blk);
-    fs_cp_commit();
-    for (; blk < nblk; blk += gridDim.x) {
-        const uint64_t nxt = blk + gridDim.x;
-        if (load && nxt < nblk) prefetch(A0 + (cur ^ 1) * E, nxt);
-        fs_cp_commit();
-        fs_cp_wait_prev();
-        __syncthreads();
-        const int bx = (int)(blk % (uint64_t)nbx), by = (int)(blk / (uint64_t)nbx);
-        fs_col_block<C, T, CW, INV, FWD, true>(a, A0 + cur * E, bx, by, red);
-        __syncthreads();
-        cur ^= 1;
-    }
-}
-
 // ---------------------------------------------------------------------------------------------
 // Ping-pong column pass: the same transforms with out-of-place stages between two shared-memory
 // buffers, so a stage needs one barrier and no thread has to hold all of its butterflies at once
-// (butterflies in rounds of T): small CTAs (two or more per SM) whose stage-0 loads overlap the
-// other CTAs' arithmetic.
+// (butterflies in rounds of T): 768 threads on eight-column blocks (two ~100 KB buffers, one CTA
+// per SM) at 80 registers and no spills, where the in-place block needs NB butterflies per thread.
 template <typename C, int D, int s, int T, int CW, typename Ad>
 __device__ __forceinline__ void fs_stage_pp(const Ad &src, const Ad &dst, const double2 *__restrict__ tw) {
     constexpr int N = C::N, R = C::r(D, s), M = C::m(D, s), nb = N / R, tot = CW * nb, OFF = C::off(D, s);
@@ -763,11 +727,11 @@ using FsRowFn = void (*)(FsRowArgs, uint64_t);
 using FsColFn = void (*)(FsColArgs, int, uint64_t);
 
 struct FsRowEntry {
-    int n, threads, rows, pipe;
+    int n, threads, rows, pipe;  // pipe: 1 persistent pipelined (two block buffers)
     FsRowFn fn;
 };
 struct FsColEntry {
-    int n, threads, cw, pipe;
+    int n, threads, cw, pipe;  // pipe: 0 in place (one block buffer), 2 ping-pong (two buffers)
     FsColFn inv_fwd, fwd, inv;
 };
 
@@ -796,18 +760,16 @@ const FsRowEntry kFsRows[] = {
     {C::N, T, CW, P, K<C, T, CW, MB, true, true>, K<C, T, CW, MB, false, true>, K<C, T, CW, MB, true, false>}
 // column codelets (index 0 = default; measured on one B200, tools/ab_fs.sh, p=4 evolutions):
 // 770 / 810 (12!): ping-pong 768 threads x 8 columns 102.4 ms, one-shot in place 640 / 512 x 8
-// 105.0 ms, ping-pong 384 x 4 111.5 ms, 256 x 4 117.0 ms, pipelined persistent 162-205 ms (its
-// block loop spills and doubled the DRAM write traffic); 840 (cfg3): one-shot 256 x 4, two CTAs
+// 105.0 ms, ping-pong 384 x 4 111.5 ms, 256 x 4 117.0 ms (a pipelined persistent form, removed,
+// spilled in its block loop and doubled the DRAM write traffic: 162-205 ms); 840 (cfg3): one-shot 256 x 4, two CTAs
 // per SM 0.622 ms, ping-pong 768 x 8 0.622 ms, one-shot 480 x 8 0.653 ms.  Four-wide blocks (64-B
 // rows) cost at HBM-resident 12!, eight-wide blocks need ~100 KB of shared memory per buffer.
 const FsColEntry kFsCols[] = {
     QVA_FS_COL(fs_colpp_kernel, C770, 768, 8, 1, 2),
     QVA_FS_COL(fs_col_kernel, C770, 640, 8, 1, 0),
-    QVA_FS_COL(fs_col_pipe_kernel, C770, 640, 8, 1, 1),
     QVA_FS_COL(fs_colpp_kernel, C770, 384, 4, 2, 2),
     QVA_FS_COL(fs_colpp_kernel, C810, 768, 8, 1, 2),
     QVA_FS_COL(fs_col_kernel, C810, 512, 8, 1, 0),
-    QVA_FS_COL(fs_col_pipe_kernel, C810, 512, 8, 1, 1),
     QVA_FS_COL(fs_colpp_kernel, C810, 384, 4, 2, 2),
     QVA_FS_COL(fs_col_kernel, C840, 256, 4, 2, 0),
     QVA_FS_COL(fs_colpp_kernel, C840, 768, 8, 1, 2),
@@ -816,20 +778,20 @@ const FsColEntry kFsCols[] = {
 #undef QVA_FS_COL
 
 template <typename C>
-void fs_fill_rad(int n, int *rad) {
+void fs_fill_rad(int n, Arr8 &rad) {
     if (n != C::N) return;
     constexpr Arr8 f = C::F;
-    for (int s = 0; s < C::S; ++s) rad[s] = f.v[s];
+    for (int s = 0; s < C::S; ++s) rad.v[s] = f.v[s];
 }
-const int *fs_radices(int n) {
-    static int rad[8] = {};
-    for (int &r : rad) r = 0;
+// forward radix order of the compiled length n (0-terminated; all zero: none)
+Arr8 fs_radices(int n) {
+    Arr8 rad{};
     fs_fill_rad<C768>(n, rad);
     fs_fill_rad<C4320>(n, rad);
     fs_fill_rad<C770>(n, rad);
     fs_fill_rad<C810>(n, rad);
     fs_fill_rad<C840>(n, rad);
-    return rad[0] ? rad : nullptr;
+    return rad;
 }
 int fs_env(const char *name) {
     const char *e = getenv(name);
@@ -856,7 +818,6 @@ const FsColEntry *fs_col_entry(int n) {
 size_t fs_col_smem(const FsColEntry &e) {
     return (size_t)(e.pipe ? 2 : 1) * e.cw * ((e.n % 2 == 0) ? e.n + 1 : e.n) * sizeof(double2);
 }
-bool fs_col_persistent(const FsColEntry &e) { return e.pipe == 1; }
 size_t fs_row_smem(const FsRowEntry &e) { return (size_t)(e.pipe ? 2 : 1) * e.rows * e.n * sizeof(double2); }
 
 DeviceOnce g_fs_attr;
@@ -897,8 +858,9 @@ int fs_col_width(int n) {
 }
 
 bool fs_stage_tables(int n, std::vector<double2> &tab) {
-    const int *rad = fs_radices(n);
-    if (!rad) return false;
+    const Arr8 ra = fs_radices(n);
+    const int *rad = ra.v;
+    if (!rad[0]) return false;
     int S = 0;
     while (S < 8 && rad[S]) ++S;
     tab.clear();
@@ -950,21 +912,7 @@ cudaError_t fs_col_launch(int n, const FsColArgs &a, int cols, int nmat, bool in
     const int nbx = cols / e->cw;
     const uint64_t nblk = (uint64_t)nbx * nmat;
     const size_t smem = fs_col_smem(*e);
-    const FsColEntry *o = nullptr;  // a pass that loads nothing (init) prefers a one-shot kernel
-    if (fs_col_persistent(*e) && a.init && !inv)
-        for (const auto &x : kFsCols)
-            if (x.n == n && !x.pipe && x.cw == e->cw) {
-                o = &x;
-                break;
-            }
-    if (o) {
-        FsColFn g = fwd ? o->fwd : o->inv;
-        g<<<dim3(nbx, nmat), o->threads, fs_col_smem(*o), s>>>(a, nbx, nblk);
-    } else if (fs_col_persistent(*e)) {
-        f<<<fs_pipe_grid(f, e->threads, smem, nblk), e->threads, smem, s>>>(a, nbx, nblk);
-    } else {
-        f<<<dim3(nbx, nmat), e->threads, smem, s>>>(a, nbx, nblk);
-    }
+    f<<<dim3(nbx, nmat), e->threads, smem, s>>>(a, nbx, nblk);
     return cudaGetLastError();
 }
 
