@@ -30,6 +30,13 @@
 // radix-R butterflies into registers, the block synchronises, then twiddles, transforms and
 // stores them in Stockham (autosort) order, so one buffer per transform suffices.
 // Direct N <= 4096: the whole p-layer evolution runs in one CTA ("whole" kernel).
+//
+// For the sub-FFT lengths with a fused-stage codelet (kernels_fft_fs.cu: 768, 4320 rows; 770,
+// 810, 840 columns) unsharded direct / three-level plans launch those passes instead (first stage
+// from global memory, last stage to global memory, forward / inverse boundary stages fused on the
+// registers); three-level plans run each layer's inner passes in groups of top-level rows on two
+// auxiliary streams (inner_rows3_grouped).  These kernels stay the path for every other length,
+// Bluestein and sharded plans.
 #include <cuda_runtime.h>
 
 #include <algorithm>
