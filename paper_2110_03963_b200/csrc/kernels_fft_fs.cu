@@ -750,6 +750,7 @@ const FsRowEntry kFsRows[] = {
     QVA_FS_ROWP(C768, 96, 2, 4),
     QVA_FS_ROW(C768, 192, 4, 3),
     QVA_FS_ROWP(C768, 192, 4, 2),
+    QVA_FS_ROW(C768, 96, 2, 6),
     QVA_FS_ROW(C4320, 288, 1, 2),
     QVA_FS_ROW(C4320, 288, 1, 1),
     QVA_FS_ROWP(C4320, 288, 1, 1),
@@ -758,21 +759,25 @@ const FsRowEntry kFsRows[] = {
 #undef QVA_FS_ROWP
 #define QVA_FS_COL(K, C, T, CW, MB, P)                                                      \
     {C::N, T, CW, P, K<C, T, CW, MB, true, true>, K<C, T, CW, MB, false, true>, K<C, T, CW, MB, true, false>}
-// column codelets (index 0 = default; measured on one B200, tools/ab_fs.sh, p=4 evolutions):
-// 770 / 810 (12!): ping-pong 768 threads x 8 columns 102.4 ms, one-shot in place 640 / 512 x 8
-// 105.0 ms, ping-pong 384 x 4 111.5 ms, 256 x 4 117.0 ms (a pipelined persistent form, removed,
-// spilled in its block loop and doubled the DRAM write traffic: 162-205 ms); 840 (cfg3): one-shot 256 x 4, two CTAs
-// per SM 0.622 ms, ping-pong 768 x 8 0.622 ms, one-shot 480 x 8 0.653 ms.  Four-wide blocks (64-B
-// rows) cost at HBM-resident 12!, eight-wide blocks need ~100 KB of shared memory per buffer.
+// column codelets (index 0 = default; measured on one B200, tools/ab_fs.sh, p=4 evolutions with
+// the grouped three-level inner passes): 770 / 810 (12!): ping-pong 896 threads x 8 columns
+// 92.1 ms, 1024 x 8 92.4 ms (small spills), 768 x 8 95.6 ms, 512 x 8 102.0 ms, one-shot in place
+// 640 / 512 x 8 98.4 ms, ping-pong four wide 384 x 4 111 ms (a pipelined persistent form, removed,
+// spilled in its block loop and doubled the DRAM write traffic: 162-205 ms); 840 (cfg3): ping-pong
+// 896 x 8 0.609 ms, 1024 x 8 0.619, one-shot 256 x 4 two CTAs per SM 0.622, 480 x 8 0.653.  More
+// warps per SM win as long as ptxas keeps the butterflies in registers.
 const FsColEntry kFsCols[] = {
+    QVA_FS_COL(fs_colpp_kernel, C770, 896, 8, 1, 2),
+    QVA_FS_COL(fs_colpp_kernel, C770, 1024, 8, 1, 2),
     QVA_FS_COL(fs_colpp_kernel, C770, 768, 8, 1, 2),
     QVA_FS_COL(fs_col_kernel, C770, 640, 8, 1, 0),
-    QVA_FS_COL(fs_colpp_kernel, C770, 384, 4, 2, 2),
+    QVA_FS_COL(fs_colpp_kernel, C810, 896, 8, 1, 2),
+    QVA_FS_COL(fs_colpp_kernel, C810, 1024, 8, 1, 2),
     QVA_FS_COL(fs_colpp_kernel, C810, 768, 8, 1, 2),
     QVA_FS_COL(fs_col_kernel, C810, 512, 8, 1, 0),
-    QVA_FS_COL(fs_colpp_kernel, C810, 384, 4, 2, 2),
+    QVA_FS_COL(fs_colpp_kernel, C840, 896, 8, 1, 2),
+    QVA_FS_COL(fs_colpp_kernel, C840, 1024, 8, 1, 2),
     QVA_FS_COL(fs_col_kernel, C840, 256, 4, 2, 0),
-    QVA_FS_COL(fs_colpp_kernel, C840, 768, 8, 1, 2),
     QVA_FS_COL(fs_col_kernel, C840, 480, 8, 1, 0),
 };
 #undef QVA_FS_COL
