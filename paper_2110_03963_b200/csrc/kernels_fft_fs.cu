@@ -517,13 +517,13 @@ __global__ void __launch_bounds__(T, MINB) fs_col_kernel(const FsColArgs a, int 
 // buffers, so a stage needs one barrier and no thread has to hold all of its butterflies at once
 // (butterflies in rounds of T): 768 threads on eight-column blocks (two ~100 KB buffers, one CTA
 // per SM) at 80 registers and no spills, where the in-place block needs NB butterflies per thread.
-template <typename C, int D, int s, int T, int CW, typename Ad>
+template <typename C, int D, int s, int T, int CW, typename Ad, bool CFAST = true>
 __device__ __forceinline__ void fs_stage_pp(const Ad &src, const Ad &dst, const double2 *__restrict__ tw) {
     constexpr int N = C::N, R = C::r(D, s), M = C::m(D, s), nb = N / R, tot = CW * nb, OFF = C::off(D, s);
 #pragma unroll
     for (int J = threadIdx.x; J < tot; J += T) {
         int c, j;
-        fs_map<true, CW, nb>(J, c, j);
+        fs_map<CFAST, CW, nb>(J, c, j);
         double2 v[R];
 #pragma unroll
         for (int t = 0; t < R; ++t) v[t] = *src.ptr(c, j + t * nb);
@@ -536,6 +536,104 @@ __device__ __forceinline__ void fs_stage_pp(const Ad &src, const Ad &dst, const 
         for (int t = 0; t < R; ++t) *dst.ptr(c, o + t * M) = v[t];
     }
     __syncthreads();
+}
+
+// Ping-pong row pass: fs_row_block's transforms with out-of-place stages between two buffers
+// (rows j-fastest, butterflies in rounds of T), so more, lighter threads fit per SM.
+template <typename C, int T, int NT, int MINB>
+__global__ void __launch_bounds__(T, MINB) fs_rowpp_kernel(const FsRowArgs a, uint64_t nblk) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int N = C::N, S = C::S;
+    static_assert(S >= 2 && C::r(0, S - 1) == C::r(1, 0), "reversed inverse order");
+    double2 *A0 = reinterpret_cast<double2 *>(smem_raw);
+    using Ad = FsAddr<C::swz()>;
+    const Ad b0{A0, N}, b1{A0 + NT * N, N};
+    const uint64_t blk = blockIdx.x;
+    double2 *rows = a.buf + blk * NT * N;
+    const int grow0 = a.row_off + (int)blk * NT;
+    {  // forward stage 0: global -> DFT -> b0
+        constexpr int R = C::r(0, 0), nb = N / R, tot = NT * nb;
+#pragma unroll
+        for (int J = threadIdx.x; J < tot; J += T) {
+            int f, j;
+            fs_map<false, NT, nb>(J, f, j);
+            const double2 *src = rows + f * N + j;
+            double2 v[R];
+#pragma unroll
+            for (int t = 0; t < R; ++t) v[t] = src[t * nb];
+            dft<R>(v, false);
+#pragma unroll
+            for (int t = 0; t < R; ++t) *b0.ptr(f, j * R + t) = v[t];
+        }
+        __syncthreads();
+    }
+    const Ad *bufs[2] = {&b0, &b1};
+    int cur = 0;
+    fs_static_for<S - 2>([&](auto sc) {
+        fs_stage_pp<C, 0, decltype(sc)::value + 1, T, NT, Ad, false>(*bufs[cur], *bufs[cur ^ 1], a.tw);
+        cur ^= 1;
+    });
+    {  // forward last stage -> spectrum -> inverse stage 0
+        constexpr int R = C::r(0, S - 1), M = C::m(0, S - 1), nb = N / R, tot = NT * nb, OFF = C::off(0, S - 1);
+        const Ad &src = *bufs[cur], &dst = *bufs[cur ^ 1];
+#pragma unroll
+        for (int J = threadIdx.x; J < tot; J += T) {
+            int f, j;
+            fs_map<false, NT, nb>(J, f, j);
+            double2 v[R];
+#pragma unroll
+            for (int t = 0; t < R; ++t) v[t] = *src.ptr(f, j + t * nb);
+#pragma unroll
+            for (int t = 1; t < R; ++t) v[t] = cmul(v[t], __ldg(a.tw + OFF + (t - 1) * M + j));
+            dft<R>(v, false);
+            if (a.spec == 0) {
+                if (j == 0 && grow0 + f == 0) v[0] = cmul(v[0], a.e0_over_ec);
+            } else {
+                const double *lam = a.lam_perm + (uint64_t)(grow0 + f) * N + j;
+#pragma unroll
+                for (int t = 0; t < R; ++t) {
+                    double sn, cs;
+                    sincos(-a.beta * __ldg(lam + t * nb), &sn, &cs);
+                    v[t] = cmul(v[t], make_double2(cs * a.scale, sn * a.scale));
+                }
+            }
+            dft<R>(v, true);
+#pragma unroll
+            for (int t = 0; t < R; ++t) *dst.ptr(f, j * R + t) = v[t];
+        }
+        __syncthreads();
+        cur ^= 1;
+    }
+    fs_static_for<S - 2>([&](auto sc) {
+        fs_stage_pp<C, 1, decltype(sc)::value + 1, T, NT, Ad, false>(*bufs[cur], *bufs[cur ^ 1], a.tw);
+        cur ^= 1;
+    });
+    {  // inverse last stage -> final twiddle -> global
+        constexpr int R = C::r(1, S - 1), M = C::m(1, S - 1), nb = N / R, tot = NT * nb, OFF = C::off(1, S - 1);
+        const Ad &src = *bufs[cur];
+#pragma unroll
+        for (int J = threadIdx.x; J < tot; J += T) {
+            int f, j;
+            fs_map<false, NT, nb>(J, f, j);
+            double2 v[R];
+#pragma unroll
+            for (int t = 0; t < R; ++t) v[t] = *src.ptr(f, j + t * nb);
+#pragma unroll
+            for (int t = 1; t < R; ++t) v[t] = cmul(v[t], __ldg(a.tw + OFF + (t - 1) * M + j));
+            dft<R>(v, true);
+            const int kr = grow0 + f;
+            const uint64_t K = (uint64_t)(a.row_mod ? kr % a.row_mod : kr);
+            double2 w = conjd(fs_big(a.big_lo, a.big_hi, a.big_shift, K * (uint64_t)j));
+            const double2 st = conjd(fs_big(a.big_lo, a.big_hi, a.big_shift, K * (uint64_t)nb));
+            if (a.spec == 0) w = cmul(w, a.ec);
+            double2 *dd = rows + f * N + j;
+#pragma unroll
+            for (int t = 0; t < R; ++t) {
+                dd[t * nb] = cmul(v[t], w);
+                if (t + 1 < R) w = cmul(w, st);
+            }
+        }
+    }
 }
 
 template <typename C, int T, int CW, int MINB, bool INV, bool FWD>
@@ -727,7 +825,7 @@ using FsRowFn = void (*)(FsRowArgs, uint64_t);
 using FsColFn = void (*)(FsColArgs, int, uint64_t);
 
 struct FsRowEntry {
-    int n, threads, rows, pipe;  // pipe: 1 persistent pipelined (two block buffers)
+    int n, threads, rows, pipe;  // pipe: 1 persistent pipelined, 2 ping-pong (two block buffers each)
     FsRowFn fn;
 };
 struct FsColEntry {
@@ -743,20 +841,26 @@ using C840 = FsC<8, 15, 7>;
 
 #define QVA_FS_ROW(C, T, NT, MB) {C::N, T, NT, 0, fs_row_kernel<C, T, NT, MB>}
 #define QVA_FS_ROWP(C, T, NT, MB) {C::N, T, NT, 1, fs_row_pipe_kernel<C, T, NT, MB>}
-// index 0 of each length is the default (measured on one B200, tools/ab_fs.sh: 12! 768-point rows
-// pipelined 96 x 2 rows 105.0 ms vs one-shot 192 x 4 rows 109.8 ms per p=4 evolution; cfg3
-// 4320-point rows one-shot two CTAs per SM 0.622 ms vs 0.721 ms one per SM, 0.979 ms pipelined)
+#define QVA_FS_ROWPP(C, T, NT, MB) {C::N, T, NT, 2, fs_rowpp_kernel<C, T, NT, MB>}
+// index 0 of each length is the default (measured on one B200, tools/ab_fs.sh, p=4 evolutions
+// with the grouped inner passes and 896-thread columns): 12! 768-point rows ping-pong 256 threads x
+// 4 rows (two CTAs per SM) 90.7 ms, pipelined persistent 192 x 4 91.4, ping-pong 384 x 4 91.8,
+// pipelined 96 x 2 92.1, ping-pong 192 x 2 92.4, one-shot 96 x 2 93.7 ms; cfg3 4320-point rows
+// one-shot two CTAs per SM 0.609 ms, ping-pong 512 / 448 threads 0.622 / 0.652, one-shot one CTA
+// per SM 0.72, pipelined 0.97 ms
 const FsRowEntry kFsRows[] = {
+    QVA_FS_ROWPP(C768, 256, 4, 2),
+    QVA_FS_ROWP(C768, 192, 4, 2),
+    QVA_FS_ROWPP(C768, 384, 4, 2),
     QVA_FS_ROWP(C768, 96, 2, 4),
     QVA_FS_ROW(C768, 192, 4, 3),
-    QVA_FS_ROWP(C768, 192, 4, 2),
-    QVA_FS_ROW(C768, 96, 2, 6),
     QVA_FS_ROW(C4320, 288, 1, 2),
+    QVA_FS_ROWPP(C4320, 512, 1, 1),
     QVA_FS_ROW(C4320, 288, 1, 1),
-    QVA_FS_ROWP(C4320, 288, 1, 1),
 };
 #undef QVA_FS_ROW
 #undef QVA_FS_ROWP
+#undef QVA_FS_ROWPP
 #define QVA_FS_COL(K, C, T, CW, MB, P)                                                      \
     {C::N, T, CW, P, K<C, T, CW, MB, true, true>, K<C, T, CW, MB, false, true>, K<C, T, CW, MB, true, false>}
 // column codelets (index 0 = default; measured on one B200, tools/ab_fs.sh, p=4 evolutions with
@@ -902,7 +1006,7 @@ cudaError_t fs_row_launch(int n, const FsRowArgs &a, uint64_t n_rows, cudaStream
     if (n_rows == 0) return cudaSuccess;
     const uint64_t nblk = n_rows / e->rows;
     const size_t smem = fs_row_smem(*e);
-    const unsigned grid = e->pipe ? fs_pipe_grid(e->fn, e->threads, smem, nblk) : (unsigned)nblk;
+    const unsigned grid = e->pipe == 1 ? fs_pipe_grid(e->fn, e->threads, smem, nblk) : (unsigned)nblk;
     e->fn<<<grid, e->threads, smem, s>>>(a, nblk);
     return cudaGetLastError();
 }
