@@ -54,7 +54,7 @@ bool fs_row_available(int n);
 bool fs_col_available(int n);
 // Stage twiddle tables of the length-n codelet: forward stages then inverse (pre-conjugated)
 // stages, entry (t - 1) * m + k of a stage (m, R) = exp(-/+ 2 pi i t k / (m R)).
-bool fs_stage_tables(int n, std::vector<double2> &tab);
+bool fs_stage_tables(int n, bool col, std::vector<double2> &tab);  // of the selected row / column codelet
 // rows: n_rows rows (a multiple of fs_row_block(n)); one pass forward -> spectrum -> inverse ->
 // final twiddle, in place
 int fs_row_block(int n);

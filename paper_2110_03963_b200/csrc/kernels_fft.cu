@@ -1247,7 +1247,7 @@ qva_status fft_plan_create(uint64_t N, int device, int G, bool force3, FftPlan *
     if (!fp->whole && !fp->bluestein && G == 1) {
         auto fs_tab = [&](int n, bool col, double2 **dst) -> bool {
             std::vector<double2> t;
-            if (!(col ? fs_col_available(n) : fs_row_available(n)) || !fs_stage_tables(n, t)) return true;
+            if (!(col ? fs_col_available(n) : fs_row_available(n)) || !fs_stage_tables(n, col, t)) return true;
             if (cudaMalloc(dst, t.size() * sizeof(double2)) != cudaSuccess) return false;
             cudaMemcpy(*dst, t.data(), t.size() * sizeof(double2), cudaMemcpyHostToDevice);
             return true;

@@ -827,10 +827,12 @@ using FsColFn = void (*)(FsColArgs, int, uint64_t);
 struct FsRowEntry {
     int n, threads, rows, pipe;  // pipe: 1 persistent pipelined, 2 ping-pong (two block buffers each)
     FsRowFn fn;
+    Arr8 rad;                    // forward radix order (the stage tables follow it)
 };
 struct FsColEntry {
     int n, threads, cw, pipe;  // pipe: 0 in place (one block buffer), 2 ping-pong (two buffers)
     FsColFn inv_fwd, fwd, inv;
+    Arr8 rad;
 };
 
 using C768 = FsC<16, 16, 3>;
@@ -839,9 +841,9 @@ using C770 = FsC<7, 11, 10>;
 using C810 = FsC<10, 9, 9>;
 using C840 = FsC<8, 15, 7>;
 
-#define QVA_FS_ROW(C, T, NT, MB) {C::N, T, NT, 0, fs_row_kernel<C, T, NT, MB>}
-#define QVA_FS_ROWP(C, T, NT, MB) {C::N, T, NT, 1, fs_row_pipe_kernel<C, T, NT, MB>}
-#define QVA_FS_ROWPP(C, T, NT, MB) {C::N, T, NT, 2, fs_rowpp_kernel<C, T, NT, MB>}
+#define QVA_FS_ROW(C, T, NT, MB) {C::N, T, NT, 0, fs_row_kernel<C, T, NT, MB>, C::F}
+#define QVA_FS_ROWP(C, T, NT, MB) {C::N, T, NT, 1, fs_row_pipe_kernel<C, T, NT, MB>, C::F}
+#define QVA_FS_ROWPP(C, T, NT, MB) {C::N, T, NT, 2, fs_rowpp_kernel<C, T, NT, MB>, C::F}
 // index 0 of each length is the default (measured on one B200, tools/ab_fs.sh, p=4 evolutions
 // with the grouped inner passes and 896-thread columns): 12! 768-point rows ping-pong 256 threads x
 // 4 rows (two CTAs per SM) 90.7 ms, pipelined persistent 192 x 4 91.4, ping-pong 384 x 4 91.8,
@@ -862,14 +864,16 @@ const FsRowEntry kFsRows[] = {
 #undef QVA_FS_ROWP
 #undef QVA_FS_ROWPP
 #define QVA_FS_COL(K, C, T, CW, MB, P)                                                      \
-    {C::N, T, CW, P, K<C, T, CW, MB, true, true>, K<C, T, CW, MB, false, true>, K<C, T, CW, MB, true, false>}
+    {C::N, T, CW, P, K<C, T, CW, MB, true, true>, K<C, T, CW, MB, false, true>, K<C, T, CW, MB, true, false>, C::F}
 // column codelets (index 0 = default; measured on one B200, tools/ab_fs.sh, p=4 evolutions with
 // the grouped three-level inner passes): 770 / 810 (12!): ping-pong 896 threads x 8 columns
 // 92.1 ms, 1024 x 8 92.4 ms (small spills), 768 x 8 95.6 ms, 512 x 8 102.0 ms, one-shot in place
 // 640 / 512 x 8 98.4 ms, ping-pong four wide 384 x 4 111 ms (a pipelined persistent form, removed,
 // spilled in its block loop and doubled the DRAM write traffic: 162-205 ms); 840 (cfg3): ping-pong
 // 896 x 8 0.609 ms, 1024 x 8 0.619, one-shot 256 x 4 two CTAs per SM 0.622, 480 x 8 0.653.  More
-// warps per SM win as long as ptxas keeps the butterflies in registers.
+// warps per SM win as long as ptxas keeps the butterflies in registers.  Other radix orders of the
+// same lengths (each entry carries its order; the stage tables follow it): 770 as 10*11*7 / 11*7*10
+// with 810 as 9*10*9 / 9*9*10: 92.1 / 93.0 ms against 90.9 ms for 7*11*10 with 10*9*9.
 const FsColEntry kFsCols[] = {
     QVA_FS_COL(fs_colpp_kernel, C770, 896, 8, 1, 2),
     QVA_FS_COL(fs_colpp_kernel, C770, 1024, 8, 1, 2),
@@ -886,22 +890,6 @@ const FsColEntry kFsCols[] = {
 };
 #undef QVA_FS_COL
 
-template <typename C>
-void fs_fill_rad(int n, Arr8 &rad) {
-    if (n != C::N) return;
-    constexpr Arr8 f = C::F;
-    for (int s = 0; s < C::S; ++s) rad.v[s] = f.v[s];
-}
-// forward radix order of the compiled length n (0-terminated; all zero: none)
-Arr8 fs_radices(int n) {
-    Arr8 rad{};
-    fs_fill_rad<C768>(n, rad);
-    fs_fill_rad<C4320>(n, rad);
-    fs_fill_rad<C770>(n, rad);
-    fs_fill_rad<C810>(n, rad);
-    fs_fill_rad<C840>(n, rad);
-    return rad;
-}
 int fs_env(const char *name) {
     const char *e = getenv(name);
     return e ? atoi(e) : 0;
@@ -966,10 +954,11 @@ int fs_col_width(int n) {
     return e ? e->cw : 0;
 }
 
-bool fs_stage_tables(int n, std::vector<double2> &tab) {
-    const Arr8 ra = fs_radices(n);
-    const int *rad = ra.v;
-    if (!rad[0]) return false;
+bool fs_stage_tables(int n, bool col, std::vector<double2> &tab) {
+    const FsRowEntry *re = col ? nullptr : fs_row_entry(n);
+    const FsColEntry *ce = col ? fs_col_entry(n) : nullptr;
+    if (!re && !ce) return false;
+    const int *rad = re ? re->rad.v : ce->rad.v;
     int S = 0;
     while (S < 8 && rad[S]) ++S;
     tab.clear();
