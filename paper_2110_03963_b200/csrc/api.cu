@@ -14,9 +14,19 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "qva_internal.h"
 
 namespace qva {
+
+// NVTX range over one C-ABI call (visible in Nsight Systems / ncu --nvtx; a no-op without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 static thread_local std::string g_last_error;
 void set_error(const std::string &msg) { g_last_error = msg; }
@@ -3260,18 +3270,21 @@ static qva_status set_q_common(qva_plan *P, const double *src, bool device, uint
 }
 
 qva_status qva_set_qualities(qva_plan *P, const double *q, uint64_t offset, uint64_t count) {
+    NvtxRange nvtx_range_("qva_set_qualities");
     if (!P || (!q && count)) return QVA_ERR_INVALID_ARGUMENT;
     DeviceGuard dg(P->device);
     return set_q_common(P, q, false, offset, count);
 }
 
 qva_status qva_set_qualities_device(qva_plan *P, const double *q, uint64_t offset, uint64_t count) {
+    NvtxRange nvtx_range_("qva_set_qualities_device");
     if (!P || (!q && count)) return QVA_ERR_INVALID_ARGUMENT;
     DeviceGuard dg(P->device);
     return set_q_common(P, q, true, offset, count);
 }
 
 qva_status qva_set_qualities_maxcut(qva_plan *P, int32_t m, const int32_t *u, const int32_t *v, const double *w) {
+    NvtxRange nvtx_range_("qva_set_qualities_maxcut");
     if (!P || m < 0 || (m > 0 && (!u || !v))) return QVA_ERR_INVALID_ARGUMENT;
     if (P->mixer != QVA_MIXER_X && P->mixer != QVA_MIXER_PARITY) {
         set_error("qva_set_qualities_maxcut: qubit (X / parity mixer) plans only");
@@ -3308,6 +3321,7 @@ qva_status qva_set_qualities_maxcut(qva_plan *P, int32_t m, const int32_t *u, co
 
 qva_status qva_set_qualities_permutation(qva_plan *P, int32_t m, int32_t k, const double *F, const double *D,
                                          const double *lin) {
+    NvtxRange nvtx_range_("qva_set_qualities_permutation");
     if (!P || m < 1 || m > kKpermMaxMHost || k < 1 || k > m || (F && !D)) {
         set_error("qva_set_qualities_permutation: need 1 <= k <= m <= 20 (and D with F)");
         return QVA_ERR_INVALID_ARGUMENT;
@@ -3664,6 +3678,7 @@ qva_status qva_reset_state(qva_plan *P) {
 static const double *q_current(qva_plan *P) { return (P->layout == 1) ? P->qB : P->q; }
 
 qva_status qva_apply_phase(qva_plan *P, double gamma) {
+    NvtxRange nvtx_range_("qva_apply_phase");
     if (!P) return QVA_ERR_INVALID_ARGUMENT;
     if (!std::isfinite(gamma)) {
         set_error("non-finite gamma");
@@ -3686,6 +3701,7 @@ qva_status qva_apply_phase(qva_plan *P, double gamma) {
 }
 
 qva_status qva_apply_mixer(qva_plan *P, double beta) {
+    NvtxRange nvtx_range_("qva_apply_mixer");
     if (!P) return QVA_ERR_INVALID_ARGUMENT;
     if (!std::isfinite(beta)) {
         set_error("non-finite beta");
@@ -3858,6 +3874,7 @@ static qva_status evolve_impl(qva_plan *P, const double *theta, int p, bool *hav
 }
 
 qva_status qva_evolve(qva_plan *P, const double *theta, int32_t p) {
+    NvtxRange nvtx_range_("qva_evolve");
     if (!P || p < 0 || (p > 0 && !theta)) return QVA_ERR_INVALID_ARGUMENT;
     QVA_TRY(check_theta(theta, 2 * (size_t)p));
     if (!P->q_set) {
@@ -3976,6 +3993,7 @@ static qva_status expect_now(qva_plan *P) {
 }
 
 qva_status qva_expectation(qva_plan *P, double *out) {
+    NvtxRange nvtx_range_("qva_expectation");
     if (!P || !out) return QVA_ERR_INVALID_ARGUMENT;
     DeviceGuard dg(P->device);
     QVA_TRY(expect_now(P));
@@ -4113,6 +4131,7 @@ static qva_status batch_local(qva_plan *P, const double *thetas, int first, int 
 }
 
 qva_status qva_evolve_ex(qva_plan *P, const double *theta, int32_t p) {
+    NvtxRange nvtx_range_("qva_evolve_ex");
     if (!P || p < 0 || (p > 0 && !theta)) return QVA_ERR_INVALID_ARGUMENT;
     QVA_TRY(ex_check(P, theta, (size_t)p * (P->g_m + 1)));
     DeviceGuard dg(P->device);
@@ -4133,6 +4152,7 @@ qva_status qva_evolve_ex(qva_plan *P, const double *theta, int32_t p) {
 }
 
 qva_status qva_evolve_ex_batch(qva_plan *P, const double *thetas, int32_t B, int32_t p, double *f_out) {
+    NvtxRange nvtx_range_("qva_evolve_ex_batch");
     if (!P || B < 0 || p < 0 || (B > 0 && (!thetas || !f_out))) return QVA_ERR_INVALID_ARGUMENT;
     const size_t per = (size_t)p * (P->g_m + 1);
     QVA_TRY(ex_check(P, thetas, (size_t)B * per));
@@ -4162,6 +4182,7 @@ qva_status qva_evolve_ex_batch(qva_plan *P, const double *thetas, int32_t B, int
 }
 
 qva_status qva_evolve_batch(qva_plan *P, const double *thetas, int32_t B, int32_t p, double *f_out) {
+    NvtxRange nvtx_range_("qva_evolve_batch");
     if (!P || B < 0 || p < 0 || (B > 0 && (!thetas || !f_out))) return QVA_ERR_INVALID_ARGUMENT;
     QVA_TRY(check_theta(thetas, (size_t)B * 2 * p));
     if (!P->q_set) {
